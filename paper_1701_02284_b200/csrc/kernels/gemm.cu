@@ -1,0 +1,365 @@
+// Host side of the tcgen05 GEMM core: tile / split-K selection, TMA
+// descriptors, the deterministic split-K reduction, and the three Convolv
+// entry points (fprop, bwd-data, bwd-filter) expressed as implicit GEMMs.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "tc_gemm.cuh"
+
+namespace tcb {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string t_last_error;
+std::atomic<unsigned long long> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+tc_status fail(tc_status st, const std::string& msg) {
+    t_last_error = msg;
+    return st;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+// ------------------------------------------------------------------ TMA
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
+                       uint32_t box_inner, uint32_t box_outer, std::string* err) {
+    auto fn = encode_fn();
+    if (!fn) {
+        *err = "cuTensorMapEncodeTiled unavailable (no CUDA driver)";
+        return false;
+    }
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride * 2) & 15)) {
+        *err = "TMA operand must be 16-byte aligned with a 16-byte multiple row stride";
+        return false;
+    }
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
+}
+
+// ------------------------------------------------------------------ split-K reduce
+// out[m, n] = epilogue( sum_s ws[s][m][n] ), fixed summation order (deterministic).
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
+                                     void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
+                                     int n_bias, int relu, float beta) {
+    const long long total = static_cast<long long>(M) * N;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i / N);
+        const int n = static_cast<int>(i - static_cast<long long>(m) * N);
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += ws[s * split_stride + i];
+        if (bias && n < n_bias) acc += bias[n];
+        if (relu) acc = fmaxf(acc, 0.f);
+        if (out_bf16) {
+            reinterpret_cast<__nv_bfloat16*>(out)[m * ldd + n] = __float2bfloat16_rn(acc);
+        } else {
+            float* o = reinterpret_cast<float*>(out) + m * ldd + n;
+            *o = beta != 0.f ? acc + beta * *o : acc;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launch
+struct LaunchPlan {
+    int bn = 128;
+    int splits = 1;
+    int kb_per_split = 1;
+    int num_kb = 1;
+};
+
+static int pick_bn(int N) {
+    int best = 256;
+    double best_eff = -1.0;
+    for (int bn : {256, 128, 64}) {
+        const double eff = static_cast<double>(N) / (static_cast<double>(ceil_div(N, bn)) * bn);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+static LaunchPlan plan_launch(int M, int N, int K, int splits_req) {
+    LaunchPlan lp;
+    lp.bn = pick_bn(N);
+    lp.num_kb = std::max(1, ceil_div(K, BK));
+    const int tiles = ceil_div(M, BM) * ceil_div(N, lp.bn);
+    int splits = splits_req;
+    if (splits <= 0) {
+        splits = 1;
+        const int sms = num_sms();
+        if (tiles < sms) splits = std::max(1, std::min(sms / tiles, lp.num_kb / 4));
+    }
+    splits = std::max(1, std::min(splits, lp.num_kb));
+    lp.kb_per_split = ceil_div(lp.num_kb, splits);
+    lp.splits = ceil_div(lp.num_kb, lp.kb_per_split);
+    return lp;
+}
+
+template <int BN>
+static tc_status launch_bn(const GemmParams& p, dim3 grid, cudaStream_t st) {
+    const int smem = TileCfg<BN>::kSmemBytes;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (attr_err != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(attr_err));
+    tc_gemm_kernel<BN><<<grid, kNumThreads, smem, st>>>(p);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
+// Common driver: fills tiling/epilogue fields of `p`, launches the main kernel
+// and (for split-K) the reduction.
+static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long long ldd, int d_bf16,
+                          const float* bias, int n_bias, int relu, float beta, void* ws, size_t ws_bytes,
+                          cudaStream_t st) {
+    p.num_kb = lp.num_kb;
+    p.kb_per_split = lp.kb_per_split;
+    p.relu = 0;
+    p.bias = nullptr;
+    p.beta = 0.f;
+    if (lp.splits > 1) {
+        const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
+        if (!ws || ws_bytes < need)
+            return fail(TC_INVALID_ARG, "split-K workspace too small: need " + std::to_string(need) + " bytes");
+        p.epi = EPI_F32_PARTIAL;
+        p.D = ws;
+        p.ldd = p.N;
+        p.split_stride = static_cast<long long>(p.M) * p.N;
+    } else {
+        p.epi = d_bf16 ? EPI_BF16 : EPI_F32;
+        p.D = D;
+        p.ldd = ldd;
+        p.bias = bias;
+        p.n_bias = n_bias;
+        p.relu = relu;
+        p.beta = beta;
+        p.split_stride = 0;
+    }
+    dim3 grid(ceil_div(p.M, BM), ceil_div(p.N, lp.bn), lp.splits);
+    tc_status s;
+    switch (lp.bn) {
+        case 256: s = launch_bn<256>(p, grid, st); break;
+        case 128: s = launch_bn<128>(p, grid, st); break;
+        default: s = launch_bn<64>(p, grid, st); break;
+    }
+    if (s != TC_OK) return s;
+    if (lp.splits > 1) {
+        const long long total = static_cast<long long>(p.M) * p.N;
+        const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(ws), lp.splits, p.M, p.N,
+                                                     p.split_stride, D, ldd, d_bf16, bias, n_bias, relu, beta);
+        TCB_LAUNCH_CHECK();
+    }
+    return TC_OK;
+}
+
+static void init_params(GemmParams& p) {
+    std::memset(&p, 0, sizeof(p));
+    p.alpha = 1.f;
+}
+
+}  // namespace tcb
+
+using namespace tcb;
+
+extern "C" {
+
+const char* tc_last_error(void) { return tcb::t_last_error.c_str(); }
+const char* tc_build_info(void) { return "tcb200 sm_100a tcgen05 kind::f16 (nvcc " __VERSION__ ")"; }
+unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load(); }
+
+size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
+    if (!a) return 0;
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits);
+    return lp.splits > 1 ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
+}
+
+tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
+    if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0) return fail(TC_INVALID_ARG, "tc_gemm_bf16: bad shape");
+    GemmParams p;
+    init_params(p);
+    p.M = a->M;
+    p.N = a->N;
+    p.K = a->K;
+    p.alpha = a->alpha;
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits);
+    std::string err;
+    if (a->a_layout == TC_LAYOUT_K) {
+        p.a_mode = OP_TMA_K;
+        if (!make_tmap_2d_bf16(&p.tmA, a->A, a->K, a->M, a->lda, BK, BM, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        p.a_mode = OP_TMA_MN;
+        if (!make_tmap_2d_bf16(&p.tmA, a->A, a->M, a->K, a->lda, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    }
+    if (a->b_layout == TC_LAYOUT_K) {
+        p.b_mode = OP_TMA_K;
+        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->K, a->N, a->ldb, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        p.b_mode = OP_TMA_MN;
+        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->N, a->K, a->ldb, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    }
+    return run_gemm(p, lp, a->D, a->ldd, a->d_dtype == TC_DTYPE_BF16, a->bias, a->N, a->relu, a->beta,
+                    a->workspace, a->workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- convolution
+static ConvGeom geom_of(const tc_conv_desc* d) {
+    ConvGeom g;
+    g.N = d->N;
+    g.H = d->H;
+    g.W = d->W;
+    g.C = d->cs;
+    g.R = d->R;
+    g.S = d->S;
+    g.stride = d->stride;
+    g.pad = d->pad;
+    g.Ho = d->Ho;
+    g.Wo = d->Wo;
+    g.Co = d->ks;
+    return g;
+}
+
+static tc_status check_conv(const tc_conv_desc* d) {
+    if (!d || d->N <= 0 || d->C <= 0 || d->K <= 0 || d->R <= 0 || d->S <= 0 || d->stride <= 0)
+        return fail(TC_INVALID_ARG, "conv: bad descriptor");
+    if ((d->cs & 7) || (d->ks & 7) || d->cs < d->C || d->ks < d->K)
+        return fail(TC_INVALID_ARG, "conv: channel strides must be multiples of 8 and >= channels");
+    if ((d->H + 2 * d->pad - d->R) / d->stride + 1 != d->Ho || (d->W + 2 * d->pad - d->S) / d->stride + 1 != d->Wo)
+        return fail(TC_SHAPE_FAULT, "conv: output extent mismatch");
+    return TC_OK;
+}
+
+static bool is_pointwise(const tc_conv_desc* d) { return d->R == 1 && d->S == 1 && d->stride == 1 && d->pad == 0; }
+
+static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
+    const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
+    const long long npix_in = static_cast<long long>(d->N) * d->H * d->W;
+    if (which == 0) return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1);
+    if (which == 1) return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1);
+    return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0);
+}
+
+size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
+    if (!d) return 0;
+    LaunchPlan lp = conv_plan(d, which);
+    if (lp.splits <= 1) return 0;
+    long long M = which == 2 ? d->K : 0, N = which == 2 ? static_cast<long long>(d->R) * d->S * d->cs : 0;
+    return static_cast<size_t>(lp.splits) * M * N * sizeof(float);
+}
+
+tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
+                        void* ws, size_t ws_bytes, void* stream) {
+    tc_status s = check_conv(d);
+    if (s != TC_OK) return s;
+    GemmParams p;
+    init_params(p);
+    p.M = d->N * d->Ho * d->Wo;
+    p.N = d->ks;  // padded output channels are written as zeros (zero filter rows, masked bias)
+    p.K = d->R * d->S * d->cs;
+    p.g = geom_of(d);
+    LaunchPlan lp = conv_plan(d, 0);
+    std::string err;
+    if (is_pointwise(d)) {
+        p.a_mode = OP_TMA_K;
+        if (!make_tmap_2d_bf16(&p.tmA, x, d->cs, p.M, d->cs, BK, BM, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        p.a_mode = OP_GATHER_K;
+        p.gather_kind = GATHER_FPROP;
+        p.gsrc = static_cast<const __nv_bfloat16*>(x);
+    }
+    p.b_mode = OP_TMA_K;
+    if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, p.K, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+    // Bias is read only for n < K; padded channels get 0 (relu(0) = 0).
+    return run_gemm(p, lp, y, d->ks, 1, bias, d->K, relu, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, void* ws,
+                             size_t ws_bytes, void* stream) {
+    tc_status s = check_conv(d);
+    if (s != TC_OK) return s;
+    GemmParams p;
+    init_params(p);
+    p.M = d->N * d->H * d->W;
+    p.N = d->cs;
+    p.K = d->R * d->S * d->ks;
+    p.g = geom_of(d);
+    LaunchPlan lp = conv_plan(d, 1);
+    std::string err;
+    if (is_pointwise(d)) {
+        p.a_mode = OP_TMA_K;
+        if (!make_tmap_2d_bf16(&p.tmA, dy, d->ks, p.M, d->ks, BK, BM, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        p.a_mode = OP_GATHER_K;
+        p.gather_kind = GATHER_DGRAD;
+        p.gsrc = static_cast<const __nv_bfloat16*>(dy);
+    }
+    p.b_mode = OP_TMA_MN;
+    if (!make_tmap_2d_bf16(&p.tmB, w_rskc, d->cs, p.K, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    return run_gemm(p, lp, dx, d->cs, 1, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void* x, float* dw, void* ws,
+                               size_t ws_bytes, void* stream) {
+    tc_status s = check_conv(d);
+    if (s != TC_OK) return s;
+    GemmParams p;
+    init_params(p);
+    const int npix = d->N * d->Ho * d->Wo;
+    p.M = d->K;
+    p.N = d->R * d->S * d->cs;
+    p.K = npix;
+    p.g = geom_of(d);
+    LaunchPlan lp = conv_plan(d, 2);
+    std::string err;
+    p.a_mode = OP_TMA_MN;
+    if (!make_tmap_2d_bf16(&p.tmA, dy, d->ks, npix, d->ks, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    if (is_pointwise(d)) {
+        p.b_mode = OP_TMA_MN;
+        if (!make_tmap_2d_bf16(&p.tmB, x, d->cs, npix, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        p.b_mode = OP_GATHER_MN;
+        p.gsrc = static_cast<const __nv_bfloat16*>(x);
+    }
+    return run_gemm(p, lp, dw, p.N, 0, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+"""tcgen05 GEMM / implicit-GEMM conv kernels vs a plain PyTorch fp32 reference.
+
+Tolerance: bf16 operands with fp32 accumulation, per-op relative error
+(max |err| / max |ref|) <= 1e-2 (BASELINE.json north_star, tensor-core ops).
+"""
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1701_02284_b200 import _native as nat  # noqa: E402
+
+TOL = 1e-2
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(out, ref):
+    return ((out.float() - ref.float()).abs().max() / ref.float().abs().max().clamp_min(1e-6)).item()
+
+
+def run_gemm(M, N, K, a_layout, b_layout, d_dtype, bias=False, relu=False, splits=0, alpha=1.0):
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16).cuda()
+    bvec = torch.randn(N, generator=g).cuda() if bias else None
+    Ast = A if a_layout == nat.TC_LAYOUT_K else A.t().contiguous()
+    Bst = B if b_layout == nat.TC_LAYOUT_K else B.t().contiguous()
+    dt = torch.bfloat16 if d_dtype == nat.TC_DTYPE_BF16 else torch.float32
+    D = torch.zeros(M, N, dtype=dt, device="cuda")
+    args = nat.GemmArgs(M=M, N=N, K=K, a_layout=a_layout, b_layout=b_layout, A=Ast.data_ptr(),
+                        lda=Ast.shape[1], B=Bst.data_ptr(), ldb=Bst.shape[1], D=D.data_ptr(), ldd=N,
+                        d_dtype=d_dtype, bias=bvec.data_ptr() if bias else None, relu=int(relu), alpha=alpha,
+                        beta=0.0, splits=splits)
+    ws_bytes = nat.lib().tc_gemm_workspace_bytes(C.byref(args))
+    ws = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device="cuda")
+    args.workspace = ws.data_ptr()
+    args.workspace_bytes = ws_bytes
+    nat.check(nat.lib().tc_gemm_bf16(C.byref(args), None))
+    torch.cuda.synchronize()
+    ref = alpha * (A.float() @ B.float().t())
+    if bias:
+        ref = ref + bvec
+    if relu:
+        ref = ref.clamp_min(0)
+    return D, ref
+
+
+@pytest.mark.parametrize("M,N,K,al,bl", [
+    (256, 256, 512, 0, 0),
+    (128, 128, 64, 0, 0),
+    (200, 96, 368, 0, 0),
+    (384, 384, 2304, 0, 0),
+    (128, 4096, 6400, 0, 0),
+    (256, 192, 256, 1, 0),
+    (256, 192, 256, 0, 1),
+    (256, 320, 512, 1, 1),
+])
+def test_gemm_layouts_bf16(M, N, K, al, bl):
+    D, ref = run_gemm(M, N, K, al, bl, nat.TC_DTYPE_BF16)
+    assert rel_err(D, ref) < TOL
+
+
+def test_gemm_bias_relu():
+    D, ref = run_gemm(300, 200, 320, 0, 0, nat.TC_DTYPE_BF16, bias=True, relu=True)
+    assert rel_err(D, ref) < TOL
+
+
+@pytest.mark.parametrize("splits", [1, 4, 0])
+def test_gemm_splitk_f32(splits):
+    D, ref = run_gemm(96, 4096, 4096, 1, 1, nat.TC_DTYPE_F32, splits=splits)
+    assert rel_err(D, ref) < TOL
+
+
+def nhwc_pad(x_nchw, cs):
+    n, c, h, w = x_nchw.shape
+    out = torch.zeros(n, h, w, cs, dtype=torch.bfloat16, device=x_nchw.device)
+    out[..., :c] = x_nchw.permute(0, 2, 3, 1).to(torch.bfloat16)
+    return out
+
+
+def conv_case(N, C_, H, W, K, R, stride, pad, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.randn(N, C_, H, W, generator=g).to(torch.bfloat16).float().cuda()
+    w = (torch.randn(K, C_, R, R, generator=g) * 0.1).to(torch.bfloat16).float().cuda()
+    b = torch.randn(K, generator=g).cuda()
+    Ho = (H + 2 * pad - R) // stride + 1
+    Wo = (W + 2 * pad - R) // stride + 1
+    cs = (C_ + 7) // 8 * 8
+    ks = (K + 7) // 8 * 8
+    d = nat.ConvDesc(N=N, C=C_, H=H, W=W, K=K, R=R, S=R, stride=stride, pad=pad, Ho=Ho, Wo=Wo, cs=cs, ks=ks)
+    return x, w, b, d
+
+
+def w_krsc(w, cs):
+    K, C_, R, S = w.shape
+    out = torch.zeros(K, R, S, cs, dtype=torch.bfloat16, device=w.device)
+    out[..., :C_] = w.permute(0, 2, 3, 1).to(torch.bfloat16)
+    return out
+
+
+def w_rskc(w, cs, ks):
+    K, C_, R, S = w.shape
+    out = torch.zeros(R, S, ks, cs, dtype=torch.bfloat16, device=w.device)
+    out[:, :, :K, :C_] = w.permute(2, 3, 0, 1).to(torch.bfloat16)
+    return out
+
+
+CONV_CASES = [
+    (2, 8, 13, 13, 64, 3, 1, 1),
+    (2, 3, 35, 35, 96, 11, 4, 0),
+    (2, 20, 12, 12, 50, 5, 1, 0),
+    (2, 64, 14, 14, 128, 1, 1, 0),
+    (2, 96, 27, 27, 256, 5, 1, 2),
+    (2, 64, 16, 16, 128, 1, 2, 0),
+    (2, 32, 15, 15, 48, 3, 2, 1),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd(case):
+    x, w, b, d = conv_case(*case)
+    xs = nhwc_pad(x, d.cs)
+    ws = w_krsc(w, d.cs)
+    y = torch.full((d.N, d.Ho, d.Wo, d.ks), float("nan"), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.lib().tc_conv2d_fwd(C.byref(d), xs.data_ptr(), ws.data_ptr(), b.data_ptr(), 0, y.data_ptr(),
+                                      None, 0, None))
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x, w, b, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
+    assert rel_err(y[..., :d.K], ref) < TOL
+    assert torch.all(y[..., d.K:] == 0)
+
+
+@pytest.mark.parametrize("case", CONV_CASES[2:] + [(2, 8, 13, 13, 64, 3, 1, 1)])
+def test_conv_bwd_data(case):
+    x, w, b, d = conv_case(*case, seed=1)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    dy = torch.randn(d.N, d.K, d.Ho, d.Wo, generator=g).to(torch.bfloat16).float().cuda()
+    dys = nhwc_pad(dy, d.ks)
+    wr = w_rskc(w, d.cs, d.ks)
+    dx = torch.full((d.N, d.H, d.W, d.cs), float("nan"), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.lib().tc_conv2d_bwd_data(C.byref(d), dys.data_ptr(), wr.data_ptr(), dx.data_ptr(), None, 0, None))
+    torch.cuda.synchronize()
+    ref = torch.nn.grad.conv2d_input(x.shape, w, dy, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
+    assert rel_err(dx[..., :d.C], ref) < TOL
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_bwd_filter(case):
+    x, w, b, d = conv_case(*case, seed=2)
+    g = torch.Generator(device="cpu").manual_seed(6)
+    dy = torch.randn(d.N, d.K, d.Ho, d.Wo, generator=g).to(torch.bfloat16).float().cuda()
+    xs = nhwc_pad(x, d.cs)
+    dys = nhwc_pad(dy, d.ks)
+    dw = torch.full((d.K, d.R, d.S, d.cs), float("nan"), dtype=torch.float32, device="cuda")
+    wsb = nat.lib().tc_conv2d_workspace_bytes(C.byref(d), 2)
+    wsp = torch.empty(max(wsb, 4), dtype=torch.uint8, device="cuda")
+    nat.check(nat.lib().tc_conv2d_bwd_filter(C.byref(d), dys.data_ptr(), xs.data_ptr(), dw.data_ptr(),
+                                             wsp.data_ptr(), wsb, None))
+    torch.cuda.synchronize()
+    ref = torch.nn.grad.conv2d_weight(x, w.shape, dy, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
+    assert rel_err(dw[..., :d.C], ref) < TOL
