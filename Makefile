@@ -2,7 +2,7 @@
 #   make            -> paper_1701_02284_b200/_lib/libtcb200.so   (product: host compiler + CUDA runtime/kernels)
 #   make oracle     -> oracle/_build/libtc_oracle.so             (test infrastructure: CPU restatement)
 NVCC      ?= /usr/local/cuda/bin/nvcc
-CXX       ?= g++
+CXX       := /usr/bin/g++
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 PKG       := paper_1701_02284_b200
 LIBDIR    := $(PKG)/_lib
@@ -13,7 +13,7 @@ NVFLAGS   := -O3 -std=c++20 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisi
 CXXFLAGS  := -O2 -std=c++20 -fPIC -Wall -Wextra -fno-fast-math -fvisibility=hidden $(INC)
 
 CU_SRC    := $(wildcard $(PKG)/csrc/kernels/*.cu) $(wildcard $(PKG)/csrc/runtime/*.cu)
-CPP_SRC   := $(wildcard $(PKG)/csrc/host/*.cpp) $(wildcard $(PKG)/csrc/runtime/*.cpp)
+CPP_SRC   := $(wildcard $(PKG)/csrc/host/*.cpp) $(wildcard $(PKG)/csrc/common/*.cpp) $(wildcard $(PKG)/csrc/runtime/*.cpp)
 CU_OBJ    := $(patsubst %.cu,$(OBJDIR)/%.o,$(CU_SRC))
 CPP_OBJ   := $(patsubst %.cpp,$(OBJDIR)/%.o,$(CPP_SRC))
 HDRS      := $(wildcard include/*.h) $(wildcard $(PKG)/csrc/*/*.cuh) $(wildcard $(PKG)/csrc/*/*.hpp) $(wildcard $(PKG)/csrc/*/*.h)

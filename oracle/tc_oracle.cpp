@@ -1,0 +1,980 @@
+// CPU ORACLE — TEST INFRASTRUCTURE ONLY (see tc_oracle.h).
+//
+// Restates the reference runtime on the host: NCHW tensors,
+// fp32 or fp64, deterministic OpenMP (static partitions, every output element
+// reduced in a fixed order by one thread).  Each kernel cites the SPEC / paper
+// line it follows.
+#include "tc_oracle.h"
+
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tc_philox.h"
+
+namespace {
+
+using i64 = int64_t;
+
+// ----------------------------------------------------------------- GEMM
+// C[M,N] (+)= op(A)[M,K] * op(B)[K,N]; row-major; every C element sums k in
+// ascending order (deterministic for any thread count).
+template <class T>
+void gemm(int M, int N, int K, const T* A, i64 lda, bool ta, const T* B, i64 ldb, bool tb, T* C, i64 ldc, bool acc) {
+    const int JB = 64, KB = 256;
+    const int nj = (N + JB - 1) / JB;
+#pragma omp parallel for schedule(static)
+    for (int jb = 0; jb < nj; ++jb) {
+        const int j0 = jb * JB, j1 = std::min(N, j0 + JB);
+        std::vector<T> bt(static_cast<size_t>(KB) * JB);
+        for (int i = 0; i < M && !acc; ++i)
+            for (int j = j0; j < j1; ++j) C[i * ldc + j] = T(0);
+        for (int k0 = 0; k0 < K; k0 += KB) {
+            const int k1 = std::min(K, k0 + KB);
+            for (int k = k0; k < k1; ++k)
+                for (int j = j0; j < j1; ++j) bt[(k - k0) * JB + (j - j0)] = tb ? B[j * ldb + k] : B[k * ldb + j];
+            for (int i = 0; i < M; ++i) {
+                T* c = C + i * ldc;
+                T cr[64];
+                for (int j = j0; j < j1; ++j) cr[j - j0] = c[j];
+                for (int k = k0; k < k1; ++k) {
+                    const T a = ta ? A[k * lda + i] : A[i * lda + k];
+                    const T* b = &bt[(k - k0) * JB];
+                    for (int j = 0; j < j1 - j0; ++j) cr[j] += a * b[j];
+                }
+                for (int j = j0; j < j1; ++j) c[j] = cr[j - j0];
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- convolution
+template <class T>
+void im2col(const T* x, T* col, int C, int H, int W, int R, int S, int stride, int pad, int Ho, int Wo) {
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < C; ++c)
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+                T* dst = col + (static_cast<i64>(c * R + r) * S + s) * Ho * Wo;
+                for (int oh = 0; oh < Ho; ++oh) {
+                    const int ih = oh * stride - pad + r;
+                    for (int ow = 0; ow < Wo; ++ow) {
+                        const int iw = ow * stride - pad + s;
+                        dst[oh * Wo + ow] = (ih >= 0 && ih < H && iw >= 0 && iw < W) ? x[(static_cast<i64>(c) * H + ih) * W + iw] : T(0);
+                    }
+                }
+            }
+}
+
+template <class T>
+void conv_fwd(const T* x, const T* w, const T* b, T* y, int N, int C, int H, int W, int K, int R, int S, int stride,
+              int pad, bool direct) {
+    const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
+    const i64 CRS = static_cast<i64>(C) * R * S, HWo = static_cast<i64>(Ho) * Wo;
+    if (direct) {
+#pragma omp parallel for collapse(2) schedule(static)
+        for (int n = 0; n < N; ++n)
+            for (int k = 0; k < K; ++k)
+                for (int oh = 0; oh < Ho; ++oh)
+                    for (int ow = 0; ow < Wo; ++ow) {
+                        T acc = T(0);
+                        for (int c = 0; c < C; ++c)
+                            for (int r = 0; r < R; ++r) {
+                                const int ih = oh * stride - pad + r;
+                                if (ih < 0 || ih >= H) continue;
+                                for (int s = 0; s < S; ++s) {
+                                    const int iw = ow * stride - pad + s;
+                                    if (iw < 0 || iw >= W) continue;
+                                    acc += x[((static_cast<i64>(n) * C + c) * H + ih) * W + iw] *
+                                           w[((static_cast<i64>(k) * C + c) * R + r) * S + s];
+                                }
+                            }
+                        y[((static_cast<i64>(n) * K + k) * Ho + oh) * Wo + ow] = acc + (b ? b[k] : T(0));
+                    }
+        return;
+    }
+    std::vector<T> col(CRS * HWo);
+    for (int n = 0; n < N; ++n) {
+        im2col(x + static_cast<i64>(n) * C * H * W, col.data(), C, H, W, R, S, stride, pad, Ho, Wo);
+        T* yn = y + static_cast<i64>(n) * K * HWo;
+        gemm<T>(K, static_cast<int>(HWo), static_cast<int>(CRS), w, CRS, false, col.data(), HWo, false, yn, HWo, false);
+        if (b)
+            for (int k = 0; k < K; ++k)
+                for (i64 i = 0; i < HWo; ++i) yn[k * HWo + i] += b[k];
+    }
+}
+
+template <class T>
+void conv_bwd_data(const T* dy, const T* w, T* dx, int N, int C, int H, int W, int K, int R, int S, int stride, int pad) {
+    const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
+    // dx[n,c,ih,iw] = sum_{k,r,s: ih = oh*stride - pad + r} dy[n,k,oh,ow] w[k,c,r,s]
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (int c = 0; c < C; ++c)
+            for (int ih = 0; ih < H; ++ih)
+                for (int iw = 0; iw < W; ++iw) {
+                    T acc = T(0);
+                    for (int k = 0; k < K; ++k)
+                        for (int r = 0; r < R; ++r) {
+                            const int nh = ih + pad - r;
+                            if (nh < 0 || nh % stride) continue;
+                            const int oh = nh / stride;
+                            if (oh >= Ho) continue;
+                            for (int s = 0; s < S; ++s) {
+                                const int nw = iw + pad - s;
+                                if (nw < 0 || nw % stride) continue;
+                                const int ow = nw / stride;
+                                if (ow >= Wo) continue;
+                                acc += dy[((static_cast<i64>(n) * K + k) * Ho + oh) * Wo + ow] *
+                                       w[((static_cast<i64>(k) * C + c) * R + r) * S + s];
+                            }
+                        }
+                    dx[((static_cast<i64>(n) * C + c) * H + ih) * W + iw] = acc;
+                }
+}
+
+template <class T>
+void conv_bwd_filter(const T* dy, const T* x, T* dw, int N, int C, int H, int W, int K, int R, int S, int stride, int pad) {
+    const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
+    const i64 CRS = static_cast<i64>(C) * R * S, HWo = static_cast<i64>(Ho) * Wo;
+    std::vector<T> col(CRS * HWo);
+    for (int n = 0; n < N; ++n) {
+        im2col(x + static_cast<i64>(n) * C * H * W, col.data(), C, H, W, R, S, stride, pad, Ho, Wo);
+        // dw[K, CRS] += dy_n[K, HWo] * col[CRS, HWo]^T
+        gemm<T>(K, static_cast<int>(CRS), static_cast<int>(HWo), dy + static_cast<i64>(n) * K * HWo, HWo, false,
+                col.data(), HWo, true, dw, CRS, n > 0);
+    }
+}
+
+template <class T>
+void conv_bwd_bias(const T* dy, T* db, int N, int K, i64 HW) {
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < K; ++k) {
+        T acc = T(0);
+        for (int n = 0; n < N; ++n)
+            for (i64 i = 0; i < HW; ++i) acc += dy[(static_cast<i64>(n) * K + k) * HW + i];
+        db[k] = acc;
+    }
+}
+
+// ----------------------------------------------------------------- pooling
+// Max: the first maximum in row-major window order wins (strict >); padded
+// cells never win.  idx = flat NCHW input index (layout independent).
+// Avg: window sum / (k*k) (padded cells count as zeros).
+template <class T>
+void pool_fwd(const T* x, T* y, int32_t* idx, int N, int C, int H, int W, int k, int stride, int pad, bool is_max) {
+    const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (int c = 0; c < C; ++c) {
+            const i64 base = (static_cast<i64>(n) * C + c) * H * W;
+            for (int oh = 0; oh < Ho; ++oh)
+                for (int ow = 0; ow < Wo; ++ow) {
+                    T best = T(0), sum = T(0);
+                    i64 bi = -1;
+                    for (int r = 0; r < k; ++r) {
+                        const int ih = oh * stride - pad + r;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int s = 0; s < k; ++s) {
+                            const int iw = ow * stride - pad + s;
+                            if (iw < 0 || iw >= W) continue;
+                            const T v = x[base + static_cast<i64>(ih) * W + iw];
+                            sum += v;
+                            if (bi < 0 || v > best) {
+                                best = v;
+                                bi = base + static_cast<i64>(ih) * W + iw;
+                            }
+                        }
+                    }
+                    const i64 o = ((static_cast<i64>(n) * C + c) * Ho + oh) * Wo + ow;
+                    y[o] = is_max ? best : sum / static_cast<T>(k * k);
+                    if (idx) idx[o] = static_cast<int32_t>(bi);
+                }
+        }
+}
+
+template <class T>
+void pool_bwd(const T* dy, const T* x, T* dx, int N, int C, int H, int W, int k, int stride, int pad, bool is_max) {
+    const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+    std::vector<int32_t> idx;
+    if (is_max) {
+        idx.resize(static_cast<size_t>(N) * C * Ho * Wo);
+        std::vector<T> tmp(idx.size());
+        pool_fwd(x, tmp.data(), idx.data(), N, C, H, W, k, stride, pad, true);
+    }
+    std::fill(dx, dx + static_cast<i64>(N) * C * H * W, T(0));
+    // Each (n, c) plane is independent; windows are visited in a fixed order.
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (int c = 0; c < C; ++c) {
+            const i64 ob = (static_cast<i64>(n) * C + c) * Ho * Wo;
+            const i64 ib = (static_cast<i64>(n) * C + c) * H * W;
+            for (int oh = 0; oh < Ho; ++oh)
+                for (int ow = 0; ow < Wo; ++ow) {
+                    const i64 o = ob + static_cast<i64>(oh) * Wo + ow;
+                    if (is_max) {
+                        dx[idx[o]] += dy[o];
+                        continue;
+                    }
+                    const T g = dy[o] / static_cast<T>(k * k);
+                    for (int r = 0; r < k; ++r) {
+                        const int ih = oh * stride - pad + r;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int s = 0; s < k; ++s) {
+                            const int iw = ow * stride - pad + s;
+                            if (iw >= 0 && iw < W) dx[ib + static_cast<i64>(ih) * W + iw] += g;
+                        }
+                    }
+                }
+        }
+}
+
+// ----------------------------------------------------------------- LRN (Caffe ACROSS_CHANNELS)
+//   scale_c = k + alpha/n * sum_{c' in [c - n/2, c + n/2]} a_{c'}^2 ;  b_c = a_c * scale_c^-beta
+template <class T>
+void lrn_scale(const T* x, std::vector<T>& sc, int N, int C, i64 HW, int size, double alpha, double k) {
+    sc.resize(static_cast<size_t>(N) * C * HW);
+    const int half = size / 2;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (i64 p = 0; p < HW; ++p)
+            for (int c = 0; c < C; ++c) {
+                T acc = T(0);
+                for (int cc = std::max(0, c - half); cc <= std::min(C - 1, c + half); ++cc) {
+                    const T v = x[(static_cast<i64>(n) * C + cc) * HW + p];
+                    acc += v * v;
+                }
+                sc[(static_cast<i64>(n) * C + c) * HW + p] = static_cast<T>(k) + static_cast<T>(alpha / size) * acc;
+            }
+}
+
+template <class T>
+void lrn_fwd(const T* x, T* y, int N, int C, i64 HW, int size, double alpha, double beta, double k) {
+    std::vector<T> sc;
+    lrn_scale(x, sc, N, C, HW, size, alpha, k);
+    const i64 n_el = static_cast<i64>(N) * C * HW;
+#pragma omp parallel for schedule(static)
+    for (i64 i = 0; i < n_el; ++i) y[i] = x[i] * std::pow(sc[i], static_cast<T>(-beta));
+}
+
+// dx_c = dy_c * s_c^-b  -  (2 a b / n) * x_c * sum_{c': c in window(c')} dy_c' * y_c' / s_c'
+template <class T>
+void lrn_bwd(const T* dy, const T* x, const T* y, T* dx, int N, int C, i64 HW, int size, double alpha, double beta,
+             double k) {
+    std::vector<T> sc;
+    lrn_scale(x, sc, N, C, HW, size, alpha, k);
+    const int half = size / 2;
+    const T coef = static_cast<T>(2.0 * alpha * beta / size);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (i64 p = 0; p < HW; ++p)
+            for (int c = 0; c < C; ++c) {
+                T acc = T(0);
+                for (int cc = std::max(0, c - half); cc <= std::min(C - 1, c + half); ++cc) {
+                    const i64 j = (static_cast<i64>(n) * C + cc) * HW + p;
+                    acc += dy[j] * y[j] / sc[j];
+                }
+                const i64 i = (static_cast<i64>(n) * C + c) * HW + p;
+                dx[i] = dy[i] * std::pow(sc[i], static_cast<T>(-beta)) - coef * x[i] * acc;
+            }
+}
+
+// ----------------------------------------------------------------- softmax
+template <class T>
+void softmax_fwd(const T* x, T* y, int rows, int cols) {
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < rows; ++r) {
+        const T* xr = x + static_cast<i64>(r) * cols;
+        T* yr = y + static_cast<i64>(r) * cols;
+        T m = xr[0];
+        for (int j = 1; j < cols; ++j) m = std::max(m, xr[j]);
+        T s = T(0);
+        for (int j = 0; j < cols; ++j) s += (yr[j] = std::exp(xr[j] - m));
+        for (int j = 0; j < cols; ++j) yr[j] /= s;
+    }
+}
+
+template <class T>
+void softmax_bwd(const T* dy, const T* y, T* dx, int rows, int cols) {
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < rows; ++r) {
+        const i64 o = static_cast<i64>(r) * cols;
+        T d = T(0);
+        for (int j = 0; j < cols; ++j) d += dy[o + j] * y[o + j];
+        for (int j = 0; j < cols; ++j) dx[o + j] = y[o + j] * (dy[o + j] - d);
+    }
+}
+
+// ----------------------------------------------------------------- batch norm
+// Training-mode batch statistics, biased variance, channel affine.
+template <class T>
+void bn_stats(const T* x, int N, int C, i64 HW, std::vector<T>& mean, std::vector<T>& istd, double eps) {
+    mean.assign(C, T(0));
+    istd.assign(C, T(0));
+    const T cnt = static_cast<T>(static_cast<i64>(N) * HW);
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < C; ++c) {
+        T s = T(0);
+        for (int n = 0; n < N; ++n)
+            for (i64 p = 0; p < HW; ++p) s += x[(static_cast<i64>(n) * C + c) * HW + p];
+        const T m = s / cnt;
+        T v = T(0);
+        for (int n = 0; n < N; ++n)
+            for (i64 p = 0; p < HW; ++p) {
+                const T d = x[(static_cast<i64>(n) * C + c) * HW + p] - m;
+                v += d * d;
+            }
+        mean[c] = m;
+        istd[c] = T(1) / std::sqrt(v / cnt + static_cast<T>(eps));
+    }
+}
+
+template <class T>
+void bn_fwd(const T* x, const T* g, const T* b, T* y, int N, int C, i64 HW, double eps) {
+    std::vector<T> mean, istd;
+    bn_stats(x, N, C, HW, mean, istd, eps);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; ++n)
+        for (int c = 0; c < C; ++c)
+            for (i64 p = 0; p < HW; ++p) {
+                const i64 i = (static_cast<i64>(n) * C + c) * HW + p;
+                y[i] = g[c] * (x[i] - mean[c]) * istd[c] + b[c];
+            }
+}
+
+template <class T>
+void bn_bwd(const T* dy, const T* x, const T* g, T* dx, T* dg, T* db, int N, int C, i64 HW, double eps) {
+    std::vector<T> mean, istd;
+    bn_stats(x, N, C, HW, mean, istd, eps);
+    const T cnt = static_cast<T>(static_cast<i64>(N) * HW);
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < C; ++c) {
+        T sdy = T(0), sdyx = T(0);
+        for (int n = 0; n < N; ++n)
+            for (i64 p = 0; p < HW; ++p) {
+                const i64 i = (static_cast<i64>(n) * C + c) * HW + p;
+                sdy += dy[i];
+                sdyx += dy[i] * (x[i] - mean[c]) * istd[c];
+            }
+        if (dg) dg[c] = sdyx;
+        if (db) db[c] = sdy;
+        if (dx) {
+            const T gs = (g ? g[c] : T(1)) * istd[c];
+            for (int n = 0; n < N; ++n)
+                for (i64 p = 0; p < HW; ++p) {
+                    const i64 i = (static_cast<i64>(n) * C + c) * HW + p;
+                    const T xh = (x[i] - mean[c]) * istd[c];
+                    dx[i] = gs * (dy[i] - sdy / cnt - xh * sdyx / cnt);
+                }
+        }
+    }
+}
+
+// ================================================================= plan execution
+struct PoolSim {  // best-fit pool, reuse or dealloc mode
+    bool reuse = false;
+    std::multimap<i64, int> free_blocks;  // bytes -> block id
+    std::unordered_map<int, std::pair<int, i64>> held;  // storage -> (block, bytes)
+    int next_block = 0;
+    orc_pool_stats st{};
+    void acquire(int storage, i64 bytes) {
+        if (reuse) {
+            auto it = free_blocks.lower_bound(bytes);
+            if (it != free_blocks.end()) {
+                held[storage] = {it->second, it->first};
+                free_blocks.erase(it);
+                st.reuses++;
+                st.live_bytes += bytes;
+                st.peak_bytes = std::max(st.peak_bytes, st.live_bytes);
+                return;
+            }
+        }
+        held[storage] = {next_block++, bytes};
+        st.allocs_from_os++;
+        st.os_bytes += bytes;
+        st.live_bytes += bytes;
+        st.peak_bytes = std::max(st.peak_bytes, st.live_bytes);
+    }
+    void release(int storage) {
+        auto it = held.find(storage);
+        if (it == held.end()) return;
+        st.releases++;
+        st.live_bytes -= it->second.second;
+        if (reuse) free_blocks.emplace(it->second.second, it->second.first);
+        else st.os_bytes -= it->second.second;
+        held.erase(it);
+    }
+};
+
+i64 count_of(const int64_t* d, int rank) {
+    i64 n = 1;
+    for (int i = 0; i < rank; ++i) n *= d[i];
+    return n;
+}
+
+struct Dims {
+    int rank = 0;
+    int64_t d[4] = {1, 1, 1, 1};
+    i64 count() const { return count_of(d, rank); }
+    i64 hw() const { return rank == 4 ? d[2] * d[3] : 1; }
+};
+
+class CtxBase {
+public:
+    virtual ~CtxBase() = default;
+};
+
+template <class T>
+class Exec : public CtxBase {
+public:
+    Exec(const tc_plan* p, uint64_t seed) : plan_(p), seed_(seed) {
+        params_.resize(p->nparams);
+        vel_.resize(p->nparams);
+        grads_.resize(p->nparams);
+        for (int i = 0; i < p->nparams; ++i) {
+            const i64 n = count_of(p->params[i].dims, p->params[i].rank);
+            params_[i].assign(n, T(0));
+            vel_[i].assign(n, T(0));
+        }
+        for (int i = 0; i < p->nvars; ++i) {
+            Dims d;
+            d.rank = p->vars[i].rank;
+            for (int j = 0; j < d.rank; ++j) d.d[j] = p->vars[i].dims[j];
+            vdims_[p->vars[i].id] = d;
+        }
+        for (int i = 0; i < p->nstmts; ++i)
+            if (p->stmts[i].kind == TC_STMT_LET) var_storage_[p->stmts[i].var] = p->stmts[i].storage;
+        pool_.reuse = p->mode == TC_MODE_REUSE;
+    }
+
+    const tc_plan* plan_;
+    uint64_t seed_;
+    std::vector<std::vector<T>> params_, vel_, grads_;
+    std::unordered_map<int, Dims> vdims_;
+    std::unordered_map<int, int> var_storage_;
+    std::unordered_map<int, std::vector<T>> store_;
+    std::vector<float> bx_;
+    std::vector<int32_t> by_;
+    bool have_batch_ = false;
+    PoolSim pool_;
+    std::vector<i64> trace_;
+    double ws_cap_mb_ = -1.0;
+    int iter_ = 0, n0_ = 0;
+
+    void init_params() {
+        for (int i = 0; i < plan_->nparams; ++i) {
+            const tc_param_desc& pd = plan_->params[i];
+            std::vector<T>& w = params_[i];
+            if (pd.init_kind == TC_INIT_CONSTANT) {
+                std::fill(w.begin(), w.end(), static_cast<T>(static_cast<float>(pd.init_value)));
+            } else if (pd.init_kind == TC_INIT_XAVIER) {
+                const double a = std::sqrt(6.0 / static_cast<double>(pd.fan_in + pd.fan_out));
+                for (size_t j = 0; j < w.size(); ++j)
+                    w[j] = static_cast<T>(static_cast<float>((2.0 * tcp_param_uniform(seed_, i, static_cast<uint32_t>(j)) - 1.0) * a));
+            } else {
+                for (size_t j = 0; j < w.size(); ++j) {
+                    const double u1 = tcp_param_uniform(seed_, i, static_cast<uint32_t>(2 * j));
+                    const double u2 = tcp_param_uniform(seed_, i, static_cast<uint32_t>(2 * j + 1));
+                    w[j] = static_cast<T>(static_cast<float>(pd.sigma * std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2)));
+                }
+            }
+            std::fill(vel_[i].begin(), vel_[i].end(), T(0));
+        }
+    }
+
+    const T* get(const tc_ref& r, Dims* d = nullptr) {
+        if (r.kind == TC_REF_PARAM) {
+            if (d) {
+                const tc_param_desc& pd = plan_->params[r.index];
+                d->rank = pd.rank;
+                for (int j = 0; j < pd.rank; ++j) d->d[j] = pd.dims[j];
+            }
+            return params_[r.index].data();
+        }
+        if (d) *d = vdims_.at(r.index);
+        auto it = store_.find(var_storage_.at(r.index));
+        if (it == store_.end()) throw std::runtime_error("oracle: read of freed/undefined var X" + std::to_string(r.index));
+        return it->second.data();
+    }
+
+    // Evaluate the right-hand side of a Let / Update into `out` (shape `od`).
+    void eval(const tc_stmt& s, std::vector<T>& out, const Dims& od) {
+        out.assign(od.count(), T(0));
+        T* y = out.data();
+        Dims a, b, c;
+        switch (s.op) {
+            case TC_OP_LOAD_X:
+                for (i64 i = 0; i < od.count(); ++i) y[i] = static_cast<T>(bx_[i]);
+                return;
+            case TC_OP_LOAD_Y:
+                for (int n = 0; n < od.d[0]; ++n) y[static_cast<i64>(n) * od.d[1] + by_[n]] = T(1);
+                return;
+            case TC_OP_CONV_FWD: {
+                const T* x = get(s.in[0], &a);
+                const T* w = get(s.in[1], &b);
+                const T* bias = s.nin > 2 ? get(s.in[2]) : nullptr;
+                bool direct = false;
+                if (ws_cap_mb_ >= 0) {
+                    const double col_mb = 4.0 * a.d[0] * a.d[1] * b.d[2] * b.d[3] * od.d[2] * od.d[3] / 1e6;
+                    direct = col_mb > ws_cap_mb_;  // SPEC.md:525 workspace fallback
+                }
+                conv_fwd(x, w, bias, y, a.d[0], a.d[1], a.d[2], a.d[3], b.d[0], b.d[2], b.d[3], s.stride, s.pad, direct);
+                return;
+            }
+            case TC_OP_CONV_BWD_DATA: {
+                const T* dy = get(s.in[0], &a);
+                const T* w = get(s.in[1], &b);
+                conv_bwd_data(dy, w, y, od.d[0], od.d[1], od.d[2], od.d[3], b.d[0], b.d[2], b.d[3], s.stride, s.pad);
+                return;
+            }
+            case TC_OP_CONV_BWD_FILTER: {
+                const T* dy = get(s.in[0], &a);
+                const T* x = get(s.in[1], &b);
+                conv_bwd_filter(dy, x, y, b.d[0], b.d[1], b.d[2], b.d[3], a.d[1], od.d[2], od.d[3], s.stride, s.pad);
+                return;
+            }
+            case TC_OP_CONV_BWD_BIAS: {
+                const T* dy = get(s.in[0], &a);
+                conv_bwd_bias(dy, y, a.d[0], a.d[1], a.hw());
+                return;
+            }
+            case TC_OP_POOL_FWD: {
+                const T* x = get(s.in[0], &a);
+                pool_fwd<T>(x, y, nullptr, a.d[0], a.d[1], a.d[2], a.d[3], s.k, s.stride, s.pad, s.max_pool);
+                return;
+            }
+            case TC_OP_POOL_BWD: {
+                const T* dy = get(s.in[0]);
+                const T* x = get(s.in[2], &c);
+                pool_bwd(dy, x, y, c.d[0], c.d[1], c.d[2], c.d[3], s.k, s.stride, s.pad, s.max_pool);
+                return;
+            }
+            case TC_OP_RELU_FWD: {
+                const T* x = get(s.in[0]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = x[i] > T(0) ? x[i] : T(0);
+                return;
+            }
+            case TC_OP_RELU_BWD: {
+                const T* dy = get(s.in[0]);
+                const T* fy = get(s.in[1]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = fy[i] > T(0) ? dy[i] : T(0);
+                return;
+            }
+            case TC_OP_SOFTMAX_FWD: softmax_fwd(get(s.in[0]), y, od.d[0], od.d[1]); return;
+            case TC_OP_SOFTMAX_BWD: softmax_bwd(get(s.in[0]), get(s.in[1]), y, od.d[0], od.d[1]); return;
+            case TC_OP_LRN_FWD: {
+                const T* x = get(s.in[0], &a);
+                lrn_fwd(x, y, a.d[0], a.d[1], a.hw(), s.lrn_size, s.alpha, s.beta, s.lrn_k);
+                return;
+            }
+            case TC_OP_LRN_BWD: {
+                const T* dy = get(s.in[0]);
+                const T* fy = get(s.in[1]);
+                const T* x = get(s.in[2], &a);
+                lrn_bwd(dy, x, fy, y, a.d[0], a.d[1], a.hw(), s.lrn_size, s.alpha, s.beta, s.lrn_k);
+                return;
+            }
+            case TC_OP_DROPOUT_MASK: {
+                const i64 per = od.count() / od.d[0];
+                for (int n = 0; n < od.d[0]; ++n)
+                    for (i64 e = 0; e < per; ++e)
+                        y[n * per + e] = static_cast<T>(tcp_dropout_value(seed_, static_cast<uint32_t>(s.var),
+                                                                          static_cast<uint32_t>(n0_ + n),
+                                                                          static_cast<uint32_t>(iter_),
+                                                                          static_cast<uint32_t>(e), static_cast<float>(s.rate)));
+                return;
+            }
+            case TC_OP_MUL: {
+                const T* p = get(s.in[0]);
+                const T* q = get(s.in[1]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] * q[i];
+                return;
+            }
+            case TC_OP_ADD: {
+                const T* p = get(s.in[0]);
+                const T* q = get(s.in[1]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] + q[i];
+                return;
+            }
+            case TC_OP_SCALE: {
+                const T* p = get(s.in[0]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] * static_cast<T>(s.scale);
+                return;
+            }
+            case TC_OP_LOG: {  // clamp at 1e-30 before Log
+                const T* p = get(s.in[0]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = std::log(std::max(p[i], static_cast<T>(1e-30)));
+                return;
+            }
+            case TC_OP_RECIP: {
+                const T* p = get(s.in[0]);
+                for (i64 i = 0; i < od.count(); ++i) y[i] = T(1) / std::max(p[i], static_cast<T>(1e-30));
+                return;
+            }
+            case TC_OP_MATMUL_FWD: {  // Y[N,out] = A[N,in] W[out,in]^T
+                const T* A = get(s.in[0], &a);
+                const T* W = get(s.in[1], &b);
+                const int in = static_cast<int>(b.d[1]);
+                gemm<T>(static_cast<int>(od.d[0]), static_cast<int>(od.d[1]), in, A, in, false, W, in, true, y, od.d[1], false);
+                return;
+            }
+            case TC_OP_MATMUL_BWD_DATA: {  // dA[N,in] = up[N,out] W[out,in]
+                const T* up = get(s.in[0], &a);
+                const T* W = get(s.in[1], &b);
+                gemm<T>(static_cast<int>(a.d[0]), static_cast<int>(b.d[1]), static_cast<int>(b.d[0]), up, a.d[1], false, W,
+                        b.d[1], false, y, b.d[1], false);
+                return;
+            }
+            case TC_OP_MATMUL_BWD_W: {  // dW[out,in] = up[N,out]^T A[N,in]
+                const T* up = get(s.in[0], &a);
+                const T* A = get(s.in[1], &b);
+                const i64 in = b.count() / b.d[0];
+                gemm<T>(static_cast<int>(a.d[1]), static_cast<int>(in), static_cast<int>(a.d[0]), up, a.d[1], true, A, in,
+                        false, y, in, false);
+                return;
+            }
+            case TC_OP_BIAS_ADD: {
+                const T* x = get(s.in[0], &a);
+                const T* bb = get(s.in[1]);
+                const i64 C = a.d[1], hw = a.hw();
+                for (i64 i = 0; i < od.count(); ++i) y[i] = x[i] + bb[(i / hw) % C];
+                return;
+            }
+            case TC_OP_BIAS_GRAD: {
+                const T* up = get(s.in[0], &a);
+                conv_bwd_bias(up, y, static_cast<int>(a.d[0]), static_cast<int>(a.d[1]), a.hw());
+                return;
+            }
+            case TC_OP_CONCAT: {
+                i64 off = 0;
+                for (int t = 0; t < s.nin; ++t) {
+                    const T* p = get(s.in[t], &a);
+                    const i64 C = a.d[1], hw = a.hw();
+                    for (int n = 0; n < od.d[0]; ++n)
+                        std::memcpy(y + (n * od.d[1] + off) * hw, p + n * C * hw, sizeof(T) * C * hw);
+                    off += C;
+                }
+                return;
+            }
+            case TC_OP_CONCAT_BWD: {
+                const T* up = get(s.in[0], &a);
+                const i64 hw = a.hw();
+                for (int n = 0; n < od.d[0]; ++n)
+                    std::memcpy(y + n * s.extent * hw, up + (n * a.d[1] + s.offset) * hw, sizeof(T) * s.extent * hw);
+                return;
+            }
+            case TC_OP_BN_FWD: {
+                const T* x = get(s.in[0], &a);
+                bn_fwd(x, get(s.in[1]), get(s.in[2]), y, a.d[0], a.d[1], a.hw(), s.eps);
+                return;
+            }
+            case TC_OP_BN_BWD_DATA: {
+                const T* up = get(s.in[0]);
+                const T* x = get(s.in[1], &a);
+                bn_bwd<T>(up, x, get(s.in[2]), y, nullptr, nullptr, a.d[0], a.d[1], a.hw(), s.eps);
+                return;
+            }
+            case TC_OP_BN_BWD_GAMMA: {
+                const T* up = get(s.in[0]);
+                const T* x = get(s.in[1], &a);
+                bn_bwd<T>(up, x, nullptr, nullptr, y, nullptr, a.d[0], a.d[1], a.hw(), s.eps);
+                return;
+            }
+            case TC_OP_BN_BWD_BETA: {
+                const T* up = get(s.in[0], &a);
+                conv_bwd_bias(up, y, static_cast<int>(a.d[0]), static_cast<int>(a.d[1]), a.hw());
+                return;
+            }
+            default: throw std::runtime_error("oracle: unsupported op " + std::to_string(s.op));
+        }
+    }
+
+    double step(int iter, int n0, bool update, bool keep) {
+        iter_ = iter;
+        n0_ = n0;
+        if (!have_batch_) synth(iter, n0);
+        have_batch_ = false;
+        store_.clear();
+        pool_.held.clear();
+        pool_.st.live_bytes = 0;
+        trace_.clear();
+        double loss = 0.0;
+        std::vector<T> tmp;
+        for (int i = 0; i < plan_->nstmts; ++i) {
+            const tc_stmt& s = plan_->stmts[i];
+            switch (s.kind) {
+                case TC_STMT_LET: {
+                    Dims od;
+                    od.rank = s.rank;
+                    for (int j = 0; j < s.rank; ++j) od.d[j] = s.dims[j];
+                    eval(s, tmp, od);
+                    if (!s.inplace) pool_.acquire(s.storage, od.count() * 4);
+                    store_[s.storage] = tmp;  // in place: same storage, new contents
+                    break;
+                }
+                case TC_STMT_DEALLOC:
+                    if (!keep) store_.erase(s.storage);
+                    pool_.release(s.storage);
+                    break;
+                case TC_STMT_UPDATE: {
+                    const tc_param_desc& pd = plan_->params[s.param];
+                    Dims od;
+                    od.rank = pd.rank;
+                    for (int j = 0; j < pd.rank; ++j) od.d[j] = pd.dims[j];
+                    eval(s, tmp, od);
+                    grads_[s.param] = tmp;
+                    if (update) {
+                        // v = momentum*v + lr_alpha*(g + decay*p); p = p + v
+                        std::vector<T>& p = params_[s.param];
+                        std::vector<T>& v = vel_[s.param];
+                        for (size_t j = 0; j < p.size(); ++j) {
+                            v[j] = static_cast<T>(s.momentum) * v[j] + static_cast<T>(s.lr_alpha) * (tmp[j] + static_cast<T>(s.decay) * p[j]);
+                            p[j] += v[j];
+                        }
+                    }
+                    break;
+                }
+                case TC_STMT_PRINT: {
+                    double l = 0.0;
+                    for (int t = 0; t < s.nterms; ++t) {
+                        Dims d;
+                        const T* yv = get(s.in[2 * t], &d);
+                        const T* lv = get(s.in[2 * t + 1]);
+                        double dot = 0.0;
+                        for (i64 j = 0; j < d.count(); ++j) dot += static_cast<double>(yv[j]) * static_cast<double>(lv[j]);
+                        l += s.coef[t] * dot;
+                    }
+                    loss = l;
+                    break;
+                }
+            }
+            trace_.push_back(pool_.st.live_bytes);
+        }
+        return loss;
+    }
+
+    double test(int iter, int n0) {
+        iter_ = iter;
+        n0_ = n0;
+        if (!have_batch_) synth(iter, n0);
+        have_batch_ = false;
+        store_.clear();
+        std::vector<T> tmp;
+        for (int i = 0; i < plan_->ntest; ++i) {
+            const tc_stmt& s = plan_->test_stmts[i];
+            Dims od;
+            od.rank = s.rank;
+            for (int j = 0; j < s.rank; ++j) od.d[j] = s.dims[j];
+            if (s.op == TC_OP_DROPOUT_MASK) {  // test-mode dropout = identity
+                tmp.assign(od.count(), T(1));
+            } else {
+                eval(s, tmp, od);
+            }
+            store_[s.storage] = tmp;
+        }
+        Dims d;
+        const T* lg = get(tc_ref{TC_REF_VAR, plan_->logits_var}, &d);
+        int hit = 0;
+        for (int n = 0; n < d.d[0]; ++n) {
+            const T* r = lg + n * d.d[1];
+            const int am = static_cast<int>(std::max_element(r, r + d.d[1]) - r);
+            hit += am == by_[n];
+        }
+        return static_cast<double>(hit) / static_cast<double>(d.d[0]);
+    }
+
+    void synth(int iter, int n0) {
+        const i64 per = plan_->input_dims[1] * plan_->input_dims[2] * plan_->input_dims[3];
+        bx_.resize(plan_->batch * per);
+        by_.resize(plan_->batch);
+        orc_synth_batch(plan_, seed_, iter, n0, bx_.data(), by_.data());
+    }
+};
+
+struct Holder {
+    std::unique_ptr<Exec<float>> f;
+    std::unique_ptr<Exec<double>> d;
+};
+
+}  // namespace
+
+struct orc_ctx {
+    Holder h;
+};
+
+template <class Fn>
+static auto with(orc_ctx* c, Fn&& fn) {
+    return c->h.f ? fn(*c->h.f) : fn(*c->h.d);
+}
+
+extern "C" {
+
+#define ORC_DEF(T, sfx)                                                                                          \
+    void orc_conv_fwd_##sfx(const T* x, const T* w, const T* b, T* y, int N, int C, int H, int W, int K, int R,   \
+                            int S, int stride, int pad, int direct) {                                            \
+        conv_fwd(x, w, b, y, N, C, H, W, K, R, S, stride, pad, direct != 0);                                     \
+    }                                                                                                            \
+    void orc_conv_bwd_data_##sfx(const T* dy, const T* w, T* dx, int N, int C, int H, int W, int K, int R, int S, \
+                                 int stride, int pad) {                                                          \
+        conv_bwd_data(dy, w, dx, N, C, H, W, K, R, S, stride, pad);                                              \
+    }                                                                                                            \
+    void orc_conv_bwd_filter_##sfx(const T* dy, const T* x, T* dw, int N, int C, int H, int W, int K, int R,      \
+                                   int S, int stride, int pad) {                                                 \
+        conv_bwd_filter(dy, x, dw, N, C, H, W, K, R, S, stride, pad);                                            \
+    }                                                                                                            \
+    void orc_conv_bwd_bias_##sfx(const T* dy, T* db, int N, int K, int HW) { conv_bwd_bias(dy, db, N, K, HW); }   \
+    void orc_pool_fwd_##sfx(const T* x, T* y, int32_t* idx, int N, int C, int H, int W, int k, int stride,        \
+                            int pad, int is_max) {                                                               \
+        pool_fwd(x, y, idx, N, C, H, W, k, stride, pad, is_max != 0);                                            \
+    }                                                                                                            \
+    void orc_pool_bwd_##sfx(const T* dy, const T* x, T* dx, int N, int C, int H, int W, int k, int stride,        \
+                            int pad, int is_max) {                                                               \
+        pool_bwd(dy, x, dx, N, C, H, W, k, stride, pad, is_max != 0);                                            \
+    }                                                                                                            \
+    void orc_lrn_fwd_##sfx(const T* x, T* y, int N, int C, int HW, int size, double alpha, double beta,          \
+                           double k) {                                                                           \
+        lrn_fwd(x, y, N, C, HW, size, alpha, beta, k);                                                           \
+    }                                                                                                            \
+    void orc_lrn_bwd_##sfx(const T* dy, const T* x, const T* y, T* dx, int N, int C, int HW, int size,           \
+                           double alpha, double beta, double k) {                                                \
+        lrn_bwd(dy, x, y, dx, N, C, HW, size, alpha, beta, k);                                                   \
+    }                                                                                                            \
+    void orc_softmax_fwd_##sfx(const T* x, T* y, int rows, int cols) { softmax_fwd(x, y, rows, cols); }           \
+    void orc_softmax_bwd_##sfx(const T* dy, const T* y, T* dx, int rows, int cols) {                              \
+        softmax_bwd(dy, y, dx, rows, cols);                                                                      \
+    }                                                                                                            \
+    void orc_bn_fwd_##sfx(const T* x, const T* g, const T* b, T* y, int N, int C, int HW, double eps) {          \
+        bn_fwd(x, g, b, y, N, C, HW, eps);                                                                       \
+    }                                                                                                            \
+    void orc_bn_bwd_##sfx(const T* dy, const T* x, const T* g, T* dx, T* dg, T* dbeta, int N, int C, int HW,      \
+                          double eps) {                                                                          \
+        bn_bwd(dy, x, g, dx, dg, dbeta, N, C, HW, eps);                                                          \
+    }                                                                                                            \
+    void orc_matmul_##sfx(const T* A, const T* B, T* C, int M, int N, int K, int ta, int tb) {                   \
+        gemm<T>(M, N, K, A, ta ? M : K, ta != 0, B, tb ? K : N, tb != 0, C, N, false);                            \
+    }
+
+ORC_DEF(float, f32)
+ORC_DEF(double, f64)
+#undef ORC_DEF
+
+orc_ctx* orc_create(const tc_plan* plan, uint64_t seed, int f64, int threads) {
+    if (threads > 0) omp_set_num_threads(threads);
+    auto* c = new orc_ctx;
+    if (f64) c->h.d = std::make_unique<Exec<double>>(plan, seed);
+    else c->h.f = std::make_unique<Exec<float>>(plan, seed);
+    return c;
+}
+void orc_destroy(orc_ctx* c) { delete c; }
+
+void orc_init_params(orc_ctx* c) {
+    with(c, [](auto& e) { e.init_params(); return 0; });
+}
+void orc_param_get(orc_ctx* c, int i, float* out) {
+    with(c, [&](auto& e) { for (size_t j = 0; j < e.params_[i].size(); ++j) out[j] = static_cast<float>(e.params_[i][j]); return 0; });
+}
+void orc_param_set(orc_ctx* c, int i, const float* in) {
+    with(c, [&](auto& e) { for (size_t j = 0; j < e.params_[i].size(); ++j) e.params_[i][j] = in[j]; return 0; });
+}
+void orc_param_get_f64(orc_ctx* c, int i, double* out) {
+    with(c, [&](auto& e) { for (size_t j = 0; j < e.params_[i].size(); ++j) out[j] = static_cast<double>(e.params_[i][j]); return 0; });
+}
+void orc_param_set_f64(orc_ctx* c, int i, const double* in) {
+    with(c, [&](auto& e) {
+        using T = typename std::decay_t<decltype(e.params_[0])>::value_type;
+        for (size_t j = 0; j < e.params_[i].size(); ++j) e.params_[i][j] = static_cast<T>(in[j]);
+        return 0;
+    });
+}
+void orc_velocity_get(orc_ctx* c, int i, float* out) {
+    with(c, [&](auto& e) { for (size_t j = 0; j < e.vel_[i].size(); ++j) out[j] = static_cast<float>(e.vel_[i][j]); return 0; });
+}
+
+void orc_synth_batch(const tc_plan* plan, uint64_t seed, int iter, int n0, float* x, int32_t* labels) {
+    const i64 per = plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
+    const uint32_t K = static_cast<uint32_t>(plan->classes);
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < static_cast<int>(plan->batch); ++n) {
+        const uint32_t ng = static_cast<uint32_t>(n0 + n);
+        const uint32_t y = tcp_label(seed, ng, static_cast<uint32_t>(iter), K);
+        labels[n] = static_cast<int32_t>(y);
+        for (i64 e = 0; e < per; ++e) {
+            float u1, u2;
+            tcp_uniform_pair(seed, ng, static_cast<uint32_t>(iter), static_cast<uint32_t>(e), &u1, &u2);
+            const double r = std::sqrt(-2.0 * std::log(static_cast<double>(u1)));
+            const double t = 6.283185307179586 * static_cast<double>(u2);
+            const double z = (e & 1) ? r * std::sin(t) : r * std::cos(t);
+            x[n * per + e] = static_cast<float>(static_cast<double>(tcp_centroid(seed, y, static_cast<uint32_t>(e))) + 0.1 * z);
+        }
+    }
+}
+
+void orc_set_batch(orc_ctx* c, const float* x, const int32_t* labels) {
+    with(c, [&](auto& e) {
+        const i64 per = e.plan_->input_dims[1] * e.plan_->input_dims[2] * e.plan_->input_dims[3];
+        e.bx_.assign(x, x + e.plan_->batch * per);
+        e.by_.assign(labels, labels + e.plan_->batch);
+        e.have_batch_ = true;
+        return 0;
+    });
+}
+
+double orc_step(orc_ctx* c, int iter, int n0, int update, int keep) {
+    try {
+        return with(c, [&](auto& e) { return e.step(iter, n0, update != 0, keep != 0); });
+    } catch (const std::exception& ex) {
+        std::fprintf(stderr, "orc_step: %s\n", ex.what());
+        return std::nan("");
+    }
+}
+double orc_test(orc_ctx* c, int iter, int n0) {
+    return with(c, [&](auto& e) { return e.test(iter, n0); });
+}
+
+int orc_var_get(orc_ctx* c, int var, float* out, int64_t max_elems) {
+    return with(c, [&](auto& e) -> int {
+        auto si = e.var_storage_.find(var);
+        if (si == e.var_storage_.end()) return -1;
+        auto it = e.store_.find(si->second);
+        if (it == e.store_.end()) return -2;
+        const i64 n = std::min<i64>(max_elems, static_cast<i64>(it->second.size()));
+        for (i64 j = 0; j < n; ++j) out[j] = static_cast<float>(it->second[j]);
+        return static_cast<int>(n);
+    });
+}
+
+int orc_grad_get(orc_ctx* c, int index, double* out, int64_t max_elems) {
+    return with(c, [&](auto& e) -> int {
+        const auto& g = e.grads_[index];
+        const i64 n = std::min<i64>(max_elems, static_cast<i64>(g.size()));
+        for (i64 j = 0; j < n; ++j) out[j] = static_cast<double>(g[j]);
+        return static_cast<int>(n);
+    });
+}
+
+void orc_pool_stats_get(orc_ctx* c, orc_pool_stats* s) {
+    with(c, [&](auto& e) { *s = e.pool_.st; return 0; });
+}
+
+int orc_live_trace(orc_ctx* c, int64_t* out, int max) {
+    return with(c, [&](auto& e) -> int {
+        const int n = std::min<int>(max, static_cast<int>(e.trace_.size()));
+        for (int j = 0; j < n; ++j) out[j] = e.trace_[j];
+        return n;
+    });
+}
+
+void orc_set_workspace_cap(orc_ctx* c, double mb) {
+    with(c, [&](auto& e) { e.ws_cap_mb_ = mb; return 0; });
+}
+
+}  // extern "C"

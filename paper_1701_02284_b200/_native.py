@@ -52,7 +52,92 @@ class ConvDesc(C.Structure):
     ]
 
 
+TC_MAX_IN = 8
+TC_STMT_LET, TC_STMT_DEALLOC, TC_STMT_UPDATE, TC_STMT_PRINT = 0, 1, 2, 3
+TC_REF_NONE, TC_REF_VAR, TC_REF_PARAM = 0, 1, 2
+TC_MODE_REUSE, TC_MODE_DEALLOC = 0, 1
+OP_NAMES = [
+    "NONE", "LOAD_X", "LOAD_Y", "CONV_FWD", "CONV_BWD_DATA", "CONV_BWD_FILTER", "CONV_BWD_BIAS", "POOL_FWD",
+    "POOL_BWD", "RELU_FWD", "RELU_BWD", "SOFTMAX_FWD", "SOFTMAX_BWD", "LRN_FWD", "LRN_BWD", "DROPOUT_MASK", "MUL",
+    "ADD", "MATMUL_FWD", "MATMUL_BWD_DATA", "MATMUL_BWD_W", "BIAS_ADD", "BIAS_GRAD", "LOG", "RECIP", "SCALE",
+    "CONCAT", "CONCAT_BWD", "BN_FWD", "BN_BWD_DATA", "BN_BWD_GAMMA", "BN_BWD_BETA", "PRINT_LOSS",
+]
+
+
+class Ref(C.Structure):
+    _fields_ = [("kind", C.c_int), ("index", C.c_int)]
+
+
+class Stmt(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("op", C.c_int), ("var", C.c_int), ("storage", C.c_int), ("inplace", C.c_int),
+        ("param", C.c_int), ("nin", C.c_int), ("inp", Ref * TC_MAX_IN), ("rank", C.c_int),
+        ("dims", C.c_int64 * 4), ("bytes", C.c_int64),
+        ("k", C.c_int), ("stride", C.c_int), ("pad", C.c_int), ("max_pool", C.c_int), ("has_bias", C.c_int),
+        ("lrn_size", C.c_int), ("slot", C.c_int),
+        ("alpha", C.c_double), ("beta", C.c_double), ("lrn_k", C.c_double), ("rate", C.c_double),
+        ("scale", C.c_double), ("eps", C.c_double), ("offset", C.c_int64), ("extent", C.c_int64),
+        ("lr_alpha", C.c_double), ("momentum", C.c_double), ("decay", C.c_double),
+        ("nterms", C.c_int), ("coef", C.c_double * 4),
+    ]
+
+
+class ParamDesc(C.Structure):
+    _fields_ = [
+        ("name", C.c_char * 64), ("rank", C.c_int), ("dims", C.c_int64 * 4), ("init_kind", C.c_int),
+        ("init_value", C.c_double), ("sigma", C.c_double), ("lr_mult", C.c_double), ("decay_mult", C.c_double),
+        ("fan_in", C.c_int64), ("fan_out", C.c_int64),
+    ]
+
+
+class VarDesc(C.Structure):
+    _fields_ = [("id", C.c_int), ("rank", C.c_int), ("dims", C.c_int64 * 4)]
+
+
+class Plan(C.Structure):
+    _fields_ = [
+        ("name", C.c_char_p), ("batch", C.c_int64), ("classes", C.c_int64), ("input_dims", C.c_int64 * 4),
+        ("nparams", C.c_int), ("params", C.POINTER(ParamDesc)),
+        ("nstmts", C.c_int), ("stmts", C.POINTER(Stmt)),
+        ("ntest", C.c_int), ("test_stmts", C.POINTER(Stmt)), ("logits_var", C.c_int),
+        ("nvars", C.c_int), ("vars", C.POINTER(VarDesc)), ("max_var", C.c_int),
+        ("lr", C.c_double), ("momentum", C.c_double), ("decay", C.c_double), ("clip", C.c_double),
+        ("mode", C.c_int),
+    ]
+
+
+class MemSummary(C.Structure):
+    _fields_ = [
+        ("peak_dealloc_mb", C.c_double), ("peak_reuse_mb", C.c_double), ("param_mb", C.c_double),
+        ("workspace_mb", C.c_double), ("peak_dealloc_bytes", C.c_int64), ("peak_reuse_bytes", C.c_int64),
+        ("param_bytes", C.c_int64), ("workspace_bytes", C.c_int64),
+    ]
+
+
+class CompileOpts(C.Structure):
+    _fields_ = [
+        ("lr", C.c_double), ("momentum", C.c_double), ("decay", C.c_double), ("clip", C.c_double),
+        ("mode", C.c_int), ("workspace_cap_mb", C.c_double), ("greedy_schedule", C.c_int),
+    ]
+
+
 _lib = None
+
+
+def _bind_plan(L: C.CDLL) -> None:
+    L.tc_net_compile.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
+    L.tc_net_destroy.argtypes = [C.c_void_p]
+    L.tc_net_destroy.restype = None
+    L.tc_net_plan.argtypes = [C.c_void_p]
+    L.tc_net_plan.restype = C.POINTER(Plan)
+    for fn in ("tc_net_ir_text", "tc_net_verify"):
+        getattr(L, fn).argtypes = [C.c_void_p]
+        getattr(L, fn).restype = C.c_char_p
+    L.tc_net_memory_table.argtypes = [C.c_void_p, C.c_int]
+    L.tc_net_memory_table.restype = C.c_char_p
+    L.tc_net_stmt_text.argtypes = [C.c_void_p, C.c_int]
+    L.tc_net_stmt_text.restype = C.c_char_p
+    L.tc_net_memory_summary.argtypes = [C.c_void_p, C.POINTER(MemSummary)]
 
 
 def lib() -> C.CDLL:
@@ -76,6 +161,7 @@ def lib() -> C.CDLL:
                                            C.c_size_t, C.c_void_p]
         L.tc_conv2d_workspace_bytes.argtypes = [C.POINTER(ConvDesc), C.c_int]
         L.tc_conv2d_workspace_bytes.restype = C.c_size_t
+        _bind_plan(L)
         _lib = L
     return _lib
 

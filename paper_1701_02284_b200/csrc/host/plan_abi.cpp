@@ -1,0 +1,296 @@
+// C ABI of the plan producers (tc_plan.h): compile a configured network and
+// expose its IrProgram as flat tc_stmt records.  This is the only place the
+// host compiler's C++ types meet the C boundary; exceptions stop here.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "host/compiler.hpp"
+#include "status.hpp"
+#include "tc_plan.h"
+
+using namespace tensorc;
+
+struct tc_net {
+    NetworkDef net;
+    IrProgram prog;
+    MemoryReport report;
+    std::vector<tc_param_desc> params;
+    std::vector<tc_stmt> stmts, test;
+    std::vector<tc_var_desc> vars;
+    tc_plan plan{};
+    std::string ir_text, table_text, table_csv, verify_text;
+};
+
+namespace {
+
+struct Flattener {
+    const IrProgram& p;
+    std::unordered_map<const ParamSpec*, int> pindex;
+
+    explicit Flattener(const IrProgram& prog) : p(prog) {
+        for (std::size_t i = 0; i < p.params.size(); ++i) pindex[p.params[i].get()] = static_cast<int>(i);
+    }
+
+    tc_ref ref(const TPtr& t) {
+        TPtr b = base_of(t);
+        if (b->kind == TKind::Param) return tc_ref{TC_REF_PARAM, pindex.at(b->param.get())};
+        return tc_ref{TC_REF_VAR, b->id};
+    }
+
+    void hyper(tc_stmt& s, const Hyper& h) {
+        s.k = h.k;
+        s.stride = h.stride;
+        s.pad = h.pad;
+        s.max_pool = h.max_pool;
+        s.has_bias = h.has_bias;
+        s.lrn_size = h.lrn_size;
+        s.alpha = h.alpha;
+        s.beta = h.beta;
+        s.lrn_k = h.lrn_k;
+        s.rate = h.rate;
+        s.scale = h.scale;
+        s.eps = h.eps;
+        s.offset = h.offset;
+        s.extent = h.extent;
+    }
+
+    void add(tc_stmt& s, const TPtr& t) { s.in[s.nin++] = ref(t); }
+
+    // op code + operand list of the expression computing a Let / Update.
+    void rhs(tc_stmt& s, const TPtr& n) {
+        hyper(s, n->hyper);
+        s.slot = n->slot;
+        if (n->kind == TKind::Load) {
+            s.op = n->hyper.indicator ? TC_OP_LOAD_Y : TC_OP_LOAD_X;
+            return;
+        }
+        if (n->kind == TKind::Concat) {
+            s.op = TC_OP_CONCAT;
+            for (const TPtr& o : n->operands) add(s, o);
+            return;
+        }
+        if (n->kind == TKind::GradPrim) {
+            add(s, n->upstream);
+            for (const TPtr& o : n->saved) add(s, o);
+            switch (n->prim) {
+                case PrimOp::Convolv:
+                    s.op = n->slot == 0 ? TC_OP_CONV_BWD_DATA : n->slot == 1 ? TC_OP_CONV_BWD_FILTER : TC_OP_CONV_BWD_BIAS;
+                    return;
+                case PrimOp::Pooling: s.op = TC_OP_POOL_BWD; return;
+                case PrimOp::ReLU: s.op = TC_OP_RELU_BWD; return;
+                case PrimOp::Softmax: s.op = TC_OP_SOFTMAX_BWD; return;
+                case PrimOp::LRN: s.op = TC_OP_LRN_BWD; return;
+                case PrimOp::MatMul: s.op = n->slot == 0 ? TC_OP_MATMUL_BWD_DATA : TC_OP_MATMUL_BWD_W; return;
+                case PrimOp::BiasAdd: s.op = TC_OP_BIAS_GRAD; return;
+                case PrimOp::Eltwise: s.op = TC_OP_MUL; return;  // d(a*b)/da = up * b
+                case PrimOp::Concat: s.op = TC_OP_CONCAT_BWD; return;
+                case PrimOp::BatchNorm:
+                    s.op = n->slot == 0 ? TC_OP_BN_BWD_DATA : n->slot == 1 ? TC_OP_BN_BWD_GAMMA : TC_OP_BN_BWD_BETA;
+                    return;
+                default: break;
+            }
+            fail(ErrKind::Internal, std::string("flatten: no runtime op for d_") + prim_name(n->prim));
+        }
+        if (n->kind != TKind::Prim) fail(ErrKind::Internal, "flatten: unexpected node kind for " + n->display_name());
+        for (const TPtr& o : n->operands) add(s, o);
+        switch (n->prim) {
+            case PrimOp::Convolv: s.op = TC_OP_CONV_FWD; return;
+            case PrimOp::Pooling: s.op = TC_OP_POOL_FWD; return;
+            case PrimOp::ReLU: s.op = TC_OP_RELU_FWD; return;
+            case PrimOp::Softmax: s.op = TC_OP_SOFTMAX_FWD; return;
+            case PrimOp::LRN: s.op = TC_OP_LRN_FWD; return;
+            case PrimOp::DropoutMask: s.op = TC_OP_DROPOUT_MASK; return;
+            case PrimOp::MatMul: s.op = TC_OP_MATMUL_FWD; return;
+            case PrimOp::BiasAdd: s.op = TC_OP_BIAS_ADD; return;
+            case PrimOp::Eltwise: s.op = n->hyper.eltwise == ELT_MUL ? TC_OP_MUL : TC_OP_ADD; return;
+            case PrimOp::Log: s.op = TC_OP_LOG; return;
+            case PrimOp::Recip: s.op = TC_OP_RECIP; return;
+            case PrimOp::Scale: s.op = TC_OP_SCALE; return;
+            case PrimOp::BatchNorm: s.op = TC_OP_BN_FWD; return;
+            default: break;
+        }
+        fail(ErrKind::Internal, std::string("flatten: no runtime op for ") + prim_name(n->prim));
+    }
+
+    // loss = sum coef * dot(Y, logS)
+    void loss_terms(tc_stmt& s, const SPtr& e, double coef) {
+        switch (e->kind) {
+            case SKind::Const:
+            case SKind::NamedConst: return;
+            case SKind::Add: loss_terms(s, e->args[0], coef); loss_terms(s, e->args[1], coef); return;
+            case SKind::Neg: loss_terms(s, e->args[0], -coef); return;
+            case SKind::Mul:
+                if (e->args[1]->kind == SKind::Const || e->args[1]->kind == SKind::NamedConst)
+                    return loss_terms(s, e->args[0], coef * e->args[1]->value);
+                return loss_terms(s, e->args[1], coef * e->args[0]->value);
+            case SKind::Div: return loss_terms(s, e->args[0], coef / e->args[1]->value);
+            case SKind::Dot:
+                if (s.nterms >= 4) fail(ErrKind::Internal, "flatten: more than 4 loss terms");
+                s.coef[s.nterms++] = coef;
+                add(s, e->tensor);
+                add(s, e->tensor2);
+                return;
+            default: fail(ErrKind::Internal, "flatten: unsupported loss form");
+        }
+    }
+
+    tc_stmt stmt(const IrStmt& ir) {
+        tc_stmt s;
+        std::memset(&s, 0, sizeof s);
+        s.var = ir.var;
+        s.storage = ir.storage;
+        s.bytes = ir.bytes;
+        s.param = -1;
+        switch (ir.kind) {
+            case StmtKind::Let:
+                s.kind = TC_STMT_LET;
+                s.inplace = ir.inplace;
+                rhs(s, ir.node);
+                s.rank = ir.shape.rank();
+                for (int i = 0; i < s.rank && i < 4; ++i) s.dims[i] = ir.shape.dims[i];
+                break;
+            case StmtKind::Dealloc: s.kind = TC_STMT_DEALLOC; break;
+            case StmtKind::Update:
+                s.kind = TC_STMT_UPDATE;
+                rhs(s, ir.node);
+                s.param = pindex.at(ir.param.get());
+                s.lr_alpha = ir.lr_alpha;
+                s.momentum = ir.momentum;
+                s.decay = ir.decay;
+                break;
+            case StmtKind::Print:
+                s.kind = TC_STMT_PRINT;
+                s.op = TC_OP_PRINT_LOSS;
+                loss_terms(s, ir.loss, 1.0);
+                break;
+        }
+        return s;
+    }
+};
+
+void fill_param(tc_param_desc& d, const ParamSpec& ps, const Shape& s) {
+    std::memset(&d, 0, sizeof d);
+    std::strncpy(d.name, ps.name.c_str(), sizeof d.name - 1);
+    d.rank = s.rank();
+    for (int i = 0; i < s.rank() && i < 4; ++i) d.dims[i] = s.dims[i];
+    d.init_kind = ps.init == InitKind::Xavier ? TC_INIT_XAVIER : ps.init == InitKind::Constant ? TC_INIT_CONSTANT
+                                                                                               : TC_INIT_GAUSSIAN;
+    d.init_value = ps.init_value;
+    d.sigma = ps.sigma;
+    d.lr_mult = ps.lr_mult;
+    d.decay_mult = ps.decay_mult;
+    // Xavier fans: conv (Cout, Cin, k, k) -> Cin*k^2, Cout*k^2; full (out, in) -> in, out.
+    if (s.rank() == 4) {
+        d.fan_in = s.dims[1] * s.dims[2] * s.dims[3];
+        d.fan_out = s.dims[0] * s.dims[2] * s.dims[3];
+    } else if (s.rank() == 2) {
+        d.fan_in = s.dims[1];
+        d.fan_out = s.dims[0];
+    } else {
+        d.fan_in = d.fan_out = s.count();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+tc_status tc_net_compile(const char* name, int64_t batch, const tc_compile_opts* opts, tc_net** out) {
+    if (!name || !out || batch <= 0) return tcb::fail(TC_INVALID_ARG, "tc_net_compile: bad arguments");
+    *out = nullptr;
+    try {
+        auto h = std::make_unique<tc_net>();
+        build_by_name(h->net, name, batch);
+        CompileOptions co;
+        if (opts) {
+            co.solver.lr = opts->lr;
+            co.solver.momentum = opts->momentum;
+            co.solver.decay = opts->decay;
+            co.solver.clip = opts->clip;
+            co.mode = opts->mode == TC_MODE_REUSE ? MemMode::Reuse : MemMode::Dealloc;
+            co.workspace_cap_mb = opts->workspace_cap_mb;
+            co.greedy_schedule = opts->greedy_schedule != 0;
+        }
+        co.solver.name = name;
+        h->prog = compile_network(h->net, co);
+        h->report = analyze(h->prog);
+        Flattener fl(h->prog);
+        for (std::size_t i = 0; i < h->prog.params.size(); ++i) {
+            tc_param_desc d;
+            fill_param(d, *h->prog.params[i], h->prog.param_shapes[i]);
+            h->params.push_back(d);
+        }
+        for (const IrStmt& s : h->prog.train) h->stmts.push_back(fl.stmt(s));
+        for (const IrStmt& s : h->prog.test) h->test.push_back(fl.stmt(s));
+        int max_var = 0;
+        for (const auto& [id, shp] : h->prog.var_shapes) {
+            tc_var_desc v;
+            std::memset(&v, 0, sizeof v);
+            v.id = id;
+            v.rank = shp.rank();
+            for (int i = 0; i < v.rank && i < 4; ++i) v.dims[i] = shp.dims[i];
+            h->vars.push_back(v);
+            max_var = std::max(max_var, id + 1);
+        }
+        std::sort(h->vars.begin(), h->vars.end(), [](const tc_var_desc& a, const tc_var_desc& b) { return a.id < b.id; });
+        h->ir_text = dump_ir(h->prog);
+        h->table_text = format_report(h->report, false);
+        h->table_csv = format_report(h->report, true);
+        h->verify_text = verify(h->prog);
+        tc_plan& p = h->plan;
+        p.name = h->net.name.c_str();
+        p.batch = h->prog.batch;
+        p.classes = h->prog.classes;
+        for (int i = 0; i < 4; ++i) p.input_dims[i] = h->prog.input_shape.dims[i];
+        p.nparams = static_cast<int>(h->params.size());
+        p.params = h->params.data();
+        p.nstmts = static_cast<int>(h->stmts.size());
+        p.stmts = h->stmts.data();
+        p.ntest = static_cast<int>(h->test.size());
+        p.test_stmts = h->test.data();
+        p.logits_var = h->prog.logits_var;
+        p.nvars = static_cast<int>(h->vars.size());
+        p.vars = h->vars.data();
+        p.max_var = max_var;
+        p.lr = co.solver.lr;
+        p.momentum = co.solver.momentum;
+        p.decay = co.solver.decay;
+        p.clip = co.solver.clip;
+        p.mode = co.mode == MemMode::Reuse ? TC_MODE_REUSE : TC_MODE_DEALLOC;
+        *out = h.release();
+        return TC_OK;
+    } catch (const CompileError& e) {
+        return tcb::fail(TC_COMPILE_ERROR, std::string(err_kind_name(e.kind)) + ": " + e.what());
+    } catch (const std::exception& e) {
+        return tcb::fail(TC_INTERNAL, e.what());
+    }
+}
+
+void tc_net_destroy(tc_net* net) { delete net; }
+const tc_plan* tc_net_plan(const tc_net* net) { return net ? &net->plan : nullptr; }
+const char* tc_net_ir_text(const tc_net* net) { return net ? net->ir_text.c_str() : ""; }
+const char* tc_net_memory_table(const tc_net* net, int csv) {
+    return net ? (csv ? net->table_csv.c_str() : net->table_text.c_str()) : "";
+}
+const char* tc_net_verify(const tc_net* net) { return net ? net->verify_text.c_str() : "null net"; }
+const char* tc_net_stmt_text(const tc_net* net, int index) {
+    if (!net || index < 0 || index >= static_cast<int>(net->prog.train.size())) return "";
+    return net->prog.train[index].text.c_str();
+}
+tc_status tc_net_memory_summary(const tc_net* net, tc_mem_summary* out) {
+    if (!net || !out) return tcb::fail(TC_INVALID_ARG, "tc_net_memory_summary: null argument");
+    const MemoryReport& r = net->report;
+    out->peak_dealloc_bytes = r.peak_dealloc_bytes;
+    out->peak_reuse_bytes = r.peak_reuse_bytes;
+    out->param_bytes = r.param_bytes;
+    out->workspace_bytes = r.workspace_bytes;
+    out->peak_dealloc_mb = r.peak_dealloc_mb();
+    out->peak_reuse_mb = r.peak_reuse_mb();
+    out->param_mb = static_cast<float>(r.param_bytes) / 1e6f;
+    out->workspace_mb = static_cast<float>(r.workspace_bytes) / 1e6f;
+    return TC_OK;
+}
+
+}  // extern "C"

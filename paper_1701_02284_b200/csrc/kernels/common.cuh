@@ -11,12 +11,11 @@
 #include <cstdio>
 #include <string>
 
+#include "status.hpp"
 #include "tc_abi.h"
 
 namespace tcb {
 
-void set_error(const std::string& msg);
-tc_status fail(tc_status st, const std::string& msg);
 extern std::atomic<unsigned long long> g_launches;
 
 inline void count_launch(unsigned n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }

@@ -10,15 +10,7 @@
 
 namespace tcb {
 
-// ------------------------------------------------------------------ errors
-static thread_local std::string t_last_error;
 std::atomic<unsigned long long> g_launches{0};
-
-void set_error(const std::string& msg) { t_last_error = msg; }
-tc_status fail(tc_status st, const std::string& msg) {
-    t_last_error = msg;
-    return st;
-}
 
 int num_sms() {
     static int n = [] {
@@ -203,7 +195,6 @@ using namespace tcb;
 
 extern "C" {
 
-const char* tc_last_error(void) { return tcb::t_last_error.c_str(); }
 const char* tc_build_info(void) { return "tcb200 sm_100a tcgen05 kind::f16 (nvcc " __VERSION__ ")"; }
 unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load(); }
 

@@ -1,0 +1,111 @@
+"""Python mirror of the plan-producer interface (tc_plan.h).
+
+The reference's host interface is C++ (expr.hpp builders + the SPEC.md
+compiler stages); this module only wraps the C ABI of this repo's own C++
+implementation of it so tests and bench.py can drive it:
+
+    net = compile_network("lenet", 500)      # elaborate + grad + IR + memplan
+    print(net.ir_text())                      # --dump-ir
+    print(net.memory_table())                 # analyze
+    net.memory_summary().peak_dealloc_mb      # 59.167999 for Fig. 2
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _native as nat
+
+
+@dataclass
+class ParamInfo:
+    index: int
+    name: str
+    dims: tuple
+    init_kind: int
+    init_value: float
+    lr_mult: float
+    decay_mult: float
+    fan_in: int
+    fan_out: int
+
+    @property
+    def count(self) -> int:
+        n = 1
+        for d in self.dims:
+            n *= d
+        return n
+
+
+class CompiledNetwork:
+    """A compiled network: IrProgram + memory report (owner of the tc_net handle)."""
+
+    def __init__(self, name: str, batch: int, *, lr: float = 0.01, momentum: float = 0.9, decay: float = 0.0005,
+                 clip: float = 0.0, mode: str = "dealloc", workspace_cap_mb: float = -1.0, greedy: bool = False):
+        L = nat.lib()
+        opts = nat.CompileOpts(lr=lr, momentum=momentum, decay=decay, clip=clip,
+                               mode=nat.TC_MODE_REUSE if mode == "reuse" else nat.TC_MODE_DEALLOC,
+                               workspace_cap_mb=workspace_cap_mb, greedy_schedule=int(greedy))
+        h = C.c_void_p()
+        nat.check(L.tc_net_compile(name.encode(), batch, C.byref(opts), C.byref(h)))
+        self._h = h
+        self.name = name
+        self.batch = batch
+        self.plan_ptr = L.tc_net_plan(h)
+        self.plan = self.plan_ptr.contents
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and nat._lib is not None:
+            nat._lib.tc_net_destroy(h)
+            self._h = None
+
+    # ---- reports
+    def ir_text(self) -> str:
+        return nat.lib().tc_net_ir_text(self._h).decode()
+
+    def memory_table(self, csv: bool = False) -> str:
+        return nat.lib().tc_net_memory_table(self._h, int(csv)).decode()
+
+    def memory_summary(self) -> nat.MemSummary:
+        s = nat.MemSummary()
+        nat.check(nat.lib().tc_net_memory_summary(self._h, C.byref(s)))
+        return s
+
+    def verify(self) -> str:
+        return nat.lib().tc_net_verify(self._h).decode()
+
+    def stmt_text(self, i: int) -> str:
+        return nat.lib().tc_net_stmt_text(self._h, i).decode()
+
+    # ---- plan views
+    @property
+    def stmts(self):
+        p = self.plan
+        return [p.stmts[i] for i in range(p.nstmts)]
+
+    @property
+    def params(self) -> list[ParamInfo]:
+        p = self.plan
+        out = []
+        for i in range(p.nparams):
+            d = p.params[i]
+            out.append(ParamInfo(i, d.name.decode(), tuple(d.dims[j] for j in range(d.rank)), d.init_kind,
+                                 d.init_value, d.lr_mult, d.decay_mult, d.fan_in, d.fan_out))
+        return out
+
+    def var_dims(self, var: int) -> tuple:
+        p = self.plan
+        for i in range(p.nvars):
+            v = p.vars[i]
+            if v.id == var:
+                return tuple(v.dims[j] for j in range(v.rank))
+        raise KeyError(var)
+
+    @property
+    def input_dims(self) -> tuple:
+        return tuple(self.plan.input_dims[i] for i in range(4))
+
+
+def compile_network(name: str, batch: int, **kw) -> CompiledNetwork:
+    return CompiledNetwork(name, batch, **kw)
