@@ -121,7 +121,41 @@ class CompileOpts(C.Structure):
     ]
 
 
+class CtxDesc(C.Structure):
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_void_p),
+                ("seed", C.c_uint64), ("use_graph", C.c_int), ("keep", C.c_int)]
+
+
+class RtMemory(C.Structure):
+    _fields_ = [("arena_bytes", C.c_int64), ("arena_keep_bytes", C.c_int64), ("param_bytes", C.c_int64),
+                ("workspace_bytes", C.c_int64), ("input_bytes", C.c_int64), ("device_used_bytes", C.c_int64)]
+
+
 _lib = None
+
+
+def _bind_runtime(L: C.CDLL) -> None:
+    vp, ci = C.c_void_p, C.c_int
+    L.tc_ctx_create.argtypes = [vp, C.POINTER(CtxDesc), C.POINTER(vp)]
+    L.tc_ctx_destroy.argtypes = [vp]
+    L.tc_ctx_destroy.restype = None
+    L.tc_ctx_stream.argtypes = [vp]
+    L.tc_ctx_stream.restype = vp
+    for fn in ("tc_param_upload", "tc_param_download", "tc_velocity_download", "tc_grad_download"):
+        getattr(L, fn).argtypes = [vp, ci, vp]
+    L.tc_init_params.argtypes = [vp]
+    L.tc_stage_batch.argtypes = [vp, vp, vp]
+    L.tc_stage_synthetic.argtypes = [vp, ci, ci]
+    L.tc_step.argtypes = [vp, ci, ci, ci]
+    L.tc_exec_stmt.argtypes = [vp, ci, ci, ci]
+    L.tc_loss.argtypes = [vp, C.POINTER(C.c_double)]
+    L.tc_var_download.argtypes = [vp, ci, vp, C.c_int64]
+    L.tc_pool_indices_download.argtypes = [vp, ci, vp, C.c_int64]
+    L.tc_sync.argtypes = [vp]
+    L.tc_memory.argtypes = [vp, C.POINTER(RtMemory)]
+    L.tc_launches_per_step.argtypes = [vp]
+    L.tc_nccl_unique_id.argtypes = [vp]
+    L.tc_profile_step.argtypes = [vp, ci, ci, ci, vp, ci]
 
 
 def _bind_plan(L: C.CDLL) -> None:
@@ -162,6 +196,7 @@ def lib() -> C.CDLL:
         L.tc_conv2d_workspace_bytes.argtypes = [C.POINTER(ConvDesc), C.c_int]
         L.tc_conv2d_workspace_bytes.restype = C.c_size_t
         _bind_plan(L)
+        _bind_runtime(L)
         _lib = L
     return _lib
 

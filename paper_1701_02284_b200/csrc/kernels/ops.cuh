@@ -1,0 +1,96 @@
+// Bandwidth-bound kernels of the training step (everything that is not a
+// contraction).  Device layouts (tc_abi.h): 4-D activations NHWC bf16 with
+// channel stride cs (multiple of 8, pad channels kept at zero); 2-D
+// activations [N][Fs] bf16 (Fs = ceil8(F)); loss-head tensors fp32 [N][F];
+// dropout keep-masks uint8.  Every kernel is deterministic: reductions use a
+// fixed partition and a fixed summation order.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tc_abi.h"
+
+namespace tcb {
+
+using bf16 = __nv_bfloat16;
+
+struct Act4 {  // NHWC activation view
+    int N, H, W, C, cs;
+    __host__ __device__ long long pixels() const { return static_cast<long long>(N) * H * W; }
+    __host__ __device__ long long elems() const { return pixels() * cs; }
+};
+
+tc_status launch_relu_fwd(const bf16* x, bf16* y, long long n, cudaStream_t st);
+tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, cudaStream_t st);
+tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, cudaStream_t st);
+// y = x * keep * scale (inverted dropout; keep is a 0/1 byte mask)
+tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16* y, long long n, cudaStream_t st);
+// keep[n, e] for every stored element; e = NCHW element index within the sample (tc_philox.h)
+tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
+                              uint32_t var, const uint32_t* iter_n0, cudaStream_t st);
+
+tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, int32_t* idx, int k, int stride, int pad,
+                          int is_max, cudaStream_t st);
+tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const int32_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
+                          int is_max, cudaStream_t st);
+tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st);
+tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
+                         float beta, float k, cudaStream_t st);
+
+// rows x F, input bf16 with row stride in_ld -> fp32 out (stride F)
+tc_status launch_softmax_fwd(const bf16* x, long long in_ld, float* y, int rows, int F, cudaStream_t st);
+// dx (bf16, stride out_ld, pad columns zeroed) = y * (dy - sum(dy*y))
+tc_status launch_softmax_bwd(const float* dy, const float* y, bf16* dx, long long out_ld, int rows, int F,
+                             cudaStream_t st);
+
+enum F32Op { F32_LOG = 0, F32_RECIP = 1, F32_SCALE = 2, F32_MUL = 3, F32_ADD = 4 };
+tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st);
+tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st);
+// loss = sum_t coef[t] * dot(a[t], b[t]) over n[t] elements -> *out (fp32 device scalar)
+tc_status launch_loss(const float* const* a, const float* const* b, const long long* n, const double* coef, int nterms,
+                      float* out, cudaStream_t st);
+
+// Column sums of a [rows][ld] bf16 matrix over its first `cols` columns -> out[cols] fp32 (deterministic).
+tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, float* out, float* partials,
+                        int max_partials, cudaStream_t st);
+size_t colsum_partials_floats(int cols);
+tc_status launch_bias_add(const bf16* x, const float* b, bf16* y, long long rows, int cols, long long ld, int relu,
+                          cudaStream_t st);
+
+// Concat: copy `c` channels of src (stride src_cs) into dst channel offset `off` (stride dst_cs).
+tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs, int off, int c, long long pixels,
+                              cudaStream_t st);
+tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
+
+// BatchNorm over NHWC [pixels][cs]: stats (mean, inv_std) per channel.
+tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
+                        int C, int cs, float eps, float* partials, int max_partials, cudaStream_t st);
+// dgamma/dbeta (may be null) and dx (may be null).
+tc_status launch_bn_bwd(const bf16* dy, const bf16* x, const float* gamma, const float* stats, bf16* dx, float* dgamma,
+                        float* dbeta, long long pixels, int C, int cs, float* partials, int max_partials,
+                        cudaStream_t st);
+
+// Input staging: NCHW fp32 -> NHWC bf16 (channel stride cs, pads zero).
+tc_status launch_nchw_to_nhwc(const float* x, bf16* y, int N, int C, int H, int W, int cs, cudaStream_t st);
+// Synthetic batch generated on the device (identical law to oracle/tc_philox.h).
+tc_status launch_synth_batch(bf16* x, int32_t* labels, int N, int C, int H, int W, int cs, int classes, uint64_t seed,
+                             uint32_t iter, uint32_t n0, cudaStream_t st);
+
+// Momentum SGD: v = mom*v + lr_alpha*(g + decay*p); p += v;
+// refreshes the bf16 shadow(s) used as GEMM operands.
+struct SgdTensor {
+    float* p;
+    float* v;
+    const float* g;
+    long long n;
+    bf16* shadow;        // same layout as p (may be null)
+    bf16* shadow_rskc;   // conv filters: [R][S][ks][cs] copy for bwd-data (may be null)
+    int K, RS, cs, ks;   // shape info for the RSKC scatter (p is [K][RS][cs])
+    float lr_alpha, momentum, decay;
+};
+tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaStream_t st);
+
+}  // namespace tcb

@@ -1,0 +1,1240 @@
+// sm_100a executor of the memory-scheduled plan (tc_runtime.h).
+//
+// Replaces the reference runtime's per-statement exec + MemoryPool
+// with:
+//   * a static device arena: every storage (alias chain from inline_inplace)
+//     and every companion buffer (max-pool argmax indices, BN statistics) gets
+//     an offset from lifetime-interval packing over the statement order, so
+//     the step performs no allocation (the paper's cudaMalloc/cudaFree churn,
+//     PAPER.md:323, 512-513, disappears);
+//   * a persistent parameter slab: fp32 master weights / velocities /
+//     gradients in device layouts plus bf16 GEMM-operand shadows refreshed by
+//     the fused momentum update;
+//   * peephole fusion of in-place BiasAdd / ReLU into the producing GEMM
+//     epilogue (adjacent statements exposed by CSE + in-place inlining);
+//   * optional NCCL gradient all-reduce (one process per GPU) before each
+//     Update, and CUDA-graph capture of the whole step.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels/common.cuh"
+#include "kernels/ops.cuh"
+#include "tc_philox.h"
+#include "tc_runtime.h"
+
+namespace tcb {
+namespace {
+
+enum DType { DT_BF16 = 0, DT_F32 = 1, DT_U8 = 2 };
+
+inline int ceil8(long long v) { return static_cast<int>((v + 7) / 8 * 8); }
+inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct VarL {
+    int id = -1;
+    int rank = 0;
+    int64_t d[4] = {1, 1, 1, 1};
+    int dtype = DT_BF16;
+    bool nhwc = false;  // device layout NHWC (4-D, or 2-D gradient of a flattened 4-D tensor)
+    int N = 1, H = 1, W = 1, C = 1, cs = 8;  // 2-D: H = W = 1, C = F, cs = row stride
+    int storage = -1;
+    int def = -1;
+    size_t bytes() const {
+        const size_t el = static_cast<size_t>(N) * H * W * cs;
+        return el * (dtype == DT_F32 ? 4 : dtype == DT_U8 ? 1 : 2);
+    }
+    long long elems() const { return static_cast<long long>(N) * H * W * cs; }
+    Act4 act() const { return Act4{N, H, W, C, cs}; }
+};
+
+struct ParamL {
+    int rank = 0;
+    int64_t d[4] = {1, 1, 1, 1};
+    enum Kind { VEC, CONV, FC } kind = VEC;
+    // conv: [K][R][S][cs]; fc: [out][in_dev]; vec: [K]
+    int K = 1, C = 1, R = 1, S = 1, cs = 8, ks = 8;
+    bool fc_from4d = false;
+    int fH = 1, fW = 1, fC = 1, fcs = 8;  // flattened 4-D input of an FC layer
+    int in_dev = 0;
+    long long n = 0;  // device elements
+    float* p = nullptr;
+    float* v = nullptr;
+    float* g = nullptr;
+    bf16* shadow = nullptr;
+    bf16* rskc = nullptr;
+};
+
+struct Item {  // arena allocation
+    size_t bytes = 0;
+    int first = 0, last = 0;
+    size_t off = 0;
+};
+
+}  // namespace
+}  // namespace tcb
+
+using namespace tcb;
+
+struct tc_ctx {
+    const tc_plan* plan = nullptr;
+    tc_ctx_desc desc{};
+    int device = 0;
+    cudaStream_t st = nullptr;
+    ncclComm_t comm = nullptr;
+
+    std::unordered_map<int, VarL> vars;
+    std::vector<ParamL> params;
+    std::unordered_map<int, int> storage_item;      // storage id -> item
+    std::unordered_map<int, int> pool_idx_item;     // pool output var -> item (int32 indices)
+    std::unordered_map<int, int> bn_stats_item;     // BN input var -> item (2*C fp32)
+    std::unordered_map<int, float> mask_rate;       // dropout mask var -> rate
+    std::vector<Item> items;
+    std::vector<uint8_t> fused;                     // stmt folded into its producer
+    std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
+    std::vector<int> fuse_bias_param;
+
+    uint8_t* arena = nullptr;
+    size_t arena_bytes = 0, arena_keep_bytes = 0;
+    uint8_t* slab = nullptr;
+    size_t slab_bytes = 0;
+    uint8_t* ws = nullptr;
+    size_t ws_bytes = 0;
+    float* partials = nullptr;
+    int max_partials = 0;
+    bf16* d_input = nullptr;
+    int32_t* d_labels = nullptr;
+    float* d_stage = nullptr;  // NCHW fp32 staging for host batches
+    float* d_loss = nullptr;
+    uint32_t* d_iter = nullptr;
+    uint32_t* h_iter = nullptr;  // pinned
+    float* h_loss = nullptr;     // pinned
+    int input_cs = 8;
+    size_t input_bytes = 0;
+
+    cudaGraph_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int runs[2] = {0, 0};
+    int launches_per_step = -1;
+    int64_t device_used = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------------ analysis
+tc_status analyze_layouts(tc_ctx* c) {
+    const tc_plan* p = c->plan;
+    for (int i = 0; i < p->nvars; ++i) {
+        VarL v;
+        v.id = p->vars[i].id;
+        v.rank = p->vars[i].rank;
+        for (int j = 0; j < v.rank; ++j) v.d[j] = p->vars[i].dims[j];
+        c->vars[v.id] = v;
+    }
+    // params
+    c->params.resize(p->nparams);
+    for (int i = 0; i < p->nparams; ++i) {
+        ParamL& q = c->params[i];
+        const tc_param_desc& pd = p->params[i];
+        q.rank = pd.rank;
+        for (int j = 0; j < pd.rank; ++j) q.d[j] = pd.dims[j];
+        if (pd.rank == 4) {
+            q.kind = ParamL::CONV;
+            q.K = static_cast<int>(pd.dims[0]);
+            q.C = static_cast<int>(pd.dims[1]);
+            q.R = static_cast<int>(pd.dims[2]);
+            q.S = static_cast<int>(pd.dims[3]);
+            q.cs = ceil8(q.C);
+            q.ks = ceil8(q.K);
+            q.n = static_cast<long long>(q.K) * q.R * q.S * q.cs;
+        } else if (pd.rank == 2) {
+            q.kind = ParamL::FC;
+            q.K = static_cast<int>(pd.dims[0]);
+            q.C = static_cast<int>(pd.dims[1]);
+        } else {
+            q.kind = ParamL::VEC;
+            q.K = static_cast<int>(pd.dims[0]);
+            q.n = q.K;
+        }
+    }
+    // dtypes and layouts, in statement order
+    std::unordered_map<int, int> fc_input_of_param;  // FC weight param -> forward input var
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind == TC_STMT_LET) {
+            VarL& v = c->vars.at(s.var);
+            v.storage = s.storage;
+            v.def = i;
+        }
+        if (s.op == TC_OP_MATMUL_FWD && s.in[1].kind == TC_REF_PARAM) fc_input_of_param[s.in[1].index] = s.in[0].index;
+        if (s.op == TC_OP_DROPOUT_MASK) c->mask_rate[s.var] = static_cast<float>(s.rate);
+    }
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET) continue;
+        VarL& v = c->vars.at(s.var);
+        int dt = DT_BF16;
+        switch (s.op) {
+            case TC_OP_LOAD_Y:
+            case TC_OP_SOFTMAX_FWD:
+            case TC_OP_LOG:
+            case TC_OP_RECIP: dt = DT_F32; break;
+            case TC_OP_DROPOUT_MASK: dt = DT_U8; break;
+            case TC_OP_SCALE:
+            case TC_OP_MUL:
+            case TC_OP_ADD:
+                for (int k = 0; k < s.nin; ++k)
+                    if (s.in[k].kind == TC_REF_VAR && c->vars.at(s.in[k].index).dtype == DT_F32) dt = DT_F32;
+                break;
+            default: break;
+        }
+        v.dtype = dt;
+        if (v.rank == 4) {
+            v.nhwc = true;
+            v.N = static_cast<int>(v.d[0]);
+            v.C = static_cast<int>(v.d[1]);
+            v.H = static_cast<int>(v.d[2]);
+            v.W = static_cast<int>(v.d[3]);
+            v.cs = ceil8(v.C);
+        } else if (v.rank == 2) {
+            v.N = static_cast<int>(v.d[0]);
+            v.C = static_cast<int>(v.d[1]);
+            v.cs = dt == DT_F32 ? v.C : ceil8(v.C);
+            if (s.op == TC_OP_MATMUL_BWD_DATA && s.in[1].kind == TC_REF_PARAM) {
+                // gradient of a flattened 4-D activation keeps that activation's NHWC layout
+                auto it = fc_input_of_param.find(s.in[1].index);
+                if (it != fc_input_of_param.end()) {
+                    const VarL& a = c->vars.at(it->second);
+                    if (a.nhwc) {
+                        v.nhwc = true;
+                        v.N = a.N;
+                        v.H = a.H;
+                        v.W = a.W;
+                        v.C = a.C;
+                        v.cs = a.cs;
+                    }
+                }
+            }
+        } else {
+            return fail(TC_SHAPE_FAULT, "runtime: unsupported var rank " + std::to_string(v.rank));
+        }
+    }
+    // FC weight device layout follows its forward input
+    for (int i = 0; i < p->nparams; ++i) {
+        ParamL& q = c->params[i];
+        if (q.kind != ParamL::FC) continue;
+        auto it = fc_input_of_param.find(i);
+        if (it != fc_input_of_param.end() && c->vars.at(it->second).nhwc) {
+            const VarL& a = c->vars.at(it->second);
+            q.fc_from4d = true;
+            q.fH = a.H;
+            q.fW = a.W;
+            q.fC = a.C;
+            q.fcs = a.cs;
+            q.in_dev = a.H * a.W * a.cs;
+        } else {
+            q.in_dev = ceil8(q.C);
+        }
+        q.n = static_cast<long long>(q.K) * q.in_dev;
+    }
+    return TC_OK;
+}
+
+// Peephole fusion: GEMM producer followed by in-place BiasAdd / ReLU on its storage.
+void plan_fusion(tc_ctx* c) {
+    const tc_plan* p = c->plan;
+    c->fused.assign(p->nstmts, 0);
+    c->fuse_bias.assign(p->nstmts, 0);
+    c->fuse_relu.assign(p->nstmts, 0);
+    c->fuse_bias_param.assign(p->nstmts, -1);
+    auto next_let = [&](int i) {
+        for (int j = i + 1; j < p->nstmts; ++j) {
+            if (p->stmts[j].kind == TC_STMT_DEALLOC) continue;
+            return p->stmts[j].kind == TC_STMT_LET ? j : -1;
+        }
+        return -1;
+    };
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET || (s.op != TC_OP_CONV_FWD && s.op != TC_OP_MATMUL_FWD)) continue;
+        int j = next_let(i);
+        if (s.op == TC_OP_MATMUL_FWD && j >= 0 && p->stmts[j].op == TC_OP_BIAS_ADD && p->stmts[j].inplace &&
+            p->stmts[j].in[0].kind == TC_REF_VAR && p->stmts[j].in[0].index == s.var &&
+            p->stmts[j].in[1].kind == TC_REF_PARAM) {
+            c->fuse_bias[i] = 1;
+            c->fuse_bias_param[i] = p->stmts[j].in[1].index;
+            c->fused[j] = 1;
+            const int prev = p->stmts[j].var;
+            j = next_let(j);
+            if (j >= 0 && p->stmts[j].op == TC_OP_RELU_FWD && p->stmts[j].inplace && p->stmts[j].in[0].index == prev) {
+                c->fuse_relu[i] = 1;
+                c->fused[j] = 1;
+            }
+            continue;
+        }
+        if (s.op == TC_OP_CONV_FWD && j >= 0 && p->stmts[j].op == TC_OP_RELU_FWD && p->stmts[j].inplace &&
+            p->stmts[j].in[0].kind == TC_REF_VAR && p->stmts[j].in[0].index == s.var) {
+            c->fuse_relu[i] = 1;
+            c->fused[j] = 1;
+        }
+    }
+}
+
+// Lifetime-interval packing of storages and companions into one arena.
+void pack_items(std::vector<Item>& items, bool keep, size_t* total, size_t* keep_total) {
+    std::vector<int> order(items.size());
+    for (size_t i = 0; i < items.size(); ++i) order[i] = static_cast<int>(i);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        if (items[a].bytes != items[b].bytes) return items[a].bytes > items[b].bytes;
+        return items[a].first < items[b].first;
+    });
+    *keep_total = 0;
+    for (const Item& it : items) *keep_total += align256(it.bytes);
+    std::vector<int> placed;
+    size_t top = 0;
+    for (int idx : order) {
+        Item& it = items[idx];
+        const size_t sz = align256(it.bytes);
+        if (keep) {
+            it.off = top;
+            top += sz;
+            continue;
+        }
+        // collect conflicting intervals sorted by offset, then first fit
+        std::vector<std::pair<size_t, size_t>> busy;
+        for (int o : placed) {
+            const Item& q = items[o];
+            if (q.last < it.first || it.last < q.first) continue;
+            busy.emplace_back(q.off, q.off + align256(q.bytes));
+        }
+        std::sort(busy.begin(), busy.end());
+        size_t off = 0;
+        for (auto& [b0, b1] : busy) {
+            if (off + sz <= b0) break;
+            off = std::max(off, b1);
+        }
+        it.off = off;
+        top = std::max(top, off + sz);
+        placed.push_back(idx);
+    }
+    *total = top;
+}
+
+tc_status plan_arena(tc_ctx* c) {
+    const tc_plan* p = c->plan;
+    const int n = p->nstmts;
+    // storage lifetimes
+    std::unordered_map<int, Item> st;
+    auto touch = [&](int storage, int i) {
+        auto& it = st[storage];
+        it.last = std::max(it.last, i);
+    };
+    for (int i = 0; i < n; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind == TC_STMT_LET) {
+            const VarL& v = c->vars.at(s.var);
+            if (s.op == TC_OP_LOAD_X) continue;  // lives in the persistent input buffer
+            auto f = st.find(s.storage);
+            if (f == st.end()) {
+                Item it;
+                it.first = i;
+                it.last = i;
+                it.bytes = v.bytes();
+                st[s.storage] = it;
+            } else {
+                f->second.bytes = std::max(f->second.bytes, v.bytes());
+                f->second.last = std::max(f->second.last, i);
+            }
+        }
+        if (s.kind == TC_STMT_LET || s.kind == TC_STMT_UPDATE || s.kind == TC_STMT_PRINT)
+            for (int k = 0; k < s.nin; ++k)
+                if (s.in[k].kind == TC_REF_VAR) {
+                    const VarL& v = c->vars.at(s.in[k].index);
+                    if (st.count(v.storage)) touch(v.storage, i);
+                }
+        if (s.kind == TC_STMT_DEALLOC && st.count(s.storage)) touch(s.storage, i);
+    }
+    for (auto& [sid, it] : st) {
+        c->storage_item[sid] = static_cast<int>(c->items.size());
+        c->items.push_back(it);
+    }
+    // companions
+    for (int i = 0; i < n; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET) continue;
+        if (s.op == TC_OP_POOL_FWD && s.max_pool) {
+            Item it;
+            it.first = i;
+            it.last = i;
+            it.bytes = static_cast<size_t>(c->vars.at(s.var).elems()) * 4;
+            for (int j = i + 1; j < n; ++j)
+                if (p->stmts[j].op == TC_OP_POOL_BWD && p->stmts[j].in[1].kind == TC_REF_VAR &&
+                    p->stmts[j].in[1].index == s.var)
+                    it.last = j;
+            c->pool_idx_item[s.var] = static_cast<int>(c->items.size());
+            c->items.push_back(it);
+        }
+        if (s.op == TC_OP_BN_FWD) {
+            const int xv = s.in[0].index;
+            Item it;
+            it.first = i;
+            it.last = i;
+            it.bytes = static_cast<size_t>(c->vars.at(xv).C) * 2 * 4;
+            for (int j = i + 1; j < n; ++j) {
+                const tc_stmt& b = p->stmts[j];
+                if ((b.op == TC_OP_BN_BWD_DATA || b.op == TC_OP_BN_BWD_GAMMA) && b.in[1].kind == TC_REF_VAR &&
+                    b.in[1].index == xv)
+                    it.last = j;
+                if (b.op == TC_OP_BN_BWD_BETA && b.in[0].kind == TC_REF_VAR) it.last = std::max(it.last, it.last);
+            }
+            c->bn_stats_item[xv] = static_cast<int>(c->items.size());
+            c->items.push_back(it);
+        }
+    }
+    pack_items(c->items, c->desc.keep != 0, &c->arena_bytes, &c->arena_keep_bytes);
+    return TC_OK;
+}
+
+// ------------------------------------------------------------------ host layout permutations
+void ref_to_dev(const ParamL& q, const float* ref, std::vector<float>& dev) {
+    dev.assign(q.n, 0.f);
+    if (q.kind == ParamL::CONV) {
+        for (int k = 0; k < q.K; ++k)
+            for (int c = 0; c < q.C; ++c)
+                for (int r = 0; r < q.R; ++r)
+                    for (int s = 0; s < q.S; ++s)
+                        dev[((static_cast<long long>(k) * q.R + r) * q.S + s) * q.cs + c] =
+                            ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s];
+    } else if (q.kind == ParamL::FC) {
+        for (int o = 0; o < q.K; ++o) {
+            if (q.fc_from4d) {
+                for (int c = 0; c < q.fC; ++c)
+                    for (int h = 0; h < q.fH; ++h)
+                        for (int w = 0; w < q.fW; ++w)
+                            dev[static_cast<long long>(o) * q.in_dev + (static_cast<long long>(h) * q.fW + w) * q.fcs + c] =
+                                ref[static_cast<long long>(o) * q.C + (static_cast<long long>(c) * q.fH + h) * q.fW + w];
+            } else {
+                for (int j = 0; j < q.C; ++j) dev[static_cast<long long>(o) * q.in_dev + j] = ref[static_cast<long long>(o) * q.C + j];
+            }
+        }
+    } else {
+        for (int k = 0; k < q.K; ++k) dev[k] = ref[k];
+    }
+}
+
+void dev_to_ref(const ParamL& q, const float* dev, float* ref) {
+    if (q.kind == ParamL::CONV) {
+        for (int k = 0; k < q.K; ++k)
+            for (int c = 0; c < q.C; ++c)
+                for (int r = 0; r < q.R; ++r)
+                    for (int s = 0; s < q.S; ++s)
+                        ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s] =
+                            dev[((static_cast<long long>(k) * q.R + r) * q.S + s) * q.cs + c];
+    } else if (q.kind == ParamL::FC) {
+        for (int o = 0; o < q.K; ++o) {
+            if (q.fc_from4d) {
+                for (int c = 0; c < q.fC; ++c)
+                    for (int h = 0; h < q.fH; ++h)
+                        for (int w = 0; w < q.fW; ++w)
+                            ref[static_cast<long long>(o) * q.C + (static_cast<long long>(c) * q.fH + h) * q.fW + w] =
+                                dev[static_cast<long long>(o) * q.in_dev + (static_cast<long long>(h) * q.fW + w) * q.fcs + c];
+            } else {
+                for (int j = 0; j < q.C; ++j) ref[static_cast<long long>(o) * q.C + j] = dev[static_cast<long long>(o) * q.in_dev + j];
+            }
+        }
+    } else {
+        for (int k = 0; k < q.K; ++k) ref[k] = dev[k];
+    }
+}
+
+uint16_t f2bf(float f) {  // round to nearest even
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+float bf2f(uint16_t b) {
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+tc_status upload_dev_param(tc_ctx* c, int i, const std::vector<float>& dev) {
+    ParamL& q = c->params[i];
+    TCB_CUDA_CHECK(cudaMemcpyAsync(q.p, dev.data(), q.n * 4, cudaMemcpyHostToDevice, c->st));
+    if (q.shadow) {
+        std::vector<uint16_t> sh(q.n);
+        for (long long j = 0; j < q.n; ++j) sh[j] = f2bf(dev[j]);
+        TCB_CUDA_CHECK(cudaMemcpyAsync(q.shadow, sh.data(), q.n * 2, cudaMemcpyHostToDevice, c->st));
+        if (q.rskc) {
+            const int RS = q.R * q.S;
+            std::vector<uint16_t> r(static_cast<size_t>(RS) * q.ks * q.cs, 0);
+            for (int k = 0; k < q.K; ++k)
+                for (int rs = 0; rs < RS; ++rs)
+                    for (int cc = 0; cc < q.cs; ++cc)
+                        r[(static_cast<size_t>(rs) * q.ks + k) * q.cs + cc] = sh[(static_cast<size_t>(k) * RS + rs) * q.cs + cc];
+            TCB_CUDA_CHECK(cudaMemcpyAsync(q.rskc, r.data(), r.size() * 2, cudaMemcpyHostToDevice, c->st));
+        }
+        TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));  // host staging vectors go out of scope
+    } else {
+        TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    }
+    return TC_OK;
+}
+
+// ------------------------------------------------------------------ execution helpers
+struct Ptrs {
+    tc_ctx* c;
+    void* var(int id) const {
+        const VarL& v = c->vars.at(id);
+        if (c->plan && v.def >= 0 && c->plan->stmts[v.def].op == TC_OP_LOAD_X) return c->d_input;
+        auto it = c->storage_item.find(v.storage);
+        return c->arena + c->items[it->second].off;
+    }
+    template <class T>
+    T* as(const tc_ref& r) const {
+        if (r.kind == TC_REF_PARAM) return reinterpret_cast<T*>(c->params[r.index].p);
+        return reinterpret_cast<T*>(var(r.index));
+    }
+    const VarL& L(const tc_ref& r) const { return c->vars.at(r.index); }
+};
+
+tc_conv_desc conv_desc(const VarL& x, const ParamL& w, const VarL& y, const tc_stmt& s) {
+    tc_conv_desc d;
+    d.N = x.N;
+    d.C = x.C;
+    d.H = x.H;
+    d.W = x.W;
+    d.K = w.K;
+    d.R = w.R;
+    d.S = w.S;
+    d.stride = s.stride;
+    d.pad = s.pad;
+    d.Ho = y.H;
+    d.Wo = y.W;
+    d.cs = x.cs;
+    d.ks = y.cs;
+    return d;
+}
+
+tc_status run_gemm_args(tc_ctx* c, tc_gemm_args& a) {
+    a.workspace = c->ws;
+    a.workspace_bytes = c->ws_bytes;
+    return tc_gemm_bf16(&a, c->st);
+}
+
+// Gradient op of an Update (or a parameter-shaped Let) into `g` (device param layout).
+tc_status compute_param_grad(tc_ctx* c, const tc_stmt& s, int pidx, float* g) {
+    Ptrs P{c};
+    const ParamL& q = c->params[pidx];
+    cudaStream_t st = c->st;
+    switch (s.op) {
+        case TC_OP_CONV_BWD_FILTER: {
+            const VarL& dy = P.L(s.in[0]);
+            const VarL& x = P.L(s.in[1]);
+            tc_conv_desc d = conv_desc(x, q, dy, s);
+            return tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
+        }
+        case TC_OP_CONV_BWD_BIAS:
+        case TC_OP_BIAS_GRAD:
+        case TC_OP_BN_BWD_BETA: {
+            const VarL& up = P.L(s.in[0]);
+            return launch_colsum(reinterpret_cast<const bf16*>(P.var(up.id)), static_cast<long long>(up.N) * up.H * up.W,
+                                 q.K, up.cs, g, c->partials, c->max_partials, st);
+        }
+        case TC_OP_MATMUL_BWD_W: {
+            const VarL& up = P.L(s.in[0]);
+            const VarL& a = P.L(s.in[1]);
+            tc_gemm_args ga{};
+            ga.M = q.K;
+            ga.N = q.in_dev;
+            ga.K = up.N;
+            ga.a_layout = TC_LAYOUT_MN;
+            ga.A = P.var(up.id);
+            ga.lda = up.cs;
+            ga.b_layout = TC_LAYOUT_MN;
+            ga.B = P.var(a.id);
+            ga.ldb = q.in_dev;
+            ga.D = g;
+            ga.ldd = q.in_dev;
+            ga.d_dtype = TC_DTYPE_F32;
+            ga.alpha = 1.f;
+            return run_gemm_args(c, ga);
+        }
+        case TC_OP_BN_BWD_GAMMA: {
+            const VarL& up = P.L(s.in[0]);
+            const VarL& x = P.L(s.in[1]);
+            const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
+            return launch_bn_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), reinterpret_cast<const bf16*>(P.var(x.id)),
+                                 nullptr, stats, nullptr, g, nullptr, static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs,
+                                 c->partials, c->max_partials, st);
+        }
+        default: break;
+    }
+    return fail(TC_INTERNAL, "runtime: unsupported parameter-gradient op " + std::to_string(s.op));
+}
+
+tc_status exec_let(tc_ctx* c, int i) {
+    const tc_stmt& s = c->plan->stmts[i];
+    Ptrs P{c};
+    cudaStream_t st = c->st;
+    const VarL& out = c->vars.at(s.var);
+    void* y = P.var(s.var);
+    switch (s.op) {
+        case TC_OP_LOAD_X: return TC_OK;  // the staged input buffer is the var's storage
+        case TC_OP_LOAD_Y: return launch_onehot(c->d_labels, reinterpret_cast<float*>(y), out.N, out.C, st);
+        case TC_OP_CONV_FWD: {
+            const VarL& x = P.L(s.in[0]);
+            const ParamL& w = c->params[s.in[1].index];
+            tc_conv_desc d = conv_desc(x, w, out, s);
+            const float* bias = s.nin > 2 ? c->params[s.in[2].index].p : nullptr;
+            return tc_conv2d_fwd(&d, P.var(x.id), w.shadow, bias, c->fuse_relu[i], y, c->ws, c->ws_bytes, st);
+        }
+        case TC_OP_CONV_BWD_DATA: {
+            const VarL& dy = P.L(s.in[0]);
+            const ParamL& w = c->params[s.in[1].index];
+            tc_conv_desc d = conv_desc(out, w, dy, s);
+            return tc_conv2d_bwd_data(&d, P.var(dy.id), w.rskc, y, c->ws, c->ws_bytes, st);
+        }
+        case TC_OP_POOL_FWD: {
+            const VarL& x = P.L(s.in[0]);
+            int32_t* idx = s.max_pool ? reinterpret_cast<int32_t*>(c->arena + c->items[c->pool_idx_item.at(s.var)].off) : nullptr;
+            return launch_pool_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), x.act(), reinterpret_cast<bf16*>(y),
+                                   out.act(), idx, s.k, s.stride, s.pad, s.max_pool, st);
+        }
+        case TC_OP_POOL_BWD: {
+            const VarL& up = P.L(s.in[0]);
+            const VarL& fy = P.L(s.in[1]);
+            const int32_t* idx = s.max_pool ? reinterpret_cast<int32_t*>(c->arena + c->items[c->pool_idx_item.at(fy.id)].off)
+                                            : nullptr;
+            Act4 ya = fy.act();
+            return launch_pool_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), ya, idx, reinterpret_cast<bf16*>(y),
+                                   out.act(), s.k, s.stride, s.pad, s.max_pool, st);
+        }
+        case TC_OP_RELU_FWD:
+            return launch_relu_fwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)), reinterpret_cast<bf16*>(y),
+                                   out.elems(), st);
+        case TC_OP_RELU_BWD:
+            return launch_relu_bwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
+                                   reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+                                   out.elems(), st);
+        case TC_OP_SOFTMAX_FWD: {
+            const VarL& x = P.L(s.in[0]);
+            return launch_softmax_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), x.cs, reinterpret_cast<float*>(y), out.N,
+                                      out.C, st);
+        }
+        case TC_OP_SOFTMAX_BWD:
+            return launch_softmax_bwd(reinterpret_cast<const float*>(P.var(s.in[0].index)),
+                                      reinterpret_cast<const float*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+                                      out.cs, out.N, out.C, st);
+        case TC_OP_LRN_FWD:
+            return launch_lrn_fwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)), reinterpret_cast<bf16*>(y), out.act(),
+                                  s.lrn_size, static_cast<float>(s.alpha), static_cast<float>(s.beta),
+                                  static_cast<float>(s.lrn_k), st);
+        case TC_OP_LRN_BWD:
+            return launch_lrn_bwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
+                                  reinterpret_cast<const bf16*>(P.var(s.in[2].index)),
+                                  reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+                                  out.act(), s.lrn_size, static_cast<float>(s.alpha), static_cast<float>(s.beta),
+                                  static_cast<float>(s.lrn_k), st);
+        case TC_OP_DROPOUT_MASK:
+            return launch_dropout_mask(reinterpret_cast<uint8_t*>(y), out.N, out.H, out.W, out.C, out.cs,
+                                       static_cast<float>(s.rate), c->desc.seed, static_cast<uint32_t>(s.var), c->d_iter,
+                                       st);
+        case TC_OP_MUL: {
+            const VarL& a = P.L(s.in[0]);
+            const VarL& b = P.L(s.in[1]);
+            if (out.dtype == DT_F32)
+                return launch_f32_ew(F32_MUL, reinterpret_cast<const float*>(P.var(a.id)),
+                                     reinterpret_cast<const float*>(P.var(b.id)), 1.f, reinterpret_cast<float*>(y),
+                                     out.elems(), st);
+            const VarL& m = b.dtype == DT_U8 ? b : a;
+            const VarL& x = b.dtype == DT_U8 ? a : b;
+            if (m.dtype != DT_U8) return fail(TC_INTERNAL, "runtime: bf16 x bf16 MUL is not in the op set");
+            const float rate = c->mask_rate.at(m.id);
+            return launch_mask_mul(reinterpret_cast<const bf16*>(P.var(x.id)), reinterpret_cast<const uint8_t*>(P.var(m.id)),
+                                   1.f / (1.f - rate), reinterpret_cast<bf16*>(y), out.elems(), st);
+        }
+        case TC_OP_ADD:
+            if (out.dtype == DT_F32)
+                return launch_f32_ew(F32_ADD, reinterpret_cast<const float*>(P.var(s.in[0].index)),
+                                     reinterpret_cast<const float*>(P.var(s.in[1].index)), 1.f, reinterpret_cast<float*>(y),
+                                     out.elems(), st);
+            return launch_add_bf16(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
+                                   reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+                                   out.elems(), st);
+        case TC_OP_SCALE:
+        case TC_OP_LOG:
+        case TC_OP_RECIP: {
+            if (out.dtype != DT_F32) return fail(TC_INTERNAL, "runtime: Log/Recip/Scale expected on fp32 loss-head tensors");
+            const int op = s.op == TC_OP_LOG ? F32_LOG : s.op == TC_OP_RECIP ? F32_RECIP : F32_SCALE;
+            return launch_f32_ew(op, reinterpret_cast<const float*>(P.var(s.in[0].index)), nullptr,
+                                 static_cast<float>(s.scale), reinterpret_cast<float*>(y), out.elems(), st);
+        }
+        case TC_OP_MATMUL_FWD: {
+            const VarL& a = P.L(s.in[0]);
+            const ParamL& w = c->params[s.in[1].index];
+            tc_gemm_args ga{};
+            ga.M = a.N;
+            ga.N = out.cs;  // padded columns come out as zeros (zero weight rows, masked bias)
+            ga.K = w.in_dev;
+            ga.a_layout = TC_LAYOUT_K;
+            ga.A = P.var(a.id);
+            ga.lda = w.in_dev;
+            ga.b_layout = TC_LAYOUT_K;
+            ga.B = w.shadow;
+            ga.ldb = w.in_dev;
+            ga.D = y;
+            ga.ldd = out.cs;
+            ga.d_dtype = TC_DTYPE_BF16;
+            ga.bias = c->fuse_bias[i] ? c->params[c->fuse_bias_param[i]].p : nullptr;
+            ga.relu = c->fuse_relu[i];
+            ga.alpha = 1.f;
+            // the GEMM reads bias[n] for n < N; the bias param has exactly out.C entries
+            if (ga.bias && out.cs != out.C) {
+                ga.bias = nullptr;
+                tc_status r = run_gemm_args(c, ga);
+                if (r != TC_OK) return r;
+                return launch_bias_add(reinterpret_cast<const bf16*>(y), c->params[c->fuse_bias_param[i]].p,
+                                       reinterpret_cast<bf16*>(y), out.N, out.C, out.cs, c->fuse_relu[i], st);
+            }
+            return run_gemm_args(c, ga);
+        }
+        case TC_OP_MATMUL_BWD_DATA: {
+            const VarL& up = P.L(s.in[0]);
+            const ParamL& w = c->params[s.in[1].index];
+            tc_gemm_args ga{};
+            ga.M = up.N;
+            ga.N = w.in_dev;
+            ga.K = w.K;
+            ga.a_layout = TC_LAYOUT_K;
+            ga.A = P.var(up.id);
+            ga.lda = up.cs;
+            ga.b_layout = TC_LAYOUT_MN;
+            ga.B = w.shadow;
+            ga.ldb = w.in_dev;
+            ga.D = y;
+            ga.ldd = w.in_dev;
+            ga.d_dtype = TC_DTYPE_BF16;
+            ga.alpha = 1.f;
+            return run_gemm_args(c, ga);
+        }
+        case TC_OP_BIAS_ADD: {
+            const VarL& x = P.L(s.in[0]);
+            return launch_bias_add(reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[1].index].p,
+                                   reinterpret_cast<bf16*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, 0, st);
+        }
+        case TC_OP_CONCAT: {
+            if (out.cs != out.C) {
+                tc_status r = launch_zero(y, out.bytes(), st);
+                if (r != TC_OK) return r;
+            }
+            int off = 0;
+            for (int k = 0; k < s.nin; ++k) {
+                const VarL& part = P.L(s.in[k]);
+                tc_status r = launch_channel_copy(reinterpret_cast<const bf16*>(P.var(part.id)), part.cs,
+                                                  reinterpret_cast<bf16*>(y), out.cs, off, part.C,
+                                                  static_cast<long long>(out.N) * out.H * out.W, st);
+                if (r != TC_OK) return r;
+                off += part.C;
+            }
+            return TC_OK;
+        }
+        case TC_OP_CONCAT_BWD: {
+            const VarL& up = P.L(s.in[0]);
+            if (out.cs != out.C) {
+                tc_status r = launch_zero(y, out.bytes(), st);
+                if (r != TC_OK) return r;
+            }
+            return launch_channel_copy(reinterpret_cast<const bf16*>(P.var(up.id)) + s.offset, up.cs,
+                                       reinterpret_cast<bf16*>(y), out.cs, 0, static_cast<int>(s.extent),
+                                       static_cast<long long>(out.N) * out.H * out.W, st);
+        }
+        case TC_OP_BN_FWD: {
+            const VarL& x = P.L(s.in[0]);
+            float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
+            return launch_bn_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[1].index].p,
+                                 c->params[s.in[2].index].p, reinterpret_cast<bf16*>(y), stats,
+                                 static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, static_cast<float>(s.eps),
+                                 c->partials, c->max_partials, st);
+        }
+        case TC_OP_BN_BWD_DATA: {
+            const VarL& up = P.L(s.in[0]);
+            const VarL& x = P.L(s.in[1]);
+            const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
+            return launch_bn_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), reinterpret_cast<const bf16*>(P.var(x.id)),
+                                 c->params[s.in[2].index].p, stats, reinterpret_cast<bf16*>(y), nullptr, nullptr,
+                                 static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, c->partials, c->max_partials, st);
+        }
+        default: break;
+    }
+    return fail(TC_INTERNAL, "runtime: unsupported Let op " + std::to_string(s.op));
+}
+
+tc_status exec_stmt(tc_ctx* c, int i) {
+    const tc_stmt& s = c->plan->stmts[i];
+    if (s.kind == TC_STMT_DEALLOC) return TC_OK;  // static arena: lifetimes were resolved at plan load
+    if (s.kind == TC_STMT_LET) return c->fused[i] ? TC_OK : exec_let(c, i);
+    if (s.kind == TC_STMT_PRINT) {
+        Ptrs P{c};
+        const float* a[4];
+        const float* b[4];
+        long long n[4];
+        double coef[4];
+        for (int t = 0; t < s.nterms; ++t) {
+            a[t] = reinterpret_cast<const float*>(P.var(s.in[2 * t].index));
+            b[t] = reinterpret_cast<const float*>(P.var(s.in[2 * t + 1].index));
+            n[t] = c->vars.at(s.in[2 * t].index).elems();
+            coef[t] = s.coef[t];
+        }
+        return launch_loss(a, b, n, coef, s.nterms, c->d_loss, c->st);
+    }
+    // Update: gradient -> (all-reduce) -> fused momentum SGD
+    ParamL& q = c->params[s.param];
+    tc_status r = compute_param_grad(c, s, s.param, q.g);
+    if (r != TC_OK) return r;
+    if (c->comm) {
+        if (ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
+            return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
+    }
+    return TC_OK;
+}
+
+tc_status apply_update(tc_ctx* c, int i, int update) {
+    const tc_stmt& s = c->plan->stmts[i];
+    if (s.kind != TC_STMT_UPDATE || !update) return TC_OK;
+    ParamL& q = c->params[s.param];
+    SgdTensor t{};
+    t.p = q.p;
+    t.v = q.v;
+    t.g = q.g;
+    t.n = q.n;
+    t.shadow = q.shadow;
+    t.shadow_rskc = q.rskc;
+    t.K = q.K;
+    t.RS = q.R * q.S;
+    t.cs = q.cs;
+    t.ks = q.ks;
+    t.lr_alpha = static_cast<float>(s.lr_alpha);
+    t.momentum = static_cast<float>(s.momentum);
+    t.decay = static_cast<float>(s.decay);
+    return launch_sgd(&t, 1, nullptr, c->st);
+}
+
+tc_status run_body(tc_ctx* c, int update) {
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
+    for (int i = 0; i < c->plan->nstmts; ++i) {
+        tc_status r = exec_stmt(c, i);
+        if (r != TC_OK) return r;
+        r = apply_update(c, i, update);
+        if (r != TC_OK) return r;
+    }
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    return TC_OK;
+}
+
+size_t workspace_need(tc_ctx* c) {
+    size_t need = 0;
+    const tc_plan* p = c->plan;
+    Ptrs P{c};
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET && s.kind != TC_STMT_UPDATE) continue;
+        switch (s.op) {
+            case TC_OP_CONV_FWD: {
+                const VarL& x = P.L(s.in[0]);
+                tc_conv_desc d = conv_desc(x, c->params[s.in[1].index], c->vars.at(s.var), s);
+                need = std::max(need, tc_conv2d_workspace_bytes(&d, 0));
+                break;
+            }
+            case TC_OP_CONV_BWD_DATA: {
+                tc_conv_desc d = conv_desc(c->vars.at(s.var), c->params[s.in[1].index], P.L(s.in[0]), s);
+                need = std::max(need, tc_conv2d_workspace_bytes(&d, 1));
+                break;
+            }
+            case TC_OP_CONV_BWD_FILTER: {
+                tc_conv_desc d = conv_desc(P.L(s.in[1]), c->params[s.param], P.L(s.in[0]), s);
+                need = std::max(need, tc_conv2d_workspace_bytes(&d, 2));
+                break;
+            }
+            case TC_OP_MATMUL_FWD:
+            case TC_OP_MATMUL_BWD_DATA:
+            case TC_OP_MATMUL_BWD_W: {
+                tc_gemm_args ga{};
+                if (s.op == TC_OP_MATMUL_FWD) {
+                    const ParamL& w = c->params[s.in[1].index];
+                    ga.M = P.L(s.in[0]).N;
+                    ga.N = c->vars.at(s.var).cs;
+                    ga.K = w.in_dev;
+                } else if (s.op == TC_OP_MATMUL_BWD_DATA) {
+                    const ParamL& w = c->params[s.in[1].index];
+                    ga.M = P.L(s.in[0]).N;
+                    ga.N = w.in_dev;
+                    ga.K = w.K;
+                } else {
+                    const ParamL& w = c->params[s.param];
+                    ga.M = w.K;
+                    ga.N = w.in_dev;
+                    ga.K = P.L(s.in[0]).N;
+                }
+                need = std::max(need, tc_gemm_workspace_bytes(&ga));
+                break;
+            }
+            default: break;
+        }
+    }
+    return need;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+tc_status tc_nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return fail(TC_NCCL_ERROR, "ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof id);
+    return TC_OK;
+}
+
+tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** out) {
+    if (!plan || !desc || !out) return fail(TC_INVALID_ARG, "tc_ctx_create: null argument");
+    *out = nullptr;
+    auto c = std::make_unique<tc_ctx>();
+    c->plan = plan;
+    c->desc = *desc;
+    if (c->desc.seed == 0) c->desc.seed = 42;
+    TCB_CUDA_CHECK(cudaSetDevice(desc->device));
+    TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    tc_status r = analyze_layouts(c.get());
+    if (r != TC_OK) return r;
+    plan_fusion(c.get());
+    r = plan_arena(c.get());
+    if (r != TC_OK) return r;
+    // parameter slab
+    size_t slab = 0;
+    auto reserve = [&](size_t bytes) {
+        const size_t off = slab;
+        slab += align256(bytes);
+        return off;
+    };
+    std::vector<size_t> offs;
+    for (ParamL& q : c->params) {
+        offs.push_back(reserve(q.n * 4));  // p
+        offs.push_back(reserve(q.n * 4));  // v
+        offs.push_back(reserve(q.n * 4));  // g
+        offs.push_back(q.kind != ParamL::VEC ? reserve(q.n * 2) : SIZE_MAX);
+        offs.push_back(q.kind == ParamL::CONV ? reserve(static_cast<size_t>(q.R) * q.S * q.ks * q.cs * 2) : SIZE_MAX);
+    }
+    c->slab_bytes = slab;
+    TCB_CUDA_CHECK(cudaMalloc(&c->slab, std::max<size_t>(slab, 256)));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->slab, 0, std::max<size_t>(slab, 256), c->st));
+    for (size_t i = 0; i < c->params.size(); ++i) {
+        ParamL& q = c->params[i];
+        q.p = reinterpret_cast<float*>(c->slab + offs[5 * i]);
+        q.v = reinterpret_cast<float*>(c->slab + offs[5 * i + 1]);
+        q.g = reinterpret_cast<float*>(c->slab + offs[5 * i + 2]);
+        if (offs[5 * i + 3] != SIZE_MAX) q.shadow = reinterpret_cast<bf16*>(c->slab + offs[5 * i + 3]);
+        if (offs[5 * i + 4] != SIZE_MAX) q.rskc = reinterpret_cast<bf16*>(c->slab + offs[5 * i + 4]);
+    }
+    // arena
+    TCB_CUDA_CHECK(cudaMalloc(&c->arena, std::max<size_t>(c->arena_bytes, 256)));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
+    // input staging: NHWC bf16 batch + labels + NCHW fp32 staging for host batches
+    c->input_cs = ceil8(plan->input_dims[1]);
+    const size_t in_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[2] * plan->input_dims[3] * c->input_cs;
+    const size_t stage_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
+    c->input_bytes = in_el * 2 + stage_el * 4;
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_input, in_el * 2));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_input, 0, in_el * 2, c->st));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_stage, stage_el * 4));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_labels, 0, plan->input_dims[0] * sizeof(int32_t), c->st));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 256));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_iter, 256));
+    TCB_CUDA_CHECK(cudaMallocHost(&c->h_iter, 256));
+    TCB_CUDA_CHECK(cudaMallocHost(&c->h_loss, 256));
+    c->h_iter[0] = c->h_iter[1] = 0;
+    c->h_loss[0] = 0.f;
+    // workspace + reduction partials
+    c->ws_bytes = workspace_need(c.get());
+    int maxc = 8;
+    for (auto& [id, v] : c->vars) maxc = std::max(maxc, v.cs);
+    for (const ParamL& q : c->params) maxc = std::max(maxc, q.K);
+    c->max_partials = static_cast<int>(colsum_partials_floats(maxc));
+    TCB_CUDA_CHECK(cudaMalloc(&c->ws, std::max<size_t>(c->ws_bytes, 256)));
+    TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 2 * maxc + 64) * sizeof(float)));
+    if (desc->world > 1) {
+        if (!desc->nccl_id) return fail(TC_INVALID_ARG, "world > 1 needs an NCCL unique id");
+        ncclUniqueId id;
+        std::memcpy(&id, desc->nccl_id, sizeof id);
+        if (ncclCommInitRank(&c->comm, desc->world, id, desc->rank) != ncclSuccess)
+            return fail(TC_NCCL_ERROR, "ncclCommInitRank failed");
+    }
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) c->device_used = static_cast<int64_t>(tot - fr);
+    *out = c.release();
+    return TC_OK;
+}
+
+void tc_ctx_destroy(tc_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->desc.device);
+    if (c->st) cudaStreamSynchronize(c->st);
+    for (int k = 0; k < 2; ++k) {
+        if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
+        if (c->graph[k]) cudaGraphDestroy(c->graph[k]);
+    }
+    if (c->comm) ncclCommDestroy(c->comm);
+    cudaFree(c->arena);
+    cudaFree(c->slab);
+    cudaFree(c->ws);
+    cudaFree(c->partials);
+    cudaFree(c->d_input);
+    cudaFree(c->d_stage);
+    cudaFree(c->d_labels);
+    cudaFree(c->d_loss);
+    cudaFree(c->d_iter);
+    cudaFreeHost(c->h_iter);
+    cudaFreeHost(c->h_loss);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+void* tc_ctx_stream(tc_ctx* c) { return c ? c->st : nullptr; }
+
+tc_status tc_param_upload(tc_ctx* c, int i, const float* host) {
+    if (!c || !host || i < 0 || i >= static_cast<int>(c->params.size())) return fail(TC_INVALID_ARG, "tc_param_upload");
+    std::vector<float> dev;
+    ref_to_dev(c->params[i], host, dev);
+    return upload_dev_param(c, i, dev);
+}
+
+static tc_status download_slab(tc_ctx* c, int i, const float* dptr, float* host) {
+    const ParamL& q = c->params[i];
+    std::vector<float> dev(q.n);
+    TCB_CUDA_CHECK(cudaMemcpyAsync(dev.data(), dptr, q.n * 4, cudaMemcpyDeviceToHost, c->st));
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    dev_to_ref(q, dev.data(), host);
+    return TC_OK;
+}
+
+tc_status tc_param_download(tc_ctx* c, int i, float* host) {
+    if (!c || !host || i < 0 || i >= static_cast<int>(c->params.size())) return fail(TC_INVALID_ARG, "tc_param_download");
+    return download_slab(c, i, c->params[i].p, host);
+}
+tc_status tc_velocity_download(tc_ctx* c, int i, float* host) {
+    if (!c || !host || i < 0 || i >= static_cast<int>(c->params.size())) return fail(TC_INVALID_ARG, "tc_velocity_download");
+    return download_slab(c, i, c->params[i].v, host);
+}
+tc_status tc_grad_download(tc_ctx* c, int i, float* host) {
+    if (!c || !host || i < 0 || i >= static_cast<int>(c->params.size())) return fail(TC_INVALID_ARG, "tc_grad_download");
+    return download_slab(c, i, c->params[i].g, host);
+}
+
+tc_status tc_init_params(tc_ctx* c) {
+    if (!c) return fail(TC_INVALID_ARG, "tc_init_params");
+    const tc_plan* p = c->plan;
+    for (int i = 0; i < p->nparams; ++i) {
+        const tc_param_desc& pd = p->params[i];
+        long long n = 1;
+        for (int j = 0; j < pd.rank; ++j) n *= pd.dims[j];
+        std::vector<float> ref(n);
+        if (pd.init_kind == TC_INIT_CONSTANT) {
+            std::fill(ref.begin(), ref.end(), static_cast<float>(pd.init_value));
+        } else if (pd.init_kind == TC_INIT_XAVIER) {
+            const double a = std::sqrt(6.0 / static_cast<double>(pd.fan_in + pd.fan_out));
+            for (long long j = 0; j < n; ++j)
+                ref[j] = static_cast<float>((2.0 * tcp_param_uniform(c->desc.seed, i, static_cast<uint32_t>(j)) - 1.0) * a);
+        } else {
+            for (long long j = 0; j < n; ++j) {
+                const double u1 = tcp_param_uniform(c->desc.seed, i, static_cast<uint32_t>(2 * j));
+                const double u2 = tcp_param_uniform(c->desc.seed, i, static_cast<uint32_t>(2 * j + 1));
+                ref[j] = static_cast<float>(pd.sigma * std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2));
+            }
+        }
+        tc_status r = tc_param_upload(c, i, ref.data());
+        if (r != TC_OK) return r;
+        TCB_CUDA_CHECK(cudaMemsetAsync(c->params[i].v, 0, c->params[i].n * 4, c->st));
+    }
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+tc_status tc_stage_batch(tc_ctx* c, const float* x, const int32_t* labels) {
+    if (!c || !x || !labels) return fail(TC_INVALID_ARG, "tc_stage_batch: null argument");
+    const tc_plan* p = c->plan;
+    const size_t el = static_cast<size_t>(p->input_dims[0]) * p->input_dims[1] * p->input_dims[2] * p->input_dims[3];
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, x, el * 4, cudaMemcpyHostToDevice, c->st));
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, labels, p->input_dims[0] * 4, cudaMemcpyHostToDevice, c->st));
+    return launch_nchw_to_nhwc(c->d_stage, c->d_input, static_cast<int>(p->input_dims[0]), static_cast<int>(p->input_dims[1]),
+                               static_cast<int>(p->input_dims[2]), static_cast<int>(p->input_dims[3]), c->input_cs, c->st);
+}
+
+tc_status tc_stage_synthetic(tc_ctx* c, int iter, int n0) {
+    if (!c) return fail(TC_INVALID_ARG, "tc_stage_synthetic");
+    const tc_plan* p = c->plan;
+    return launch_synth_batch(c->d_input, c->d_labels, static_cast<int>(p->input_dims[0]), static_cast<int>(p->input_dims[1]),
+                              static_cast<int>(p->input_dims[2]), static_cast<int>(p->input_dims[3]), c->input_cs,
+                              static_cast<int>(p->classes), c->desc.seed, static_cast<uint32_t>(iter),
+                              static_cast<uint32_t>(n0), c->st);
+}
+
+tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
+    if (!c) return fail(TC_INVALID_ARG, "tc_step");
+    TCB_CUDA_CHECK(cudaSetDevice(c->desc.device));
+    const int k = update ? 1 : 0;
+    // iteration counters are read by the dropout kernels through device memory,
+    // so a captured graph replays correctly for every iteration
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    c->h_iter[0] = static_cast<uint32_t>(iter);
+    c->h_iter[1] = static_cast<uint32_t>(n0);
+    if (c->gexec[k]) {
+        TCB_CUDA_CHECK(cudaGraphLaunch(c->gexec[k], c->st));
+        count_launch(static_cast<unsigned>(std::max(0, c->launches_per_step)));
+        return TC_OK;
+    }
+    const bool capture = c->desc.use_graph && c->runs[k] >= 1 && !c->comm;
+    const unsigned long long before = g_launches.load();
+    if (capture) TCB_CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    tc_status r = run_body(c, update);
+    if (capture) {
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->st, &g);
+        if (r != TC_OK) return r;
+        if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(e));
+        c->graph[k] = g;
+        TCB_CUDA_CHECK(cudaGraphInstantiate(&c->gexec[k], g, 0));
+        TCB_CUDA_CHECK(cudaGraphLaunch(c->gexec[k], c->st));
+    }
+    if (r != TC_OK) return r;
+    if (c->launches_per_step < 0) c->launches_per_step = static_cast<int>(g_launches.load() - before);
+    c->runs[k]++;
+    return TC_OK;
+}
+
+tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
+    if (!c || index < 0 || index >= c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_exec_stmt");
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    c->h_iter[0] = static_cast<uint32_t>(iter);
+    c->h_iter[1] = static_cast<uint32_t>(n0);
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 8, cudaMemcpyHostToDevice, c->st));
+    tc_status r = exec_stmt(c, index);
+    if (r != TC_OK) return r;
+    return apply_update(c, index, 1);
+}
+
+tc_status tc_loss(tc_ctx* c, double* loss) {
+    if (!c || !loss) return fail(TC_INVALID_ARG, "tc_loss");
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    *loss = c->h_loss[0];
+    return TC_OK;
+}
+
+tc_status tc_sync(tc_ctx* c) {
+    if (!c) return fail(TC_INVALID_ARG, "tc_sync");
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+tc_status tc_var_download(tc_ctx* c, int var, float* host, int64_t max_elems) {
+    if (!c || !host) return fail(TC_INVALID_ARG, "tc_var_download");
+    auto it = c->vars.find(var);
+    if (it == c->vars.end() || it->second.def < 0) return fail(TC_INVALID_ARG, "tc_var_download: unknown var");
+    const VarL& v = it->second;
+    Ptrs P{c};
+    std::vector<uint8_t> raw(v.bytes());
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    TCB_CUDA_CHECK(cudaMemcpy(raw.data(), P.var(var), raw.size(), cudaMemcpyDeviceToHost));
+    auto at = [&](long long e) -> float {
+        if (v.dtype == DT_F32) return reinterpret_cast<const float*>(raw.data())[e];
+        if (v.dtype == DT_U8) return raw[e] ? 1.f / (1.f - c->mask_rate.at(var)) : 0.f;
+        return bf2f(reinterpret_cast<const uint16_t*>(raw.data())[e]);
+    };
+    long long count = 1;
+    for (int j = 0; j < v.rank; ++j) count *= v.d[j];
+    if (count > max_elems) return fail(TC_INVALID_ARG, "tc_var_download: buffer too small");
+    if (v.nhwc) {  // reference NCHW order (also for the 2-D view of a flattened tensor)
+        for (int n = 0; n < v.N; ++n)
+            for (int ch = 0; ch < v.C; ++ch)
+                for (int h = 0; h < v.H; ++h)
+                    for (int w = 0; w < v.W; ++w)
+                        host[((static_cast<long long>(n) * v.C + ch) * v.H + h) * v.W + w] =
+                            at(((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch);
+    } else {
+        for (int n = 0; n < v.N; ++n)
+            for (int f = 0; f < v.C; ++f) host[static_cast<long long>(n) * v.C + f] = at(static_cast<long long>(n) * v.cs + f);
+    }
+    return TC_OK;
+}
+
+tc_status tc_pool_indices_download(tc_ctx* c, int var, int32_t* host, int64_t max_elems) {
+    if (!c || !host) return fail(TC_INVALID_ARG, "tc_pool_indices_download");
+    auto it = c->pool_idx_item.find(var);
+    if (it == c->pool_idx_item.end()) return fail(TC_INVALID_ARG, "not a max-pool output var");
+    const VarL& v = c->vars.at(var);
+    std::vector<int32_t> raw(v.elems());
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    TCB_CUDA_CHECK(cudaMemcpy(raw.data(), c->arena + c->items[it->second].off, raw.size() * 4, cudaMemcpyDeviceToHost));
+    const long long count = static_cast<long long>(v.N) * v.C * v.H * v.W;
+    if (count > max_elems) return fail(TC_INVALID_ARG, "buffer too small");
+    for (int n = 0; n < v.N; ++n)
+        for (int ch = 0; ch < v.C; ++ch)
+            for (int h = 0; h < v.H; ++h)
+                for (int w = 0; w < v.W; ++w)
+                    host[((static_cast<long long>(n) * v.C + ch) * v.H + h) * v.W + w] =
+                        raw[((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch];
+    return TC_OK;
+}
+
+tc_status tc_memory(tc_ctx* c, tc_rt_memory* out) {
+    if (!c || !out) return fail(TC_INVALID_ARG, "tc_memory");
+    out->arena_bytes = static_cast<int64_t>(c->arena_bytes);
+    out->arena_keep_bytes = static_cast<int64_t>(c->arena_keep_bytes);
+    out->param_bytes = static_cast<int64_t>(c->slab_bytes);
+    out->workspace_bytes = static_cast<int64_t>(c->ws_bytes);
+    out->input_bytes = static_cast<int64_t>(c->input_bytes);
+    out->device_used_bytes = c->device_used;
+    return TC_OK;
+}
+
+int tc_launches_per_step(tc_ctx* c) { return c ? c->launches_per_step : -1; }
+
+tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_ms, int max) {
+    if (!c || !stmt_ms || max < c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_profile_step");
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    c->h_iter[0] = static_cast<uint32_t>(iter);
+    c->h_iter[1] = static_cast<uint32_t>(n0);
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 8, cudaMemcpyHostToDevice, c->st));
+    const int n = c->plan->nstmts;
+    std::vector<cudaEvent_t> ev(n + 1);
+    for (auto& e : ev) TCB_CUDA_CHECK(cudaEventCreate(&e));
+    TCB_CUDA_CHECK(cudaEventRecord(ev[0], c->st));
+    tc_status r = TC_OK;
+    for (int i = 0; i < n && r == TC_OK; ++i) {
+        r = exec_stmt(c, i);
+        if (r == TC_OK) r = apply_update(c, i, update);
+        cudaEventRecord(ev[i + 1], c->st);
+    }
+    cudaStreamSynchronize(c->st);
+    for (int i = 0; i < n; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        stmt_ms[i] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return r;
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+"""Whole-step parity of the sm_100a executor against the CPU oracle on the same
+plan, the same parameters and the same synthetic batch (BASELINE.json
+north_star tolerances):
+
+  * max-pool argmax indices: bit-exact (checked per op on identical inputs);
+  * tensor-core / bf16-storage ops: relative error (max|err| / max|ref|)
+    <= 1e-2 per op; whole-step intermediates are checked at 5e-2 because bf16
+    rounding compounds through the chain;
+  * loss: 1e-2 relative; 100-step LeNet loss trajectory within 2e-2 absolute
+    (bf16 activations; fp32 master weights).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as orc  # noqa: E402
+from paper_1701_02284_b200 import _native as nat  # noqa: E402
+from paper_1701_02284_b200.network import compile_network  # noqa: E402
+from paper_1701_02284_b200.runtime import Trainer  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+STEP_TOL = 5e-2
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-6))
+
+
+def make_pair(name, batch, seed=11, keep=True, use_graph=False, **kw):
+    net = compile_network(name, batch, **kw)
+    tr = Trainer(net, keep=keep, use_graph=use_graph, seed=seed)
+    tr.init_params()
+    o = orc.Oracle(net, seed=seed)
+    o.init_params()
+    for i in range(len(net.params)):  # identical starting point
+        np.testing.assert_array_equal(tr.get_param(i), o.get_param(i))
+    return net, tr, o
+
+
+def storage_final_vars(net):
+    """Last alias of every storage (what both executors hold after the step)."""
+    last = {}
+    for s in net.stmts:
+        if s.kind == nat.TC_STMT_LET:
+            last[s.storage] = s.var
+    return sorted(last.values())
+
+
+@pytest.mark.parametrize("name,batch", [("lenet", 16), ("inception", 4), ("alexnet", 2)])
+def test_step_parity(name, batch):
+    net, tr, o = make_pair(name, batch)
+    x, y = orc.synth_batch(net, 11, 0)
+    tr.stage_batch(x, y)
+    o.set_batch(x, y)
+    tr.step(0, update=False)
+    lg = tr.loss()
+    lo = o.step(0, update=False, keep=True)
+    assert abs(lg - lo) <= 1e-2 * abs(lo), (lg, lo)
+    worst = []
+    for v in storage_final_vars(net):
+        dev = tr.var(v)
+        ref = o.var(v)
+        worst.append((rel(dev, ref), v))
+    worst.sort(reverse=True)
+    assert worst[0][0] <= STEP_TOL, worst[:5]
+    for i, p in enumerate(net.params):
+        e = rel(tr.grad(i), o.grad(i))
+        assert e <= STEP_TOL, (p.name, e)
+
+
+def test_pool_indices_bit_exact():
+    net, tr, o = make_pair("lenet", 8)
+    x, y = orc.synth_batch(net, 11, 0)
+    tr.stage_batch(x, y)
+    tr.step(0, update=False)
+    pools = [s for s in net.stmts if s.kind == nat.TC_STMT_LET and nat.OP_NAMES[s.op] == "POOL_FWD"]
+    assert pools
+    L = orc.lib()
+    for s in pools:
+        xin = tr.var(s.inp[0].index)  # the device's own (bf16) input, exactly representable in fp32
+        n, c, h, w = xin.shape
+        ho, wo = net.var_dims(s.var)[2:]
+        ref_y = np.empty((n, c, ho, wo), np.float32)
+        ref_i = np.empty((n, c, ho, wo), np.int32)
+        L.orc_pool_fwd_f32(np.ascontiguousarray(xin), ref_y, ref_i.ctypes.data, n, c, h, w, s.k, s.stride, s.pad, 1)
+        np.testing.assert_array_equal(tr.pool_indices(s.var), ref_i)
+        np.testing.assert_array_equal(tr.var(s.var), ref_y)
+
+
+def test_graph_replay_matches_eager():
+    net = compile_network("lenet", 16)
+    a = Trainer(net, use_graph=False, seed=3)
+    b = Trainer(net, use_graph=True, seed=3)
+    a.init_params()
+    b.init_params()
+    la, lb = [], []
+    for it in range(4):
+        for t, out in ((a, la), (b, lb)):
+            t.stage_synthetic(it)
+            t.step(it)
+            out.append(t.loss())
+    assert la == lb
+    for i in range(len(net.params)):
+        np.testing.assert_array_equal(a.get_param(i), b.get_param(i))
+
+
+def test_device_synthetic_matches_oracle():
+    net = compile_network("lenet", 8)
+    tr = Trainer(net, keep=True, seed=42)
+    tr.stage_synthetic(5, 16)
+    tr.init_params()
+    tr.step(5, 16, update=False)
+    x, y = orc.synth_batch(net, 42, 5, 16)
+    xv = tr.var(min(s.var for s in net.stmts if s.kind == nat.TC_STMT_LET))  # Cuda(X)
+    assert np.max(np.abs(xv - x)) <= 2e-2 * np.max(np.abs(x))  # bf16 storage of identical fp32 draws
+
+
+def test_lenet_loss_trajectory_100_steps():
+    """100-step training trajectory vs the oracle on identical batches."""
+    net, tr, o = make_pair("lenet", 64, keep=False, use_graph=True, seed=42)
+    lg, lo = [], []
+    for it in range(100):
+        x, y = orc.synth_batch(net, 42, it)
+        tr.stage_batch(x, y)
+        tr.step(it)
+        lg.append(tr.loss())
+        o.set_batch(x, y)
+        lo.append(o.step(it))
+    lg, lo = np.array(lg), np.array(lo)
+    assert abs(lg[0] - np.log(10)) < 0.1
+    assert np.max(np.abs(lg - lo)) < 2e-2, np.max(np.abs(lg - lo))
+    assert lg[-10:].mean() < lg[:10].mean() * 0.7
+
+
+@pytest.mark.parametrize("name,batch", [("googlenet", 2), ("resnet50", 2)])
+def test_big_network_step_parity(name, batch):
+    net, tr, o = make_pair(name, batch)
+    x, y = orc.synth_batch(net, 11, 0)
+    tr.stage_batch(x, y)
+    o.set_batch(x, y)
+    tr.step(0, update=False)
+    lg = tr.loss()
+    lo = o.step(0, update=False, keep=True)
+    assert abs(lg - lo) <= 2e-2 * abs(lo), (lg, lo)
+    errs = sorted(((rel(tr.grad(i), o.grad(i)), p.name) for i, p in enumerate(net.params)), reverse=True)
+    assert errs[0][0] <= 0.1, errs[:5]
