@@ -228,10 +228,10 @@ def run_gpu(args):
         f, b = stmt_work(net, s, nat)
         if f:
             flops_tc += f
-            t_tc += stmt_ms[i]
+            t_tc += float(stmt_ms[i])
         else:
             bytes_bw += b
-            t_bw += stmt_ms[i]
+            t_bw += float(stmt_ms[i])
 
     times = torch.tensor([ms, e2e_ms], dtype=torch.float64)
     if world > 1:

@@ -44,8 +44,8 @@ def lib() -> C.CDLL:
             getattr(L, f"orc_softmax_fwd_{sfx}").argtypes = [P, P, ci, ci]
             getattr(L, f"orc_softmax_bwd_{sfx}").argtypes = [P, P, P, ci, ci]
             getattr(L, f"orc_bn_fwd_{sfx}").argtypes = [P, P, P, P, ci, ci, ci, C.c_double]
-            getattr(L, f"orc_bn_bwd_{sfx}").argtypes = [P, P, P, C.c_void_p, C.c_void_p, C.c_void_p, ci, ci, ci,
-                                                        C.c_double]
+            getattr(L, f"orc_bn_bwd_{sfx}").argtypes = [P, P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, ci,
+                                                        ci, ci, C.c_double]
             getattr(L, f"orc_matmul_{sfx}").argtypes = [P, P, P, ci, ci, ci, ci, ci]
         L.orc_create.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int]
         L.orc_create.restype = C.c_void_p
@@ -67,6 +67,7 @@ def lib() -> C.CDLL:
         L.orc_pool_stats_get.argtypes = [C.c_void_p, C.POINTER(PoolStats)]
         L.orc_live_trace.argtypes = [C.c_void_p, np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"), C.c_int]
         L.orc_set_workspace_cap.argtypes = [C.c_void_p, C.c_double]
+        L.orc_set_bf16_storage.argtypes = [C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -149,3 +150,7 @@ class Oracle:
 
     def set_workspace_cap(self, mb: float) -> None:
         lib().orc_set_workspace_cap(self._c, mb)
+
+    def set_bf16_storage(self, on: bool = True) -> None:
+        """Emulate the device's bf16 activation storage / bf16 weight operands."""
+        lib().orc_set_bf16_storage(self._c, int(on))

@@ -469,6 +469,35 @@ public:
     std::vector<i64> trace_;
     double ws_cap_mb_ = -1.0;
     int iter_ = 0, n0_ = 0;
+    bool bf16_ = false;  // emulate the device's bf16 activation storage and bf16 GEMM weight operands
+    std::unordered_map<int, bool> f32_var_;  // vars the device keeps in fp32 / as masks (not rounded)
+
+    static T round_bf16(T v) {
+        float f = static_cast<float>(v);
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+        u &= 0xffff0000u;
+        std::memcpy(&f, &u, 4);
+        return static_cast<T>(f);
+    }
+
+    // Device dtype rule (runtime.cu analyze_layouts): loss-head tensors fp32, masks u8, rest bf16.
+    void classify_vars() {
+        std::unordered_map<int, int> dt;  // 0 bf16, 1 f32, 2 mask
+        for (int i = 0; i < plan_->nstmts; ++i) {
+            const tc_stmt& s = plan_->stmts[i];
+            if (s.kind != TC_STMT_LET) continue;
+            int d = 0;
+            if (s.op == TC_OP_LOAD_Y || s.op == TC_OP_SOFTMAX_FWD || s.op == TC_OP_LOG || s.op == TC_OP_RECIP) d = 1;
+            if (s.op == TC_OP_DROPOUT_MASK) d = 2;
+            if (s.op == TC_OP_SCALE || s.op == TC_OP_MUL || s.op == TC_OP_ADD)
+                for (int k = 0; k < s.nin; ++k)
+                    if (s.in[k].kind == TC_REF_VAR && dt[s.in[k].index] == 1) d = 1;
+            dt[s.var] = d;
+            f32_var_[s.var] = d != 0;  // not rounded to bf16
+        }
+    }
 
     void init_params() {
         for (int i = 0; i < plan_->nparams; ++i) {
@@ -491,13 +520,16 @@ public:
         }
     }
 
+    std::vector<std::vector<T>> wq_;  // bf16-rounded GEMM weight operands (bf16 emulation)
+
     const T* get(const tc_ref& r, Dims* d = nullptr) {
         if (r.kind == TC_REF_PARAM) {
+            const tc_param_desc& pd = plan_->params[r.index];
             if (d) {
-                const tc_param_desc& pd = plan_->params[r.index];
                 d->rank = pd.rank;
                 for (int j = 0; j < pd.rank; ++j) d->d[j] = pd.dims[j];
             }
+            if (bf16_ && pd.rank >= 2) return wq_[r.index].data();
             return params_[r.index].data();
         }
         if (d) *d = vdims_.at(r.index);
@@ -707,6 +739,15 @@ public:
         pool_.held.clear();
         pool_.st.live_bytes = 0;
         trace_.clear();
+        if (bf16_) {
+            if (f32_var_.empty()) classify_vars();
+            wq_.assign(params_.size(), {});
+            for (size_t i = 0; i < params_.size(); ++i)
+                if (plan_->params[i].rank >= 2) {
+                    wq_[i] = params_[i];
+                    for (auto& v : wq_[i]) v = round_bf16(v);
+                }
+        }
         double loss = 0.0;
         std::vector<T> tmp;
         for (int i = 0; i < plan_->nstmts; ++i) {
@@ -717,6 +758,8 @@ public:
                     od.rank = s.rank;
                     for (int j = 0; j < s.rank; ++j) od.d[j] = s.dims[j];
                     eval(s, tmp, od);
+                    if (bf16_ && !f32_var_[s.var])
+                        for (auto& v : tmp) v = round_bf16(v);
                     if (!s.inplace) pool_.acquire(s.storage, od.count() * 4);
                     store_[s.storage] = tmp;  // in place: same storage, new contents
                     break;
@@ -975,6 +1018,10 @@ int orc_live_trace(orc_ctx* c, int64_t* out, int max) {
 
 void orc_set_workspace_cap(orc_ctx* c, double mb) {
     with(c, [&](auto& e) { e.ws_cap_mb_ = mb; return 0; });
+}
+
+void orc_set_bf16_storage(orc_ctx* c, int on) {
+    with(c, [&](auto& e) { e.bf16_ = on != 0; return 0; });
 }
 
 }  // extern "C"

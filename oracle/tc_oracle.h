@@ -88,6 +88,10 @@ ORC_API void orc_pool_stats_get(orc_ctx* c, orc_pool_stats* s);
 /* Per-statement live-bytes trace of the last step (dealloc mode), one entry per stmt. */
 ORC_API int orc_live_trace(orc_ctx* c, int64_t* out, int max);
 ORC_API void orc_set_workspace_cap(orc_ctx* c, double mb);
+/* Emulate the device's storage precision: round every bf16-stored activation
+ * to bf16 after each statement and use bf16-rounded weights as contraction
+ * operands.  Used to measure the rounding envelope of the step. */
+ORC_API void orc_set_bf16_storage(orc_ctx* c, int on);
 
 #ifdef __cplusplus
 }

@@ -178,7 +178,7 @@ def test_fd_batchnorm():
         return float((y * cw).sum())
 
     dx, dg, db = np.empty_like(x), np.empty_like(g), np.empty_like(b)
-    L.orc_bn_bwd_f64(cw, x, g, dx.ctypes.data, dg.ctypes.data, db.ctypes.data, N, C, HW, 1e-5)
+    L.orc_bn_bwd_f64(cw, x, g.ctypes.data, dx.ctypes.data, dg.ctypes.data, db.ctypes.data, N, C, HW, 1e-5)
     fd_check(f, x, dx)
     fd_check(f, g, dg)
     fd_check(f, b, db)
