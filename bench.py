@@ -142,7 +142,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_1701_02284_b200 import _native as nat
-    from paper_1701_02284_b200.network import compile_network
+    from paper_1701_02284_b200.parallel import compile_shard
     from paper_1701_02284_b200.runtime import Trainer, nccl_unique_id
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -158,7 +158,7 @@ def run_gpu(args):
         nid = None
 
     batch = args.batch or BATCH
-    net = compile_network(NET, batch)
+    net = compile_shard(NET, batch, world)  # loss / |world * batch|: summed gradients = global-batch gradient
     tr = Trainer(net, device=local, seed=SEED, use_graph=True, rank=rank, world=world, nccl_id=nid)
     tr.init_params()
     stream = torch.cuda.ExternalStream(tr.stream)

@@ -137,6 +137,7 @@ typedef struct tc_compile_opts {
     int mode;                           /* TC_MODE_* */
     double workspace_cap_mb;            /* < 0: unlimited */
     int greedy_schedule;
+    int64_t global_batch;               /* loss cardinality |N| (data parallel: G*B); 0 = batch */
 } tc_compile_opts;
 
 typedef struct tc_net tc_net;  /* a compiled network (plan producer output) */

@@ -148,7 +148,8 @@ FunPtr LayerFactory::seq(const std::vector<FunPtr>& fs) {
 SPtr LayerFactory::log_loss(const TPtr& softmax_out, double weight, const std::string& weight_name) {
     // (0 - (Y . Log S)) / |N|; Log gets the next SSA number.
     TPtr logs = t_prim(PrimOp::Log, Hyper{}, {softmax_out}, 2, net_.ctx.fresh_id());
-    SPtr l = s_div(s_add(s_const(0.0), s_neg(s_dot(net_.y_load, logs))), s_card(net_.batch));
+    SPtr l = s_div(s_add(s_const(0.0), s_neg(s_dot(net_.y_load, logs))),
+                   s_card(net_.loss_card > 0 ? net_.loss_card : net_.batch));
     if (!weight_name.empty()) l = s_mul(l, s_named(weight, weight_name));
     return l;
 }

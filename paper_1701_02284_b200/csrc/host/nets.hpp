@@ -32,6 +32,7 @@ struct ParamInit {
 struct NetworkDef {
     std::string name;
     std::int64_t batch = 0;
+    std::int64_t loss_card = 0;  // |N| of the log-loss; data parallel: global batch (0 = batch)
     Shape input_shape;       // (N, C, H, W)
     std::int64_t classes = 0;
     ExprContext ctx;

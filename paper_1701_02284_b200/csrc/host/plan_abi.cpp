@@ -202,6 +202,7 @@ tc_status tc_net_compile(const char* name, int64_t batch, const tc_compile_opts*
     *out = nullptr;
     try {
         auto h = std::make_unique<tc_net>();
+        if (opts && opts->global_batch > 0) h->net.loss_card = opts->global_batch;
         build_by_name(h->net, name, batch);
         CompileOptions co;
         if (opts) {
