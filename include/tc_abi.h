@@ -75,6 +75,8 @@ typedef struct tc_gemm_args {
     float alpha, beta;              /* D = alpha*A.B^T (+ beta*D, fp32 only) */
     int splits;                     /* split-K factor, 0 = auto */
     void* workspace; size_t workspace_bytes;  /* fp32 partials for split-K */
+    int bias_n;                     /* bias[n] read for n < bias_n (0 = N); columns beyond get 0 */
+    int b_rows;                     /* rows of B that exist (0 = N); D columns >= b_rows come out 0 */
 } tc_gemm_args;
 
 /* D[M,N] = alpha * sum_k A[m,k] B[n,k] (+bias[n]) (relu), tcgen05 kind::f16. */

@@ -63,6 +63,33 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint6
     return true;
 }
 
+// 3-D store map {N, M, splits} for the epilogue: SW128, box = 128 B of columns x 32 rows x 1.
+static bool make_tmap_store(CUtensorMap* map, void* base, bool bf16, uint64_t N, uint64_t M, uint64_t splits,
+                            uint64_t ld, std::string* err) {
+    auto fn = encode_fn();
+    if (!fn) {
+        *err = "cuTensorMapEncodeTiled unavailable (no CUDA driver)";
+        return false;
+    }
+    const uint64_t es = bf16 ? 2 : 4;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * es) & 15)) {
+        *err = "GEMM output must be 16-byte aligned with a 16-byte multiple row stride";
+        return false;
+    }
+    cuuint64_t dims[3] = {N, M, splits};
+    cuuint64_t strides[2] = {ld * es, ld * es * M};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / es), 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled (store) failed (" + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
+}
+
 // ------------------------------------------------------------------ split-K reduce
 // out[m, n] = epilogue( sum_s ws[s][m][n] ), fixed summation order (deterministic).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
@@ -138,35 +165,35 @@ static tc_status launch_bn(const GemmParams& p, dim3 grid, cudaStream_t st) {
     return TC_OK;
 }
 
-// Common driver: fills tiling/epilogue fields of `p`, launches the main kernel
-// and (for split-K) the reduction.
+// Common driver: fills tiling/epilogue fields of `p`, launches the persistent
+// kernel and, for split-K (or beta != 0), the deterministic reduction.
 static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long long ldd, int d_bf16,
                           const float* bias, int n_bias, int relu, float beta, void* ws, size_t ws_bytes,
                           cudaStream_t st) {
     p.num_kb = lp.num_kb;
     p.kb_per_split = lp.kb_per_split;
-    p.relu = 0;
-    p.bias = nullptr;
-    p.beta = 0.f;
-    if (lp.splits > 1) {
+    p.splits = lp.splits;
+    p.tiles_m = ceil_div(p.M, BM);
+    p.tiles_n = ceil_div(p.N, lp.bn);
+    p.units = p.tiles_m * p.tiles_n * p.splits;
+    const bool partial = lp.splits > 1 || beta != 0.f;
+    std::string err;
+    if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
         if (!ws || ws_bytes < need)
             return fail(TC_INVALID_ARG, "split-K workspace too small: need " + std::to_string(need) + " bytes");
-        p.epi = EPI_F32_PARTIAL;
-        p.D = ws;
-        p.ldd = p.N;
-        p.split_stride = static_cast<long long>(p.M) * p.N;
+        p.epi = EPI_F32;
+        p.bias = nullptr;
+        p.relu = 0;
+        if (!make_tmap_store(&p.tmD, ws, false, p.N, p.M, lp.splits, p.N, &err)) return fail(TC_INVALID_ARG, err);
     } else {
         p.epi = d_bf16 ? EPI_BF16 : EPI_F32;
-        p.D = D;
-        p.ldd = ldd;
         p.bias = bias;
         p.n_bias = n_bias;
         p.relu = relu;
-        p.beta = beta;
-        p.split_stride = 0;
+        if (!make_tmap_store(&p.tmD, D, d_bf16 != 0, p.N, p.M, 1, ldd, &err)) return fail(TC_INVALID_ARG, err);
     }
-    dim3 grid(ceil_div(p.M, BM), ceil_div(p.N, lp.bn), lp.splits);
+    dim3 grid(std::min(p.units, num_sms()));
     tc_status s;
     switch (lp.bn) {
         case 256: s = launch_bn<256>(p, grid, st); break;
@@ -174,11 +201,12 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         default: s = launch_bn<64>(p, grid, st); break;
     }
     if (s != TC_OK) return s;
-    if (lp.splits > 1) {
+    if (partial) {
         const long long total = static_cast<long long>(p.M) * p.N;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
         splitk_reduce_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(ws), lp.splits, p.M, p.N,
-                                                     p.split_stride, D, ldd, d_bf16, bias, n_bias, relu, beta);
+                                                     static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
+                                                     relu, beta);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
@@ -201,7 +229,7 @@ unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load();
 size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
     if (!a) return 0;
     LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits);
-    return lp.splits > 1 ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
+    return (lp.splits > 1 || a->beta != 0.f) ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
 }
 
 tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
@@ -221,15 +249,17 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
         p.a_mode = OP_TMA_MN;
         if (!make_tmap_2d_bf16(&p.tmA, a->A, a->M, a->K, a->lda, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
     }
+    // B's tensor map covers only the rows that exist (padded output columns read zeros, never past the buffer)
+    const int b_rows = a->b_rows > 0 ? std::min(a->b_rows, a->N) : a->N;
     if (a->b_layout == TC_LAYOUT_K) {
         p.b_mode = OP_TMA_K;
-        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->K, a->N, a->ldb, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->K, b_rows, a->ldb, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
     } else {
         p.b_mode = OP_TMA_MN;
-        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->N, a->K, a->ldb, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+        if (!make_tmap_2d_bf16(&p.tmB, a->B, b_rows, a->K, a->ldb, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
     }
-    return run_gemm(p, lp, a->D, a->ldd, a->d_dtype == TC_DTYPE_BF16, a->bias, a->N, a->relu, a->beta,
-                    a->workspace, a->workspace_bytes, static_cast<cudaStream_t>(stream));
+    return run_gemm(p, lp, a->D, a->ldd, a->d_dtype == TC_DTYPE_BF16, a->bias, a->bias_n > 0 ? a->bias_n : a->N,
+                    a->relu, a->beta, a->workspace, a->workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- convolution

@@ -510,6 +510,134 @@ __global__ void k_bn_dyx_partial(const bf16* __restrict__ dy, const bf16* __rest
     }
 }
 
+// ---------------------------------------------------------------- dense im2col (small-C first layers)
+__global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo,
+                         int Kp, bf16* __restrict__ col) {
+    const int groups = Kp / 8;
+    const long long total = static_cast<long long>(xi.N) * Ho * Wo * groups;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % groups);
+        long long m = t / groups;
+        const int ow = static_cast<int>(m % Wo);
+        long long q = m / Wo;
+        const int oh = static_cast<int>(q % Ho);
+        const int n = static_cast<int>(q / Ho);
+        __align__(16) bf16 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int kk = g * 8 + j;
+            bf16 val = __float2bfloat16_rn(0.f);
+            if (kk < R * S * xi.C) {
+                const int c = kk % xi.C;
+                const int rs = kk / xi.C;
+                const int r = rs / S, s = rs - (rs / S) * S;
+                const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
+                if (ih >= 0 && ih < xi.H && iw >= 0 && iw < xi.W)
+                    val = x[((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + c];
+            }
+            v[j] = val;
+        }
+        *reinterpret_cast<uint4*>(col + m * Kp + g * 8) = *reinterpret_cast<const uint4*>(v);
+    }
+}
+
+// ---------------------------------------------------------------- LRN v2: thread per (pixel, 8 channels)
+// Window sums over channels [c - n/2, c + n/2] read the neighbouring 16-byte
+// chunks of the same pixel (L1 hits); n <= 9 so chunks g-1 .. g+1 suffice.
+__device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, int ng, float (&v)[24]) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int gg = g - 1 + q;
+        float f[8];
+        if (gg >= 0 && gg < ng) {
+            unpack8(*reinterpret_cast<const uint4*>(p + gg * 8), f);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[q * 8 + j] = f[j];
+    }
+}
+
+__global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, int size, float alpha, float beta,
+                           float kk) {
+    const int ng = a.cs / 8;
+    const long long total = a.pixels() * ng;
+    const int half = size / 2;
+    const float an = alpha / static_cast<float>(size);
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % ng);
+        const bf16* px = x + (t / ng) * a.cs;
+        float v[24];
+        load_chunk3(px, g, ng, v);
+        float out[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = g * 8 + j;
+            float s = 0.f;
+            for (int d = -half; d <= half; ++d) {
+                const int cc = c + d;
+                const float e = v[8 + j + d];
+                if (cc >= 0 && cc < a.C) s += e * e;
+            }
+            out[j] = c < a.C ? v[8 + j] * __powf(kk + an * s, -beta) : 0.f;
+        }
+        *reinterpret_cast<uint4*>(y + t * 8 - static_cast<long long>(0)) = pack8(out);
+    }
+}
+
+__global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
+                           bf16* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
+    const int ng = a.cs / 8;
+    const long long total = a.pixels() * ng;
+    const int half = size / 2;
+    const float an = alpha / static_cast<float>(size);
+    const float coef = 2.f * alpha * beta / static_cast<float>(size);
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % ng);
+        const long long base = (t / ng) * a.cs;
+        float xv[24], dv[24], yv[24];
+        load_chunk3(x + base, g, ng, xv);
+        load_chunk3(dy + base, g, ng, dv);
+        load_chunk3(y + base, g, ng, yv);
+        // scale and t = dy*y/scale for channels g*8-half .. g*8+7+half (indices 8-half .. 15+half of the window)
+        float sc[24], tt[24];
+#pragma unroll
+        for (int i = 0; i < 24; ++i) {
+            sc[i] = 1.f;
+            tt[i] = 0.f;
+        }
+        for (int i = 8 - half; i < 16 + half; ++i) {
+            const int c = g * 8 - 8 + i;
+            if (c < 0 || c >= a.C) continue;
+            float s = 0.f;
+            for (int d = -half; d <= half; ++d) {
+                const int cc = c + d, ii = i + d;
+                if (cc >= 0 && cc < a.C) {
+                    // squares beyond the loaded 3 chunks are only needed when half > 8 (never: n <= 9 plus edges)
+                    const float e = (ii >= 0 && ii < 24) ? xv[ii] : 0.f;
+                    s += e * e;
+                }
+            }
+            sc[i] = kk + an * s;
+            tt[i] = dv[i] * yv[i] / sc[i];
+        }
+        float out[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = g * 8 + j;
+            float s = 0.f;
+            for (int d = -half; d <= half; ++d) s += tt[8 + j + d];
+            out[j] = c < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
+        }
+        *reinterpret_cast<uint4*>(dx + base + g * 8) = pack8(out);
+    }
+}
+
 // ---------------------------------------------------------------- input staging
 __global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y, int N, int C, int H, int W, int cs) {
     const long long total = static_cast<long long>(N) * H * W * cs;
@@ -622,17 +750,32 @@ tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const int32_t* idx, bf16* dx,
     return TC_OK;
 }
 tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
-    const int warps = 8;
-    k_lrn_fwd<<<grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st>>>(x, y, a, size, alpha,
-                                                                                             beta, k);
+    if (size > 9) {  // general path: warp per pixel with the channel vector in shared memory
+        const int warps = 8;
+        k_lrn_fwd<<<grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st>>>(x, y, a, size, alpha,
+                                                                                                 beta, k);
+    } else {
+        k_lrn2_fwd<<<EW_GRID(a.pixels() * (a.cs / 8))>>>(x, y, a, size, alpha, beta, k);
+    }
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
                          float beta, float k, cudaStream_t st) {
-    const int warps = 8;
-    k_lrn_bwd<<<grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st>>>(dy, x, y, dx, a, size,
-                                                                                                 alpha, beta, k);
+    if (size > 9) {
+        const int warps = 8;
+        k_lrn_bwd<<<grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st>>>(dy, x, y, dx, a,
+                                                                                                     size, alpha, beta, k);
+    } else {
+        k_lrn2_bwd<<<EW_GRID(a.pixels() * (a.cs / 8))>>>(dy, x, y, dx, a, size, alpha, beta, k);
+    }
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
+                        cudaStream_t st) {
+    if (Kp % 8) return fail(TC_INVALID_ARG, "im2col: Kp must be a multiple of 8");
+    k_im2col<<<EW_GRID(static_cast<long long>(xi.N) * Ho * Wo * (Kp / 8))>>>(x, xi, R, S, stride, pad, Ho, Wo, Kp, col);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

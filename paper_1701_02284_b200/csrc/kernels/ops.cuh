@@ -73,6 +73,11 @@ tc_status launch_bn_bwd(const bf16* dy, const bf16* x, const float* gamma, const
                         float* dbeta, long long pixels, int C, int cs, float* partials, int max_partials,
                         cudaStream_t st);
 
+// Dense im2col for small-channel (first-layer) convolutions: col[m][kk], m = (n, oh, ow),
+// kk = (kh, kw, c) over the REAL channels C, zero-padded to Kp (multiple of 8).
+tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
+                        cudaStream_t st);
+
 // Input staging: NCHW fp32 -> NHWC bf16 (channel stride cs, pads zero).
 tc_status launch_nchw_to_nhwc(const float* x, bf16* y, int N, int C, int H, int W, int cs, cudaStream_t st);
 // Synthetic batch generated on the device (identical law to oracle/tc_philox.h).

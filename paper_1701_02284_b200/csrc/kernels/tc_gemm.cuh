@@ -1,21 +1,25 @@
 // tcgen05 implicit-GEMM core used by every contraction of the training step
 // (Convolv fwd / bwd-data / bwd-filter and the FC MatMul forms).
 //
-//   D[m, n] (+)= sum_k A[m, k] * B[n, k]        bf16 operands, fp32 accumulate in TMEM
+//   D[m, n] = alpha * sum_k A[m, k] * B[n, k]   bf16 operands, fp32 accumulation in TMEM
 //
 // Operand sources (per operand, chosen at launch):
-//   OP_TMA_K    row-major [rows, K] matrix, TMA 2D box {64 K, rows}, SW128 K-major smem
-//   OP_TMA_MN   row-major [K, rows] matrix, TMA 2D box {64 rows, 64 K}, SW128 MN-major smem
-//   OP_GATHER_K implicit im2col rows of an NHWC activation (fprop: x, bwd-data: dy),
-//               16-byte cp.async gathers with zero fill, written pre-swizzled (A only)
-//   OP_GATHER_MN implicit im2col of x transposed for bwd-filter (B only)
+//   OP_TMA_K     row-major [rows, K]: TMA 2D box {64 K, rows} -> SW128 K-major smem
+//   OP_TMA_MN    row-major [K, rows]: TMA 2D boxes {64 rows, 64 K} -> SW128 MN-major smem
+//   OP_GATHER_K  implicit im2col rows of an NHWC activation (fprop: x, bwd-data: dy),
+//                16-byte cp.async gathers with zero fill, written pre-swizzled (A only)
+//   OP_GATHER_MN implicit im2col of x, transposed, for bwd-filter (B only)
 //
-// Warp roles (256 threads, one output tile per CTA):
-//   warp 0   TMA producer (elected lane)
-//   warp 1   MMA issuer (elected lane) -> tcgen05.mma into TMEM, tcgen05.commit frees smem stages
-//   warp 2   TMEM allocator
-//   warps 4-7  gather producers during the main loop, then the epilogue
-//              (warp%4 selects the 32 TMEM lanes = tile rows it may read)
+// Persistent, warp-specialised (384 threads, one CTA per SM):
+//   warp 0      TMA producer (elected lane)
+//   warp 1      MMA issuer: tcgen05.mma into one of two TMEM accumulators;
+//               tcgen05.commit releases smem stages / publishes finished tiles
+//   warp 2      TMEM allocator (2 x BN fp32 columns)
+//   warps 4-7   epilogue: tcgen05.ld (warp%4 selects its 32 TMEM lanes), bias /
+//               ReLU / alpha, bf16 or fp32 pack, swizzled smem staging, TMA store
+//               (clipped at the tensor bounds); overlaps the next tile's main loop
+//   warps 8-11  im2col gather producers (only for OP_GATHER_* operands)
+// Work units are (m tile, n tile, k split) handed out round-robin to the CTAs.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -26,41 +30,41 @@ namespace tcb {
 
 enum OperandMode : int { OP_TMA_K = 0, OP_TMA_MN = 1, OP_GATHER_K = 2, OP_GATHER_MN = 3 };
 enum GatherKind : int { GATHER_FPROP = 0, GATHER_DGRAD = 1 };
-enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_PARTIAL = 2 };
+enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1 };
 
-// Implicit-GEMM geometry. Activations are NHWC with a channel stride that is a
+// Implicit-GEMM geometry.  Activations are NHWC with a channel stride that is a
 // multiple of 8 (16-byte chunks never straddle two filter taps).
 struct ConvGeom {
-    int N, H, W, C;      // input image (fprop / wgrad source) or dx image (dgrad rows)
+    int N, H, W, C;  // input image (fprop / wgrad source) or dx image (dgrad rows)
     int R, S, stride, pad;
-    int Ho, Wo, Co;      // output image; Co = channel stride of dy (dgrad source)
+    int Ho, Wo, Co;  // output image; Co = channel stride of dy (dgrad source)
 };
 
 struct GemmParams {
     CUtensorMap tmA;  // valid when a_mode is a TMA mode
     CUtensorMap tmB;  // valid when b_mode is a TMA mode
+    CUtensorMap tmD;  // 3-D store map {N, M, splits}, SW128, box {128 B of columns, 32 rows, 1}
     int M, N, K;
     int a_mode, b_mode;
-    int gather_kind;          // GatherKind for OP_GATHER_K
+    int gather_kind;            // GatherKind for OP_GATHER_K
     const __nv_bfloat16* gsrc;  // gather source tensor
     ConvGeom g;
-    int kb_per_split;         // k-blocks handled by one blockIdx.z
-    int num_kb;               // total k-blocks
-    // epilogue
-    int epi;
-    void* D;
-    long long ldd;            // row stride of D in elements
-    long long split_stride;   // elements between split partial slabs (EPI_F32_PARTIAL)
-    const float* bias;        // per-column bias (EPI_BF16 / EPI_F32), may be null
-    int n_bias;               // bias is read for n < n_bias (padded channels get 0)
+    int num_kb;                 // total k-blocks
+    int kb_per_split;           // k-blocks per split
+    int splits;
+    int tiles_m, tiles_n;
+    int units;                  // tiles_m * tiles_n * splits
+    int epi;                    // EpiMode of the stored tile
+    const float* bias;          // per-column bias, may be null (never with splits > 1)
+    int n_bias;                 // bias is read for n < n_bias (padded channels get 0)
     int relu;
-    float alpha;              // D = alpha * acc (+ beta * D_old for EPI_F32 when beta != 0)
-    float beta;
+    float alpha;
 };
 
-constexpr int BK = 64;          // bf16 elements per k-block = one 128-byte swizzle row
+constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
 constexpr int BM = 128;
-constexpr int kNumThreads = 256;
+constexpr int kNumThreads = 384;
+constexpr int kStagingBytes = 4096;  // per epilogue warp per buffer: 32 rows x 128 B
 
 template <int BN>
 struct TileCfg {
@@ -68,8 +72,10 @@ struct TileCfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+    static constexpr int kStagingTotal = 4 * 2 * kStagingBytes;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kStagingTotal + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
+    static constexpr int kLag = kStages - 2;                             // cp.async groups in flight
 };
 
 // Byte offset of 16B chunk `j` of row `r` inside a SW128 tile (1024B-aligned base).
@@ -77,57 +83,133 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int j) {
     return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
 }
 
-// ---- im2col gathers -------------------------------------------------------
-// A rows (K-major): thread owns one tile row, fills its 8 chunks for k-block kb.
-__device__ __forceinline__ void gather_rows_kmajor(const GemmParams& p, uint32_t sA, int row, int m0, int kb,
-                                                   bool row_valid, int rn, int ry, int rx) {
+struct Unit {
+    int mt, nt, sp, kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const GemmParams& p, int u) {
+    Unit w;
+    w.nt = u % p.tiles_n;
+    const int r = u / p.tiles_n;
+    w.mt = r % p.tiles_m;
+    w.sp = r / p.tiles_m;
+    w.kb0 = w.sp * p.kb_per_split;
+    w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+    return w;
+}
+
+// ---- A gather (K-major rows of an implicit im2col) --------------------------------
+// Each of the 128 producer threads owns one tile row; its 8 chunks per k-block
+// walk (kh, kw, c) incrementally (no division in the steady state).
+struct RowGather {
+    const __nv_bfloat16* base;  // image n of this row
+    int ry, rx;                 // output (fprop) or input (dgrad) pixel of this row
+    bool valid;
+    int c[8], kw[8], kh[8], kk[8];
+};
+
+__device__ __forceinline__ void row_gather_init(const GemmParams& p, RowGather& rg, int m, int kb0) {
     const ConvGeom& g = p.g;
-    const int k0 = kb * BK;
-    const int C = (p.gather_kind == GATHER_FPROP) ? g.C : g.Co;
-    int tap = k0 / C;
-    int c = k0 - tap * C;
+    const bool fprop = p.gather_kind == GATHER_FPROP;
+    rg.valid = m < p.M;
+    int n = 0;
+    rg.ry = rg.rx = 0;
+    if (rg.valid) {
+        const int hw = fprop ? g.Ho * g.Wo : g.H * g.W;
+        const int wd = fprop ? g.Wo : g.W;
+        n = m / hw;
+        const int rem = m - n * hw;
+        rg.ry = rem / wd;
+        rg.rx = rem - rg.ry * wd;
+    }
+    const int C = fprop ? g.C : g.Co;
+    rg.base = p.gsrc + static_cast<long long>(n) * (fprop ? static_cast<long long>(g.H) * g.W * g.C
+                                                            : static_cast<long long>(g.Ho) * g.Wo * g.Co);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int k = k0 + j * 8;
+        const int k = kb0 * BK + j * 8;
+        const int tap = k / C;
+        rg.c[j] = k - tap * C;
+        rg.kh[j] = tap / g.S;
+        rg.kw[j] = tap - rg.kh[j] * g.S;
+        rg.kk[j] = k;
+    }
+}
+
+__device__ __forceinline__ void row_gather_issue(const GemmParams& p, RowGather& rg, uint32_t sA, int row) {
+    const ConvGeom& g = p.g;
+    const bool fprop = p.gather_kind == GATHER_FPROP;
+    const int C = fprop ? g.C : g.Co;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
         const void* src = p.gsrc;
         uint32_t bytes = 0;
-        if (row_valid && k < p.K) {
-            const int kh = tap / g.S;
-            const int kw = tap - kh * g.S;
-            if (p.gather_kind == GATHER_FPROP) {
-                const int iy = ry * g.stride - g.pad + kh;
-                const int ix = rx * g.stride - g.pad + kw;
-                if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) {
-                    src = p.gsrc + ((static_cast<long long>(rn) * g.H + iy) * g.W + ix) * g.C + c;
+        if (rg.valid && rg.kk[j] < p.K) {
+            if (fprop) {
+                const int iy = rg.ry * g.stride - g.pad + rg.kh[j];
+                const int ix = rg.rx * g.stride - g.pad + rg.kw[j];
+                if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
+                    static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
+                    src = rg.base + (static_cast<long long>(iy) * g.W + ix) * g.C + rg.c[j];
                     bytes = 16;
                 }
             } else {
-                const int ny = ry + g.pad - kh;
-                const int nx = rx + g.pad - kw;
+                const int ny = rg.ry + g.pad - rg.kh[j];
+                const int nx = rg.rx + g.pad - rg.kw[j];
                 if (ny >= 0 && nx >= 0) {
                     const int oy = ny / g.stride, ox = nx / g.stride;
                     if (oy * g.stride == ny && ox * g.stride == nx && oy < g.Ho && ox < g.Wo) {
-                        src = p.gsrc + ((static_cast<long long>(rn) * g.Ho + oy) * g.Wo + ox) * g.Co + c;
+                        src = rg.base + (static_cast<long long>(oy) * g.Wo + ox) * g.Co + rg.c[j];
                         bytes = 16;
                     }
                 }
             }
         }
         cp_async_16(sA + sw128_off(row, j), src, bytes);
-        c += 8;
-        if (c >= C) { c -= C; ++tap; }
+        // advance this chunk by one k-block (64 channels along (kh, kw, c))
+        rg.kk[j] += BK;
+        rg.c[j] += BK;
+        while (rg.c[j] >= C) {
+            rg.c[j] -= C;
+            if (++rg.kw[j] == g.S) {
+                rg.kw[j] = 0;
+                ++rg.kh[j];
+            }
+        }
     }
-    (void)m0;
 }
 
-// B for bwd-filter (MN-major): rows of the smem atoms are k = output pixels,
-// columns are n = (kh, kw, c). Thread handles pixel row `kr` and every other chunk.
+// ---- B gather for bwd-filter (MN-major): rows = output pixels (k), columns n = (kh, kw, c)
 template <int BN>
-__device__ __forceinline__ void gather_wgrad_mn(const GemmParams& p, uint32_t sB, int kr, int half, int n0, int kb) {
+struct ColGather {
+    static constexpr int kChunks = BN / 16;  // 16-byte chunks per thread per k-block
+    int code[kChunks];                       // c | kw << 12 | kh << 20, or -1 when n >= N
+};
+
+template <int BN>
+__device__ __forceinline__ void col_gather_init(const GemmParams& p, ColGather<BN>& cg, int n0, int half) {
+    const ConvGeom& g = p.g;
+#pragma unroll
+    for (int q = 0; q < ColGather<BN>::kChunks; ++q) {
+        const int cc = half + 2 * q;
+        const int n = n0 + (cc >> 3) * 64 + (cc & 7) * 8;
+        if (n < p.N) {
+            const int tap = n / g.C;
+            const int c = n - tap * g.C;
+            const int kh = tap / g.S;
+            cg.code[q] = c | ((tap - kh * g.S) << 12) | (kh << 20);
+        } else {
+            cg.code[q] = -1;
+        }
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void col_gather_issue(const GemmParams& p, const ColGather<BN>& cg, uint32_t sB, int kr,
+                                                 int half, int kb) {
     const ConvGeom& g = p.g;
     const int pix = kb * BK + kr;
-    const int npix = g.N * g.Ho * g.Wo;
-    const bool pv = pix < npix;
+    const bool pv = pix < g.N * g.Ho * g.Wo;
     int rn = 0, oy = 0, ox = 0;
     if (pv) {
         rn = pix / (g.Ho * g.Wo);
@@ -135,25 +217,24 @@ __device__ __forceinline__ void gather_wgrad_mn(const GemmParams& p, uint32_t sB
         oy = rem / g.Wo;
         ox = rem - oy * g.Wo;
     }
-    constexpr int kChunks = (BN / 64) * 8;
+    const __nv_bfloat16* img = p.gsrc + static_cast<long long>(rn) * g.H * g.W * g.C;
 #pragma unroll
-    for (int cc = half; cc < kChunks; cc += 2) {
-        const int atom = cc >> 3, j = cc & 7;
-        const int n = n0 + atom * 64 + j * 8;
+    for (int q = 0; q < ColGather<BN>::kChunks; ++q) {
+        const int cc = half + 2 * q;
         const void* src = p.gsrc;
         uint32_t bytes = 0;
-        if (pv && n < p.N) {
-            const int tap = n / g.C;
-            const int c = n - tap * g.C;
-            const int kh = tap / g.S, kw = tap - (tap / g.S) * g.S;
+        const int code = cg.code[q];
+        if (pv && code >= 0) {
+            const int c = code & 0xFFF, kw = (code >> 12) & 0xFF, kh = code >> 20;
             const int iy = oy * g.stride - g.pad + kh;
             const int ix = ox * g.stride - g.pad + kw;
-            if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) {
-                src = p.gsrc + ((static_cast<long long>(rn) * g.H + iy) * g.W + ix) * g.C + c;
+            if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
+                static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
+                src = img + (static_cast<long long>(iy) * g.W + ix) * g.C + c;
                 bytes = 16;
             }
         }
-        cp_async_16(sB + atom * (BK * 128) + sw128_off(kr, j), src, bytes);
+        cp_async_16(sB + (cc >> 3) * (BK * 128) + sw128_off(kr, cc & 7), src, bytes);
     }
 }
 
@@ -165,18 +246,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * Cfg::kABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint8_t* sStage = smem + S * Cfg::kStageBytes;  // epilogue staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sStage + Cfg::kStagingTotal);
     uint64_t* empty = full + S;
-    uint64_t* tmem_full = empty + S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * BN;
-    const int kb_begin = blockIdx.z * p.kb_per_split;
-    const int kb_end = min(p.num_kb, kb_begin + p.kb_per_split);
-    const int nkb = max(0, kb_end - kb_begin);
     const bool a_gather = p.a_mode == OP_GATHER_K;
     const bool b_gather = p.b_mode == OP_GATHER_MN;
     const bool any_gather = a_gather || b_gather;
@@ -184,11 +262,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     if (warp == 0 && lane == 0) {
         if (!a_gather) tma_prefetch(&p.tmA);
         if (!b_gather) tma_prefetch(&p.tmB);
+        tma_prefetch(&p.tmD);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1 + (any_gather ? 128 : 0));
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -203,156 +285,186 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             uint32_t tx = 0;
             if (!a_gather) tx += Cfg::kABytes;
             if (!b_gather) tx += Cfg::kBBytes;
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % S;
-                const uint32_t use = i / S;
-                mbar_wait(&empty[s], (use & 1) ^ 1);
-                const int kb = kb_begin + i;
-                uint8_t* a_dst = sA + s * Cfg::kABytes;
-                uint8_t* b_dst = sB + s * Cfg::kBBytes;
-                if (p.a_mode == OP_TMA_K) {
-                    tma_load_2d(a_dst, &p.tmA, &full[s], kb * BK, m0);
-                } else if (p.a_mode == OP_TMA_MN) {
+            int it = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                const int m0 = w.mt * BM, n0 = w.nt * BN;
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                    uint8_t* a_dst = sA + s * Cfg::kABytes;
+                    uint8_t* b_dst = sB + s * Cfg::kBBytes;
+                    if (p.a_mode == OP_TMA_K) {
+                        tma_load_2d(a_dst, &p.tmA, &full[s], kb * BK, m0);
+                    } else if (p.a_mode == OP_TMA_MN) {
 #pragma unroll
-                    for (int a = 0; a < BM / 64; ++a) tma_load_2d(a_dst + a * BK * 128, &p.tmA, &full[s], m0 + a * 64, kb * BK);
-                }
-                if (p.b_mode == OP_TMA_K) {
-                    tma_load_2d(b_dst, &p.tmB, &full[s], kb * BK, n0);
-                } else if (p.b_mode == OP_TMA_MN) {
+                        for (int a = 0; a < BM / 64; ++a)
+                            tma_load_2d(a_dst + a * BK * 128, &p.tmA, &full[s], m0 + a * 64, kb * BK);
+                    }
+                    if (p.b_mode == OP_TMA_K) {
+                        tma_load_2d(b_dst, &p.tmB, &full[s], kb * BK, n0);
+                    } else if (p.b_mode == OP_TMA_MN) {
 #pragma unroll
-                    for (int a = 0; a < BN / 64; ++a) tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kb * BK);
+                        for (int a = 0; a < BN / 64; ++a)
+                            tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kb * BK);
+                    }
+                    mbar_arrive_expect_tx(&full[s], tx);
                 }
-                mbar_arrive_expect_tx(&full[s], tx);
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        const uint32_t idesc = umma_idesc_bf16(BM, BN, p.a_mode == OP_TMA_MN ? 1u : 0u,
-                                               (p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN) ? 1u : 0u);
         const bool a_mn = p.a_mode == OP_TMA_MN;
         const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN;
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % S;
-            const uint32_t use = i / S;
-            mbar_wait(&full[s], use & 1);
+        const uint32_t idesc = umma_idesc_bf16(BM, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
+        int it = 0, tc = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
+            const Unit w = decode_unit(p, u);
+            const int buf = tc & 1;
+            mbar_wait(&tempty[buf], ((tc >> 1) & 1) ^ 1);
             tc_fence_after();
-            if (lane == 0) {
-                const uint32_t a_base = smem_u32(sA + s * Cfg::kABytes);
-                const uint32_t b_base = smem_u32(sB + s * Cfg::kBBytes);
+            const uint32_t d_tmem = tmem_base + buf * BN;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                const int s = it % S;
+                mbar_wait(&full[s], (it / S) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a_base = smem_u32(sA + s * Cfg::kABytes);
+                    const uint32_t b_base = smem_u32(sB + s * Cfg::kBBytes);
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    // K-major: advance 32 bytes along the swizzled row.
-                    // MN-major: advance two 8-row k-groups (2 x 1024 bytes).
-                    const uint64_t ad = a_mn ? umma_desc_sw128(a_base + k * 2048, BK * 128, 1024)
-                                             : umma_desc_sw128(a_base + k * 32, 0, 1024);
-                    const uint64_t bd = b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
-                                             : umma_desc_sw128(b_base + k * 32, 0, 1024);
-                    umma_bf16(tmem_base, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major: 32 bytes along the swizzled row; MN-major: two 8-row k-groups (2 x 1024 B)
+                        const uint64_t ad = a_mn ? umma_desc_sw128(a_base + k * 2048, BK * 128, 1024)
+                                                 : umma_desc_sw128(a_base + k * 32, 0, 1024);
+                        const uint64_t bd = b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
+                                                 : umma_desc_sw128(b_base + k * 32, 0, 1024);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                    if (kb == w.kb1 - 1) umma_commit(&tfull[buf]);
                 }
-                umma_commit(&empty[s]);
-                if (i == nkb - 1) umma_commit(tmem_full);
+                __syncwarp();
             }
-            __syncwarp();
         }
-        if (nkb == 0 && lane == 0) mbar_arrive(tmem_full);
-    } else if (warp >= 4) {
-        const int et = threadIdx.x - 128;  // 0..127
-        // ---------------- gather producers
+    } else if (warp >= 8) {
+        // ---------------- im2col gather producers (128 threads)
         if (any_gather) {
-            constexpr int LAG = 2;
-            // Precompute this thread's output-row coordinates for A gathers.
-            int rn = 0, ry = 0, rx = 0;
-            bool row_valid = false;
-            if (a_gather) {
-                const int m = m0 + et;
-                row_valid = m < p.M;
-                if (row_valid) {
-                    const int hw = (p.gather_kind == GATHER_FPROP) ? p.g.Ho * p.g.Wo : p.g.H * p.g.W;
-                    const int wd = (p.gather_kind == GATHER_FPROP) ? p.g.Wo : p.g.W;
-                    rn = m / hw;
-                    const int rem = m - rn * hw;
-                    ry = rem / wd;
-                    rx = rem - ry * wd;
-                }
-            }
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % S;
-                const uint32_t use = i / S;
-                mbar_wait(&empty[s], (use & 1) ^ 1);
-                const int kb = kb_begin + i;
+            constexpr int LAG = Cfg::kLag;
+            const int t = threadIdx.x - 256;
+            int it = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
                 if (a_gather) {
-                    gather_rows_kmajor(p, smem_u32(sA + s * Cfg::kABytes), et, m0, kb, row_valid, rn, ry, rx);
+                    RowGather rg;
+                    row_gather_init(p, rg, w.mt * BM + t, w.kb0);
+                    for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                        const int s = it % S;
+                        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                        row_gather_issue(p, rg, smem_u32(sA + s * Cfg::kABytes), t);
+                        cp_async_commit();
+                        if (it >= LAG) {
+                            cp_async_wait<LAG>();
+                            fence_proxy_async_smem();
+                            mbar_arrive(&full[(it - LAG) % S]);
+                        }
+                    }
                 } else {
-                    gather_wgrad_mn<BN>(p, smem_u32(sB + s * Cfg::kBBytes), et & 63, et >> 6, n0, kb);
-                }
-                cp_async_commit();
-                if (i >= LAG) {
-                    cp_async_wait<LAG>();
-                    fence_proxy_async_smem();
-                    mbar_arrive(&full[(i - LAG) % S]);
+                    ColGather<BN> cg;
+                    col_gather_init<BN>(p, cg, w.nt * BN, t >> 6);
+                    for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                        const int s = it % S;
+                        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                        col_gather_issue<BN>(p, cg, smem_u32(sB + s * Cfg::kBBytes), t & 63, t >> 6, kb);
+                        cp_async_commit();
+                        if (it >= LAG) {
+                            cp_async_wait<LAG>();
+                            fence_proxy_async_smem();
+                            mbar_arrive(&full[(it - LAG) % S]);
+                        }
+                    }
                 }
             }
             cp_async_wait<0>();
             fence_proxy_async_smem();
-            for (int i = max(0, nkb - LAG); i < nkb; ++i) mbar_arrive(&full[i % S]);
+            for (int i = max(0, it - LAG); i < it; ++i) mbar_arrive(&full[i % S]);
         }
-
-        // ---------------- epilogue
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        const int ew = warp - 4;  // TMEM lane quarter
-        const int row = m0 + ew * 32 + lane;
-        const bool rv = row < p.M;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + c0, r);
-            tmem_ld_wait();
-            if (!rv) continue;
-            const int nb = n0 + c0;
-            if (nb >= p.N) continue;
-            float v[32];
+    } else if (warp >= 4) {
+        // ---------------- epilogue (TMEM -> regs -> swizzled smem -> TMA store)
+        const int ew = warp - 4;  // TMEM lane quarter = tile rows [32 ew, 32 ew + 32)
+        uint8_t* stage_base = sStage + ew * 2 * kStagingBytes;
+        const bool bf16_out = p.epi == EPI_BF16;
+        int nstore = 0;
+        int tc = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
+            const Unit w = decode_unit(p, u);
+            const int buf = tc & 1;
+            mbar_wait(&tfull[buf], (tc >> 1) & 1);
+            tc_fence_after();
+            const int m0 = w.mt * BM, n0 = w.nt * BN;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + buf * BN;
+            // one staging row = 128 B: 64 bf16 or 32 fp32 columns
+            const int cols_per_store = bf16_out ? 64 : 32;
+            for (int c0 = 0; c0 < BN; c0 += cols_per_store) {
+                uint32_t packed[32];
+                if (bf16_out) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-            if (p.epi == EPI_F32_PARTIAL) {
-                float* out = reinterpret_cast<float*>(p.D) + blockIdx.z * p.split_stride + row * p.ldd + nb;
-                if (nb + 32 <= p.N && (p.ldd & 3) == 0) {
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t r[32];
+                        tmem_ld32(t_row + c0 + h * 32, r);
+                        tmem_ld_wait();
+                        const int nb = n0 + c0 + h * 32;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                } else {
-                    for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = v[j];
-                }
-                continue;
-            }
-            if (p.bias) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (nb + j < p.n_bias) v[j] += __ldg(p.bias + nb + j);
-            }
-            if (p.relu) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-            }
-            if (p.epi == EPI_BF16) {
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.D) + row * p.ldd + nb;
-                if (nb + 32 <= p.N && (p.ldd & 7) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 q;
-                        q.x = pack_bf16x2(v[j], v[j + 1]);
-                        q.y = pack_bf16x2(v[j + 2], v[j + 3]);
-                        q.z = pack_bf16x2(v[j + 4], v[j + 5]);
-                        q.w = pack_bf16x2(v[j + 6], v[j + 7]);
-                        *reinterpret_cast<uint4*>(out + j) = q;
+                        for (int j = 0; j < 32; j += 2) {
+                            float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
+                            if (p.bias) {
+                                if (nb + j < p.n_bias) v0 += __ldg(p.bias + nb + j);
+                                if (nb + j + 1 < p.n_bias) v1 += __ldg(p.bias + nb + j + 1);
+                            }
+                            if (p.relu) {
+                                v0 = fmaxf(v0, 0.f);
+                                v1 = fmaxf(v1, 0.f);
+                            }
+                            packed[h * 16 + j / 2] = pack_bf16x2(v0, v1);
+                        }
                     }
                 } else {
-                    for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = __float2bfloat16_rn(v[j]);
+                    tmem_ld32(t_row + c0, packed);
+                    tmem_ld_wait();
+                    const int nb = n0 + c0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float v = __uint_as_float(packed[j]) * p.alpha;
+                        if (p.bias && nb + j < p.n_bias) v += __ldg(p.bias + nb + j);
+                        if (p.relu) v = fmaxf(v, 0.f);
+                        packed[j] = __float_as_uint(v);
+                    }
                 }
-            } else {  // EPI_F32
-                float* out = reinterpret_cast<float*>(p.D) + row * p.ldd + nb;
-                for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = p.beta != 0.f ? v[j] + p.beta * out[j] : v[j];
+                if (c0 + cols_per_store >= BN) {
+                    // all TMEM reads of this accumulator are done: hand it back to the MMA warp
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                }
+                // staging buffer reuse: the TMA store issued two stores ago must have read it
+                uint8_t* stg = stage_base + (nstore & 1) * kStagingBytes;
+                if (nstore >= 2 && lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                const uint32_t row_addr = smem_u32(stg);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    st_shared_v4(row_addr + sw128_off(lane, q), packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
+                                 packed[4 * q + 3]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&p.tmD, stg, n0 + c0, m0 + ew * 32, w.sp);
+                    bulk_commit();
+                }
+                ++nstore;
             }
         }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
     }
 
     tc_fence_before();

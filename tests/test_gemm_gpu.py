@@ -72,6 +72,39 @@ def test_gemm_splitk_f32(splits):
     assert rel_err(D, ref) < TOL
 
 
+@pytest.mark.parametrize("b_layout", [0, 1])
+def test_gemm_padded_columns_never_read_past_b(b_layout):
+    """D has N = ceil8(out) columns but B has only `out` rows: the rows after B
+    (here NaN poison) must never be read, and padded columns come out 0."""
+    M, out, N, K = 64, 10, 16, 504
+    g = torch.Generator(device="cpu").manual_seed(3)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    Breal = torch.randn(out, K, generator=g).to(torch.bfloat16)
+    if b_layout == 0:
+        buf = torch.full((N, K), float("nan"), dtype=torch.bfloat16)
+        buf[:out] = Breal
+        ldb = K
+    else:
+        buf = torch.full((K, N), float("nan"), dtype=torch.bfloat16)
+        buf[:, :out] = Breal.t()
+        ldb = N
+    buf = buf.cuda()
+    D = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    bias = torch.randn(out, generator=g).cuda()
+    args = nat.GemmArgs(M=M, N=N, K=K, a_layout=0, b_layout=b_layout, A=A.data_ptr(), lda=K, B=buf.data_ptr(),
+                        ldb=ldb, D=D.data_ptr(), ldd=N, d_dtype=nat.TC_DTYPE_BF16, bias=bias.data_ptr(), relu=1,
+                        alpha=1.0, bias_n=out, b_rows=out)
+    ws_bytes = nat.lib().tc_gemm_workspace_bytes(C.byref(args))
+    ws = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device="cuda")
+    args.workspace, args.workspace_bytes = ws.data_ptr(), ws_bytes
+    nat.check(nat.lib().tc_gemm_bf16(C.byref(args), None))
+    torch.cuda.synchronize()
+    ref = (A.float() @ Breal.float().cuda().t() + bias).clamp_min(0)
+    assert torch.isfinite(D.float()).all()
+    assert torch.all(D[:, out:] == 0)
+    assert rel_err(D[:, :out], ref) < TOL
+
+
 def nhwc_pad(x_nchw, cs):
     n, c, h, w = x_nchw.shape
     out = torch.zeros(n, h, w, cs, dtype=torch.bfloat16, device=x_nchw.device)
