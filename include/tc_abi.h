@@ -92,7 +92,9 @@ typedef struct tc_conv_desc {
     int K, R, S;         /* output channels, kernel */
     int stride, pad;
     int Ho, Wo;          /* output spatial (floor((H+2p-R)/s)+1) */
-    int cs, ks;          /* channel strides (multiples of 8) of x and y */
+    int cs, ks;          /* channel strides of x and y: multiples of 8, or cs = 4 for a
+                            first-layer input (fwd / bwd-filter only, 8-byte gathers) */
+    int wld;             /* filter row stride in elements (0 = R*S*cs); multiple of 8 */
 } tc_conv_desc;
 
 TC_API tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w_krsc, const float* bias, int relu,

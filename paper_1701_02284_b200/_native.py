@@ -49,7 +49,7 @@ class ConvDesc(C.Structure):
         ("K", C.c_int), ("R", C.c_int), ("S", C.c_int),
         ("stride", C.c_int), ("pad", C.c_int),
         ("Ho", C.c_int), ("Wo", C.c_int),
-        ("cs", C.c_int), ("ks", C.c_int),
+        ("cs", C.c_int), ("ks", C.c_int), ("wld", C.c_int),
     ]
 
 

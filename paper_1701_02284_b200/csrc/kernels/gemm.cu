@@ -282,14 +282,19 @@ static ConvGeom geom_of(const tc_conv_desc* d) {
 static tc_status check_conv(const tc_conv_desc* d) {
     if (!d || d->N <= 0 || d->C <= 0 || d->K <= 0 || d->R <= 0 || d->S <= 0 || d->stride <= 0)
         return fail(TC_INVALID_ARG, "conv: bad descriptor");
-    if ((d->cs & 7) || (d->ks & 7) || d->cs < d->C || d->ks < d->K)
-        return fail(TC_INVALID_ARG, "conv: channel strides must be multiples of 8 and >= channels");
+    if ((d->cs & 7 && d->cs != 4) || (d->ks & 7) || d->cs < d->C || d->ks < d->K)
+        return fail(TC_INVALID_ARG, "conv: channel strides must be multiples of 8 (or 4 for the input) and >= channels");
+    if (d->wld && (d->wld < d->R * d->S * d->cs || (d->wld & 7)))
+        return fail(TC_INVALID_ARG, "conv: filter row stride must be >= R*S*cs and a multiple of 8");
     if ((d->H + 2 * d->pad - d->R) / d->stride + 1 != d->Ho || (d->W + 2 * d->pad - d->S) / d->stride + 1 != d->Wo)
         return fail(TC_SHAPE_FAULT, "conv: output extent mismatch");
     return TC_OK;
 }
 
-static bool is_pointwise(const tc_conv_desc* d) { return d->R == 1 && d->S == 1 && d->stride == 1 && d->pad == 0; }
+static bool is_pointwise(const tc_conv_desc* d) {
+    return d->R == 1 && d->S == 1 && d->stride == 1 && d->pad == 0 && d->cs % 8 == 0;
+}
+static int filter_ld(const tc_conv_desc* d) { return d->wld ? d->wld : d->R * d->S * d->cs; }
 
 static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
     const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
@@ -328,7 +333,7 @@ tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, con
         p.gsrc = static_cast<const __nv_bfloat16*>(x);
     }
     p.b_mode = OP_TMA_K;
-    if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, p.K, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+    if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, filter_ld(d), BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
     // Bias is read only for n < K; padded channels get 0 (relu(0) = 0).
     return run_gemm(p, lp, y, d->ks, 1, bias, d->K, relu, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
@@ -337,6 +342,7 @@ tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* 
                              size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (d->cs % 8) return fail(TC_INVALID_ARG, "conv bwd-data needs a channel stride multiple of 8");
     GemmParams p;
     init_params(p);
     p.M = d->N * d->H * d->W;
@@ -380,7 +386,7 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
         p.b_mode = OP_GATHER_MN;
         p.gsrc = static_cast<const __nv_bfloat16*>(x);
     }
-    return run_gemm(p, lp, dw, p.N, 0, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return run_gemm(p, lp, dw, filter_ld(d), 0, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

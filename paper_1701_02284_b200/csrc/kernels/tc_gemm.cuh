@@ -238,6 +238,120 @@ __device__ __forceinline__ void col_gather_issue(const GemmParams& p, const ColG
     }
 }
 
+// ---- channel-stride-4 gathers (first-layer convs, 3 real channels + 1 zero pad) ----
+// One 8-byte chunk = one filter tap; a 64-element k-block = 16 taps.
+struct RowGather4 {
+    const __nv_bfloat16* base;
+    int ry, rx, kh, kw, tap;
+    bool valid;
+};
+
+__device__ __forceinline__ void row_gather4_init(const GemmParams& p, RowGather4& rg, int m, int kb0) {
+    const ConvGeom& g = p.g;
+    rg.valid = m < p.M;
+    int n = 0;
+    rg.ry = rg.rx = 0;
+    if (rg.valid) {
+        n = m / (g.Ho * g.Wo);
+        const int rem = m - n * g.Ho * g.Wo;
+        rg.ry = rem / g.Wo;
+        rg.rx = rem - rg.ry * g.Wo;
+    }
+    rg.base = p.gsrc + static_cast<long long>(n) * g.H * g.W * 4;
+    rg.tap = kb0 * (BK / 4);
+    rg.kh = rg.tap / g.S;
+    rg.kw = rg.tap - rg.kh * g.S;
+}
+
+__device__ __forceinline__ void row_gather4_issue(const GemmParams& p, RowGather4& rg, uint32_t sA, int row) {
+    const ConvGeom& g = p.g;
+    const int ntaps = g.R * g.S;
+#pragma unroll
+    for (int jj = 0; jj < BK / 4; ++jj) {
+        const void* src = p.gsrc;
+        uint32_t bytes = 0;
+        if (rg.valid && rg.tap < ntaps) {
+            const int iy = rg.ry * g.stride - g.pad + rg.kh;
+            const int ix = rg.rx * g.stride - g.pad + rg.kw;
+            if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
+                static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
+                src = rg.base + (static_cast<long long>(iy) * g.W + ix) * 4;
+                bytes = 8;
+            }
+        }
+        cp_async_8(sA + static_cast<uint32_t>(row * 128 + (((jj >> 1) ^ (row & 7)) << 4) + (jj & 1) * 8), src, bytes);
+        ++rg.tap;
+        if (++rg.kw == g.S) {
+            rg.kw = 0;
+            ++rg.kh;
+        }
+    }
+}
+
+template <int BN>
+struct ColGather4 {
+    static constexpr int kChunks = BN / 16;
+    int code[kChunks][2];  // (kh << 8 | kw) of the two taps in a 16-byte chunk, -1 = beyond N
+};
+
+template <int BN>
+__device__ __forceinline__ void col_gather4_init(const GemmParams& p, ColGather4<BN>& cg, int n0, int half) {
+    const ConvGeom& g = p.g;
+#pragma unroll
+    for (int q = 0; q < ColGather4<BN>::kChunks; ++q) {
+        const int cc = half + 2 * q;
+        const int n = n0 + (cc >> 3) * 64 + (cc & 7) * 8;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int nn = n + 4 * h;
+            if (nn < p.N) {
+                const int tap = nn >> 2;
+                const int kh = tap / g.S;
+                cg.code[q][h] = (kh << 8) | (tap - kh * g.S);
+            } else {
+                cg.code[q][h] = -1;
+            }
+        }
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void col_gather4_issue(const GemmParams& p, const ColGather4<BN>& cg, uint32_t sB, int kr,
+                                                  int half, int kb) {
+    const ConvGeom& g = p.g;
+    const int pix = kb * BK + kr;
+    const bool pv = pix < g.N * g.Ho * g.Wo;
+    int rn = 0, oy = 0, ox = 0;
+    if (pv) {
+        rn = pix / (g.Ho * g.Wo);
+        const int rem = pix - rn * g.Ho * g.Wo;
+        oy = rem / g.Wo;
+        ox = rem - oy * g.Wo;
+    }
+    const __nv_bfloat16* img = p.gsrc + static_cast<long long>(rn) * g.H * g.W * 4;
+#pragma unroll
+    for (int q = 0; q < ColGather4<BN>::kChunks; ++q) {
+        const int cc = half + 2 * q;
+        const uint32_t dst = sB + (cc >> 3) * (BK * 128) + sw128_off(kr, cc & 7);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const void* src = p.gsrc;
+            uint32_t bytes = 0;
+            const int code = cg.code[q][h];
+            if (pv && code >= 0) {
+                const int iy = oy * g.stride - g.pad + (code >> 8);
+                const int ix = ox * g.stride - g.pad + (code & 0xFF);
+                if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
+                    static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
+                    src = img + (static_cast<long long>(iy) * g.W + ix) * 4;
+                    bytes = 8;
+                }
+            }
+            cp_async_8(dst + h * 8, src, bytes);
+        }
+    }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_constant__ GemmParams p) {
     using Cfg = TileCfg<BN>;
@@ -352,9 +466,38 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             constexpr int LAG = Cfg::kLag;
             const int t = threadIdx.x - 256;
             int it = 0;
+            const bool c4 = p.g.C == 4;  // channel-stride-4 first-layer input (fprop A / wgrad B)
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
                 const Unit w = decode_unit(p, u);
-                if (a_gather) {
+                if (a_gather && c4) {
+                    RowGather4 rg;
+                    row_gather4_init(p, rg, w.mt * BM + t, w.kb0);
+                    for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                        const int s = it % S;
+                        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                        row_gather4_issue(p, rg, smem_u32(sA + s * Cfg::kABytes), t);
+                        cp_async_commit();
+                        if (it >= LAG) {
+                            cp_async_wait<LAG>();
+                            fence_proxy_async_smem();
+                            mbar_arrive(&full[(it - LAG) % S]);
+                        }
+                    }
+                } else if (b_gather && c4) {
+                    ColGather4<BN> cg;
+                    col_gather4_init<BN>(p, cg, w.nt * BN, t >> 6);
+                    for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                        const int s = it % S;
+                        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                        col_gather4_issue<BN>(p, cg, smem_u32(sB + s * Cfg::kBBytes), t & 63, t >> 6, kb);
+                        cp_async_commit();
+                        if (it >= LAG) {
+                            cp_async_wait<LAG>();
+                            fence_proxy_async_smem();
+                            mbar_arrive(&full[(it - LAG) % S]);
+                        }
+                    }
+                } else if (a_gather) {
                     RowGather rg;
                     row_gather_init(p, rg, w.mt * BM + t, w.kb0);
                     for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {

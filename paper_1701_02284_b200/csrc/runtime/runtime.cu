@@ -62,10 +62,9 @@ struct ParamL {
     int K = 1, C = 1, R = 1, S = 1, cs = 8, ks = 8;
     bool fc_from4d = false;
     int fH = 1, fW = 1, fC = 1, fcs = 8;  // flattened 4-D input of an FC layer
-    // First-layer convs with few input channels run as dense im2col + GEMM over the
-    // real channels: p / v / g / shadow are [K][Kp], Kp = ceil8(R*S*C) (no bwd-data).
-    bool packed = false;
-    int Kp = 0;
+    // conv filter row stride: Kw = ceil8(R*S*cs) (== R*S*cs unless cs = 4, the
+    // channel-stride-4 first-layer input whose taps are gathered 8 bytes at a time)
+    int Kw = 0;
     int in_dev = 0;
     long long n = 0;  // device elements
     float* p = nullptr;
@@ -110,8 +109,6 @@ struct tc_ctx {
     size_t slab_bytes = 0;
     uint8_t* ws = nullptr;
     size_t ws_bytes = 0;
-    bf16* col = nullptr;  // shared im2col workspace of the packed first-layer convs
-    size_t col_bytes = 0;
     float* partials = nullptr;
     int max_partials = 0;
     bf16* d_input = nullptr;
@@ -207,7 +204,8 @@ tc_status analyze_layouts(tc_ctx* c) {
             v.C = static_cast<int>(v.d[1]);
             v.H = static_cast<int>(v.d[2]);
             v.W = static_cast<int>(v.d[3]);
-            v.cs = ceil8(v.C);
+            // the input image of <= 4 channels is staged with channel stride 4 (8-byte taps)
+            v.cs = (s.op == TC_OP_LOAD_X && v.C <= 4) ? 4 : ceil8(v.C);
         } else if (v.rank == 2) {
             v.N = static_cast<int>(v.d[0]);
             v.C = static_cast<int>(v.d[1]);
@@ -231,16 +229,17 @@ tc_status analyze_layouts(tc_ctx* c) {
             return fail(TC_SHAPE_FAULT, "runtime: unsupported var rank " + std::to_string(v.rank));
         }
     }
-    // first-layer small-channel convs: dense im2col path
+    // conv filters follow their input's channel stride (cs = 4 for a <= 4-channel input image)
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET || s.op != TC_OP_CONV_FWD || s.in[0].kind != TC_REF_VAR) continue;
-        const VarL& x = c->vars.at(s.in[0].index);
-        if (x.def < 0 || p->stmts[x.def].op != TC_OP_LOAD_X || x.C >= 8) continue;
         ParamL& q = c->params[s.in[1].index];
-        q.packed = true;
-        q.Kp = ceil8(static_cast<long long>(q.R) * q.S * q.C);
-        q.n = static_cast<long long>(q.K) * q.Kp;
+        q.cs = c->vars.at(s.in[0].index).cs;
+    }
+    for (ParamL& q : c->params) {
+        if (q.kind != ParamL::CONV) continue;
+        q.Kw = ceil8(static_cast<long long>(q.R) * q.S * q.cs);
+        q.n = static_cast<long long>(q.K) * q.Kw;
     }
     // FC weight device layout follows its forward input
     for (int i = 0; i < p->nparams; ++i) {
@@ -421,19 +420,12 @@ tc_status plan_arena(tc_ctx* c) {
 // ------------------------------------------------------------------ host layout permutations
 void ref_to_dev(const ParamL& q, const float* ref, std::vector<float>& dev) {
     dev.assign(q.n, 0.f);
-    if (q.kind == ParamL::CONV && q.packed) {
+    if (q.kind == ParamL::CONV) {  // [K][Kw], Kw >= R*S*cs, (r, s, c) order
         for (int k = 0; k < q.K; ++k)
             for (int c = 0; c < q.C; ++c)
                 for (int r = 0; r < q.R; ++r)
                     for (int s = 0; s < q.S; ++s)
-                        dev[static_cast<long long>(k) * q.Kp + (r * q.S + s) * q.C + c] =
-                            ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s];
-    } else if (q.kind == ParamL::CONV) {
-        for (int k = 0; k < q.K; ++k)
-            for (int c = 0; c < q.C; ++c)
-                for (int r = 0; r < q.R; ++r)
-                    for (int s = 0; s < q.S; ++s)
-                        dev[((static_cast<long long>(k) * q.R + r) * q.S + s) * q.cs + c] =
+                        dev[static_cast<long long>(k) * q.Kw + (static_cast<long long>(r) * q.S + s) * q.cs + c] =
                             ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s];
     } else if (q.kind == ParamL::FC) {
         for (int o = 0; o < q.K; ++o) {
@@ -453,20 +445,13 @@ void ref_to_dev(const ParamL& q, const float* ref, std::vector<float>& dev) {
 }
 
 void dev_to_ref(const ParamL& q, const float* dev, float* ref) {
-    if (q.kind == ParamL::CONV && q.packed) {
+    if (q.kind == ParamL::CONV) {
         for (int k = 0; k < q.K; ++k)
             for (int c = 0; c < q.C; ++c)
                 for (int r = 0; r < q.R; ++r)
                     for (int s = 0; s < q.S; ++s)
                         ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s] =
-                            dev[static_cast<long long>(k) * q.Kp + (r * q.S + s) * q.C + c];
-    } else if (q.kind == ParamL::CONV) {
-        for (int k = 0; k < q.K; ++k)
-            for (int c = 0; c < q.C; ++c)
-                for (int r = 0; r < q.R; ++r)
-                    for (int s = 0; s < q.S; ++s)
-                        ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + s] =
-                            dev[((static_cast<long long>(k) * q.R + r) * q.S + s) * q.cs + c];
+                            dev[static_cast<long long>(k) * q.Kw + (static_cast<long long>(r) * q.S + s) * q.cs + c];
     } else if (q.kind == ParamL::FC) {
         for (int o = 0; o < q.K; ++o) {
             if (q.fc_from4d) {
@@ -554,6 +539,7 @@ tc_conv_desc conv_desc(const VarL& x, const ParamL& w, const VarL& y, const tc_s
     d.Wo = y.W;
     d.cs = x.cs;
     d.ks = y.cs;
+    d.wld = w.Kw;
     return d;
 }
 
@@ -572,26 +558,6 @@ tc_status compute_param_grad(tc_ctx* c, const tc_stmt& s, int pidx, float* g) {
         case TC_OP_CONV_BWD_FILTER: {
             const VarL& dy = P.L(s.in[0]);
             const VarL& x = P.L(s.in[1]);
-            if (q.packed) {  // dW[K][Kp] = dy^T . im2col(x)
-                tc_status r = launch_im2col(reinterpret_cast<const bf16*>(P.var(x.id)), x.act(), q.R, q.S, s.stride,
-                                            s.pad, dy.H, dy.W, q.Kp, c->col, st);
-                if (r != TC_OK) return r;
-                tc_gemm_args ga{};
-                ga.M = q.K;
-                ga.N = q.Kp;
-                ga.K = dy.N * dy.H * dy.W;
-                ga.a_layout = TC_LAYOUT_MN;
-                ga.A = P.var(dy.id);
-                ga.lda = dy.cs;
-                ga.b_layout = TC_LAYOUT_MN;
-                ga.B = c->col;
-                ga.ldb = q.Kp;
-                ga.D = g;
-                ga.ldd = q.Kp;
-                ga.d_dtype = TC_DTYPE_F32;
-                ga.alpha = 1.f;
-                return run_gemm_args(c, ga);
-            }
             tc_conv_desc d = conv_desc(x, q, dy, s);
             return tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
         }
@@ -647,30 +613,6 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& x = P.L(s.in[0]);
             const ParamL& w = c->params[s.in[1].index];
             const float* bias = s.nin > 2 ? c->params[s.in[2].index].p : nullptr;
-            if (w.packed) {  // y[M][ks] = im2col(x)[M][Kp] . W[K][Kp]^T (+bias, relu)
-                tc_status r = launch_im2col(reinterpret_cast<const bf16*>(P.var(x.id)), x.act(), w.R, w.S, s.stride,
-                                            s.pad, out.H, out.W, w.Kp, c->col, st);
-                if (r != TC_OK) return r;
-                tc_gemm_args ga{};
-                ga.M = out.N * out.H * out.W;
-                ga.N = out.cs;
-                ga.K = w.Kp;
-                ga.a_layout = TC_LAYOUT_K;
-                ga.A = c->col;
-                ga.lda = w.Kp;
-                ga.b_layout = TC_LAYOUT_K;
-                ga.B = w.shadow;
-                ga.ldb = w.Kp;
-                ga.D = y;
-                ga.ldd = out.cs;
-                ga.d_dtype = TC_DTYPE_BF16;
-                ga.bias = bias;
-                ga.bias_n = w.K;
-                ga.b_rows = w.K;  // the packed filter has K rows; padded output channels come out 0
-                ga.relu = c->fuse_relu[i];
-                ga.alpha = 1.f;
-                return run_gemm_args(c, ga);
-            }
             tc_conv_desc d = conv_desc(x, w, out, s);
             return tc_conv2d_fwd(&d, P.var(x.id), w.shadow, bias, c->fuse_relu[i], y, c->ws, c->ws_bytes, st);
         }
@@ -918,25 +860,6 @@ size_t workspace_need(tc_ctx* c) {
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET && s.kind != TC_STMT_UPDATE) continue;
-        const int pk = s.op == TC_OP_CONV_FWD ? s.in[1].index : s.op == TC_OP_CONV_BWD_FILTER ? s.param : -1;
-        if (pk >= 0 && c->params[pk].packed) {
-            const ParamL& q = c->params[pk];
-            const VarL& y = s.op == TC_OP_CONV_FWD ? c->vars.at(s.var) : P.L(s.in[0]);
-            const long long M = static_cast<long long>(y.N) * y.H * y.W;
-            c->col_bytes = std::max(c->col_bytes, static_cast<size_t>(M) * q.Kp * 2);
-            tc_gemm_args ga{};
-            if (s.op == TC_OP_CONV_FWD) {
-                ga.M = static_cast<int>(M);
-                ga.N = y.cs;
-                ga.K = q.Kp;
-            } else {
-                ga.M = q.K;
-                ga.N = q.Kp;
-                ga.K = static_cast<int>(M);
-            }
-            need = std::max(need, tc_gemm_workspace_bytes(&ga));
-            continue;
-        }
         switch (s.op) {
             case TC_OP_CONV_FWD: {
                 const VarL& x = P.L(s.in[0]);
@@ -1022,7 +945,7 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
         offs.push_back(reserve(q.n * 4));  // v
         offs.push_back(reserve(q.n * 4));  // g
         offs.push_back(q.kind != ParamL::VEC ? reserve(q.n * 2) : SIZE_MAX);
-        offs.push_back(q.kind == ParamL::CONV && !q.packed ? reserve(static_cast<size_t>(q.R) * q.S * q.ks * q.cs * 2)
+        offs.push_back(q.kind == ParamL::CONV && q.cs % 8 == 0 ? reserve(static_cast<size_t>(q.R) * q.S * q.ks * q.cs * 2)
                                                            : SIZE_MAX);
     }
     c->slab_bytes = slab;
@@ -1040,7 +963,7 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMalloc(&c->arena, std::max<size_t>(c->arena_bytes, 256)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
     // input staging: NHWC bf16 batch + labels + NCHW fp32 staging for host batches
-    c->input_cs = ceil8(plan->input_dims[1]);
+    c->input_cs = plan->input_dims[1] <= 4 ? 4 : ceil8(plan->input_dims[1]);  // must match the LOAD_X var layout
     const size_t in_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[2] * plan->input_dims[3] * c->input_cs;
     const size_t stage_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
     c->input_bytes = in_el * 2 + stage_el * 4;
@@ -1062,7 +985,6 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     for (const ParamL& q : c->params) maxc = std::max(maxc, q.K);
     c->max_partials = static_cast<int>(colsum_partials_floats(maxc));
     TCB_CUDA_CHECK(cudaMalloc(&c->ws, std::max<size_t>(c->ws_bytes, 256)));
-    if (c->col_bytes) TCB_CUDA_CHECK(cudaMalloc(&c->col, c->col_bytes));
     TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 2 * maxc + 64) * sizeof(float)));
     if (desc->world > 1) {
         if (!desc->nccl_id) return fail(TC_INVALID_ARG, "world > 1 needs an NCCL unique id");
@@ -1090,7 +1012,6 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->arena);
     cudaFree(c->slab);
     cudaFree(c->ws);
-    cudaFree(c->col);
     cudaFree(c->partials);
     cudaFree(c->d_input);
     cudaFree(c->d_stage);
@@ -1294,7 +1215,7 @@ tc_status tc_memory(tc_ctx* c, tc_rt_memory* out) {
     out->arena_bytes = static_cast<int64_t>(c->arena_bytes);
     out->arena_keep_bytes = static_cast<int64_t>(c->arena_keep_bytes);
     out->param_bytes = static_cast<int64_t>(c->slab_bytes);
-    out->workspace_bytes = static_cast<int64_t>(c->ws_bytes + c->col_bytes);
+    out->workspace_bytes = static_cast<int64_t>(c->ws_bytes);
     out->input_bytes = static_cast<int64_t>(c->input_bytes);
     out->device_used_bytes = c->device_used;
     return TC_OK;

@@ -150,6 +150,35 @@ CONV_CASES = [
 ]
 
 
+@pytest.mark.parametrize("case", [(2, 3, 35, 35, 96, 11, 4, 0), (2, 3, 32, 32, 64, 7, 2, 3), (2, 1, 28, 28, 20, 5, 1, 0)])
+def test_conv_channel_stride4_fwd_and_filter(case):
+    """First-layer convs: input staged with channel stride 4 (8-byte tap gathers),
+    filter rows padded to a multiple of 8 (wld)."""
+    x, w, b, d = conv_case(*case)
+    d.cs = 4
+    d.wld = (d.R * d.S * 4 + 7) // 8 * 8
+    xs = nhwc_pad(x, 4)
+    wk = torch.zeros(d.K, d.wld, dtype=torch.bfloat16, device="cuda")
+    wk[:, :d.R * d.S * 4] = w_krsc(w, 4).reshape(d.K, -1)
+    y = torch.full((d.N, d.Ho, d.Wo, d.ks), float("nan"), dtype=torch.bfloat16, device="cuda")
+    nat.check(nat.lib().tc_conv2d_fwd(C.byref(d), xs.data_ptr(), wk.data_ptr(), b.data_ptr(), 0, y.data_ptr(),
+                                      None, 0, None))
+    ref = torch.nn.functional.conv2d(x, w, b, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
+    torch.cuda.synchronize()
+    assert rel_err(y[..., :d.K], ref) < TOL
+    g = torch.Generator(device="cpu").manual_seed(6)
+    dy = torch.randn(d.N, d.K, d.Ho, d.Wo, generator=g).to(torch.bfloat16).float().cuda()
+    dw = torch.full((d.K, d.wld), float("nan"), dtype=torch.float32, device="cuda")
+    wsb = nat.lib().tc_conv2d_workspace_bytes(C.byref(d), 2)
+    wsp = torch.empty(max(wsb, 4), dtype=torch.uint8, device="cuda")
+    nat.check(nat.lib().tc_conv2d_bwd_filter(C.byref(d), nhwc_pad(dy, d.ks).data_ptr(), xs.data_ptr(), dw.data_ptr(),
+                                             wsp.data_ptr(), wsb, None))
+    torch.cuda.synchronize()
+    refw = torch.nn.grad.conv2d_weight(x, w.shape, dy, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
+    got = dw[:, :d.R * d.S * 4].reshape(d.K, d.R, d.S, 4)[..., :d.C]
+    assert rel_err(got, refw) < TOL
+
+
 @pytest.mark.parametrize("case", CONV_CASES)
 def test_conv_fwd(case):
     x, w, b, d = conv_case(*case)
