@@ -561,41 +561,41 @@ __device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, i
     }
 }
 
-__global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, int size, float alpha, float beta,
+// HALF = n/2 is a template parameter so every window loop unrolls and the
+// per-thread channel windows stay in registers.
+template <int HALF>
+__global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, float alpha, float beta,
                            float kk) {
     const int ng = a.cs / 8;
     const long long total = a.pixels() * ng;
-    const int half = size / 2;
-    const float an = alpha / static_cast<float>(size);
+    const float an = alpha / static_cast<float>(2 * HALF + 1);
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int g = static_cast<int>(t % ng);
         const bf16* px = x + (t / ng) * a.cs;
         float v[24];
         load_chunk3(px, g, ng, v);
+        // channels outside [0, C) contribute nothing (pads are zero, neighbours beyond the tensor loaded as 0)
         float out[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int c = g * 8 + j;
             float s = 0.f;
-            for (int d = -half; d <= half; ++d) {
-                const int cc = c + d;
-                const float e = v[8 + j + d];
-                if (cc >= 0 && cc < a.C) s += e * e;
-            }
-            out[j] = c < a.C ? v[8 + j] * __powf(kk + an * s, -beta) : 0.f;
+#pragma unroll
+            for (int d = -HALF; d <= HALF; ++d) s += v[8 + j + d] * v[8 + j + d];
+            out[j] = (g * 8 + j) < a.C ? v[8 + j] * __powf(kk + an * s, -beta) : 0.f;
         }
-        *reinterpret_cast<uint4*>(y + t * 8 - static_cast<long long>(0)) = pack8(out);
+        *reinterpret_cast<uint4*>(y + t * 8) = pack8(out);
     }
 }
 
+template <int HALF>
 __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
-                           bf16* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
+                           bf16* __restrict__ dx, Act4 a, float alpha, float beta, float kk) {
     const int ng = a.cs / 8;
     const long long total = a.pixels() * ng;
-    const int half = size / 2;
-    const float an = alpha / static_cast<float>(size);
-    const float coef = 2.f * alpha * beta / static_cast<float>(size);
+    const float an = alpha / static_cast<float>(2 * HALF + 1);
+    const float coef = 2.f * alpha * beta / static_cast<float>(2 * HALF + 1);
+    constexpr int L = 8 - HALF, U = 16 + HALF;  // window of channels g*8-HALF .. g*8+7+HALF
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int g = static_cast<int>(t % ng);
@@ -604,35 +604,23 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
         load_chunk3(x + base, g, ng, xv);
         load_chunk3(dy + base, g, ng, dv);
         load_chunk3(y + base, g, ng, yv);
-        // scale and t = dy*y/scale for channels g*8-half .. g*8+7+half (indices 8-half .. 15+half of the window)
         float sc[24], tt[24];
 #pragma unroll
-        for (int i = 0; i < 24; ++i) {
-            sc[i] = 1.f;
-            tt[i] = 0.f;
-        }
-        for (int i = 8 - half; i < 16 + half; ++i) {
-            const int c = g * 8 - 8 + i;
-            if (c < 0 || c >= a.C) continue;
+        for (int i = L; i < U; ++i) {
             float s = 0.f;
-            for (int d = -half; d <= half; ++d) {
-                const int cc = c + d, ii = i + d;
-                if (cc >= 0 && cc < a.C) {
-                    // squares beyond the loaded 3 chunks are only needed when half > 8 (never: n <= 9 plus edges)
-                    const float e = (ii >= 0 && ii < 24) ? xv[ii] : 0.f;
-                    s += e * e;
-                }
-            }
+#pragma unroll
+            for (int d = -HALF; d <= HALF; ++d) s += xv[i + d] * xv[i + d];
             sc[i] = kk + an * s;
-            tt[i] = dv[i] * yv[i] / sc[i];
+            // zero for channels outside [0, C): dy and y are zero there
+            tt[i] = dv[i] * yv[i] * __frcp_rn(sc[i]);
         }
         float out[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int c = g * 8 + j;
             float s = 0.f;
-            for (int d = -half; d <= half; ++d) s += tt[8 + j + d];
-            out[j] = c < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
+#pragma unroll
+            for (int d = -HALF; d <= HALF; ++d) s += tt[8 + j + d];
+            out[j] = (g * 8 + j) < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
         }
         *reinterpret_cast<uint4*>(dx + base + g * 8) = pack8(out);
     }
@@ -750,24 +738,34 @@ tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const int32_t* idx, bf16* dx,
     return TC_OK;
 }
 tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
-    if (size > 9) {  // general path: warp per pixel with the channel vector in shared memory
-        const int warps = 8;
-        k_lrn_fwd<<<grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st>>>(x, y, a, size, alpha,
-                                                                                                 beta, k);
-    } else {
-        k_lrn2_fwd<<<EW_GRID(a.pixels() * (a.cs / 8))>>>(x, y, a, size, alpha, beta, k);
+    const long long n = a.pixels() * (a.cs / 8);
+    switch (size) {  // odd windows up to 9: register-resident template kernels
+        case 3: k_lrn2_fwd<1><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
+        case 5: k_lrn2_fwd<2><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
+        case 7: k_lrn2_fwd<3><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
+        case 9: k_lrn2_fwd<4><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
+        default: {  // general path: warp per pixel with the channel vector in shared memory
+            const int warps = 8;
+            k_lrn_fwd<<<grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st>>>(x, y, a, size,
+                                                                                                     alpha, beta, k);
+        }
     }
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
                          float beta, float k, cudaStream_t st) {
-    if (size > 9) {
-        const int warps = 8;
-        k_lrn_bwd<<<grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st>>>(dy, x, y, dx, a,
-                                                                                                     size, alpha, beta, k);
-    } else {
-        k_lrn2_bwd<<<EW_GRID(a.pixels() * (a.cs / 8))>>>(dy, x, y, dx, a, size, alpha, beta, k);
+    const long long n = a.pixels() * (a.cs / 8);
+    switch (size) {
+        case 3: k_lrn2_bwd<1><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
+        case 5: k_lrn2_bwd<2><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
+        case 7: k_lrn2_bwd<3><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
+        case 9: k_lrn2_bwd<4><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
+        default: {
+            const int warps = 8;
+            k_lrn_bwd<<<grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st>>>(
+                dy, x, y, dx, a, size, alpha, beta, k);
+        }
     }
     TCB_LAUNCH_CHECK();
     return TC_OK;

@@ -136,36 +136,53 @@ __device__ __forceinline__ void row_gather_init(const GemmParams& p, RowGather& 
     }
 }
 
+// Source pixel of (row, tap) or null when the tap falls into padding / a stride hole.
+__device__ __forceinline__ const __nv_bfloat16* tap_source(const GemmParams& p, const RowGather& rg, int kh, int kw) {
+    const ConvGeom& g = p.g;
+    if (p.gather_kind == GATHER_FPROP) {
+        const int iy = rg.ry * g.stride - g.pad + kh;
+        const int ix = rg.rx * g.stride - g.pad + kw;
+        if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) && static_cast<unsigned>(ix) < static_cast<unsigned>(g.W))
+            return rg.base + (static_cast<long long>(iy) * g.W + ix) * g.C;
+        return nullptr;
+    }
+    int oy = rg.ry + g.pad - kh, ox = rg.rx + g.pad - kw;
+    if (oy < 0 || ox < 0) return nullptr;
+    if (g.stride != 1) {
+        const int qy = oy / g.stride, qx = ox / g.stride;
+        if (qy * g.stride != oy || qx * g.stride != ox) return nullptr;
+        oy = qy;
+        ox = qx;
+    }
+    if (oy >= g.Ho || ox >= g.Wo) return nullptr;
+    return rg.base + (static_cast<long long>(oy) * g.Wo + ox) * g.Co;
+}
+
 __device__ __forceinline__ void row_gather_issue(const GemmParams& p, RowGather& rg, uint32_t sA, int row) {
     const ConvGeom& g = p.g;
     const bool fprop = p.gather_kind == GATHER_FPROP;
     const int C = fprop ? g.C : g.Co;
+    if (C % BK == 0) {
+        // the whole k-block is one filter tap: one address, 128 contiguous bytes
+        const __nv_bfloat16* src = (rg.valid && rg.kk[0] < p.K) ? tap_source(p, rg, rg.kh[0], rg.kw[0]) : nullptr;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const void* src = p.gsrc;
-        uint32_t bytes = 0;
-        if (rg.valid && rg.kk[j] < p.K) {
-            if (fprop) {
-                const int iy = rg.ry * g.stride - g.pad + rg.kh[j];
-                const int ix = rg.rx * g.stride - g.pad + rg.kw[j];
-                if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
-                    static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
-                    src = rg.base + (static_cast<long long>(iy) * g.W + ix) * g.C + rg.c[j];
-                    bytes = 16;
-                }
-            } else {
-                const int ny = rg.ry + g.pad - rg.kh[j];
-                const int nx = rg.rx + g.pad - rg.kw[j];
-                if (ny >= 0 && nx >= 0) {
-                    const int oy = ny / g.stride, ox = nx / g.stride;
-                    if (oy * g.stride == ny && ox * g.stride == nx && oy < g.Ho && ox < g.Wo) {
-                        src = rg.base + (static_cast<long long>(oy) * g.Wo + ox) * g.Co + rg.c[j];
-                        bytes = 16;
-                    }
-                }
+        for (int j = 0; j < 8; ++j)
+            cp_async_16(sA + sw128_off(row, j), src ? src + rg.c[0] + j * 8 : p.gsrc, src ? 16u : 0u);
+        rg.kk[0] += BK;
+        rg.c[0] += BK;
+        if (rg.c[0] >= C) {
+            rg.c[0] = 0;
+            if (++rg.kw[0] == g.S) {
+                rg.kw[0] = 0;
+                ++rg.kh[0];
             }
         }
-        cp_async_16(sA + sw128_off(row, j), src, bytes);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const __nv_bfloat16* src = (rg.valid && rg.kk[j] < p.K) ? tap_source(p, rg, rg.kh[j], rg.kw[j]) : nullptr;
+        cp_async_16(sA + sw128_off(row, j), src ? src + rg.c[j] : p.gsrc, src ? 16u : 0u);
         // advance this chunk by one k-block (64 channels along (kh, kw, c))
         rg.kk[j] += BK;
         rg.c[j] += BK;
