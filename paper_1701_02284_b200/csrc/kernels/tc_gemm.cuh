@@ -9,6 +9,9 @@
 //   OP_GATHER_K  implicit im2col rows of an NHWC activation (fprop: x, bwd-data: dy),
 //                16-byte cp.async gathers with zero fill, written pre-swizzled (A only)
 //   OP_GATHER_MN implicit im2col of x, transposed, for bwd-filter (B only)
+//   OP_IM2COL_K  TMA im2col of an NHWC activation: one {64 channels x 128 pixels} box per
+//                k-block = (filter tap, 64-channel block), tap passed as the im2col offset (A only)
+//   OP_IM2COL_MN TMA im2col of x for bwd-filter: {64 channels x 64 pixels} boxes (B only)
 //
 // Persistent, warp-specialised (384 threads, one CTA per SM):
 //   warp 0      TMA producer (elected lane)
@@ -28,7 +31,7 @@
 
 namespace tcb {
 
-enum OperandMode : int { OP_TMA_K = 0, OP_TMA_MN = 1, OP_GATHER_K = 2, OP_GATHER_MN = 3 };
+enum OperandMode : int { OP_TMA_K = 0, OP_TMA_MN = 1, OP_GATHER_K = 2, OP_GATHER_MN = 3, OP_IM2COL_K = 4, OP_IM2COL_MN = 5 };
 enum GatherKind : int { GATHER_FPROP = 0, GATHER_DGRAD = 1 };
 enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1 };
 
@@ -59,6 +62,12 @@ struct GemmParams {
     int n_bias;                 // bias is read for n < n_bias (padded channels get 0)
     int relu;
     float alpha;
+    // TMA im2col operand: tmA (OP_IM2COL_K) or tmB (OP_IM2COL_MN) is a 4-D {c, w, h, n} im2col map
+    int i2c_cpb;             // 64-channel blocks per filter tap (A side)
+    int i2c_ldk;             // k coordinate of tap t in the other operand = t * i2c_ldk + 64 * block
+    int i2c_lo_w, i2c_lo_h;  // first source pixel of output pixel (y, x) = (y * stride + lo_h, x * stride + lo_w)
+    int i2c_flip;            // bwd-data: tap (kh, kw) is the offset (R-1-kh, S-1-kw)
+    int i2c_P, i2c_Q;        // pixel grid the rows (A) / k-blocks (B) walk: P x Q per image
 };
 
 constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
@@ -416,28 +425,65 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             uint32_t tx = 0;
             if (!a_gather) tx += Cfg::kABytes;
             if (!b_gather) tx += Cfg::kBBytes;
+            const ConvGeom& g = p.g;
             int it = 0;
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
                 const Unit w = decode_unit(p, u);
                 const int m0 = w.mt * BM, n0 = w.nt * BN;
+                // im2col A: first pixel of this row tile
+                int a_n = 0, a_y = 0, a_x = 0;
+                if (p.a_mode == OP_IM2COL_K) {
+                    const int pq = p.i2c_P * p.i2c_Q;
+                    a_n = m0 / pq;
+                    const int rem = m0 - a_n * pq;
+                    const int oy = rem / p.i2c_Q;
+                    a_y = oy * g.stride + p.i2c_lo_h;
+                    a_x = (rem - oy * p.i2c_Q) * g.stride + p.i2c_lo_w;
+                }
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
                     const int s = it % S;
                     mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
                     uint8_t* a_dst = sA + s * Cfg::kABytes;
                     uint8_t* b_dst = sB + s * Cfg::kBBytes;
+                    int kc = kb * BK;  // k coordinate of this block in the plain-TMA operand
                     if (p.a_mode == OP_TMA_K) {
-                        tma_load_2d(a_dst, &p.tmA, &full[s], kb * BK, m0);
+                        tma_load_2d(a_dst, &p.tmA, &full[s], kc, m0);
                     } else if (p.a_mode == OP_TMA_MN) {
 #pragma unroll
                         for (int a = 0; a < BM / 64; ++a)
-                            tma_load_2d(a_dst + a * BK * 128, &p.tmA, &full[s], m0 + a * 64, kb * BK);
+                            tma_load_2d(a_dst + a * BK * 128, &p.tmA, &full[s], m0 + a * 64, kc);
+                    } else if (p.a_mode == OP_IM2COL_K) {
+                        const int tap = kb / p.i2c_cpb, cb = kb - tap * p.i2c_cpb;
+                        const int kh = tap / g.S, kw = tap - kh * g.S;
+                        const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
+                        tma_load_im2col_4d(a_dst, &p.tmA, &full[s], cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
+                                           static_cast<uint16_t>(oh));
+                        kc = tap * p.i2c_ldk + cb * 64;
                     }
                     if (p.b_mode == OP_TMA_K) {
-                        tma_load_2d(b_dst, &p.tmB, &full[s], kb * BK, n0);
+                        tma_load_2d(b_dst, &p.tmB, &full[s], kc, n0);
                     } else if (p.b_mode == OP_TMA_MN) {
 #pragma unroll
                         for (int a = 0; a < BN / 64; ++a)
-                            tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kb * BK);
+                            tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kc);
+                    } else if (p.b_mode == OP_IM2COL_MN) {
+                        // 64 output pixels of this k-block; columns n = tap * cs + c in 64-channel atoms
+                        const int pq = p.i2c_P * p.i2c_Q;
+                        const int pix = kb * BK;
+                        const int bn_img = pix / pq;
+                        const int rem = pix - bn_img * pq;
+                        const int oy = rem / p.i2c_Q;
+                        const int by = oy * g.stride + p.i2c_lo_h;
+                        const int bx = (rem - oy * p.i2c_Q) * g.stride + p.i2c_lo_w;
+#pragma unroll
+                        for (int a = 0; a < BN / 64; ++a) {
+                            int n = n0 + a * 64;
+                            if (n >= p.N) n = 0;  // columns past N are clipped by the store; load finite data
+                            const int tap = n / g.C, c = n - tap * g.C;
+                            const int kh = tap / g.S, kw = tap - kh * g.S;
+                            tma_load_im2col_4d(b_dst + a * BK * 128, &p.tmB, &full[s], c, bx, by, bn_img,
+                                               static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
+                        }
                     }
                     mbar_arrive_expect_tx(&full[s], tx);
                 }
@@ -446,7 +492,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     } else if (warp == 1) {
         // ---------------- MMA issuer
         const bool a_mn = p.a_mode == OP_TMA_MN;
-        const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN;
+        const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN;
         const uint32_t idesc = umma_idesc_bf16(BM, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
         int it = 0, tc = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {

@@ -149,6 +149,16 @@ CONV_CASES = [
     (2, 32, 15, 15, 48, 3, 2, 1),
 ]
 
+# channel strides that are whole 64-channel blocks take the TMA im2col operand path
+# (fprop A, bwd-data A for stride 1, bwd-filter B); odd extents, pad 0/1/2, strides 1/2
+IM2COL_CASES = [
+    (2, 64, 13, 13, 128, 3, 1, 1),
+    (2, 128, 15, 15, 64, 3, 2, 1),
+    (3, 64, 9, 11, 192, 5, 1, 2),
+    (5, 64, 7, 7, 64, 3, 1, 0),
+    (1, 256, 13, 13, 384, 3, 1, 1),
+]
+
 
 @pytest.mark.parametrize("case", [(2, 3, 35, 35, 96, 11, 4, 0), (2, 3, 32, 32, 64, 7, 2, 3), (2, 1, 28, 28, 20, 5, 1, 0)])
 def test_conv_channel_stride4_fwd_and_filter(case):
@@ -179,7 +189,7 @@ def test_conv_channel_stride4_fwd_and_filter(case):
     assert rel_err(got, refw) < TOL
 
 
-@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES)
 def test_conv_fwd(case):
     x, w, b, d = conv_case(*case)
     xs = nhwc_pad(x, d.cs)
@@ -193,7 +203,7 @@ def test_conv_fwd(case):
     assert torch.all(y[..., d.K:] == 0)
 
 
-@pytest.mark.parametrize("case", CONV_CASES[2:] + [(2, 8, 13, 13, 64, 3, 1, 1)])
+@pytest.mark.parametrize("case", CONV_CASES[2:] + [(2, 8, 13, 13, 64, 3, 1, 1)] + IM2COL_CASES)
 def test_conv_bwd_data(case):
     x, w, b, d = conv_case(*case, seed=1)
     g = torch.Generator(device="cpu").manual_seed(5)
@@ -207,7 +217,7 @@ def test_conv_bwd_data(case):
     assert rel_err(dx[..., :d.C], ref) < TOL
 
 
-@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES)
 def test_conv_bwd_filter(case):
     x, w, b, d = conv_case(*case, seed=2)
     g = torch.Generator(device="cpu").manual_seed(6)
