@@ -28,6 +28,14 @@ sys.path.insert(0, ROOT)
 
 NET, BATCH = "alexnet", 128
 SEED = 42
+# per-GPU batch of each BASELINE.json config (weak scaling)
+CONFIG_BATCH = {"lenet": 64, "alexnet": 128, "vgg16": 64, "googlenet": 128, "resnet50": 64}
+
+
+def set_workload(args):
+    global NET, BATCH
+    NET = args.net
+    BATCH = CONFIG_BATCH[NET]
 
 
 def load_peaks():
@@ -97,10 +105,10 @@ def parse_clocks(path):
 
 
 # ------------------------------------------------------------------ CPU arms
-def cpu_oracle_rate(batch, steps, warmup, threads):
+def cpu_oracle_rate(batch, steps, warmup, threads, name=None):
     from oracle.oracle import Oracle
     from paper_1701_02284_b200.network import compile_network
-    net = compile_network(NET, batch)
+    net = compile_network(name or NET, batch)
     o = Oracle(net, seed=SEED, threads=threads)
     o.init_params()
     for it in range(warmup):
@@ -297,7 +305,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--net", default=NET, choices=["alexnet", "vgg16", "googlenet", "resnet50", "lenet"],
+                    help="workload (default: BASELINE.json configs[1], AlexNet b128)")
     args = ap.parse_args()
+    set_workload(args)
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)

@@ -196,9 +196,19 @@ static int pick_bn(int N) {
     return best;
 }
 
+// TCB_FORCE_BN=64|128|256 pins the tile width (kernel experiments / A-B comparisons).
+static int forced_bn() {
+    static const int v = [] {
+        const char* e = std::getenv("TCB_FORCE_BN");
+        const int b = e ? std::atoi(e) : 0;
+        return (b == 64 || b == 128 || b == 256) ? b : 0;
+    }();
+    return v;
+}
+
 static LaunchPlan plan_launch(int M, int N, int K, int splits_req) {
     LaunchPlan lp;
-    lp.bn = pick_bn(N);
+    lp.bn = forced_bn() ? forced_bn() : pick_bn(N);
     lp.num_kb = std::max(1, ceil_div(K, BK));
     const int tiles = ceil_div(M, BM) * ceil_div(N, lp.bn);
     int splits = splits_req;

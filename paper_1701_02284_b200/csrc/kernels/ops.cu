@@ -110,8 +110,12 @@ __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, 
 }
 
 // ---------------------------------------------------------------- pooling (NHWC, 8 channels per thread)
+// Max pooling stores the argmax as a 1-byte window-local position r*k + s (255 =
+// empty window); the flat NCHW index the reference reports is
+// reconstructed from it on download (tc_pool_indices_download), so the index
+// stream costs 1 B per output instead of 4.
 __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
-                           int32_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
+                           uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
     const int cg = xi.cs / 8;
     const long long total = yo.pixels() * cg;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
@@ -128,8 +132,9 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
         for (int j = 0; j < 8; ++j) {
             best[j] = 0.f;
             sum[j] = 0.f;
-            bi[j] = -1;
+            bi[j] = 255;
         }
+        const bf16* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
         for (int r = 0; r < k; ++r) {
             const int ih = oh * stride - pad + r;
             if (ih < 0 || ih >= xi.H) continue;
@@ -137,13 +142,13 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
                 const int iw = ow * stride - pad + s;
                 if (iw < 0 || iw >= xi.W) continue;
                 float f[8];
-                unpack8(*reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8), f);
+                unpack8(__ldg(reinterpret_cast<const uint4*>(img + (static_cast<long long>(ih) * xi.W + iw) * xi.cs)), f);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     sum[j] += f[j];
-                    if (bi[j] < 0 || f[j] > best[j]) {  // first maximum in row-major window order
+                    if (bi[j] == 255 || f[j] > best[j]) {  // first maximum in row-major window order
                         best[j] = f[j];
-                        bi[j] = ih * xi.W + iw;
+                        bi[j] = r * k + s;
                     }
                 }
             }
@@ -155,20 +160,19 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
         for (int j = 0; j < 8; ++j) out[j] = is_max ? best[j] : sum[j] * inv;
         *reinterpret_cast<uint4*>(y + o) = pack8(out);
         if (idx) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int c = g * 8 + j;
-                // flat NCHW input index: layout independent, compared bit-exactly with the oracle
-                idx[o + j] = (c < xi.C && bi[j] >= 0)
-                                 ? static_cast<int32_t>((static_cast<long long>(n) * xi.C + c) * xi.H * xi.W + bi[j])
-                                 : -1;
-            }
+            uint2 q;
+            q.x = static_cast<uint32_t>(bi[0]) | static_cast<uint32_t>(bi[1]) << 8 | static_cast<uint32_t>(bi[2]) << 16 |
+                  static_cast<uint32_t>(bi[3]) << 24;
+            q.y = static_cast<uint32_t>(bi[4]) | static_cast<uint32_t>(bi[5]) << 8 | static_cast<uint32_t>(bi[6]) << 16 |
+                  static_cast<uint32_t>(bi[7]) << 24;
+            *reinterpret_cast<uint2*>(idx + o) = q;
         }
     }
 }
 
-// Gather formulation: each input element sums the windows that selected it.
-__global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const int32_t* __restrict__ idx,
+// Gather formulation: each input element sums the windows that selected it
+// (no atomics; fixed window order, deterministic).
+__global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
                            bf16* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
     const int cg = xi.cs / 8;
     const long long total = xi.pixels() * cg;
@@ -189,17 +193,19 @@ __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const int32_t* 
         float acc[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        const long long obase = static_cast<long long>(n) * yo.H * yo.W * yo.cs + g * 8;
         for (int oh = oh0; oh <= oh1; ++oh)
             for (int ow = ow0; ow <= ow1; ++ow) {
-                const long long o = ((static_cast<long long>(n) * yo.H + oh) * yo.W + ow) * yo.cs + g * 8;
+                const long long o = obase + (static_cast<long long>(oh) * yo.W + ow) * yo.cs;
                 float d[8];
-                unpack8(*reinterpret_cast<const uint4*>(dy + o), d);
+                unpack8(__ldg(reinterpret_cast<const uint4*>(dy + o)), d);
                 if (is_max) {
+                    const uint32_t me = static_cast<uint32_t>((ih - (oh * stride - pad)) * k + (iw - (ow * stride - pad)));
+                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(idx + o));
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int c = g * 8 + j;
-                        const int me = static_cast<int>((static_cast<long long>(n) * xi.C + c) * xi.H * xi.W + ih * xi.W + iw);
-                        if (c < xi.C && idx[o + j] == me) acc[j] += d[j];
+                        const uint32_t w = ((j < 4 ? q.x : q.y) >> (8 * (j & 3))) & 0xFFu;
+                        if (w == me) acc[j] += d[j];
                     }
                 } else {
 #pragma unroll
@@ -340,97 +346,227 @@ struct LossArgs {
 };
 
 // One block, fixed strided partition + fixed tree: deterministic.
-__global__ void k_loss(LossArgs args, float* out) {
-    __shared__ double red[1024];
+// Deterministic two-level reduction in one launch: kLossBlocks blocks write fp64
+// partials; the last block to finish (ticket counter) sums them in block order and
+// resets the counter for the next step (graph replays).
+constexpr int kLossBlocks = 32;
+__global__ void __launch_bounds__(256) k_loss(LossArgs args, float* out, double* partial, unsigned* ticket) {
+    __shared__ double red[256];
+    __shared__ bool last;
     double acc = 0.0;
     for (int t = 0; t < args.nterms; ++t) {
         double s = 0.0;
-        for (long long i = threadIdx.x; i < args.n[t]; i += blockDim.x)
+        for (long long i = blockIdx.x * 256ll + threadIdx.x; i < args.n[t]; i += 256ll * gridDim.x)
             s += static_cast<double>(args.a[t][i]) * static_cast<double>(args.b[t][i]);
         acc += args.coef[t] * s;
     }
     red[threadIdx.x] = acc;
     __syncthreads();
-    for (int s = blockDim.x / 2; s; s >>= 1) {
+    for (int s = 128; s; s >>= 1) {
         if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = static_cast<float>(red[0]);
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x] = red[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (int b = 0; b < static_cast<int>(gridDim.x); ++b) tot += static_cast<volatile double*>(partial)[b];
+        *out = static_cast<float>(tot);
+        *ticket = 0;
+    }
 }
 
-// ---------------------------------------------------------------- column reductions
-// Stage 1: block b sums rows [b*rpb, (b+1)*rpb) for every column, 8 columns per thread.
-__global__ void k_colsum_partial(const bf16* __restrict__ x, long long rows, int cols, long long ld, long long rpb,
-                                 float* __restrict__ part, const float* __restrict__ center, int mode) {
-    // mode 0: sum x ; mode 1: sum (x - center)^2
-    extern __shared__ float sm[];
-    const int tpr = (cols + 7) / 8;             // threads per row
-    const int rpi = max(1, blockDim.x / tpr);   // rows per iteration
-    const int tr = threadIdx.x / tpr, tc = threadIdx.x % tpr;
-    float acc[8];
+// ---------------------------------------------------------------- channel reductions
+// Column (channel) sums over the rows (pixels) of an NHWC / [rows][ld] bf16 matrix.
+// Stage 1: grid (channel tiles, row splits); each thread owns 8 channels (one
+// 16-byte load per row) and strides over its split's rows; the row slots of a
+// block are combined in shared memory in a fixed order and written as one partial
+// per (split, channel).  Stage 2 sums the partials of a channel in split order.
+// Deterministic for a fixed shape (the partition depends only on rows / ld).
+//   RED_SUM   a = sum x
+//   RED_STATS a = sum (x - x0), b = sum (x - x0)^2   (x0 = row 0: shifted single pass)
+//   RED_BNBWD a = sum dy,       b = sum dy * (x - mean) * istd
+enum RedMode { RED_SUM = 0, RED_STATS = 1, RED_BNBWD = 2 };
+constexpr int kRedThreads = 256;
+
+struct RedPlan {
+    int ct;        // channels per tile (multiple of 8, <= 512)
+    int tiles;     // channel tiles
+    int splits;    // row splits
+    long long rps; // rows per split
+};
+
+RedPlan red_plan(long long rows, int ld) {
+    RedPlan r;
+    r.ct = std::min(ld, 512);
+    r.tiles = (ld + r.ct - 1) / r.ct;
+    const int rpi = kRedThreads / (r.ct / 8);
+    const long long target = static_cast<long long>(num_sms()) * 4;
+    long long sp = std::max<long long>(1, target / r.tiles);
+    sp = std::min<long long>(sp, std::max<long long>(1, rows / (4LL * rpi)));  // >= 4 row iterations per thread
+    sp = std::min<long long>(sp, 1024);
+    r.rps = (rows + sp - 1) / sp;
+    r.splits = static_cast<int>((rows + r.rps - 1) / r.rps);
+    return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restrict__ x, const bf16* __restrict__ x2,
+                                                             const float* __restrict__ stats, long long rows, int C,
+                                                             int ld, int ct, long long rps, int splits,
+                                                             float* __restrict__ part) {
+    __shared__ __align__(16) float sm[(MODE == RED_SUM ? 1 : 2) * kRedThreads * 8];
+    const int tpr = ct >> 3;
+    const int rpi = kRedThreads / tpr;
+    const int tr = threadIdx.x / tpr, tc = threadIdx.x - tr * tpr;
+    const int c0 = blockIdx.x * ct + tc * 8;
+    float a[8], b[8], m[8], is[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    const long long r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
-    if (tr < rpi) {
+    for (int j = 0; j < 8; ++j) a[j] = b[j] = m[j] = is[j] = 0.f;
+    const bool live = tr < rpi && c0 < ld;
+    if (live) {
+        if (MODE == RED_STATS) {
+            unpack8(*reinterpret_cast<const uint4*>(x + c0), m);
+        } else if (MODE == RED_BNBWD) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = min(c0 + j, C - 1);
+                m[j] = stats[c];
+                is[j] = stats[C + c];
+            }
+        }
+        const long long r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
+        const bf16* px = x + r0 * ld + c0;
+        const bf16* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
         for (long long r = r0 + tr; r < r1; r += rpi) {
+            const long long o = (r - r0) * ld;
             float f[8];
-            unpack8(*reinterpret_cast<const uint4*>(x + r * ld + tc * 8), f);
-            if (mode == 1) {
+            unpack8(__ldcs(reinterpret_cast<const uint4*>(px + o)), f);
+            if (MODE == RED_SUM) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[j] += f[j];
+            } else if (MODE == RED_STATS) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int c = tc * 8 + j;
-                    const float d = f[j] - (c < cols ? center[c] : 0.f);
-                    f[j] = d * d;
+                    const float d = f[j] - m[j];
+                    a[j] += d;
+                    b[j] = fmaf(d, d, b[j]);
+                }
+            } else {
+                float g[8];
+                unpack8(__ldcs(reinterpret_cast<const uint4*>(p2 + o)), g);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    a[j] += f[j];
+                    b[j] = fmaf(f[j], (g[j] - m[j]) * is[j], b[j]);
                 }
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += f[j];
         }
     }
-    // reduce over the rpi row-slots in a fixed order
-    const int width = tpr * 8;
-    for (int i = threadIdx.x; i < rpi * width; i += blockDim.x) sm[i] = 0.f;
+    // row-slot tr, channel offset tc*8 within the tile: sm[tr][ct]
+    if (tr < rpi) {
+        float4* d = reinterpret_cast<float4*>(sm + tr * ct + tc * 8);
+        d[0] = make_float4(a[0], a[1], a[2], a[3]);
+        d[1] = make_float4(a[4], a[5], a[6], a[7]);
+        if (MODE != RED_SUM) {
+            float4* e = reinterpret_cast<float4*>(sm + kRedThreads * 8 + tr * ct + tc * 8);
+            e[0] = make_float4(b[0], b[1], b[2], b[3]);
+            e[1] = make_float4(b[4], b[5], b[6], b[7]);
+        }
+    }
     __syncthreads();
-    if (tr < rpi)
+    for (int cc = threadIdx.x; cc < ct; cc += kRedThreads) {
+        const int c = blockIdx.x * ct + cc;
+        if (c >= C) continue;
+        float sa = 0.f, sb = 0.f;
+        for (int q = 0; q < rpi; ++q) {
+            sa += sm[q * ct + cc];
+            if (MODE != RED_SUM) sb += sm[kRedThreads * 8 + q * ct + cc];
+        }
+        part[static_cast<long long>(blockIdx.y) * C + c] = sa;
+        if (MODE != RED_SUM) part[static_cast<long long>(splits + blockIdx.y) * C + c] = sb;
+    }
+}
+
+// Stage 2.  RED_SUM: out[c] = scale * sum.  RED_STATS: stats = (mean, istd), coef =
+// (gamma * istd, beta - mean * gamma * istd).  RED_BNBWD: out = (sum dy, sum dy*xhat).
+template <int MODE>
+__global__ void k_chan_final(const float* __restrict__ part, int splits, int C, float scale, float* __restrict__ out,
+                             const bf16* __restrict__ x, long long rows, float eps, const float* __restrict__ gamma,
+                             const float* __restrict__ beta, float* __restrict__ coef) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+        float sa = 0.f, sb = 0.f;
+        for (int q = 0; q < splits; ++q) {
+            sa += part[static_cast<long long>(q) * C + c];
+            if (MODE != RED_SUM) sb += part[static_cast<long long>(splits + q) * C + c];
+        }
+        if (MODE == RED_SUM) {
+            out[c] = sa * scale;
+        } else if (MODE == RED_STATS) {
+            const float inv = 1.f / static_cast<float>(rows);
+            const float m1 = sa * inv;
+            const float mean = __bfloat162float(x[c]) + m1;
+            const float var = fmaxf(sb * inv - m1 * m1, 0.f);
+            const float istd = rsqrtf(var + eps);
+            out[c] = mean;
+            out[C + c] = istd;
+            const float g = gamma[c] * istd;
+            coef[c] = g;
+            coef[C + c] = beta[c] - mean * g;
+        } else {
+            out[c] = sa;
+            out[C + c] = sb;
+        }
+    }
+}
+
+// y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
+__global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restrict__ coef, uint4* __restrict__ y,
+                              long long n8, int ld8, int C) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c0 = static_cast<int>(i % ld8) * 8;
+        float f[8];
+        unpack8(__ldcs(x + i), f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sm[tr * width + tc * 8 + j] = acc[j];
-    __syncthreads();
-    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-        float s = 0.f;
-        for (int q = 0; q < rpi; ++q) s += sm[q * width + c];
-        part[blockIdx.x * static_cast<long long>(cols) + c] = s;
+        for (int j = 0; j < 8; ++j) f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
+        y[i] = pack8(f);
     }
 }
 
-__global__ void k_colsum_final(const float* __restrict__ part, int nparts, int cols, float* __restrict__ out, float scale) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int b = 0; b < nparts; ++b) s += part[b * static_cast<long long>(cols) + c];
-        out[c] = s * scale;
+// dx = gamma*istd*(dy - sum(dy)/M - xhat*sum(dy*xhat)/M) = k1*dy + k2*x + k3 (per channel)
+__global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __restrict__ stats,
+                              const float* __restrict__ sums, float* __restrict__ k, int C, float invm) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const float is = stats[C + c], mean = stats[c];
+    const float g = gamma[c] * is;
+    const float t = sums[C + c] * invm * is;  // sum(dy*xhat)/M * istd
+    k[c] = g;
+    k[C + c] = -g * t;
+    k[2 * C + c] = -g * sums[c] * invm + g * t * mean;
+}
+
+__global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ k,
+                               uint4* __restrict__ dx, long long n8, int ld8, int C) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c0 = static_cast<int>(i % ld8) * 8;
+        float f[8], g[8];
+        unpack8(__ldcs(dy + i), f);
+        unpack8(__ldcs(x + i), g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = c0 + j;
+            f[j] = c < C ? fmaf(__ldg(k + c), f[j], fmaf(__ldg(k + C + c), g[j], __ldg(k + 2 * C + c))) : 0.f;
+        }
+        dx[i] = pack8(f);
     }
-}
-
-int colsum_blocks(long long rows, int cols, int max_partials) {
-    const long long by_rows = (rows + 255) / 256;
-    long long b = std::min<long long>(by_rows, static_cast<long long>(num_sms()) * 4);
-    b = std::min<long long>(b, std::max(1, max_partials / std::max(1, cols)));
-    return static_cast<int>(std::max<long long>(1, b));
-}
-
-tc_status colsum_run(const bf16* x, long long rows, int cols, long long ld, float* out, float* partials, int max_partials,
-                     const float* center, int mode, float scale, cudaStream_t st) {
-    if ((ld & 7) || (reinterpret_cast<uintptr_t>(x) & 15)) return fail(TC_INVALID_ARG, "colsum: misaligned operand");
-    const int nb = colsum_blocks(rows, cols, max_partials);
-    const long long rpb = (rows + nb - 1) / nb;
-    const int tpr = (cols + 7) / 8;
-    const int threads = std::min(1024, std::max(kThreads, ((tpr + 31) / 32) * 32));
-    const int rpi = std::max(1, threads / tpr);
-    const size_t smem = static_cast<size_t>(rpi) * tpr * 8 * sizeof(float);
-    k_colsum_partial<<<nb, threads, smem, st>>>(x, rows, cols, ld, rpb, partials, center, mode);
-    TCB_LAUNCH_CHECK();
-    k_colsum_final<<<(cols + 255) / 256, 256, 0, st>>>(partials, nb, cols, out, scale);
-    TCB_LAUNCH_CHECK();
-    return TC_OK;
 }
 
 __global__ void k_bias_add(const bf16* __restrict__ x, const float* __restrict__ b, bf16* __restrict__ y, long long rows,
@@ -453,60 +589,6 @@ __global__ void k_channel_copy(const bf16* __restrict__ src, int src_cs, bf16* _
         const long long p = i / c;
         const int ch = static_cast<int>(i - p * c);
         dst[p * dst_cs + off + ch] = src[p * src_cs + ch];
-    }
-}
-
-// ---------------------------------------------------------------- batch norm
-__global__ void k_bn_finish_stats(const float* __restrict__ mean, const float* __restrict__ var, float* stats, int C,
-                                  float eps) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < C) {
-        stats[c] = mean[c];
-        stats[C + c] = rsqrtf(var[c] + eps);
-    }
-}
-
-__global__ void k_bn_apply(const bf16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
-                           const float* __restrict__ stats, bf16* __restrict__ y, long long pixels, int C, int cs) {
-    const long long total = pixels * cs;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % cs);
-        float v = 0.f;
-        if (c < C) v = gamma[c] * (__bfloat162float(x[i]) - stats[c]) * stats[C + c] + beta[c];
-        y[i] = __float2bfloat16_rn(v);
-    }
-}
-
-// dx = g*istd*(dy - sum(dy)/M - xhat*sum(dy*xhat)/M)
-__global__ void k_bn_bwd_apply(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
-                               const float* __restrict__ stats, const float* __restrict__ sdy,
-                               const float* __restrict__ sdyx, bf16* __restrict__ dx, long long pixels, int C, int cs) {
-    const long long total = pixels * cs;
-    const float invm = 1.f / static_cast<float>(pixels);
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % cs);
-        float v = 0.f;
-        if (c < C) {
-            const float is = stats[C + c];
-            const float xh = (__bfloat162float(x[i]) - stats[c]) * is;
-            v = gamma[c] * is * (__bfloat162float(dy[i]) - sdy[c] * invm - xh * sdyx[c] * invm);
-        }
-        dx[i] = __float2bfloat16_rn(v);
-    }
-}
-
-// sum(dy * xhat) per channel, partial stage (fixed partition)
-__global__ void k_bn_dyx_partial(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ stats,
-                                 long long pixels, int C, int cs, long long rpb, float* __restrict__ part) {
-    const long long r0 = blockIdx.x * rpb, r1 = min(pixels, r0 + rpb);
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        float s = 0.f;
-        const float m = stats[c], is = stats[C + c];
-        for (long long r = r0; r < r1; ++r)
-            s += __bfloat162float(dy[r * cs + c]) * (__bfloat162float(x[r * cs + c]) - m) * is;
-        part[blockIdx.x * static_cast<long long>(C) + c] = s;
     }
 }
 
@@ -670,22 +752,76 @@ __global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, int 
 }
 
 // ---------------------------------------------------------------- SGD
-__global__ void k_sgd(SgdTensor t) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < t.n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const float p = t.p[i];
-        const float v = t.momentum * t.v[i] + t.lr_alpha * (t.g[i] + t.decay * p);
-        const float np = p + v;
-        t.v[i] = v;
-        t.p[i] = np;
-        const bf16 b = __float2bfloat16_rn(np);
-        if (t.shadow) t.shadow[i] = b;
-        if (t.shadow_rskc) {
-            const int c = static_cast<int>(i % t.cs);
-            const long long q = i / t.cs;
-            const int rs = static_cast<int>(q % t.RS);
-            const int k = static_cast<int>(q / t.RS);
-            t.shadow_rskc[(static_cast<long long>(rs) * t.ks + k) * t.cs + c] = b;
+__global__ void k_set_iter(uint32_t* d, uint32_t iter, uint32_t n0) {
+    d[0] = iter;
+    d[1] = n0;
+}
+
+// Multi-tensor momentum SGD: one launch updates a whole gradient bucket.  Work is
+// split into 4-element units (float4 p / v / g, 8-byte bf16 shadow stores); unit u
+// belongs to the tensor whose prefix range [start4[t], start4[t+1]) holds it.
+constexpr int kMaxSgd = 48;
+struct SgdBatch {
+    SgdTensor t[kMaxSgd];
+    long long start4[kMaxSgd + 1];
+    int nt;
+};
+
+__device__ __forceinline__ void sgd_scalar(const SgdTensor& t, long long i) {
+    const float p = t.p[i];
+    const float v = t.momentum * t.v[i] + t.lr_alpha * (t.g[i] + t.decay * p);
+    const float np = p + v;
+    t.v[i] = v;
+    t.p[i] = np;
+    const bf16 b = __float2bfloat16_rn(np);
+    if (t.shadow) t.shadow[i] = b;
+    if (t.shadow_rskc) {
+        const int c = static_cast<int>(i % t.cs);
+        const long long q = i / t.cs;
+        const int rs = static_cast<int>(q % t.RS);
+        const int k = static_cast<int>(q / t.RS);
+        t.shadow_rskc[(static_cast<long long>(rs) * t.ks + k) * t.cs + c] = b;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b) {
+    const long long total = b.start4[b.nt];
+    for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < total;
+         u += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = b.nt - 1;  // last t with start4[t] <= u
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (b.start4[mid] <= u) lo = mid; else hi = mid - 1;
+        }
+        const SgdTensor& t = b.t[lo];
+        const long long i = (u - b.start4[lo]) * 4;
+        if (i + 4 > t.n) {
+            for (long long j = i; j < t.n; ++j) sgd_scalar(t, j);
+            continue;
+        }
+        const float4 p = *reinterpret_cast<const float4*>(t.p + i);
+        const float4 g = __ldcs(reinterpret_cast<const float4*>(t.g + i));
+        float4 v = *reinterpret_cast<const float4*>(t.v + i);
+        v.x = t.momentum * v.x + t.lr_alpha * (g.x + t.decay * p.x);
+        v.y = t.momentum * v.y + t.lr_alpha * (g.y + t.decay * p.y);
+        v.z = t.momentum * v.z + t.lr_alpha * (g.z + t.decay * p.z);
+        v.w = t.momentum * v.w + t.lr_alpha * (g.w + t.decay * p.w);
+        const float4 np = make_float4(p.x + v.x, p.y + v.y, p.z + v.z, p.w + v.w);
+        *reinterpret_cast<float4*>(t.v + i) = v;
+        *reinterpret_cast<float4*>(t.p + i) = np;
+        if (t.shadow || t.shadow_rskc) {
+            uint2 h;
+            h.x = pack_bf16x2(np.x, np.y);
+            h.y = pack_bf16x2(np.z, np.w);
+            if (t.shadow) *reinterpret_cast<uint2*>(t.shadow + i) = h;
+            if (t.shadow_rskc) {  // 4 consecutive channels share (k, rs): cs is a multiple of 8 here
+                const unsigned ui = static_cast<unsigned>(i);
+                const unsigned c = ui % static_cast<unsigned>(t.cs);
+                const unsigned q = ui / static_cast<unsigned>(t.cs);
+                const unsigned rs = q % static_cast<unsigned>(t.RS);
+                const unsigned k = q / static_cast<unsigned>(t.RS);
+                *reinterpret_cast<uint2*>(t.shadow_rskc + (static_cast<long long>(rs) * t.ks + k) * t.cs + c) = h;
+            }
         }
     }
 }
@@ -725,13 +861,14 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, int32_t* idx, int k, int stride, int pad,
+tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
+    if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
     k_pool_fwd<<<EW_GRID(yo.pixels() * (xi.cs / 8))>>>(x, xi, y, yo, idx, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const int32_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
+tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
     k_pool_bwd<<<EW_GRID(xi.pixels() * (xi.cs / 8))>>>(dy, yo, idx, dx, xi, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
@@ -809,14 +946,44 @@ tc_status launch_loss(const float* const* a, const float* const* b, const long l
         args.n[t] = n[t];
         args.coef[t] = coef[t];
     }
-    k_loss<<<1, 1024, 0, st>>>(args, out);
+    // out[0] = loss; out + 16 holds kLossBlocks fp64 partials, then the ticket counter (zero-initialised)
+    double* partial = reinterpret_cast<double*>(out + 16);
+    unsigned* ticket = reinterpret_cast<unsigned*>(partial + kLossBlocks);
+    k_loss<<<kLossBlocks, 256, 0, st>>>(args, out, partial, ticket);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-size_t colsum_partials_floats(int cols) { return static_cast<size_t>(num_sms()) * 4 * std::max(cols, 8) + 64; }
+size_t colsum_partials_floats(int cols) {
+    // 2 accumulators x splits x C, with splits * tiles <= 4 * SMs and ct >= min(C, 512)
+    const int ld = std::max(8, (cols + 7) / 8 * 8);
+    const int tiles = (ld + 511) / 512;
+    return 2ull * (static_cast<size_t>(num_sms()) * 4 / tiles + 1) * ld + 3ull * ld + 64;
+}
+
+template <int MODE>
+static tc_status chan_reduce(const bf16* x, const bf16* x2, const float* stats, long long rows, int C, long long ld,
+                             float* part, int max_partials, cudaStream_t st, RedPlan* out_plan) {
+    if ((ld & 7) || (reinterpret_cast<uintptr_t>(x) & 15) || (x2 && (reinterpret_cast<uintptr_t>(x2) & 15)))
+        return fail(TC_INVALID_ARG, "channel reduction: misaligned operand");
+    RedPlan rp = red_plan(rows, static_cast<int>(ld));
+    if (2ll * rp.splits * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
+    dim3 grid(rp.tiles, rp.splits);
+    k_chan_reduce<MODE><<<grid, kRedThreads, 0, st>>>(x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
+                                                      rp.splits, part);
+    TCB_LAUNCH_CHECK();
+    *out_plan = rp;
+    return TC_OK;
+}
+
 tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, float* out, float* partials,
                         int max_partials, cudaStream_t st) {
-    return colsum_run(x, rows, cols, ld, out, partials, max_partials, nullptr, 0, 1.f, st);
+    RedPlan rp;
+    tc_status s = chan_reduce<RED_SUM>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
+    if (s != TC_OK) return s;
+    k_chan_final<RED_SUM><<<(cols + 255) / 256, 256, 0, st>>>(partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
+                                                               nullptr, nullptr, nullptr);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
 }
 tc_status launch_bias_add(const bf16* x, const float* b, bf16* y, long long rows, int cols, long long ld, int relu,
                           cudaStream_t st) {
@@ -837,39 +1004,40 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st) {
 
 tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
                         int C, int cs, float eps, float* partials, int max_partials, cudaStream_t st) {
-    // two-pass statistics: mean, then mean of squared deviations (biased variance)
-    float* mean = partials + max_partials;  // caller sizes partials to max_partials + 2*C
-    float* var = mean + C;
-    tc_status s = colsum_run(x, pixels, C, cs, mean, partials, max_partials, nullptr, 0, 1.f / pixels, st);
+    RedPlan rp;
+    float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
+    tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    s = colsum_run(x, pixels, C, cs, var, partials, max_partials, mean, 1, 1.f / pixels, st);
-    if (s != TC_OK) return s;
-    k_bn_finish_stats<<<(C + 255) / 256, 256, 0, st>>>(mean, var, stats, C, eps);
+    k_chan_final<RED_STATS><<<(C + 255) / 256, 256, 0, st>>>(partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+                                                              beta, coef);
     TCB_LAUNCH_CHECK();
-    k_bn_apply<<<EW_GRID(pixels * cs)>>>(x, gamma, beta, stats, y, pixels, C, cs);
+    const long long n8 = pixels * cs / 8;
+    k_chan_affine<<<EW_GRID(n8)>>>(reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
-tc_status launch_bn_bwd(const bf16* dy, const bf16* x, const float* gamma, const float* stats, bf16* dx, float* dgamma,
-                        float* dbeta, long long pixels, int C, int cs, float* partials, int max_partials,
-                        cudaStream_t st) {
-    float* sdy = partials + max_partials;
-    float* sdyx = sdy + C;
-    tc_status s = colsum_run(dy, pixels, C, cs, sdy, partials, max_partials, nullptr, 0, 1.f, st);
+tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats, float* sums, long long pixels, int C,
+                               int cs, float* partials, int max_partials, cudaStream_t st) {
+    RedPlan rp;
+    tc_status s = chan_reduce<RED_BNBWD>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    const int nb = colsum_blocks(pixels, C, max_partials);
-    const long long rpb = (pixels + nb - 1) / nb;
-    k_bn_dyx_partial<<<nb, 256, 0, st>>>(dy, x, stats, pixels, C, cs, rpb, partials);
+    k_chan_final<RED_BNBWD><<<(C + 255) / 256, 256, 0, st>>>(partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
+                                                              nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
-    k_colsum_final<<<(C + 255) / 256, 256, 0, st>>>(partials, nb, C, sdyx, 1.f);
+    return TC_OK;
+}
+
+tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma, const float* stats, const float* sums,
+                              bf16* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+                              cudaStream_t st) {
+    float* k = partials + max_partials;
+    k_bn_coef_bwd<<<(C + 255) / 256, 256, 0, st>>>(gamma, stats, sums, k, C, 1.f / static_cast<float>(pixels));
     TCB_LAUNCH_CHECK();
-    if (dgamma) TCB_CUDA_CHECK(cudaMemcpyAsync(dgamma, sdyx, C * sizeof(float), cudaMemcpyDeviceToDevice, st));
-    if (dbeta) TCB_CUDA_CHECK(cudaMemcpyAsync(dbeta, sdy, C * sizeof(float), cudaMemcpyDeviceToDevice, st));
-    if (dx) {
-        k_bn_bwd_apply<<<EW_GRID(pixels * cs)>>>(dy, x, gamma, stats, sdy, sdyx, dx, pixels, C, cs);
-        TCB_LAUNCH_CHECK();
-    }
+    const long long n8 = pixels * cs / 8;
+    k_bn_bwd_apply<<<EW_GRID(n8)>>>(reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), k,
+                                     reinterpret_cast<uint4*>(dx), n8, cs / 8, C);
+    TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
@@ -885,10 +1053,28 @@ tc_status launch_synth_batch(bf16* x, int32_t* labels, int N, int C, int H, int 
     return TC_OK;
 }
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
-    for (int i = 0; i < nt; ++i) {
-        k_sgd<<<EW_GRID(ts[i].n)>>>(ts[i]);
+    for (int base = 0; base < nt; base += kMaxSgd) {
+        SgdBatch b;
+        b.nt = std::min(kMaxSgd, nt - base);
+        b.start4[0] = 0;
+        for (int i = 0; i < b.nt; ++i) {
+            const SgdTensor& t = ts[base + i];
+            if ((reinterpret_cast<uintptr_t>(t.p) | reinterpret_cast<uintptr_t>(t.v) | reinterpret_cast<uintptr_t>(t.g)) & 15)
+                return fail(TC_INVALID_ARG, "sgd: p / v / g must be 16-byte aligned");
+            if (t.shadow_rskc && (t.cs % 4 || t.n >= (1ll << 31)))
+                return fail(TC_INVALID_ARG, "sgd: RSKC shadow needs cs % 4 == 0 and n < 2^31");
+            b.t[i] = t;
+            b.start4[i + 1] = b.start4[i] + (t.n + 3) / 4;
+        }
+        k_sgd<<<grid_for(b.start4[b.nt]), kThreads, 0, st>>>(b);
         TCB_LAUNCH_CHECK();
     }
+    return TC_OK;
+}
+
+tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st) {
+    k_set_iter<<<1, 1, 0, st>>>(d_iter, iter, n0);
+    TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 

@@ -32,9 +32,10 @@ tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16*
 tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st);
 
-tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, int32_t* idx, int k, int stride, int pad,
+// Max pooling argmax: 1 byte per output element, window-local position r*k + s (255 = empty).
+tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
                           int is_max, cudaStream_t st);
-tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const int32_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
+tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st);
 tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st);
 tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
@@ -49,7 +50,8 @@ tc_status launch_softmax_bwd(const float* dy, const float* y, bf16* dx, long lon
 enum F32Op { F32_LOG = 0, F32_RECIP = 1, F32_SCALE = 2, F32_MUL = 3, F32_ADD = 4 };
 tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st);
 tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st);
-// loss = sum_t coef[t] * dot(a[t], b[t]) over n[t] elements -> *out (fp32 device scalar)
+// loss = sum_t coef[t] * dot(a[t], b[t]) over n[t] elements -> *out (fp32 device scalar).
+// `out` must point at >= 512 zero-initialised bytes (reduction partials + ticket follow the scalar).
 tc_status launch_loss(const float* const* a, const float* const* b, const long long* n, const double* coef, int nterms,
                       float* out, cudaStream_t st);
 
@@ -65,13 +67,17 @@ tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs
                               cudaStream_t st);
 tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 
-// BatchNorm over NHWC [pixels][cs]: stats (mean, inv_std) per channel.
+// BatchNorm over NHWC [pixels][cs] (training-mode batch statistics, biased variance):
+// stats = (mean[C], istd[C]); y = gamma * (x - mean) * istd + beta.
+// `partials` holds max_partials floats of reduction scratch plus 3*C coefficient floats.
 tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
                         int C, int cs, float eps, float* partials, int max_partials, cudaStream_t st);
-// dgamma/dbeta (may be null) and dx (may be null).
-tc_status launch_bn_bwd(const bf16* dy, const bf16* x, const float* gamma, const float* stats, bf16* dx, float* dgamma,
-                        float* dbeta, long long pixels, int C, int cs, float* partials, int max_partials,
-                        cudaStream_t st);
+// sums = (sum dy[C], sum dy * xhat[C]) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) and dx
+tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats, float* sums, long long pixels, int C,
+                               int cs, float* partials, int max_partials, cudaStream_t st);
+tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma, const float* stats, const float* sums,
+                              bf16* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+                              cudaStream_t st);
 
 // Dense im2col for small-channel (first-layer) convolutions: col[m][kk], m = (n, oh, ow),
 // kk = (kh, kw, c) over the REAL channels C, zero-padded to Kp (multiple of 8).
@@ -97,5 +103,8 @@ struct SgdTensor {
     float lr_alpha, momentum, decay;
 };
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaStream_t st);
+
+// d_iter[0] = iter, d_iter[1] = n0 (kernel arguments travel with the launch: no host sync)
+tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st);
 
 }  // namespace tcb

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -66,6 +67,7 @@ struct ParamL {
     // channel-stride-4 first-layer input whose taps are gathered 8 bytes at a time)
     int Kw = 0;
     int in_dev = 0;
+    int update_stmt = -1;  // the param's Update statement
     long long n = 0;  // device elements
     float* p = nullptr;
     float* v = nullptr;
@@ -95,9 +97,18 @@ struct tc_ctx {
     std::unordered_map<int, VarL> vars;
     std::vector<ParamL> params;
     std::unordered_map<int, int> storage_item;      // storage id -> item
-    std::unordered_map<int, int> pool_idx_item;     // pool output var -> item (int32 indices)
+    std::unordered_map<int, int> pool_idx_item;     // pool output var -> item (1-byte window-local argmax)
     std::unordered_map<int, int> bn_stats_item;     // BN input var -> item (2*C fp32)
     std::unordered_map<int, float> mask_rate;       // dropout mask var -> rate
+    // BatchNorm backward: the BETA / DATA / GAMMA statements of one BN share the
+    // reductions (sum dy, sum dy*xhat), computed once at the group's first statement
+    struct BnGroup {
+        int x_var = -1, up_var = -1, first = -1;
+        float* sums = nullptr;  // 2*C persistent floats
+    };
+    std::vector<BnGroup> bn_groups;
+    std::unordered_map<int, int> stmt_bn_group;     // BN_BWD_* stmt -> group
+    float* bn_sums = nullptr;
     std::vector<Item> items;
     std::vector<uint8_t> fused;                     // stmt folded into its producer
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
@@ -120,6 +131,23 @@ struct tc_ctx {
     float* h_loss = nullptr;     // pinned
     int input_cs = 8;
     size_t input_bytes = 0;
+
+    // gradient buckets (backward production order); all-reduce + fused momentum
+    // update run on comm_st, overlapped with the rest of the backward
+    struct Bucket {
+        int last_stmt = -1;      // Update statement that completes the bucket
+        size_t off = 0;          // float offset into grads
+        long long n = 0;         // floats (all-reduce count, includes alignment gaps)
+        std::vector<int> params;
+        cudaEvent_t ready = nullptr;
+    };
+    std::vector<Bucket> buckets;
+    std::vector<int> stmt_bucket;  // stmt -> bucket it completes, or -1
+    float* grads = nullptr;        // contiguous gradient region inside the slab
+    long long grads_n = 0;
+    cudaStream_t comm_st = nullptr;
+    cudaEvent_t join_ev = nullptr;
+    bool overlap = true;
 
     cudaGraph_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -388,7 +416,7 @@ tc_status plan_arena(tc_ctx* c) {
             Item it;
             it.first = i;
             it.last = i;
-            it.bytes = static_cast<size_t>(c->vars.at(s.var).elems()) * 4;
+            it.bytes = static_cast<size_t>(c->vars.at(s.var).elems());
             for (int j = i + 1; j < n; ++j)
                 if (p->stmts[j].op == TC_OP_POOL_BWD && p->stmts[j].in[1].kind == TC_REF_VAR &&
                     p->stmts[j].in[1].index == s.var)
@@ -549,8 +577,28 @@ tc_status run_gemm_args(tc_ctx* c, tc_gemm_args& a) {
     return tc_gemm_bf16(&a, c->st);
 }
 
+// (sum dy, sum dy*xhat) of the BN group of BN_BWD_* statement i; reduced at the group's first statement.
+tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
+    auto it = c->stmt_bn_group.find(i);
+    if (it == c->stmt_bn_group.end()) return fail(TC_INTERNAL, "runtime: BN backward statement without a group");
+    const tc_ctx::BnGroup& gr = c->bn_groups[it->second];
+    if (gr.first == i) {
+        Ptrs P{c};
+        const VarL& x = c->vars.at(gr.x_var);
+        const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
+        tc_status r = launch_bn_bwd_reduce(reinterpret_cast<const bf16*>(P.var(gr.up_var)),
+                                           reinterpret_cast<const bf16*>(P.var(x.id)), stats, gr.sums,
+                                           static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, c->partials,
+                                           c->max_partials, c->st);
+        if (r != TC_OK) return r;
+    }
+    *sums = gr.sums;
+    return TC_OK;
+}
+
 // Gradient op of an Update (or a parameter-shaped Let) into `g` (device param layout).
-tc_status compute_param_grad(tc_ctx* c, const tc_stmt& s, int pidx, float* g) {
+tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
+    const tc_stmt& s = c->plan->stmts[idx];
     Ptrs P{c};
     const ParamL& q = c->params[pidx];
     cudaStream_t st = c->st;
@@ -561,9 +609,17 @@ tc_status compute_param_grad(tc_ctx* c, const tc_stmt& s, int pidx, float* g) {
             tc_conv_desc d = conv_desc(x, q, dy, s);
             return tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
         }
+        case TC_OP_BN_BWD_BETA:
+        case TC_OP_BN_BWD_GAMMA: {
+            const float* sums = nullptr;
+            tc_status r = bn_group_sums(c, idx, &sums);
+            if (r != TC_OK) return r;
+            TCB_CUDA_CHECK(cudaMemcpyAsync(g, sums + (s.op == TC_OP_BN_BWD_GAMMA ? q.K : 0), q.K * sizeof(float),
+                                           cudaMemcpyDeviceToDevice, st));
+            return TC_OK;
+        }
         case TC_OP_CONV_BWD_BIAS:
-        case TC_OP_BIAS_GRAD:
-        case TC_OP_BN_BWD_BETA: {
+        case TC_OP_BIAS_GRAD: {
             const VarL& up = P.L(s.in[0]);
             return launch_colsum(reinterpret_cast<const bf16*>(P.var(up.id)), static_cast<long long>(up.N) * up.H * up.W,
                                  q.K, up.cs, g, c->partials, c->max_partials, st);
@@ -586,14 +642,6 @@ tc_status compute_param_grad(tc_ctx* c, const tc_stmt& s, int pidx, float* g) {
             ga.d_dtype = TC_DTYPE_F32;
             ga.alpha = 1.f;
             return run_gemm_args(c, ga);
-        }
-        case TC_OP_BN_BWD_GAMMA: {
-            const VarL& up = P.L(s.in[0]);
-            const VarL& x = P.L(s.in[1]);
-            const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
-            return launch_bn_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), reinterpret_cast<const bf16*>(P.var(x.id)),
-                                 nullptr, stats, nullptr, g, nullptr, static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs,
-                                 c->partials, c->max_partials, st);
         }
         default: break;
     }
@@ -624,14 +672,14 @@ tc_status exec_let(tc_ctx* c, int i) {
         }
         case TC_OP_POOL_FWD: {
             const VarL& x = P.L(s.in[0]);
-            int32_t* idx = s.max_pool ? reinterpret_cast<int32_t*>(c->arena + c->items[c->pool_idx_item.at(s.var)].off) : nullptr;
+            uint8_t* idx = s.max_pool ? reinterpret_cast<uint8_t*>(c->arena + c->items[c->pool_idx_item.at(s.var)].off) : nullptr;
             return launch_pool_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), x.act(), reinterpret_cast<bf16*>(y),
                                    out.act(), idx, s.k, s.stride, s.pad, s.max_pool, st);
         }
         case TC_OP_POOL_BWD: {
             const VarL& up = P.L(s.in[0]);
             const VarL& fy = P.L(s.in[1]);
-            const int32_t* idx = s.max_pool ? reinterpret_cast<int32_t*>(c->arena + c->items[c->pool_idx_item.at(fy.id)].off)
+            const uint8_t* idx = s.max_pool ? reinterpret_cast<uint8_t*>(c->arena + c->items[c->pool_idx_item.at(fy.id)].off)
                                             : nullptr;
             Act4 ya = fy.act();
             return launch_pool_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), ya, idx, reinterpret_cast<bf16*>(y),
@@ -782,9 +830,13 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& up = P.L(s.in[0]);
             const VarL& x = P.L(s.in[1]);
             const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
-            return launch_bn_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), reinterpret_cast<const bf16*>(P.var(x.id)),
-                                 c->params[s.in[2].index].p, stats, reinterpret_cast<bf16*>(y), nullptr, nullptr,
-                                 static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, c->partials, c->max_partials, st);
+            const float* sums = nullptr;
+            tc_status r = bn_group_sums(c, i, &sums);
+            if (r != TC_OK) return r;
+            return launch_bn_bwd_apply(reinterpret_cast<const bf16*>(P.var(up.id)),
+                                       reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[2].index].p, stats,
+                                       sums, reinterpret_cast<bf16*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C,
+                                       x.cs, c->partials, c->max_partials, st);
         }
         default: break;
     }
@@ -809,21 +861,14 @@ tc_status exec_stmt(tc_ctx* c, int i) {
         }
         return launch_loss(a, b, n, coef, s.nterms, c->d_loss, c->st);
     }
-    // Update: gradient -> (all-reduce) -> fused momentum SGD
+    // Update: the gradient only; all-reduce + momentum SGD run per bucket (flush_bucket)
     ParamL& q = c->params[s.param];
-    tc_status r = compute_param_grad(c, s, s.param, q.g);
-    if (r != TC_OK) return r;
-    if (c->comm) {
-        if (ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
-            return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
-    }
-    return TC_OK;
+    return compute_param_grad(c, i, s.param, q.g);
 }
 
-tc_status apply_update(tc_ctx* c, int i, int update) {
-    const tc_stmt& s = c->plan->stmts[i];
-    if (s.kind != TC_STMT_UPDATE || !update) return TC_OK;
-    ParamL& q = c->params[s.param];
+SgdTensor sgd_tensor(tc_ctx* c, int pidx) {
+    const ParamL& q = c->params[pidx];
+    const tc_stmt& s = c->plan->stmts[q.update_stmt];
     SgdTensor t{};
     t.p = q.p;
     t.v = q.v;
@@ -838,16 +883,43 @@ tc_status apply_update(tc_ctx* c, int i, int update) {
     t.lr_alpha = static_cast<float>(s.lr_alpha);
     t.momentum = static_cast<float>(s.momentum);
     t.decay = static_cast<float>(s.decay);
-    return launch_sgd(&t, 1, nullptr, c->st);
+    return t;
 }
 
-tc_status run_body(tc_ctx* c, int update) {
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
+// Gradient all-reduce (world > 1) and the fused multi-tensor momentum update of one
+// bucket.  With overlap, both run on comm_st after the bucket's last gradient: every
+// read of these parameters by the backward precedes their Update statements in the
+// plan (PAPER.md:292-293 ordering), hence precedes the event.
+tc_status flush_bucket(tc_ctx* c, int b, int update, bool overlap) {
+    tc_ctx::Bucket& bk = c->buckets[b];
+    cudaStream_t s2 = c->st;
+    if (overlap) {
+        TCB_CUDA_CHECK(cudaEventRecord(bk.ready, c->st));
+        TCB_CUDA_CHECK(cudaStreamWaitEvent(c->comm_st, bk.ready, 0));
+        s2 = c->comm_st;
+    }
+    if (c->comm && ncclAllReduce(c->grads + bk.off, c->grads + bk.off, bk.n, ncclFloat, ncclSum, c->comm, s2) != ncclSuccess)
+        return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
+    if (!update) return TC_OK;
+    std::vector<SgdTensor> ts;
+    for (int pidx : bk.params) ts.push_back(sgd_tensor(c, pidx));
+    return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+}
+
+tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
+    tc_status r = set_iter ? launch_set_iter(c->d_iter, c->h_iter[0], c->h_iter[1], c->st) : TC_OK;
+    if (r != TC_OK) return r;
     for (int i = 0; i < c->plan->nstmts; ++i) {
-        tc_status r = exec_stmt(c, i);
+        r = exec_stmt(c, i);
         if (r != TC_OK) return r;
-        r = apply_update(c, i, update);
-        if (r != TC_OK) return r;
+        if (c->stmt_bucket[i] >= 0) {
+            r = flush_bucket(c, c->stmt_bucket[i], update, overlap);
+            if (r != TC_OK) return r;
+        }
+    }
+    if (overlap) {
+        TCB_CUDA_CHECK(cudaEventRecord(c->join_ev, c->comm_st));
+        TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->join_ev, 0));
     }
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
     return TC_OK;
@@ -932,8 +1004,40 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     plan_fusion(c.get());
     r = plan_arena(c.get());
     if (r != TC_OK) return r;
-    // parameter slab
-    size_t slab = 0;
+    // gradient buckets: parameters in Update-statement order (backward production order)
+    std::vector<int> order;
+    for (int i = 0; i < plan->nstmts; ++i) {
+        const tc_stmt& s = plan->stmts[i];
+        if (s.kind != TC_STMT_UPDATE) continue;
+        ParamL& q = c->params.at(s.param);
+        if (q.update_stmt >= 0) return fail(TC_INTERNAL, "runtime: parameter with two Update statements");
+        q.update_stmt = i;
+        order.push_back(s.param);
+    }
+    for (size_t i = 0; i < c->params.size(); ++i)
+        if (c->params[i].update_stmt < 0) return fail(TC_INTERNAL, "runtime: parameter without an Update statement");
+    const char* bmb = std::getenv("TCB_BUCKET_MB");
+    const long long bucket_cap = static_cast<long long>((bmb ? std::atof(bmb) : 32.0) * (1 << 20) / 4);
+    c->stmt_bucket.assign(plan->nstmts, -1);
+    long long goff = 0;
+    for (size_t j = 0; j < order.size(); ++j) {
+        ParamL& q = c->params[order[j]];
+        if (c->buckets.empty() || c->buckets.back().last_stmt >= 0) {
+            c->buckets.emplace_back();
+            c->buckets.back().off = static_cast<size_t>(goff);
+        }
+        tc_ctx::Bucket& bk = c->buckets.back();
+        bk.params.push_back(order[j]);
+        goff += (q.n + 63) / 64 * 64;  // 256-byte aligned gradient tensors
+        bk.n = goff - static_cast<long long>(bk.off);
+        if (bk.n >= bucket_cap || j + 1 == order.size() || bk.params.size() >= 32) {
+            bk.last_stmt = q.update_stmt;
+            c->stmt_bucket[q.update_stmt] = static_cast<int>(c->buckets.size()) - 1;
+        }
+    }
+    c->grads_n = goff;
+    // parameter slab: [gradients (contiguous, bucket order)] then per parameter p, v, bf16 shadows
+    size_t slab = static_cast<size_t>(goff) * 4;
     auto reserve = [&](size_t bytes) {
         const size_t off = slab;
         slab += align256(bytes);
@@ -943,7 +1047,6 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     for (ParamL& q : c->params) {
         offs.push_back(reserve(q.n * 4));  // p
         offs.push_back(reserve(q.n * 4));  // v
-        offs.push_back(reserve(q.n * 4));  // g
         offs.push_back(q.kind != ParamL::VEC ? reserve(q.n * 2) : SIZE_MAX);
         offs.push_back(q.kind == ParamL::CONV && q.cs % 8 == 0 ? reserve(static_cast<size_t>(q.R) * q.S * q.ks * q.cs * 2)
                                                            : SIZE_MAX);
@@ -951,14 +1054,28 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     c->slab_bytes = slab;
     TCB_CUDA_CHECK(cudaMalloc(&c->slab, std::max<size_t>(slab, 256)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->slab, 0, std::max<size_t>(slab, 256), c->st));
+    c->grads = reinterpret_cast<float*>(c->slab);
+    {
+        long long o = 0;
+        for (int pi : order) {
+            c->params[pi].g = c->grads + o;
+            o += (c->params[pi].n + 63) / 64 * 64;
+        }
+    }
     for (size_t i = 0; i < c->params.size(); ++i) {
         ParamL& q = c->params[i];
-        q.p = reinterpret_cast<float*>(c->slab + offs[5 * i]);
-        q.v = reinterpret_cast<float*>(c->slab + offs[5 * i + 1]);
-        q.g = reinterpret_cast<float*>(c->slab + offs[5 * i + 2]);
-        if (offs[5 * i + 3] != SIZE_MAX) q.shadow = reinterpret_cast<bf16*>(c->slab + offs[5 * i + 3]);
-        if (offs[5 * i + 4] != SIZE_MAX) q.rskc = reinterpret_cast<bf16*>(c->slab + offs[5 * i + 4]);
+        q.p = reinterpret_cast<float*>(c->slab + offs[4 * i]);
+        q.v = reinterpret_cast<float*>(c->slab + offs[4 * i + 1]);
+        if (offs[4 * i + 2] != SIZE_MAX) q.shadow = reinterpret_cast<bf16*>(c->slab + offs[4 * i + 2]);
+        if (offs[4 * i + 3] != SIZE_MAX) q.rskc = reinterpret_cast<bf16*>(c->slab + offs[4 * i + 3]);
     }
+    {
+        const char* ov = std::getenv("TCB_OVERLAP");
+        c->overlap = !(ov && ov[0] == '0');
+    }
+    TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking));
+    TCB_CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    for (auto& bk : c->buckets) TCB_CUDA_CHECK(cudaEventCreateWithFlags(&bk.ready, cudaEventDisableTiming));
     // arena
     TCB_CUDA_CHECK(cudaMalloc(&c->arena, std::max<size_t>(c->arena_bytes, 256)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
@@ -972,7 +1089,8 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMalloc(&c->d_stage, stage_el * 4));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->d_labels, 0, plan->input_dims[0] * sizeof(int32_t), c->st));
-    TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 256));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 1024));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_loss, 0, 1024, c->st));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_iter, 256));
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_iter, 256));
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_loss, 256));
@@ -985,7 +1103,49 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     for (const ParamL& q : c->params) maxc = std::max(maxc, q.K);
     c->max_partials = static_cast<int>(colsum_partials_floats(maxc));
     TCB_CUDA_CHECK(cudaMalloc(&c->ws, std::max<size_t>(c->ws_bytes, 256)));
-    TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 2 * maxc + 64) * sizeof(float)));
+    TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 3 * maxc + 64) * sizeof(float)));
+    // BN backward groups
+    {
+        std::unordered_map<int, int> beta_x, group_of_x;
+        for (int i = 0; i < plan->nstmts; ++i) {
+            const tc_stmt& s = plan->stmts[i];
+            if (s.kind == TC_STMT_LET && s.op == TC_OP_BN_FWD) beta_x[s.in[2].index] = s.in[0].index;
+        }
+        size_t total = 0;
+        std::vector<size_t> offs;
+        for (int i = 0; i < plan->nstmts; ++i) {
+            const tc_stmt& s = plan->stmts[i];
+            if (s.op != TC_OP_BN_BWD_BETA && s.op != TC_OP_BN_BWD_DATA && s.op != TC_OP_BN_BWD_GAMMA) continue;
+            if (s.kind != TC_STMT_LET && s.kind != TC_STMT_UPDATE) continue;
+            int xv = -1;
+            if (s.op == TC_OP_BN_BWD_BETA) {
+                auto f = beta_x.find(s.kind == TC_STMT_UPDATE ? s.param : s.in[1].index);
+                if (f == beta_x.end()) return fail(TC_INTERNAL, "runtime: BN beta gradient without its BatchNorm");
+                xv = f->second;
+            } else {
+                xv = s.in[1].index;
+            }
+            auto g = group_of_x.find(xv);
+            if (g == group_of_x.end()) {
+                tc_ctx::BnGroup gr;
+                gr.x_var = xv;
+                gr.up_var = s.in[0].index;
+                gr.first = i;
+                group_of_x[xv] = static_cast<int>(c->bn_groups.size());
+                c->bn_groups.push_back(gr);
+                offs.push_back(total);
+                total += 2 * static_cast<size_t>(c->vars.at(xv).C) + 64;
+                g = group_of_x.find(xv);
+            } else if (c->bn_groups[g->second].up_var != s.in[0].index) {
+                return fail(TC_INTERNAL, "runtime: BN backward statements disagree on the upstream gradient");
+            }
+            c->stmt_bn_group[i] = g->second;
+        }
+        if (total) {
+            TCB_CUDA_CHECK(cudaMalloc(&c->bn_sums, total * sizeof(float)));
+            for (size_t k = 0; k < c->bn_groups.size(); ++k) c->bn_groups[k].sums = c->bn_sums + offs[k];
+        }
+    }
     if (desc->world > 1) {
         if (!desc->nccl_id) return fail(TC_INVALID_ARG, "world > 1 needs an NCCL unique id");
         ncclUniqueId id;
@@ -1008,11 +1168,17 @@ void tc_ctx_destroy(tc_ctx* c) {
         if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
         if (c->graph[k]) cudaGraphDestroy(c->graph[k]);
     }
+    if (c->comm_st) cudaStreamSynchronize(c->comm_st);
     if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& bk : c->buckets)
+        if (bk.ready) cudaEventDestroy(bk.ready);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
+    if (c->comm_st) cudaStreamDestroy(c->comm_st);
     cudaFree(c->arena);
     cudaFree(c->slab);
     cudaFree(c->ws);
     cudaFree(c->partials);
+    cudaFree(c->bn_sums);
     cudaFree(c->d_input);
     cudaFree(c->d_stage);
     cudaFree(c->d_labels);
@@ -1107,20 +1273,27 @@ tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
     if (!c) return fail(TC_INVALID_ARG, "tc_step");
     TCB_CUDA_CHECK(cudaSetDevice(c->desc.device));
     const int k = update ? 1 : 0;
-    // iteration counters are read by the dropout kernels through device memory,
-    // so a captured graph replays correctly for every iteration
-    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
-    c->h_iter[0] = static_cast<uint32_t>(iter);
-    c->h_iter[1] = static_cast<uint32_t>(n0);
+    // The iteration / first-sample counters that the dropout kernels read live in
+    // device memory; a one-thread kernel sets them ahead of the (captured) step, so
+    // the host never waits for the previous step.
     if (c->gexec[k]) {
+        tc_status r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+        if (r != TC_OK) return r;
         TCB_CUDA_CHECK(cudaGraphLaunch(c->gexec[k], c->st));
-        count_launch(static_cast<unsigned>(std::max(0, c->launches_per_step)));
+        count_launch(static_cast<unsigned>(std::max(0, c->launches_per_step - 1)));
         return TC_OK;
     }
-    const bool capture = c->desc.use_graph && c->runs[k] >= 1 && !c->comm;
+    c->h_iter[0] = static_cast<uint32_t>(iter);
+    c->h_iter[1] = static_cast<uint32_t>(n0);
+    const char* ng = std::getenv("TCB_NCCL_GRAPH");
+    const bool capture = c->desc.use_graph && c->runs[k] >= 1 && (!c->comm || !(ng && ng[0] == '0'));
     const unsigned long long before = g_launches.load();
-    if (capture) TCB_CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-    tc_status r = run_body(c, update);
+    if (capture) {
+        tc_status r = launch_set_iter(c->d_iter, c->h_iter[0], c->h_iter[1], c->st);
+        if (r != TC_OK) return r;
+        TCB_CUDA_CHECK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    }
+    tc_status r = run_body(c, update, c->overlap, /*set_iter=*/!capture);
     if (capture) {
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(c->st, &g);
@@ -1138,13 +1311,18 @@ tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
 
 tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
     if (!c || index < 0 || index >= c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_exec_stmt");
-    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
-    c->h_iter[0] = static_cast<uint32_t>(iter);
-    c->h_iter[1] = static_cast<uint32_t>(n0);
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 8, cudaMemcpyHostToDevice, c->st));
-    tc_status r = exec_stmt(c, index);
+    tc_status r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
     if (r != TC_OK) return r;
-    return apply_update(c, index, 1);
+    r = exec_stmt(c, index);
+    if (r != TC_OK) return r;
+    const tc_stmt& s = c->plan->stmts[index];
+    if (s.kind != TC_STMT_UPDATE) return TC_OK;
+    // single-statement form: this parameter's all-reduce + update, in stream order
+    ParamL& q = c->params[s.param];
+    if (c->comm && ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
+        return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
+    SgdTensor t = sgd_tensor(c, s.param);
+    return launch_sgd(&t, 1, nullptr, c->st);
 }
 
 tc_status tc_loss(tc_ctx* c, double* loss) {
@@ -1196,17 +1374,26 @@ tc_status tc_pool_indices_download(tc_ctx* c, int var, int32_t* host, int64_t ma
     auto it = c->pool_idx_item.find(var);
     if (it == c->pool_idx_item.end()) return fail(TC_INVALID_ARG, "not a max-pool output var");
     const VarL& v = c->vars.at(var);
-    std::vector<int32_t> raw(v.elems());
+    const tc_stmt& s = c->plan->stmts[v.def];
+    const VarL& x = c->vars.at(s.in[0].index);
+    std::vector<uint8_t> raw(v.elems());
     TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
-    TCB_CUDA_CHECK(cudaMemcpy(raw.data(), c->arena + c->items[it->second].off, raw.size() * 4, cudaMemcpyDeviceToHost));
+    TCB_CUDA_CHECK(cudaMemcpy(raw.data(), c->arena + c->items[it->second].off, raw.size(), cudaMemcpyDeviceToHost));
     const long long count = static_cast<long long>(v.N) * v.C * v.H * v.W;
     if (count > max_elems) return fail(TC_INVALID_ARG, "buffer too small");
+    // window-local argmax (r*k + s) -> flat NCHW index of the input
     for (int n = 0; n < v.N; ++n)
         for (int ch = 0; ch < v.C; ++ch)
             for (int h = 0; h < v.H; ++h)
-                for (int w = 0; w < v.W; ++w)
-                    host[((static_cast<long long>(n) * v.C + ch) * v.H + h) * v.W + w] =
-                        raw[((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch];
+                for (int w = 0; w < v.W; ++w) {
+                    const int loc = raw[((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch];
+                    int32_t flat = -1;
+                    if (loc != 255) {
+                        const int ih = h * s.stride - s.pad + loc / s.k, iw = w * s.stride - s.pad + loc % s.k;
+                        flat = static_cast<int32_t>(((static_cast<long long>(n) * x.C + ch) * x.H + ih) * x.W + iw);
+                    }
+                    host[((static_cast<long long>(n) * v.C + ch) * v.H + h) * v.W + w] = flat;
+                }
     return TC_OK;
 }
 
@@ -1225,18 +1412,17 @@ int tc_launches_per_step(tc_ctx* c) { return c ? c->launches_per_step : -1; }
 
 tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_ms, int max) {
     if (!c || !stmt_ms || max < c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_profile_step");
-    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
-    c->h_iter[0] = static_cast<uint32_t>(iter);
-    c->h_iter[1] = static_cast<uint32_t>(n0);
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_iter, c->h_iter, 8, cudaMemcpyHostToDevice, c->st));
+    tc_status r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    if (r != TC_OK) return r;
     const int n = c->plan->nstmts;
     std::vector<cudaEvent_t> ev(n + 1);
     for (auto& e : ev) TCB_CUDA_CHECK(cudaEventCreate(&e));
     TCB_CUDA_CHECK(cudaEventRecord(ev[0], c->st));
-    tc_status r = TC_OK;
+    // serial form (bucket all-reduce + update on the main stream, charged to the
+    // statement that completes the bucket)
     for (int i = 0; i < n && r == TC_OK; ++i) {
         r = exec_stmt(c, i);
-        if (r == TC_OK) r = apply_update(c, i, update);
+        if (r == TC_OK && c->stmt_bucket[i] >= 0) r = flush_bucket(c, c->stmt_bucket[i], update, false);
         cudaEventRecord(ev[i + 1], c->st);
     }
     cudaStreamSynchronize(c->st);

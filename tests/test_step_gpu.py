@@ -177,3 +177,28 @@ def test_big_network_step_parity(name, batch):
     bad = [(p.name, rel(tr.grad(i), o.grad(i)), env[i]) for i, p in enumerate(net.params)
            if rel(tr.grad(i), o.grad(i)) > 3 * env[i] + 2e-2]
     assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("name,batch", [("alexnet", 8), ("resnet50", 2)])
+def test_bucket_overlap_matches_serial(name, batch, monkeypatch):
+    """Bucketed multi-tensor updates on the side stream (default) give bit-identical
+    parameters, velocities and losses to the serial schedule (TCB_OVERLAP=0), also
+    when the step is replayed from a CUDA graph with small buckets."""
+    outs = []
+    for overlap, bucket_mb in (("0", "32"), ("1", "1")):
+        monkeypatch.setenv("TCB_OVERLAP", overlap)
+        monkeypatch.setenv("TCB_BUCKET_MB", bucket_mb)
+        net = compile_network(name, batch)
+        tr = Trainer(net, use_graph=True, seed=5)
+        tr.init_params()
+        losses = []
+        for it in range(4):
+            tr.stage_synthetic(it, 0)
+            tr.step(it)
+            losses.append(tr.loss())
+        outs.append((losses, [tr.get_param(i) for i in range(len(net.params))],
+                     [tr.velocity(i) for i in range(len(net.params))]))
+        tr.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1] + outs[0][2], outs[1][1] + outs[1][2]):
+        np.testing.assert_array_equal(a, b)

@@ -1,0 +1,114 @@
+#!/usr/bin/env python3
+"""Kernel-level timing of the tcgen05 GEMM / implicit-GEMM conv entry points (CUDA events,
+median of reps, inputs resident).  Shapes: plain GEMMs and the conv layers of the configs.
+
+    python tools/gemm_bench.py [--which gemm,conv] [--net alexnet]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1701_02284_b200 import _native as nat  # noqa: E402
+
+CONVS = {  # (N, C, H, W, K, R, S, stride, pad)
+    "alexnet": [(128, 3, 224, 224, 96, 11, 11, 4, 0), (128, 96, 26, 26, 256, 5, 5, 1, 2),
+                (128, 256, 12, 12, 384, 3, 3, 1, 1), (128, 384, 12, 12, 384, 3, 3, 1, 1),
+                (128, 384, 12, 12, 256, 3, 3, 1, 1)],
+    "vgg16": [(64, 64, 224, 224, 64, 3, 3, 1, 1), (64, 128, 112, 112, 128, 3, 3, 1, 1),
+              (64, 256, 56, 56, 256, 3, 3, 1, 1), (64, 512, 28, 28, 512, 3, 3, 1, 1),
+              (64, 512, 14, 14, 512, 3, 3, 1, 1)],
+    "resnet50": [(64, 64, 56, 56, 64, 3, 3, 1, 1), (64, 64, 56, 56, 256, 1, 1, 1, 0),
+                 (64, 256, 56, 56, 64, 1, 1, 1, 0), (64, 256, 14, 14, 256, 3, 3, 1, 1),
+                 (64, 1024, 14, 14, 256, 1, 1, 1, 0), (64, 512, 7, 7, 512, 3, 3, 1, 1)],
+}
+
+
+def timeit(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def gemm_case(M, N, K):
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    args = nat.GemmArgs(M=M, N=N, K=K, a_layout=0, b_layout=0, A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K,
+                        D=D.data_ptr(), ldd=N, d_dtype=nat.TC_DTYPE_BF16, alpha=1.0, beta=0.0, splits=1)
+    ms = timeit(lambda: nat.check(nat.lib().tc_gemm_bf16(C.byref(args), None)))
+    return ms, 2.0 * M * N * K / (ms * 1e-3) / 1e12
+
+
+def ceil8(v):
+    return (v + 7) // 8 * 8
+
+
+def conv_case(n, c, h, w, k, r, s, st, pad):
+    L = nat.lib()
+    ho, wo = (h + 2 * pad - r) // st + 1, (w + 2 * pad - s) // st + 1
+    cs = 4 if c <= 4 else ceil8(c)
+    ks = ceil8(k)
+    d = nat.ConvDesc(N=n, C=c, H=h, W=w, K=k, R=r, S=s, stride=st, pad=pad, Ho=ho, Wo=wo, cs=cs, ks=ks,
+                     wld=ceil8(r * s * cs))
+    x = torch.randn(n, h, w, cs, device="cuda").to(torch.bfloat16)
+    y = torch.randn(n, ho, wo, ks, device="cuda").to(torch.bfloat16)
+    wt = torch.randn(k, d.wld, device="cuda").to(torch.bfloat16)
+    wr = torch.randn(r * s * ks * max(cs, 8), device="cuda").to(torch.bfloat16)
+    dw = torch.empty(k, d.wld, device="cuda")
+    out = {}
+    flops = 2.0 * n * ho * wo * k * c * r * s
+    for which in range(3):
+        wsb = L.tc_conv2d_workspace_bytes(C.byref(d), which)
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+        if which == 0:
+            fn = lambda: nat.check(L.tc_conv2d_fwd(C.byref(d), x.data_ptr(), wt.data_ptr(), None, 0, y.data_ptr(),  # noqa
+                                                   ws.data_ptr(), wsb, None))
+        elif which == 1:
+            if cs % 8:
+                continue
+            fn = lambda: nat.check(L.tc_conv2d_bwd_data(C.byref(d), y.data_ptr(), wr.data_ptr(), x.data_ptr(),  # noqa
+                                                        ws.data_ptr(), wsb, None))
+        else:
+            fn = lambda: nat.check(L.tc_conv2d_bwd_filter(C.byref(d), y.data_ptr(), x.data_ptr(), dw.data_ptr(),  # noqa
+                                                          ws.data_ptr(), wsb, None))
+        ms = timeit(fn)
+        out[["fwd", "dgrad", "wgrad"][which]] = (ms, flops / (ms * 1e-3) / 1e12)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="gemm,conv")
+    ap.add_argument("--net", default="alexnet,vgg16,resnet50")
+    args = ap.parse_args()
+    print(f"TCB_FORCE_BN={os.environ.get('TCB_FORCE_BN', '')} TCB_IM2COL={os.environ.get('TCB_IM2COL', '')}")
+    if "gemm" in args.which:
+        for M, N, K in [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096),
+                        (4096, 4096, 4096)]:
+            ms, tf = gemm_case(M, N, K)
+            print(f"gemm {M}x{N}x{K}: {ms:.3f} ms {tf:.0f} TF/s")
+    if "conv" in args.which:
+        for net in args.net.split(","):
+            for cv in CONVS[net]:
+                r = conv_case(*cv)
+                print(f"{net} conv {cv}: " + "  ".join(f"{k} {v[0]:.3f} ms {v[1]:.0f} TF/s" for k, v in r.items()))
+
+
+if __name__ == "__main__":
+    main()
