@@ -81,10 +81,11 @@ static EncodeIm2colFn encode_im2col_fn() {
     return fn;
 }
 
-// 4-D im2col map over an NHWC bf16 tensor {cs, W, H, N}: a load yields `pixels` rows of 64 channels
-// (128 B, SW128).  The pixel bounding box is [lo, extent - 1 + up] per spatial dim, walked with `stride`.
+// 4-D im2col map over an NHWC bf16 tensor {cs, W, H, N}: a load yields `pixels` rows of `chans`
+// channels (64: 128 B rows, SW128; 32: 64 B rows, SW64).  The pixel bounding box is
+// [lo, extent - 1 + up] per spatial dim, walked with `stride`.
 static bool make_tmap_im2col(CUtensorMap* map, const void* base, int N, int H, int W, int cs, int lo_w, int lo_h,
-                             int up_w, int up_h, int stride, int pixels, std::string* err) {
+                             int up_w, int up_h, int stride, int pixels, std::string* err, int chans = 64) {
     auto fn = encode_im2col_fn();
     if (!fn) {
         *err = "cuTensorMapEncodeIm2col unavailable (no CUDA driver)";
@@ -100,8 +101,9 @@ static bool make_tmap_im2col(CUtensorMap* map, const void* base, int N, int H, i
     cuuint64_t strides[3] = {row, row * W, row * W * H};
     int lo[2] = {lo_w, lo_h}, up[2] = {up_w, up_h};
     cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lo, up, 64,
-                    static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lo, up,
+                    static_cast<cuuint32_t>(chans), static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    chans == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         *err = "cuTensorMapEncodeIm2col failed (" + std::to_string(static_cast<int>(r)) + ")";
@@ -122,6 +124,16 @@ static bool im2col_enabled() {
         return !(e && e[0] == '0');
     }();
     return on;
+}
+// TCB_EPI_DIRECT=1 selects the direct-store epilogue (registers -> st.global) instead of
+// the swizzled-smem + TMA-store path.  Measured slower on every shape tried (ResNet 1x1
+// K=64: 88 vs 52 us), so it is opt-in for experiments only.
+static int epi_direct_env() {
+    static const int v = [] {
+        const char* e = std::getenv("TCB_EPI_DIRECT");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return v;
 }
 static bool corner_ok(int v) { return v >= -128 && v <= 127; }
 
@@ -183,19 +195,6 @@ struct LaunchPlan {
     int num_kb = 1;
 };
 
-static int pick_bn(int N) {
-    int best = 256;
-    double best_eff = -1.0;
-    for (int bn : {256, 128, 64}) {
-        const double eff = static_cast<double>(N) / (static_cast<double>(ceil_div(N, bn)) * bn);
-        if (eff > best_eff + 1e-9) {
-            best_eff = eff;
-            best = bn;
-        }
-    }
-    return best;
-}
-
 // TCB_FORCE_BN=64|128|256 pins the tile width (kernel experiments / A-B comparisons).
 static int forced_bn() {
     static const int v = [] {
@@ -206,38 +205,44 @@ static int forced_bn() {
     return v;
 }
 
-static LaunchPlan plan_launch(int M, int N, int K, int splits_req) {
-    LaunchPlan lp;
-    lp.bn = forced_bn() ? forced_bn() : pick_bn(N);
-    lp.num_kb = std::max(1, ceil_div(K, BK));
-    const int tiles = ceil_div(M, BM) * ceil_div(N, lp.bn);
-    int splits = splits_req;
-    if (splits <= 0) {
-        // Cost model over the persistent grid: waves x k-blocks per unit (wave quantisation on 148 SMs)
-        // plus the fp32 partial traffic of the deterministic split-K reduce.
-        const int sms = num_sms();
-        const double t_kb = 0.45e-6 * lp.bn / 128.0;            // one 128 x BN x 64 block, measured order
-        const double mn = static_cast<double>(M) * N;
-        double best_t = 1e30;
-        splits = 1;
-        const int max_s = std::max(1, std::min(128, lp.num_kb / 4));
+// Per-CTA time of one 128 x BN x 64 k-block, measured on B200 with plain TMA operands
+// (8192^3: BN=256 1284 TF/s, BN=128 853 TF/s (shared-memory bound: A+B bytes per MMA
+// cycle), BN=64 461 TF/s; tools/gemm_bench.py).
+static double t_kblock(int bn) { return bn == 256 ? 0.48e-6 : bn == 128 ? 0.36e-6 : 0.335e-6; }
+
+// Tile width and split-K chosen by a cost model over the persistent grid: waves of
+// units, each unit max(main loop, epilogue store) since the double-buffered TMEM
+// accumulator overlaps a tile's store with the next tile's main loop; split-K adds
+// the fp32 partial round trip of the deterministic reduce.
+static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes) {
+    LaunchPlan best;
+    double best_t = 1e30;
+    const int sms = num_sms();
+    const int num_kb = std::max(1, ceil_div(K, BK));
+    const double mn = static_cast<double>(M) * N;
+    for (int bn : {256, 128, 64}) {
+        if (forced_bn() && bn != forced_bn()) continue;
+        const int tiles = ceil_div(M, BM) * ceil_div(N, bn);
+        const int max_s = splits_req > 0 ? 1 : std::max(1, std::min(128, num_kb / 4));
         for (int s = 1; s <= max_s; ++s) {
-            const int kbs = ceil_div(lp.num_kb, s);
-            const int s_eff = ceil_div(lp.num_kb, kbs);
+            const int req = splits_req > 0 ? std::min(splits_req, num_kb) : s;
+            const int kbs = ceil_div(num_kb, req);
+            const int s_eff = ceil_div(num_kb, kbs);
             const long long units = static_cast<long long>(tiles) * s_eff;
             const double waves = static_cast<double>((units + sms - 1) / sms);
-            double t = waves * kbs * t_kb;
-            if (s_eff > 1) t += (s_eff * mn * 8.0 + mn * 4.0) / 5.0e12 + 3.0e-6;
+            const double epi = static_cast<double>(BM) * bn * (s_eff > 1 ? 4 : out_bytes) / 40e9;
+            double t = waves * std::max(kbs * t_kblock(bn), epi) + 2e-6;
+            if (s_eff > 1) t += (s_eff * mn * 8.0 + mn * out_bytes) / 5.0e12 + 3.0e-6;
             if (t < best_t * 0.97) {
                 best_t = t;
-                splits = s_eff;
+                best.bn = bn;
+                best.num_kb = num_kb;
+                best.kb_per_split = kbs;
+                best.splits = s_eff;
             }
         }
     }
-    splits = std::max(1, std::min(splits, lp.num_kb));
-    lp.kb_per_split = ceil_div(lp.num_kb, splits);
-    lp.splits = ceil_div(lp.num_kb, lp.kb_per_split);
-    return lp;
+    return best;
 }
 
 template <int BN>
@@ -266,6 +271,11 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
     const bool partial = lp.splits > 1 || beta != 0.f;
+    const int de = epi_direct_env();
+    p.direct = de > 0 ? 1 : 0;
+    p.d_ptr = partial ? ws : D;
+    p.d_ld = partial ? p.N : ldd;
+    p.d_split_stride = partial ? static_cast<long long>(p.M) * p.N : 0;
     std::string err;
     if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
@@ -317,7 +327,7 @@ unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load();
 
 size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
     if (!a) return 0;
-    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits);
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4);
     return (lp.splits > 1 || a->beta != 0.f) ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
 }
 
@@ -329,7 +339,7 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     p.N = a->N;
     p.K = a->K;
     p.alpha = a->alpha;
-    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits);
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4);
     std::string err;
     if (a->a_layout == TC_LAYOUT_K) {
         p.a_mode = OP_TMA_K;
@@ -385,27 +395,30 @@ static bool is_pointwise(const tc_conv_desc* d) {
 }
 static int filter_ld(const tc_conv_desc* d) { return d->wld ? d->wld : d->R * d->S * d->cs; }
 
-// Which operand path each Convolv form takes (TMA im2col needs whole 64-channel blocks per tap).
-static bool fprop_im2col(const tc_conv_desc* d) {
-    return im2col_enabled() && !is_pointwise(d) && d->cs % 64 == 0 && d->stride <= 8 && corner_ok(-d->pad) &&
-           corner_ok(d->pad - (d->S - 1)) && corner_ok(d->pad - (d->R - 1));
+// Which operand path each Convolv form takes: TMA im2col needs whole 64-channel (SW128)
+// or 32-channel (SW64) blocks per tap; returns the block width, 0 = cp.async gather.
+static int chan_block(int cs) { return cs % 64 == 0 ? 64 : cs % 32 == 0 ? 32 : 0; }
+static int fprop_im2col(const tc_conv_desc* d) {
+    if (!im2col_enabled() || is_pointwise(d) || d->stride > 8 || !corner_ok(-d->pad) || !corner_ok(d->pad - (d->S - 1)) ||
+        !corner_ok(d->pad - (d->R - 1)))
+        return 0;
+    return chan_block(d->cs);
 }
-static bool dgrad_im2col(const tc_conv_desc* d) {
-    return im2col_enabled() && !is_pointwise(d) && d->ks % 64 == 0 && d->stride == 1 &&
-           corner_ok(d->pad - (d->S - 1)) && corner_ok(d->pad - (d->R - 1)) &&
-           corner_ok(d->pad - (d->S - 1) + d->W - d->Wo) && corner_ok(d->pad - (d->R - 1) + d->H - d->Ho);
+static int dgrad_im2col(const tc_conv_desc* d) {
+    if (!im2col_enabled() || is_pointwise(d) || d->stride != 1 || !corner_ok(d->pad - (d->S - 1)) ||
+        !corner_ok(d->pad - (d->R - 1)) || !corner_ok(d->pad - (d->S - 1) + d->W - d->Wo) ||
+        !corner_ok(d->pad - (d->R - 1) + d->H - d->Ho))
+        return 0;
+    return chan_block(d->ks);
 }
-static bool wgrad_im2col(const tc_conv_desc* d) {
-    return im2col_enabled() && !is_pointwise(d) && d->cs % 64 == 0 && d->stride <= 8 && corner_ok(-d->pad) &&
-           corner_ok(d->pad - (d->S - 1)) && corner_ok(d->pad - (d->R - 1));
-}
+static int wgrad_im2col(const tc_conv_desc* d) { return fprop_im2col(d); }
 
 static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
     const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
     const long long npix_in = static_cast<long long>(d->N) * d->H * d->W;
-    if (which == 0) return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1);
-    if (which == 1) return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1);
-    return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0);
+    if (which == 0) return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2);
+    if (which == 1) return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2);
+    return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0, 4);
 }
 
 size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
@@ -431,15 +444,15 @@ tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, con
     if (is_pointwise(d)) {
         p.a_mode = OP_TMA_K;
         if (!make_tmap_2d_bf16(&p.tmA, x, d->cs, p.M, d->cs, BK, BM, &err)) return fail(TC_INVALID_ARG, err);
-    } else if (fprop_im2col(d)) {
-        p.a_mode = OP_IM2COL_K;
-        p.i2c_cpb = d->cs / 64;
+    } else if (const int cb = fprop_im2col(d)) {
+        p.a_mode = cb == 64 ? OP_IM2COL_K : OP_IM2COL32_K;
+        p.i2c_cpb = d->cs / cb;
         p.i2c_ldk = d->cs;
         p.i2c_lo_w = p.i2c_lo_h = -d->pad;
         p.i2c_P = d->Ho;
         p.i2c_Q = d->Wo;
         if (!make_tmap_im2col(&p.tmA, x, d->N, d->H, d->W, d->cs, -d->pad, -d->pad, d->pad - (d->S - 1),
-                              d->pad - (d->R - 1), d->stride, BM, &err))
+                              d->pad - (d->R - 1), d->stride, BM, &err, cb))
             return fail(TC_INVALID_ARG, err);
     } else {
         p.a_mode = OP_GATHER_K;
@@ -468,10 +481,10 @@ tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* 
     if (is_pointwise(d)) {
         p.a_mode = OP_TMA_K;
         if (!make_tmap_2d_bf16(&p.tmA, dy, d->ks, p.M, d->ks, BK, BM, &err)) return fail(TC_INVALID_ARG, err);
-    } else if (dgrad_im2col(d)) {
+    } else if (const int cb = dgrad_im2col(d)) {
         // dx(y, x) = sum_taps dy(y + pad - kh, x + pad - kw): source start y + pad - (R-1), offset R-1-kh
-        p.a_mode = OP_IM2COL_K;
-        p.i2c_cpb = d->ks / 64;
+        p.a_mode = cb == 64 ? OP_IM2COL_K : OP_IM2COL32_K;
+        p.i2c_cpb = d->ks / cb;
         p.i2c_ldk = d->ks;
         p.i2c_lo_w = d->pad - (d->S - 1);
         p.i2c_lo_h = d->pad - (d->R - 1);
@@ -479,7 +492,7 @@ tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* 
         p.i2c_P = d->H;
         p.i2c_Q = d->W;
         if (!make_tmap_im2col(&p.tmA, dy, d->N, d->Ho, d->Wo, d->ks, p.i2c_lo_w, p.i2c_lo_h,
-                              p.i2c_lo_w + d->W - d->Wo, p.i2c_lo_h + d->H - d->Ho, 1, BM, &err))
+                              p.i2c_lo_w + d->W - d->Wo, p.i2c_lo_h + d->H - d->Ho, 1, BM, &err, cb))
             return fail(TC_INVALID_ARG, err);
     } else {
         p.a_mode = OP_GATHER_K;
@@ -509,13 +522,13 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
     if (is_pointwise(d)) {
         p.b_mode = OP_TMA_MN;
         if (!make_tmap_2d_bf16(&p.tmB, x, d->cs, npix, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
-    } else if (wgrad_im2col(d)) {
-        p.b_mode = OP_IM2COL_MN;
+    } else if (const int cb = wgrad_im2col(d)) {
+        p.b_mode = cb == 64 ? OP_IM2COL_MN : OP_IM2COL32_MN;
         p.i2c_lo_w = p.i2c_lo_h = -d->pad;
         p.i2c_P = d->Ho;
         p.i2c_Q = d->Wo;
         if (!make_tmap_im2col(&p.tmB, x, d->N, d->H, d->W, d->cs, -d->pad, -d->pad, d->pad - (d->S - 1),
-                              d->pad - (d->R - 1), d->stride, BK, &err))
+                              d->pad - (d->R - 1), d->stride, BK, &err, cb))
             return fail(TC_INVALID_ARG, err);
     } else {
         p.b_mode = OP_GATHER_MN;

@@ -408,7 +408,7 @@ RedPlan red_plan(long long rows, int ld) {
     const int rpi = kRedThreads / (r.ct / 8);
     const long long target = static_cast<long long>(num_sms()) * 4;
     long long sp = std::max<long long>(1, target / r.tiles);
-    sp = std::min<long long>(sp, std::max<long long>(1, rows / (4LL * rpi)));  // >= 4 row iterations per thread
+    sp = std::min<long long>(sp, std::max<long long>(1, rows / (8LL * rpi)));  // >= 8 rows per thread
     sp = std::min<long long>(sp, 1024);
     r.rps = (rows + sp - 1) / sp;
     r.splits = static_cast<int>((rows + r.rps - 1) / r.rps);
@@ -443,27 +443,39 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
         const long long r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
         const bf16* px = x + r0 * ld + c0;
         const bf16* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
-        for (long long r = r0 + tr; r < r1; r += rpi) {
-            const long long o = (r - r0) * ld;
-            float f[8];
-            unpack8(__ldcs(reinterpret_cast<const uint4*>(px + o)), f);
-            if (MODE == RED_SUM) {
+        constexpr int U = 4;  // rows in flight per thread
+        for (long long rb = tr; r0 + rb < r1; rb += U * rpi) {
+            uint4 q[U], q2[U];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] += f[j];
-            } else if (MODE == RED_STATS) {
+            for (int u = 0; u < U; ++u) {
+                const long long r = rb + u * rpi;
+                const bool ok = r0 + r < r1;
+                q[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(px + r * ld)) : make_uint4(0, 0, 0, 0);
+                if (MODE == RED_BNBWD) q2[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(p2 + r * ld)) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float d = f[j] - m[j];
-                    a[j] += d;
-                    b[j] = fmaf(d, d, b[j]);
-                }
-            } else {
-                float g[8];
-                unpack8(__ldcs(reinterpret_cast<const uint4*>(p2 + o)), g);
+            for (int u = 0; u < U; ++u) {
+                if (r0 + rb + u * rpi >= r1) break;
+                float f[8];
+                unpack8(q[u], f);
+                if (MODE == RED_SUM) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    a[j] += f[j];
-                    b[j] = fmaf(f[j], (g[j] - m[j]) * is[j], b[j]);
+                    for (int j = 0; j < 8; ++j) a[j] += f[j];
+                } else if (MODE == RED_STATS) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float d = f[j] - m[j];
+                        a[j] += d;
+                        b[j] = fmaf(d, d, b[j]);
+                    }
+                } else {
+                    float g[8];
+                    unpack8(q2[u], g);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        a[j] += f[j];
+                        b[j] = fmaf(f[j], (g[j] - m[j]) * is[j], b[j]);
+                    }
                 }
             }
         }
@@ -496,46 +508,72 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
 // Stage 2.  RED_SUM: out[c] = scale * sum.  RED_STATS: stats = (mean, istd), coef =
 // (gamma * istd, beta - mean * gamma * istd).  RED_BNBWD: out = (sum dy, sum dy*xhat).
 template <int MODE>
-__global__ void k_chan_final(const float* __restrict__ part, int splits, int C, float scale, float* __restrict__ out,
-                             const bf16* __restrict__ x, long long rows, float eps, const float* __restrict__ gamma,
-                             const float* __restrict__ beta, float* __restrict__ coef) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-        float sa = 0.f, sb = 0.f;
-        for (int q = 0; q < splits; ++q) {
+__global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ part, int splits, int C, float scale,
+                                                    float* __restrict__ out, const bf16* __restrict__ x, long long rows,
+                                                    float eps, const float* __restrict__ gamma,
+                                                    const float* __restrict__ beta, float* __restrict__ coef) {
+    // 32 channels per block; 8 split-lanes per channel, each summing a fixed strided subset,
+    // combined in lane order (deterministic)
+    __shared__ float sa_sm[8][33], sb_sm[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + tx;
+    float sa = 0.f, sb = 0.f;
+    if (c < C) {
+        for (int q = ty; q < splits; q += 8) {
             sa += part[static_cast<long long>(q) * C + c];
             if (MODE != RED_SUM) sb += part[static_cast<long long>(splits + q) * C + c];
         }
-        if (MODE == RED_SUM) {
-            out[c] = sa * scale;
-        } else if (MODE == RED_STATS) {
-            const float inv = 1.f / static_cast<float>(rows);
-            const float m1 = sa * inv;
-            const float mean = __bfloat162float(x[c]) + m1;
-            const float var = fmaxf(sb * inv - m1 * m1, 0.f);
-            const float istd = rsqrtf(var + eps);
-            out[c] = mean;
-            out[C + c] = istd;
-            const float g = gamma[c] * istd;
-            coef[c] = g;
-            coef[C + c] = beta[c] - mean * g;
-        } else {
-            out[c] = sa;
-            out[C + c] = sb;
-        }
+    }
+    sa_sm[ty][tx] = sa;
+    sb_sm[ty][tx] = sb;
+    __syncthreads();
+    if (ty != 0 || c >= C) return;
+    sa = 0.f;
+    sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        sa += sa_sm[q][tx];
+        sb += sb_sm[q][tx];
+    }
+    if (MODE == RED_SUM) {
+        out[c] = sa * scale;
+    } else if (MODE == RED_STATS) {
+        const float inv = 1.f / static_cast<float>(rows);
+        const float m1 = sa * inv;
+        const float mean = __bfloat162float(x[c]) + m1;
+        const float var = fmaxf(sb * inv - m1 * m1, 0.f);
+        const float istd = rsqrtf(var + eps);
+        out[c] = mean;
+        out[C + c] = istd;
+        const float g = gamma[c] * istd;
+        coef[c] = g;
+        coef[C + c] = beta[c] - mean * g;
+    } else {
+        out[c] = sa;
+        out[C + c] = sb;
     }
 }
 
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
 __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restrict__ coef, uint4* __restrict__ y,
                               long long n8, int ld8, int C) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c0 = static_cast<int>(i % ld8) * 8;
-        float f[8];
-        unpack8(__ldcs(x + i), f);
+    const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
+        uint4 q[2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
-        y[i] = pack8(f);
+        for (int u = 0; u < 2; ++u) q[u] = i0 + u * S < n8 ? __ldcs(x + i0 + u * S) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const long long i = i0 + u * S;
+            if (i >= n8) break;
+            const int c0 = static_cast<int>(i % ld8) * 8;
+            float f[8];
+            unpack8(q[u], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
+            y[i] = pack8(f);
+        }
     }
 }
 
@@ -554,18 +592,30 @@ __global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __re
 
 __global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ k,
                                uint4* __restrict__ dx, long long n8, int ld8, int C) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c0 = static_cast<int>(i % ld8) * 8;
-        float f[8], g[8];
-        unpack8(__ldcs(dy + i), f);
-        unpack8(__ldcs(x + i), g);
+    const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
+        uint4 q[2], r[2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int c = c0 + j;
-            f[j] = c < C ? fmaf(__ldg(k + c), f[j], fmaf(__ldg(k + C + c), g[j], __ldg(k + 2 * C + c))) : 0.f;
+        for (int u = 0; u < 2; ++u) {
+            const bool ok = i0 + u * S < n8;
+            q[u] = ok ? __ldcs(dy + i0 + u * S) : make_uint4(0, 0, 0, 0);
+            r[u] = ok ? __ldcs(x + i0 + u * S) : make_uint4(0, 0, 0, 0);
         }
-        dx[i] = pack8(f);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const long long i = i0 + u * S;
+            if (i >= n8) break;
+            const int c0 = static_cast<int>(i % ld8) * 8;
+            float f[8], g[8];
+            unpack8(q[u], f);
+            unpack8(r[u], g);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j;
+                f[j] = c < C ? fmaf(__ldg(k + c), f[j], fmaf(__ldg(k + C + c), g[j], __ldg(k + 2 * C + c))) : 0.f;
+            }
+            dx[i] = pack8(f);
+        }
     }
 }
 
@@ -980,7 +1030,7 @@ tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, f
     RedPlan rp;
     tc_status s = chan_reduce<RED_SUM>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_SUM><<<(cols + 255) / 256, 256, 0, st>>>(partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
+    k_chan_final<RED_SUM><<<(cols + 31) / 32, 256, 0, st>>>(partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -1008,7 +1058,7 @@ tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_STATS><<<(C + 255) / 256, 256, 0, st>>>(partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+    k_chan_final<RED_STATS><<<(C + 31) / 32, 256, 0, st>>>(partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
@@ -1022,7 +1072,7 @@ tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_BNBWD><<<(C + 255) / 256, 256, 0, st>>>(partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
+    k_chan_final<RED_BNBWD><<<(C + 31) / 32, 256, 0, st>>>(partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
                                                               nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;

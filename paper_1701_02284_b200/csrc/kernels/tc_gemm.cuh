@@ -12,6 +12,10 @@
 //   OP_IM2COL_K  TMA im2col of an NHWC activation: one {64 channels x 128 pixels} box per
 //                k-block = (filter tap, 64-channel block), tap passed as the im2col offset (A only)
 //   OP_IM2COL_MN TMA im2col of x for bwd-filter: {64 channels x 64 pixels} boxes (B only)
+//   OP_IM2COL32_K / OP_IM2COL32_MN  the same for channel strides that are multiples of 32
+//                but not 64: 32-channel boxes in SWIZZLE_64B layout; a 64-wide k-block of A
+//                is two 8 KB halves (each one (tap, 32-channel block)), B's columns come in
+//                32-wide atoms
 //
 // Persistent, warp-specialised (384 threads, one CTA per SM):
 //   warp 0      TMA producer (elected lane)
@@ -31,7 +35,16 @@
 
 namespace tcb {
 
-enum OperandMode : int { OP_TMA_K = 0, OP_TMA_MN = 1, OP_GATHER_K = 2, OP_GATHER_MN = 3, OP_IM2COL_K = 4, OP_IM2COL_MN = 5 };
+enum OperandMode : int {
+    OP_TMA_K = 0,
+    OP_TMA_MN = 1,
+    OP_GATHER_K = 2,
+    OP_GATHER_MN = 3,
+    OP_IM2COL_K = 4,
+    OP_IM2COL_MN = 5,
+    OP_IM2COL32_K = 6,
+    OP_IM2COL32_MN = 7
+};
 enum GatherKind : int { GATHER_FPROP = 0, GATHER_DGRAD = 1 };
 enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1 };
 
@@ -63,11 +76,18 @@ struct GemmParams {
     int relu;
     float alpha;
     // TMA im2col operand: tmA (OP_IM2COL_K) or tmB (OP_IM2COL_MN) is a 4-D {c, w, h, n} im2col map
-    int i2c_cpb;             // 64-channel blocks per filter tap (A side)
+    int i2c_cpb;             // 64-channel (32 for OP_IM2COL32_K) blocks per filter tap (A side)
     int i2c_ldk;             // k coordinate of tap t in the other operand = t * i2c_ldk + 64 * block
     int i2c_lo_w, i2c_lo_h;  // first source pixel of output pixel (y, x) = (y * stride + lo_h, x * stride + lo_w)
     int i2c_flip;            // bwd-data: tap (kh, kw) is the offset (R-1-kh, S-1-kw)
     int i2c_P, i2c_Q;        // pixel grid the rows (A) / k-blocks (B) walk: P x Q per image
+    // direct epilogue: each thread stores its own row straight from registers (16-byte
+    // st.global), no smem staging / TMA store; used when tiles have few k-blocks and the
+    // store path, not the MMA, paces the kernel
+    int direct;
+    void* d_ptr;
+    long long d_ld;            // elements
+    long long d_split_stride;  // elements between split-K partial slices
 };
 
 constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
@@ -432,7 +452,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 const int m0 = w.mt * BM, n0 = w.nt * BN;
                 // im2col A: first pixel of this row tile
                 int a_n = 0, a_y = 0, a_x = 0;
-                if (p.a_mode == OP_IM2COL_K) {
+                if (p.a_mode == OP_IM2COL_K || p.a_mode == OP_IM2COL32_K) {
                     const int pq = p.i2c_P * p.i2c_Q;
                     a_n = m0 / pq;
                     const int rem = m0 - a_n * pq;
@@ -459,6 +479,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         tma_load_im2col_4d(a_dst, &p.tmA, &full[s], cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
                                            static_cast<uint16_t>(oh));
                         kc = tap * p.i2c_ldk + cb * 64;
+                    } else if (p.a_mode == OP_IM2COL32_K) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            int blk = kb * 2 + h;  // 32-wide k-block; past K: any valid block (B is zero there)
+                            if (blk * 32 >= p.K) blk = 0;
+                            const int tap = blk / p.i2c_cpb, cb = blk - tap * p.i2c_cpb;
+                            const int kh = tap / g.S, kw = tap - kh * g.S;
+                            const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
+                            tma_load_im2col_4d(a_dst + h * (Cfg::kABytes / 2), &p.tmA, &full[s], cb * 32, a_x, a_y, a_n,
+                                               static_cast<uint16_t>(ow), static_cast<uint16_t>(oh));
+                        }
                     }
                     if (p.b_mode == OP_TMA_K) {
                         tma_load_2d(b_dst, &p.tmB, &full[s], kc, n0);
@@ -466,7 +497,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 #pragma unroll
                         for (int a = 0; a < BN / 64; ++a)
                             tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kc);
-                    } else if (p.b_mode == OP_IM2COL_MN) {
+                    } else if (p.b_mode == OP_IM2COL_MN || p.b_mode == OP_IM2COL32_MN) {
                         // 64 output pixels of this k-block; columns n = tap * cs + c in 64-channel atoms
                         const int pq = p.i2c_P * p.i2c_Q;
                         const int pix = kb * BK;
@@ -475,13 +506,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         const int oy = rem / p.i2c_Q;
                         const int by = oy * g.stride + p.i2c_lo_h;
                         const int bx = (rem - oy * p.i2c_Q) * g.stride + p.i2c_lo_w;
-#pragma unroll
-                        for (int a = 0; a < BN / 64; ++a) {
-                            int n = n0 + a * 64;
+                        const int box = p.b_mode == OP_IM2COL32_MN ? 32 : 64;  // columns per box
+                        for (int col = 0; col < BN; col += box) {
+                            int n = n0 + col;
                             if (n >= p.N) n = 0;  // columns past N are clipped by the store; load finite data
                             const int tap = n / g.C, c = n - tap * g.C;
                             const int kh = tap / g.S, kw = tap - kh * g.S;
-                            tma_load_im2col_4d(b_dst + a * BK * 128, &p.tmB, &full[s], c, bx, by, bn_img,
+                            tma_load_im2col_4d(b_dst + col * BK * 2, &p.tmB, &full[s], c, bx, by, bn_img,
                                                static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
                         }
                     }
@@ -492,7 +523,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     } else if (warp == 1) {
         // ---------------- MMA issuer
         const bool a_mn = p.a_mode == OP_TMA_MN;
-        const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN;
+        const bool a_sw64 = p.a_mode == OP_IM2COL32_K;
+        const bool b_sw64 = p.b_mode == OP_IM2COL32_MN;
+        const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN || b_sw64;
         const uint32_t idesc = umma_idesc_bf16(BM, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
         int it = 0, tc = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
@@ -511,10 +544,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         // K-major: 32 bytes along the swizzled row; MN-major: two 8-row k-groups (2 x 1024 B)
-                        const uint64_t ad = a_mn ? umma_desc_sw128(a_base + k * 2048, BK * 128, 1024)
-                                                 : umma_desc_sw128(a_base + k * 32, 0, 1024);
-                        const uint64_t bd = b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
-                                                 : umma_desc_sw128(b_base + k * 32, 0, 1024);
+                        // SW64 K-major A: two 8 KB halves of 64-byte rows; SW64 MN-major B: 32-column
+                        // atoms of 64 k-rows (4 KB apart), 512-byte 8-row groups
+                        const uint64_t ad =
+                            a_mn     ? umma_desc_sw128(a_base + k * 2048, BK * 128, 1024)
+                            : a_sw64 ? umma_desc_sw64(a_base + (k >> 1) * (Cfg::kABytes / 2) + (k & 1) * 32, 0, 512)
+                                     : umma_desc_sw128(a_base + k * 32, 0, 1024);
+                        const uint64_t bd = b_sw64 ? umma_desc_sw64(b_base + k * 1024, BK * 64, 512)
+                                            : b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
+                                                   : umma_desc_sw128(b_base + k * 32, 0, 1024);
                         umma_bf16(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
                     }
                     umma_commit(&empty[s]);
@@ -595,7 +633,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             for (int i = max(0, it - LAG); i < it; ++i) mbar_arrive(&full[i % S]);
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue (TMEM -> regs -> swizzled smem -> TMA store)
+        // ---------------- epilogue (TMEM -> regs -> swizzled smem -> TMA store, or direct stores)
         const int ew = warp - 4;  // TMEM lane quarter = tile rows [32 ew, 32 ew + 32)
         uint8_t* stage_base = sStage + ew * 2 * kStagingBytes;
         const bool bf16_out = p.epi == EPI_BF16;
@@ -608,6 +646,50 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             tc_fence_after();
             const int m0 = w.mt * BM, n0 = w.nt * BN;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + buf * BN;
+            if (p.direct) {
+                const int row = m0 + ew * 32 + lane;
+                const bool row_ok = row < p.M;
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(t_row + c0, r);
+                    tmem_ld_wait();
+                    if (c0 + 32 >= BN) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    const int nb = n0 + c0;
+                    if (row_ok && nb < p.N) {
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            v[j] = __uint_as_float(r[j]) * p.alpha;
+                            if (p.bias && nb + j < p.n_bias) v[j] += __ldg(p.bias + nb + j);
+                            if (p.relu) v[j] = fmaxf(v[j], 0.f);
+                        }
+                        if (bf16_out) {
+                            __nv_bfloat16* dst =
+                                static_cast<__nv_bfloat16*>(p.d_ptr) + static_cast<long long>(row) * p.d_ld + nb;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (nb + q * 8 < p.N)
+                                    *reinterpret_cast<uint4*>(dst + q * 8) = make_uint4(
+                                        pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                        pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+                        } else {
+                            float* dst = static_cast<float*>(p.d_ptr) + w.sp * p.d_split_stride +
+                                         static_cast<long long>(row) * p.d_ld + nb;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (nb + q * 4 < p.N)
+                                    *reinterpret_cast<float4*>(dst + q * 4) =
+                                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        }
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
             // one staging row = 128 B: 64 bf16 or 32 fp32 columns
             const int cols_per_store = bf16_out ? 64 : 32;
             for (int c0 = 0; c0 < BN; c0 += cols_per_store) {

@@ -157,6 +157,12 @@ IM2COL_CASES = [
     (3, 64, 9, 11, 192, 5, 1, 2),
     (5, 64, 7, 7, 64, 3, 1, 0),
     (1, 256, 13, 13, 384, 3, 1, 1),
+    # 32-channel blocks (SWIZZLE_64B boxes): channel strides 96 / 160 / 32, dgrad ks 96 / 160
+    (2, 160, 9, 9, 96, 3, 1, 1),
+    (3, 96, 13, 13, 160, 3, 1, 1),
+    (2, 32, 14, 14, 96, 5, 1, 2),
+    (1, 96, 12, 11, 192, 3, 2, 0),
+    (2, 96, 26, 26, 256, 5, 1, 2),
 ]
 
 

@@ -54,7 +54,7 @@ def storage_final_vars(net):
     return sorted(last.values())
 
 
-def sensitivity(net, x, y, seed=11):
+def sensitivity(net, x, y, seed=11, with_loss=False):
     """Rounding envelope of the step: distance between the fp32 oracle and the
     same oracle emulating the device's storage precision (every bf16-stored
     activation rounded to bf16, bf16 weight operands).  Deep ReLU / max-pool /
@@ -67,10 +67,12 @@ def sensitivity(net, x, y, seed=11):
     a.init_params()
     b.init_params()
     b.set_bf16_storage(True)
+    losses = []
     for o in (a, b):
         o.set_batch(x, y)
-        o.step(0, update=False)
-    return [rel(b.grad(i), a.grad(i)) for i in range(len(net.params))]
+        losses.append(o.step(0, update=False))
+    env = [rel(b.grad(i), a.grad(i)) for i in range(len(net.params))]
+    return (env, abs(losses[1] - losses[0])) if with_loss else env
 
 
 @pytest.mark.parametrize("name,batch", [("lenet", 16), ("inception", 4), ("alexnet", 2)])
@@ -172,8 +174,10 @@ def test_big_network_step_parity(name, batch):
     tr.step(0, update=False)
     lg = tr.loss()
     lo = o.step(0, update=False, keep=True)
-    assert abs(lg - lo) <= 2e-2 * abs(lo), (lg, lo)
-    env = sensitivity(net, x, y)
+    env, loss_env = sensitivity(net, x, y, with_loss=True)
+    # 50+ BN/ReLU layers at batch 2: the bf16 rounding walk of the forward moves the loss by
+    # ~1-3% (the oracle's own bf16-storage run shows it); judged against that envelope
+    assert abs(lg - lo) <= max(2e-2 * abs(lo), 3 * loss_env), (lg, lo, loss_env)
     bad = [(p.name, rel(tr.grad(i), o.grad(i)), env[i]) for i, p in enumerate(net.params)
            if rel(tr.grad(i), o.grad(i)) > 3 * env[i] + 2e-2]
     assert not bad, bad[:5]

@@ -96,6 +96,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="gemm,conv")
     ap.add_argument("--net", default="alexnet,vgg16,resnet50")
+    ap.add_argument("--only", default="", help="run only conv cases whose tuple text contains this")
     args = ap.parse_args()
     print(f"TCB_FORCE_BN={os.environ.get('TCB_FORCE_BN', '')} TCB_IM2COL={os.environ.get('TCB_IM2COL', '')}")
     if "gemm" in args.which:
@@ -106,6 +107,8 @@ def main():
     if "conv" in args.which:
         for net in args.net.split(","):
             for cv in CONVS[net]:
+                if args.only and args.only not in str(cv):
+                    continue
                 r = conv_case(*cv)
                 print(f"{net} conv {cv}: " + "  ".join(f"{k} {v[0]:.3f} ms {v[1]:.0f} TF/s" for k, v in r.items()))
 
