@@ -40,3 +40,10 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# Kernel A/B variant: make variant VARIANT=name VFLAGS="-DFOO" -> _lib/libtcb200_name.so (TCB_LIB_VARIANT=name)
+variant:
+	rm -rf build/v_$(VARIANT) && mkdir -p build/v_$(VARIANT)
+	for f in $(CU_SRC); do $(NVCC) $(NVFLAGS) $(VFLAGS) -c $$f -o build/v_$(VARIANT)/$$(basename $$f).o || exit 1; done
+	for f in $(CPP_SRC); do $(CXX) $(CXXFLAGS) -c $$f -o build/v_$(VARIANT)/$$(basename $$f).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $(LIBDIR)/libtcb200_$(VARIANT).so build/v_$(VARIANT)/*.o -cudart static -lnccl -ldl -lpthread

@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtcb200.so")
+# TCB_LIB_VARIANT=<name> loads _lib/libtcb200_<name>.so (kernel A/B experiments)
+LIB_PATH = os.path.join(_HERE, "_lib", "libtcb200" + (f"_{os.environ['TCB_LIB_VARIANT']}" if os.environ.get(
+    "TCB_LIB_VARIANT") else "") + ".so")
 
 TC_OK = 0
 STATUS_NAMES = {

@@ -125,16 +125,6 @@ static bool im2col_enabled() {
     }();
     return on;
 }
-// TCB_EPI_DIRECT=1 selects the direct-store epilogue (registers -> st.global) instead of
-// the swizzled-smem + TMA-store path.  Measured slower on every shape tried (ResNet 1x1
-// K=64: 88 vs 52 us), so it is opt-in for experiments only.
-static int epi_direct_env() {
-    static const int v = [] {
-        const char* e = std::getenv("TCB_EPI_DIRECT");
-        return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
-    return v;
-}
 static bool corner_ok(int v) { return v >= -128 && v <= 127; }
 
 // 3-D store map {N, M, splits} for the epilogue: SW128, box = 128 B of columns x 32 rows x 1.
@@ -271,11 +261,6 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
     const bool partial = lp.splits > 1 || beta != 0.f;
-    const int de = epi_direct_env();
-    p.direct = de > 0 ? 1 : 0;
-    p.d_ptr = partial ? ws : D;
-    p.d_ld = partial ? p.N : ldd;
-    p.d_split_stride = partial ? static_cast<long long>(p.M) * p.N : 0;
     std::string err;
     if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);

@@ -81,13 +81,6 @@ struct GemmParams {
     int i2c_lo_w, i2c_lo_h;  // first source pixel of output pixel (y, x) = (y * stride + lo_h, x * stride + lo_w)
     int i2c_flip;            // bwd-data: tap (kh, kw) is the offset (R-1-kh, S-1-kw)
     int i2c_P, i2c_Q;        // pixel grid the rows (A) / k-blocks (B) walk: P x Q per image
-    // direct epilogue: each thread stores its own row straight from registers (16-byte
-    // st.global), no smem staging / TMA store; used when tiles have few k-blocks and the
-    // store path, not the MMA, paces the kernel
-    int direct;
-    void* d_ptr;
-    long long d_ld;            // elements
-    long long d_split_stride;  // elements between split-K partial slices
 };
 
 constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
@@ -429,7 +422,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
+            mbar_init(&tempty[b], any_gather ? 4 : 8);  // one arrival per epilogue warp
         }
         fence_mbar_init();
     }
@@ -561,7 +554,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 __syncwarp();
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= 8 && any_gather) {
         // ---------------- im2col gather producers (128 threads)
         if (any_gather) {
             constexpr int LAG = Cfg::kLag;
@@ -633,9 +626,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             for (int i = max(0, it - LAG); i < it; ++i) mbar_arrive(&full[i % S]);
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue (TMEM -> regs -> swizzled smem -> TMA store, or direct stores)
-        const int ew = warp - 4;  // TMEM lane quarter = tile rows [32 ew, 32 ew + 32)
-        uint8_t* stage_base = sStage + ew * 2 * kStagingBytes;
+        // ---------------- epilogue (TMEM -> regs -> swizzled smem -> TMA store)
+        // Without im2col gathers, warps 8-11 join the epilogue: warp e (0..7) reads TMEM lane
+        // quarter e % 4 (tile rows [32 (e % 4), +32)) and the 64-column chunks of its group
+        // e / 4; the 8 staging buffers are then one per warp instead of two.
+        const int ew = warp - 4;
+        const int quarter = ew & 3, grp = ew >> 2;
+        const int ngrp = any_gather ? 1 : 2;
+        const int nbuf = 2 / ngrp;
+        uint8_t* stage_base = sStage + ew * nbuf * kStagingBytes;
         const bool bf16_out = p.epi == EPI_BF16;
         int nstore = 0;
         int tc = 0;
@@ -645,110 +644,80 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             mbar_wait(&tfull[buf], (tc >> 1) & 1);
             tc_fence_after();
             const int m0 = w.mt * BM, n0 = w.nt * BN;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + buf * BN;
-            if (p.direct) {
-                const int row = m0 + ew * 32 + lane;
-                const bool row_ok = row < p.M;
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(t_row + c0, r);
-                    tmem_ld_wait();
-                    if (c0 + 32 >= BN) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[buf]);
-                    }
-                    const int nb = n0 + c0;
-                    if (row_ok && nb < p.N) {
-                        float v[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            v[j] = __uint_as_float(r[j]) * p.alpha;
-                            if (p.bias && nb + j < p.n_bias) v[j] += __ldg(p.bias + nb + j);
-                            if (p.relu) v[j] = fmaxf(v[j], 0.f);
-                        }
-                        if (bf16_out) {
-                            __nv_bfloat16* dst =
-                                static_cast<__nv_bfloat16*>(p.d_ptr) + static_cast<long long>(row) * p.d_ld + nb;
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if (nb + q * 8 < p.N)
-                                    *reinterpret_cast<uint4*>(dst + q * 8) = make_uint4(
-                                        pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                                        pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-                        } else {
-                            float* dst = static_cast<float*>(p.d_ptr) + w.sp * p.d_split_stride +
-                                         static_cast<long long>(row) * p.d_ld + nb;
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (nb + q * 4 < p.N)
-                                    *reinterpret_cast<float4*>(dst + q * 4) =
-                                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                        }
-                    }
-                    __syncwarp();
-                }
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
+            if (grp * 64 >= BN) {  // no chunk for this warp (BN = 64 with two groups)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
                 continue;
             }
-            // one staging row = 128 B: 64 bf16 or 32 fp32 columns
-            const int cols_per_store = bf16_out ? 64 : 32;
-            for (int c0 = 0; c0 < BN; c0 += cols_per_store) {
-                uint32_t packed[32];
-                if (bf16_out) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t r[32];
-                        tmem_ld32(t_row + c0 + h * 32, r);
-                        tmem_ld_wait();
-                        const int nb = n0 + c0 + h * 32;
-#pragma unroll
-                        for (int j = 0; j < 32; j += 2) {
-                            float v0 = __uint_as_float(r[j]) * p.alpha, v1 = __uint_as_float(r[j + 1]) * p.alpha;
-                            if (p.bias) {
-                                if (nb + j < p.n_bias) v0 += __ldg(p.bias + nb + j);
-                                if (nb + j + 1 < p.n_bias) v1 += __ldg(p.bias + nb + j + 1);
-                            }
-                            if (p.relu) {
-                                v0 = fmaxf(v0, 0.f);
-                                v1 = fmaxf(v1, 0.f);
-                            }
-                            packed[h * 16 + j / 2] = pack_bf16x2(v0, v1);
-                        }
-                    }
-                } else {
-                    tmem_ld32(t_row + c0, packed);
-                    tmem_ld_wait();
-                    const int nb = n0 + c0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        float v = __uint_as_float(packed[j]) * p.alpha;
-                        if (p.bias && nb + j < p.n_bias) v += __ldg(p.bias + nb + j);
-                        if (p.relu) v = fmaxf(v, 0.f);
-                        packed[j] = __float_as_uint(v);
-                    }
+            // One staging row = 128 B (64 bf16 or 32 fp32 columns).  The two TMEM reads of a
+            // 64-column chunk are issued back to back and waited once; the chunk's bias values
+            // are fetched one per lane meanwhile and broadcast with shuffles.
+            for (int c0 = grp * 64; c0 < BN; c0 += 64 * ngrp) {
+                uint32_t r0[32], r1[32];
+                tmem_ld32(t_row + c0, r0);
+                tmem_ld32(t_row + c0 + 32, r1);
+                const int nb = n0 + c0;
+                float b0 = 0.f, b1 = 0.f;
+                if (p.bias) {
+                    if (nb + lane < p.n_bias) b0 = __ldg(p.bias + nb + lane);
+                    if (nb + 32 + lane < p.n_bias) b1 = __ldg(p.bias + nb + 32 + lane);
                 }
-                if (c0 + cols_per_store >= BN) {
-                    // all TMEM reads of this accumulator are done: hand it back to the MMA warp
+                tmem_ld_wait();
+                if (c0 + 64 * ngrp >= BN) {
+                    // this warp's TMEM reads of the accumulator are done: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[buf]);
                 }
-                // staging buffer reuse: the TMA store issued two stores ago must have read it
-                uint8_t* stg = stage_base + (nstore & 1) * kStagingBytes;
-                if (nstore >= 2 && lane == 0) bulk_wait_read<1>();
-                __syncwarp();
-                const uint32_t row_addr = smem_u32(stg);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    st_shared_v4(row_addr + sw128_off(lane, q), packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                 packed[4 * q + 3]);
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_3d(&p.tmD, stg, n0 + c0, m0 + ew * 32, w.sp);
-                    bulk_commit();
+                for (int j = 0; j < 32; ++j) {
+                    float v0 = __uint_as_float(r0[j]) * p.alpha, v1 = __uint_as_float(r1[j]) * p.alpha;
+                    if (p.bias) {
+                        v0 += __shfl_sync(0xffffffffu, b0, j);
+                        v1 += __shfl_sync(0xffffffffu, b1, j);
+                    }
+                    if (p.relu) {
+                        v0 = fmaxf(v0, 0.f);
+                        v1 = fmaxf(v1, 0.f);
+                    }
+                    r0[j] = __float_as_uint(v0);
+                    r1[j] = __float_as_uint(v1);
                 }
-                ++nstore;
+                const int nrows = bf16_out ? 1 : 2;  // 128-byte staging rows in this chunk
+                for (int sub = 0; sub < nrows; ++sub) {
+                    uint32_t packed[32];
+                    if (bf16_out) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            packed[j] = pack_bf16x2(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+                            packed[16 + j] = pack_bf16x2(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) packed[j] = sub ? r1[j] : r0[j];
+                    }
+                    // staging buffer reuse: the TMA store issued two stores ago must have read it
+                    uint8_t* stg = stage_base + (nstore % nbuf) * kStagingBytes;
+                    if (lane == 0 && nstore >= nbuf) {
+                        if (nbuf == 2) bulk_wait_read<1>();
+                        else bulk_wait_read<0>();
+                    }
+                    __syncwarp();
+                    const uint32_t row_addr = smem_u32(stg);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        st_shared_v4(row_addr + sw128_off(lane, q), packed[4 * q], packed[4 * q + 1],
+                                     packed[4 * q + 2], packed[4 * q + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&p.tmD, stg, nb + sub * 32, m0 + quarter * 32, w.sp);
+                        bulk_commit();
+                    }
+                    ++nstore;
+                }
             }
         }
         if (lane == 0) bulk_wait<0>();

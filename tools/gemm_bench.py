@@ -96,12 +96,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="gemm,conv")
     ap.add_argument("--net", default="alexnet,vgg16,resnet50")
+    ap.add_argument("--small-k", action="store_true", help="GEMM shapes of 1x1 convs (epilogue-paced)")
     ap.add_argument("--only", default="", help="run only conv cases whose tuple text contains this")
     args = ap.parse_args()
     print(f"TCB_FORCE_BN={os.environ.get('TCB_FORCE_BN', '')} TCB_IM2COL={os.environ.get('TCB_IM2COL', '')}")
     if "gemm" in args.which:
-        for M, N, K in [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096),
-                        (4096, 4096, 4096)]:
+        shapes = [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096), (4096, 4096, 4096)]
+        if args.small_k:
+            shapes = [(200704, 256, k) for k in (64, 128, 256, 512, 1024)] + [(200704, 64, 256), (50176, 1024, 256)]
+        for M, N, K in shapes:
             ms, tf = gemm_case(M, N, K)
             print(f"gemm {M}x{N}x{K}: {ms:.3f} ms {tf:.0f} TF/s")
     if "conv" in args.which:
