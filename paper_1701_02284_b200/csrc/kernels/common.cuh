@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "status.hpp"
 #include "tc_abi.h"
@@ -38,6 +39,34 @@ inline void count_launch(unsigned n = 1) { g_launches.fetch_add(n, std::memory_o
 // outer = row count, row_stride in elements.
 bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
                        uint32_t box_inner, uint32_t box_outer, std::string* err);
+
+// Programmatic dependent launch (PDL): every kernel of the step is launched with
+// programmatic stream serialisation, starts with griddepcontrol.wait (no global memory
+// access before the previous kernel has completed and flushed) and immediately allows
+// its own dependents to launch, so a kernel's launch latency and prologue (barrier
+// init, TMEM allocation, tensor-map prefetch) overlap the tail of its predecessor.
+// Off by default (TCB_PDL=1 enables the attribute; see pdl_enabled()).
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#define TCB_LAUNCH(kernel, ...) ::tcb::launch_kernel(kernel, __VA_ARGS__)  // (kernel, grid, block, smem, stream, args...)
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 int num_sms();

@@ -13,6 +13,16 @@ namespace tcb {
 
 std::atomic<unsigned long long> g_launches{0};
 
+// Measured neutral-to-slightly-negative on the AlexNet / ResNet-50 steps (the graph already
+// hides launch latency and a GEMM CTA owns the whole register file), so it is opt-in: TCB_PDL=1.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 int num_sms() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -159,6 +169,8 @@ static bool make_tmap_store(CUtensorMap* map, void* base, bool bf16, uint64_t N,
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
                                      int n_bias, int relu, float beta) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = static_cast<long long>(M) * N;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -244,7 +256,7 @@ static tc_status launch_bn(const GemmParams& p, dim3 grid, cudaStream_t st) {
         attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (attr_err != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(attr_err));
-    tc_gemm_kernel<BN><<<grid, kNumThreads, smem, st>>>(p);
+    TCB_LAUNCH((tc_gemm_kernel<BN>), grid, kNumThreads, smem, st, p);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -288,7 +300,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (partial) {
         const long long total = static_cast<long long>(p.M) * p.N;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
-        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(ws), lp.splits, p.M, p.N,
+        TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
                                                      static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
                                                      relu, beta);
         TCB_LAUNCH_CHECK();

@@ -38,6 +38,8 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 // ---------------------------------------------------------------- elementwise (8 x bf16 per thread)
 __global__ void k_relu_fwd(const uint4* __restrict__ x, uint4* __restrict__ y, long long n8) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float f[8];
@@ -50,6 +52,8 @@ __global__ void k_relu_fwd(const uint4* __restrict__ x, uint4* __restrict__ y, l
 
 __global__ void k_relu_bwd(const uint4* __restrict__ dy, const uint4* __restrict__ y, uint4* __restrict__ dx,
                            long long n8) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float g[8], f[8];
@@ -62,6 +66,8 @@ __global__ void k_relu_bwd(const uint4* __restrict__ dy, const uint4* __restrict
 }
 
 __global__ void k_add(const uint4* __restrict__ a, const uint4* __restrict__ b, uint4* __restrict__ y, long long n8) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float p[8], q[8];
@@ -75,6 +81,8 @@ __global__ void k_add(const uint4* __restrict__ a, const uint4* __restrict__ b, 
 
 __global__ void k_mask_mul(const uint4* __restrict__ x, const uint2* __restrict__ keep, float scale,
                            uint4* __restrict__ y, long long n8) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float f[8];
@@ -90,6 +98,8 @@ __global__ void k_mask_mul(const uint4* __restrict__ x, const uint2* __restrict_
 // keep mask for every stored element of an NHWC (or [N][Fs] with H=W=1) tensor.
 __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, int C, int cs, float rate,
                                uint64_t seed, uint32_t var, const uint32_t* iter_n0) {
+    pdl_wait();
+    pdl_trigger();
     const uint32_t iter = iter_n0[0], n0 = iter_n0[1];
     const long long total = static_cast<long long>(N) * H * W * cs;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -116,6 +126,8 @@ __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, 
 // stream costs 1 B per output instead of 4.
 __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
                            uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
+    pdl_wait();
+    pdl_trigger();
     const int cg = xi.cs / 8;
     const long long total = yo.pixels() * cg;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
@@ -174,6 +186,8 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
 // (no atomics; fixed window order, deterministic).
 __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
                            bf16* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
+    pdl_wait();
+    pdl_trigger();
     const int cg = xi.cs / 8;
     const long long total = xi.pixels() * cg;
     const float inv = 1.f / static_cast<float>(k * k);
@@ -219,6 +233,8 @@ __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* 
 // ---------------------------------------------------------------- LRN (across channels, one warp per pixel)
 __global__ void k_lrn_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, int size, float alpha, float beta,
                           float kk) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float sm[];
     const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
     float* sq = sm + wid * a.cs;
@@ -248,6 +264,8 @@ __global__ void k_lrn_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4
 
 __global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
                           bf16* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float sm[];
     const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
     float* sq = sm + wid * 3 * a.cs;
@@ -286,6 +304,8 @@ __global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ 
 
 // ---------------------------------------------------------------- softmax / loss head (fp32)
 __global__ void k_softmax_fwd(const bf16* __restrict__ x, long long ld, float* __restrict__ y, int rows, int F) {
+    pdl_wait();
+    pdl_trigger();
     const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int r = blockIdx.x * warps + wid; r < rows; r += gridDim.x * warps) {
         const bf16* xr = x + r * ld;
@@ -302,6 +322,8 @@ __global__ void k_softmax_fwd(const bf16* __restrict__ x, long long ld, float* _
 
 __global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restrict__ y, bf16* __restrict__ dx,
                               long long ld, int rows, int F) {
+    pdl_wait();
+    pdl_trigger();
     const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int r = blockIdx.x * warps + wid; r < rows; r += gridDim.x * warps) {
         const long long o = static_cast<long long>(r) * F;
@@ -315,6 +337,8 @@ __global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restr
 
 __global__ void k_f32_ew(int op, const float* __restrict__ a, const float* __restrict__ b, float scale,
                          float* __restrict__ y, long long n) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const float v = a[i];
@@ -331,6 +355,8 @@ __global__ void k_f32_ew(int op, const float* __restrict__ a, const float* __res
 }
 
 __global__ void k_onehot(const int32_t* __restrict__ labels, float* __restrict__ y, int N, int K) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = static_cast<long long>(N) * K;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -351,6 +377,8 @@ struct LossArgs {
 // resets the counter for the next step (graph replays).
 constexpr int kLossBlocks = 32;
 __global__ void __launch_bounds__(256) k_loss(LossArgs args, float* out, double* partial, unsigned* ticket) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double red[256];
     __shared__ bool last;
     double acc = 0.0;
@@ -420,6 +448,8 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
                                                              const float* __restrict__ stats, long long rows, int C,
                                                              int ld, int ct, long long rps, int splits,
                                                              float* __restrict__ part) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float sm[(MODE == RED_SUM ? 1 : 2) * kRedThreads * 8];
     const int tpr = ct >> 3;
     const int rpi = kRedThreads / tpr;
@@ -512,6 +542,8 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
                                                     float* __restrict__ out, const bf16* __restrict__ x, long long rows,
                                                     float eps, const float* __restrict__ gamma,
                                                     const float* __restrict__ beta, float* __restrict__ coef) {
+    pdl_wait();
+    pdl_trigger();
     // 32 channels per block; 8 split-lanes per channel, each summing a fixed strided subset,
     // combined in lane order (deterministic)
     __shared__ float sa_sm[8][33], sb_sm[8][33];
@@ -557,6 +589,8 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
 __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restrict__ coef, uint4* __restrict__ y,
                               long long n8, int ld8, int C) {
+    pdl_wait();
+    pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
         uint4 q[2];
@@ -580,6 +614,8 @@ __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restri
 // dx = gamma*istd*(dy - sum(dy)/M - xhat*sum(dy*xhat)/M) = k1*dy + k2*x + k3 (per channel)
 __global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __restrict__ stats,
                               const float* __restrict__ sums, float* __restrict__ k, int C, float invm) {
+    pdl_wait();
+    pdl_trigger();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     const float is = stats[C + c], mean = stats[c];
@@ -592,6 +628,8 @@ __global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __re
 
 __global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ k,
                                uint4* __restrict__ dx, long long n8, int ld8, int C) {
+    pdl_wait();
+    pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
         uint4 q[2], r[2];
@@ -621,6 +659,8 @@ __global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __rest
 
 __global__ void k_bias_add(const bf16* __restrict__ x, const float* __restrict__ b, bf16* __restrict__ y, long long rows,
                            int cols, long long ld, int relu) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = rows * ld;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -633,6 +673,8 @@ __global__ void k_bias_add(const bf16* __restrict__ x, const float* __restrict__
 
 __global__ void k_channel_copy(const bf16* __restrict__ src, int src_cs, bf16* __restrict__ dst, int dst_cs, int off,
                                int c, long long pixels) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = pixels * c;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -645,6 +687,8 @@ __global__ void k_channel_copy(const bf16* __restrict__ src, int src_cs, bf16* _
 // ---------------------------------------------------------------- dense im2col (small-C first layers)
 __global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo,
                          int Kp, bf16* __restrict__ col) {
+    pdl_wait();
+    pdl_trigger();
     const int groups = Kp / 8;
     const long long total = static_cast<long long>(xi.N) * Ho * Wo * groups;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
@@ -698,6 +742,8 @@ __device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, i
 template <int HALF>
 __global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, float alpha, float beta,
                            float kk) {
+    pdl_wait();
+    pdl_trigger();
     const int ng = a.cs / 8;
     const long long total = a.pixels() * ng;
     const float an = alpha / static_cast<float>(2 * HALF + 1);
@@ -723,6 +769,8 @@ __global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act
 template <int HALF>
 __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
                            bf16* __restrict__ dx, Act4 a, float alpha, float beta, float kk) {
+    pdl_wait();
+    pdl_trigger();
     const int ng = a.cs / 8;
     const long long total = a.pixels() * ng;
     const float an = alpha / static_cast<float>(2 * HALF + 1);
@@ -759,37 +807,59 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
 }
 
 // ---------------------------------------------------------------- input staging
-__global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y, int N, int C, int H, int W, int cs) {
-    const long long total = static_cast<long long>(N) * H * W * cs;
+// Source coordinates of staged element i; false for padding (channel pad or outside the image).
+__device__ __forceinline__ bool stage_src(const StageLayout& L, long long i, int& n, int& c, int& h, int& w) {
+    if (!L.s2d) {
+        c = static_cast<int>(i % L.cs);
+        long long p = i / L.cs;
+        w = static_cast<int>(p % L.W);
+        p /= L.W;
+        h = static_cast<int>(p % L.H);
+        n = static_cast<int>(p / L.H);
+        return c < L.C;
+    }
+    const int cc = L.s2d * L.s2d * L.cs;
+    const int ch = static_cast<int>(i % cc);
+    long long p = i / cc;
+    const int Q = static_cast<int>(p % L.Ws);
+    p /= L.Ws;
+    const int P = static_cast<int>(p % L.Hs);
+    n = static_cast<int>(p / L.Hs);
+    c = ch % L.cs;
+    const int ij = ch / L.cs;
+    h = P * L.s2d + ij / L.s2d - L.pad;
+    w = Q * L.s2d + ij % L.s2d - L.pad;
+    return c < L.C && h >= 0 && h < L.H && w >= 0 && w < L.W;
+}
+
+__global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y, StageLayout L) {
+    pdl_wait();
+    pdl_trigger();
+    const long long total = L.elems();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % cs);
-        long long p = i / cs;
-        const int w = static_cast<int>(p % W);
-        p /= W;
-        const int h = static_cast<int>(p % H);
-        const int n = static_cast<int>(p / H);
-        y[i] = __float2bfloat16_rn(c < C ? x[((static_cast<long long>(n) * C + c) * H + h) * W + w] : 0.f);
+        int n, c, h, w;
+        const bool ok = stage_src(L, i, n, c, h, w);
+        y[i] = __float2bfloat16_rn(ok ? x[((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W + w] : 0.f);
     }
 }
 
-__global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, int N, int C, int H, int W, int cs,
-                        int classes, uint64_t seed, uint32_t iter, uint32_t n0) {
-    const long long total = static_cast<long long>(N) * H * W * cs;
+__global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, StageLayout L, int classes, uint64_t seed,
+                        uint32_t iter, uint32_t n0) {
+    pdl_wait();
+    pdl_trigger();
+    const long long total = L.elems();
+    const long long per_img = total / L.N;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % cs);
-        long long p = i / cs;
-        const int w = static_cast<int>(p % W);
-        p /= W;
-        const int h = static_cast<int>(p % H);
-        const int n = static_cast<int>(p / H);
+        int n, c, h, w;
+        const bool ok = stage_src(L, i, n, c, h, w);
         const uint32_t ng = n0 + n;
         const uint32_t y = tcp_label(seed, ng, iter, classes);
-        if (c == 0 && h == 0 && w == 0) labels[n] = static_cast<int32_t>(y);
+        if (i % per_img == 0) labels[n] = static_cast<int32_t>(y);
         float v = 0.f;
-        if (c < C) {
-            const uint32_t e = static_cast<uint32_t>((static_cast<long long>(c) * H + h) * W + w);
+        if (ok) {
+            const uint32_t e = static_cast<uint32_t>((static_cast<long long>(c) * L.H + h) * L.W + w);
             float u1, u2;
             tcp_uniform_pair(seed, ng, iter, e, &u1, &u2);
             const double r = sqrt(-2.0 * log(static_cast<double>(u1)));
@@ -801,8 +871,25 @@ __global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, int 
     }
 }
 
+__global__ void k_s2d_mask_grad(float* __restrict__ g, int K, long long ld, int Rp, int s, int cs, int R, int S) {
+    pdl_wait();
+    pdl_trigger();
+    const int cols = Rp * Rp * s * s * cs;
+    const long long total = static_cast<long long>(K) * cols;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int col = static_cast<int>(t % cols);
+        const int k = static_cast<int>(t / cols);
+        const int ab = col / (s * s * cs), ij = (col / cs) % (s * s);
+        const int kh = (ab / Rp) * s + ij / s, kw = (ab % Rp) * s + ij % s;
+        if (kh >= R || kw >= S) g[k * ld + col] = 0.f;
+    }
+}
+
 // ---------------------------------------------------------------- SGD
 __global__ void k_set_iter(uint32_t* d, uint32_t iter, uint32_t n0) {
+    pdl_wait();
+    pdl_trigger();
     d[0] = iter;
     d[1] = n0;
 }
@@ -835,6 +922,8 @@ __device__ __forceinline__ void sgd_scalar(const SgdTensor& t, long long i) {
 }
 
 __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = b.start4[b.nt];
     for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < total;
          u += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -882,24 +971,24 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
 #define EW_GRID(n) grid_for((n)), kThreads, 0, st
 
 tc_status launch_relu_fwd(const bf16* x, bf16* y, long long n, cudaStream_t st) {
-    k_relu_fwd<<<EW_GRID(n / 8)>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), n / 8);
+    TCB_LAUNCH(k_relu_fwd, EW_GRID(n / 8), reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, cudaStream_t st) {
-    k_relu_bwd<<<EW_GRID(n / 8)>>>(reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y),
+    TCB_LAUNCH(k_relu_bwd, EW_GRID(n / 8), reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y),
                                     reinterpret_cast<uint4*>(dx), n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, cudaStream_t st) {
-    k_add<<<EW_GRID(n / 8)>>>(reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
+    TCB_LAUNCH(k_add, EW_GRID(n / 8), reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
                                reinterpret_cast<uint4*>(y), n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16* y, long long n, cudaStream_t st) {
-    k_mask_mul<<<EW_GRID(n / 8)>>>(reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint2*>(keep), scale,
+    TCB_LAUNCH(k_mask_mul, EW_GRID(n / 8), reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint2*>(keep), scale,
                                     reinterpret_cast<uint4*>(y), n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -907,33 +996,33 @@ tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16*
 tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st) {
     const long long n = static_cast<long long>(N) * H * W * cs;
-    k_dropout_mask<<<EW_GRID(n)>>>(keep, N, H, W, C, cs, rate, seed, var, iter_n0);
+    TCB_LAUNCH(k_dropout_mask, EW_GRID(n), keep, N, H, W, C, cs, rate, seed, var, iter_n0);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
     if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
-    k_pool_fwd<<<EW_GRID(yo.pixels() * (xi.cs / 8))>>>(x, xi, y, yo, idx, k, stride, pad, is_max);
+    TCB_LAUNCH(k_pool_fwd, EW_GRID(yo.pixels() * (xi.cs / 8)), x, xi, y, yo, idx, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
-    k_pool_bwd<<<EW_GRID(xi.pixels() * (xi.cs / 8))>>>(dy, yo, idx, dx, xi, k, stride, pad, is_max);
+    TCB_LAUNCH(k_pool_bwd, EW_GRID(xi.pixels() * (xi.cs / 8)), dy, yo, idx, dx, xi, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
     switch (size) {  // odd windows up to 9: register-resident template kernels
-        case 3: k_lrn2_fwd<1><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
-        case 5: k_lrn2_fwd<2><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
-        case 7: k_lrn2_fwd<3><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
-        case 9: k_lrn2_fwd<4><<<EW_GRID(n)>>>(x, y, a, alpha, beta, k); break;
+        case 3: TCB_LAUNCH((k_lrn2_fwd<1>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 5: TCB_LAUNCH((k_lrn2_fwd<2>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 7: TCB_LAUNCH((k_lrn2_fwd<3>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 9: TCB_LAUNCH((k_lrn2_fwd<4>), EW_GRID(n), x, y, a, alpha, beta, k); break;
         default: {  // general path: warp per pixel with the channel vector in shared memory
             const int warps = 8;
-            k_lrn_fwd<<<grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st>>>(x, y, a, size,
+            TCB_LAUNCH(k_lrn_fwd, grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st, x, y, a, size,
                                                                                                      alpha, beta, k);
         }
     }
@@ -944,13 +1033,13 @@ tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx,
                          float beta, float k, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
     switch (size) {
-        case 3: k_lrn2_bwd<1><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
-        case 5: k_lrn2_bwd<2><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
-        case 7: k_lrn2_bwd<3><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
-        case 9: k_lrn2_bwd<4><<<EW_GRID(n)>>>(dy, x, y, dx, a, alpha, beta, k); break;
+        case 3: TCB_LAUNCH((k_lrn2_bwd<1>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 5: TCB_LAUNCH((k_lrn2_bwd<2>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 7: TCB_LAUNCH((k_lrn2_bwd<3>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 9: TCB_LAUNCH((k_lrn2_bwd<4>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
         default: {
             const int warps = 8;
-            k_lrn_bwd<<<grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st>>>(
+            TCB_LAUNCH(k_lrn_bwd, grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st, 
                 dy, x, y, dx, a, size, alpha, beta, k);
         }
     }
@@ -960,28 +1049,28 @@ tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx,
 tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
                         cudaStream_t st) {
     if (Kp % 8) return fail(TC_INVALID_ARG, "im2col: Kp must be a multiple of 8");
-    k_im2col<<<EW_GRID(static_cast<long long>(xi.N) * Ho * Wo * (Kp / 8))>>>(x, xi, R, S, stride, pad, Ho, Wo, Kp, col);
+    TCB_LAUNCH(k_im2col, EW_GRID(static_cast<long long>(xi.N) * Ho * Wo * (Kp / 8)), x, xi, R, S, stride, pad, Ho, Wo, Kp, col);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_softmax_fwd(const bf16* x, long long in_ld, float* y, int rows, int F, cudaStream_t st) {
-    k_softmax_fwd<<<grid_for(rows, 8), 256, 0, st>>>(x, in_ld, y, rows, F);
+    TCB_LAUNCH(k_softmax_fwd, grid_for(rows, 8), 256, 0, st, x, in_ld, y, rows, F);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_softmax_bwd(const float* dy, const float* y, bf16* dx, long long out_ld, int rows, int F,
                              cudaStream_t st) {
-    k_softmax_bwd<<<grid_for(rows, 8), 256, 0, st>>>(dy, y, dx, out_ld, rows, F);
+    TCB_LAUNCH(k_softmax_bwd, grid_for(rows, 8), 256, 0, st, dy, y, dx, out_ld, rows, F);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st) {
-    k_f32_ew<<<EW_GRID(n)>>>(op, a, b, scale, y, n);
+    TCB_LAUNCH(k_f32_ew, EW_GRID(n), op, a, b, scale, y, n);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st) {
-    k_onehot<<<EW_GRID(static_cast<long long>(N) * K)>>>(labels, y, N, K);
+    TCB_LAUNCH(k_onehot, EW_GRID(static_cast<long long>(N) * K), labels, y, N, K);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -999,7 +1088,7 @@ tc_status launch_loss(const float* const* a, const float* const* b, const long l
     // out[0] = loss; out + 16 holds kLossBlocks fp64 partials, then the ticket counter (zero-initialised)
     double* partial = reinterpret_cast<double*>(out + 16);
     unsigned* ticket = reinterpret_cast<unsigned*>(partial + kLossBlocks);
-    k_loss<<<kLossBlocks, 256, 0, st>>>(args, out, partial, ticket);
+    TCB_LAUNCH(k_loss, kLossBlocks, 256, 0, st, args, out, partial, ticket);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1018,7 +1107,7 @@ static tc_status chan_reduce(const bf16* x, const bf16* x2, const float* stats, 
     RedPlan rp = red_plan(rows, static_cast<int>(ld));
     if (2ll * rp.splits * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
     dim3 grid(rp.tiles, rp.splits);
-    k_chan_reduce<MODE><<<grid, kRedThreads, 0, st>>>(x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
+    TCB_LAUNCH((k_chan_reduce<MODE>), grid, kRedThreads, 0, st, x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
                                                       rp.splits, part);
     TCB_LAUNCH_CHECK();
     *out_plan = rp;
@@ -1030,20 +1119,20 @@ tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, f
     RedPlan rp;
     tc_status s = chan_reduce<RED_SUM>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_SUM><<<(cols + 31) / 32, 256, 0, st>>>(partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_SUM>), (cols + 31) / 32, 256, 0, st, partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_bias_add(const bf16* x, const float* b, bf16* y, long long rows, int cols, long long ld, int relu,
                           cudaStream_t st) {
-    k_bias_add<<<EW_GRID(rows * ld)>>>(x, b, y, rows, cols, ld, relu);
+    TCB_LAUNCH(k_bias_add, EW_GRID(rows * ld), x, b, y, rows, cols, ld, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st) {
-    k_channel_copy<<<EW_GRID(pixels * c)>>>(src, src_cs, dst, dst_cs, off, c, pixels);
+    TCB_LAUNCH(k_channel_copy, EW_GRID(pixels * c), src, src_cs, dst, dst_cs, off, c, pixels);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1058,11 +1147,11 @@ tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_STATS><<<(C + 31) / 32, 256, 0, st>>>(partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+    TCB_LAUNCH((k_chan_final<RED_STATS>), (C + 31) / 32, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    k_chan_affine<<<EW_GRID(n8)>>>(reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C);
+    TCB_LAUNCH(k_chan_affine, EW_GRID(n8), reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1072,7 +1161,7 @@ tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    k_chan_final<RED_BNBWD><<<(C + 31) / 32, 256, 0, st>>>(partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_BNBWD>), (C + 31) / 32, 256, 0, st, partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
                                                               nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -1082,23 +1171,28 @@ tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma,
                               bf16* dx, long long pixels, int C, int cs, float* partials, int max_partials,
                               cudaStream_t st) {
     float* k = partials + max_partials;
-    k_bn_coef_bwd<<<(C + 255) / 256, 256, 0, st>>>(gamma, stats, sums, k, C, 1.f / static_cast<float>(pixels));
+    TCB_LAUNCH(k_bn_coef_bwd, (C + 255) / 256, 256, 0, st, gamma, stats, sums, k, C, 1.f / static_cast<float>(pixels));
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    k_bn_bwd_apply<<<EW_GRID(n8)>>>(reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), k,
+    TCB_LAUNCH(k_bn_bwd_apply, EW_GRID(n8), reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), k,
                                      reinterpret_cast<uint4*>(dx), n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
-tc_status launch_nchw_to_nhwc(const float* x, bf16* y, int N, int C, int H, int W, int cs, cudaStream_t st) {
-    k_nchw_to_nhwc<<<EW_GRID(static_cast<long long>(N) * H * W * cs)>>>(x, y, N, C, H, W, cs);
+tc_status launch_nchw_to_nhwc(const float* x, bf16* y, StageLayout L, cudaStream_t st) {
+    TCB_LAUNCH(k_nchw_to_nhwc, EW_GRID(L.elems()), x, y, L);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_synth_batch(bf16* x, int32_t* labels, int N, int C, int H, int W, int cs, int classes, uint64_t seed,
-                             uint32_t iter, uint32_t n0, cudaStream_t st) {
-    k_synth<<<EW_GRID(static_cast<long long>(N) * H * W * cs)>>>(x, labels, N, C, H, W, cs, classes, seed, iter, n0);
+tc_status launch_synth_batch(bf16* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
+                             uint32_t n0, cudaStream_t st) {
+    TCB_LAUNCH(k_synth, EW_GRID(L.elems()), x, labels, L, classes, seed, iter, n0);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+tc_status launch_s2d_mask_grad(float* g, int K, long long ld, int Rp, int s, int cs, int R, int S, cudaStream_t st) {
+    TCB_LAUNCH(k_s2d_mask_grad, EW_GRID(static_cast<long long>(K) * Rp * Rp * s * s * cs), g, K, ld, Rp, s, cs, R, S);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1116,14 +1210,14 @@ tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
             b.t[i] = t;
             b.start4[i + 1] = b.start4[i] + (t.n + 3) / 4;
         }
-        k_sgd<<<grid_for(b.start4[b.nt]), kThreads, 0, st>>>(b);
+        TCB_LAUNCH(k_sgd, grid_for(b.start4[b.nt]), kThreads, 0, st, b);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
 }
 
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st) {
-    k_set_iter<<<1, 1, 0, st>>>(d_iter, iter, n0);
+    TCB_LAUNCH(k_set_iter, 1, 1, 0, st, d_iter, iter, n0);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

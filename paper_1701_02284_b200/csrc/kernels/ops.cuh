@@ -84,11 +84,24 @@ tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma,
 tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
                         cudaStream_t st);
 
-// Input staging: NCHW fp32 -> NHWC bf16 (channel stride cs, pads zero).
-tc_status launch_nchw_to_nhwc(const float* x, bf16* y, int N, int C, int H, int W, int cs, cudaStream_t st);
+// Device layout of the staged input image.  s2d = 0: NHWC bf16 with channel stride cs.
+// s2d = s > 0 (space-to-depth for a stride-s first-layer conv): [N][Hs][Ws][s*s*cs] with
+// element (P, Q, (i*s + j)*cs + c) = x(n, c, s*P + i - pad, s*Q + j - pad) (0 outside).
+struct StageLayout {
+    int N, C, H, W, cs;
+    int s2d, pad, Hs, Ws;
+    __host__ __device__ long long elems() const {
+        return s2d ? static_cast<long long>(N) * Hs * Ws * s2d * s2d * cs : static_cast<long long>(N) * H * W * cs;
+    }
+};
+// Input staging: NCHW fp32 -> the staged layout (bf16, pads zero).
+tc_status launch_nchw_to_nhwc(const float* x, bf16* y, StageLayout L, cudaStream_t st);
 // Synthetic batch generated on the device (identical law to oracle/tc_philox.h).
-tc_status launch_synth_batch(bf16* x, int32_t* labels, int N, int C, int H, int W, int cs, int classes, uint64_t seed,
-                             uint32_t iter, uint32_t n0, cudaStream_t st);
+tc_status launch_synth_batch(bf16* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
+                             uint32_t n0, cudaStream_t st);
+// Space-to-depth filter gradient [K][ld]: zero the taps outside the original R x S window
+// (column (a*Rp + b)*s*s*cs + (i*s + j)*cs + c is tap (s*a + i, s*b + j)).
+tc_status launch_s2d_mask_grad(float* g, int K, long long ld, int Rp, int s, int cs, int R, int S, cudaStream_t st);
 
 // Momentum SGD: v = mom*v + lr_alpha*(g + decay*p); p += v;
 // refreshes the bf16 shadow(s) used as GEMM operands.

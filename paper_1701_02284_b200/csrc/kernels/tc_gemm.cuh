@@ -431,6 +431,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the prologue above overlapped the previous kernel; no global access before this
+    pdl_trigger();
+    pdl_wait();
 
     if (warp == 0) {
         // ---------------- TMA producer

@@ -68,6 +68,9 @@ struct ParamL {
     int Kw = 0;
     int in_dev = 0;
     int update_stmt = -1;  // the param's Update statement
+    // space-to-depth first-layer conv: taps regrouped into an Rp x Rp stride-1 conv over
+    // s2d*s2d*cs channels; device layout [K][Rp][Rp][s2d][s2d][cs] (taps outside R x S are 0)
+    int s2d = 0, Rp = 0;
     long long n = 0;  // device elements
     float* p = nullptr;
     float* v = nullptr;
@@ -130,6 +133,7 @@ struct tc_ctx {
     uint32_t* h_iter = nullptr;  // pinned
     float* h_loss = nullptr;     // pinned
     int input_cs = 8;
+    StageLayout in_layout{};  // staged input image layout (space-to-depth when in_layout.s2d > 0)
     size_t input_bytes = 0;
 
     // gradient buckets (backward production order); all-reduce + fused momentum
@@ -264,9 +268,52 @@ tc_status analyze_layouts(tc_ctx* c) {
         ParamL& q = c->params[s.in[1].index];
         q.cs = c->vars.at(s.in[0].index).cs;
     }
+    // Space-to-depth for a strided first-layer conv on the cs = 4 input (AlexNet 11x11/4):
+    // staging the image as [N][Hs][Ws][s*s*4] turns it into a stride-1 Rp x Rp conv over
+    // s*s*4 = 64 channels, which takes the TMA im2col operand path instead of 8-byte gathers.
+    {
+        int xv = -1;
+        for (int i = 0; i < p->nstmts; ++i)
+            if (p->stmts[i].kind == TC_STMT_LET && p->stmts[i].op == TC_OP_LOAD_X) xv = p->stmts[i].var;
+        int fwd = -1, uses = 0, other = 0;
+        for (int i = 0; xv >= 0 && i < p->nstmts; ++i) {
+            const tc_stmt& s = p->stmts[i];
+            for (int k = 0; k < s.nin; ++k) {
+                if (s.in[k].kind != TC_REF_VAR || s.in[k].index != xv) continue;
+                if (s.op == TC_OP_CONV_FWD && k == 0) {
+                    fwd = i;
+                    ++uses;
+                } else if (s.op != TC_OP_CONV_BWD_FILTER) {
+                    ++other;
+                }
+            }
+        }
+        const char* e = std::getenv("TCB_S2D");
+        const bool allowed = !(e && e[0] == '0');
+        if (allowed && xv >= 0 && uses == 1 && other == 0) {
+            const tc_stmt& s = p->stmts[fwd];
+            const VarL& x = c->vars.at(xv);
+            const VarL& y = c->vars.at(s.var);
+            ParamL& q = c->params[s.in[1].index];
+            const int st = s.stride;
+            bool ok = x.cs == 4 && st >= 2 && st <= 8 && (st * st * 4) % 64 == 0 && q.R == q.S;
+            for (int i = 0; ok && i < p->nstmts; ++i)
+                if (p->stmts[i].op == TC_OP_CONV_BWD_DATA && p->stmts[i].in[1].kind == TC_REF_PARAM &&
+                    p->stmts[i].in[1].index == s.in[1].index)
+                    ok = false;
+            if (ok) {
+                q.s2d = st;
+                q.Rp = (q.R + st - 1) / st;
+                c->in_layout.s2d = st;
+                c->in_layout.pad = s.pad;
+                c->in_layout.Hs = y.H + q.Rp - 1;
+                c->in_layout.Ws = y.W + q.Rp - 1;
+            }
+        }
+    }
     for (ParamL& q : c->params) {
         if (q.kind != ParamL::CONV) continue;
-        q.Kw = ceil8(static_cast<long long>(q.R) * q.S * q.cs);
+        q.Kw = q.s2d ? q.Rp * q.Rp * q.s2d * q.s2d * q.cs : ceil8(static_cast<long long>(q.R) * q.S * q.cs);
         q.n = static_cast<long long>(q.K) * q.Kw;
     }
     // FC weight device layout follows its forward input
@@ -446,9 +493,22 @@ tc_status plan_arena(tc_ctx* c) {
 }
 
 // ------------------------------------------------------------------ host layout permutations
+// Device column of tap (r, s), channel c of a space-to-depth filter.
+long long s2d_col(const ParamL& q, int r, int sx, int c) {
+    const int st = q.s2d;
+    return ((static_cast<long long>(r / st) * q.Rp + sx / st) * st * st + (r % st) * st + sx % st) * q.cs + c;
+}
+
 void ref_to_dev(const ParamL& q, const float* ref, std::vector<float>& dev) {
     dev.assign(q.n, 0.f);
-    if (q.kind == ParamL::CONV) {  // [K][Kw], Kw >= R*S*cs, (r, s, c) order
+    if (q.kind == ParamL::CONV && q.s2d) {
+        for (int k = 0; k < q.K; ++k)
+            for (int c = 0; c < q.C; ++c)
+                for (int r = 0; r < q.R; ++r)
+                    for (int sx = 0; sx < q.S; ++sx)
+                        dev[static_cast<long long>(k) * q.Kw + s2d_col(q, r, sx, c)] =
+                            ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + sx];
+    } else if (q.kind == ParamL::CONV) {  // [K][Kw], Kw >= R*S*cs, (r, s, c) order
         for (int k = 0; k < q.K; ++k)
             for (int c = 0; c < q.C; ++c)
                 for (int r = 0; r < q.R; ++r)
@@ -473,7 +533,14 @@ void ref_to_dev(const ParamL& q, const float* ref, std::vector<float>& dev) {
 }
 
 void dev_to_ref(const ParamL& q, const float* dev, float* ref) {
-    if (q.kind == ParamL::CONV) {
+    if (q.kind == ParamL::CONV && q.s2d) {
+        for (int k = 0; k < q.K; ++k)
+            for (int c = 0; c < q.C; ++c)
+                for (int r = 0; r < q.R; ++r)
+                    for (int sx = 0; sx < q.S; ++sx)
+                        ref[((static_cast<long long>(k) * q.C + c) * q.R + r) * q.S + sx] =
+                            dev[static_cast<long long>(k) * q.Kw + s2d_col(q, r, sx, c)];
+    } else if (q.kind == ParamL::CONV) {
         for (int k = 0; k < q.K; ++k)
             for (int c = 0; c < q.C; ++c)
                 for (int r = 0; r < q.R; ++r)
@@ -554,6 +621,22 @@ struct Ptrs {
 
 tc_conv_desc conv_desc(const VarL& x, const ParamL& w, const VarL& y, const tc_stmt& s) {
     tc_conv_desc d;
+    if (w.s2d) {  // stride-1 Rp x Rp conv over the space-to-depth staged input
+        d.N = x.N;
+        d.C = w.s2d * w.s2d * w.cs;
+        d.H = y.H + w.Rp - 1;
+        d.W = y.W + w.Rp - 1;
+        d.K = w.K;
+        d.R = d.S = w.Rp;
+        d.stride = 1;
+        d.pad = 0;
+        d.Ho = y.H;
+        d.Wo = y.W;
+        d.cs = d.C;
+        d.ks = y.cs;
+        d.wld = w.Kw;
+        return d;
+    }
     d.N = x.N;
     d.C = x.C;
     d.H = x.H;
@@ -607,7 +690,9 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
             const VarL& dy = P.L(s.in[0]);
             const VarL& x = P.L(s.in[1]);
             tc_conv_desc d = conv_desc(x, q, dy, s);
-            return tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
+            tc_status r = tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
+            if (r != TC_OK || !q.s2d) return r;
+            return launch_s2d_mask_grad(g, q.K, q.Kw, q.Rp, q.s2d, q.cs, q.R, q.S, st);
         }
         case TC_OP_BN_BWD_BETA:
         case TC_OP_BN_BWD_GAMMA: {
@@ -1081,7 +1166,12 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
     // input staging: NHWC bf16 batch + labels + NCHW fp32 staging for host batches
     c->input_cs = plan->input_dims[1] <= 4 ? 4 : ceil8(plan->input_dims[1]);  // must match the LOAD_X var layout
-    const size_t in_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[2] * plan->input_dims[3] * c->input_cs;
+    c->in_layout.N = static_cast<int>(plan->input_dims[0]);
+    c->in_layout.C = static_cast<int>(plan->input_dims[1]);
+    c->in_layout.H = static_cast<int>(plan->input_dims[2]);
+    c->in_layout.W = static_cast<int>(plan->input_dims[3]);
+    c->in_layout.cs = c->input_cs;
+    const size_t in_el = static_cast<size_t>(c->in_layout.elems());
     const size_t stage_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
     c->input_bytes = in_el * 2 + stage_el * 4;
     TCB_CUDA_CHECK(cudaMalloc(&c->d_input, in_el * 2));
@@ -1256,17 +1346,14 @@ tc_status tc_stage_batch(tc_ctx* c, const float* x, const int32_t* labels) {
     const size_t el = static_cast<size_t>(p->input_dims[0]) * p->input_dims[1] * p->input_dims[2] * p->input_dims[3];
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, x, el * 4, cudaMemcpyHostToDevice, c->st));
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, labels, p->input_dims[0] * 4, cudaMemcpyHostToDevice, c->st));
-    return launch_nchw_to_nhwc(c->d_stage, c->d_input, static_cast<int>(p->input_dims[0]), static_cast<int>(p->input_dims[1]),
-                               static_cast<int>(p->input_dims[2]), static_cast<int>(p->input_dims[3]), c->input_cs, c->st);
+    return launch_nchw_to_nhwc(c->d_stage, c->d_input, c->in_layout, c->st);
 }
 
 tc_status tc_stage_synthetic(tc_ctx* c, int iter, int n0) {
     if (!c) return fail(TC_INVALID_ARG, "tc_stage_synthetic");
     const tc_plan* p = c->plan;
-    return launch_synth_batch(c->d_input, c->d_labels, static_cast<int>(p->input_dims[0]), static_cast<int>(p->input_dims[1]),
-                              static_cast<int>(p->input_dims[2]), static_cast<int>(p->input_dims[3]), c->input_cs,
-                              static_cast<int>(p->classes), c->desc.seed, static_cast<uint32_t>(iter),
-                              static_cast<uint32_t>(n0), c->st);
+    return launch_synth_batch(c->d_input, c->d_labels, c->in_layout, static_cast<int>(p->classes), c->desc.seed,
+                              static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
 }
 
 tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
@@ -1344,7 +1431,8 @@ tc_status tc_var_download(tc_ctx* c, int var, float* host, int64_t max_elems) {
     if (it == c->vars.end() || it->second.def < 0) return fail(TC_INVALID_ARG, "tc_var_download: unknown var");
     const VarL& v = it->second;
     Ptrs P{c};
-    std::vector<uint8_t> raw(v.bytes());
+    const bool s2d_input = c->in_layout.s2d && c->plan->stmts[v.def].op == TC_OP_LOAD_X;
+    std::vector<uint8_t> raw(s2d_input ? static_cast<size_t>(c->in_layout.elems()) * 2 : v.bytes());
     TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
     TCB_CUDA_CHECK(cudaMemcpy(raw.data(), P.var(var), raw.size(), cudaMemcpyDeviceToHost));
     auto at = [&](long long e) -> float {
@@ -1355,7 +1443,21 @@ tc_status tc_var_download(tc_ctx* c, int var, float* host, int64_t max_elems) {
     long long count = 1;
     for (int j = 0; j < v.rank; ++j) count *= v.d[j];
     if (count > max_elems) return fail(TC_INVALID_ARG, "tc_var_download: buffer too small");
-    if (v.nhwc) {  // reference NCHW order (also for the 2-D view of a flattened tensor)
+    if (s2d_input) {  // space-to-depth staged image -> NCHW (pixels past the last window are not staged: 0)
+        const StageLayout& L = c->in_layout;
+        for (int n = 0; n < v.N; ++n)
+            for (int ch = 0; ch < v.C; ++ch)
+                for (int h = 0; h < v.H; ++h)
+                    for (int w = 0; w < v.W; ++w) {
+                        const int hp = h + L.pad, wp = w + L.pad;
+                        const int P = hp / L.s2d, Q = wp / L.s2d;
+                        float val = 0.f;
+                        if (P < L.Hs && Q < L.Ws)
+                            val = at((((static_cast<long long>(n) * L.Hs + P) * L.Ws + Q) * L.s2d * L.s2d +
+                                      (hp % L.s2d) * L.s2d + wp % L.s2d) * L.cs + ch);
+                        host[((static_cast<long long>(n) * v.C + ch) * v.H + h) * v.W + w] = val;
+                    }
+    } else if (v.nhwc) {  // reference NCHW order (also for the 2-D view of a flattened tensor)
         for (int n = 0; n < v.N; ++n)
             for (int ch = 0; ch < v.C; ++ch)
                 for (int h = 0; h < v.H; ++h)
