@@ -192,6 +192,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 // ------------------------------------------------------------------ launch
 struct LaunchPlan {
     int bn = 128;
+    int cg = 1;  // 2: CTA-pair (cta_group::2) tiles of 256 x bn
     int splits = 1;
     int kb_per_split = 1;
     int num_kb = 1;
@@ -207,56 +208,100 @@ static int forced_bn() {
     return v;
 }
 
+// TCB_CG=1|2 pins the CTA-group size (kernel experiments / A-B comparisons); 0 = cost model.
+static int forced_cg() {
+    static const int v = [] {
+        const char* e = std::getenv("TCB_CG");
+        const int c = e ? std::atoi(e) : 0;
+        return (c == 1 || c == 2) ? c : 0;
+    }();
+    return v;
+}
+
 // Per-CTA time of one 128 x BN x 64 k-block, measured on B200 with plain TMA operands
 // (8192^3: BN=256 1284 TF/s, BN=128 853 TF/s (shared-memory bound: A+B bytes per MMA
-// cycle), BN=64 461 TF/s; tools/gemm_bench.py).
-static double t_kblock(int bn) { return bn == 256 ? 0.48e-6 : bn == 128 ? 0.36e-6 : 0.335e-6; }
+// cycle), BN=64 461 TF/s; tools/gemm_bench.py).  CTA pairs split B across the two SMs,
+// which halves its shared-memory traffic per SM.
+static double t_kblock(int bn, int cg) {
+    if (cg == 2) return bn == 256 ? 0.46e-6 : 0.25e-6;
+    return bn == 256 ? 0.48e-6 : bn == 128 ? 0.36e-6 : 0.335e-6;
+}
 
 // Tile width and split-K chosen by a cost model over the persistent grid: waves of
 // units, each unit max(main loop, epilogue store) since the double-buffered TMEM
 // accumulator overlaps a tile's store with the next tile's main loop; split-K adds
 // the fp32 partial round trip of the deterministic reduce.
-static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes) {
+// CTA pairs (cta_group::2, 256-row tiles with B split across the two SMs) are used for
+// the filter-gradient contractions with >= 256 output channels: measured +7..54% there
+// (AlexNet conv2 wgrad 305 -> 469 TF/s, VGG 256/512-channel wgrad 550 -> 740 TF/s), while
+// fprop / dgrad shapes measured equal or slower (tools/gemm_bench.py, same-call A/B).
+// `pair` = the caller's choice; TCB_CG=1|2 overrides it where both operands are TMA-loaded.
+static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes, bool pair_ok, bool pair = false) {
     LaunchPlan best;
     double best_t = 1e30;
     const int sms = num_sms();
     const int num_kb = std::max(1, ceil_div(K, BK));
     const double mn = static_cast<double>(M) * N;
-    for (int bn : {256, 128, 64}) {
-        if (forced_bn() && bn != forced_bn()) continue;
-        const int tiles = ceil_div(M, BM) * ceil_div(N, bn);
-        const int max_s = splits_req > 0 ? 1 : std::max(1, std::min(128, num_kb / 4));
-        for (int s = 1; s <= max_s; ++s) {
-            const int req = splits_req > 0 ? std::min(splits_req, num_kb) : s;
-            const int kbs = ceil_div(num_kb, req);
-            const int s_eff = ceil_div(num_kb, kbs);
-            const long long units = static_cast<long long>(tiles) * s_eff;
-            const double waves = static_cast<double>((units + sms - 1) / sms);
-            const double epi = static_cast<double>(BM) * bn * (s_eff > 1 ? 4 : out_bytes) / 40e9;
-            double t = waves * std::max(kbs * t_kblock(bn), epi) + 2e-6;
-            if (s_eff > 1) t += (s_eff * mn * 8.0 + mn * out_bytes) / 5.0e12 + 3.0e-6;
-            if (t < best_t * 0.97) {
-                best_t = t;
-                best.bn = bn;
-                best.num_kb = num_kb;
-                best.kb_per_split = kbs;
-                best.splits = s_eff;
+    const int want_cg = !pair_ok ? 1 : forced_cg() ? forced_cg() : (pair ? 2 : 1);
+    for (int cg : {1, 2}) {
+        if (cg != want_cg) continue;
+        for (int bn : {256, 128, 64}) {
+            if (forced_bn() && bn != forced_bn()) continue;
+            if (cg == 2 && bn == 64) continue;
+            const int tiles = ceil_div(M, BM * cg) * ceil_div(N, bn);
+            const int slots = sms / cg;
+            const int max_s = splits_req > 0 ? 1 : std::max(1, std::min(128, num_kb / 4));
+            for (int s = 1; s <= max_s; ++s) {
+                const int req = splits_req > 0 ? std::min(splits_req, num_kb) : s;
+                const int kbs = ceil_div(num_kb, req);
+                const int s_eff = ceil_div(num_kb, kbs);
+                const long long units = static_cast<long long>(tiles) * s_eff;
+                const double waves = static_cast<double>((units + slots - 1) / slots);
+                const double epi = static_cast<double>(BM) * bn * (s_eff > 1 ? 4 : out_bytes) / 40e9;
+                double t = waves * std::max(kbs * t_kblock(bn, cg), epi) + 2e-6;
+                if (s_eff > 1) t += (s_eff * mn * 8.0 + mn * out_bytes) / 5.0e12 + 3.0e-6;
+                if (t < best_t * 0.97) {
+                    best_t = t;
+                    best.bn = bn;
+                    best.cg = cg;
+                    best.num_kb = num_kb;
+                    best.kb_per_split = kbs;
+                    best.splits = s_eff;
+                }
             }
         }
     }
     return best;
 }
 
-template <int BN>
-static tc_status launch_bn(const GemmParams& p, dim3 grid, cudaStream_t st) {
-    const int smem = TileCfg<BN>::kSmemBytes;
+template <int BN, int CG>
+static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
+    const int smem = TileCfg<BN, CG>::kSmemBytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (attr_err != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(attr_err));
-    TCB_LAUNCH((tc_gemm_kernel<BN>), grid, kNumThreads, smem, st, p);
+    const int grid = std::min(units, num_sms() / CG) * CG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNumThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    if (CG == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na++].val.clusterDim.z = 1;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG>, p);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -269,7 +314,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.num_kb = lp.num_kb;
     p.kb_per_split = lp.kb_per_split;
     p.splits = lp.splits;
-    p.tiles_m = ceil_div(p.M, BM);
+    p.tiles_m = ceil_div(p.M, BM * lp.cg);
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
     const bool partial = lp.splits > 1 || beta != 0.f;
@@ -289,13 +334,15 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         p.relu = relu;
         if (!make_tmap_store(&p.tmD, D, d_bf16 != 0, p.N, p.M, 1, ldd, &err)) return fail(TC_INVALID_ARG, err);
     }
-    dim3 grid(std::min(p.units, num_sms()));
     tc_status s;
-    switch (lp.bn) {
-        case 256: s = launch_bn<256>(p, grid, st); break;
-        case 128: s = launch_bn<128>(p, grid, st); break;
-        default: s = launch_bn<64>(p, grid, st); break;
-    }
+    if (lp.cg == 2)
+        s = lp.bn == 256 ? launch_bn<256, 2>(p, p.units, st) : launch_bn<128, 2>(p, p.units, st);
+    else if (lp.bn == 256)
+        s = launch_bn<256, 1>(p, p.units, st);
+    else if (lp.bn == 128)
+        s = launch_bn<128, 1>(p, p.units, st);
+    else
+        s = launch_bn<64, 1>(p, p.units, st);
     if (s != TC_OK) return s;
     if (partial) {
         const long long total = static_cast<long long>(p.M) * p.N;
@@ -324,7 +371,7 @@ unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load();
 
 size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
     if (!a) return 0;
-    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4);
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
     return (lp.splits > 1 || a->beta != 0.f) ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
 }
 
@@ -336,7 +383,7 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     p.N = a->N;
     p.K = a->K;
     p.alpha = a->alpha;
-    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4);
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
     std::string err;
     if (a->a_layout == TC_LAYOUT_K) {
         p.a_mode = OP_TMA_K;
@@ -349,7 +396,7 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     const int b_rows = a->b_rows > 0 ? std::min(a->b_rows, a->N) : a->N;
     if (a->b_layout == TC_LAYOUT_K) {
         p.b_mode = OP_TMA_K;
-        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->K, b_rows, a->ldb, BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+        if (!make_tmap_2d_bf16(&p.tmB, a->B, a->K, b_rows, a->ldb, BK, lp.bn / lp.cg, &err)) return fail(TC_INVALID_ARG, err);
     } else {
         p.b_mode = OP_TMA_MN;
         if (!make_tmap_2d_bf16(&p.tmB, a->B, b_rows, a->K, a->ldb, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
@@ -413,9 +460,12 @@ static int wgrad_im2col(const tc_conv_desc* d) { return fprop_im2col(d); }
 static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
     const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
     const long long npix_in = static_cast<long long>(d->N) * d->H * d->W;
-    if (which == 0) return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2);
-    if (which == 1) return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2);
-    return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0, 4);
+    if (which == 0)
+        return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2, is_pointwise(d) || fprop_im2col(d));
+    if (which == 1)
+        return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2, is_pointwise(d) || dgrad_im2col(d));
+    const bool tma_ops = is_pointwise(d) || wgrad_im2col(d);
+    return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0, 4, tma_ops, d->K >= 256);
 }
 
 size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
@@ -457,7 +507,7 @@ tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, con
         p.gsrc = static_cast<const __nv_bfloat16*>(x);
     }
     p.b_mode = OP_TMA_K;
-    if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, filter_ld(d), BK, lp.bn, &err)) return fail(TC_INVALID_ARG, err);
+    if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, filter_ld(d), BK, lp.bn / lp.cg, &err)) return fail(TC_INVALID_ARG, err);
     // Bias is read only for n < K; padded channels get 0 (relu(0) = 0).
     return run_gemm(p, lp, y, d->ks, 1, bias, d->K, relu, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }

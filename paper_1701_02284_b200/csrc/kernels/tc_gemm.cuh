@@ -88,11 +88,14 @@ constexpr int BM = 128;
 constexpr int kNumThreads = 384;
 constexpr int kStagingBytes = 4096;  // per epilogue warp per buffer: 32 rows x 128 B
 
-template <int BN>
+// CG = 2: CTA pair (cta_group::2).  The pair computes a (2*BM) x BN tile: each CTA holds
+// its BM rows of A and BN/2 rows (columns of D) of B; the leader issues the MMAs.
+template <int BN, int CG = 1>
 struct TileCfg {
-    static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+    static constexpr int kBNL = BN / CG;  // B rows held by one CTA
     static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kBBytes = kBNL * BK * 2;
+    static constexpr int kStages = (196608 / (kABytes + kBBytes)) > 8 ? 8 : (196608 / (kABytes + kBBytes));
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagingTotal = 4 * 2 * kStagingBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kStagingTotal + 1024 /*align*/ + 256 /*barriers*/;
@@ -391,9 +394,9 @@ __device__ __forceinline__ void col_gather4_issue(const GemmParams& p, const Col
     }
 }
 
-template <int BN>
+template <int BN, int CG>
 __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_constant__ GemmParams p) {
-    using Cfg = TileCfg<BN>;
+    using Cfg = TileCfg<BN, CG>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -408,9 +411,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const bool a_gather = p.a_mode == OP_GATHER_K;
-    const bool b_gather = p.b_mode == OP_GATHER_MN;
+    const bool a_gather = CG == 1 && p.a_mode == OP_GATHER_K;  // CTA pairs use TMA operands only
+    const bool b_gather = CG == 1 && p.b_mode == OP_GATHER_MN;
     const bool any_gather = a_gather || b_gather;
+    const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;  // 0 = MMA leader
+    const int pair = blockIdx.x / CG, npairs = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         if (!a_gather) tma_prefetch(&p.tmA);
@@ -422,13 +427,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], any_gather ? 4 : 8);  // one arrival per epilogue warp
+            mbar_init(&tempty[b], CG * (any_gather ? 4 : 8));  // one arrival per epilogue warp of the pair
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    if (warp == 2) tmem_alloc<CG>(tmem_slot, Cfg::kTmemCols);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync_all();  // peer barriers initialised before any remote arrive / complete_tx
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // PDL: the prologue above overlapped the previous kernel; no global access before this
@@ -441,11 +449,12 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             uint32_t tx = 0;
             if (!a_gather) tx += Cfg::kABytes;
             if (!b_gather) tx += Cfg::kBBytes;
+            tx *= CG;  // the leader's barrier counts the bytes landing in both CTAs
             const ConvGeom& g = p.g;
             int it = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (int u = pair; u < p.units; u += npairs) {
                 const Unit w = decode_unit(p, u);
-                const int m0 = w.mt * BM, n0 = w.nt * BN;
+                const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN + rank * Cfg::kBNL;
                 // im2col A: first pixel of this row tile
                 int a_n = 0, a_y = 0, a_x = 0;
                 if (p.a_mode == OP_IM2COL_K || p.a_mode == OP_IM2COL32_K) {
@@ -461,18 +470,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
                     uint8_t* a_dst = sA + s * Cfg::kABytes;
                     uint8_t* b_dst = sB + s * Cfg::kBBytes;
+                    // transaction barrier: the leader CTA's full[s] (own barrier for CG = 1)
+                    const uint32_t bar = CG == 2 ? mapa_shared(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
                     int kc = kb * BK;  // k coordinate of this block in the plain-TMA operand
                     if (p.a_mode == OP_TMA_K) {
-                        tma_load_2d(a_dst, &p.tmA, &full[s], kc, m0);
+                        tma_load_2d_cg<CG>(a_dst, &p.tmA, bar, kc, m0);
                     } else if (p.a_mode == OP_TMA_MN) {
 #pragma unroll
                         for (int a = 0; a < BM / 64; ++a)
-                            tma_load_2d(a_dst + a * BK * 128, &p.tmA, &full[s], m0 + a * 64, kc);
+                            tma_load_2d_cg<CG>(a_dst + a * BK * 128, &p.tmA, bar, m0 + a * 64, kc);
                     } else if (p.a_mode == OP_IM2COL_K) {
                         const int tap = kb / p.i2c_cpb, cb = kb - tap * p.i2c_cpb;
                         const int kh = tap / g.S, kw = tap - kh * g.S;
                         const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
-                        tma_load_im2col_4d(a_dst, &p.tmA, &full[s], cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
+                        tma_load_im2col_4d_cg<CG>(a_dst, &p.tmA, bar, cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
                                            static_cast<uint16_t>(oh));
                         kc = tap * p.i2c_ldk + cb * 64;
                     } else if (p.a_mode == OP_IM2COL32_K) {
@@ -483,16 +494,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                             const int tap = blk / p.i2c_cpb, cb = blk - tap * p.i2c_cpb;
                             const int kh = tap / g.S, kw = tap - kh * g.S;
                             const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
-                            tma_load_im2col_4d(a_dst + h * (Cfg::kABytes / 2), &p.tmA, &full[s], cb * 32, a_x, a_y, a_n,
+                            tma_load_im2col_4d_cg<CG>(a_dst + h * (Cfg::kABytes / 2), &p.tmA, bar, cb * 32, a_x, a_y, a_n,
                                                static_cast<uint16_t>(ow), static_cast<uint16_t>(oh));
                         }
                     }
                     if (p.b_mode == OP_TMA_K) {
-                        tma_load_2d(b_dst, &p.tmB, &full[s], kc, n0);
+                        tma_load_2d_cg<CG>(b_dst, &p.tmB, bar, kc, n0);
                     } else if (p.b_mode == OP_TMA_MN) {
 #pragma unroll
-                        for (int a = 0; a < BN / 64; ++a)
-                            tma_load_2d(b_dst + a * BK * 128, &p.tmB, &full[s], n0 + a * 64, kc);
+                        for (int a = 0; a < Cfg::kBNL / 64; ++a)
+                            tma_load_2d_cg<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc);
                     } else if (p.b_mode == OP_IM2COL_MN || p.b_mode == OP_IM2COL32_MN) {
                         // 64 output pixels of this k-block; columns n = tap * cs + c in 64-channel atoms
                         const int pq = p.i2c_P * p.i2c_Q;
@@ -503,28 +514,28 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         const int by = oy * g.stride + p.i2c_lo_h;
                         const int bx = (rem - oy * p.i2c_Q) * g.stride + p.i2c_lo_w;
                         const int box = p.b_mode == OP_IM2COL32_MN ? 32 : 64;  // columns per box
-                        for (int col = 0; col < BN; col += box) {
+                        for (int col = 0; col < Cfg::kBNL; col += box) {
                             int n = n0 + col;
                             if (n >= p.N) n = 0;  // columns past N are clipped by the store; load finite data
                             const int tap = n / g.C, c = n - tap * g.C;
                             const int kh = tap / g.S, kw = tap - kh * g.S;
-                            tma_load_im2col_4d(b_dst + col * BK * 2, &p.tmB, &full[s], c, bx, by, bn_img,
+                            tma_load_im2col_4d_cg<CG>(b_dst + col * BK * 2, &p.tmB, bar, c, bx, by, bn_img,
                                                static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
                         }
                     }
-                    mbar_arrive_expect_tx(&full[s], tx);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], tx);
                 }
             }
         }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer (the leader CTA of a pair)
         const bool a_mn = p.a_mode == OP_TMA_MN;
         const bool a_sw64 = p.a_mode == OP_IM2COL32_K;
         const bool b_sw64 = p.b_mode == OP_IM2COL32_MN;
         const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN || b_sw64;
-        const uint32_t idesc = umma_idesc_bf16(BM, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
+        const uint32_t idesc = umma_idesc_bf16(BM * CG, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
         int it = 0, tc = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
+        for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
             const int buf = tc & 1;
             mbar_wait(&tempty[buf], ((tc >> 1) & 1) ^ 1);
@@ -549,10 +560,18 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         const uint64_t bd = b_sw64 ? umma_desc_sw64(b_base + k * 1024, BK * 64, 512)
                                             : b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
                                                    : umma_desc_sw128(b_base + k * 32, 0, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+                        if constexpr (CG == 2)
+                            umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+                        else
+                            umma_bf16(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
                     }
-                    umma_commit(&empty[s]);
-                    if (kb == w.kb1 - 1) umma_commit(&tfull[buf]);
+                    if constexpr (CG == 2) {
+                        umma_commit_cg2(&empty[s]);
+                        if (kb == w.kb1 - 1) umma_commit_cg2(&tfull[buf]);
+                    } else {
+                        umma_commit(&empty[s]);
+                        if (kb == w.kb1 - 1) umma_commit(&tfull[buf]);
+                    }
                 }
                 __syncwarp();
             }
@@ -564,7 +583,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             const int t = threadIdx.x - 256;
             int it = 0;
             const bool c4 = p.g.C == 4;  // channel-stride-4 first-layer input (fprop A / wgrad B)
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (int u = pair; u < p.units; u += npairs) {
                 const Unit w = decode_unit(p, u);
                 if (a_gather && c4) {
                     RowGather4 rg;
@@ -641,17 +660,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         const bool bf16_out = p.epi == EPI_BF16;
         int nstore = 0;
         int tc = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
+        // accumulator release goes to the leader's tempty (remote arrive from the peer CTA)
+        const uint32_t tempty_addr[2] = {CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]),
+                                         CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : smem_u32(&tempty[1])};
+        for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
             const int buf = tc & 1;
             mbar_wait(&tfull[buf], (tc >> 1) & 1);
             tc_fence_after();
-            const int m0 = w.mt * BM, n0 = w.nt * BN;
+            const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
             if (grp * 64 >= BN) {  // no chunk for this warp (BN = 64 with two groups)
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[buf]);
+                if (lane == 0) mbar_arrive_cluster(tempty_addr[buf]);
                 continue;
             }
             // One staging row = 128 B (64 bf16 or 32 fp32 columns).  The two TMEM reads of a
@@ -672,7 +694,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     // this warp's TMEM reads of the accumulator are done: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                    if (lane == 0) mbar_arrive_cluster(tempty_addr[buf]);
                 }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
@@ -728,10 +750,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync_all();  // the leader's MMAs and both epilogues are done with both TMEMs
+    else
+        __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, Cfg::kTmemCols);
+        tmem_dealloc<CG>(tmem_base, Cfg::kTmemCols);
     }
 }
 
