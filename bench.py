@@ -203,29 +203,32 @@ def run_gpu(args):
     clocks = parse_clocks(clk_file) if rank == 0 else None
     loss_val = tr.loss()
 
-    # ---- e2e: public API with a host batch each step (pinned H2D) + loss D2H
-    x_host = torch.empty((batch, 3, 224, 224), dtype=torch.float32).pin_memory()
+    # ---- e2e: public API with a host batch each step (pinned H2D) + loss D2H.  The input
+    # pipeline stages batch i+1 (H2D on the context's copy stream) while step i runs, as a
+    # training loop with a prefetching loader does; every step's H2D copy and its loss
+    # read-back are inside the timed region, which is wall clock (host + device).
+    x_host = torch.empty(tuple(net.input_dims), dtype=torch.float32).pin_memory()
     y_host = torch.empty((batch,), dtype=torch.int32).pin_memory()
     from oracle.oracle import synth_batch  # host-side generator of the same law (input pipeline stand-in)
     xs, ys = synth_batch(net, SEED, 0, rank * batch)
     x_host.copy_(torch.from_numpy(xs))
     y_host.copy_(torch.from_numpy(ys))
+    xh, yh = x_host.numpy(), y_host.numpy()
+    tr.stage_batch(xh, yh)
     for it in range(2):
-        tr.stage_batch(x_host.numpy(), y_host.numpy())
         tr.step(it, rank * batch)
+        tr.stage_batch(xh, yh)
         tr.loss()
+    tr.sync()
     barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    t0 = time.perf_counter()
     for it in range(args.steps):
-        tr.stage_batch(x_host.numpy(), y_host.numpy())
         tr.step(it, rank * batch)
+        tr.stage_batch(xh, yh)  # next step's batch, overlapping this step
         tr.loss()  # D2H of the step's loss, synchronising like a training loop that logs it
-    e1.record(stream)
-    e1.synchronize()
+    tr.sync()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
 
     # ---- per-statement profile (one eager step) for the roofline
     stmt_ms = tr.profile_step(args.warmup + args.steps, rank * batch)

@@ -54,7 +54,11 @@ TC_API tc_status tc_grad_download(tc_ctx* ctx, int index, float* host);
 /* Xavier / constant init from the shared counter RNG (tc_philox.h); identical to the oracle. */
 TC_API tc_status tc_init_params(tc_ctx* ctx);
 
-/* Stage a batch: x NCHW fp32 (batch, C, H, W) and int32 labels, host memory (H2D on the stream). */
+/* Stage a batch: x NCHW fp32 (batch, C, H, W) and int32 labels, host memory.  Asynchronous
+ * input pipeline: the H2D copy runs on the context's copy stream into one of two device
+ * staging slots (overlapping a running step when the host memory is pinned); the next
+ * tc_step / tc_exec_stmt converts it to the device layout.  The host buffers are borrowed
+ * until tc_sync() or until the step after the consuming one has been enqueued. */
 TC_API tc_status tc_stage_batch(tc_ctx* ctx, const float* x_host, const int32_t* labels_host);
 /* Generate the synthetic batch of `iter` on the device (global samples [n0, n0+batch)). */
 TC_API tc_status tc_stage_synthetic(tc_ctx* ctx, int iter, int n0);

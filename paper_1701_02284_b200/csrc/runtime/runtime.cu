@@ -127,7 +127,14 @@ struct tc_ctx {
     int max_partials = 0;
     bf16* d_input = nullptr;
     int32_t* d_labels = nullptr;
-    float* d_stage = nullptr;  // NCHW fp32 staging for host batches
+    // Input pipeline: host batches are copied (NCHW fp32 + labels) into one of two
+    // device staging slots on copy_st, overlapping the running step; the next step
+    // converts the pending slot into the staged input layout on the main stream.
+    float* d_stage[2] = {nullptr, nullptr};
+    int32_t* d_label_stage[2] = {nullptr, nullptr};
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t h2d_done[2] = {nullptr, nullptr}, conv_done[2] = {nullptr, nullptr};
+    int stage_pending = -1, stage_next = 0;
     float* d_loss = nullptr;
     uint32_t* d_iter = nullptr;
     uint32_t* h_iter = nullptr;  // pinned
@@ -1173,10 +1180,17 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     c->in_layout.cs = c->input_cs;
     const size_t in_el = static_cast<size_t>(c->in_layout.elems());
     const size_t stage_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
-    c->input_bytes = in_el * 2 + stage_el * 4;
+    c->input_bytes = in_el * 2 + 2 * stage_el * 4;
     TCB_CUDA_CHECK(cudaMalloc(&c->d_input, in_el * 2));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->d_input, 0, in_el * 2, c->st));
-    TCB_CUDA_CHECK(cudaMalloc(&c->d_stage, stage_el * 4));
+    for (int k = 0; k < 2; ++k) {
+        TCB_CUDA_CHECK(cudaMalloc(&c->d_stage[k], stage_el * 4));
+        TCB_CUDA_CHECK(cudaMalloc(&c->d_label_stage[k], plan->input_dims[0] * sizeof(int32_t)));
+        TCB_CUDA_CHECK(cudaEventCreateWithFlags(&c->h2d_done[k], cudaEventDisableTiming));
+        TCB_CUDA_CHECK(cudaEventCreateWithFlags(&c->conv_done[k], cudaEventDisableTiming));
+        TCB_CUDA_CHECK(cudaEventRecord(c->conv_done[k], c->st));
+    }
+    TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->d_labels, 0, plan->input_dims[0] * sizeof(int32_t), c->st));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 1024));
@@ -1270,7 +1284,14 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->partials);
     cudaFree(c->bn_sums);
     cudaFree(c->d_input);
-    cudaFree(c->d_stage);
+    if (c->copy_st) cudaStreamSynchronize(c->copy_st);
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(c->d_stage[k]);
+        cudaFree(c->d_label_stage[k]);
+        if (c->h2d_done[k]) cudaEventDestroy(c->h2d_done[k]);
+        if (c->conv_done[k]) cudaEventDestroy(c->conv_done[k]);
+    }
+    if (c->copy_st) cudaStreamDestroy(c->copy_st);
     cudaFree(c->d_labels);
     cudaFree(c->d_loss);
     cudaFree(c->d_iter);
@@ -1344,13 +1365,35 @@ tc_status tc_stage_batch(tc_ctx* c, const float* x, const int32_t* labels) {
     if (!c || !x || !labels) return fail(TC_INVALID_ARG, "tc_stage_batch: null argument");
     const tc_plan* p = c->plan;
     const size_t el = static_cast<size_t>(p->input_dims[0]) * p->input_dims[1] * p->input_dims[2] * p->input_dims[3];
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, x, el * 4, cudaMemcpyHostToDevice, c->st));
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, labels, p->input_dims[0] * 4, cudaMemcpyHostToDevice, c->st));
-    return launch_nchw_to_nhwc(c->d_stage, c->d_input, c->in_layout, c->st);
+    // the slot's previous batch must have been converted by its step before it is overwritten
+    const int k = c->stage_next;
+    TCB_CUDA_CHECK(cudaStreamWaitEvent(c->copy_st, c->conv_done[k], 0));
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], x, el * 4, cudaMemcpyHostToDevice, c->copy_st));
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_label_stage[k], labels, p->input_dims[0] * 4, cudaMemcpyHostToDevice, c->copy_st));
+    TCB_CUDA_CHECK(cudaEventRecord(c->h2d_done[k], c->copy_st));
+    c->stage_pending = k;
+    c->stage_next = k ^ 1;
+    return TC_OK;
+}
+
+// Convert a pending host batch (if any) into the staged input layout on the main stream.
+static tc_status consume_staged(tc_ctx* c) {
+    const int k = c->stage_pending;
+    if (k < 0) return TC_OK;
+    c->stage_pending = -1;
+    TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->h2d_done[k], 0));
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, c->d_label_stage[k], c->plan->input_dims[0] * sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, c->st));
+    tc_status r = launch_nchw_to_nhwc(c->d_stage[k], c->d_input, c->in_layout, c->st);
+    if (r != TC_OK) return r;
+    TCB_CUDA_CHECK(cudaEventRecord(c->conv_done[k], c->st));
+    return TC_OK;
 }
 
 tc_status tc_stage_synthetic(tc_ctx* c, int iter, int n0) {
     if (!c) return fail(TC_INVALID_ARG, "tc_stage_synthetic");
+    tc_status r0 = consume_staged(c);  // keep slot bookkeeping consistent; the synthetic batch wins
+    if (r0 != TC_OK) return r0;
     const tc_plan* p = c->plan;
     return launch_synth_batch(c->d_input, c->d_labels, c->in_layout, static_cast<int>(p->classes), c->desc.seed,
                               static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
@@ -1359,6 +1402,10 @@ tc_status tc_stage_synthetic(tc_ctx* c, int iter, int n0) {
 tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
     if (!c) return fail(TC_INVALID_ARG, "tc_step");
     TCB_CUDA_CHECK(cudaSetDevice(c->desc.device));
+    {
+        tc_status r0 = consume_staged(c);
+        if (r0 != TC_OK) return r0;
+    }
     const int k = update ? 1 : 0;
     // The iteration / first-sample counters that the dropout kernels read live in
     // device memory; a one-thread kernel sets them ahead of the (captured) step, so
@@ -1398,7 +1445,9 @@ tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
 
 tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
     if (!c || index < 0 || index >= c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_exec_stmt");
-    tc_status r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    tc_status r = consume_staged(c);
+    if (r != TC_OK) return r;
+    r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
     if (r != TC_OK) return r;
     r = exec_stmt(c, index);
     if (r != TC_OK) return r;
@@ -1421,6 +1470,7 @@ tc_status tc_loss(tc_ctx* c, double* loss) {
 
 tc_status tc_sync(tc_ctx* c) {
     if (!c) return fail(TC_INVALID_ARG, "tc_sync");
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->copy_st));
     TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
     return TC_OK;
 }
@@ -1514,7 +1564,9 @@ int tc_launches_per_step(tc_ctx* c) { return c ? c->launches_per_step : -1; }
 
 tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_ms, int max) {
     if (!c || !stmt_ms || max < c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_profile_step");
-    tc_status r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    tc_status r = consume_staged(c);
+    if (r != TC_OK) return r;
+    r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
     if (r != TC_OK) return r;
     const int n = c->plan->nstmts;
     std::vector<cudaEvent_t> ev(n + 1);

@@ -65,7 +65,8 @@ class Trainer:
     def stage_batch(self, x, y):
         x = np.ascontiguousarray(x, np.float32)
         y = np.ascontiguousarray(y, np.int32)
-        self._staged = (x, y)  # keep host buffers alive until the async copy is done
+        # host buffers stay alive while their async copy may be in flight (two staging slots)
+        self._staged = (getattr(self, "_staged", (None,))[-1], (x, y))
         nat.check(nat.lib().tc_stage_batch(self._h, x.ctypes.data, y.ctypes.data))
 
     def stage_synthetic(self, it: int, n0: int = 0):

@@ -206,3 +206,29 @@ def test_bucket_overlap_matches_serial(name, batch, monkeypatch):
     assert outs[0][0] == outs[1][0]
     for a, b in zip(outs[0][1] + outs[0][2], outs[1][1] + outs[1][2]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_async_input_pipeline_matches_serial():
+    """Batches staged one step ahead (H2D on the copy stream overlapping the running step,
+    two staging slots) train exactly like batches staged and consumed one at a time."""
+    net = compile_network("alexnet", 4)
+    batches = [orc.synth_batch(net, 3, it) for it in range(4)]
+    runs = []
+    for ahead in (False, True):
+        tr = Trainer(net, use_graph=True, seed=9)
+        tr.init_params()
+        losses = []
+        if ahead:
+            tr.stage_batch(*batches[0])
+        for it in range(4):
+            if not ahead:
+                tr.stage_batch(*batches[it])
+            tr.step(it)
+            if ahead and it + 1 < 4:
+                tr.stage_batch(*batches[it + 1])
+            losses.append(tr.loss())
+        runs.append((losses, [tr.get_param(i) for i in range(len(net.params))]))
+        tr.close()
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        np.testing.assert_array_equal(a, b)
