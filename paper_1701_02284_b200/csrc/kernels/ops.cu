@@ -124,16 +124,19 @@ __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, 
 // empty window); the flat NCHW index the reference reports is
 // reconstructed from it on download (tc_pool_indices_download), so the index
 // stream costs 1 B per output instead of 4.
+// IT: index type of the element loop (int when the tensor has < 2^31 chunks: 64-bit
+// division is ~4x the cost of 32-bit on this path)
+template <typename IT>
 __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
                            uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
-    const long long total = yo.pixels() * cg;
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const IT total = static_cast<IT>(yo.pixels() * cg);
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
         const int g = static_cast<int>(t % cg);
-        long long p = t / cg;
+        IT p = t / cg;
         const int ow = static_cast<int>(p % yo.W);
         p /= yo.W;
         const int oh = static_cast<int>(p % yo.H);
@@ -184,17 +187,18 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
 
 // Gather formulation: each input element sums the windows that selected it
 // (no atomics; fixed window order, deterministic).
+template <typename IT>
 __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
                            bf16* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
-    const long long total = xi.pixels() * cg;
+    const IT total = static_cast<IT>(xi.pixels() * cg);
     const float inv = 1.f / static_cast<float>(k * k);
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
         const int g = static_cast<int>(t % cg);
-        long long p = t / cg;
+        IT p = t / cg;
         const int iw = static_cast<int>(p % xi.W);
         p /= xi.W;
         const int ih = static_cast<int>(p % xi.H);
@@ -544,29 +548,22 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
                                                     const float* __restrict__ beta, float* __restrict__ coef) {
     pdl_wait();
     pdl_trigger();
-    // 32 channels per block; 8 split-lanes per channel, each summing a fixed strided subset,
-    // combined in lane order (deterministic)
-    __shared__ float sa_sm[8][33], sb_sm[8][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + tx;
+    // one warp per channel: lane l sums splits l, l+32, ...; the warp combines the 32 lane sums
+    // with a fixed xor tree (deterministic)
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= C) return;
     float sa = 0.f, sb = 0.f;
-    if (c < C) {
-        for (int q = ty; q < splits; q += 8) {
-            sa += part[static_cast<long long>(q) * C + c];
-            if (MODE != RED_SUM) sb += part[static_cast<long long>(splits + q) * C + c];
-        }
+    for (int q = lane; q < splits; q += 32) {
+        sa += part[static_cast<long long>(q) * C + c];
+        if (MODE != RED_SUM) sb += part[static_cast<long long>(splits + q) * C + c];
     }
-    sa_sm[ty][tx] = sa;
-    sb_sm[ty][tx] = sb;
-    __syncthreads();
-    if (ty != 0 || c >= C) return;
-    sa = 0.f;
-    sb = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        sa += sa_sm[q][tx];
-        sb += sb_sm[q][tx];
+    for (int o = 16; o; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        if (MODE != RED_SUM) sb += __shfl_xor_sync(0xffffffffu, sb, o);
     }
+    if (lane != 0) return;
     if (MODE == RED_SUM) {
         out[c] = sa * scale;
     } else if (MODE == RED_STATS) {
@@ -600,7 +597,7 @@ __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restri
         for (int u = 0; u < 2; ++u) {
             const long long i = i0 + u * S;
             if (i >= n8) break;
-            const int c0 = static_cast<int>(i % ld8) * 8;
+            const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
             float f[8];
             unpack8(q[u], f);
 #pragma unroll
@@ -643,7 +640,7 @@ __global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __rest
         for (int u = 0; u < 2; ++u) {
             const long long i = i0 + u * S;
             if (i >= n8) break;
-            const int c0 = static_cast<int>(i % ld8) * 8;
+            const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
             float f[8], g[8];
             unpack8(q[u], f);
             unpack8(r[u], g);
@@ -721,19 +718,42 @@ __global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int 
 // ---------------------------------------------------------------- LRN v2: thread per (pixel, 8 channels)
 // Window sums over channels [c - n/2, c + n/2] read the neighbouring 16-byte
 // chunks of the same pixel (L1 hits); n <= 9 so chunks g-1 .. g+1 suffice.
+// v[8..16) = channels g*8..g*8+7 and NEED channels either side (zero beyond the tensor).
+// NEED <= 4 reads the neighbours with 8-byte loads, otherwise whole neighbour chunks.
+template <int NEED>
 __device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, int ng, float (&v)[24]) {
+    static_assert(NEED <= 8, "LRN window too wide");
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(p + g * 8), f);
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const int gg = g - 1 + q;
-        float f[8];
-        if (gg >= 0 && gg < ng) {
-            unpack8(*reinterpret_cast<const uint4*>(p + gg * 8), f);
-        } else {
+    for (int j = 0; j < 8; ++j) v[8 + j] = f[j];
+    if constexpr (NEED <= 4) {
+        uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
+        if (g > 0) lo = *reinterpret_cast<const uint2*>(p + g * 8 - 4);
+        if (g + 1 < ng) hi = *reinterpret_cast<const uint2*>(p + g * 8 + 8);
+        const __nv_bfloat162* l2 = reinterpret_cast<const __nv_bfloat162*>(&lo);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hi);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) f[j] = 0.f;
+        for (int i = 0; i < 2; ++i) {
+            const float2 a = __bfloat1622float2(l2[i]), b = __bfloat1622float2(h2[i]);
+            v[4 + 2 * i] = a.x;
+            v[5 + 2 * i] = a.y;
+            v[16 + 2 * i] = b.x;
+            v[17 + 2 * i] = b.y;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[q * 8 + j] = f[j];
+        for (int j = 0; j < 4; ++j) v[j] = v[20 + j] = 0.f;
+    } else {
+        float lo[8], hi[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lo[j] = hi[j] = 0.f;
+        if (g > 0) unpack8(*reinterpret_cast<const uint4*>(p + g * 8 - 8), lo);
+        if (g + 1 < ng) unpack8(*reinterpret_cast<const uint4*>(p + g * 8 + 8), hi);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = lo[j];
+            v[16 + j] = hi[j];
+        }
     }
 }
 
@@ -749,10 +769,11 @@ __global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act
     const float an = alpha / static_cast<float>(2 * HALF + 1);
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(t % ng);
-        const bf16* px = x + (t / ng) * a.cs;
+        const bool i32 = total < (1ll << 31);
+        const int g = i32 ? static_cast<int>(t) % ng : static_cast<int>(t % ng);
+        const bf16* px = x + (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
         float v[24];
-        load_chunk3(px, g, ng, v);
+        load_chunk3<HALF>(px, g, ng, v);
         // channels outside [0, C) contribute nothing (pads are zero, neighbours beyond the tensor loaded as 0)
         float out[8];
 #pragma unroll
@@ -778,12 +799,13 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
     constexpr int L = 8 - HALF, U = 16 + HALF;  // window of channels g*8-HALF .. g*8+7+HALF
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(t % ng);
-        const long long base = (t / ng) * a.cs;
+        const bool i32 = total < (1ll << 31);
+        const int g = i32 ? static_cast<int>(t) % ng : static_cast<int>(t % ng);
+        const long long base = (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
         float xv[24], dv[24], yv[24];
-        load_chunk3(x + base, g, ng, xv);
-        load_chunk3(dy + base, g, ng, dv);
-        load_chunk3(y + base, g, ng, yv);
+        load_chunk3<2 * HALF>(x + base, g, ng, xv);
+        load_chunk3<HALF>(dy + base, g, ng, dv);
+        load_chunk3<HALF>(y + base, g, ng, yv);
         float sc[24], tt[24];
 #pragma unroll
         for (int i = L; i < U; ++i) {
@@ -792,7 +814,7 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
             for (int d = -HALF; d <= HALF; ++d) s += xv[i + d] * xv[i + d];
             sc[i] = kk + an * s;
             // zero for channels outside [0, C): dy and y are zero there
-            tt[i] = dv[i] * yv[i] * __frcp_rn(sc[i]);
+            tt[i] = __fdividef(dv[i] * yv[i], sc[i]);  // MUFU reciprocal: output is bf16
         }
         float out[8];
 #pragma unroll
@@ -830,6 +852,45 @@ __device__ __forceinline__ bool stage_src(const StageLayout& L, long long i, int
     h = P * L.s2d + ij / L.s2d - L.pad;
     w = Q * L.s2d + ij % L.s2d - L.pad;
     return c < L.C && h >= 0 && h < L.H && w >= 0 && w < L.W;
+}
+
+// Row-tiled staging: block (n, output row) reads the source rows it needs coalesced into
+// shared memory ([c][row][w] fp32, zero outside the image), then writes the output row as
+// 16-byte chunks.  Output row = image row h (NHWC) or space-to-depth row P (rows s*P - pad + i).
+__global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x, bf16* __restrict__ y, StageLayout L,
+                                                    int log2_cs, int log2_s) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ float tile[];
+    const int rows_out = L.s2d ? L.Hs : L.H;
+    const int n = blockIdx.x / rows_out, r = blockIdx.x - n * rows_out;
+    const int s = 1 << log2_s;
+    const int h0 = L.s2d ? r * s - L.pad : r;
+    const int C = L.C, W = L.W;
+    for (int ci = 0; ci < C * s; ++ci) {  // tile row (c, i): source row h0 + i of channel c
+        const int c = ci >> log2_s, h = h0 + (ci & (s - 1));
+        const bool ok = h >= 0 && h < L.H;
+        const float* src = x + ((static_cast<long long>(n) * C + c) * L.H + h) * W;
+        for (int w = threadIdx.x; w < W; w += blockDim.x) tile[ci * W + w] = ok ? __ldcs(src + w) : 0.f;
+    }
+    __syncthreads();
+    const int log2_cc = 2 * log2_s + log2_cs;  // output channels per output pixel = s*s*cs
+    const int wout = L.s2d ? L.Ws : L.W;
+    const int chunks = (wout << log2_cc) >> 3;
+    uint4* out = reinterpret_cast<uint4*>(y + (static_cast<long long>(n) * rows_out + r) * (static_cast<long long>(wout) << log2_cc));
+    for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
+        const int e0 = q << 3;
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int Q = (e0 + j) >> log2_cc, ch = (e0 + j) & ((1 << log2_cc) - 1);
+            const int c = ch & ((1 << log2_cs) - 1), ij = ch >> log2_cs;
+            const int i = ij >> log2_s, jj = ij & (s - 1);
+            const int w = L.s2d ? (Q << log2_s) + jj - L.pad : Q;
+            f[j] = (c < C && w >= 0 && w < W) ? tile[((c << log2_s) + i) * W + w] : 0.f;
+        }
+        out[q] = pack8(f);
+    }
 }
 
 __global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y, StageLayout L) {
@@ -1003,13 +1064,21 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
 tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
     if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
-    TCB_LAUNCH(k_pool_fwd, EW_GRID(yo.pixels() * (xi.cs / 8)), x, xi, y, yo, idx, k, stride, pad, is_max);
+    const long long n = yo.pixels() * (xi.cs / 8);
+    if (n < (1ll << 31))
+        TCB_LAUNCH((k_pool_fwd<int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
+    else
+        TCB_LAUNCH((k_pool_fwd<long long>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
-    TCB_LAUNCH(k_pool_bwd, EW_GRID(xi.pixels() * (xi.cs / 8)), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+    const long long n = xi.pixels() * (xi.cs / 8);
+    if (n < (1ll << 31))
+        TCB_LAUNCH((k_pool_bwd<int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+    else
+        TCB_LAUNCH((k_pool_bwd<long long>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1119,7 +1188,7 @@ tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, f
     RedPlan rp;
     tc_status s = chan_reduce<RED_SUM>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_SUM>), (cols + 31) / 32, 256, 0, st, partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_SUM>), (cols + 7) / 8, 256, 0, st, partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -1147,7 +1216,7 @@ tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_STATS>), (C + 31) / 32, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+    TCB_LAUNCH((k_chan_final<RED_STATS>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
@@ -1161,7 +1230,7 @@ tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_BNBWD>), (C + 31) / 32, 256, 0, st, partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_BNBWD>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
                                                               nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -1181,6 +1250,16 @@ tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma,
 }
 
 tc_status launch_nchw_to_nhwc(const float* x, bf16* y, StageLayout L, cudaStream_t st) {
+    const int s = L.s2d ? L.s2d : 1;
+    const size_t smem = static_cast<size_t>(L.C) * s * L.W * sizeof(float);
+    const int wout = L.s2d ? L.Ws : L.W;
+    auto log2i = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
+    const int lcs = log2i(L.cs), ls = log2i(s);
+    if (smem <= 48 * 1024 && lcs >= 0 && ls >= 0 && (static_cast<long long>(wout) * s * s * L.cs) % 8 == 0) {
+        TCB_LAUNCH(k_stage_rows, L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
+        TCB_LAUNCH_CHECK();
+        return TC_OK;
+    }
     TCB_LAUNCH(k_nchw_to_nhwc, EW_GRID(L.elems()), x, y, L);
     TCB_LAUNCH_CHECK();
     return TC_OK;

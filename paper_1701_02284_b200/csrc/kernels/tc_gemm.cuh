@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         const bool a_sw64 = p.a_mode == OP_IM2COL32_K;
         const bool b_sw64 = p.b_mode == OP_IM2COL32_MN;
         const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN || b_sw64;
-        const uint32_t idesc = umma_idesc_bf16(BM * CG, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
+        const uint32_t idesc_full = umma_idesc_bf16(BM * CG, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
         int it = 0, tc = 0;
         for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
@@ -541,6 +541,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             mbar_wait(&tempty[buf], ((tc >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + buf * BN;
+            // the last column tile issues only the columns that exist (rounded to 16): N = 96 on
+            // a 128-wide tile costs 96/128 of the MMA time (single-CTA tiles)
+            uint32_t idesc = idesc_full;
+            if (CG == 1) {
+                // K-major B: any multiple of 16; MN-major B: whole swizzle atoms (64 / 32 columns)
+                const int gran = b_sw64 ? 32 : b_mn ? 64 : 16;
+                const int n_left = p.N - w.nt * BN;
+                if (n_left < BN)
+                    idesc = umma_idesc_bf16(BM, static_cast<uint32_t>((n_left + gran - 1) / gran * gran), a_mn ? 1u : 0u,
+                                            b_mn ? 1u : 0u);
+            }
             for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
                 const int s = it % S;
                 mbar_wait(&full[s], (it / S) & 1);
