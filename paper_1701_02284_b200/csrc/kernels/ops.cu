@@ -65,17 +65,29 @@ __global__ void k_relu_bwd(const uint4* __restrict__ dy, const uint4* __restrict
     }
 }
 
-__global__ void k_add(const uint4* __restrict__ a, const uint4* __restrict__ b, uint4* __restrict__ y, long long n8) {
+__global__ void k_add(const uint4* __restrict__ a, const uint4* __restrict__ b, uint4* __restrict__ y, long long n8,
+                      int relu) {
     pdl_wait();
     pdl_trigger();
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float p[8], q[8];
-        unpack8(a[i], p);
-        unpack8(b[i], q);
+    const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
+        uint4 qa[2], qb[2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) p[j] += q[j];
-        y[i] = pack8(p);
+        for (int u = 0; u < 2; ++u) {
+            const bool ok = i0 + u * S < n8;
+            qa[u] = ok ? a[i0 + u * S] : make_uint4(0, 0, 0, 0);
+            qb[u] = ok ? b[i0 + u * S] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (i0 + u * S >= n8) break;
+            float p[8], q[8];
+            unpack8(qa[u], p);
+            unpack8(qb[u], q);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) p[j] = relu ? fmaxf(p[j] + q[j], 0.f) : p[j] + q[j];
+            y[i0 + u * S] = pack8(p);
+        }
     }
 }
 
@@ -585,7 +597,7 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
 
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
 __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restrict__ coef, uint4* __restrict__ y,
-                              long long n8, int ld8, int C) {
+                              long long n8, int ld8, int C, int relu) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -601,8 +613,10 @@ __global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restri
             float f[8];
             unpack8(q[u], f);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 8; ++j) {
                 f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
+                if (relu) f[j] = fmaxf(f[j], 0.f);
+            }
             y[i] = pack8(f);
         }
     }
@@ -1042,9 +1056,9 @@ tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, 
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, cudaStream_t st) {
+tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, int relu, cudaStream_t st) {
     TCB_LAUNCH(k_add, EW_GRID(n / 8), reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
-                               reinterpret_cast<uint4*>(y), n / 8);
+                               reinterpret_cast<uint4*>(y), n / 8, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1211,7 +1225,7 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st) {
 }
 
 tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
-                        int C, int cs, float eps, float* partials, int max_partials, cudaStream_t st) {
+                        int C, int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st) {
     RedPlan rp;
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
@@ -1220,7 +1234,8 @@ tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    TCB_LAUNCH(k_chan_affine, EW_GRID(n8), reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C);
+    TCB_LAUNCH(k_chan_affine, EW_GRID(n8), reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C,
+               relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

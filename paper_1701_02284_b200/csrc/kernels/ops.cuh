@@ -25,7 +25,8 @@ struct Act4 {  // NHWC activation view
 
 tc_status launch_relu_fwd(const bf16* x, bf16* y, long long n, cudaStream_t st);
 tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, cudaStream_t st);
-tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, cudaStream_t st);
+// y = a + b (then max(y, 0) when relu: a residual add followed by an in-place ReLU)
+tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, int relu, cudaStream_t st);
 // y = x * keep * scale (inverted dropout; keep is a 0/1 byte mask)
 tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16* y, long long n, cudaStream_t st);
 // keep[n, e] for every stored element; e = NCHW element index within the sample (tc_philox.h)
@@ -68,10 +69,11 @@ tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs
 tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 
 // BatchNorm over NHWC [pixels][cs] (training-mode batch statistics, biased variance):
-// stats = (mean[C], istd[C]); y = gamma * (x - mean) * istd + beta.
+// stats = (mean[C], istd[C]); y = gamma * (x - mean) * istd + beta (then max(y, 0) when relu: the
+// in-place ReLU that follows a BN is folded into the apply pass).
 // `partials` holds max_partials floats of reduction scratch plus 3*C coefficient floats.
 tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
-                        int C, int cs, float eps, float* partials, int max_partials, cudaStream_t st);
+                        int C, int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st);
 // sums = (sum dy[C], sum dy * xhat[C]) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) and dx
 tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats, float* sums, long long pixels, int C,
                                int cs, float* partials, int max_partials, cudaStream_t st);

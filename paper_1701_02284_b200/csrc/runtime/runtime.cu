@@ -360,7 +360,9 @@ void plan_fusion(tc_ctx* c) {
     };
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
-        if (s.kind != TC_STMT_LET || (s.op != TC_OP_CONV_FWD && s.op != TC_OP_MATMUL_FWD)) continue;
+        if (s.kind != TC_STMT_LET || (s.op != TC_OP_CONV_FWD && s.op != TC_OP_MATMUL_FWD && s.op != TC_OP_BN_FWD &&
+                                      s.op != TC_OP_ADD))
+            continue;
         int j = next_let(i);
         if (s.op == TC_OP_MATMUL_FWD && j >= 0 && p->stmts[j].op == TC_OP_BIAS_ADD && p->stmts[j].inplace &&
             p->stmts[j].in[0].kind == TC_REF_VAR && p->stmts[j].in[0].index == s.var &&
@@ -376,7 +378,9 @@ void plan_fusion(tc_ctx* c) {
             }
             continue;
         }
-        if (s.op == TC_OP_CONV_FWD && j >= 0 && p->stmts[j].op == TC_OP_RELU_FWD && p->stmts[j].inplace &&
+        if ((s.op == TC_OP_CONV_FWD || s.op == TC_OP_BN_FWD || s.op == TC_OP_ADD) && j >= 0 &&
+            p->stmts[j].op == TC_OP_RELU_FWD &&
+            p->stmts[j].inplace &&
             p->stmts[j].in[0].kind == TC_REF_VAR && p->stmts[j].in[0].index == s.var) {
             c->fuse_relu[i] = 1;
             c->fused[j] = 1;
@@ -828,7 +832,7 @@ tc_status exec_let(tc_ctx* c, int i) {
                                      out.elems(), st);
             return launch_add_bf16(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
                                    reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
-                                   out.elems(), st);
+                                   out.elems(), c->fuse_relu[i], st);
         case TC_OP_SCALE:
         case TC_OP_LOG:
         case TC_OP_RECIP: {
@@ -916,7 +920,7 @@ tc_status exec_let(tc_ctx* c, int i) {
             return launch_bn_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[1].index].p,
                                  c->params[s.in[2].index].p, reinterpret_cast<bf16*>(y), stats,
                                  static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, static_cast<float>(s.eps),
-                                 c->partials, c->max_partials, st);
+                                 c->fuse_relu[i], c->partials, c->max_partials, st);
         }
         case TC_OP_BN_BWD_DATA: {
             const VarL& up = P.L(s.in[0]);
