@@ -31,7 +31,12 @@ typedef struct tc_ctx_desc {
     uint64_t seed;           /* TENSORC_SEED, default 42 */
     int use_graph;           /* capture the step in a CUDA graph after the first run */
     int keep;                /* parity mode: every storage gets its own arena range */
+    int precision;           /* TC_PREC_BF16 (default): bf16 activations, bf16 tensor-core operands;
+                                TC_PREC_F32: fp32 activations, every contraction as a 3 x bf16 split
+                                (hi*hi + hi*lo + lo*hi, ~16-bit mantissa) on the same tcgen05 kernels */
 } tc_ctx_desc;
+
+enum { TC_PREC_BF16 = 0, TC_PREC_F32 = 1 };
 
 typedef struct tc_rt_memory {
     int64_t arena_bytes;       /* activation arena (per-step peak, device dtypes) */

@@ -127,7 +127,10 @@ class CompileOpts(C.Structure):
 
 class CtxDesc(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_void_p),
-                ("seed", C.c_uint64), ("use_graph", C.c_int), ("keep", C.c_int)]
+                ("seed", C.c_uint64), ("use_graph", C.c_int), ("keep", C.c_int), ("precision", C.c_int)]
+
+
+TC_PREC_BF16, TC_PREC_F32 = 0, 1
 
 
 class RtMemory(C.Structure):

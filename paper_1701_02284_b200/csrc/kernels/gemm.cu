@@ -476,8 +476,13 @@ size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     return static_cast<size_t>(lp.splits) * M * N * sizeof(float);
 }
 
-tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
-                        void* ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace tcb {
+// fprop / bwd-data with the output stored in bf16 (y_f32 = 0, the C ABI) or fp32 (the parity
+// precision mode's 3 x bf16 split contractions)
+tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
+                      int y_f32, void* ws, size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
     GemmParams p;
@@ -509,11 +514,12 @@ tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, con
     p.b_mode = OP_TMA_K;
     if (!make_tmap_2d_bf16(&p.tmB, w, p.K, d->K, filter_ld(d), BK, lp.bn / lp.cg, &err)) return fail(TC_INVALID_ARG, err);
     // Bias is read only for n < K; padded channels get 0 (relu(0) = 0).
-    return run_gemm(p, lp, y, d->ks, 1, bias, d->K, relu, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return run_gemm(p, lp, y, d->ks, y_f32 ? 0 : 1, bias, d->K, relu, 0.f, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream));
 }
 
-tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, void* ws,
-                             size_t ws_bytes, void* stream) {
+tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
+                           size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
     if (d->cs % 8) return fail(TC_INVALID_ARG, "conv bwd-data needs a channel stride multiple of 8");
@@ -548,7 +554,21 @@ tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* 
     }
     p.b_mode = OP_TMA_MN;
     if (!make_tmap_2d_bf16(&p.tmB, w_rskc, d->cs, p.K, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
-    return run_gemm(p, lp, dx, d->cs, 1, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return run_gemm(p, lp, dx, d->cs, dx_f32 ? 0 : 1, nullptr, 0, 0, 0.f, ws, ws_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+}  // namespace tcb
+
+extern "C" {
+
+tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
+                        void* ws, size_t ws_bytes, void* stream) {
+    return conv_fwd_ex(d, x, w, bias, relu, y, 0, ws, ws_bytes, stream);
+}
+
+tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, void* ws,
+                             size_t ws_bytes, void* stream) {
+    return conv_bwd_data_ex(d, dy, w_rskc, dx, 0, ws, ws_bytes, stream);
 }
 
 tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void* x, float* dw, void* ws,

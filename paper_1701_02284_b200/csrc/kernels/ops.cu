@@ -36,74 +36,119 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
     return q;
 }
 
-// ---------------------------------------------------------------- elementwise (8 x bf16 per thread)
-__global__ void k_relu_fwd(const uint4* __restrict__ x, uint4* __restrict__ y, long long n8) {
+// Storage-type generic access: activations are bf16 (default) or fp32 (the parity precision
+// mode); every kernel computes in fp32 and touches 8 consecutive elements per access.
+__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+__device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
+__device__ __forceinline__ void ld8(const float* p, float (&f)[8]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+// raw (packed) 8-element registers, unpacked later: keeps loads in flight without widening
+template <typename T>
+struct Raw8 {
+    uint4 q;
+};
+template <>
+struct Raw8<float> {
+    float4 a, b;
+};
+__device__ __forceinline__ Raw8<bf16> ld_raw8cs(const bf16* p) { return Raw8<bf16>{__ldcs(reinterpret_cast<const uint4*>(p))}; }
+__device__ __forceinline__ Raw8<float> ld_raw8cs(const float* p) {
+    return Raw8<float>{__ldcs(reinterpret_cast<const float4*>(p)), __ldcs(reinterpret_cast<const float4*>(p) + 1)};
+}
+template <typename T>
+__device__ __forceinline__ Raw8<T> raw8_zero() {
+    Raw8<T> r;
+    if constexpr (sizeof(T) == 2) r.q = make_uint4(0, 0, 0, 0);
+    else r.a = r.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    return r;
+}
+__device__ __forceinline__ void unpack_raw(const Raw8<bf16>& r, float (&f)[8]) { unpack8(r.q, f); }
+__device__ __forceinline__ void unpack_raw(const Raw8<float>& r, float (&f)[8]) {
+    f[0] = r.a.x, f[1] = r.a.y, f[2] = r.a.z, f[3] = r.a.w, f[4] = r.b.x, f[5] = r.b.y, f[6] = r.b.z, f[7] = r.b.w;
+}
+__device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) { *reinterpret_cast<uint4*>(p) = pack8(f); }
+__device__ __forceinline__ void st8(float* p, const float (&f)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+}
+
+// ---------------------------------------------------------------- elementwise (8 elements per thread)
+template <typename T>
+__global__ void k_relu_fwd(const T* __restrict__ x, T* __restrict__ y, long long n8) {
     pdl_wait();
     pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float f[8];
-        unpack8(x[i], f);
+        ld8(x + i * 8, f);
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
-        y[i] = pack8(f);
+        st8(y + i * 8, f);
     }
 }
 
-__global__ void k_relu_bwd(const uint4* __restrict__ dy, const uint4* __restrict__ y, uint4* __restrict__ dx,
-                           long long n8) {
+template <typename T>
+__global__ void k_relu_bwd(const T* __restrict__ dy, const T* __restrict__ y, T* __restrict__ dx, long long n8) {
     pdl_wait();
     pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float g[8], f[8];
-        unpack8(dy[i], g);
-        unpack8(y[i], f);
+        ld8(dy + i * 8, g);
+        ld8(y + i * 8, f);
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[j] = f[j] > 0.f ? g[j] : 0.f;
-        dx[i] = pack8(g);
+        st8(dx + i * 8, g);
     }
 }
 
-__global__ void k_add(const uint4* __restrict__ a, const uint4* __restrict__ b, uint4* __restrict__ y, long long n8,
-                      int relu) {
+template <typename T>
+__global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y, long long n8, int relu) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
-        uint4 qa[2], qb[2];
+        float p[2][8], q[2][8];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const bool ok = i0 + u * S < n8;
-            qa[u] = ok ? a[i0 + u * S] : make_uint4(0, 0, 0, 0);
-            qb[u] = ok ? b[i0 + u * S] : make_uint4(0, 0, 0, 0);
+            if (i0 + u * S < n8) {
+                ld8(a + (i0 + u * S) * 8, p[u]);
+                ld8(b + (i0 + u * S) * 8, q[u]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             if (i0 + u * S >= n8) break;
-            float p[8], q[8];
-            unpack8(qa[u], p);
-            unpack8(qb[u], q);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) p[j] = relu ? fmaxf(p[j] + q[j], 0.f) : p[j] + q[j];
-            y[i0 + u * S] = pack8(p);
+            for (int j = 0; j < 8; ++j) p[u][j] = relu ? fmaxf(p[u][j] + q[u][j], 0.f) : p[u][j] + q[u][j];
+            st8(y + (i0 + u * S) * 8, p[u]);
         }
     }
 }
 
-__global__ void k_mask_mul(const uint4* __restrict__ x, const uint2* __restrict__ keep, float scale,
-                           uint4* __restrict__ y, long long n8) {
+template <typename T>
+__global__ void k_mask_mul(const T* __restrict__ x, const uint2* __restrict__ keep, float scale, T* __restrict__ y,
+                           long long n8) {
     pdl_wait();
     pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float f[8];
-        unpack8(x[i], f);
+        ld8(x + i * 8, f);
         const uint2 m = keep[i];
         const uint8_t* mb = reinterpret_cast<const uint8_t*>(&m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = mb[j] ? f[j] * scale : 0.f;
-        y[i] = pack8(f);
+        st8(y + i * 8, f);
     }
 }
 
@@ -138,8 +183,8 @@ __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, 
 // stream costs 1 B per output instead of 4.
 // IT: index type of the element loop (int when the tensor has < 2^31 chunks: 64-bit
 // division is ~4x the cost of 32-bit on this path)
-template <typename IT>
-__global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
+template <typename T, typename IT>
+__global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, Act4 yo,
                            uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
     pdl_wait();
     pdl_trigger();
@@ -161,7 +206,7 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
             sum[j] = 0.f;
             bi[j] = 255;
         }
-        const bf16* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
+        const T* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
         for (int r = 0; r < k; ++r) {
             const int ih = oh * stride - pad + r;
             if (ih < 0 || ih >= xi.H) continue;
@@ -169,7 +214,7 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
                 const int iw = ow * stride - pad + s;
                 if (iw < 0 || iw >= xi.W) continue;
                 float f[8];
-                unpack8(__ldg(reinterpret_cast<const uint4*>(img + (static_cast<long long>(ih) * xi.W + iw) * xi.cs)), f);
+                ld8(img + (static_cast<long long>(ih) * xi.W + iw) * xi.cs, f);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     sum[j] += f[j];
@@ -185,7 +230,7 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
         const float inv = 1.f / static_cast<float>(k * k);
 #pragma unroll
         for (int j = 0; j < 8; ++j) out[j] = is_max ? best[j] : sum[j] * inv;
-        *reinterpret_cast<uint4*>(y + o) = pack8(out);
+        st8(y + o, out);
         if (idx) {
             uint2 q;
             q.x = static_cast<uint32_t>(bi[0]) | static_cast<uint32_t>(bi[1]) << 8 | static_cast<uint32_t>(bi[2]) << 16 |
@@ -199,9 +244,9 @@ __global__ void k_pool_fwd(const bf16* __restrict__ x, Act4 xi, bf16* __restrict
 
 // Gather formulation: each input element sums the windows that selected it
 // (no atomics; fixed window order, deterministic).
-template <typename IT>
-__global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
-                           bf16* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
+template <typename T, typename IT>
+__global__ void k_pool_bwd(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
+                           T* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
@@ -228,7 +273,7 @@ __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* 
             for (int ow = ow0; ow <= ow1; ++ow) {
                 const long long o = obase + (static_cast<long long>(oh) * yo.W + ow) * yo.cs;
                 float d[8];
-                unpack8(__ldg(reinterpret_cast<const uint4*>(dy + o)), d);
+                ld8(dy + o, d);
                 if (is_max) {
                     const uint32_t me = static_cast<uint32_t>((ih - (oh * stride - pad)) * k + (iw - (ow * stride - pad)));
                     const uint2 q = __ldg(reinterpret_cast<const uint2*>(idx + o));
@@ -242,12 +287,13 @@ __global__ void k_pool_bwd(const bf16* __restrict__ dy, Act4 yo, const uint8_t* 
                     for (int j = 0; j < 8; ++j) acc[j] += d[j] * inv;
                 }
             }
-        *reinterpret_cast<uint4*>(dx + ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8) = pack8(acc);
+        st8(dx + ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8, acc);
     }
 }
 
 // ---------------------------------------------------------------- LRN (across channels, one warp per pixel)
-__global__ void k_lrn_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, int size, float alpha, float beta,
+template <typename T>
+__global__ void k_lrn_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, int size, float alpha, float beta,
                           float kk) {
     pdl_wait();
     pdl_trigger();
@@ -258,9 +304,9 @@ __global__ void k_lrn_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4
     const float an = alpha / static_cast<float>(size);
     for (long long p = blockIdx.x * static_cast<long long>(warps) + wid; p < a.pixels();
          p += static_cast<long long>(gridDim.x) * warps) {
-        const bf16* xp = x + p * a.cs;
+        const T* xp = x + p * a.cs;
         for (int c = lane; c < a.cs; c += 32) {
-            const float v = __bfloat162float(xp[c]);
+            const float v = to_f(xp[c]);
             sq[c] = v * v;
         }
         __syncwarp();
@@ -270,16 +316,17 @@ __global__ void k_lrn_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4
                 float s = 0.f;
                 for (int cc = max(0, c - half); cc <= min(a.C - 1, c + half); ++cc) s += sq[cc];
                 const float scale = kk + an * s;
-                out = __bfloat162float(xp[c]) * powf(scale, -beta);
+                out = to_f(xp[c]) * powf(scale, -beta);
             }
-            y[p * a.cs + c] = __float2bfloat16_rn(out);
+            y[p * a.cs + c] = from_f<T>(out);
         }
         __syncwarp();
     }
 }
 
-__global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
-                          bf16* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
+template <typename T>
+__global__ void k_lrn_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
+                          T* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ float sm[];
@@ -294,7 +341,7 @@ __global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ 
          p += static_cast<long long>(gridDim.x) * warps) {
         const long long o = p * a.cs;
         for (int c = lane; c < a.cs; c += 32) {
-            const float v = __bfloat162float(x[o + c]);
+            const float v = to_f(x[o + c]);
             sq[c] = v * v;
         }
         __syncwarp();
@@ -302,7 +349,7 @@ __global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ 
             float s = 0.f;
             for (int cc = max(0, c - half); cc <= min(a.C - 1, c + half); ++cc) s += sq[cc];
             sc[c] = kk + an * s;
-            tt[c] = __bfloat162float(dy[o + c]) * __bfloat162float(y[o + c]) / sc[c];
+            tt[c] = to_f(dy[o + c]) * to_f(y[o + c]) / sc[c];
         }
         __syncwarp();
         for (int c = lane; c < a.cs; c += 32) {
@@ -310,33 +357,35 @@ __global__ void k_lrn_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ 
             if (c < a.C) {
                 float s = 0.f;
                 for (int cc = max(0, c - half); cc <= min(a.C - 1, c + half); ++cc) s += tt[cc];
-                out = __bfloat162float(dy[o + c]) * powf(sc[c], -beta) - coef * __bfloat162float(x[o + c]) * s;
+                out = to_f(dy[o + c]) * powf(sc[c], -beta) - coef * to_f(x[o + c]) * s;
             }
-            dx[o + c] = __float2bfloat16_rn(out);
+            dx[o + c] = from_f<T>(out);
         }
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------- softmax / loss head (fp32)
-__global__ void k_softmax_fwd(const bf16* __restrict__ x, long long ld, float* __restrict__ y, int rows, int F) {
+template <typename T>
+__global__ void k_softmax_fwd(const T* __restrict__ x, long long ld, float* __restrict__ y, int rows, int F) {
     pdl_wait();
     pdl_trigger();
     const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int r = blockIdx.x * warps + wid; r < rows; r += gridDim.x * warps) {
-        const bf16* xr = x + r * ld;
+        const T* xr = x + r * ld;
         float m = -INFINITY;
-        for (int j = lane; j < F; j += 32) m = fmaxf(m, __bfloat162float(xr[j]));
+        for (int j = lane; j < F; j += 32) m = fmaxf(m, to_f(xr[j]));
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         float s = 0.f;
-        for (int j = lane; j < F; j += 32) s += expf(__bfloat162float(xr[j]) - m);
+        for (int j = lane; j < F; j += 32) s += expf(to_f(xr[j]) - m);
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         const float inv = 1.f / s;
-        for (int j = lane; j < F; j += 32) y[static_cast<long long>(r) * F + j] = expf(__bfloat162float(xr[j]) - m) * inv;
+        for (int j = lane; j < F; j += 32) y[static_cast<long long>(r) * F + j] = expf(to_f(xr[j]) - m) * inv;
     }
 }
 
-__global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restrict__ y, bf16* __restrict__ dx,
+template <typename T>
+__global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restrict__ y, T* __restrict__ dx,
                               long long ld, int rows, int F) {
     pdl_wait();
     pdl_trigger();
@@ -347,7 +396,7 @@ __global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restr
         for (int j = lane; j < F; j += 32) d += dy[o + j] * y[o + j];
         for (int s = 16; s; s >>= 1) d += __shfl_xor_sync(0xffffffffu, d, s);
         for (int j = lane; j < ld; j += 32)
-            dx[r * ld + j] = __float2bfloat16_rn(j < F ? y[o + j] * (dy[o + j] - d) : 0.f);
+            dx[r * ld + j] = from_f<T>(j < F ? y[o + j] * (dy[o + j] - d) : 0.f);
     }
 }
 
@@ -459,8 +508,8 @@ RedPlan red_plan(long long rows, int ld) {
     return r;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restrict__ x, const bf16* __restrict__ x2,
+template <int MODE, typename T>
+__global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const T* __restrict__ x, const T* __restrict__ x2,
                                                              const float* __restrict__ stats, long long rows, int C,
                                                              int ld, int ct, long long rps, int splits,
                                                              float* __restrict__ part) {
@@ -477,7 +526,7 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
     const bool live = tr < rpi && c0 < ld;
     if (live) {
         if (MODE == RED_STATS) {
-            unpack8(*reinterpret_cast<const uint4*>(x + c0), m);
+            ld8(x + c0, m);
         } else if (MODE == RED_BNBWD) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -487,23 +536,23 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
             }
         }
         const long long r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
-        const bf16* px = x + r0 * ld + c0;
-        const bf16* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
+        const T* px = x + r0 * ld + c0;
+        const T* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
         constexpr int U = 4;  // rows in flight per thread
         for (long long rb = tr; r0 + rb < r1; rb += U * rpi) {
-            uint4 q[U], q2[U];
+            Raw8<T> q[U], q2[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const long long r = rb + u * rpi;
                 const bool ok = r0 + r < r1;
-                q[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(px + r * ld)) : make_uint4(0, 0, 0, 0);
-                if (MODE == RED_BNBWD) q2[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(p2 + r * ld)) : make_uint4(0, 0, 0, 0);
+                q[u] = ok ? ld_raw8cs(px + r * ld) : raw8_zero<T>();
+                if (MODE == RED_BNBWD) q2[u] = ok ? ld_raw8cs(p2 + r * ld) : raw8_zero<T>();
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (r0 + rb + u * rpi >= r1) break;
                 float f[8];
-                unpack8(q[u], f);
+                unpack_raw(q[u], f);
                 if (MODE == RED_SUM) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) a[j] += f[j];
@@ -516,7 +565,7 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
                     }
                 } else {
                     float g[8];
-                    unpack8(q2[u], g);
+                    unpack_raw(q2[u], g);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         a[j] += f[j];
@@ -553,9 +602,9 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const bf16* __restr
 
 // Stage 2.  RED_SUM: out[c] = scale * sum.  RED_STATS: stats = (mean, istd), coef =
 // (gamma * istd, beta - mean * gamma * istd).  RED_BNBWD: out = (sum dy, sum dy*xhat).
-template <int MODE>
+template <int MODE, typename T>
 __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ part, int splits, int C, float scale,
-                                                    float* __restrict__ out, const bf16* __restrict__ x, long long rows,
+                                                    float* __restrict__ out, const T* __restrict__ x, long long rows,
                                                     float eps, const float* __restrict__ gamma,
                                                     const float* __restrict__ beta, float* __restrict__ coef) {
     pdl_wait();
@@ -581,7 +630,7 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
     } else if (MODE == RED_STATS) {
         const float inv = 1.f / static_cast<float>(rows);
         const float m1 = sa * inv;
-        const float mean = __bfloat162float(x[c]) + m1;
+        const float mean = to_f(x[c]) + m1;
         const float var = fmaxf(sb * inv - m1 * m1, 0.f);
         const float istd = rsqrtf(var + eps);
         out[c] = mean;
@@ -596,28 +645,29 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
 }
 
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
-__global__ void k_chan_affine(const uint4* __restrict__ x, const float* __restrict__ coef, uint4* __restrict__ y,
+template <typename T>
+__global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__ coef, T* __restrict__ y,
                               long long n8, int ld8, int C, int relu) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
-        uint4 q[2];
+        Raw8<T> q[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) q[u] = i0 + u * S < n8 ? __ldcs(x + i0 + u * S) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 2; ++u) q[u] = i0 + u * S < n8 ? ld_raw8cs(x + (i0 + u * S) * 8) : raw8_zero<T>();
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const long long i = i0 + u * S;
             if (i >= n8) break;
             const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
             float f[8];
-            unpack8(q[u], f);
+            unpack_raw(q[u], f);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
                 if (relu) f[j] = fmaxf(f[j], 0.f);
             }
-            y[i] = pack8(f);
+            st8(y + i * 8, f);
         }
     }
 }
@@ -637,18 +687,19 @@ __global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __re
     k[2 * C + c] = -g * sums[c] * invm + g * t * mean;
 }
 
-__global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ k,
-                               uint4* __restrict__ dx, long long n8, int ld8, int C) {
+template <typename T>
+__global__ void k_bn_bwd_apply(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ k,
+                               T* __restrict__ dx, long long n8, int ld8, int C) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
-        uint4 q[2], r[2];
+        Raw8<T> q[2], r[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const bool ok = i0 + u * S < n8;
-            q[u] = ok ? __ldcs(dy + i0 + u * S) : make_uint4(0, 0, 0, 0);
-            r[u] = ok ? __ldcs(x + i0 + u * S) : make_uint4(0, 0, 0, 0);
+            q[u] = ok ? ld_raw8cs(dy + (i0 + u * S) * 8) : raw8_zero<T>();
+            r[u] = ok ? ld_raw8cs(x + (i0 + u * S) * 8) : raw8_zero<T>();
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -656,19 +707,20 @@ __global__ void k_bn_bwd_apply(const uint4* __restrict__ dy, const uint4* __rest
             if (i >= n8) break;
             const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
             float f[8], g[8];
-            unpack8(q[u], f);
-            unpack8(r[u], g);
+            unpack_raw(q[u], f);
+            unpack_raw(r[u], g);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int c = c0 + j;
                 f[j] = c < C ? fmaf(__ldg(k + c), f[j], fmaf(__ldg(k + C + c), g[j], __ldg(k + 2 * C + c))) : 0.f;
             }
-            dx[i] = pack8(f);
+            st8(dx + i * 8, f);
         }
     }
 }
 
-__global__ void k_bias_add(const bf16* __restrict__ x, const float* __restrict__ b, bf16* __restrict__ y, long long rows,
+template <typename T>
+__global__ void k_bias_add(const T* __restrict__ x, const float* __restrict__ b, T* __restrict__ y, long long rows,
                            int cols, long long ld, int relu) {
     pdl_wait();
     pdl_trigger();
@@ -676,13 +728,14 @@ __global__ void k_bias_add(const bf16* __restrict__ x, const float* __restrict__
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int c = static_cast<int>(i % ld);
-        float v = c < cols ? __bfloat162float(x[i]) + b[c] : 0.f;
+        float v = c < cols ? to_f(x[i]) + b[c] : 0.f;
         if (relu) v = fmaxf(v, 0.f);
-        y[i] = __float2bfloat16_rn(v);
+        y[i] = from_f<T>(v);
     }
 }
 
-__global__ void k_channel_copy(const bf16* __restrict__ src, int src_cs, bf16* __restrict__ dst, int dst_cs, int off,
+template <typename T>
+__global__ void k_channel_copy(const T* __restrict__ src, int src_cs, T* __restrict__ dst, int dst_cs, int off,
                                int c, long long pixels) {
     pdl_wait();
     pdl_trigger();
@@ -734,14 +787,22 @@ __global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int 
 // chunks of the same pixel (L1 hits); n <= 9 so chunks g-1 .. g+1 suffice.
 // v[8..16) = channels g*8..g*8+7 and NEED channels either side (zero beyond the tensor).
 // NEED <= 4 reads the neighbours with 8-byte loads, otherwise whole neighbour chunks.
-template <int NEED>
-__device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, int ng, float (&v)[24]) {
+template <int NEED, typename T>
+__device__ __forceinline__ void load_chunk3(const T* __restrict__ p, int g, int ng, float (&v)[24]) {
     static_assert(NEED <= 8, "LRN window too wide");
     float f[8];
-    unpack8(*reinterpret_cast<const uint4*>(p + g * 8), f);
+    ld8(p + g * 8, f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[8 + j] = f[j];
-    if constexpr (NEED <= 4) {
+    if constexpr (NEED <= 4 && sizeof(T) == 4) {
+        float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+        if (g > 0) lo = *reinterpret_cast<const float4*>(p + g * 8 - 4);
+        if (g + 1 < ng) hi = *reinterpret_cast<const float4*>(p + g * 8 + 8);
+        v[4] = lo.x, v[5] = lo.y, v[6] = lo.z, v[7] = lo.w;
+        v[16] = hi.x, v[17] = hi.y, v[18] = hi.z, v[19] = hi.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = v[20 + j] = 0.f;
+    } else if constexpr (NEED <= 4) {
         uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
         if (g > 0) lo = *reinterpret_cast<const uint2*>(p + g * 8 - 4);
         if (g + 1 < ng) hi = *reinterpret_cast<const uint2*>(p + g * 8 + 8);
@@ -761,8 +822,8 @@ __device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, i
         float lo[8], hi[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) lo[j] = hi[j] = 0.f;
-        if (g > 0) unpack8(*reinterpret_cast<const uint4*>(p + g * 8 - 8), lo);
-        if (g + 1 < ng) unpack8(*reinterpret_cast<const uint4*>(p + g * 8 + 8), hi);
+        if (g > 0) ld8(p + g * 8 - 8, lo);
+        if (g + 1 < ng) ld8(p + g * 8 + 8, hi);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             v[j] = lo[j];
@@ -773,8 +834,8 @@ __device__ __forceinline__ void load_chunk3(const bf16* __restrict__ p, int g, i
 
 // HALF = n/2 is a template parameter so every window loop unrolls and the
 // per-thread channel windows stay in registers.
-template <int HALF>
-__global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act4 a, float alpha, float beta,
+template <int HALF, typename T>
+__global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, float alpha, float beta,
                            float kk) {
     pdl_wait();
     pdl_trigger();
@@ -785,7 +846,7 @@ __global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const bool i32 = total < (1ll << 31);
         const int g = i32 ? static_cast<int>(t) % ng : static_cast<int>(t % ng);
-        const bf16* px = x + (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
+        const T* px = x + (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
         float v[24];
         load_chunk3<HALF>(px, g, ng, v);
         // channels outside [0, C) contribute nothing (pads are zero, neighbours beyond the tensor loaded as 0)
@@ -797,13 +858,13 @@ __global__ void k_lrn2_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, Act
             for (int d = -HALF; d <= HALF; ++d) s += v[8 + j + d] * v[8 + j + d];
             out[j] = (g * 8 + j) < a.C ? v[8 + j] * __powf(kk + an * s, -beta) : 0.f;
         }
-        *reinterpret_cast<uint4*>(y + t * 8) = pack8(out);
+        st8(y + t * 8, out);
     }
 }
 
-template <int HALF>
-__global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ y,
-                           bf16* __restrict__ dx, Act4 a, float alpha, float beta, float kk) {
+template <int HALF, typename T>
+__global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
+                           T* __restrict__ dx, Act4 a, float alpha, float beta, float kk) {
     pdl_wait();
     pdl_trigger();
     const int ng = a.cs / 8;
@@ -828,7 +889,7 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
             for (int d = -HALF; d <= HALF; ++d) s += xv[i + d] * xv[i + d];
             sc[i] = kk + an * s;
             // zero for channels outside [0, C): dy and y are zero there
-            tt[i] = __fdividef(dv[i] * yv[i], sc[i]);  // MUFU reciprocal: output is bf16
+            tt[i] = __fdividef(dv[i] * yv[i], sc[i]);  // MUFU reciprocal (2 ulp)
         }
         float out[8];
 #pragma unroll
@@ -838,7 +899,7 @@ __global__ void k_lrn2_bwd(const bf16* __restrict__ dy, const bf16* __restrict__
             for (int d = -HALF; d <= HALF; ++d) s += tt[8 + j + d];
             out[j] = (g * 8 + j) < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
         }
-        *reinterpret_cast<uint4*>(dx + base + g * 8) = pack8(out);
+        st8(dx + base + g * 8, out);
     }
 }
 
@@ -871,7 +932,8 @@ __device__ __forceinline__ bool stage_src(const StageLayout& L, long long i, int
 // Row-tiled staging: block (n, output row) reads the source rows it needs coalesced into
 // shared memory ([c][row][w] fp32, zero outside the image), then writes the output row as
 // 16-byte chunks.  Output row = image row h (NHWC) or space-to-depth row P (rows s*P - pad + i).
-__global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x, bf16* __restrict__ y, StageLayout L,
+template <typename T>
+__global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x, T* __restrict__ y, StageLayout L,
                                                     int log2_cs, int log2_s) {
     pdl_wait();
     pdl_trigger();
@@ -891,7 +953,7 @@ __global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x,
     const int log2_cc = 2 * log2_s + log2_cs;  // output channels per output pixel = s*s*cs
     const int wout = L.s2d ? L.Ws : L.W;
     const int chunks = (wout << log2_cc) >> 3;
-    uint4* out = reinterpret_cast<uint4*>(y + (static_cast<long long>(n) * rows_out + r) * (static_cast<long long>(wout) << log2_cc));
+    T* out = y + (static_cast<long long>(n) * rows_out + r) * (static_cast<long long>(wout) << log2_cc);
     for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
         const int e0 = q << 3;
         float f[8];
@@ -903,11 +965,12 @@ __global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x,
             const int w = L.s2d ? (Q << log2_s) + jj - L.pad : Q;
             f[j] = (c < C && w >= 0 && w < W) ? tile[((c << log2_s) + i) * W + w] : 0.f;
         }
-        out[q] = pack8(f);
+        st8(out + q * 8, f);
     }
 }
 
-__global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y, StageLayout L) {
+template <typename T>
+__global__ void k_nchw_to_nhwc(const float* __restrict__ x, T* __restrict__ y, StageLayout L) {
     pdl_wait();
     pdl_trigger();
     const long long total = L.elems();
@@ -915,11 +978,12 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, bf16* __restrict__ y
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         int n, c, h, w;
         const bool ok = stage_src(L, i, n, c, h, w);
-        y[i] = __float2bfloat16_rn(ok ? x[((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W + w] : 0.f);
+        y[i] = from_f<T>(ok ? x[((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W + w] : 0.f);
     }
 }
 
-__global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, StageLayout L, int classes, uint64_t seed,
+template <typename T>
+__global__ void k_synth(T* __restrict__ x, int32_t* __restrict__ labels, StageLayout L, int classes, uint64_t seed,
                         uint32_t iter, uint32_t n0) {
     pdl_wait();
     pdl_trigger();
@@ -942,7 +1006,7 @@ __global__ void k_synth(bf16* __restrict__ x, int32_t* __restrict__ labels, Stag
             const double z = (e & 1) ? r * sin(t) : r * cos(t);
             v = static_cast<float>(static_cast<double>(tcp_centroid(seed, y, e)) + 0.1 * z);
         }
-        x[i] = __float2bfloat16_rn(v);
+        x[i] = from_f<T>(v);
     }
 }
 
@@ -958,6 +1022,65 @@ __global__ void k_s2d_mask_grad(float* __restrict__ g, int K, long long ld, int 
         const int ab = col / (s * s * cs), ij = (col / cs) % (s * s);
         const int kh = (ab / Rp) * s + ij / s, kw = (ab % Rp) * s + ij % s;
         if (kh >= R || kw >= S) g[k * ld + col] = 0.f;
+    }
+}
+
+// ---------------------------------------------------------------- fp32 parity mode: bf16 split
+// x = hi + mid + lo (hi = bf16(x), mid = bf16(x - hi), lo = bf16(x - hi - mid): 24-bit
+// mantissa).  A contraction over fp32 operands runs as one bf16 contraction over kSplitN
+// operand copies whose products hi*hi + hi*mid + mid*hi + hi*lo + mid*mid + lo*hi are the
+// terms of the fp32 product down to 2^-24; the copies sit side by side along the contraction
+// index (channels / columns: SPLIT_COLS) or stacked along it (rows / images: SPLIT_ROWS).
+// parts: 2 bits per copy (0 hi, 1 mid, 2 lo).
+__device__ __forceinline__ float split_part(float v, int part) {
+    const float hi = __bfloat162float(__float2bfloat16_rn(v));
+    if (part == 0) return hi;
+    const float mid = __bfloat162float(__float2bfloat16_rn(v - hi));
+    return part == 1 ? mid : v - hi - mid;
+}
+// src [rows_src][ld_src] (L used columns, rows >= rows_src read as 0) ->
+//   SPLIT_COLS: dst [R][n*L]      dst[r][j*L + e]
+//   SPLIT_ROWS: dst [n*R][L]      dst[j*R + r][e]
+__global__ void k_splitn(const float* __restrict__ src, long long rows_src, long long ld_src, bf16* __restrict__ dst,
+                         long long R, int L, int rows_mode, int n, int parts) {
+    pdl_wait();
+    pdl_trigger();
+    const long long total = n * R * L;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        long long r;
+        int j, e;
+        if (rows_mode) {
+            const long long jr = i / L;
+            e = static_cast<int>(i - jr * L);
+            j = static_cast<int>(jr / R);
+            r = jr - static_cast<long long>(j) * R;
+        } else {
+            r = i / (static_cast<long long>(n) * L);
+            const int je = static_cast<int>(i - r * n * L);
+            j = je / L;
+            e = je - j * L;
+        }
+        const float v = r < rows_src ? src[r * ld_src + e] : 0.f;
+        dst[i] = __float2bfloat16_rn(split_part(v, (parts >> (2 * j)) & 3));
+    }
+}
+// conv filter p [K][RS][cs] (row stride ld) -> bwd-data operand [RS][n ks][cs]:
+//   dst[(rs*n*ks + j*ks + k)*cs + c] = part_j(p[k][rs][c])  (k >= K: 0)
+__global__ void k_splitn_rskc(const float* __restrict__ p, long long ld, int K, int RS, int cs, int ks,
+                              bf16* __restrict__ dst, int n, int parts) {
+    pdl_wait();
+    pdl_trigger();
+    const long long total = static_cast<long long>(RS) * n * ks * cs;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % cs);
+        const long long q = i / cs;
+        const int kk = static_cast<int>(q % (n * ks));
+        const int rs = static_cast<int>(q / (n * ks));
+        const int j = kk / ks, k = kk - j * ks;
+        const float v = k < K ? p[k * ld + static_cast<long long>(rs) * cs + c] : 0.f;
+        dst[i] = __float2bfloat16_rn(split_part(v, (parts >> (2 * j)) & 3));
     }
 }
 
@@ -1045,26 +1168,27 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
 // ================================================================ launchers
 #define EW_GRID(n) grid_for((n)), kThreads, 0, st
 
-tc_status launch_relu_fwd(const bf16* x, bf16* y, long long n, cudaStream_t st) {
-    TCB_LAUNCH(k_relu_fwd, EW_GRID(n / 8), reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), n / 8);
+template <typename T>
+tc_status launch_relu_fwd(const T* x, T* y, long long n, cudaStream_t st) {
+    TCB_LAUNCH(k_relu_fwd<T>, EW_GRID(n / 8), x, y, n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, cudaStream_t st) {
-    TCB_LAUNCH(k_relu_bwd, EW_GRID(n / 8), reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y),
-                                    reinterpret_cast<uint4*>(dx), n / 8);
+template <typename T>
+tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStream_t st) {
+    TCB_LAUNCH(k_relu_bwd<T>, EW_GRID(n / 8), dy, y, dx, n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, int relu, cudaStream_t st) {
-    TCB_LAUNCH(k_add, EW_GRID(n / 8), reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
-                               reinterpret_cast<uint4*>(y), n / 8, relu);
+template <typename T>
+tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st) {
+    TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16* y, long long n, cudaStream_t st) {
-    TCB_LAUNCH(k_mask_mul, EW_GRID(n / 8), reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint2*>(keep), scale,
-                                    reinterpret_cast<uint4*>(y), n / 8);
+template <typename T>
+tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st) {
+    TCB_LAUNCH(k_mask_mul<T>, EW_GRID(n / 8), x, reinterpret_cast<const uint2*>(keep), scale, y, n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1075,54 +1199,58 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
-                          int is_max, cudaStream_t st) {
+template <typename T>
+tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
+                          cudaStream_t st) {
     if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
     const long long n = yo.pixels() * (xi.cs / 8);
     if (n < (1ll << 31))
-        TCB_LAUNCH((k_pool_fwd<int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_fwd<T, int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
     else
-        TCB_LAUNCH((k_pool_fwd<long long>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_fwd<T, long long>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
+template <typename T>
+tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st) {
     const long long n = xi.pixels() * (xi.cs / 8);
     if (n < (1ll << 31))
-        TCB_LAUNCH((k_pool_bwd<int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_bwd<T, int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
     else
-        TCB_LAUNCH((k_pool_bwd<long long>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_bwd<T, long long>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
+template <typename T>
+tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
     switch (size) {  // odd windows up to 9: register-resident template kernels
-        case 3: TCB_LAUNCH((k_lrn2_fwd<1>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 5: TCB_LAUNCH((k_lrn2_fwd<2>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 7: TCB_LAUNCH((k_lrn2_fwd<3>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 9: TCB_LAUNCH((k_lrn2_fwd<4>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 3: TCB_LAUNCH((k_lrn2_fwd<1, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 5: TCB_LAUNCH((k_lrn2_fwd<2, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 7: TCB_LAUNCH((k_lrn2_fwd<3, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 9: TCB_LAUNCH((k_lrn2_fwd<4, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
         default: {  // general path: warp per pixel with the channel vector in shared memory
             const int warps = 8;
-            TCB_LAUNCH(k_lrn_fwd, grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st, x, y, a, size,
+            TCB_LAUNCH(k_lrn_fwd<T>, grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st, x, y, a, size,
                                                                                                      alpha, beta, k);
         }
     }
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
-                         float beta, float k, cudaStream_t st) {
+template <typename T>
+tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int size, float alpha, float beta,
+                         float k, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
     switch (size) {
-        case 3: TCB_LAUNCH((k_lrn2_bwd<1>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 5: TCB_LAUNCH((k_lrn2_bwd<2>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 7: TCB_LAUNCH((k_lrn2_bwd<3>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 9: TCB_LAUNCH((k_lrn2_bwd<4>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 3: TCB_LAUNCH((k_lrn2_bwd<1, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 5: TCB_LAUNCH((k_lrn2_bwd<2, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 7: TCB_LAUNCH((k_lrn2_bwd<3, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 9: TCB_LAUNCH((k_lrn2_bwd<4, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
         default: {
             const int warps = 8;
-            TCB_LAUNCH(k_lrn_bwd, grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st, 
+            TCB_LAUNCH(k_lrn_bwd<T>, grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st, 
                 dy, x, y, dx, a, size, alpha, beta, k);
         }
     }
@@ -1136,14 +1264,16 @@ tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pa
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_softmax_fwd(const bf16* x, long long in_ld, float* y, int rows, int F, cudaStream_t st) {
-    TCB_LAUNCH(k_softmax_fwd, grid_for(rows, 8), 256, 0, st, x, in_ld, y, rows, F);
+template <typename T>
+tc_status launch_softmax_fwd(const T* x, long long in_ld, float* y, int rows, int F, cudaStream_t st) {
+    TCB_LAUNCH(k_softmax_fwd<T>, grid_for(rows, 8), 256, 0, st, x, in_ld, y, rows, F);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_softmax_bwd(const float* dy, const float* y, bf16* dx, long long out_ld, int rows, int F,
+template <typename T>
+tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long out_ld, int rows, int F,
                              cudaStream_t st) {
-    TCB_LAUNCH(k_softmax_bwd, grid_for(rows, 8), 256, 0, st, dy, y, dx, out_ld, rows, F);
+    TCB_LAUNCH(k_softmax_bwd<T>, grid_for(rows, 8), 256, 0, st, dy, y, dx, out_ld, rows, F);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1182,40 +1312,44 @@ size_t colsum_partials_floats(int cols) {
     return 2ull * (static_cast<size_t>(num_sms()) * 4 / tiles + 1) * ld + 3ull * ld + 64;
 }
 
-template <int MODE>
-static tc_status chan_reduce(const bf16* x, const bf16* x2, const float* stats, long long rows, int C, long long ld,
+template <int MODE, typename T>
+static tc_status chan_reduce(const T* x, const T* x2, const float* stats, long long rows, int C, long long ld,
                              float* part, int max_partials, cudaStream_t st, RedPlan* out_plan) {
     if ((ld & 7) || (reinterpret_cast<uintptr_t>(x) & 15) || (x2 && (reinterpret_cast<uintptr_t>(x2) & 15)))
         return fail(TC_INVALID_ARG, "channel reduction: misaligned operand");
     RedPlan rp = red_plan(rows, static_cast<int>(ld));
     if (2ll * rp.splits * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
     dim3 grid(rp.tiles, rp.splits);
-    TCB_LAUNCH((k_chan_reduce<MODE>), grid, kRedThreads, 0, st, x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
+    TCB_LAUNCH((k_chan_reduce<MODE, T>), grid, kRedThreads, 0, st, x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
                                                       rp.splits, part);
     TCB_LAUNCH_CHECK();
     *out_plan = rp;
     return TC_OK;
 }
 
-tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, float* out, float* partials,
+template <typename T>
+tc_status launch_colsum(const T* x, long long rows, int cols, long long ld, float* out, float* partials,
                         int max_partials, cudaStream_t st) {
     RedPlan rp;
-    tc_status s = chan_reduce<RED_SUM>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
+    tc_status s = chan_reduce<RED_SUM, T>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_SUM>), (cols + 7) / 8, 256, 0, st, partials, rp.splits, cols, 1.f, out, nullptr, rows, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_SUM, T>), (cols + 7) / 8, 256, 0, st, partials, rp.splits, cols, 1.f, out,
+               static_cast<const T*>(nullptr), rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_bias_add(const bf16* x, const float* b, bf16* y, long long rows, int cols, long long ld, int relu,
+template <typename T>
+tc_status launch_bias_add(const T* x, const float* b, T* y, long long rows, int cols, long long ld, int relu,
                           cudaStream_t st) {
-    TCB_LAUNCH(k_bias_add, EW_GRID(rows * ld), x, b, y, rows, cols, ld, relu);
+    TCB_LAUNCH(k_bias_add<T>, EW_GRID(rows * ld), x, b, y, rows, cols, ld, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs, int off, int c, long long pixels,
+template <typename T>
+tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st) {
-    TCB_LAUNCH(k_channel_copy, EW_GRID(pixels * c), src, src_cs, dst, dst_cs, off, c, pixels);
+    TCB_LAUNCH(k_channel_copy<T>, EW_GRID(pixels * c), src, src_cs, dst, dst_cs, off, c, pixels);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1224,64 +1358,68 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st) {
     return TC_OK;
 }
 
-tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
-                        int C, int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st) {
+template <typename T>
+tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y, float* stats, long long pixels, int C,
+                        int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st) {
     RedPlan rp;
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
-    tc_status s = chan_reduce<RED_STATS>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
+    tc_status s = chan_reduce<RED_STATS, T>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_STATS>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+    TCB_LAUNCH((k_chan_final<RED_STATS, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    TCB_LAUNCH(k_chan_affine, EW_GRID(n8), reinterpret_cast<const uint4*>(x), coef, reinterpret_cast<uint4*>(y), n8, cs / 8, C,
-               relu);
+    TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
-tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats, float* sums, long long pixels, int C,
-                               int cs, float* partials, int max_partials, cudaStream_t st) {
+template <typename T>
+tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* stats, float* sums, long long pixels, int C, int cs,
+                               float* partials, int max_partials, cudaStream_t st) {
     RedPlan rp;
-    tc_status s = chan_reduce<RED_BNBWD>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
+    tc_status s = chan_reduce<RED_BNBWD, T>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_BNBWD>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, sums, nullptr, pixels, 0.f,
+    TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, sums,
+               static_cast<const T*>(nullptr), pixels, 0.f,
                                                               nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
-tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma, const float* stats, const float* sums,
-                              bf16* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+template <typename T>
+tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* gamma, const float* stats, const float* sums,
+                              T* dx, long long pixels, int C, int cs, float* partials, int max_partials,
                               cudaStream_t st) {
     float* k = partials + max_partials;
     TCB_LAUNCH(k_bn_coef_bwd, (C + 255) / 256, 256, 0, st, gamma, stats, sums, k, C, 1.f / static_cast<float>(pixels));
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    TCB_LAUNCH(k_bn_bwd_apply, EW_GRID(n8), reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), k,
-                                     reinterpret_cast<uint4*>(dx), n8, cs / 8, C);
+    TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
-tc_status launch_nchw_to_nhwc(const float* x, bf16* y, StageLayout L, cudaStream_t st) {
+template <typename T>
+tc_status launch_nchw_to_nhwc(const float* x, T* y, StageLayout L, cudaStream_t st) {
     const int s = L.s2d ? L.s2d : 1;
     const size_t smem = static_cast<size_t>(L.C) * s * L.W * sizeof(float);
     const int wout = L.s2d ? L.Ws : L.W;
     auto log2i = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
     const int lcs = log2i(L.cs), ls = log2i(s);
     if (smem <= 48 * 1024 && lcs >= 0 && ls >= 0 && (static_cast<long long>(wout) * s * s * L.cs) % 8 == 0) {
-        TCB_LAUNCH(k_stage_rows, L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
+        TCB_LAUNCH(k_stage_rows<T>, L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
         TCB_LAUNCH_CHECK();
         return TC_OK;
     }
-    TCB_LAUNCH(k_nchw_to_nhwc, EW_GRID(L.elems()), x, y, L);
+    TCB_LAUNCH(k_nchw_to_nhwc<T>, EW_GRID(L.elems()), x, y, L);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_synth_batch(bf16* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
+template <typename T>
+tc_status launch_synth_batch(T* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
                              uint32_t n0, cudaStream_t st) {
-    TCB_LAUNCH(k_synth, EW_GRID(L.elems()), x, labels, L, classes, seed, iter, n0);
+    TCB_LAUNCH(k_synth<T>, EW_GRID(L.elems()), x, labels, L, classes, seed, iter, n0);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1315,5 +1453,63 @@ tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStre
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+
+tc_status launch_split(const float* src, long long rows_src, long long ld_src, bf16* dst, long long R, int L,
+                       int rows_mode, int parts, cudaStream_t st) {
+    TCB_LAUNCH(k_splitn, EW_GRID(kSplitN * R * L), src, rows_src, ld_src, dst, R, L, rows_mode, kSplitN, parts);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+tc_status launch_split_rskc(const float* p, long long ld, int K, int RS, int cs, int ks, bf16* dst, int parts,
+                            cudaStream_t st) {
+    TCB_LAUNCH(k_splitn_rskc, EW_GRID(static_cast<long long>(RS) * kSplitN * ks * cs), p, ld, K, RS, cs, ks, dst, kSplitN,
+               parts);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
+// storage types: bf16 (default) and fp32 (parity precision mode)
+template tc_status launch_relu_fwd<bf16>(const bf16*, bf16*, long long, cudaStream_t);
+template tc_status launch_relu_bwd<bf16>(const bf16*, const bf16*, bf16*, long long, cudaStream_t);
+template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t);
+template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t);
+template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int, cudaStream_t);
+template tc_status launch_lrn_fwd<bf16>(const bf16*, bf16*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_lrn_bwd<bf16>(const bf16*, const bf16*, const bf16*, bf16*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_softmax_fwd<bf16>(const bf16*, long long, float*, int, int, cudaStream_t);
+template tc_status launch_softmax_bwd<bf16>(const float*, const float*, bf16*, long long, int, int, cudaStream_t);
+template tc_status launch_colsum<bf16>(const bf16*, long long, int, long long, float*, float*, int, cudaStream_t);
+template tc_status launch_bias_add<bf16>(const bf16*, const float*, bf16*, long long, int, long long, int, cudaStream_t);
+template tc_status launch_channel_copy<bf16>(const bf16*, int, bf16*, int, int, int, long long, cudaStream_t);
+template tc_status launch_bn_fwd<bf16>(const bf16*, const float*, const float*, bf16*, float*, long long, int, int, float, int,
+                                     float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const float*, float*, long long, int, int, float*, int,
+                                            cudaStream_t);
+template tc_status launch_bn_bwd_apply<bf16>(const bf16*, const bf16*, const float*, const float*, const float*, bf16*, long long,
+                                           int, int, float*, int, cudaStream_t);
+template tc_status launch_nchw_to_nhwc<bf16>(const float*, bf16*, StageLayout, cudaStream_t);
+template tc_status launch_synth_batch<bf16>(bf16*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
+template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaStream_t);
+template tc_status launch_relu_bwd<float>(const float*, const float*, float*, long long, cudaStream_t);
+template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t);
+template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t);
+template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int, cudaStream_t);
+template tc_status launch_lrn_fwd<float>(const float*, float*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_lrn_bwd<float>(const float*, const float*, const float*, float*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_softmax_fwd<float>(const float*, long long, float*, int, int, cudaStream_t);
+template tc_status launch_softmax_bwd<float>(const float*, const float*, float*, long long, int, int, cudaStream_t);
+template tc_status launch_colsum<float>(const float*, long long, int, long long, float*, float*, int, cudaStream_t);
+template tc_status launch_bias_add<float>(const float*, const float*, float*, long long, int, long long, int, cudaStream_t);
+template tc_status launch_channel_copy<float>(const float*, int, float*, int, int, int, long long, cudaStream_t);
+template tc_status launch_bn_fwd<float>(const float*, const float*, const float*, float*, float*, long long, int, int, float, int,
+                                     float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const float*, float*, long long, int, int, float*, int,
+                                            cudaStream_t);
+template tc_status launch_bn_bwd_apply<float>(const float*, const float*, const float*, const float*, const float*, float*, long long,
+                                           int, int, float*, int, cudaStream_t);
+template tc_status launch_nchw_to_nhwc<float>(const float*, float*, StageLayout, cudaStream_t);
+template tc_status launch_synth_batch<float>(float*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 
 }  // namespace tcb

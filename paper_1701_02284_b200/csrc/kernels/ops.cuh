@@ -23,29 +23,41 @@ struct Act4 {  // NHWC activation view
     __host__ __device__ long long elems() const { return pixels() * cs; }
 };
 
-tc_status launch_relu_fwd(const bf16* x, bf16* y, long long n, cudaStream_t st);
-tc_status launch_relu_bwd(const bf16* dy, const bf16* y, bf16* dx, long long n, cudaStream_t st);
+// Activation launchers are templates on the storage type T: bf16 (default) or float (the fp32
+// parity precision mode); both are instantiated in ops.cu.
+template <typename T>
+tc_status launch_relu_fwd(const T* x, T* y, long long n, cudaStream_t st);
+template <typename T>
+tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStream_t st);
 // y = a + b (then max(y, 0) when relu: a residual add followed by an in-place ReLU)
-tc_status launch_add_bf16(const bf16* a, const bf16* b, bf16* y, long long n, int relu, cudaStream_t st);
+template <typename T>
+tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st);
 // y = x * keep * scale (inverted dropout; keep is a 0/1 byte mask)
-tc_status launch_mask_mul(const bf16* x, const uint8_t* keep, float scale, bf16* y, long long n, cudaStream_t st);
+template <typename T>
+tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st);
 // keep[n, e] for every stored element; e = NCHW element index within the sample (tc_philox.h)
 tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st);
 
 // Max pooling argmax: 1 byte per output element, window-local position r*k + s (255 = empty).
-tc_status launch_pool_fwd(const bf16* x, Act4 xi, bf16* y, Act4 yo, uint8_t* idx, int k, int stride, int pad,
+template <typename T>
+tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
+                          cudaStream_t st);
+template <typename T>
+tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, cudaStream_t st);
-tc_status launch_pool_bwd(const bf16* dy, Act4 yo, const uint8_t* idx, bf16* dx, Act4 xi, int k, int stride, int pad,
-                          int is_max, cudaStream_t st);
-tc_status launch_lrn_fwd(const bf16* x, bf16* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st);
-tc_status launch_lrn_bwd(const bf16* dy, const bf16* x, const bf16* y, bf16* dx, Act4 a, int size, float alpha,
-                         float beta, float k, cudaStream_t st);
+template <typename T>
+tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st);
+template <typename T>
+tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int size, float alpha, float beta,
+                         float k, cudaStream_t st);
 
 // rows x F, input bf16 with row stride in_ld -> fp32 out (stride F)
-tc_status launch_softmax_fwd(const bf16* x, long long in_ld, float* y, int rows, int F, cudaStream_t st);
+template <typename T>
+tc_status launch_softmax_fwd(const T* x, long long in_ld, float* y, int rows, int F, cudaStream_t st);
 // dx (bf16, stride out_ld, pad columns zeroed) = y * (dy - sum(dy*y))
-tc_status launch_softmax_bwd(const float* dy, const float* y, bf16* dx, long long out_ld, int rows, int F,
+template <typename T>
+tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long out_ld, int rows, int F,
                              cudaStream_t st);
 
 enum F32Op { F32_LOG = 0, F32_RECIP = 1, F32_SCALE = 2, F32_MUL = 3, F32_ADD = 4 };
@@ -57,14 +69,17 @@ tc_status launch_loss(const float* const* a, const float* const* b, const long l
                       float* out, cudaStream_t st);
 
 // Column sums of a [rows][ld] bf16 matrix over its first `cols` columns -> out[cols] fp32 (deterministic).
-tc_status launch_colsum(const bf16* x, long long rows, int cols, long long ld, float* out, float* partials,
+template <typename T>
+tc_status launch_colsum(const T* x, long long rows, int cols, long long ld, float* out, float* partials,
                         int max_partials, cudaStream_t st);
 size_t colsum_partials_floats(int cols);
-tc_status launch_bias_add(const bf16* x, const float* b, bf16* y, long long rows, int cols, long long ld, int relu,
+template <typename T>
+tc_status launch_bias_add(const T* x, const float* b, T* y, long long rows, int cols, long long ld, int relu,
                           cudaStream_t st);
 
 // Concat: copy `c` channels of src (stride src_cs) into dst channel offset `off` (stride dst_cs).
-tc_status launch_channel_copy(const bf16* src, int src_cs, bf16* dst, int dst_cs, int off, int c, long long pixels,
+template <typename T>
+tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st);
 tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 
@@ -72,13 +87,16 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 // stats = (mean[C], istd[C]); y = gamma * (x - mean) * istd + beta (then max(y, 0) when relu: the
 // in-place ReLU that follows a BN is folded into the apply pass).
 // `partials` holds max_partials floats of reduction scratch plus 3*C coefficient floats.
-tc_status launch_bn_fwd(const bf16* x, const float* gamma, const float* beta, bf16* y, float* stats, long long pixels,
-                        int C, int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st);
+template <typename T>
+tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y, float* stats, long long pixels, int C,
+                        int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st);
 // sums = (sum dy[C], sum dy * xhat[C]) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) and dx
-tc_status launch_bn_bwd_reduce(const bf16* dy, const bf16* x, const float* stats, float* sums, long long pixels, int C,
-                               int cs, float* partials, int max_partials, cudaStream_t st);
-tc_status launch_bn_bwd_apply(const bf16* dy, const bf16* x, const float* gamma, const float* stats, const float* sums,
-                              bf16* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+template <typename T>
+tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* stats, float* sums, long long pixels, int C, int cs,
+                               float* partials, int max_partials, cudaStream_t st);
+template <typename T>
+tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* gamma, const float* stats, const float* sums,
+                              T* dx, long long pixels, int C, int cs, float* partials, int max_partials,
                               cudaStream_t st);
 
 // Dense im2col for small-channel (first-layer) convolutions: col[m][kk], m = (n, oh, ow),
@@ -97,9 +115,11 @@ struct StageLayout {
     }
 };
 // Input staging: NCHW fp32 -> the staged layout (bf16, pads zero).
-tc_status launch_nchw_to_nhwc(const float* x, bf16* y, StageLayout L, cudaStream_t st);
+template <typename T>
+tc_status launch_nchw_to_nhwc(const float* x, T* y, StageLayout L, cudaStream_t st);
 // Synthetic batch generated on the device (identical law to oracle/tc_philox.h).
-tc_status launch_synth_batch(bf16* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
+template <typename T>
+tc_status launch_synth_batch(T* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
                              uint32_t n0, cudaStream_t st);
 // Space-to-depth filter gradient [K][ld]: zero the taps outside the original R x S window
 // (column (a*Rp + b)*s*s*cs + (i*s + j)*cs + c is tap (s*a + i, s*b + j)).
@@ -118,6 +138,22 @@ struct SgdTensor {
     float lr_alpha, momentum, decay;
 };
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaStream_t st);
+
+// fp32 parity mode: bf16 operand splits (see ops.cu).  kSplitN copies per operand; the part
+// (0 hi, 1 mid, 2 lo) of copy j is (parts >> 2j) & 3.  A-side and B-side part lists pair up as
+// hi*hi, hi*mid, mid*hi, hi*lo, mid*mid, lo*hi.
+constexpr int kSplitN = 6;
+enum { SPLIT_COLS = 0, SPLIT_ROWS = 1, SPLIT_A = 0x910, SPLIT_B = 0x184 };
+tc_status launch_split(const float* src, long long rows_src, long long ld_src, bf16* dst, long long R, int L,
+                       int rows_mode, int parts, cudaStream_t st);
+tc_status launch_split_rskc(const float* p, long long ld, int K, int RS, int cs, int ks, bf16* dst, int parts,
+                            cudaStream_t st);
+
+// Convolv fprop / bwd-data with an fp32 output (y_f32 / dx_f32 = 1) — gemm.cu
+tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
+                      int y_f32, void* ws, size_t ws_bytes, void* stream);
+tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
+                           size_t ws_bytes, void* stream);
 
 // d_iter[0] = iter, d_iter[1] = n0 (kernel arguments travel with the launch: no host sync)
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st);

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -125,7 +126,7 @@ struct tc_ctx {
     size_t ws_bytes = 0;
     float* partials = nullptr;
     int max_partials = 0;
-    bf16* d_input = nullptr;
+    void* d_input = nullptr;  // staged input batch (bf16, or fp32 in TC_PREC_F32)
     int32_t* d_labels = nullptr;
     // Input pipeline: host batches are copied (NCHW fp32 + labels) into one of two
     // device staging slots on copy_st, overlapping the running step; the next step
@@ -141,6 +142,9 @@ struct tc_ctx {
     float* h_loss = nullptr;     // pinned
     int input_cs = 8;
     StageLayout in_layout{};  // staged input image layout (space-to-depth when in_layout.s2d > 0)
+    bool f32 = false;         // TC_PREC_F32: fp32 activations, 3 x bf16 split contractions
+    uint8_t* split_buf = nullptr;  // split operand copies of the current contraction (f32 mode)
+    size_t split_bytes = 0;
     size_t input_bytes = 0;
 
     // gradient buckets (backward production order); all-reduce + fused momentum
@@ -236,6 +240,8 @@ tc_status analyze_layouts(tc_ctx* c) {
                 break;
             default: break;
         }
+        const bool head = dt == DT_F32;  // loss-head tensors: fp32 [N][F] in both precisions
+        if (c->f32 && dt == DT_BF16) dt = DT_F32;
         v.dtype = dt;
         if (v.rank == 4) {
             v.nhwc = true;
@@ -244,11 +250,11 @@ tc_status analyze_layouts(tc_ctx* c) {
             v.H = static_cast<int>(v.d[2]);
             v.W = static_cast<int>(v.d[3]);
             // the input image of <= 4 channels is staged with channel stride 4 (8-byte taps)
-            v.cs = (s.op == TC_OP_LOAD_X && v.C <= 4) ? 4 : ceil8(v.C);
+            v.cs = (s.op == TC_OP_LOAD_X && v.C <= 4 && !c->f32) ? 4 : ceil8(v.C);
         } else if (v.rank == 2) {
             v.N = static_cast<int>(v.d[0]);
             v.C = static_cast<int>(v.d[1]);
-            v.cs = dt == DT_F32 ? v.C : ceil8(v.C);
+            v.cs = head ? v.C : ceil8(v.C);
             if (s.op == TC_OP_MATMUL_BWD_DATA && s.in[1].kind == TC_REF_PARAM) {
                 // gradient of a flattened 4-D activation keeps that activation's NHWC layout
                 auto it = fc_input_of_param.find(s.in[1].index);
@@ -296,7 +302,7 @@ tc_status analyze_layouts(tc_ctx* c) {
             }
         }
         const char* e = std::getenv("TCB_S2D");
-        const bool allowed = !(e && e[0] == '0');
+        const bool allowed = !(e && e[0] == '0') && !c->f32;
         if (allowed && xv >= 0 && uses == 1 && other == 0) {
             const tc_stmt& s = p->stmts[fwd];
             const VarL& x = c->vars.at(xv);
@@ -671,7 +677,72 @@ tc_status run_gemm_args(tc_ctx* c, tc_gemm_args& a) {
     return tc_gemm_bf16(&a, c->st);
 }
 
+// ---- fp32 precision mode: every contraction as one bf16 contraction over kSplitN bf16
+// operand copies (hi / mid / lo parts pairing to the fp32 product down to 2^-24), laid side
+// by side along channels / columns or stacked along images / rows (ops.cuh launch_split).
+// Same tcgen05 kernels, fp32 outputs.
+inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+
+tc_conv_desc split_desc(const tc_conv_desc& d0, int which) {
+    tc_conv_desc d = d0;
+    if (which == 0) {  // fprop: input channels x3
+        d.cs = d.C = kSplitN * d0.cs;
+        d.wld = d0.R * d0.S * d.cs;
+    } else if (which == 1) {  // bwd-data: output-gradient channels x3
+        d.ks = kSplitN * d0.ks;
+    } else {  // bwd-filter: images x3
+        d.N = kSplitN * d0.N;
+    }
+    return d;
+}
+
+// bytes of the split operand copies of a contraction (A' then B', 256-aligned)
+size_t split_need(const tc_conv_desc& d0, int which, const ParamL& w) {
+    const size_t pin = static_cast<size_t>(d0.N) * d0.H * d0.W, pout = static_cast<size_t>(d0.N) * d0.Ho * d0.Wo;
+    const size_t rs = static_cast<size_t>(d0.R) * d0.S;
+    if (which == 0) return al256(pin * kSplitN * d0.cs * 2) + al256(static_cast<size_t>(w.K) * rs * kSplitN * d0.cs * 2);
+    if (which == 1) return al256(pout * kSplitN * d0.ks * 2) + al256(rs * kSplitN * d0.ks * d0.cs * 2);
+    return al256(kSplitN * pout * d0.ks * 2) + al256(kSplitN * pin * d0.cs * 2);
+}
+
+// which: 0 fprop (act = x; aux = bias), 1 bwd-data (act = dy), 2 bwd-filter (act = dy; aux = x)
+tc_status split_conv(tc_ctx* c, int which, const tc_conv_desc& d0, const ParamL& w, const float* act, const float* aux,
+                     int relu, float* out) {
+    bf16* A = reinterpret_cast<bf16*>(c->split_buf);
+    const size_t pin = static_cast<size_t>(d0.N) * d0.H * d0.W, pout = static_cast<size_t>(d0.N) * d0.Ho * d0.Wo;
+    const int RS = d0.R * d0.S;
+    const tc_conv_desc d = split_desc(d0, which);
+    tc_status r;
+    if (which == 0) {  // act = x [pin][cs]; weights p [K][RS][cs]
+        bf16* B = A + al256(pin * kSplitN * d0.cs * 2) / 2;
+        r = launch_split(act, pin, d0.cs, A, pin, d0.cs, SPLIT_COLS, SPLIT_A, c->st);
+        if (r == TC_OK) r = launch_split(w.p, static_cast<long long>(w.K) * RS, d0.cs, B, static_cast<long long>(w.K) * RS,
+                                          d0.cs, SPLIT_COLS, SPLIT_B, c->st);
+        if (r == TC_OK) r = conv_fwd_ex(&d, A, B, aux, relu, out, 1, c->ws, c->ws_bytes, c->st);
+    } else if (which == 1) {  // act = dy [pout][ks]
+        bf16* B = A + al256(pout * kSplitN * d0.ks * 2) / 2;
+        r = launch_split(act, pout, d0.ks, A, pout, d0.ks, SPLIT_COLS, SPLIT_A, c->st);
+        if (r == TC_OK) r = launch_split_rskc(w.p, w.Kw, w.K, RS, d0.cs, d0.ks, B, SPLIT_B, c->st);
+        if (r == TC_OK) r = conv_bwd_data_ex(&d, A, B, out, 1, c->ws, c->ws_bytes, c->st);
+    } else {  // act = dy [pout][ks], aux = x [pin][cs]
+        bf16* B = A + al256(kSplitN * pout * d0.ks * 2) / 2;
+        r = launch_split(act, pout, d0.ks, A, pout, d0.ks, SPLIT_ROWS, SPLIT_A, c->st);
+        if (r == TC_OK) r = launch_split(aux, pin, d0.cs, B, pin, d0.cs, SPLIT_ROWS, SPLIT_B, c->st);
+        if (r == TC_OK) r = tc_conv2d_bwd_filter(&d, A, B, out, c->ws, c->ws_bytes, c->st);
+    }
+    return r;
+}
+
+// FC forms: 0 fwd  Y[M][N] = A[M][K] W[N][K]^T;  1 bwd-data  dX = dY[M][Kd] W[Kd][N] (W rows Kr <= Kd);
+//           2 bwd-W  dW[Nout][N] = dY^T (rows = batch)
+size_t split_fc_need(int form, int M, int N, int K) {
+    if (form == 0) return al256(static_cast<size_t>(M) * kSplitN * K * 2) + al256(static_cast<size_t>(N) * kSplitN * K * 2);
+    if (form == 1) return al256(static_cast<size_t>(M) * kSplitN * K * 2) + al256(static_cast<size_t>(kSplitN) * K * N * 2);
+    return al256(static_cast<size_t>(kSplitN) * K * M * 2) + al256(static_cast<size_t>(kSplitN) * K * N * 2);
+}
+
 // (sum dy, sum dy*xhat) of the BN group of BN_BWD_* statement i; reduced at the group's first statement.
+template <typename T>
 tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
     auto it = c->stmt_bn_group.find(i);
     if (it == c->stmt_bn_group.end()) return fail(TC_INTERNAL, "runtime: BN backward statement without a group");
@@ -680,8 +751,8 @@ tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
         Ptrs P{c};
         const VarL& x = c->vars.at(gr.x_var);
         const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
-        tc_status r = launch_bn_bwd_reduce(reinterpret_cast<const bf16*>(P.var(gr.up_var)),
-                                           reinterpret_cast<const bf16*>(P.var(x.id)), stats, gr.sums,
+        tc_status r = launch_bn_bwd_reduce(reinterpret_cast<const T*>(P.var(gr.up_var)),
+                                           reinterpret_cast<const T*>(P.var(x.id)), stats, gr.sums,
                                            static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, c->partials,
                                            c->max_partials, c->st);
         if (r != TC_OK) return r;
@@ -691,6 +762,7 @@ tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
 }
 
 // Gradient op of an Update (or a parameter-shaped Let) into `g` (device param layout).
+template <typename T>
 tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
     const tc_stmt& s = c->plan->stmts[idx];
     Ptrs P{c};
@@ -701,6 +773,9 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
             const VarL& dy = P.L(s.in[0]);
             const VarL& x = P.L(s.in[1]);
             tc_conv_desc d = conv_desc(x, q, dy, s);
+            if constexpr (std::is_same_v<T, float>)
+                return split_conv(c, 2, d, q, static_cast<const float*>(P.var(dy.id)), static_cast<const float*>(P.var(x.id)),
+                                  0, g);
             tc_status r = tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
             if (r != TC_OK || !q.s2d) return r;
             return launch_s2d_mask_grad(g, q.K, q.Kw, q.Rp, q.s2d, q.cs, q.R, q.S, st);
@@ -708,7 +783,7 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
         case TC_OP_BN_BWD_BETA:
         case TC_OP_BN_BWD_GAMMA: {
             const float* sums = nullptr;
-            tc_status r = bn_group_sums(c, idx, &sums);
+            tc_status r = bn_group_sums<T>(c, idx, &sums);
             if (r != TC_OK) return r;
             TCB_CUDA_CHECK(cudaMemcpyAsync(g, sums + (s.op == TC_OP_BN_BWD_GAMMA ? q.K : 0), q.K * sizeof(float),
                                            cudaMemcpyDeviceToDevice, st));
@@ -717,13 +792,37 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
         case TC_OP_CONV_BWD_BIAS:
         case TC_OP_BIAS_GRAD: {
             const VarL& up = P.L(s.in[0]);
-            return launch_colsum(reinterpret_cast<const bf16*>(P.var(up.id)), static_cast<long long>(up.N) * up.H * up.W,
+            return launch_colsum(reinterpret_cast<const T*>(P.var(up.id)), static_cast<long long>(up.N) * up.H * up.W,
                                  q.K, up.cs, g, c->partials, c->max_partials, st);
         }
         case TC_OP_MATMUL_BWD_W: {
             const VarL& up = P.L(s.in[0]);
             const VarL& a = P.L(s.in[1]);
             tc_gemm_args ga{};
+            if constexpr (std::is_same_v<T, float>) {  // K = batch: copies stacked along the rows
+                bf16* As = reinterpret_cast<bf16*>(c->split_buf);
+                bf16* Bs = As + al256(static_cast<size_t>(kSplitN) * up.N * up.cs * 2) / 2;
+                tc_status r = launch_split(static_cast<const float*>(P.var(up.id)), up.N, up.cs, As, up.N, up.cs,
+                                            SPLIT_ROWS, SPLIT_A, st);
+                if (r == TC_OK)
+                    r = launch_split(static_cast<const float*>(P.var(a.id)), up.N, q.in_dev, Bs, up.N, q.in_dev, SPLIT_ROWS,
+                                      SPLIT_B, st);
+                if (r != TC_OK) return r;
+                ga.M = q.K;
+                ga.N = q.in_dev;
+                ga.K = kSplitN * up.N;
+                ga.a_layout = TC_LAYOUT_MN;
+                ga.A = As;
+                ga.lda = up.cs;
+                ga.b_layout = TC_LAYOUT_MN;
+                ga.B = Bs;
+                ga.ldb = q.in_dev;
+                ga.D = g;
+                ga.ldd = q.in_dev;
+                ga.d_dtype = TC_DTYPE_F32;
+                ga.alpha = 1.f;
+                return run_gemm_args(c, ga);
+            }
             ga.M = q.K;
             ga.N = q.in_dev;
             ga.K = up.N;
@@ -744,6 +843,7 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
     return fail(TC_INTERNAL, "runtime: unsupported parameter-gradient op " + std::to_string(s.op));
 }
 
+template <typename T>
 tc_status exec_let(tc_ctx* c, int i) {
     const tc_stmt& s = c->plan->stmts[i];
     Ptrs P{c};
@@ -758,18 +858,23 @@ tc_status exec_let(tc_ctx* c, int i) {
             const ParamL& w = c->params[s.in[1].index];
             const float* bias = s.nin > 2 ? c->params[s.in[2].index].p : nullptr;
             tc_conv_desc d = conv_desc(x, w, out, s);
+            if constexpr (std::is_same_v<T, float>)
+                return split_conv(c, 0, d, w, static_cast<const float*>(P.var(x.id)), bias, c->fuse_relu[i],
+                                  static_cast<float*>(y));
             return tc_conv2d_fwd(&d, P.var(x.id), w.shadow, bias, c->fuse_relu[i], y, c->ws, c->ws_bytes, st);
         }
         case TC_OP_CONV_BWD_DATA: {
             const VarL& dy = P.L(s.in[0]);
             const ParamL& w = c->params[s.in[1].index];
             tc_conv_desc d = conv_desc(out, w, dy, s);
+            if constexpr (std::is_same_v<T, float>)
+                return split_conv(c, 1, d, w, static_cast<const float*>(P.var(dy.id)), nullptr, 0, static_cast<float*>(y));
             return tc_conv2d_bwd_data(&d, P.var(dy.id), w.rskc, y, c->ws, c->ws_bytes, st);
         }
         case TC_OP_POOL_FWD: {
             const VarL& x = P.L(s.in[0]);
             uint8_t* idx = s.max_pool ? reinterpret_cast<uint8_t*>(c->arena + c->items[c->pool_idx_item.at(s.var)].off) : nullptr;
-            return launch_pool_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), x.act(), reinterpret_cast<bf16*>(y),
+            return launch_pool_fwd(reinterpret_cast<const T*>(P.var(x.id)), x.act(), reinterpret_cast<T*>(y),
                                    out.act(), idx, s.k, s.stride, s.pad, s.max_pool, st);
         }
         case TC_OP_POOL_BWD: {
@@ -778,33 +883,33 @@ tc_status exec_let(tc_ctx* c, int i) {
             const uint8_t* idx = s.max_pool ? reinterpret_cast<uint8_t*>(c->arena + c->items[c->pool_idx_item.at(fy.id)].off)
                                             : nullptr;
             Act4 ya = fy.act();
-            return launch_pool_bwd(reinterpret_cast<const bf16*>(P.var(up.id)), ya, idx, reinterpret_cast<bf16*>(y),
+            return launch_pool_bwd(reinterpret_cast<const T*>(P.var(up.id)), ya, idx, reinterpret_cast<T*>(y),
                                    out.act(), s.k, s.stride, s.pad, s.max_pool, st);
         }
         case TC_OP_RELU_FWD:
-            return launch_relu_fwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)), reinterpret_cast<bf16*>(y),
+            return launch_relu_fwd(reinterpret_cast<const T*>(P.var(s.in[0].index)), reinterpret_cast<T*>(y),
                                    out.elems(), st);
         case TC_OP_RELU_BWD:
-            return launch_relu_bwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
-                                   reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+            return launch_relu_bwd(reinterpret_cast<const T*>(P.var(s.in[0].index)),
+                                   reinterpret_cast<const T*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
                                    out.elems(), st);
         case TC_OP_SOFTMAX_FWD: {
             const VarL& x = P.L(s.in[0]);
-            return launch_softmax_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), x.cs, reinterpret_cast<float*>(y), out.N,
+            return launch_softmax_fwd(reinterpret_cast<const T*>(P.var(x.id)), x.cs, reinterpret_cast<float*>(y), out.N,
                                       out.C, st);
         }
         case TC_OP_SOFTMAX_BWD:
             return launch_softmax_bwd(reinterpret_cast<const float*>(P.var(s.in[0].index)),
-                                      reinterpret_cast<const float*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+                                      reinterpret_cast<const float*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
                                       out.cs, out.N, out.C, st);
         case TC_OP_LRN_FWD:
-            return launch_lrn_fwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)), reinterpret_cast<bf16*>(y), out.act(),
+            return launch_lrn_fwd(reinterpret_cast<const T*>(P.var(s.in[0].index)), reinterpret_cast<T*>(y), out.act(),
                                   s.lrn_size, static_cast<float>(s.alpha), static_cast<float>(s.beta),
                                   static_cast<float>(s.lrn_k), st);
         case TC_OP_LRN_BWD:
-            return launch_lrn_bwd(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
-                                  reinterpret_cast<const bf16*>(P.var(s.in[2].index)),
-                                  reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+            return launch_lrn_bwd(reinterpret_cast<const T*>(P.var(s.in[0].index)),
+                                  reinterpret_cast<const T*>(P.var(s.in[2].index)),
+                                  reinterpret_cast<const T*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
                                   out.act(), s.lrn_size, static_cast<float>(s.alpha), static_cast<float>(s.beta),
                                   static_cast<float>(s.lrn_k), st);
         case TC_OP_DROPOUT_MASK:
@@ -814,24 +919,25 @@ tc_status exec_let(tc_ctx* c, int i) {
         case TC_OP_MUL: {
             const VarL& a = P.L(s.in[0]);
             const VarL& b = P.L(s.in[1]);
-            if (out.dtype == DT_F32)
+            if (out.dtype == DT_F32 && a.dtype != DT_U8 && b.dtype != DT_U8)  // loss-head product
                 return launch_f32_ew(F32_MUL, reinterpret_cast<const float*>(P.var(a.id)),
                                      reinterpret_cast<const float*>(P.var(b.id)), 1.f, reinterpret_cast<float*>(y),
                                      out.elems(), st);
             const VarL& m = b.dtype == DT_U8 ? b : a;
             const VarL& x = b.dtype == DT_U8 ? a : b;
-            if (m.dtype != DT_U8) return fail(TC_INTERNAL, "runtime: bf16 x bf16 MUL is not in the op set");
+            if (m.dtype != DT_U8) return fail(TC_INTERNAL, "runtime: activation x activation MUL is not in the op set");
             const float rate = c->mask_rate.at(m.id);
-            return launch_mask_mul(reinterpret_cast<const bf16*>(P.var(x.id)), reinterpret_cast<const uint8_t*>(P.var(m.id)),
-                                   1.f / (1.f - rate), reinterpret_cast<bf16*>(y), out.elems(), st);
+            return launch_mask_mul(reinterpret_cast<const T*>(P.var(x.id)), reinterpret_cast<const uint8_t*>(P.var(m.id)),
+                                   1.f / (1.f - rate), reinterpret_cast<T*>(y), out.elems(), st);
         }
         case TC_OP_ADD:
-            if (out.dtype == DT_F32)
+            // loss-head sums (fp32, unpadded rows) take the scalar kernel; activations the vector one
+            if (out.dtype == DT_F32 && (!std::is_same_v<T, float> || out.cs % 8))
                 return launch_f32_ew(F32_ADD, reinterpret_cast<const float*>(P.var(s.in[0].index)),
                                      reinterpret_cast<const float*>(P.var(s.in[1].index)), 1.f, reinterpret_cast<float*>(y),
                                      out.elems(), st);
-            return launch_add_bf16(reinterpret_cast<const bf16*>(P.var(s.in[0].index)),
-                                   reinterpret_cast<const bf16*>(P.var(s.in[1].index)), reinterpret_cast<bf16*>(y),
+            return launch_add(reinterpret_cast<const T*>(P.var(s.in[0].index)),
+                                   reinterpret_cast<const T*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
                                    out.elems(), c->fuse_relu[i], st);
         case TC_OP_SCALE:
         case TC_OP_LOG:
@@ -845,6 +951,33 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& a = P.L(s.in[0]);
             const ParamL& w = c->params[s.in[1].index];
             tc_gemm_args ga{};
+            if constexpr (std::is_same_v<T, float>) {  // copies side by side along K
+                bf16* As = reinterpret_cast<bf16*>(c->split_buf);
+                bf16* Bs = As + al256(static_cast<size_t>(a.N) * kSplitN * w.in_dev * 2) / 2;
+                tc_status r = launch_split(static_cast<const float*>(P.var(a.id)), a.N, w.in_dev, As, a.N, w.in_dev,
+                                            SPLIT_COLS, SPLIT_A, st);
+                if (r == TC_OK)
+                    r = launch_split(w.p, out.C, w.in_dev, Bs, out.C, w.in_dev, SPLIT_COLS, SPLIT_B, st);
+                if (r != TC_OK) return r;
+                ga.M = a.N;
+                ga.N = out.cs;
+                ga.K = kSplitN * w.in_dev;
+                ga.a_layout = TC_LAYOUT_K;
+                ga.A = As;
+                ga.lda = kSplitN * w.in_dev;
+                ga.b_layout = TC_LAYOUT_K;
+                ga.B = Bs;
+                ga.ldb = kSplitN * w.in_dev;
+                ga.D = y;
+                ga.ldd = out.cs;
+                ga.d_dtype = TC_DTYPE_F32;
+                ga.bias = c->fuse_bias[i] ? c->params[c->fuse_bias_param[i]].p : nullptr;
+                ga.bias_n = out.C;
+                ga.b_rows = out.C;
+                ga.relu = c->fuse_relu[i];
+                ga.alpha = 1.f;
+                return run_gemm_args(c, ga);
+            }
             ga.M = a.N;
             ga.N = out.cs;  // padded columns come out as zeros (zero weight rows, masked bias)
             ga.K = w.in_dev;
@@ -868,6 +1001,29 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& up = P.L(s.in[0]);
             const ParamL& w = c->params[s.in[1].index];
             tc_gemm_args ga{};
+            if constexpr (std::is_same_v<T, float>) {  // K = up.cs: A copies side by side, W copies stacked
+                bf16* As = reinterpret_cast<bf16*>(c->split_buf);
+                bf16* Bs = As + al256(static_cast<size_t>(up.N) * kSplitN * up.cs * 2) / 2;
+                tc_status r = launch_split(static_cast<const float*>(P.var(up.id)), up.N, up.cs, As, up.N, up.cs,
+                                            SPLIT_COLS, SPLIT_A, st);
+                if (r == TC_OK)
+                    r = launch_split(w.p, w.K, w.in_dev, Bs, up.cs, w.in_dev, SPLIT_ROWS, SPLIT_B, st);
+                if (r != TC_OK) return r;
+                ga.M = up.N;
+                ga.N = w.in_dev;
+                ga.K = kSplitN * up.cs;
+                ga.a_layout = TC_LAYOUT_K;
+                ga.A = As;
+                ga.lda = kSplitN * up.cs;
+                ga.b_layout = TC_LAYOUT_MN;
+                ga.B = Bs;
+                ga.ldb = w.in_dev;
+                ga.D = y;
+                ga.ldd = w.in_dev;
+                ga.d_dtype = TC_DTYPE_F32;
+                ga.alpha = 1.f;
+                return run_gemm_args(c, ga);
+            }
             ga.M = up.N;
             ga.N = w.in_dev;
             ga.K = w.K;
@@ -885,8 +1041,8 @@ tc_status exec_let(tc_ctx* c, int i) {
         }
         case TC_OP_BIAS_ADD: {
             const VarL& x = P.L(s.in[0]);
-            return launch_bias_add(reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[1].index].p,
-                                   reinterpret_cast<bf16*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, 0, st);
+            return launch_bias_add(reinterpret_cast<const T*>(P.var(x.id)), c->params[s.in[1].index].p,
+                                   reinterpret_cast<T*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, 0, st);
         }
         case TC_OP_CONCAT: {
             if (out.cs != out.C) {
@@ -896,8 +1052,8 @@ tc_status exec_let(tc_ctx* c, int i) {
             int off = 0;
             for (int k = 0; k < s.nin; ++k) {
                 const VarL& part = P.L(s.in[k]);
-                tc_status r = launch_channel_copy(reinterpret_cast<const bf16*>(P.var(part.id)), part.cs,
-                                                  reinterpret_cast<bf16*>(y), out.cs, off, part.C,
+                tc_status r = launch_channel_copy(reinterpret_cast<const T*>(P.var(part.id)), part.cs,
+                                                  reinterpret_cast<T*>(y), out.cs, off, part.C,
                                                   static_cast<long long>(out.N) * out.H * out.W, st);
                 if (r != TC_OK) return r;
                 off += part.C;
@@ -910,15 +1066,15 @@ tc_status exec_let(tc_ctx* c, int i) {
                 tc_status r = launch_zero(y, out.bytes(), st);
                 if (r != TC_OK) return r;
             }
-            return launch_channel_copy(reinterpret_cast<const bf16*>(P.var(up.id)) + s.offset, up.cs,
-                                       reinterpret_cast<bf16*>(y), out.cs, 0, static_cast<int>(s.extent),
+            return launch_channel_copy(reinterpret_cast<const T*>(P.var(up.id)) + s.offset, up.cs,
+                                       reinterpret_cast<T*>(y), out.cs, 0, static_cast<int>(s.extent),
                                        static_cast<long long>(out.N) * out.H * out.W, st);
         }
         case TC_OP_BN_FWD: {
             const VarL& x = P.L(s.in[0]);
             float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
-            return launch_bn_fwd(reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[1].index].p,
-                                 c->params[s.in[2].index].p, reinterpret_cast<bf16*>(y), stats,
+            return launch_bn_fwd(reinterpret_cast<const T*>(P.var(x.id)), c->params[s.in[1].index].p,
+                                 c->params[s.in[2].index].p, reinterpret_cast<T*>(y), stats,
                                  static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, static_cast<float>(s.eps),
                                  c->fuse_relu[i], c->partials, c->max_partials, st);
         }
@@ -927,11 +1083,11 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& x = P.L(s.in[1]);
             const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
             const float* sums = nullptr;
-            tc_status r = bn_group_sums(c, i, &sums);
+            tc_status r = bn_group_sums<T>(c, i, &sums);
             if (r != TC_OK) return r;
-            return launch_bn_bwd_apply(reinterpret_cast<const bf16*>(P.var(up.id)),
-                                       reinterpret_cast<const bf16*>(P.var(x.id)), c->params[s.in[2].index].p, stats,
-                                       sums, reinterpret_cast<bf16*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C,
+            return launch_bn_bwd_apply(reinterpret_cast<const T*>(P.var(up.id)),
+                                       reinterpret_cast<const T*>(P.var(x.id)), c->params[s.in[2].index].p, stats,
+                                       sums, reinterpret_cast<T*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C,
                                        x.cs, c->partials, c->max_partials, st);
         }
         default: break;
@@ -942,7 +1098,7 @@ tc_status exec_let(tc_ctx* c, int i) {
 tc_status exec_stmt(tc_ctx* c, int i) {
     const tc_stmt& s = c->plan->stmts[i];
     if (s.kind == TC_STMT_DEALLOC) return TC_OK;  // static arena: lifetimes were resolved at plan load
-    if (s.kind == TC_STMT_LET) return c->fused[i] ? TC_OK : exec_let(c, i);
+    if (s.kind == TC_STMT_LET) return c->fused[i] ? TC_OK : c->f32 ? exec_let<float>(c, i) : exec_let<bf16>(c, i);
     if (s.kind == TC_STMT_PRINT) {
         Ptrs P{c};
         const float* a[4];
@@ -959,7 +1115,7 @@ tc_status exec_stmt(tc_ctx* c, int i) {
     }
     // Update: the gradient only; all-reduce + momentum SGD run per bucket (flush_bucket)
     ParamL& q = c->params[s.param];
-    return compute_param_grad(c, i, s.param, q.g);
+    return c->f32 ? compute_param_grad<float>(c, i, s.param, q.g) : compute_param_grad<bf16>(c, i, s.param, q.g);
 }
 
 SgdTensor sgd_tensor(tc_ctx* c, int pidx) {
@@ -1021,49 +1177,64 @@ tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
     return TC_OK;
 }
 
-size_t workspace_need(tc_ctx* c) {
-    size_t need = 0;
+// Largest split-K workspace over the plan's contractions (and, in TC_PREC_F32, the largest
+// split-operand buffer, returned through *split).
+size_t workspace_need(tc_ctx* c, size_t* split) {
+    size_t need = 0, sp = 0;
     const tc_plan* p = c->plan;
     Ptrs P{c};
+    auto conv = [&](tc_conv_desc d, int which, const ParamL& w) {
+        if (c->f32) {
+            sp = std::max(sp, split_need(d, which, w));
+            d = split_desc(d, which);
+        }
+        need = std::max(need, tc_conv2d_workspace_bytes(&d, which));
+    };
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET && s.kind != TC_STMT_UPDATE) continue;
         switch (s.op) {
             case TC_OP_CONV_FWD: {
-                const VarL& x = P.L(s.in[0]);
-                tc_conv_desc d = conv_desc(x, c->params[s.in[1].index], c->vars.at(s.var), s);
-                need = std::max(need, tc_conv2d_workspace_bytes(&d, 0));
+                const ParamL& w = c->params[s.in[1].index];
+                conv(conv_desc(P.L(s.in[0]), w, c->vars.at(s.var), s), 0, w);
                 break;
             }
             case TC_OP_CONV_BWD_DATA: {
-                tc_conv_desc d = conv_desc(c->vars.at(s.var), c->params[s.in[1].index], P.L(s.in[0]), s);
-                need = std::max(need, tc_conv2d_workspace_bytes(&d, 1));
+                const ParamL& w = c->params[s.in[1].index];
+                conv(conv_desc(c->vars.at(s.var), w, P.L(s.in[0]), s), 1, w);
                 break;
             }
             case TC_OP_CONV_BWD_FILTER: {
-                tc_conv_desc d = conv_desc(P.L(s.in[1]), c->params[s.param], P.L(s.in[0]), s);
-                need = std::max(need, tc_conv2d_workspace_bytes(&d, 2));
+                const ParamL& w = c->params[s.param];
+                conv(conv_desc(P.L(s.in[1]), w, P.L(s.in[0]), s), 2, w);
                 break;
             }
             case TC_OP_MATMUL_FWD:
             case TC_OP_MATMUL_BWD_DATA:
             case TC_OP_MATMUL_BWD_W: {
                 tc_gemm_args ga{};
+                ga.d_dtype = c->f32 ? TC_DTYPE_F32 : TC_DTYPE_BF16;
                 if (s.op == TC_OP_MATMUL_FWD) {
                     const ParamL& w = c->params[s.in[1].index];
                     ga.M = P.L(s.in[0]).N;
                     ga.N = c->vars.at(s.var).cs;
-                    ga.K = w.in_dev;
+                    ga.K = c->f32 ? kSplitN * w.in_dev : w.in_dev;
+                    if (c->f32) sp = std::max(sp, split_fc_need(0, ga.M, ga.N, w.in_dev));
                 } else if (s.op == TC_OP_MATMUL_BWD_DATA) {
                     const ParamL& w = c->params[s.in[1].index];
-                    ga.M = P.L(s.in[0]).N;
+                    const VarL& up = P.L(s.in[0]);
+                    ga.M = up.N;
                     ga.N = w.in_dev;
-                    ga.K = w.K;
+                    ga.K = c->f32 ? kSplitN * up.cs : w.K;
+                    if (c->f32) sp = std::max(sp, split_fc_need(1, ga.M, ga.N, up.cs));
                 } else {
                     const ParamL& w = c->params[s.param];
+                    const VarL& up = P.L(s.in[0]);
                     ga.M = w.K;
                     ga.N = w.in_dev;
-                    ga.K = P.L(s.in[0]).N;
+                    ga.K = c->f32 ? kSplitN * up.N : up.N;
+                    ga.d_dtype = TC_DTYPE_F32;
+                    if (c->f32) sp = std::max(sp, split_fc_need(2, up.cs, ga.N, up.N));
                 }
                 need = std::max(need, tc_gemm_workspace_bytes(&ga));
                 break;
@@ -1071,6 +1242,7 @@ size_t workspace_need(tc_ctx* c) {
             default: break;
         }
     }
+    if (split) *split = sp;
     return need;
 }
 
@@ -1095,6 +1267,7 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     if (c->desc.seed == 0) c->desc.seed = 42;
     TCB_CUDA_CHECK(cudaSetDevice(desc->device));
     TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->f32 = desc->precision == TC_PREC_F32;
     tc_status r = analyze_layouts(c.get());
     if (r != TC_OK) return r;
     plan_fusion(c.get());
@@ -1176,17 +1349,18 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMalloc(&c->arena, std::max<size_t>(c->arena_bytes, 256)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
     // input staging: NHWC bf16 batch + labels + NCHW fp32 staging for host batches
-    c->input_cs = plan->input_dims[1] <= 4 ? 4 : ceil8(plan->input_dims[1]);  // must match the LOAD_X var layout
+    c->input_cs = plan->input_dims[1] <= 4 && !c->f32 ? 4 : ceil8(plan->input_dims[1]);  // = the LOAD_X var layout
     c->in_layout.N = static_cast<int>(plan->input_dims[0]);
     c->in_layout.C = static_cast<int>(plan->input_dims[1]);
     c->in_layout.H = static_cast<int>(plan->input_dims[2]);
     c->in_layout.W = static_cast<int>(plan->input_dims[3]);
     c->in_layout.cs = c->input_cs;
     const size_t in_el = static_cast<size_t>(c->in_layout.elems());
+    const size_t in_es = c->f32 ? 4 : 2;
     const size_t stage_el = static_cast<size_t>(plan->input_dims[0]) * plan->input_dims[1] * plan->input_dims[2] * plan->input_dims[3];
-    c->input_bytes = in_el * 2 + 2 * stage_el * 4;
-    TCB_CUDA_CHECK(cudaMalloc(&c->d_input, in_el * 2));
-    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_input, 0, in_el * 2, c->st));
+    c->input_bytes = in_el * in_es + 2 * stage_el * 4;
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_input, in_el * in_es));
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_input, 0, in_el * in_es, c->st));
     for (int k = 0; k < 2; ++k) {
         TCB_CUDA_CHECK(cudaMalloc(&c->d_stage[k], stage_el * 4));
         TCB_CUDA_CHECK(cudaMalloc(&c->d_label_stage[k], plan->input_dims[0] * sizeof(int32_t)));
@@ -1205,7 +1379,8 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     c->h_iter[0] = c->h_iter[1] = 0;
     c->h_loss[0] = 0.f;
     // workspace + reduction partials
-    c->ws_bytes = workspace_need(c.get());
+    c->ws_bytes = workspace_need(c.get(), &c->split_bytes);
+    if (c->split_bytes) TCB_CUDA_CHECK(cudaMalloc(&c->split_buf, c->split_bytes));
     int maxc = 8;
     for (auto& [id, v] : c->vars) maxc = std::max(maxc, v.cs);
     for (const ParamL& q : c->params) maxc = std::max(maxc, q.K);
@@ -1285,6 +1460,7 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->arena);
     cudaFree(c->slab);
     cudaFree(c->ws);
+    cudaFree(c->split_buf);
     cudaFree(c->partials);
     cudaFree(c->bn_sums);
     cudaFree(c->d_input);
@@ -1388,7 +1564,8 @@ static tc_status consume_staged(tc_ctx* c) {
     TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->h2d_done[k], 0));
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, c->d_label_stage[k], c->plan->input_dims[0] * sizeof(int32_t),
                                    cudaMemcpyDeviceToDevice, c->st));
-    tc_status r = launch_nchw_to_nhwc(c->d_stage[k], c->d_input, c->in_layout, c->st);
+    tc_status r = c->f32 ? launch_nchw_to_nhwc(c->d_stage[k], static_cast<float*>(c->d_input), c->in_layout, c->st)
+                         : launch_nchw_to_nhwc(c->d_stage[k], static_cast<bf16*>(c->d_input), c->in_layout, c->st);
     if (r != TC_OK) return r;
     TCB_CUDA_CHECK(cudaEventRecord(c->conv_done[k], c->st));
     return TC_OK;
@@ -1399,8 +1576,11 @@ tc_status tc_stage_synthetic(tc_ctx* c, int iter, int n0) {
     tc_status r0 = consume_staged(c);  // keep slot bookkeeping consistent; the synthetic batch wins
     if (r0 != TC_OK) return r0;
     const tc_plan* p = c->plan;
-    return launch_synth_batch(c->d_input, c->d_labels, c->in_layout, static_cast<int>(p->classes), c->desc.seed,
-                              static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    if (c->f32)
+        return launch_synth_batch(static_cast<float*>(c->d_input), c->d_labels, c->in_layout, static_cast<int>(p->classes),
+                                  c->desc.seed, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    return launch_synth_batch(static_cast<bf16*>(c->d_input), c->d_labels, c->in_layout, static_cast<int>(p->classes),
+                              c->desc.seed, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
 }
 
 tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {

@@ -15,13 +15,15 @@ from .network import CompiledNetwork
 
 class Trainer:
     def __init__(self, net: CompiledNetwork, device: int = 0, seed: int = 42, use_graph: bool = True,
-                 keep: bool = False, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+                 keep: bool = False, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 precision: str = "bf16"):
         L = nat.lib()
         self.net = net
         self._id_buf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = nat.CtxDesc(device=device, rank=rank, world=world,
                         nccl_id=C.cast(self._id_buf, C.c_void_p) if self._id_buf else None, seed=seed,
-                        use_graph=int(use_graph), keep=int(keep))
+                        use_graph=int(use_graph), keep=int(keep),
+                        precision=nat.TC_PREC_F32 if precision == "f32" else nat.TC_PREC_BF16)
         h = C.c_void_p()
         nat.check(L.tc_ctx_create(net.plan_ptr, C.byref(d), C.byref(h)))
         self._h = h

@@ -33,9 +33,9 @@ def final_alias(net):
     return set(last.values())
 
 
-def run_device(name, batch, seed=5):
+def run_device(name, batch, seed=5, precision="bf16"):
     net = compile_network(name, batch)
-    tr = Trainer(net, keep=True, use_graph=False, seed=seed)
+    tr = Trainer(net, keep=True, use_graph=False, seed=seed, precision=precision)
     tr.init_params()
     x, y = orc.synth_batch(net, seed, 0)
     tr.stage_batch(x, y)
@@ -176,3 +176,43 @@ def test_dropout_masks_bit_exact():
     o.step(0, update=False, keep=True)
     for s in masks:
         np.testing.assert_array_equal(tr.var(s.var), o.var(s.var))
+
+
+# fp32 precision mode: element-wise / per-pixel ops within the north star's 1e-5 (fp32 ops);
+# contractions (6-term hi/mid/lo bf16 split, tensor-core fp32 accumulation over up to 6 x 4608
+# terms) and long fp32 reductions (bias / BN sums over up to 2e5 pixels, whose result can be
+# small against its terms) within 1e-4 relative to max|ref| — an fp32 summation-order bound;
+# pooling values and argmax indices bit-exact.
+F32_TOL = {"CONV_FWD": 1e-4, "CONV_BWD_DATA": 1e-4, "CONV_BWD_FILTER": 1e-4, "MATMUL_BWD_DATA": 1e-4,
+           "MATMUL_BWD_W": 1e-4, "CONV_BWD_BIAS": 1e-4, "BIAS_GRAD": 1e-4, "BN_BWD_BETA": 1e-4,
+           "BN_BWD_GAMMA": 1e-4}
+
+
+@pytest.mark.parametrize("name,batch", [("lenet", 8), ("alexnet", 2), ("inception", 4), ("resnet50", 2)])
+def test_per_op_parity_f32(name, batch):
+    net, tr = run_device(name, batch, precision="f32")
+    final = final_alias(net)
+    overwritten = {s.inp[0].index for s in net.stmts if s.kind == nat.TC_STMT_LET and s.inplace}
+    worst, failures = {}, []
+    for s in net.stmts:
+        if s.kind not in (nat.TC_STMT_LET, nat.TC_STMT_UPDATE):
+            continue
+        if s.kind == nat.TC_STMT_LET and s.var not in final:
+            continue
+        if any(s.inp[i].kind == nat.TC_REF_VAR and s.inp[i].index in overwritten and s.inp[i].index not in final
+               for i in range(s.nin)):
+            continue
+        op = nat.OP_NAMES[s.op]
+        if op in ("MATMUL_FWD", "BIAS_ADD", "RELU_FWD", "LOAD_X", "LOAD_Y", "MUL", "ADD", "PRINT_LOSS"):
+            continue
+        ref = oracle_op(net, tr, s)
+        if ref is None:
+            continue
+        dev = tr.var(s.var) if s.kind == nat.TC_STMT_LET else tr.grad(s.param)
+        err = maxrel(dev, ref)
+        worst[op] = max(worst.get(op, 0.0), err)
+        tol = F32_TOL.get(op, 1e-5)
+        if (op == "POOL_FWD" and s.max_pool and not np.array_equal(dev, ref)) or err > tol:
+            failures.append((op, s.var, s.param, err))
+    print(name, "f32 per-op worst", worst)
+    assert not failures, failures
