@@ -644,6 +644,18 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
     }
 }
 
+// 8 per-channel coefficients starting at channel c0 (a multiple of 8): two 16-byte loads when
+// the array offset is 16-byte aligned and all 8 channels exist, else guarded scalars.
+__device__ __forceinline__ void ld_coef8(const float* __restrict__ a, int c0, int C, float (&v)[8]) {
+    if (c0 + 8 <= C && (reinterpret_cast<uintptr_t>(a + c0) & 15) == 0) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(a + c0)), y = __ldg(reinterpret_cast<const float4*>(a + c0) + 1);
+        v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z, v[7] = y.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = c0 + j < C ? __ldg(a + c0 + j) : 0.f;
+    }
+}
+
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
 template <typename T>
 __global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__ coef, T* __restrict__ y,
@@ -660,11 +672,13 @@ __global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__
             const long long i = i0 + u * S;
             if (i >= n8) break;
             const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
-            float f[8];
+            float f[8], a[8], b[8];
             unpack_raw(q[u], f);
+            ld_coef8(coef, c0, C, a);
+            ld_coef8(coef + C, c0, C, b);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                f[j] = c0 + j < C ? fmaf(f[j], __ldg(coef + c0 + j), __ldg(coef + C + c0 + j)) : 0.f;
+                f[j] = c0 + j < C ? fmaf(f[j], a[j], b[j]) : 0.f;
                 if (relu) f[j] = fmaxf(f[j], 0.f);
             }
             st8(y + i * 8, f);
@@ -706,14 +720,14 @@ __global__ void k_bn_bwd_apply(const T* __restrict__ dy, const T* __restrict__ x
             const long long i = i0 + u * S;
             if (i >= n8) break;
             const int c0 = static_cast<int>(n8 < (1ll << 31) ? static_cast<int>(i) % ld8 : i % ld8) * 8;
-            float f[8], g[8];
+            float f[8], g[8], k1[8], k2[8], k3[8];
             unpack_raw(q[u], f);
             unpack_raw(r[u], g);
+            ld_coef8(k, c0, C, k1);
+            ld_coef8(k + C, c0, C, k2);
+            ld_coef8(k + 2 * C, c0, C, k3);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int c = c0 + j;
-                f[j] = c < C ? fmaf(__ldg(k + c), f[j], fmaf(__ldg(k + C + c), g[j], __ldg(k + 2 * C + c))) : 0.f;
-            }
+            for (int j = 0; j < 8; ++j) f[j] = c0 + j < C ? fmaf(k1[j], f[j], fmaf(k2[j], g[j], k3[j])) : 0.f;
             st8(dx + i * 8, f);
         }
     }
@@ -1309,7 +1323,8 @@ size_t colsum_partials_floats(int cols) {
     // 2 accumulators x splits x C, with splits * tiles <= 4 * SMs and ct >= min(C, 512)
     const int ld = std::max(8, (cols + 7) / 8 * 8);
     const int tiles = (ld + 511) / 512;
-    return 2ull * (static_cast<size_t>(num_sms()) * 4 / tiles + 1) * ld + 3ull * ld + 64;
+    const size_t n = 2ull * (static_cast<size_t>(num_sms()) * 4 / tiles + 1) * ld + 3ull * ld + 64;
+    return (n + 63) / 64 * 64;  // keeps the coefficient area behind the partials 16-byte aligned
 }
 
 template <int MODE, typename T>

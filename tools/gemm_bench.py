@@ -97,6 +97,7 @@ def main():
     ap.add_argument("--which", default="gemm,conv")
     ap.add_argument("--net", default="alexnet,vgg16,resnet50")
     ap.add_argument("--small-k", action="store_true", help="GEMM shapes of 1x1 convs (epilogue-paced)")
+    ap.add_argument("--conv-as-gemm", action="store_true", help="AlexNet conv GEMM views with dense operands")
     ap.add_argument("--only", default="", help="run only conv cases whose tuple text contains this")
     args = ap.parse_args()
     print(f"TCB_FORCE_BN={os.environ.get('TCB_FORCE_BN', '')} TCB_IM2COL={os.environ.get('TCB_IM2COL', '')}")
@@ -104,6 +105,8 @@ def main():
         shapes = [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096), (4096, 4096, 4096)]
         if args.small_k:
             shapes = [(200704, 256, k) for k in (64, 128, 256, 512, 1024)] + [(200704, 64, 256), (50176, 1024, 256)]
+        if args.conv_as_gemm:  # the GEMM views of im2col convs with dense operands (im2col cost excluded)
+            shapes = [(86528, 96, 6400), (373248, 96, 576), (86528, 256, 2400), (18432, 384, 2304), (18432, 256, 3456)]
         for M, N, K in shapes:
             ms, tf = gemm_case(M, N, K)
             print(f"gemm {M}x{N}x{K}: {ms:.3f} ms {tf:.0f} TF/s")
