@@ -762,6 +762,24 @@ __global__ void k_channel_copy(const T* __restrict__ src, int src_cs, T* __restr
     }
 }
 
+// 8-channel chunks when strides, offset and width are multiples of 8 (every GoogLeNet concat)
+template <typename T>
+__global__ void k_channel_copy8(const T* __restrict__ src, int src_cs, T* __restrict__ dst, int dst_cs, int off, int c8,
+                                long long pixels) {
+    pdl_wait();
+    pdl_trigger();
+    const long long total = pixels * c8;
+    const bool i32 = total < (1ll << 31);
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long p = i32 ? static_cast<long long>(static_cast<int>(t) / c8) : t / c8;
+        const int g = static_cast<int>(t - p * c8);
+        float f[8];
+        ld8(src + p * src_cs + g * 8, f);
+        st8(dst + p * dst_cs + off + g * 8, f);
+    }
+}
+
 // ---------------------------------------------------------------- dense im2col (small-C first layers)
 __global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo,
                          int Kp, bf16* __restrict__ col) {
@@ -1364,6 +1382,11 @@ tc_status launch_bias_add(const T* x, const float* b, T* y, long long rows, int 
 template <typename T>
 tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st) {
+    if ((src_cs | dst_cs | off | c) % 8 == 0 && (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0) {
+        TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
+        TCB_LAUNCH_CHECK();
+        return TC_OK;
+    }
     TCB_LAUNCH(k_channel_copy<T>, EW_GRID(pixels * c), src, src_cs, dst, dst_cs, off, c, pixels);
     TCB_LAUNCH_CHECK();
     return TC_OK;
