@@ -601,7 +601,10 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const T* __restrict
 }
 
 // Stage 2.  RED_SUM: out[c] = scale * sum.  RED_STATS: stats = (mean, istd), coef =
-// (gamma * istd, beta - mean * gamma * istd).  RED_BNBWD: out = (sum dy, sum dy*xhat).
+// (gamma * istd, beta - mean * gamma * istd).  RED_BNBWD: out = (sum dy, sum dy*xhat) and, when
+// gamma is given, the data-gradient coefficients (k1, k2, k3) at out + 2C, with `beta` = the
+// forward statistics (mean, istd) and `scale` = 1 / rows:
+//   dx = gamma*istd*(dy - sum(dy)/M - xhat*sum(dy*xhat)/M) = k1*dy + k2*x + k3
 template <int MODE, typename T>
 __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ part, int splits, int C, float scale,
                                                     float* __restrict__ out, const T* __restrict__ x, long long rows,
@@ -641,6 +644,14 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
     } else {
         out[c] = sa;
         out[C + c] = sb;
+        if (gamma) {
+            const float is = beta[C + c], mean = beta[c];
+            const float g = gamma[c] * is;
+            const float t = sb * scale * is;  // sum(dy*xhat)/M * istd
+            out[2 * C + c] = g;
+            out[3 * C + c] = -g * t;
+            out[4 * C + c] = -g * sa * scale + g * t * mean;
+        }
     }
 }
 
@@ -686,21 +697,7 @@ __global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__
     }
 }
 
-// dx = gamma*istd*(dy - sum(dy)/M - xhat*sum(dy*xhat)/M) = k1*dy + k2*x + k3 (per channel)
-__global__ void k_bn_coef_bwd(const float* __restrict__ gamma, const float* __restrict__ stats,
-                              const float* __restrict__ sums, float* __restrict__ k, int C, float invm) {
-    pdl_wait();
-    pdl_trigger();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
-    const float is = stats[C + c], mean = stats[c];
-    const float g = gamma[c] * is;
-    const float t = sums[C + c] * invm * is;  // sum(dy*xhat)/M * istd
-    k[c] = g;
-    k[C + c] = -g * t;
-    k[2 * C + c] = -g * sums[c] * invm + g * t * mean;
-}
-
+// dx = k1*dy + k2*x + k3 per channel (coefficients from k_chan_final<RED_BNBWD>)
 template <typename T>
 __global__ void k_bn_bwd_apply(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ k,
                                T* __restrict__ dx, long long n8, int ld8, int C) {
@@ -1413,25 +1410,21 @@ tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y,
 }
 
 template <typename T>
-tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* stats, float* sums, long long pixels, int C, int cs,
-                               float* partials, int max_partials, cudaStream_t st) {
+tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* gamma, const float* stats, float* sums,
+                               long long pixels, int C, int cs, float* partials, int max_partials, cudaStream_t st) {
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD, T>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, sums,
-               static_cast<const T*>(nullptr), pixels, 0.f,
-                                                              nullptr, nullptr, nullptr);
+    TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C,
+               1.f / static_cast<float>(pixels), sums, static_cast<const T*>(nullptr), pixels, 0.f, gamma, stats,
+               static_cast<float*>(nullptr));
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 
 template <typename T>
-tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* gamma, const float* stats, const float* sums,
-                              T* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, long long pixels, int C, int cs,
                               cudaStream_t st) {
-    float* k = partials + max_partials;
-    TCB_LAUNCH(k_bn_coef_bwd, (C + 255) / 256, 256, 0, st, gamma, stats, sums, k, C, 1.f / static_cast<float>(pixels));
-    TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
     TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
@@ -1522,10 +1515,10 @@ template tc_status launch_bias_add<bf16>(const bf16*, const float*, bf16*, long 
 template tc_status launch_channel_copy<bf16>(const bf16*, int, bf16*, int, int, int, long long, cudaStream_t);
 template tc_status launch_bn_fwd<bf16>(const bf16*, const float*, const float*, bf16*, float*, long long, int, int, float, int,
                                      float*, int, cudaStream_t);
-template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const float*, float*, long long, int, int, float*, int,
-                                            cudaStream_t);
-template tc_status launch_bn_bwd_apply<bf16>(const bf16*, const bf16*, const float*, const float*, const float*, bf16*, long long,
-                                           int, int, float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const float*, const float*, float*, long long,
+                                            int, int, float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_apply<bf16>(const bf16*, const bf16*, const float*, bf16*, long long, int, int,
+                                           cudaStream_t);
 template tc_status launch_nchw_to_nhwc<bf16>(const float*, bf16*, StageLayout, cudaStream_t);
 template tc_status launch_synth_batch<bf16>(bf16*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaStream_t);
@@ -1543,10 +1536,10 @@ template tc_status launch_bias_add<float>(const float*, const float*, float*, lo
 template tc_status launch_channel_copy<float>(const float*, int, float*, int, int, int, long long, cudaStream_t);
 template tc_status launch_bn_fwd<float>(const float*, const float*, const float*, float*, float*, long long, int, int, float, int,
                                      float*, int, cudaStream_t);
-template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const float*, float*, long long, int, int, float*, int,
-                                            cudaStream_t);
-template tc_status launch_bn_bwd_apply<float>(const float*, const float*, const float*, const float*, const float*, float*, long long,
-                                           int, int, float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const float*, const float*, float*, long long,
+                                            int, int, float*, int, cudaStream_t);
+template tc_status launch_bn_bwd_apply<float>(const float*, const float*, const float*, float*, long long, int, int,
+                                           cudaStream_t);
 template tc_status launch_nchw_to_nhwc<float>(const float*, float*, StageLayout, cudaStream_t);
 template tc_status launch_synth_batch<float>(float*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 

@@ -90,13 +90,14 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 template <typename T>
 tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y, float* stats, long long pixels, int C,
                         int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st);
-// sums = (sum dy[C], sum dy * xhat[C]) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) and dx
+// sums[0..2C) = (sum dy, sum dy * xhat) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) —
+// and sums[2C..5C) = the data-gradient coefficients (k1, k2, k3) from gamma and the forward stats
 template <typename T>
-tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* stats, float* sums, long long pixels, int C, int cs,
-                               float* partials, int max_partials, cudaStream_t st);
+tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* gamma, const float* stats, float* sums,
+                               long long pixels, int C, int cs, float* partials, int max_partials, cudaStream_t st);
+// dx = k1*dy + k2*x + k3 per channel, k = sums + 2C of launch_bn_bwd_reduce
 template <typename T>
-tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* gamma, const float* stats, const float* sums,
-                              T* dx, long long pixels, int C, int cs, float* partials, int max_partials,
+tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, long long pixels, int C, int cs,
                               cudaStream_t st);
 
 // Dense im2col for small-channel (first-layer) convolutions: col[m][kk], m = (n, oh, ow),

@@ -107,8 +107,8 @@ struct tc_ctx {
     // BatchNorm backward: the BETA / DATA / GAMMA statements of one BN share the
     // reductions (sum dy, sum dy*xhat), computed once at the group's first statement
     struct BnGroup {
-        int x_var = -1, up_var = -1, first = -1;
-        float* sums = nullptr;  // 2*C persistent floats
+        int x_var = -1, up_var = -1, first = -1, gamma = -1;
+        float* sums = nullptr;  // 5*C persistent floats: sum dy, sum dy*xhat, data-gradient k1..k3
     };
     std::vector<BnGroup> bn_groups;
     std::unordered_map<int, int> stmt_bn_group;     // BN_BWD_* stmt -> group
@@ -752,7 +752,7 @@ tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
         const VarL& x = c->vars.at(gr.x_var);
         const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
         tc_status r = launch_bn_bwd_reduce(reinterpret_cast<const T*>(P.var(gr.up_var)),
-                                           reinterpret_cast<const T*>(P.var(x.id)), stats, gr.sums,
+                                           reinterpret_cast<const T*>(P.var(x.id)), c->params[gr.gamma].p, stats, gr.sums,
                                            static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, c->partials,
                                            c->max_partials, c->st);
         if (r != TC_OK) return r;
@@ -1081,14 +1081,12 @@ tc_status exec_let(tc_ctx* c, int i) {
         case TC_OP_BN_BWD_DATA: {
             const VarL& up = P.L(s.in[0]);
             const VarL& x = P.L(s.in[1]);
-            const float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
-            const float* sums = nullptr;
+            const float* sums = nullptr;  // sums[2C..5C): k1..k3 from the group's reduction
             tc_status r = bn_group_sums<T>(c, i, &sums);
             if (r != TC_OK) return r;
             return launch_bn_bwd_apply(reinterpret_cast<const T*>(P.var(up.id)),
-                                       reinterpret_cast<const T*>(P.var(x.id)), c->params[s.in[2].index].p, stats,
-                                       sums, reinterpret_cast<T*>(y), static_cast<long long>(x.N) * x.H * x.W, x.C,
-                                       x.cs, c->partials, c->max_partials, st);
+                                       reinterpret_cast<const T*>(P.var(x.id)), sums + 2 * x.C, reinterpret_cast<T*>(y),
+                                       static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, st);
         }
         default: break;
     }
@@ -1389,10 +1387,13 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 3 * maxc + 64) * sizeof(float)));
     // BN backward groups
     {
-        std::unordered_map<int, int> beta_x, group_of_x;
+        std::unordered_map<int, int> beta_x, gamma_of_x, group_of_x;
         for (int i = 0; i < plan->nstmts; ++i) {
             const tc_stmt& s = plan->stmts[i];
-            if (s.kind == TC_STMT_LET && s.op == TC_OP_BN_FWD) beta_x[s.in[2].index] = s.in[0].index;
+            if (s.kind == TC_STMT_LET && s.op == TC_OP_BN_FWD) {
+                beta_x[s.in[2].index] = s.in[0].index;
+                gamma_of_x[s.in[0].index] = s.in[1].index;
+            }
         }
         size_t total = 0;
         std::vector<size_t> offs;
@@ -1414,10 +1415,11 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
                 gr.x_var = xv;
                 gr.up_var = s.in[0].index;
                 gr.first = i;
+                gr.gamma = gamma_of_x.at(xv);
                 group_of_x[xv] = static_cast<int>(c->bn_groups.size());
                 c->bn_groups.push_back(gr);
                 offs.push_back(total);
-                total += 2 * static_cast<size_t>(c->vars.at(xv).C) + 64;
+                total += 5 * static_cast<size_t>(c->vars.at(xv).C) + 64;
                 g = group_of_x.find(xv);
             } else if (c->bn_groups[g->second].up_var != s.in[0].index) {
                 return fail(TC_INTERNAL, "runtime: BN backward statements disagree on the upstream gradient");
