@@ -73,3 +73,23 @@ def test_two_rank_gradient_equals_global_batch(name, per_gpu):
         g = o.grad(i)
         gd = np.array(grads_dp[i]).reshape(g.shape)
         assert np.max(np.abs(g - gd)) <= 1e-4 * max(1e-6, np.max(np.abs(g))), net.params[i].name
+
+
+def test_reference_arm_under_torchrun_world2():
+    """The driver launches `bench.py --impl reference` with torchrun for N > 1: rank 0 alone
+    times the reference CPU path and prints one JSON line; the other rank exits 0 silently."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "1"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
