@@ -77,6 +77,9 @@ typedef struct tc_gemm_args {
     void* workspace; size_t workspace_bytes;  /* fp32 partials for split-K */
     int bias_n;                     /* bias[n] read for n < bias_n (0 = N); columns beyond get 0 */
     int b_rows;                     /* rows of B that exist (0 = N); D columns >= b_rows come out 0 */
+    const void* relu_mask;          /* bf16 [M][mask_ld], may be NULL: D *= [relu_mask > 0] (ReLU backward
+                                       folded into the epilogue; bf16 D, no split-K / beta) */
+    long long mask_ld;
 } tc_gemm_args;
 
 /* D[M,N] = alpha * sum_k A[m,k] B[n,k] (+bias[n]) (relu), tcgen05 kind::f16. */

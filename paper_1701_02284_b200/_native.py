@@ -41,7 +41,7 @@ class GemmArgs(C.Structure):
         ("alpha", C.c_float), ("beta", C.c_float),
         ("splits", C.c_int),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-        ("bias_n", C.c_int), ("b_rows", C.c_int),
+        ("bias_n", C.c_int), ("b_rows", C.c_int), ("relu_mask", C.c_void_p), ("mask_ld", C.c_longlong),
     ]
 
 

@@ -318,6 +318,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
     const bool partial = lp.splits > 1 || beta != 0.f;
+    if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
     if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
@@ -383,6 +384,8 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     p.N = a->N;
     p.K = a->K;
     p.alpha = a->alpha;
+    p.mask = static_cast<const __nv_bfloat16*>(a->relu_mask);
+    p.mask_ld = a->mask_ld;
     LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
     std::string err;
     if (a->a_layout == TC_LAYOUT_K) {
@@ -519,12 +522,14 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
 }
 
 tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
-                           size_t ws_bytes, void* stream) {
+                           size_t ws_bytes, void* stream, const void* relu_mask) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
     if (d->cs % 8) return fail(TC_INVALID_ARG, "conv bwd-data needs a channel stride multiple of 8");
     GemmParams p;
     init_params(p);
+    p.mask = static_cast<const __nv_bfloat16*>(relu_mask);
+    p.mask_ld = d->cs;
     p.M = d->N * d->H * d->W;
     p.N = d->cs;
     p.K = d->R * d->S * d->ks;
@@ -568,7 +573,7 @@ tc_status tc_conv2d_fwd(const tc_conv_desc* d, const void* x, const void* w, con
 
 tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, void* ws,
                              size_t ws_bytes, void* stream) {
-    return conv_bwd_data_ex(d, dy, w_rskc, dx, 0, ws, ws_bytes, stream);
+    return conv_bwd_data_ex(d, dy, w_rskc, dx, 0, ws, ws_bytes, stream, nullptr);
 }
 
 tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void* x, float* dw, void* ws,

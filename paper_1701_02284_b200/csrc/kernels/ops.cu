@@ -246,7 +246,8 @@ __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, 
 // (no atomics; fixed window order, deterministic).
 template <typename T, typename IT>
 __global__ void k_pool_bwd(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
-                           T* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max) {
+                           T* __restrict__ dx, Act4 xi, int k, int stride, int pad, int is_max,
+                           const T* __restrict__ relu_y) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
@@ -287,7 +288,15 @@ __global__ void k_pool_bwd(const T* __restrict__ dy, Act4 yo, const uint8_t* __r
                     for (int j = 0; j < 8; ++j) acc[j] += d[j] * inv;
                 }
             }
-        st8(dx + ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8, acc);
+        const long long o = ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8;
+        if (relu_y) {  // folded ReLU backward: relu_y is the ReLU output (= the pooling input)
+            float m[8];
+            ld8(relu_y + o, m);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (!(m[j] > 0.f)) acc[j] = 0.f;
+        }
+        st8(dx + o, acc);
     }
 }
 
@@ -326,7 +335,7 @@ __global__ void k_lrn_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, in
 
 template <typename T>
 __global__ void k_lrn_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
-                          T* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk) {
+                          T* __restrict__ dx, Act4 a, int size, float alpha, float beta, float kk, int relu) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ float sm[];
@@ -358,6 +367,7 @@ __global__ void k_lrn_bwd(const T* __restrict__ dy, const T* __restrict__ x, con
                 float s = 0.f;
                 for (int cc = max(0, c - half); cc <= min(a.C - 1, c + half); ++cc) s += tt[cc];
                 out = to_f(dy[o + c]) * powf(sc[c], -beta) - coef * to_f(x[o + c]) * s;
+                if (relu && !(to_f(x[o + c]) > 0.f)) out = 0.f;
             }
             dx[o + c] = from_f<T>(out);
         }
@@ -893,7 +903,7 @@ __global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, f
 
 template <int HALF, typename T>
 __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
-                           T* __restrict__ dx, Act4 a, float alpha, float beta, float kk) {
+                           T* __restrict__ dx, Act4 a, float alpha, float beta, float kk, int relu) {
     pdl_wait();
     pdl_trigger();
     const int ng = a.cs / 8;
@@ -927,6 +937,7 @@ __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, co
 #pragma unroll
             for (int d = -HALF; d <= HALF; ++d) s += tt[8 + j + d];
             out[j] = (g * 8 + j) < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
+            if (relu && !(xv[8 + j] > 0.f)) out[j] = 0.f;  // folded ReLU backward: x is the ReLU output
         }
         st8(dx + base + g * 8, out);
     }
@@ -1242,12 +1253,12 @@ tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int 
 }
 template <typename T>
 tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,
-                          int is_max, cudaStream_t st) {
+                          int is_max, const T* relu_y, cudaStream_t st) {
     const long long n = xi.pixels() * (xi.cs / 8);
     if (n < (1ll << 31))
-        TCB_LAUNCH((k_pool_bwd<T, int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_bwd<T, int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max, relu_y);
     else
-        TCB_LAUNCH((k_pool_bwd<T, long long>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_bwd<T, long long>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max, relu_y);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1270,17 +1281,17 @@ tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float 
 }
 template <typename T>
 tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int size, float alpha, float beta,
-                         float k, cudaStream_t st) {
+                         float k, int relu, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
     switch (size) {
-        case 3: TCB_LAUNCH((k_lrn2_bwd<1, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 5: TCB_LAUNCH((k_lrn2_bwd<2, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 7: TCB_LAUNCH((k_lrn2_bwd<3, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
-        case 9: TCB_LAUNCH((k_lrn2_bwd<4, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k); break;
+        case 3: TCB_LAUNCH((k_lrn2_bwd<1, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 5: TCB_LAUNCH((k_lrn2_bwd<2, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 7: TCB_LAUNCH((k_lrn2_bwd<3, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 9: TCB_LAUNCH((k_lrn2_bwd<4, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
         default: {
             const int warps = 8;
             TCB_LAUNCH(k_lrn_bwd<T>, grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st, 
-                dy, x, y, dx, a, size, alpha, beta, k);
+                dy, x, y, dx, a, size, alpha, beta, k, relu);
         }
     }
     TCB_LAUNCH_CHECK();
@@ -1505,9 +1516,11 @@ template tc_status launch_relu_bwd<bf16>(const bf16*, const bf16*, bf16*, long l
 template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t);
 template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t);
 template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
-template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int,
+                                         const bf16*, cudaStream_t);
 template tc_status launch_lrn_fwd<bf16>(const bf16*, bf16*, Act4, int, float, float, float, cudaStream_t);
-template tc_status launch_lrn_bwd<bf16>(const bf16*, const bf16*, const bf16*, bf16*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_lrn_bwd<bf16>(const bf16*, const bf16*, const bf16*, bf16*, Act4, int, float, float, float,
+                                        int, cudaStream_t);
 template tc_status launch_softmax_fwd<bf16>(const bf16*, long long, float*, int, int, cudaStream_t);
 template tc_status launch_softmax_bwd<bf16>(const float*, const float*, bf16*, long long, int, int, cudaStream_t);
 template tc_status launch_colsum<bf16>(const bf16*, long long, int, long long, float*, float*, int, cudaStream_t);
@@ -1526,9 +1539,11 @@ template tc_status launch_relu_bwd<float>(const float*, const float*, float*, lo
 template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t);
 template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t);
 template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
-template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int,
+                                         const float*, cudaStream_t);
 template tc_status launch_lrn_fwd<float>(const float*, float*, Act4, int, float, float, float, cudaStream_t);
-template tc_status launch_lrn_bwd<float>(const float*, const float*, const float*, float*, Act4, int, float, float, float, cudaStream_t);
+template tc_status launch_lrn_bwd<float>(const float*, const float*, const float*, float*, Act4, int, float, float, float,
+                                        int, cudaStream_t);
 template tc_status launch_softmax_fwd<float>(const float*, long long, float*, int, int, cudaStream_t);
 template tc_status launch_softmax_bwd<float>(const float*, const float*, float*, long long, int, int, cudaStream_t);
 template tc_status launch_colsum<float>(const float*, long long, int, long long, float*, float*, int, cudaStream_t);

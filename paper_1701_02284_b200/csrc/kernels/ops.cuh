@@ -43,14 +43,16 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
 template <typename T>
 tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
                           cudaStream_t st);
+// relu_y (may be null): the ReLU output feeding the pooling; dx *= [relu_y > 0] (ReLU backward folded in)
 template <typename T>
 tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,
-                          int is_max, cudaStream_t st);
+                          int is_max, const T* relu_y, cudaStream_t st);
 template <typename T>
 tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st);
+// relu != 0: x is a ReLU output and the ReLU backward is folded in (dx *= [x > 0])
 template <typename T>
 tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int size, float alpha, float beta,
-                         float k, cudaStream_t st);
+                         float k, int relu, cudaStream_t st);
 
 // rows x F, input bf16 with row stride in_ld -> fp32 out (stride F)
 template <typename T>
@@ -153,8 +155,9 @@ tc_status launch_split_rskc(const float* p, long long ld, int K, int RS, int cs,
 // Convolv fprop / bwd-data with an fp32 output (y_f32 / dx_f32 = 1) — gemm.cu
 tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
                       int y_f32, void* ws, size_t ws_bytes, void* stream);
+// relu_mask: bf16 [N*H*W][cs] forward ReLU output; dx *= [mask > 0] in the epilogue (may be null)
 tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
-                           size_t ws_bytes, void* stream);
+                           size_t ws_bytes, void* stream, const void* relu_mask = nullptr);
 
 // d_iter[0] = iter, d_iter[1] = n0 (kernel arguments travel with the launch: no host sync)
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st);

@@ -75,6 +75,10 @@ struct GemmParams {
     int n_bias;                 // bias is read for n < n_bias (padded channels get 0)
     int relu;
     float alpha;
+    // ReLU-backward folded into the epilogue (bf16 output, no split-K): D *= [mask > 0], mask is
+    // the forward ReLU output, same row / column indexing as D with row stride mask_ld
+    const __nv_bfloat16* mask;
+    long long mask_ld;
     // TMA im2col operand: tmA (OP_IM2COL_K) or tmB (OP_IM2COL_MN) is a 4-D {c, w, h, n} im2col map
     int i2c_cpb;             // 64-channel (32 for OP_IM2COL32_K) blocks per filter tap (A side)
     int i2c_ldk;             // k coordinate of tap t in the other operand = t * i2c_ldk + 64 * block
@@ -707,9 +711,30 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_addr[buf]);
                 }
+                uint64_t mbits = ~0ull;  // bit j: column nb + j passes the ReLU mask
+                if (p.mask) {
+                    mbits = 0;
+                    const int row = m0 + quarter * 32 + lane;
+                    if (row < p.M) {
+                        const uint4* mp = reinterpret_cast<const uint4*>(p.mask + row * p.mask_ld + nb);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (nb + q * 8 >= p.N) break;
+                            const uint4 m = __ldg(mp + q);
+                            const uint32_t w[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+                            for (int h = 0; h < 8; ++h) {
+                                const uint32_t b = (w[h >> 1] >> ((h & 1) * 16)) & 0xFFFFu;
+                                if (!(b & 0x8000u) && (b & 0x7FFFu)) mbits |= 1ull << (q * 8 + h);
+                            }
+                        }
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     float v0 = __uint_as_float(r0[j]) * p.alpha, v1 = __uint_as_float(r1[j]) * p.alpha;
+                    if (!((mbits >> j) & 1)) v0 = 0.f;
+                    if (!((mbits >> (32 + j)) & 1)) v1 = 0.f;
                     if (p.bias) {
                         v0 += __shfl_sync(0xffffffffu, b0, j);
                         v1 += __shfl_sync(0xffffffffu, b1, j);

@@ -117,6 +117,7 @@ struct tc_ctx {
     std::vector<uint8_t> fused;                     // stmt folded into its producer
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
     std::vector<int> fuse_bias_param;
+    std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
 
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0, arena_keep_bytes = 0;
@@ -357,6 +358,7 @@ void plan_fusion(tc_ctx* c) {
     c->fuse_bias.assign(p->nstmts, 0);
     c->fuse_relu.assign(p->nstmts, 0);
     c->fuse_bias_param.assign(p->nstmts, -1);
+    c->fuse_mask_var.assign(p->nstmts, -1);
     auto next_let = [&](int i) {
         for (int j = i + 1; j < p->nstmts; ++j) {
             if (p->stmts[j].kind == TC_STMT_DEALLOC) continue;
@@ -364,6 +366,44 @@ void plan_fusion(tc_ctx* c) {
         }
         return -1;
     };
+    // In-place ReLU backward folded into the statement that produces its upstream gradient:
+    // data-gradient GEMMs (bf16 mode: the epilogue multiplies by [relu output > 0] before the
+    // store), pooling backward and LRN backward (both precisions)
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET) continue;
+        static const bool gemm_fold = [] {
+            const char* e = std::getenv("TCB_GEMM_RELU_FOLD");
+            return !(e && e[0] == '0');
+        }();
+        const bool gemm = gemm_fold && (s.op == TC_OP_CONV_BWD_DATA || s.op == TC_OP_MATMUL_BWD_DATA);
+        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD) continue;
+        // the next Let, skipping Update / Print statements that do not read this output (the
+        // filter-gradient Update sits between a data gradient and its ReLU backward)
+        int j = -1;
+        for (int k = i + 1; k < p->nstmts; ++k) {
+            const tc_stmt& t = p->stmts[k];
+            if (t.kind == TC_STMT_DEALLOC) continue;
+            if (t.kind == TC_STMT_LET) {
+                j = k;
+                break;
+            }
+            bool reads = false;
+            for (int q = 0; q < t.nin; ++q) reads |= t.in[q].kind == TC_REF_VAR && t.in[q].index == s.var;
+            if (reads) break;
+        }
+        if (j < 0) continue;
+        const tc_stmt& r = p->stmts[j];
+        if (r.op != TC_OP_RELU_BWD || !r.inplace || r.in[0].kind != TC_REF_VAR || r.in[0].index != s.var ||
+            r.in[1].kind != TC_REF_VAR)
+            continue;
+        const VarL& y = c->vars.at(s.var);
+        const VarL& m = c->vars.at(r.in[1].index);
+        if (m.dtype != y.dtype || m.cs != y.cs || m.elems() != y.elems()) continue;
+        if (s.op == TC_OP_LRN_BWD && r.in[1].index != s.in[2].index) continue;  // mask must be the LRN input
+        c->fuse_mask_var[i] = r.in[1].index;
+        c->fused[j] = 1;
+    }
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET || (s.op != TC_OP_CONV_FWD && s.op != TC_OP_MATMUL_FWD && s.op != TC_OP_BN_FWD &&
@@ -869,7 +909,8 @@ tc_status exec_let(tc_ctx* c, int i) {
             tc_conv_desc d = conv_desc(out, w, dy, s);
             if constexpr (std::is_same_v<T, float>)
                 return split_conv(c, 1, d, w, static_cast<const float*>(P.var(dy.id)), nullptr, 0, static_cast<float*>(y));
-            return tc_conv2d_bwd_data(&d, P.var(dy.id), w.rskc, y, c->ws, c->ws_bytes, st);
+            return conv_bwd_data_ex(&d, P.var(dy.id), w.rskc, y, 0, c->ws, c->ws_bytes, st,
+                                    c->fuse_mask_var[i] >= 0 ? P.var(c->fuse_mask_var[i]) : nullptr);
         }
         case TC_OP_POOL_FWD: {
             const VarL& x = P.L(s.in[0]);
@@ -884,7 +925,10 @@ tc_status exec_let(tc_ctx* c, int i) {
                                             : nullptr;
             Act4 ya = fy.act();
             return launch_pool_bwd(reinterpret_cast<const T*>(P.var(up.id)), ya, idx, reinterpret_cast<T*>(y),
-                                   out.act(), s.k, s.stride, s.pad, s.max_pool, st);
+                                   out.act(), s.k, s.stride, s.pad, s.max_pool,
+                                   c->fuse_mask_var[i] >= 0 ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i]))
+                                                            : static_cast<const T*>(nullptr),
+                                   st);
         }
         case TC_OP_RELU_FWD:
             return launch_relu_fwd(reinterpret_cast<const T*>(P.var(s.in[0].index)), reinterpret_cast<T*>(y),
@@ -911,7 +955,7 @@ tc_status exec_let(tc_ctx* c, int i) {
                                   reinterpret_cast<const T*>(P.var(s.in[2].index)),
                                   reinterpret_cast<const T*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
                                   out.act(), s.lrn_size, static_cast<float>(s.alpha), static_cast<float>(s.beta),
-                                  static_cast<float>(s.lrn_k), st);
+                                  static_cast<float>(s.lrn_k), c->fuse_mask_var[i] >= 0 ? 1 : 0, st);
         case TC_OP_DROPOUT_MASK:
             return launch_dropout_mask(reinterpret_cast<uint8_t*>(y), out.N, out.H, out.W, out.C, out.cs,
                                        static_cast<float>(s.rate), c->desc.seed, static_cast<uint32_t>(s.var), c->d_iter,
@@ -1037,6 +1081,11 @@ tc_status exec_let(tc_ctx* c, int i) {
             ga.ldd = w.in_dev;
             ga.d_dtype = TC_DTYPE_BF16;
             ga.alpha = 1.f;
+            if (c->fuse_mask_var[i] >= 0) {  // the following ReLU backward, folded into the epilogue
+                ga.relu_mask = P.var(c->fuse_mask_var[i]);
+                ga.mask_ld = w.in_dev;
+                ga.splits = 1;  // the mask is applied by the tile epilogue, not by a split-K reduce
+            }
             return run_gemm_args(c, ga);
         }
         case TC_OP_BIAS_ADD: {
