@@ -1,6 +1,8 @@
 // Bandwidth-bound kernels of the training step.  See ops.cuh for layouts.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ops.cuh"
@@ -239,6 +241,135 @@ __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, 
                   static_cast<uint32_t>(bi[7]) << 24;
             *reinterpret_cast<uint2*>(idx + o) = q;
         }
+    }
+}
+
+// Fixed-window max pooling on bf16 storage (K x K window, stride S known at compile time): the
+// K*K taps are unrolled so all loads are in flight together, and the compare / select runs on
+// packed bf16 pairs (one HGT2 mask + two LOP3 per channel pair and tap instead of ~5 fp32
+// instructions per channel).  The argmax half-words track the first maximum in row-major
+// window order exactly like k_pool_fwd; the max of bf16 values is one of them, so y is
+// bit-identical to the fp32-compare path.
+template <typename IT, int K, int S>
+__global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
+                                   uint8_t* __restrict__ idx, int pad) {
+    pdl_wait();
+    pdl_trigger();
+    const int cg = xi.cs / 8;
+    const IT total = static_cast<IT>(yo.pixels() * cg);
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % cg);
+        IT p = t / cg;
+        const int ow = static_cast<int>(p % yo.W);
+        p /= yo.W;
+        const int oh = static_cast<int>(p % yo.H);
+        const int n = static_cast<int>(p / yo.H);
+        const int ih0 = oh * S - pad, iw0 = ow * S - pad;
+        const bf16* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
+        uint4 v[K * K];
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int ih = ih0 + r, iw = iw0 + s;
+                if (ih >= 0 && ih < xi.H && iw >= 0 && iw < xi.W)
+                    v[r * K + s] = *reinterpret_cast<const uint4*>(img + (static_cast<long long>(ih) * xi.W + iw) * xi.cs);
+                else
+                    v[r * K + s] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf: never wins
+            }
+        // Start from the first in-bounds tap (a window always holds one), then keep strict maxima.
+        const int r0 = ih0 < 0 ? -ih0 : 0, s0 = iw0 < 0 ? -iw0 : 0;
+        uint32_t best[4], bi[4];
+        const uint32_t first = static_cast<uint32_t>(r0 * K + s0) * 0x10001u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            best[i] = 0xFF80FF80u;
+            bi[i] = first;
+        }
+#pragma unroll
+        for (int tap = 0; tap < K * K; ++tap) {
+            const uint32_t tid = static_cast<uint32_t>(tap) * 0x10001u;
+            const uint32_t* f = reinterpret_cast<const uint32_t*>(&v[tap]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t m = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&f[i]),
+                                               *reinterpret_cast<const __nv_bfloat162*>(&best[i]));
+                best[i] = (f[i] & m) | (best[i] & ~m);
+                bi[i] = (tid & m) | (bi[i] & ~m);
+            }
+        }
+        const long long o = ((static_cast<long long>(n) * yo.H + oh) * yo.W + ow) * yo.cs + g * 8;
+        *reinterpret_cast<uint4*>(y + o) = make_uint4(best[0], best[1], best[2], best[3]);
+        if (idx)
+            *reinterpret_cast<uint2*>(idx + o) =
+                make_uint2(__byte_perm(bi[0], bi[1], 0x6420), __byte_perm(bi[2], bi[3], 0x6420));
+    }
+}
+
+// Fixed-window max-pool backward: at most ceil(K/S)^2 windows cover an input element; their
+// dy / argmax loads are issued together (predicated), then accumulated in the same
+// (oh, ow)-ascending order as k_pool_bwd (bit-identical sums).
+template <typename T, typename IT, int K, int S>
+__global__ void k_maxpool_bwd_fixed(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
+                                    T* __restrict__ dx, Act4 xi, int pad, const T* __restrict__ relu_y) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NW = (K + S - 1) / S;
+    const int cg = xi.cs / 8;
+    const IT total = static_cast<IT>(xi.pixels() * cg);
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % cg);
+        IT p = t / cg;
+        const int iw = static_cast<int>(p % xi.W);
+        p /= xi.W;
+        const int ih = static_cast<int>(p % xi.H);
+        const int n = static_cast<int>(p / xi.H);
+        const int nh = ih + pad - K + 1, nw = iw + pad - K + 1;
+        const int oh0 = nh <= 0 ? 0 : (nh + S - 1) / S;
+        const int ow0 = nw <= 0 ? 0 : (nw + S - 1) / S;
+        const int oh1 = min(yo.H - 1, (ih + pad) / S);
+        const int ow1 = min(yo.W - 1, (iw + pad) / S);
+        const long long obase = static_cast<long long>(n) * yo.H * yo.W * yo.cs + g * 8;
+        float d[NW * NW][8];
+        uint2 q[NW * NW];
+#pragma unroll
+        for (int a = 0; a < NW; ++a)
+#pragma unroll
+            for (int b = 0; b < NW; ++b) {
+                const int oh = oh0 + a, ow = ow0 + b;
+                if (oh <= oh1 && ow <= ow1) {
+                    const long long o = obase + (static_cast<long long>(oh) * yo.W + ow) * yo.cs;
+                    ld8(dy + o, d[a * NW + b]);
+                    q[a * NW + b] = __ldg(reinterpret_cast<const uint2*>(idx + o));
+                }
+            }
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+        for (int a = 0; a < NW; ++a)
+#pragma unroll
+            for (int b = 0; b < NW; ++b) {
+                const int oh = oh0 + a, ow = ow0 + b;
+                if (oh > oh1 || ow > ow1) continue;
+                const uint32_t me = static_cast<uint32_t>((ih - (oh * S - pad)) * K + (iw - (ow * S - pad)));
+                const uint32_t mm = me * 0x01010101u;
+                const uint32_t e0 = __vcmpeq4(q[a * NW + b].x, mm), e1 = __vcmpeq4(q[a * NW + b].y, mm);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((((j < 4 ? e0 : e1) >> (8 * (j & 3))) & 1u) != 0u) acc[j] += d[a * NW + b][j];
+            }
+        const long long o = ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8;
+        if (relu_y) {
+            float m[8];
+            ld8(relu_y + o, m);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (!(m[j] > 0.f)) acc[j] = 0.f;
+        }
+        st8(dx + o, acc);
     }
 }
 
@@ -1239,11 +1370,38 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+// TCB_FIXED_POOL=0 routes every pooling through the generic runtime-window kernels (A/B switch).
+bool fixed_pool_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_FIXED_POOL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 template <typename T>
 tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
                           cudaStream_t st) {
     if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
     const long long n = yo.pixels() * (xi.cs / 8);
+    if constexpr (std::is_same<T, bf16>::value) {
+        if (is_max && n < (1ll << 31) && fixed_pool_enabled()) {
+            if (k == 3 && stride == 2) {
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 2>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH_CHECK();
+                return TC_OK;
+            }
+            if (k == 2 && stride == 2) {
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 2, 2>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH_CHECK();
+                return TC_OK;
+            }
+            if (k == 3 && stride == 1) {
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 1>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH_CHECK();
+                return TC_OK;
+            }
+        }
+    }
     if (n < (1ll << 31))
         TCB_LAUNCH((k_pool_fwd<T, int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
     else
@@ -1255,6 +1413,23 @@ template <typename T>
 tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,
                           int is_max, const T* relu_y, cudaStream_t st) {
     const long long n = xi.pixels() * (xi.cs / 8);
+    if (is_max && n < (1ll << 31) && fixed_pool_enabled()) {
+        if (k == 3 && stride == 2) {
+            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 3, 2>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+        if (k == 2 && stride == 2) {
+            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 2, 2>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+        if (k == 3 && stride == 1) {
+            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 3, 1>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+    }
     if (n < (1ll << 31))
         TCB_LAUNCH((k_pool_bwd<T, int>), EW_GRID(n), dy, yo, idx, dx, xi, k, stride, pad, is_max, relu_y);
     else

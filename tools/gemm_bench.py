@@ -20,7 +20,7 @@ CONVS = {  # (N, C, H, W, K, R, S, stride, pad)
     "alexnet": [(128, 3, 224, 224, 96, 11, 11, 4, 0), (128, 96, 26, 26, 256, 5, 5, 1, 2),
                 (128, 256, 12, 12, 384, 3, 3, 1, 1), (128, 384, 12, 12, 384, 3, 3, 1, 1),
                 (128, 384, 12, 12, 256, 3, 3, 1, 1)],
-    "vgg16": [(64, 64, 224, 224, 64, 3, 3, 1, 1), (64, 128, 112, 112, 128, 3, 3, 1, 1),
+    "vgg16": [(64, 3, 224, 224, 64, 3, 3, 1, 1), (64, 64, 224, 224, 64, 3, 3, 1, 1), (64, 128, 112, 112, 128, 3, 3, 1, 1),
               (64, 256, 56, 56, 256, 3, 3, 1, 1), (64, 512, 28, 28, 512, 3, 3, 1, 1),
               (64, 512, 14, 14, 512, 3, 3, 1, 1)],
     "resnet50": [(64, 64, 56, 56, 64, 3, 3, 1, 1), (64, 64, 56, 56, 256, 1, 1, 1, 0),
