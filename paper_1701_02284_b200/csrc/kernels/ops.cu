@@ -66,6 +66,10 @@ __device__ __forceinline__ Raw8<bf16> ld_raw8cs(const bf16* p) { return Raw8<bf1
 __device__ __forceinline__ Raw8<float> ld_raw8cs(const float* p) {
     return Raw8<float>{__ldcs(reinterpret_cast<const float4*>(p)), __ldcs(reinterpret_cast<const float4*>(p) + 1)};
 }
+__device__ __forceinline__ Raw8<bf16> ld_raw8(const bf16* p) { return Raw8<bf16>{*reinterpret_cast<const uint4*>(p)}; }
+__device__ __forceinline__ Raw8<float> ld_raw8(const float* p) {
+    return Raw8<float>{reinterpret_cast<const float4*>(p)[0], reinterpret_cast<const float4*>(p)[1]};
+}
 template <typename T>
 __device__ __forceinline__ Raw8<T> raw8_zero() {
     Raw8<T> r;
@@ -187,7 +191,7 @@ __global__ void k_dropout_mask(uint8_t* __restrict__ keep, int N, int H, int W, 
 // division is ~4x the cost of 32-bit on this path)
 template <typename T, typename IT>
 __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, Act4 yo,
-                           uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max) {
+                           uint8_t* __restrict__ idx, int k, int stride, int pad, int is_max, int flag_nonpos) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
@@ -234,6 +238,11 @@ __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, 
         for (int j = 0; j < 8; ++j) out[j] = is_max ? best[j] : sum[j] * inv;
         st8(y + o, out);
         if (idx) {
+            if (flag_nonpos) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (!(best[j] > 0.f)) bi[j] |= 0x80;
+            }
             uint2 q;
             q.x = static_cast<uint32_t>(bi[0]) | static_cast<uint32_t>(bi[1]) << 8 | static_cast<uint32_t>(bi[2]) << 16 |
                   static_cast<uint32_t>(bi[3]) << 24;
@@ -252,7 +261,7 @@ __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, 
 // bit-identical to the fp32-compare path.
 template <typename IT, int K, int S>
 __global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
-                                   uint8_t* __restrict__ idx, int pad) {
+                                   uint8_t* __restrict__ idx, int pad, int flag_nonpos) {
     pdl_wait();
     pdl_trigger();
     const int cg = xi.cs / 8;
@@ -301,75 +310,98 @@ __global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __
         }
         const long long o = ((static_cast<long long>(n) * yo.H + oh) * yo.W + ow) * yo.cs + g * 8;
         *reinterpret_cast<uint4*>(y + o) = make_uint4(best[0], best[1], best[2], best[3]);
-        if (idx)
+        if (idx) {
+            if (flag_nonpos) {  // folded ReLU backward: a window whose maximum is <= 0 passes no gradient
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    bi[i] |= ~__hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&best[i]), __float2bfloat162_rn(0.f)) &
+                             0x00800080u;
+            }
             *reinterpret_cast<uint2*>(idx + o) =
                 make_uint2(__byte_perm(bi[0], bi[1], 0x6420), __byte_perm(bi[2], bi[3], 0x6420));
+        }
     }
 }
 
-// Fixed-window max-pool backward: at most ceil(K/S)^2 windows cover an input element; their
-// dy / argmax loads are issued together (predicated), then accumulated in the same
-// (oh, ow)-ascending order as k_pool_bwd (bit-identical sums).
-template <typename T, typename IT, int K, int S>
-__global__ void k_maxpool_bwd_fixed(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
+// Fixed-window max-pool backward, patch formulation.  Input rows r = a*S - pad + u (0 <= u < S)
+// of patch a are covered exactly by the windows oh = a - (NW-1) + da, 0 <= da < NW = ceil(K/S),
+// and the window-local tap of (u, da) is u + (NW-1-da)*S: a compile-time constant.  One thread
+// owns an S x S patch x 8 channels: it loads the NW x NW covering windows' dy / argmax once and
+// sends every pixel its matching taps, accumulating in the (oh, ow)-ascending order of
+// k_pool_bwd (bit-identical sums).  An argmax byte with bit 7 set (flagged forward) matches no
+// tap, which is how a folded ReLU backward is applied without reading the ReLU output.
+template <typename T, int K, int S>
+__global__ void k_maxpool_bwd_patch(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
                                     T* __restrict__ dx, Act4 xi, int pad, const T* __restrict__ relu_y) {
     pdl_wait();
     pdl_trigger();
     constexpr int NW = (K + S - 1) / S;
     const int cg = xi.cs / 8;
-    const IT total = static_cast<IT>(xi.pixels() * cg);
-    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<IT>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(t % cg);
-        IT p = t / cg;
-        const int iw = static_cast<int>(p % xi.W);
-        p /= xi.W;
-        const int ih = static_cast<int>(p % xi.H);
-        const int n = static_cast<int>(p / xi.H);
-        const int nh = ih + pad - K + 1, nw = iw + pad - K + 1;
-        const int oh0 = nh <= 0 ? 0 : (nh + S - 1) / S;
-        const int ow0 = nw <= 0 ? 0 : (nw + S - 1) / S;
-        const int oh1 = min(yo.H - 1, (ih + pad) / S);
-        const int ow1 = min(yo.W - 1, (iw + pad) / S);
+    const int PA = (xi.H + pad + S - 1) / S, PB = (xi.W + pad + S - 1) / S;
+    const int total = xi.N * PA * PB * cg;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int g = t % cg;
+        int p = t / cg;
+        const int pb = p % PB;
+        p /= PB;
+        const int pa = p % PA;
+        const int n = p / PA;
         const long long obase = static_cast<long long>(n) * yo.H * yo.W * yo.cs + g * 8;
-        float d[NW * NW][8];
+        Raw8<T> d[NW * NW];
         uint2 q[NW * NW];
 #pragma unroll
-        for (int a = 0; a < NW; ++a)
+        for (int da = 0; da < NW; ++da)
 #pragma unroll
-            for (int b = 0; b < NW; ++b) {
-                const int oh = oh0 + a, ow = ow0 + b;
-                if (oh <= oh1 && ow <= ow1) {
+            for (int db = 0; db < NW; ++db) {
+                const int oh = pa - (NW - 1) + da, ow = pb - (NW - 1) + db;
+                if (oh >= 0 && oh < yo.H && ow >= 0 && ow < yo.W) {
                     const long long o = obase + (static_cast<long long>(oh) * yo.W + ow) * yo.cs;
-                    ld8(dy + o, d[a * NW + b]);
-                    q[a * NW + b] = __ldg(reinterpret_cast<const uint2*>(idx + o));
+                    d[da * NW + db] = ld_raw8(dy + o);
+                    q[da * NW + db] = __ldg(reinterpret_cast<const uint2*>(idx + o));
+                } else {
+                    q[da * NW + db] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // matches no tap
+                    d[da * NW + db] = raw8_zero<T>();
                 }
             }
-        float acc[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int u = 0; u < S; ++u) {
+            const int ih = pa * S - pad + u;
+            if (ih < 0 || ih >= xi.H) continue;
 #pragma unroll
-        for (int a = 0; a < NW; ++a)
+            for (int v = 0; v < S; ++v) {
+                const int iw = pb * S - pad + v;
+                if (iw < 0 || iw >= xi.W) continue;
+                float acc[8];
 #pragma unroll
-            for (int b = 0; b < NW; ++b) {
-                const int oh = oh0 + a, ow = ow0 + b;
-                if (oh > oh1 || ow > ow1) continue;
-                const uint32_t me = static_cast<uint32_t>((ih - (oh * S - pad)) * K + (iw - (ow * S - pad)));
-                const uint32_t mm = me * 0x01010101u;
-                const uint32_t e0 = __vcmpeq4(q[a * NW + b].x, mm), e1 = __vcmpeq4(q[a * NW + b].y, mm);
+                for (int j = 0; j < 8; ++j) acc[j] = 0.f;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if ((((j < 4 ? e0 : e1) >> (8 * (j & 3))) & 1u) != 0u) acc[j] += d[a * NW + b][j];
+                for (int da = 0; da < NW; ++da) {
+                    const int tr = u + (NW - 1 - da) * S;
+                    if (tr >= K) continue;
+#pragma unroll
+                    for (int db = 0; db < NW; ++db) {
+                        const int tc = v + (NW - 1 - db) * S;
+                        if (tc >= K) continue;
+                        const uint32_t mm = static_cast<uint32_t>(tr * K + tc) * 0x01010101u;
+                        const uint32_t e0 = __vcmpeq4(q[da * NW + db].x, mm), e1 = __vcmpeq4(q[da * NW + db].y, mm);
+                        float f[8];
+                        unpack_raw(d[da * NW + db], f);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if ((((j < 4 ? e0 : e1) >> (8 * (j & 3))) & 1u) != 0u) acc[j] += f[j];
+                    }
+                }
+                const long long o = ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8;
+                if (relu_y) {
+                    float m[8];
+                    ld8(relu_y + o, m);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (!(m[j] > 0.f)) acc[j] = 0.f;
+                }
+                st8(dx + o, acc);
             }
-        const long long o = ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8;
-        if (relu_y) {
-            float m[8];
-            ld8(relu_y + o, m);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (!(m[j] > 0.f)) acc[j] = 0.f;
         }
-        st8(dx + o, acc);
     }
 }
 
@@ -1371,6 +1403,9 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
     return TC_OK;
 }
 // TCB_FIXED_POOL=0 routes every pooling through the generic runtime-window kernels (A/B switch).
+long long patch_threads(const Act4& xi, int pad, int S) {
+    return static_cast<long long>(xi.N) * ((xi.H + pad + S - 1) / S) * ((xi.W + pad + S - 1) / S) * (xi.cs / 8);
+}
 bool fixed_pool_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TCB_FIXED_POOL");
@@ -1380,32 +1415,33 @@ bool fixed_pool_enabled() {
 }
 template <typename T>
 tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
-                          cudaStream_t st) {
+                          int flag_nonpos, cudaStream_t st) {
     if (idx && k * k > 255) return fail(TC_INVALID_ARG, "max pooling: window too large for 1-byte argmax");
+    if (flag_nonpos && k * k > 127) return fail(TC_INVALID_ARG, "max pooling: window too large for a flagged argmax");
     const long long n = yo.pixels() * (xi.cs / 8);
     if constexpr (std::is_same<T, bf16>::value) {
         if (is_max && n < (1ll << 31) && fixed_pool_enabled()) {
             if (k == 3 && stride == 2) {
-                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 2>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 2>), EW_GRID(n), x, xi, y, yo, idx, pad, flag_nonpos);
                 TCB_LAUNCH_CHECK();
                 return TC_OK;
             }
             if (k == 2 && stride == 2) {
-                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 2, 2>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 2, 2>), EW_GRID(n), x, xi, y, yo, idx, pad, flag_nonpos);
                 TCB_LAUNCH_CHECK();
                 return TC_OK;
             }
             if (k == 3 && stride == 1) {
-                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 1>), EW_GRID(n), x, xi, y, yo, idx, pad);
+                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 1>), EW_GRID(n), x, xi, y, yo, idx, pad, flag_nonpos);
                 TCB_LAUNCH_CHECK();
                 return TC_OK;
             }
         }
     }
     if (n < (1ll << 31))
-        TCB_LAUNCH((k_pool_fwd<T, int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_fwd<T, int>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max, flag_nonpos);
     else
-        TCB_LAUNCH((k_pool_fwd<T, long long>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max);
+        TCB_LAUNCH((k_pool_fwd<T, long long>), EW_GRID(n), x, xi, y, yo, idx, k, stride, pad, is_max, flag_nonpos);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1415,17 +1451,17 @@ tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 
     const long long n = xi.pixels() * (xi.cs / 8);
     if (is_max && n < (1ll << 31) && fixed_pool_enabled()) {
         if (k == 3 && stride == 2) {
-            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 3, 2>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH((k_maxpool_bwd_patch<T, 3, 2>), EW_GRID(patch_threads(xi, pad, 2)), dy, yo, idx, dx, xi, pad, relu_y);
             TCB_LAUNCH_CHECK();
             return TC_OK;
         }
         if (k == 2 && stride == 2) {
-            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 2, 2>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH((k_maxpool_bwd_patch<T, 2, 2>), EW_GRID(patch_threads(xi, pad, 2)), dy, yo, idx, dx, xi, pad, relu_y);
             TCB_LAUNCH_CHECK();
             return TC_OK;
         }
         if (k == 3 && stride == 1) {
-            TCB_LAUNCH((k_maxpool_bwd_fixed<T, int, 3, 1>), EW_GRID(n), dy, yo, idx, dx, xi, pad, relu_y);
+            TCB_LAUNCH((k_maxpool_bwd_patch<T, 3, 1>), EW_GRID(patch_threads(xi, pad, 1)), dy, yo, idx, dx, xi, pad, relu_y);
             TCB_LAUNCH_CHECK();
             return TC_OK;
         }
@@ -1690,7 +1726,7 @@ template tc_status launch_relu_fwd<bf16>(const bf16*, bf16*, long long, cudaStre
 template tc_status launch_relu_bwd<bf16>(const bf16*, const bf16*, bf16*, long long, cudaStream_t);
 template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t);
 template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t);
-template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int,
                                          const bf16*, cudaStream_t);
 template tc_status launch_lrn_fwd<bf16>(const bf16*, bf16*, Act4, int, float, float, float, cudaStream_t);
@@ -1713,7 +1749,7 @@ template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaS
 template tc_status launch_relu_bwd<float>(const float*, const float*, float*, long long, cudaStream_t);
 template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t);
 template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t);
-template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, cudaStream_t);
+template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int,
                                          const float*, cudaStream_t);
 template tc_status launch_lrn_fwd<float>(const float*, float*, Act4, int, float, float, float, cudaStream_t);

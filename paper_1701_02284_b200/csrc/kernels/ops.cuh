@@ -40,9 +40,12 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st);
 
 // Max pooling argmax: 1 byte per output element, window-local position r*k + s (255 = empty).
+// flag_nonpos (k*k <= 127): the pooling input is a ReLU output whose backward is folded into the
+// pooling backward; a window whose maximum is <= 0 gets bit 7 set, so it routes no gradient
+// (the ReLU mask at the argmax) and the backward never reads the ReLU output.
 template <typename T>
 tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int k, int stride, int pad, int is_max,
-                          cudaStream_t st);
+                          int flag_nonpos, cudaStream_t st);
 // relu_y (may be null): the ReLU output feeding the pooling; dx *= [relu_y > 0] (ReLU backward folded in)
 template <typename T>
 tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 xi, int k, int stride, int pad,

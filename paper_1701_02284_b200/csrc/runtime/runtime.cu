@@ -118,6 +118,8 @@ struct tc_ctx {
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
     std::vector<int> fuse_bias_param;
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
+    std::vector<char> pool_flag_nonpos;             // max-pool forward: flag windows with max <= 0 in the index
+    std::vector<char> pool_mask_in_idx;             // max-pool backward: its folded ReLU mask is in the index
 
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0, arena_keep_bytes = 0;
@@ -352,6 +354,15 @@ tc_status analyze_layouts(tc_ctx* c) {
 }
 
 // Peephole fusion: GEMM producer followed by in-place BiasAdd / ReLU on its storage.
+// TCB_POOL_IDX_FLAG=0 keeps the ReLU output read in the pooling backward (A/B switch).
+static bool pool_idx_flag_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_POOL_IDX_FLAG");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void plan_fusion(tc_ctx* c) {
     const tc_plan* p = c->plan;
     c->fused.assign(p->nstmts, 0);
@@ -359,6 +370,8 @@ void plan_fusion(tc_ctx* c) {
     c->fuse_relu.assign(p->nstmts, 0);
     c->fuse_bias_param.assign(p->nstmts, -1);
     c->fuse_mask_var.assign(p->nstmts, -1);
+    c->pool_flag_nonpos.assign(p->nstmts, 0);
+    c->pool_mask_in_idx.assign(p->nstmts, 0);
     auto next_let = [&](int i) {
         for (int j = i + 1; j < p->nstmts; ++j) {
             if (p->stmts[j].kind == TC_STMT_DEALLOC) continue;
@@ -403,6 +416,15 @@ void plan_fusion(tc_ctx* c) {
         if (s.op == TC_OP_LRN_BWD && r.in[1].index != s.in[2].index) continue;  // mask must be the LRN input
         c->fuse_mask_var[i] = r.in[1].index;
         c->fused[j] = 1;
+        if (s.op == TC_OP_POOL_BWD && s.max_pool && s.k * s.k <= 127 && pool_idx_flag_enabled()) {
+            // max pooling over the ReLU output: the mask at the argmax travels in the index byte
+            const int f = c->vars.at(s.in[1].index).def;
+            if (f >= 0 && p->stmts[f].op == TC_OP_POOL_FWD && p->stmts[f].in[0].kind == TC_REF_VAR &&
+                p->stmts[f].in[0].index == r.in[1].index) {
+                c->pool_flag_nonpos[f] = 1;
+                c->pool_mask_in_idx[i] = 1;
+            }
+        }
     }
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
@@ -916,7 +938,7 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& x = P.L(s.in[0]);
             uint8_t* idx = s.max_pool ? reinterpret_cast<uint8_t*>(c->arena + c->items[c->pool_idx_item.at(s.var)].off) : nullptr;
             return launch_pool_fwd(reinterpret_cast<const T*>(P.var(x.id)), x.act(), reinterpret_cast<T*>(y),
-                                   out.act(), idx, s.k, s.stride, s.pad, s.max_pool, st);
+                                   out.act(), idx, s.k, s.stride, s.pad, s.max_pool, c->pool_flag_nonpos[i], st);
         }
         case TC_OP_POOL_BWD: {
             const VarL& up = P.L(s.in[0]);
@@ -926,7 +948,8 @@ tc_status exec_let(tc_ctx* c, int i) {
             Act4 ya = fy.act();
             return launch_pool_bwd(reinterpret_cast<const T*>(P.var(up.id)), ya, idx, reinterpret_cast<T*>(y),
                                    out.act(), s.k, s.stride, s.pad, s.max_pool,
-                                   c->fuse_mask_var[i] >= 0 ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i]))
+                                   c->fuse_mask_var[i] >= 0 && !c->pool_mask_in_idx[i]
+                                       ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i]))
                                                             : static_cast<const T*>(nullptr),
                                    st);
         }
@@ -1773,9 +1796,10 @@ tc_status tc_pool_indices_download(tc_ctx* c, int var, int32_t* host, int64_t ma
         for (int ch = 0; ch < v.C; ++ch)
             for (int h = 0; h < v.H; ++h)
                 for (int w = 0; w < v.W; ++w) {
-                    const int loc = raw[((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch];
+                    int loc = raw[((static_cast<long long>(n) * v.H + h) * v.W + w) * v.cs + ch];
                     int32_t flat = -1;
                     if (loc != 255) {
+                        if (c->pool_flag_nonpos[v.def]) loc &= 0x7F;  // drop the folded-ReLU flag
                         const int ih = h * s.stride - s.pad + loc / s.k, iw = w * s.stride - s.pad + loc % s.k;
                         flat = static_cast<int32_t>(((static_cast<long long>(n) * x.C + ch) * x.H + ih) * x.W + iw);
                     }
