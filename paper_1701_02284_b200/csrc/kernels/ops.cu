@@ -48,7 +48,10 @@ template <>
 __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
 template <>
 __device__ __forceinline__ float from_f<float>(float v) { return v; }
-__device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
+__device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);  // one 16-byte load (unpack8 reads through a reference)
+    unpack8(q, f);
+}
 __device__ __forceinline__ void ld8(const float* p, float (&f)[8]) {
     const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
     f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
@@ -1034,6 +1037,21 @@ __device__ __forceinline__ void load_chunk3(const T* __restrict__ p, int g, int 
     }
 }
 
+// LRN scale terms are >= k > 0 and far from the denormal range: pow / reciprocal straight on the
+// MUFU approximations (the same lg2 / ex2 / rcp __powf and __fdividef use, minus their
+// denormal-range fix-ups and branches).
+__device__ __forceinline__ float pow_pos(float x, float e) {
+    float l, r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * e));
+    return r;
+}
+__device__ __forceinline__ float rcp_pos(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // HALF = n/2 is a template parameter so every window loop unrolls and the
 // per-thread channel windows stay in registers.
 template <int HALF, typename T>
@@ -1058,7 +1076,7 @@ __global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, f
             float s = 0.f;
 #pragma unroll
             for (int d = -HALF; d <= HALF; ++d) s += v[8 + j + d] * v[8 + j + d];
-            out[j] = (g * 8 + j) < a.C ? v[8 + j] * __powf(kk + an * s, -beta) : 0.f;
+            out[j] = (g * 8 + j) < a.C ? v[8 + j] * pow_pos(kk + an * s, -beta) : 0.f;
         }
         st8(y + t * 8, out);
     }
@@ -1091,7 +1109,7 @@ __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, co
             for (int d = -HALF; d <= HALF; ++d) s += xv[i + d] * xv[i + d];
             sc[i] = kk + an * s;
             // zero for channels outside [0, C): dy and y are zero there
-            tt[i] = __fdividef(dv[i] * yv[i], sc[i]);  // MUFU reciprocal (2 ulp)
+            tt[i] = dv[i] * yv[i] * rcp_pos(sc[i]);  // MUFU reciprocal
         }
         float out[8];
 #pragma unroll
@@ -1099,10 +1117,132 @@ __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, co
             float s = 0.f;
 #pragma unroll
             for (int d = -HALF; d <= HALF; ++d) s += tt[8 + j + d];
-            out[j] = (g * 8 + j) < a.C ? dv[8 + j] * __powf(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
+            out[j] = (g * 8 + j) < a.C ? dv[8 + j] * pow_pos(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
             if (relu && !(xv[8 + j] > 0.f)) out[j] = 0.f;  // folded ReLU backward: x is the ReLU output
         }
         st8(dx + base + g * 8, out);
+    }
+}
+
+// ---------------------------------------------------------------- LRN v3: pixel-aligned warps
+// ng = cs/8 <= 32 lanes own one pixel's channel chunks (32/ng pixels per warp, the spare lanes
+// idle); every lane loads only its own 8 channels and takes the HALF channels either side from
+// the neighbouring lanes with shuffles (zero at the pixel's first / last chunk).  Compared with
+// v2 this drops the neighbour loads and, in the backward, the 1.5x-redundant scale / t terms of
+// the window margin (each lane computes them for its own channels only).  Same arithmetic and
+// summation order as v2.
+struct LrnLanes {
+    int ng, ppw;
+    long long pix;
+    bool active;
+    int g;
+};
+__device__ __forceinline__ LrnLanes lrn_lanes(const Act4& a, long long warp, int lane) {
+    LrnLanes r;
+    r.ng = a.cs / 8;
+    r.ppw = 32 / r.ng;
+    const int pl = lane / r.ng;
+    r.g = lane - pl * r.ng;
+    r.pix = warp * r.ppw + pl;
+    r.active = pl < r.ppw && r.pix < a.pixels();
+    return r;
+}
+// w[HALF + j] = v[j]; w[0..HALF) from the previous chunk, w[HALF+8..) from the next one
+template <int HALF>
+__device__ __forceinline__ void lrn_window(const float (&v)[8], int g, int ng, float (&w)[8 + 2 * HALF]) {
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) {
+        const float l = __shfl_up_sync(0xffffffffu, v[8 - HALF + i], 1);
+        const float r = __shfl_down_sync(0xffffffffu, v[i], 1);
+        w[i] = g > 0 ? l : 0.f;
+        w[HALF + 8 + i] = g + 1 < ng ? r : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[HALF + j] = v[j];
+}
+
+template <int HALF, typename T>
+__global__ void k_lrn3_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, float alpha, float beta, float kk) {
+    pdl_wait();
+    pdl_trigger();
+    const float an = alpha / static_cast<float>(2 * HALF + 1);
+    const int lane = threadIdx.x & 31;
+    const long long nw = (a.pixels() + 32 / (a.cs / 8) - 1) / (32 / (a.cs / 8));
+    for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < nw;
+         w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+        const LrnLanes L = lrn_lanes(a, w, lane);
+        const long long o = L.pix * a.cs + L.g * 8;
+        float xv[8], q[8];
+        if (L.active)
+            ld8(x + o, xv);
+        else
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xv[j] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = xv[j] * xv[j];
+        float qw[8 + 2 * HALF];
+        lrn_window<HALF>(q, L.g, L.ng, qw);
+        float out[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * HALF; ++d) s += qw[j + d];
+            // pad channels (>= C) hold x = 0, so the product is already zero there
+            out[j] = xv[j] * pow_pos(kk + an * s, -beta);
+        }
+        if (L.active) st8(y + o, out);
+    }
+}
+
+template <int HALF, typename T>
+__global__ void k_lrn3_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
+                           T* __restrict__ dx, Act4 a, float alpha, float beta, float kk, int relu) {
+    pdl_wait();
+    pdl_trigger();
+    const float an = alpha / static_cast<float>(2 * HALF + 1);
+    const float coef = 2.f * alpha * beta / static_cast<float>(2 * HALF + 1);
+    const int lane = threadIdx.x & 31;
+    const long long nw = (a.pixels() + 32 / (a.cs / 8) - 1) / (32 / (a.cs / 8));
+    for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < nw;
+         w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+        const LrnLanes L = lrn_lanes(a, w, lane);
+        const long long o = L.pix * a.cs + L.g * 8;
+        float xv[8], dv[8], yv[8];
+        if (L.active) {
+            ld8(x + o, xv);
+            ld8(dy + o, dv);
+            ld8(y + o, yv);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xv[j] = dv[j] = yv[j] = 0.f;
+        }
+        float q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = xv[j] * xv[j];
+        float qw[8 + 2 * HALF];
+        lrn_window<HALF>(q, L.g, L.ng, qw);
+        float sc[8], tt[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * HALF; ++d) s += qw[j + d];
+            sc[j] = kk + an * s;
+            tt[j] = dv[j] * yv[j] * rcp_pos(sc[j]);  // zero outside [0, C): dy and y are zero there
+        }
+        float tw[8 + 2 * HALF];
+        lrn_window<HALF>(tt, L.g, L.ng, tw);
+        float out[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float s = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * HALF; ++d) s += tw[j + d];
+            out[j] = dv[j] * pow_pos(sc[j], -beta) - coef * xv[j] * s;  // zero on pad channels (dy = x = 0)
+            if (relu && !(xv[j] > 0.f)) out[j] = 0.f;  // folded ReLU backward: x is the ReLU output
+        }
+        if (L.active) st8(dx + o, out);
     }
 }
 
@@ -1473,9 +1613,35 @@ tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+// TCB_LRN3: 0 = v2 (neighbour-load) kernels only, 1 (default) = v3 backward where lanes tile
+// pixels exactly, 2 = v3 everywhere (A/B switch).
+int lrn3_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("TCB_LRN3");
+        return e ? std::atoi(e) : 1;
+    }();
+    return m;
+}
 template <typename T>
 tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float beta, float k, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
+    // measured (AlexNet b128): the v3 forward is no faster than v2 for 32 % ng == 0 and 16% slower
+    // with idle lanes, so it is opt-in (TCB_LRN3=2)
+    if (a.cs / 8 <= 32 && lrn3_mode() == 2) {
+        const long long threads = (a.pixels() + 32 / (a.cs / 8) - 1) / (32 / (a.cs / 8)) * 32;
+        bool done = true;
+        switch (size) {
+            case 3: TCB_LAUNCH((k_lrn3_fwd<1, T>), EW_GRID(threads), x, y, a, alpha, beta, k); break;
+            case 5: TCB_LAUNCH((k_lrn3_fwd<2, T>), EW_GRID(threads), x, y, a, alpha, beta, k); break;
+            case 7: TCB_LAUNCH((k_lrn3_fwd<3, T>), EW_GRID(threads), x, y, a, alpha, beta, k); break;
+            case 9: TCB_LAUNCH((k_lrn3_fwd<4, T>), EW_GRID(threads), x, y, a, alpha, beta, k); break;
+            default: done = false;
+        }
+        if (done) {
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+    }
     switch (size) {  // odd windows up to 9: register-resident template kernels
         case 3: TCB_LAUNCH((k_lrn2_fwd<1, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
         case 5: TCB_LAUNCH((k_lrn2_fwd<2, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
@@ -1494,6 +1660,22 @@ template <typename T>
 tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int size, float alpha, float beta,
                          float k, int relu, cudaStream_t st) {
     const long long n = a.pixels() * (a.cs / 8);
+    // v3 backward when the pixel's chunks tile the warp exactly (no idle lanes): -7% vs v2 at C=256
+    if (a.cs / 8 <= 32 && (lrn3_mode() == 2 || (lrn3_mode() == 1 && 32 % (a.cs / 8) == 0))) {
+        const long long threads = (a.pixels() + 32 / (a.cs / 8) - 1) / (32 / (a.cs / 8)) * 32;
+        bool done = true;
+        switch (size) {
+            case 3: TCB_LAUNCH((k_lrn3_bwd<1, T>), EW_GRID(threads), dy, x, y, dx, a, alpha, beta, k, relu); break;
+            case 5: TCB_LAUNCH((k_lrn3_bwd<2, T>), EW_GRID(threads), dy, x, y, dx, a, alpha, beta, k, relu); break;
+            case 7: TCB_LAUNCH((k_lrn3_bwd<3, T>), EW_GRID(threads), dy, x, y, dx, a, alpha, beta, k, relu); break;
+            case 9: TCB_LAUNCH((k_lrn3_bwd<4, T>), EW_GRID(threads), dy, x, y, dx, a, alpha, beta, k, relu); break;
+            default: done = false;
+        }
+        if (done) {
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+    }
     switch (size) {
         case 3: TCB_LAUNCH((k_lrn2_bwd<1, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
         case 5: TCB_LAUNCH((k_lrn2_bwd<2, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
