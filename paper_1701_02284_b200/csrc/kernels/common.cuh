@@ -47,6 +47,11 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint6
 // init, TMEM allocation, tensor-map prefetch) overlap the tail of its predecessor.
 // Off by default (TCB_PDL=1 enables the attribute; see pdl_enabled()).
 bool pdl_enabled();
+// Timing ablation (diagnostics only, results are wrong): TCB_ABLATE is a bit mask of kernel
+// classes whose launches are skipped, so the step-time delta is that class's in-graph cost.
+//   1 channel-reduction finals, 2 channel reductions, 4 BN forward apply, 8 BN backward apply,
+//   16 residual add, 32 ReLU backward, 64 split-K reduce, 128 channel copy (concat)
+bool ablate(int bit);
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -64,6 +69,26 @@ inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+// Same, launched as thread-block clusters of `cluster` CTAs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                         dim3 cluster, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster.x;
+    attr[1].val.clusterDim.y = cluster.y;
+    attr[1].val.clusterDim.z = cluster.z;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 #define TCB_LAUNCH(kernel, ...) ::tcb::launch_kernel(kernel, __VA_ARGS__)  // (kernel, grid, block, smem, stream, args...)

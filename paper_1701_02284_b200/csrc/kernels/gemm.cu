@@ -23,6 +23,14 @@ bool pdl_enabled() {
     return on;
 }
 
+bool ablate(int bit) {
+    static const int mask = [] {
+        const char* e = std::getenv("TCB_ABLATE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return (mask & bit) != 0;
+}
+
 int num_sms() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -348,7 +356,8 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (partial) {
         const long long total = static_cast<long long>(p.M) * p.N;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
-        TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
+        if (!ablate(64))
+            TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
                                                      static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
                                                      relu, beta);
         TCB_LAUNCH_CHECK();

@@ -659,33 +659,45 @@ __global__ void __launch_bounds__(256) k_loss(LossArgs args, float* out, double*
 // Deterministic for a fixed shape (the partition depends only on rows / ld).
 //   RED_SUM   a = sum x
 //   RED_STATS a = sum (x - x0), b = sum (x - x0)^2   (x0 = row 0: shifted single pass)
-//   RED_BNBWD a = sum dy,       b = sum dy * (x - mean) * istd
+//   RED_BNBWD a = sum dy,       b = sum dy * (x - mean)   (x istd in the final stage)
 enum RedMode { RED_SUM = 0, RED_STATS = 1, RED_BNBWD = 2 };
 constexpr int kRedThreads = 256;
+
+// Blocks of one channel tile are grouped in clusters of kRedCluster along the split axis; the
+// cluster combines its blocks' sums through distributed shared memory and writes ONE partial,
+// so the final kernel reads 4x fewer partials (it is latency-bound on them).
+constexpr int kRedCluster = 4;
+constexpr int kRedBlocksPerSm = 3;  // __launch_bounds__ minimum: <= 85 registers per thread
 
 struct RedPlan {
     int ct;        // channels per tile (multiple of 8, <= 512)
     int tiles;     // channel tiles
-    int splits;    // row splits
+    int splits;    // row splits (blocks along y, a multiple of kRedCluster)
+    int parts;     // partials per channel = splits / kRedCluster
     long long rps; // rows per split
 };
 
-RedPlan red_plan(long long rows, int ld) {
+// max_clusters: co-resident clusters of the kernel (cudaOccupancyMaxActiveClusters); clusters
+// are placed per GPC, so the one-wave block count is max_clusters * kRedCluster, which is below
+// SMs * blocks-per-SM (a second partial wave costs ~40% of the kernel).
+RedPlan red_plan(long long rows, int ld, int max_clusters) {
     RedPlan r;
     r.ct = std::min(ld, 512);
     r.tiles = (ld + r.ct - 1) / r.ct;
     const int rpi = kRedThreads / (r.ct / 8);
-    const long long target = static_cast<long long>(num_sms()) * 4;
-    long long sp = std::max<long long>(1, target / r.tiles);
+    const long long target = static_cast<long long>(max_clusters) * kRedCluster;  // one wave
+    long long sp = std::max<long long>(1, target / r.tiles / kRedCluster * kRedCluster);
     sp = std::min<long long>(sp, std::max<long long>(1, rows / (8LL * rpi)));  // >= 8 rows per thread
     sp = std::min<long long>(sp, 1024);
     r.rps = (rows + sp - 1) / sp;
-    r.splits = static_cast<int>((rows + r.rps - 1) / r.rps);
+    const int used = static_cast<int>((rows + r.rps - 1) / r.rps);
+    r.splits = (used + kRedCluster - 1) / kRedCluster * kRedCluster;  // trailing blocks see no rows
+    r.parts = r.splits / kRedCluster;
     return r;
 }
 
 template <int MODE, typename T>
-__global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const T* __restrict__ x, const T* __restrict__ x2,
+__global__ void __launch_bounds__(kRedThreads, kRedBlocksPerSm) k_chan_reduce(const T* __restrict__ x, const T* __restrict__ x2,
                                                              const float* __restrict__ stats, long long rows, int C,
                                                              int ld, int ct, long long rps, int splits,
                                                              float* __restrict__ part) {
@@ -696,25 +708,21 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const T* __restrict
     const int rpi = kRedThreads / tpr;
     const int tr = threadIdx.x / tpr, tc = threadIdx.x - tr * tpr;
     const int c0 = blockIdx.x * ct + tc * 8;
-    float a[8], b[8], m[8], is[8];
+    float a[8], b[8], m[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a[j] = b[j] = m[j] = is[j] = 0.f;
+    for (int j = 0; j < 8; ++j) a[j] = b[j] = m[j] = 0.f;
     const bool live = tr < rpi && c0 < ld;
     if (live) {
         if (MODE == RED_STATS) {
             ld8(x + c0, m);
         } else if (MODE == RED_BNBWD) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int c = min(c0 + j, C - 1);
-                m[j] = stats[c];
-                is[j] = stats[C + c];
-            }
+            for (int j = 0; j < 8; ++j) m[j] = stats[min(c0 + j, C - 1)];
         }
         const long long r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
         const T* px = x + r0 * ld + c0;
         const T* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
-        constexpr int U = 4;  // rows in flight per thread
+        constexpr int U = (MODE == RED_BNBWD ? 4 : 8) * 2 / static_cast<int>(sizeof(T));  // 64 B / tensor in flight
         for (long long rb = tr; r0 + rb < r1; rb += U * rpi) {
             Raw8<T> q[U], q2[U];
 #pragma unroll
@@ -745,35 +753,72 @@ __global__ void __launch_bounds__(kRedThreads) k_chan_reduce(const T* __restrict
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         a[j] += f[j];
-                        b[j] = fmaf(f[j], (g[j] - m[j]) * is[j], b[j]);
+                        b[j] = fmaf(f[j], g[j] - m[j], b[j]);  // x istd applied in the final stage
                     }
                 }
             }
         }
     }
     // row-slot tr, channel offset tc*8 within the tile: sm[tr][ct]
+    constexpr int NB = MODE == RED_SUM ? 1 : 2;
+    auto put = [&](int slot, const float (&v)[8], int which) {
+        float4* d = reinterpret_cast<float4*>(sm + which * kRedThreads * 8 + slot * ct + tc * 8);
+        d[0] = make_float4(v[0], v[1], v[2], v[3]);
+        d[1] = make_float4(v[4], v[5], v[6], v[7]);
+    };
     if (tr < rpi) {
-        float4* d = reinterpret_cast<float4*>(sm + tr * ct + tc * 8);
-        d[0] = make_float4(a[0], a[1], a[2], a[3]);
-        d[1] = make_float4(a[4], a[5], a[6], a[7]);
-        if (MODE != RED_SUM) {
-            float4* e = reinterpret_cast<float4*>(sm + kRedThreads * 8 + tr * ct + tc * 8);
-            e[0] = make_float4(b[0], b[1], b[2], b[3]);
-            e[1] = make_float4(b[4], b[5], b[6], b[7]);
-        }
+        put(tr, a, 0);
+        if (NB == 2) put(tr, b, 1);
     }
     __syncthreads();
-    for (int cc = threadIdx.x; cc < ct; cc += kRedThreads) {
-        const int c = blockIdx.x * ct + cc;
-        if (c >= C) continue;
-        float sa = 0.f, sb = 0.f;
-        for (int q = 0; q < rpi; ++q) {
-            sa += sm[q * ct + cc];
-            if (MODE != RED_SUM) sb += sm[kRedThreads * 8 + q * ct + cc];
+    // fixed pairwise tree over the row slots (deterministic for a given shape)
+    int span = 1;
+    while (span < rpi) span <<= 1;
+    for (int h = span >> 1; h > 0; h >>= 1) {
+        if (tr < h && tr + h < rpi) {
+#pragma unroll
+            for (int w = 0; w < NB; ++w) {
+                float4* d = reinterpret_cast<float4*>(sm + w * kRedThreads * 8 + tr * ct + tc * 8);
+                const float4* e = reinterpret_cast<const float4*>(sm + w * kRedThreads * 8 + (tr + h) * ct + tc * 8);
+                const float4 d0 = d[0], d1 = d[1], e0 = e[0], e1 = e[1];
+                d[0] = make_float4(d0.x + e0.x, d0.y + e0.y, d0.z + e0.z, d0.w + e0.w);
+                d[1] = make_float4(d1.x + e1.x, d1.y + e1.y, d1.z + e1.z, d1.w + e1.w);
+            }
         }
-        part[static_cast<long long>(blockIdx.y) * C + c] = sa;
-        if (MODE != RED_SUM) part[static_cast<long long>(splits + blockIdx.y) * C + c] = sb;
+        __syncthreads();
     }
+    // cluster combine: rank 0 sums the kRedCluster blocks' slot-0 rows in rank order
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank == 0) {
+        const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        for (int cc = threadIdx.x; cc < ct; cc += kRedThreads) {
+            const int c = blockIdx.x * ct + cc;
+            if (c >= C) continue;
+            float sa = 0.f, sb = 0.f;
+#pragma unroll
+            for (int r = 0; r < kRedCluster; ++r) {
+                uint32_t ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + cc * 4), "r"(r));
+                float va, vb = 0.f;
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(va) : "r"(ra));
+                if (NB == 2) {
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                 : "=r"(rb)
+                                 : "r"(base + (kRedThreads * 8 + cc) * 4), "r"(r));
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(vb) : "r"(rb));
+                }
+                sa += va;
+                sb += vb;
+            }
+            const int q = blockIdx.y / kRedCluster;
+            part[static_cast<long long>(q) * C + c] = sa;
+            if (MODE != RED_SUM) part[static_cast<long long>(splits / kRedCluster + q) * C + c] = sb;
+        }
+    }
+    // keep every block's shared memory alive until rank 0 has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Stage 2.  RED_SUM: out[c] = scale * sum.  RED_STATS: stats = (mean, istd), coef =
@@ -794,6 +839,7 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
     const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (c >= C) return;
     float sa = 0.f, sb = 0.f;
+#pragma unroll 4
     for (int q = lane; q < splits; q += 32) {
         sa += part[static_cast<long long>(q) * C + c];
         if (MODE != RED_SUM) sb += part[static_cast<long long>(splits + q) * C + c];
@@ -818,6 +864,7 @@ __global__ void __launch_bounds__(256) k_chan_final(const float* __restrict__ pa
         coef[c] = g;
         coef[C + c] = beta[c] - mean * g;
     } else {
+        sb *= beta[C + c];  // sum dy*(x - mean) -> sum dy*xhat
         out[c] = sa;
         out[C + c] = sb;
         if (gamma) {
@@ -1519,13 +1566,15 @@ tc_status launch_relu_fwd(const T* x, T* y, long long n, cudaStream_t st) {
 }
 template <typename T>
 tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStream_t st) {
-    TCB_LAUNCH(k_relu_bwd<T>, EW_GRID(n / 8), dy, y, dx, n / 8);
+    if (!ablate(32))
+        TCB_LAUNCH(k_relu_bwd<T>, EW_GRID(n / 8), dy, y, dx, n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 template <typename T>
 tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st) {
-    TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
+    if (!ablate(16))
+        TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1751,11 +1800,30 @@ static tc_status chan_reduce(const T* x, const T* x2, const float* stats, long l
                              float* part, int max_partials, cudaStream_t st, RedPlan* out_plan) {
     if ((ld & 7) || (reinterpret_cast<uintptr_t>(x) & 15) || (x2 && (reinterpret_cast<uintptr_t>(x2) & 15)))
         return fail(TC_INVALID_ARG, "channel reduction: misaligned operand");
-    RedPlan rp = red_plan(rows, static_cast<int>(ld));
-    if (2ll * rp.splits * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
+    static const int max_clusters = [] {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(1, kRedCluster * 64);
+        cfg.blockDim = dim3(kRedThreads);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = kRedCluster;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_chan_reduce<MODE, T>, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = num_sms() * kRedBlocksPerSm / kRedCluster * 7 / 8;
+        }
+        return n;
+    }();
+    RedPlan rp = red_plan(rows, static_cast<int>(ld), max_clusters);
+    if (2ll * rp.parts * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
     dim3 grid(rp.tiles, rp.splits);
-    TCB_LAUNCH((k_chan_reduce<MODE, T>), grid, kRedThreads, 0, st, x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps,
-                                                      rp.splits, part);
+    if (!ablate(2))
+        TCB_CUDA_CHECK(launch_kernel_cluster((k_chan_reduce<MODE, T>), grid, dim3(kRedThreads), 0, st, dim3(1, kRedCluster, 1),
+                                         x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps, rp.splits, part));
     TCB_LAUNCH_CHECK();
     *out_plan = rp;
     return TC_OK;
@@ -1767,7 +1835,8 @@ tc_status launch_colsum(const T* x, long long rows, int cols, long long ld, floa
     RedPlan rp;
     tc_status s = chan_reduce<RED_SUM, T>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_SUM, T>), (cols + 7) / 8, 256, 0, st, partials, rp.splits, cols, 1.f, out,
+    if (!ablate(1))
+        TCB_LAUNCH((k_chan_final<RED_SUM, T>), (cols + 7) / 8, 256, 0, st, partials, rp.parts, cols, 1.f, out,
                static_cast<const T*>(nullptr), rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
@@ -1784,7 +1853,8 @@ template <typename T>
 tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st) {
     if ((src_cs | dst_cs | off | c) % 8 == 0 && (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0) {
-        TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
+        if (!ablate(128))
+            TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
         TCB_LAUNCH_CHECK();
         return TC_OK;
     }
@@ -1804,11 +1874,13 @@ tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y,
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS, T>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_STATS, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C, 1.f, stats, x, pixels, eps, gamma,
+    if (!ablate(1))
+        TCB_LAUNCH((k_chan_final<RED_STATS, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu);
+    if (!ablate(4))
+        TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1819,7 +1891,8 @@ tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* gamma, cons
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD, T>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.splits, C,
+    if (!ablate(1))
+        TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C,
                1.f / static_cast<float>(pixels), sums, static_cast<const T*>(nullptr), pixels, 0.f, gamma, stats,
                static_cast<float*>(nullptr));
     TCB_LAUNCH_CHECK();
@@ -1830,7 +1903,8 @@ template <typename T>
 tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, long long pixels, int C, int cs,
                               cudaStream_t st) {
     const long long n8 = pixels * cs / 8;
-    TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
+    if (!ablate(8))
+        TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
