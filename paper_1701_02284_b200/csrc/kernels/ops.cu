@@ -667,7 +667,13 @@ constexpr int kRedThreads = 256;
 // cluster combines its blocks' sums through distributed shared memory and writes ONE partial,
 // so the final kernel reads 4x fewer partials (it is latency-bound on them).
 constexpr int kRedCluster = 4;
-constexpr int kRedBlocksPerSm = 3;  // __launch_bounds__ minimum: <= 85 registers per thread
+#ifndef TCB_RED_BPS
+#define TCB_RED_BPS 3
+#endif
+#ifndef TCB_RED_U
+#define TCB_RED_U 8
+#endif
+constexpr int kRedBlocksPerSm = TCB_RED_BPS;  // __launch_bounds__ minimum: <= 85 registers per thread
 
 struct RedPlan {
     int ct;        // channels per tile (multiple of 8, <= 512)
@@ -722,7 +728,7 @@ __global__ void __launch_bounds__(kRedThreads, kRedBlocksPerSm) k_chan_reduce(co
         const long long r0 = blockIdx.y * rps, r1 = min(rows, r0 + rps);
         const T* px = x + r0 * ld + c0;
         const T* p2 = MODE == RED_BNBWD ? x2 + r0 * ld + c0 : nullptr;
-        constexpr int U = (MODE == RED_BNBWD ? 4 : 8) * 2 / static_cast<int>(sizeof(T));  // 64 B / tensor in flight
+        constexpr int U = (MODE == RED_BNBWD ? TCB_RED_U / 2 : TCB_RED_U) * 2 / static_cast<int>(sizeof(T));  // 64 B / tensor in flight
         for (long long rb = tr; r0 + rb < r1; rb += U * rpi) {
             Raw8<T> q[U], q2[U];
 #pragma unroll
@@ -893,14 +899,17 @@ __device__ __forceinline__ void ld_coef8(const float* __restrict__ a, int c0, in
 // y = x * coef[c] + coef[C + c] over 8 channels per thread; pad channels -> 0.
 template <typename T>
 __global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__ coef, T* __restrict__ y,
-                              long long n8, int ld8, int C, int relu) {
+                              long long n8, int ld8, int C, int relu, const T* __restrict__ res) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
-        Raw8<T> q[2];
+        Raw8<T> q[2], rq[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) q[u] = i0 + u * S < n8 ? ld_raw8cs(x + (i0 + u * S) * 8) : raw8_zero<T>();
+        for (int u = 0; u < 2; ++u) {
+            q[u] = i0 + u * S < n8 ? ld_raw8cs(x + (i0 + u * S) * 8) : raw8_zero<T>();
+            if (res) rq[u] = i0 + u * S < n8 ? ld_raw8cs(res + (i0 + u * S) * 8) : raw8_zero<T>();
+        }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const long long i = i0 + u * S;
@@ -910,9 +919,20 @@ __global__ void k_chan_affine(const T* __restrict__ x, const float* __restrict__
             unpack_raw(q[u], f);
             ld_coef8(coef, c0, C, a);
             ld_coef8(coef + C, c0, C, b);
+            if (res) {
+                // folded residual add: the BN output is rounded to the storage type first, exactly
+                // as the separate add would have read it
+                float r[8];
+                unpack_raw(rq[u], r);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = to_f(from_f<T>(fmaf(f[j], a[j], b[j]))) + r[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = fmaf(f[j], a[j], b[j]);
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                f[j] = c0 + j < C ? fmaf(f[j], a[j], b[j]) : 0.f;
+                f[j] = c0 + j < C ? f[j] : 0.f;
                 if (relu) f[j] = fmaxf(f[j], 0.f);
             }
             st8(y + i * 8, f);
@@ -1869,7 +1889,7 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st) {
 
 template <typename T>
 tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y, float* stats, long long pixels, int C,
-                        int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st) {
+                        int cs, float eps, int relu, const T* res, float* partials, int max_partials, cudaStream_t st) {
     RedPlan rp;
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS, T>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
@@ -1880,7 +1900,7 @@ tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y,
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
     if (!ablate(4))
-        TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu);
+        TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu, res);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1993,7 +2013,7 @@ template tc_status launch_softmax_bwd<bf16>(const float*, const float*, bf16*, l
 template tc_status launch_colsum<bf16>(const bf16*, long long, int, long long, float*, float*, int, cudaStream_t);
 template tc_status launch_bias_add<bf16>(const bf16*, const float*, bf16*, long long, int, long long, int, cudaStream_t);
 template tc_status launch_channel_copy<bf16>(const bf16*, int, bf16*, int, int, int, long long, cudaStream_t);
-template tc_status launch_bn_fwd<bf16>(const bf16*, const float*, const float*, bf16*, float*, long long, int, int, float, int,
+template tc_status launch_bn_fwd<bf16>(const bf16*, const float*, const float*, bf16*, float*, long long, int, int, float, int, const bf16*,
                                      float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const float*, const float*, float*, long long,
                                             int, int, float*, int, cudaStream_t);
@@ -2016,7 +2036,7 @@ template tc_status launch_softmax_bwd<float>(const float*, const float*, float*,
 template tc_status launch_colsum<float>(const float*, long long, int, long long, float*, float*, int, cudaStream_t);
 template tc_status launch_bias_add<float>(const float*, const float*, float*, long long, int, long long, int, cudaStream_t);
 template tc_status launch_channel_copy<float>(const float*, int, float*, int, int, int, long long, cudaStream_t);
-template tc_status launch_bn_fwd<float>(const float*, const float*, const float*, float*, float*, long long, int, int, float, int,
+template tc_status launch_bn_fwd<float>(const float*, const float*, const float*, float*, float*, long long, int, int, float, int, const float*,
                                      float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const float*, const float*, float*, long long,
                                             int, int, float*, int, cudaStream_t);

@@ -93,8 +93,9 @@ tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 // in-place ReLU that follows a BN is folded into the apply pass).
 // `partials` holds max_partials floats of reduction scratch plus 3*C coefficient floats.
 template <typename T>
+// res (may be null): a residual added to the (storage-rounded) BN output before the optional ReLU
 tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y, float* stats, long long pixels, int C,
-                        int cs, float eps, int relu, float* partials, int max_partials, cudaStream_t st);
+                        int cs, float eps, int relu, const T* res, float* partials, int max_partials, cudaStream_t st);
 // sums[0..2C) = (sum dy, sum dy * xhat) — shared by dgamma (= sum dy*xhat), dbeta (= sum dy) —
 // and sums[2C..5C) = the data-gradient coefficients (k1, k2, k3) from gamma and the forward stats
 template <typename T>

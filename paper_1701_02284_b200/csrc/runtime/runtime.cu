@@ -118,6 +118,7 @@ struct tc_ctx {
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
     std::vector<int> fuse_bias_param;
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
+    std::vector<int> fuse_add_res, fuse_add_out;    // BN forward: folded residual add (other operand, output var)
     std::vector<char> pool_flag_nonpos;             // max-pool forward: flag windows with max <= 0 in the index
     std::vector<char> pool_mask_in_idx;             // max-pool backward: its folded ReLU mask is in the index
 
@@ -371,6 +372,8 @@ void plan_fusion(tc_ctx* c) {
     c->fuse_bias_param.assign(p->nstmts, -1);
     c->fuse_mask_var.assign(p->nstmts, -1);
     c->pool_flag_nonpos.assign(p->nstmts, 0);
+    c->fuse_add_res.assign(p->nstmts, -1);
+    c->fuse_add_out.assign(p->nstmts, -1);
     c->pool_mask_in_idx.assign(p->nstmts, 0);
     auto next_let = [&](int i) {
         for (int j = i + 1; j < p->nstmts; ++j) {
@@ -453,6 +456,38 @@ void plan_fusion(tc_ctx* c) {
             c->fuse_relu[i] = 1;
             c->fused[j] = 1;
         }
+    }
+    // BatchNorm followed by the residual add that is its only reader (ResNet's y = relu(BN(x) + r)):
+    // the BN apply pass reads r and writes the add's output (and its folded ReLU), saving the
+    // write + re-read of the BN output.  Not in keep mode, where every var is materialised.
+    static const bool bn_add = [] {
+        const char* e = std::getenv("TCB_BN_ADD_FOLD");
+        return !(e && e[0] == '0');
+    }();
+    for (int i = 0; bn_add && !c->desc.keep && i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind != TC_STMT_LET || s.op != TC_OP_BN_FWD || c->fused[i] || c->fuse_relu[i]) continue;
+        const int j = next_let(i);
+        if (j < 0 || c->fused[j]) continue;
+        const tc_stmt& a = p->stmts[j];
+        if (a.op != TC_OP_ADD || a.nin != 2 || a.in[0].kind != TC_REF_VAR || a.in[1].kind != TC_REF_VAR) continue;
+        const int k = a.in[0].index == s.var ? 1 : a.in[1].index == s.var ? 0 : -1;
+        if (k < 0 || a.in[k].index == s.var) continue;
+        int readers = 0;
+        for (int q = 0; q < p->nstmts; ++q)
+            for (int r = 0; p->stmts[q].kind != TC_STMT_DEALLOC && r < p->stmts[q].nin; ++r)
+                readers += p->stmts[q].in[r].kind == TC_REF_VAR && p->stmts[q].in[r].index == s.var;
+        if (readers != 1) continue;
+        const VarL& y = c->vars.at(s.var);
+        const VarL& r = c->vars.at(a.in[k].index);
+        const VarL& o = c->vars.at(a.var);
+        if (r.dtype != y.dtype || o.dtype != y.dtype || r.cs != y.cs || o.cs != y.cs || r.elems() != y.elems() ||
+            o.elems() != y.elems())
+            continue;
+        c->fuse_add_res[i] = a.in[k].index;
+        c->fuse_add_out[i] = a.var;
+        c->fuse_relu[i] = c->fuse_relu[j];
+        c->fused[j] = 1;
     }
 }
 
@@ -1145,10 +1180,14 @@ tc_status exec_let(tc_ctx* c, int i) {
         case TC_OP_BN_FWD: {
             const VarL& x = P.L(s.in[0]);
             float* stats = reinterpret_cast<float*>(c->arena + c->items[c->bn_stats_item.at(x.id)].off);
+            const bool add = c->fuse_add_res[i] >= 0;  // folded residual add (its output var is written)
             return launch_bn_fwd(reinterpret_cast<const T*>(P.var(x.id)), c->params[s.in[1].index].p,
-                                 c->params[s.in[2].index].p, reinterpret_cast<T*>(y), stats,
+                                 c->params[s.in[2].index].p,
+                                 reinterpret_cast<T*>(add ? P.var(c->fuse_add_out[i]) : y), stats,
                                  static_cast<long long>(x.N) * x.H * x.W, x.C, x.cs, static_cast<float>(s.eps),
-                                 c->fuse_relu[i], c->partials, c->max_partials, st);
+                                 c->fuse_relu[i],
+                                 add ? reinterpret_cast<const T*>(P.var(c->fuse_add_res[i])) : static_cast<const T*>(nullptr),
+                                 c->partials, c->max_partials, st);
         }
         case TC_OP_BN_BWD_DATA: {
             const VarL& up = P.L(s.in[0]);
