@@ -282,13 +282,13 @@ static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes
     return best;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int SK = 0>
 static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
-    const int smem = TileCfg<BN, CG>::kSmemBytes;
+    const int smem = TileCfg<BN, CG, SK>::kSmemBytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (attr_err != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(attr_err));
     const int grid = std::min(units, num_sms() / CG) * CG;
@@ -309,7 +309,7 @@ static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG>, p);
+    cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CG, SK>, p);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

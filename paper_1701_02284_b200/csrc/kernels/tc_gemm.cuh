@@ -94,14 +94,19 @@ constexpr int kStagingBytes = 4096;  // per epilogue warp per buffer: 32 rows x 
 
 // CG = 2: CTA pair (cta_group::2).  The pair computes a (2*BM) x BN tile: each CTA holds
 // its BM rows of A and BN/2 rows (columns of D) of B; the leader issues the MMAs.
-template <int BN, int CG = 1>
+// SK = 1 (short-K): half the operand ring and 4x the epilogue staging (4 buffers per epilogue
+// warp).  Measured neutral-to-slower on the short-K contractions of the configs (the store
+// issue rate was not the limit once the accumulator release stopped fencing at GPU scope), so
+// no launch path instantiates it; kept for experiments (launch_bn<BN, 1, 1>).
+template <int BN, int CG = 1, int SK = 0>
 struct TileCfg {
     static constexpr int kBNL = BN / CG;  // B rows held by one CTA
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = kBNL * BK * 2;
-    static constexpr int kStages = (196608 / (kABytes + kBBytes)) > 8 ? 8 : (196608 / (kABytes + kBBytes));
+    static constexpr int kRing = SK ? 98304 : 196608;
+    static constexpr int kStages = (kRing / (kABytes + kBBytes)) > 8 ? 8 : (kRing / (kABytes + kBBytes));
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStagingTotal = 4 * 2 * kStagingBytes;
+    static constexpr int kStagingTotal = (SK ? 32 : 8) * kStagingBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kStagingTotal + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
     static constexpr int kLag = kStages - 2;                             // cp.async groups in flight
@@ -398,9 +403,9 @@ __device__ __forceinline__ void col_gather4_issue(const GemmParams& p, const Col
     }
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int SK>
 __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_constant__ GemmParams p) {
-    using Cfg = TileCfg<BN, CG>;
+    using Cfg = TileCfg<BN, CG, SK>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -670,12 +675,21 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         const int ew = warp - 4;
         const int quarter = ew & 3, grp = ew >> 2;
         const int ngrp = any_gather ? 1 : 2;
-        const int nbuf = 2 / ngrp;
+        constexpr int kBufs8 = Cfg::kStagingTotal / kStagingBytes / 8;  // buffers per warp with 8 warps
+        const int nbuf = kBufs8 * 2 / ngrp;
         uint8_t* stage_base = sStage + ew * nbuf * kStagingBytes;
         const bool bf16_out = p.epi == EPI_BF16;
         int nstore = 0;
         int tc = 0;
-        // accumulator release goes to the leader's tempty (remote arrive from the peer CTA)
+        // accumulator release goes to the leader's tempty (remote arrive from the peer CTA).  A
+        // single CTA arrives locally: the cluster-scope release compiles to a GPU-scope MEMBAR
+        // that measured ~18% of the stall samples of short-K GEMMs.
+        auto release_accum = [&](uint32_t remote, uint64_t* local) {
+            if constexpr (CG == 2)
+                mbar_arrive_cluster(remote);
+            else
+                mbar_arrive(local);
+        };
         const uint32_t tempty_addr[2] = {CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]),
                                          CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : smem_u32(&tempty[1])};
         for (int u = pair; u < p.units; u += npairs, ++tc) {
@@ -688,7 +702,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             if (grp * 64 >= BN) {  // no chunk for this warp (BN = 64 with two groups)
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(tempty_addr[buf]);
+                if (lane == 0) release_accum(tempty_addr[buf], &tempty[buf]);
                 continue;
             }
             // One staging row = 128 B (64 bf16 or 32 fp32 columns).  The two TMEM reads of a
@@ -709,7 +723,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     // this warp's TMEM reads of the accumulator are done: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(tempty_addr[buf]);
+                    if (lane == 0) release_accum(tempty_addr[buf], &tempty[buf]);
                 }
                 uint64_t mbits = ~0ull;  // bit j: column nb + j passes the ReLU mask
                 if (p.mask) {
@@ -762,7 +776,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     // staging buffer reuse: the TMA store issued two stores ago must have read it
                     uint8_t* stg = stage_base + (nstore % nbuf) * kStagingBytes;
                     if (lane == 0 && nstore >= nbuf) {
-                        if (nbuf == 2) bulk_wait_read<1>();
+                        if (nbuf >= 8) bulk_wait_read<7>();
+                        else if (nbuf >= 4) bulk_wait_read<3>();
+                        else if (nbuf == 2) bulk_wait_read<1>();
                         else bulk_wait_read<0>();
                     }
                     __syncwarp();

@@ -859,9 +859,28 @@ tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
 }
 
 // Gradient op of an Update (or a parameter-shaped Let) into `g` (device param layout).
+// Timing ablation (diagnostics only, results are wrong): TCB_ABLATE_OPS="28,4" skips every Let
+// of those TC_OP_* codes, so the step-time delta is their in-graph cost.
+static bool ablate_op(int op) {
+    static const std::vector<int> ops = [] {
+        std::vector<int> v;
+        if (const char* e = std::getenv("TCB_ABLATE_OPS"))
+            for (const char* q = e; *q;) {
+                char* end = nullptr;
+                const long x = std::strtol(q, &end, 10);
+                if (end == q) break;
+                v.push_back(static_cast<int>(x));
+                q = *end ? end + 1 : end;
+            }
+        return v;
+    }();
+    return std::find(ops.begin(), ops.end(), op) != ops.end();
+}
+
 template <typename T>
 tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
     const tc_stmt& s = c->plan->stmts[idx];
+    if (ablate_op(s.op)) return TC_OK;
     Ptrs P{c};
     const ParamL& q = c->params[pidx];
     cudaStream_t st = c->st;
@@ -943,6 +962,7 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
 template <typename T>
 tc_status exec_let(tc_ctx* c, int i) {
     const tc_stmt& s = c->plan->stmts[i];
+    if (ablate_op(s.op)) return TC_OK;
     Ptrs P{c};
     cudaStream_t st = c->st;
     const VarL& out = c->vars.at(s.var);

@@ -55,6 +55,22 @@ def gemm_case(M, N, K):
     return ms, 2.0 * M * N * K / (ms * 1e-3) / 1e12
 
 
+def fc_case(M, N, K, a_mn, b_mn, f32_out):
+    """FC-layer GEMMs of the step: wgrad is M=out, N=in, K=batch with both operands MN-major
+    (activations stored [batch][features]) and an fp32 gradient; fwd / dgrad are K-major."""
+    A = torch.randn(K, M, device="cuda").to(torch.bfloat16) if a_mn else torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(K, N, device="cuda").to(torch.bfloat16) if b_mn else torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    D = torch.empty(M, N, device="cuda", dtype=torch.float32 if f32_out else torch.bfloat16)
+    ws = torch.empty(256 << 20, device="cuda", dtype=torch.uint8)
+    args = nat.GemmArgs(workspace=ws.data_ptr(), workspace_bytes=ws.numel(), M=M, N=N, K=K, a_layout=nat.TC_LAYOUT_MN if a_mn else nat.TC_LAYOUT_K, A=A.data_ptr(),
+                        lda=M if a_mn else K, b_layout=nat.TC_LAYOUT_MN if b_mn else nat.TC_LAYOUT_K, B=B.data_ptr(),
+                        ldb=N if b_mn else K, D=D.data_ptr(), ldd=N,
+                        d_dtype=nat.TC_DTYPE_F32 if f32_out else nat.TC_DTYPE_BF16, alpha=1.0, beta=0.0, splits=0)
+    ms = timeit(lambda: nat.check(nat.lib().tc_gemm_bf16(C.byref(args), None)))
+    byts = 2 * (M * K + N * K) + D.element_size() * M * N
+    return ms, 2.0 * M * N * K / (ms * 1e-3) / 1e12, byts / (ms * 1e-3) / 1e9
+
+
 def ceil8(v):
     return (v + 7) // 8 * 8
 
@@ -96,11 +112,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="gemm,conv")
     ap.add_argument("--net", default="alexnet,vgg16,resnet50")
+    ap.add_argument("--fc", action="store_true", help="AlexNet FC GEMMs (fwd, dgrad, fp32 wgrad)")
     ap.add_argument("--small-k", action="store_true", help="GEMM shapes of 1x1 convs (epilogue-paced)")
     ap.add_argument("--conv-as-gemm", action="store_true", help="AlexNet conv GEMM views with dense operands")
     ap.add_argument("--only", default="", help="run only conv cases whose tuple text contains this")
     args = ap.parse_args()
     print(f"TCB_FORCE_BN={os.environ.get('TCB_FORCE_BN', '')} TCB_IM2COL={os.environ.get('TCB_IM2COL', '')}")
+    if args.fc:
+        for name, M, N, K, amn, bmn, f32 in [("fc6 fwd", 128, 4096, 9216, 0, 0, 0), ("fc6 dgrad", 128, 9216, 4096, 0, 1, 0),
+                                             ("fc6 wgrad", 4096, 9216, 128, 1, 1, 1), ("fc7 fwd", 128, 4096, 4096, 0, 0, 0),
+                                             ("fc7 wgrad", 4096, 4096, 128, 1, 1, 1)]:
+            ms, tf, gbs = fc_case(M, N, K, amn, bmn, f32)
+            print(f"{name:10s} M={M} N={N} K={K}: {ms*1e3:8.1f} us  {tf:7.1f} TF/s  {gbs:7.0f} GB/s")
+        return
     if "gemm" in args.which:
         shapes = [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096), (4096, 4096, 4096)]
         if args.small_k:
