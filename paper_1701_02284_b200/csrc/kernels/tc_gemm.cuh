@@ -744,21 +744,35 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         }
                     }
                 }
+                // each optional stage is one warp-uniform branch around a fully unrolled pass (no
+                // per-element branches: the plain store path is just the pack)
+                if (p.alpha != 1.f) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    float v0 = __uint_as_float(r0[j]) * p.alpha, v1 = __uint_as_float(r1[j]) * p.alpha;
-                    if (!((mbits >> j) & 1)) v0 = 0.f;
-                    if (!((mbits >> (32 + j)) & 1)) v1 = 0.f;
-                    if (p.bias) {
-                        v0 += __shfl_sync(0xffffffffu, b0, j);
-                        v1 += __shfl_sync(0xffffffffu, b1, j);
+                    for (int j = 0; j < 32; ++j) {
+                        r0[j] = __float_as_uint(__uint_as_float(r0[j]) * p.alpha);
+                        r1[j] = __float_as_uint(__uint_as_float(r1[j]) * p.alpha);
                     }
-                    if (p.relu) {
-                        v0 = fmaxf(v0, 0.f);
-                        v1 = fmaxf(v1, 0.f);
+                }
+                if (p.mask) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (!((mbits >> j) & 1)) r0[j] = 0u;
+                        if (!((mbits >> (32 + j)) & 1)) r1[j] = 0u;
                     }
-                    r0[j] = __float_as_uint(v0);
-                    r1[j] = __float_as_uint(v1);
+                }
+                if (p.bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        r0[j] = __float_as_uint(__uint_as_float(r0[j]) + __shfl_sync(0xffffffffu, b0, j));
+                        r1[j] = __float_as_uint(__uint_as_float(r1[j]) + __shfl_sync(0xffffffffu, b1, j));
+                    }
+                }
+                if (p.relu) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        r0[j] = __float_as_uint(fmaxf(__uint_as_float(r0[j]), 0.f));
+                        r1[j] = __float_as_uint(fmaxf(__uint_as_float(r1[j]), 0.f));
+                    }
                 }
                 const int nrows = bf16_out ? 1 : 2;  // 128-byte staging rows in this chunk
                 for (int sub = 0; sub < nrows; ++sub) {
