@@ -710,8 +710,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             // are fetched one per lane meanwhile and broadcast with shuffles.
             for (int c0 = grp * 64; c0 < BN; c0 += 64 * ngrp) {
                 uint32_t r0[32], r1[32];
+#ifdef TCB_EXP_NOTMEM
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r0[j] = r1[j] = j + c0;
+#else
                 tmem_ld32(t_row + c0, r0);
                 tmem_ld32(t_row + c0 + 32, r1);
+#endif
                 const int nb = n0 + c0;
                 float b0 = 0.f, b1 = 0.f;
                 if (p.bias) {
@@ -804,7 +809,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
+#ifndef TCB_EXP_NOSTORE
                         tma_store_3d(&p.tmD, stg, nb + sub * 32, m0 + quarter * 32, w.sp);
+#endif
                         bulk_commit();
                     }
                     ++nstore;

@@ -112,6 +112,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="gemm,conv")
     ap.add_argument("--net", default="alexnet,vgg16,resnet50")
+    ap.add_argument("--shapes", default="", help="explicit GEMM shapes MxNxK,MxNxK (bf16 out, K-major)")
     ap.add_argument("--fc", action="store_true", help="AlexNet FC GEMMs (fwd, dgrad, fp32 wgrad)")
     ap.add_argument("--small-k", action="store_true", help="GEMM shapes of 1x1 convs (epilogue-paced)")
     ap.add_argument("--conv-as-gemm", action="store_true", help="AlexNet conv GEMM views with dense operands")
@@ -129,6 +130,8 @@ def main():
         shapes = [(8192, 8192, 8192), (16384, 256, 4096), (16384, 128, 4096), (16384, 64, 4096), (4096, 4096, 4096)]
         if args.small_k:
             shapes = [(200704, 256, k) for k in (64, 128, 256, 512, 1024)] + [(200704, 64, 256), (50176, 1024, 256)]
+        if args.shapes:
+            shapes = [tuple(int(v) for v in t.split("x")) for t in args.shapes.split(",")]
         if args.conv_as_gemm:  # the GEMM views of im2col convs with dense operands (im2col cost excluded)
             shapes = [(86528, 96, 6400), (373248, 96, 576), (86528, 256, 2400), (18432, 384, 2304), (18432, 256, 3456)]
         for M, N, K in shapes:
