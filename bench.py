@@ -261,6 +261,14 @@ def run_gpu(args):
         rate, _ = cpu_oracle_rate(cb, 1, 1, os.cpu_count() or 1)
         cpu = {"value": round(rate, 4), "unit": "images/s", "cores": os.cpu_count() or 1, "kind": "port",
                "sample": f"{NET} batch {cb}: 1 timed step after 1 warm-up on the CPU oracle"}
+    # DRAM traffic of the contraction kernels per step, from the committed ncu capture of this
+    # configuration (profiles/r1_gemm_traffic_<net>_b<batch>.json; null when none was taken)
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"r1_gemm_traffic_{NET}_b{batch}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            ps = json.load(f)["per_step"]
+        traffic = ps["dram_read_bytes"] + ps["dram_write_bytes"]
     mem = tr.memory()
     summ = net.memory_summary()
     line = {
@@ -278,7 +286,8 @@ def run_gpu(args):
         "roofline": {"bound": "tensor", "kernel": "tcgen05 implicit-GEMM contractions (conv fwd/dgrad/wgrad, FC)",
                      "achieved": round(achieved_tf, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / peak_tf, 4), "peak_kind": f"{peak_kind} sustained bf16",
-                     "traffic": None, "flops_per_step": flops_tc, "contraction_ms": round(float(t_tc), 4)},
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per step (ncu, all contraction launches)",
+                     "flops_per_step": flops_tc, "contraction_ms": round(float(t_tc), 4)},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "t_meas_ms": round(ms, 4),
                           "frac": round(t_roof * 1e3 / ms, 4), "bandwidth_ms": round(float(t_bw), 4),
                           "bandwidth_bytes": bytes_bw,

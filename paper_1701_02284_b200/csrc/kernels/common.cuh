@@ -50,7 +50,7 @@ bool pdl_enabled();
 // Timing ablation (diagnostics only, results are wrong): TCB_ABLATE is a bit mask of kernel
 // classes whose launches are skipped, so the step-time delta is that class's in-graph cost.
 //   1 channel-reduction finals, 2 channel reductions, 4 BN forward apply, 8 BN backward apply,
-//   16 residual add, 32 ReLU backward, 64 split-K reduce, 128 channel copy (concat)
+//   16 residual add, 32 ReLU backward, 64 split-K reduce, 128 channel copy (concat), 256 SGD
 bool ablate(int bit);
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

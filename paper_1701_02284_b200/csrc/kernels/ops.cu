@@ -1971,7 +1971,8 @@ tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
             b.t[i] = t;
             b.start4[i + 1] = b.start4[i] + (t.n + 3) / 4;
         }
-        TCB_LAUNCH(k_sgd, grid_for(b.start4[b.nt]), kThreads, 0, st, b);
+        if (!ablate(256))
+            TCB_LAUNCH(k_sgd, grid_for(b.start4[b.nt]), kThreads, 0, st, b);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
