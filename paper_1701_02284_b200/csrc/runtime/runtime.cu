@@ -356,13 +356,12 @@ tc_status analyze_layouts(tc_ctx* c) {
 
 // Peephole fusion: GEMM producer followed by in-place BiasAdd / ReLU on its storage.
 // TCB_POOL_IDX_FLAG=0 keeps the ReLU output read in the pooling backward (A/B switch).
-static bool pool_idx_flag_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("TCB_POOL_IDX_FLAG");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+// Fusion switches are read per context (plan_fusion), so tests can A/B them in one process.
+static bool env_on(const char* name) {
+    const char* e = std::getenv(name);
+    return !(e && e[0] == '0');
 }
+static bool pool_idx_flag_enabled() { return env_on("TCB_POOL_IDX_FLAG"); }
 
 void plan_fusion(tc_ctx* c) {
     const tc_plan* p = c->plan;
@@ -388,10 +387,7 @@ void plan_fusion(tc_ctx* c) {
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET) continue;
-        static const bool gemm_fold = [] {
-            const char* e = std::getenv("TCB_GEMM_RELU_FOLD");
-            return !(e && e[0] == '0');
-        }();
+        const bool gemm_fold = env_on("TCB_GEMM_RELU_FOLD");
         const bool gemm = gemm_fold && (s.op == TC_OP_CONV_BWD_DATA || s.op == TC_OP_MATMUL_BWD_DATA);
         if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD) continue;
         // the next Let, skipping Update / Print statements that do not read this output (the
@@ -460,10 +456,7 @@ void plan_fusion(tc_ctx* c) {
     // BatchNorm followed by the residual add that is its only reader (ResNet's y = relu(BN(x) + r)):
     // the BN apply pass reads r and writes the add's output (and its folded ReLU), saving the
     // write + re-read of the BN output.  Not in keep mode, where every var is materialised.
-    static const bool bn_add = [] {
-        const char* e = std::getenv("TCB_BN_ADD_FOLD");
-        return !(e && e[0] == '0');
-    }();
+    const bool bn_add = env_on("TCB_BN_ADD_FOLD");
     for (int i = 0; bn_add && !c->desc.keep && i < p->nstmts; ++i) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET || s.op != TC_OP_BN_FWD || c->fused[i] || c->fuse_relu[i]) continue;

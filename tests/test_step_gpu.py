@@ -236,6 +236,33 @@ def test_async_input_pipeline_matches_serial():
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,batch", [("resnet50", 2), ("vgg16", 2), ("alexnet", 4)])
+def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
+    """The producer-side folds of the non-keep (bench) plan compute exactly what the separate
+    statements compute: BN apply + residual add (+ ReLU), ReLU backward in the data-gradient
+    GEMM epilogue, and the ReLU mask carried in the max-pool argmax byte.  Two training steps
+    with every fold on vs off give bit-identical losses, parameters and velocities."""
+    runs = []
+    for on in ("1", "0"):
+        for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG"):
+            monkeypatch.setenv(var, on)
+        net = compile_network(name, batch)
+        tr = Trainer(net, use_graph=True, seed=13)
+        tr.init_params()
+        losses = []
+        for it in range(2):
+            tr.stage_synthetic(it, 0)
+            tr.step(it)
+            losses.append(tr.loss())
+        runs.append((losses, [tr.get_param(i) for i in range(len(net.params))],
+                     [tr.velocity(i) for i in range(len(net.params))], tr.launches_per_step))
+        tr.close()
+    assert runs[0][3] < runs[1][3], (runs[0][3], runs[1][3])  # the folds removed launches
+    assert runs[0][0] == runs[1][0], (runs[0][0], runs[1][0])
+    for a, b in zip(runs[0][1] + runs[0][2], runs[1][1] + runs[1][2]):
+        np.testing.assert_array_equal(a, b)
+
+
 # ---------------------------------------------------------------- fp32 precision mode
 # TC_PREC_F32: fp32 activations; every contraction runs on the same tcgen05 kernels over a
 # 3 x bf16 split of its operands (hi*hi + hi*lo + lo*hi: ~16-bit mantissa, rel. error ~1e-5).
