@@ -56,6 +56,16 @@ bool ablate(int bit);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Launch priority: the step's kernels run at the device's greatest priority and the
+// side-stream momentum update (launch_sgd) at the least, so the block scheduler fills SMs
+// with update blocks only when no step kernel is waiting for them (a persistent GEMM CTA needs
+// a whole SM).  TCB_PRIO=0 launches everything at the default priority.
+int launch_priority();
+struct LowPriorityScope {  // launches inside the scope get the least priority
+    LowPriorityScope();
+    ~LowPriorityScope();
+};
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                  Args&&... args) {
@@ -64,11 +74,13 @@ inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = launch_priority();
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 // Same, launched as thread-block clusters of `cluster` CTAs.
@@ -80,15 +92,17 @@ inline cudaError_t launch_kernel_cluster(void (*kernel)(KArgs...), dim3 grid, di
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = cluster.x;
     attr[1].val.clusterDim.y = cluster.y;
     attr[1].val.clusterDim.z = cluster.z;
+    attr[2].id = cudaLaunchAttributePriority;
+    attr[2].val.priority = launch_priority();
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 3;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 #define TCB_LAUNCH(kernel, ...) ::tcb::launch_kernel(kernel, __VA_ARGS__)  // (kernel, grid, block, smem, stream, args...)

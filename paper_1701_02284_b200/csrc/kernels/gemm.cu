@@ -23,6 +23,25 @@ bool pdl_enabled() {
     return on;
 }
 
+static int priority_range(bool least) {
+    static int lo = 0, hi = 0;
+    static const bool init = [] {
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) {
+            cudaGetLastError();
+            lo = hi = 0;
+        }
+        const char* e = std::getenv("TCB_PRIO");
+        if (e && e[0] == '0') lo = hi = 0;
+        return true;
+    }();
+    (void)init;
+    return least ? lo : hi;
+}
+static thread_local int tl_low_priority = 0;
+int launch_priority() { return priority_range(tl_low_priority > 0); }
+LowPriorityScope::LowPriorityScope() { ++tl_low_priority; }
+LowPriorityScope::~LowPriorityScope() { --tl_low_priority; }
+
 bool ablate(int bit) {
     static const int mask = [] {
         const char* e = std::getenv("TCB_ABLATE");
@@ -297,10 +316,12 @@ static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
     cfg.blockDim = dim3(kNumThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     int na = 0;
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na++].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na++].val.priority = launch_priority();
     if (CG == 2) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
         attr[na].val.clusterDim.x = 2;

@@ -1958,6 +1958,7 @@ tc_status launch_s2d_mask_grad(float* g, int K, long long ld, int Rp, int s, int
     return TC_OK;
 }
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
+    LowPriorityScope low;  // yields SMs to the step's kernels (see launch_priority)
     for (int base = 0; base < nt; base += kMaxSgd) {
         SgdBatch b;
         b.nt = std::min(kMaxSgd, nt - base);
@@ -1971,8 +1972,17 @@ tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
             b.t[i] = t;
             b.start4[i + 1] = b.start4[i] + (t.n + 3) / 4;
         }
+        // TCB_SGD_SHORT=1: one 4-element unit per thread (many short blocks the scheduler can
+        // interleave with step kernels) instead of a grid-stride grid of SMs x 32 blocks
+        static const bool short_blocks = [] {
+            const char* e = std::getenv("TCB_SGD_SHORT");
+            return e && e[0] == '1';
+        }();
+        const long long units = b.start4[b.nt];
+        const int blocks = short_blocks ? static_cast<int>(std::min<long long>((units + kThreads - 1) / kThreads, 1ll << 30))
+                                        : grid_for(units);
         if (!ablate(256))
-            TCB_LAUNCH(k_sgd, grid_for(b.start4[b.nt]), kThreads, 0, st, b);
+            TCB_LAUNCH(k_sgd, blocks, kThreads, 0, st, b);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;

@@ -108,7 +108,10 @@ struct TileCfg {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagingTotal = (SK ? 32 : 8) * kStagingBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kStagingTotal + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
+    // TMEM accumulators: 4 for BN <= 128 (the MMA runs up to 3 tiles ahead of the epilogue
+    // on short-K tiles), 2 for BN = 256; 512 columns at most
+    static constexpr int kAcc = BN <= 128 ? 4 : 2;
+    static constexpr uint32_t kTmemCols = kAcc * BN < 32 ? 32 : kAcc * BN;
     static constexpr int kLag = kStages - 2;                             // cp.async groups in flight
 };
 
@@ -415,8 +418,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     uint64_t* full = reinterpret_cast<uint64_t*>(sStage + Cfg::kStagingTotal);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    constexpr int NACC = Cfg::kAcc;
+    uint64_t* tempty = tfull + NACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             mbar_init(&full[s], 1 + (any_gather ? 128 : 0));
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NACC; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], CG * (any_gather ? 4 : 8));  // one arrival per epilogue warp of the pair
         }
@@ -546,8 +550,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         int it = 0, tc = 0;
         for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
-            const int buf = tc & 1;
-            mbar_wait(&tempty[buf], ((tc >> 1) & 1) ^ 1);
+            const int buf = tc % NACC;
+            mbar_wait(&tempty[buf], ((tc / NACC) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + buf * BN;
             // the last column tile issues only the columns that exist (rounded to 16): N = 96 on
@@ -690,16 +694,21 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             else
                 mbar_arrive(local);
         };
-        const uint32_t tempty_addr[2] = {CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]),
-                                         CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : smem_u32(&tempty[1])};
+        uint32_t tempty_addr[NACC];
+#pragma unroll
+        for (int b = 0; b < NACC; ++b)
+            tempty_addr[b] = CG == 2 ? mapa_shared(smem_u32(&tempty[b]), 0) : smem_u32(&tempty[b]);
+        // BN = 64 with two warp groups: the groups take alternate tiles (one 64-column chunk
+        // each) instead of group 1 idling, so two tiles drain concurrently
+        const bool alternate = BN == 64 && ngrp == 2;
         for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
-            const int buf = tc & 1;
-            mbar_wait(&tfull[buf], (tc >> 1) & 1);
+            const int buf = tc % NACC;
+            mbar_wait(&tfull[buf], (tc / NACC) & 1);
             tc_fence_after();
             const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
-            if (grp * 64 >= BN) {  // no chunk for this warp (BN = 64 with two groups)
+            if (alternate ? grp != (tc & 1) : grp * 64 >= BN) {  // no chunk of this tile for this warp
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_accum(tempty_addr[buf], &tempty[buf]);
@@ -708,7 +717,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             // One staging row = 128 B (64 bf16 or 32 fp32 columns).  The two TMEM reads of a
             // 64-column chunk are issued back to back and waited once; the chunk's bias values
             // are fetched one per lane meanwhile and broadcast with shuffles.
-            for (int c0 = grp * 64; c0 < BN; c0 += 64 * ngrp) {
+            for (int c0 = alternate ? 0 : grp * 64; c0 < BN; c0 += 64 * ngrp) {
                 uint32_t r0[32], r1[32];
 #ifdef TCB_EXP_NOTMEM
 #pragma unroll
