@@ -286,8 +286,9 @@ tc_status analyze_layouts(tc_ctx* c) {
         q.cs = c->vars.at(s.in[0].index).cs;
     }
     // Space-to-depth for a strided first-layer conv on the cs = 4 input (AlexNet 11x11/4):
-    // staging the image as [N][Hs][Ws][s*s*4] turns it into a stride-1 Rp x Rp conv over
-    // s*s*4 = 64 channels, which takes the TMA im2col operand path instead of 8-byte gathers.
+    // staging the image as [N][Hs][Ws][s*s*cs] turns it into a stride-1 Rp x Rp conv over
+    // s*s*cs channels, which takes the TMA im2col operand path instead of 8-byte gathers:
+    // 64 channels (SW128 boxes) for stride 4.
     {
         int xv = -1;
         for (int i = 0; i < p->nstmts; ++i)
@@ -309,16 +310,21 @@ tc_status analyze_layouts(tc_ctx* c) {
         const bool allowed = !(e && e[0] == '0') && !c->f32;
         if (allowed && xv >= 0 && uses == 1 && other == 0) {
             const tc_stmt& s = p->stmts[fwd];
-            const VarL& x = c->vars.at(xv);
+            VarL& x = c->vars.at(xv);
             const VarL& y = c->vars.at(s.var);
             ParamL& q = c->params[s.in[1].index];
             const int st = s.stride;
-            bool ok = x.cs == 4 && st >= 2 && st <= 8 && (st * st * 4) % 64 == 0 && q.R == q.S;
+            // (a stride-2 variant staging the image with channel stride 8 -> 32-channel SW64 boxes
+            // measured slower for ResNet-50 / GoogLeNet conv1: wgrad 0.43 -> 0.56 ms)
+            const int cs = (st * st * 4) % 64 == 0 ? 4 : 0;
+            bool ok = x.cs == 4 && cs > 0 && st >= 2 && st <= 8 && q.R == q.S;
             for (int i = 0; ok && i < p->nstmts; ++i)
                 if (p->stmts[i].op == TC_OP_CONV_BWD_DATA && p->stmts[i].in[1].kind == TC_REF_PARAM &&
                     p->stmts[i].in[1].index == s.in[1].index)
                     ok = false;
             if (ok) {
+                x.cs = cs;
+                q.cs = cs;
                 q.s2d = st;
                 q.Rp = (q.R + st - 1) / st;
                 c->in_layout.s2d = st;
@@ -1471,7 +1477,10 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMalloc(&c->arena, std::max<size_t>(c->arena_bytes, 256)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->arena, 0, std::max<size_t>(c->arena_bytes, 256), c->st));
     // input staging: NHWC bf16 batch + labels + NCHW fp32 staging for host batches
-    c->input_cs = plan->input_dims[1] <= 4 && !c->f32 ? 4 : ceil8(plan->input_dims[1]);  // = the LOAD_X var layout
+    c->input_cs = plan->input_dims[1] <= 4 && !c->f32 ? 4 : ceil8(plan->input_dims[1]);
+    for (int i = 0; i < plan->nstmts; ++i)  // = the LOAD_X var layout (cs 8 for a stride-2 space-to-depth)
+        if (plan->stmts[i].kind == TC_STMT_LET && plan->stmts[i].op == TC_OP_LOAD_X)
+            c->input_cs = c->vars.at(plan->stmts[i].var).cs;
     c->in_layout.N = static_cast<int>(plan->input_dims[0]);
     c->in_layout.C = static_cast<int>(plan->input_dims[1]);
     c->in_layout.H = static_cast<int>(plan->input_dims[2]);
