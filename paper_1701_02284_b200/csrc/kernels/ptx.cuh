@@ -107,6 +107,35 @@ __device__ __forceinline__ void tma_load_2d_cg(void* dst, const CUtensorMap* m, 
             : "memory");
     }
 }
+// L2 cache-policy variants (createpolicy): evict_last keeps re-read operands (filters) in L2,
+// evict_first streams single-use ones.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_cg_hint(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
+                                                    uint64_t pol) {
+    if constexpr (CG == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+            : "memory");
+    } else {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+            : "memory");
+    }
+}
 template <int CG>
 __device__ __forceinline__ void tma_load_im2col_4d_cg(void* dst, const CUtensorMap* m, uint32_t bar, int c, int w, int h,
                                                       int n, uint16_t off_w, uint16_t off_h) {

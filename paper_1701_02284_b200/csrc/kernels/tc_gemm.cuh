@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         // ---------------- TMA producer
         if (lane == 0) {
             uint32_t tx = 0;
+#ifdef TCB_L2HINT
+            const uint64_t pol_b = l2_policy_evict_last();
+#endif
             if (!a_gather) tx += Cfg::kABytes;
             if (!b_gather) tx += Cfg::kBBytes;
             tx *= CG;  // the leader's barrier counts the bytes landing in both CTAs
@@ -512,11 +515,19 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         }
                     }
                     if (p.b_mode == OP_TMA_K) {
+#ifdef TCB_L2HINT
+                        tma_load_2d_cg_hint<CG>(b_dst, &p.tmB, bar, kc, n0, pol_b);
+#else
                         tma_load_2d_cg<CG>(b_dst, &p.tmB, bar, kc, n0);
+#endif
                     } else if (p.b_mode == OP_TMA_MN) {
 #pragma unroll
                         for (int a = 0; a < Cfg::kBNL / 64; ++a)
+#ifdef TCB_L2HINT
+                            tma_load_2d_cg_hint<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc, pol_b);
+#else
                             tma_load_2d_cg<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc);
+#endif
                     } else if (p.b_mode == OP_IM2COL_MN || p.b_mode == OP_IM2COL32_MN) {
                         // 64 output pixels of this k-block; columns n = tap * cs + c in 64-channel atoms
                         const int pq = p.i2c_P * p.i2c_Q;
