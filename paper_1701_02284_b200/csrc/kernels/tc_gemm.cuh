@@ -489,6 +489,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     // transaction barrier: the leader CTA's full[s] (own barrier for CG = 1)
                     const uint32_t bar = CG == 2 ? mapa_shared(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
                     int kc = kb * BK;  // k coordinate of this block in the plain-TMA operand
+#ifdef TCB_EXP_NOLOAD
+                    if (rank == 0) mbar_arrive(&full[s]);  // experiment: MMA / epilogue pipeline without operand loads
+                    continue;
+#endif
                     if (p.a_mode == OP_TMA_K) {
                         tma_load_2d_cg<CG>(a_dst, &p.tmA, bar, kc, m0);
                     } else if (p.a_mode == OP_TMA_MN) {
@@ -558,6 +562,29 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         const bool b_sw64 = p.b_mode == OP_IM2COL32_MN;
         const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN || b_sw64;
         const uint32_t idesc_full = umma_idesc_bf16(BM * CG, BN, a_mn ? 1u : 0u, b_mn ? 1u : 0u);
+        // Operand descriptors are built once: stage-0 bases plus per-k-step offsets (the start
+        // address field is the low 14 bits in 16-byte units; every other field is fixed per
+        // operand mode), so the issue loop is 4 MMAs and adds per k-block.
+        //   K-major SW128: 32 bytes along the swizzled row per k-step; MN-major SW128: two 8-row
+        //   k-groups (2 x 1024 B); SW64 K-major A: two 8 KB halves of 64-byte rows; SW64
+        //   MN-major B: 32-column atoms of 64 k-rows (4 KB apart), 512-byte 8-row groups
+        auto a_desc_at = [&](uint32_t base, int k) -> uint64_t {
+            return a_mn ? umma_desc_sw128(base + k * 2048, BK * 128, 1024)
+                   : a_sw64 ? umma_desc_sw64(base + (k >> 1) * (Cfg::kABytes / 2) + (k & 1) * 32, 0, 512)
+                            : umma_desc_sw128(base + k * 32, 0, 1024);
+        };
+        auto b_desc_at = [&](uint32_t base, int k) -> uint64_t {
+            return b_sw64 ? umma_desc_sw64(base + k * 1024, BK * 64, 512)
+                   : b_mn ? umma_desc_sw128(base + k * 2048, BK * 128, 1024)
+                          : umma_desc_sw128(base + k * 32, 0, 1024);
+        };
+        const uint64_t a_desc0 = a_desc_at(smem_u32(sA), 0), b_desc0 = b_desc_at(smem_u32(sB), 0);
+        uint64_t a_koff[BK / 16], b_koff[BK / 16];
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+            a_koff[k] = a_desc_at(smem_u32(sA), k) - a_desc0;
+            b_koff[k] = b_desc_at(smem_u32(sB), k) - b_desc0;
+        }
         int it = 0, tc = 0;
         for (int u = pair; u < p.units; u += npairs, ++tc) {
             const Unit w = decode_unit(p, u);
@@ -576,25 +603,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     idesc = umma_idesc_bf16(BM, static_cast<uint32_t>((n_left + gran - 1) / gran * gran), a_mn ? 1u : 0u,
                                             b_mn ? 1u : 0u);
             }
-            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                const int s = it % S;
-                mbar_wait(&full[s], (it / S) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a_base = smem_u32(sA + s * Cfg::kABytes);
-                    const uint32_t b_base = smem_u32(sB + s * Cfg::kBBytes);
+            if (lane == 0) {
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&full[s], (it / S) & 1);
+                    tc_fence_after();
+                    // stage s descriptors = stage-0 descriptors + the stage offset in 16-byte units
+                    const uint64_t a_s = a_desc0 + static_cast<uint64_t>(s * (Cfg::kABytes >> 4));
+                    const uint64_t b_s = b_desc0 + static_cast<uint64_t>(s * (Cfg::kBBytes >> 4));
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
-                        // K-major: 32 bytes along the swizzled row; MN-major: two 8-row k-groups (2 x 1024 B)
-                        // SW64 K-major A: two 8 KB halves of 64-byte rows; SW64 MN-major B: 32-column
-                        // atoms of 64 k-rows (4 KB apart), 512-byte 8-row groups
-                        const uint64_t ad =
-                            a_mn     ? umma_desc_sw128(a_base + k * 2048, BK * 128, 1024)
-                            : a_sw64 ? umma_desc_sw64(a_base + (k >> 1) * (Cfg::kABytes / 2) + (k & 1) * 32, 0, 512)
-                                     : umma_desc_sw128(a_base + k * 32, 0, 1024);
-                        const uint64_t bd = b_sw64 ? umma_desc_sw64(b_base + k * 1024, BK * 64, 512)
-                                            : b_mn ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
-                                                   : umma_desc_sw128(b_base + k * 32, 0, 1024);
+                        const uint64_t ad = a_s + a_koff[k], bd = b_s + b_koff[k];
                         if constexpr (CG == 2)
                             umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
                         else
@@ -608,8 +627,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         if (kb == w.kb1 - 1) umma_commit(&tfull[buf]);
                     }
                 }
-                __syncwarp();
             }
+            __syncwarp();
         }
     } else if (warp >= 8 && any_gather) {
         // ---------------- im2col gather producers (128 threads)
