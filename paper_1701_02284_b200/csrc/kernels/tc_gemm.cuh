@@ -603,32 +603,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     idesc = umma_idesc_bf16(BM, static_cast<uint32_t>((n_left + gran - 1) / gran * gran), a_mn ? 1u : 0u,
                                             b_mn ? 1u : 0u);
             }
-            if (lane == 0) {
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                    const int s = it % S;
-                    mbar_wait(&full[s], (it / S) & 1);
-                    tc_fence_after();
-                    // stage s descriptors = stage-0 descriptors + the stage offset in 16-byte units
-                    const uint64_t a_s = a_desc0 + static_cast<uint64_t>(s * (Cfg::kABytes >> 4));
-                    const uint64_t b_s = b_desc0 + static_cast<uint64_t>(s * (Cfg::kBBytes >> 4));
+            // warp-converged loop; the MMA / commit helpers elect the issuing lane
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                const int s = it % S;
+                mbar_wait(&full[s], (it / S) & 1);
+                tc_fence_after();
+                // stage s descriptors = stage-0 descriptors + the stage offset in 16-byte units
+                const uint64_t a_s = a_desc0 + static_cast<uint64_t>(s * (Cfg::kABytes >> 4));
+                const uint64_t b_s = b_desc0 + static_cast<uint64_t>(s * (Cfg::kBBytes >> 4));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = a_s + a_koff[k], bd = b_s + b_koff[k];
-                        if constexpr (CG == 2)
-                            umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
-                        else
-                            umma_bf16(d_tmem, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
-                    }
-                    if constexpr (CG == 2) {
-                        umma_commit_cg2(&empty[s]);
-                        if (kb == w.kb1 - 1) umma_commit_cg2(&tfull[buf]);
-                    } else {
-                        umma_commit(&empty[s]);
-                        if (kb == w.kb1 - 1) umma_commit(&tfull[buf]);
-                    }
-                }
+                for (int k = 0; k < BK / 16; ++k)
+                    umma_bf16_elect<CG>(d_tmem, a_s + a_koff[k], b_s + b_koff[k], idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+                umma_commit_elect<CG>(&empty[s]);
+                if (kb == w.kb1 - 1) umma_commit_elect<CG>(&tfull[buf]);
             }
-            __syncwarp();
         }
     } else if (warp >= 8 && any_gather) {
         // ---------------- im2col gather producers (128 threads)
