@@ -260,8 +260,8 @@ static double t_kblock(int bn, int cg) {
 // the fp32 partial round trip of the deterministic reduce.
 // CTA pairs (cta_group::2, 256-row tiles with B split across the two SMs) are used for
 // the filter-gradient contractions with >= 256 output channels: measured +7..54% there
-// (AlexNet conv2 wgrad 305 -> 469 TF/s, VGG 256/512-channel wgrad 550 -> 740 TF/s), while
-// fprop / dgrad shapes measured equal or slower (tools/gemm_bench.py, same-call A/B).
+// (AlexNet conv2 wgrad 305 -> 469 TF/s, VGG 256/512-channel wgrad 550 -> 740 TF/s); fprop /
+// dgrad shapes pay only when deep, wide and numerous enough (below; tools/gemm_bench.py A/B).
 // `pair` = the caller's choice; TCB_CG=1|2 overrides it where both operands are TMA-loaded.
 static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes, bool pair_ok, bool pair = false) {
     LaunchPlan best;
@@ -269,6 +269,12 @@ static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes
     const int sms = num_sms();
     const int num_kb = std::max(1, ceil_div(K, BK));
     const double mn = static_cast<double>(M) * N;
+    // Beyond the caller's choice, 256-wide pair tiles also pay for fprop / dgrad when N is a
+    // multiple of 256 and there are at least two waves of pair tiles (measured after the MMA
+    // issue fix: 8192^3 1294 -> 1485 TF/s, VGG 256/512-channel fprop +5%, dgrad +10-15%; fewer
+    // tiles or N = 384 / 128 measured slower)
+    if (!pair && N % 256 == 0 && num_kb >= 8 && static_cast<long long>(ceil_div(M, 2 * BM)) * (N / 256) >= sms)
+        pair = true;  // (short-K tiles are store-paced: ResNet-50's 1x1 convs measured -1.6% as pairs)
     const int want_cg = !pair_ok ? 1 : forced_cg() ? forced_cg() : (pair ? 2 : 1);
     for (int cg : {1, 2}) {
         if (cg != want_cg) continue;
