@@ -457,8 +457,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     pdl_wait();
 
     if (warp == 0) {
-        // ---------------- TMA producer
-        if (lane == 0) {
+        // ---------------- TMA producer (warp-converged; the issue helpers elect one lane)
+        {
             uint32_t tx = 0;
 #ifdef TCB_L2HINT
             const uint64_t pol_b = l2_policy_evict_last();
@@ -490,20 +490,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     const uint32_t bar = CG == 2 ? mapa_shared(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
                     int kc = kb * BK;  // k coordinate of this block in the plain-TMA operand
 #ifdef TCB_EXP_NOLOAD
-                    if (rank == 0) mbar_arrive(&full[s]);  // experiment: MMA / epilogue pipeline without operand loads
+                    if (rank == 0 && lane == 0) mbar_arrive(&full[s]);  // experiment: MMA / epilogue pipeline without operand loads
                     continue;
 #endif
                     if (p.a_mode == OP_TMA_K) {
-                        tma_load_2d_cg<CG>(a_dst, &p.tmA, bar, kc, m0);
+                        tma_load_2d_e<CG>(a_dst, &p.tmA, bar, kc, m0);
                     } else if (p.a_mode == OP_TMA_MN) {
 #pragma unroll
                         for (int a = 0; a < BM / 64; ++a)
-                            tma_load_2d_cg<CG>(a_dst + a * BK * 128, &p.tmA, bar, m0 + a * 64, kc);
+                            tma_load_2d_e<CG>(a_dst + a * BK * 128, &p.tmA, bar, m0 + a * 64, kc);
                     } else if (p.a_mode == OP_IM2COL_K) {
                         const int tap = kb / p.i2c_cpb, cb = kb - tap * p.i2c_cpb;
                         const int kh = tap / g.S, kw = tap - kh * g.S;
                         const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
-                        tma_load_im2col_4d_cg<CG>(a_dst, &p.tmA, bar, cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
+                        tma_load_im2col_4d_e<CG>(a_dst, &p.tmA, bar, cb * 64, a_x, a_y, a_n, static_cast<uint16_t>(ow),
                                            static_cast<uint16_t>(oh));
                         kc = tap * p.i2c_ldk + cb * 64;
                     } else if (p.a_mode == OP_IM2COL32_K) {
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                             const int tap = blk / p.i2c_cpb, cb = blk - tap * p.i2c_cpb;
                             const int kh = tap / g.S, kw = tap - kh * g.S;
                             const int ow = p.i2c_flip ? g.S - 1 - kw : kw, oh = p.i2c_flip ? g.R - 1 - kh : kh;
-                            tma_load_im2col_4d_cg<CG>(a_dst + h * (Cfg::kABytes / 2), &p.tmA, bar, cb * 32, a_x, a_y, a_n,
+                            tma_load_im2col_4d_e<CG>(a_dst + h * (Cfg::kABytes / 2), &p.tmA, bar, cb * 32, a_x, a_y, a_n,
                                                static_cast<uint16_t>(ow), static_cast<uint16_t>(oh));
                         }
                     }
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 #ifdef TCB_L2HINT
                         tma_load_2d_cg_hint<CG>(b_dst, &p.tmB, bar, kc, n0, pol_b);
 #else
-                        tma_load_2d_cg<CG>(b_dst, &p.tmB, bar, kc, n0);
+                        tma_load_2d_e<CG>(b_dst, &p.tmB, bar, kc, n0);
 #endif
                     } else if (p.b_mode == OP_TMA_MN) {
 #pragma unroll
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 #ifdef TCB_L2HINT
                             tma_load_2d_cg_hint<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc, pol_b);
 #else
-                            tma_load_2d_cg<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc);
+                            tma_load_2d_e<CG>(b_dst + a * BK * 128, &p.tmB, bar, n0 + a * 64, kc);
 #endif
                     } else if (p.b_mode == OP_IM2COL_MN || p.b_mode == OP_IM2COL32_MN) {
                         // 64 output pixels of this k-block; columns n = tap * cs + c in 64-channel atoms
@@ -547,11 +547,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                             if (n >= p.N) n = 0;  // columns past N are clipped by the store; load finite data
                             const int tap = n / g.C, c = n - tap * g.C;
                             const int kh = tap / g.S, kw = tap - kh * g.S;
-                            tma_load_im2col_4d_cg<CG>(b_dst + col * BK * 2, &p.tmB, bar, c, bx, by, bn_img,
+                            tma_load_im2col_4d_e<CG>(b_dst + col * BK * 2, &p.tmB, bar, c, bx, by, bn_img,
                                                static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
                         }
                     }
-                    if (rank == 0) mbar_arrive_expect_tx(&full[s], tx);
+                    if (rank == 0) mbar_arrive_expect_tx_e(&full[s], tx);
                 }
             }
         }
