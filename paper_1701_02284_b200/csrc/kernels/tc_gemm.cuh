@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     }
                     // staging buffer reuse: the TMA store issued two stores ago must have read it
                     uint8_t* stg = stage_base + (nstore % nbuf) * kStagingBytes;
-                    if (lane == 0 && nstore >= nbuf) {
+                    if (nstore >= nbuf) {  // every lane: only the issuing lane has groups
                         if (nbuf >= 8) bulk_wait_read<7>();
                         else if (nbuf >= 4) bulk_wait_read<3>();
                         else if (nbuf == 2) bulk_wait_read<1>();
@@ -835,17 +835,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                                      packed[4 * q + 2], packed[4 * q + 3]);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
 #ifndef TCB_EXP_NOSTORE
-                        tma_store_3d(&p.tmD, stg, nb + sub * 32, m0 + quarter * 32, w.sp);
+                    tma_store_3d_e(&p.tmD, stg, nb + sub * 32, m0 + quarter * 32, w.sp);
 #endif
-                        bulk_commit();
-                    }
+                    bulk_commit();
                     ++nstore;
                 }
             }
         }
-        if (lane == 0) bulk_wait<0>();
+        bulk_wait<0>();
         __syncwarp();
     }
 
