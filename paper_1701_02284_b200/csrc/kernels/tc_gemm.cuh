@@ -422,7 +422,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
     uint64_t* tempty = tfull + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
-    const int warp = threadIdx.x >> 5;
+    // warp index broadcast from lane 0: provably warp-uniform, so the role branches below and
+    // the loop state inside them can live in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const bool a_gather = CG == 1 && p.a_mode == OP_GATHER_K;  // CTA pairs use TMA operands only
     const bool b_gather = CG == 1 && p.b_mode == OP_GATHER_MN;
