@@ -295,49 +295,52 @@ __device__ __forceinline__ void col_gather_issue(const GemmParams& p, const ColG
 // ---- channel-stride-4 gathers (first-layer convs, 3 real channels + 1 zero pad) ----
 // One 8-byte chunk = one filter tap; a 64-element k-block = 16 taps.
 struct RowGather4 {
-    const __nv_bfloat16* base;
-    int ry, rx, kh, kw, tap;
+    const __nv_bfloat16* base;  // tap (0, 0) of this output pixel (may lie outside the image)
+    uint32_t rowmask, colmask;  // bit kh / kw: that filter row / column lands inside the image
+    int kh, kw, tap, off;       // current tap and its element offset from base
     bool valid;
 };
 
+// Per-tap work is a mask test, a select and the copy: the image-bounds tests are folded into
+// two per-pixel bit masks (R, S <= 32) and the tap address advances incrementally.
 __device__ __forceinline__ void row_gather4_init(const GemmParams& p, RowGather4& rg, int m, int kb0) {
     const ConvGeom& g = p.g;
     rg.valid = m < p.M;
-    int n = 0;
-    rg.ry = rg.rx = 0;
+    int n = 0, ry = 0, rx = 0;
     if (rg.valid) {
         n = m / (g.Ho * g.Wo);
         const int rem = m - n * g.Ho * g.Wo;
-        rg.ry = rem / g.Wo;
-        rg.rx = rem - rg.ry * g.Wo;
+        ry = rem / g.Wo;
+        rx = rem - ry * g.Wo;
     }
-    rg.base = p.gsrc + static_cast<long long>(n) * g.H * g.W * 4;
+    const int iy0 = ry * g.stride - g.pad, ix0 = rx * g.stride - g.pad;
+    rg.rowmask = rg.colmask = 0;
+    for (int k = 0; k < g.R; ++k)
+        if (static_cast<unsigned>(iy0 + k) < static_cast<unsigned>(g.H)) rg.rowmask |= 1u << k;
+    for (int k = 0; k < g.S; ++k)
+        if (static_cast<unsigned>(ix0 + k) < static_cast<unsigned>(g.W)) rg.colmask |= 1u << k;
+    rg.base = p.gsrc + (static_cast<long long>(n) * g.H * g.W + static_cast<long long>(iy0) * g.W + ix0) * 4;
     rg.tap = kb0 * (BK / 4);
     rg.kh = rg.tap / g.S;
     rg.kw = rg.tap - rg.kh * g.S;
+    rg.off = (rg.kh * g.W + rg.kw) * 4;
 }
 
 __device__ __forceinline__ void row_gather4_issue(const GemmParams& p, RowGather4& rg, uint32_t sA, int row) {
     const ConvGeom& g = p.g;
     const int ntaps = g.R * g.S;
+    const int wrap = (g.W - g.S) * 4;
 #pragma unroll
     for (int jj = 0; jj < BK / 4; ++jj) {
-        const void* src = p.gsrc;
-        uint32_t bytes = 0;
-        if (rg.valid && rg.tap < ntaps) {
-            const int iy = rg.ry * g.stride - g.pad + rg.kh;
-            const int ix = rg.rx * g.stride - g.pad + rg.kw;
-            if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
-                static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
-                src = rg.base + (static_cast<long long>(iy) * g.W + ix) * 4;
-                bytes = 8;
-            }
-        }
-        cp_async_8(sA + static_cast<uint32_t>(row * 128 + (((jj >> 1) ^ (row & 7)) << 4) + (jj & 1) * 8), src, bytes);
+        const bool v = rg.valid && rg.tap < ntaps && ((rg.rowmask >> rg.kh) & (rg.colmask >> rg.kw) & 1u);
+        cp_async_8(sA + static_cast<uint32_t>(row * 128 + (((jj >> 1) ^ (row & 7)) << 4) + (jj & 1) * 8),
+                   v ? static_cast<const void*>(rg.base + rg.off) : static_cast<const void*>(p.gsrc), v ? 8u : 0u);
         ++rg.tap;
+        rg.off += 4;
         if (++rg.kw == g.S) {
             rg.kw = 0;
             ++rg.kh;
+            rg.off += wrap;
         }
     }
 }
@@ -346,6 +349,7 @@ template <int BN>
 struct ColGather4 {
     static constexpr int kChunks = BN / 16;
     int code[kChunks][2];  // (kh << 8 | kw) of the two taps in a 16-byte chunk, -1 = beyond N
+    int off[kChunks][2];   // element offset of that tap from the pixel's tap (0, 0)
 };
 
 template <int BN>
@@ -362,13 +366,17 @@ __device__ __forceinline__ void col_gather4_init(const GemmParams& p, ColGather4
                 const int tap = nn >> 2;
                 const int kh = tap / g.S;
                 cg.code[q][h] = (kh << 8) | (tap - kh * g.S);
+                cg.off[q][h] = (kh * g.W + (tap - kh * g.S)) * 4;
             } else {
                 cg.code[q][h] = -1;
+                cg.off[q][h] = 0;
             }
         }
     }
 }
 
+// One k-row (output pixel) per thread per k-block: its image-bounds tests become two bit
+// masks, then every tap is a mask test, a select and the copy.
 template <int BN>
 __device__ __forceinline__ void col_gather4_issue(const GemmParams& p, const ColGather4<BN>& cg, uint32_t sB, int kr,
                                                   int half, int kb) {
@@ -382,26 +390,26 @@ __device__ __forceinline__ void col_gather4_issue(const GemmParams& p, const Col
         oy = rem / g.Wo;
         ox = rem - oy * g.Wo;
     }
-    const __nv_bfloat16* img = p.gsrc + static_cast<long long>(rn) * g.H * g.W * 4;
+    const int iy0 = oy * g.stride - g.pad, ix0 = ox * g.stride - g.pad;
+    uint32_t rowmask = 0, colmask = 0;
+    if (pv) {
+        for (int k = 0; k < g.R; ++k)
+            if (static_cast<unsigned>(iy0 + k) < static_cast<unsigned>(g.H)) rowmask |= 1u << k;
+        for (int k = 0; k < g.S; ++k)
+            if (static_cast<unsigned>(ix0 + k) < static_cast<unsigned>(g.W)) colmask |= 1u << k;
+    }
+    const __nv_bfloat16* base =
+        p.gsrc + (static_cast<long long>(rn) * g.H * g.W + static_cast<long long>(iy0) * g.W + ix0) * 4;
 #pragma unroll
     for (int q = 0; q < ColGather4<BN>::kChunks; ++q) {
         const int cc = half + 2 * q;
         const uint32_t dst = sB + (cc >> 3) * (BK * 128) + sw128_off(kr, cc & 7);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const void* src = p.gsrc;
-            uint32_t bytes = 0;
             const int code = cg.code[q][h];
-            if (pv && code >= 0) {
-                const int iy = oy * g.stride - g.pad + (code >> 8);
-                const int ix = ox * g.stride - g.pad + (code & 0xFF);
-                if (static_cast<unsigned>(iy) < static_cast<unsigned>(g.H) &&
-                    static_cast<unsigned>(ix) < static_cast<unsigned>(g.W)) {
-                    src = img + (static_cast<long long>(iy) * g.W + ix) * 4;
-                    bytes = 8;
-                }
-            }
-            cp_async_8(dst + h * 8, src, bytes);
+            const bool v = code >= 0 && ((rowmask >> (code >> 8)) & (colmask >> (code & 0xFF)) & 1u);
+            cp_async_8(dst + h * 8, v ? static_cast<const void*>(base + cg.off[q][h]) : static_cast<const void*>(p.gsrc),
+                       v ? 8u : 0u);
         }
     }
 }
