@@ -75,6 +75,52 @@ def stmt_work(net, s, nat):
     return 0, 2 * (reads + n_out)
 
 
+class NvmlClockSampler:
+    """SM clock / throttle-reason samples every ~5 ms on a host thread (NVML), so even a
+    timed region of a few tens of milliseconds is covered."""
+
+    def __init__(self, device_index):
+        import threading
+        import pynvml as nv
+        import torch
+        self.nv = nv
+        nv.nvmlInit()
+        try:  # the CUDA device by UUID (NVML's index order need not match CUDA's)
+            self.h = nv.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(device_index).uuid))
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(device_index)
+        self.rows, self.stop = [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, smax, r))
+            except Exception:
+                pass
+            if self.stop.wait(0.005):
+                break
+
+    def result(self):
+        self.stop.set()
+        self.t.join()
+        nv = self.nv
+        if not self.rows:
+            return None
+        names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({k for _, _, r in self.rows for k, bit in names.items() if r & bit})
+        return {"sm_mhz": float(np.median([a for a, _, _ in self.rows])), "sm_max_mhz": float(max(b for _, b, _ in self.rows)),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
+
+
 def sample_clocks(stop_file, out_file):
     cmd = ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
            "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -184,7 +230,13 @@ def run_gpu(args):
     tr.sync()
     launches0 = nat.lib().tc_kernel_launch_count()
     clk_file = f"/tmp/bench_clocks_{os.getpid()}.csv"
-    proc = sample_clocks(None, clk_file) if rank == 0 else None
+    nvml = None
+    if rank == 0:
+        try:
+            nvml = NvmlClockSampler(torch.cuda.current_device())
+        except Exception:
+            nvml = None
+    proc = sample_clocks(None, clk_file) if rank == 0 and nvml is None else None
     time.sleep(0.3 if proc else 0)
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -200,7 +252,7 @@ def run_gpu(args):
     if proc:
         proc.terminate()
         proc.wait()
-    clocks = parse_clocks(clk_file) if rank == 0 else None
+    clocks = (nvml.result() if nvml else parse_clocks(clk_file)) if rank == 0 else None
     loss_val = tr.loss()
 
     # ---- e2e: public API with a host batch each step (pinned H2D) + loss D2H.  The input
