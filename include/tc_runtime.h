@@ -32,8 +32,9 @@ typedef struct tc_ctx_desc {
     int use_graph;           /* capture the step in a CUDA graph after the first run */
     int keep;                /* parity mode: every storage gets its own arena range */
     int precision;           /* TC_PREC_BF16 (default): bf16 activations, bf16 tensor-core operands;
-                                TC_PREC_F32: fp32 activations, every contraction as a 3 x bf16 split
-                                (hi*hi + hi*lo + lo*hi, ~16-bit mantissa) on the same tcgen05 kernels */
+                                TC_PREC_F32: fp32 activations, every contraction as a 3-part bf16 split
+                                of each operand, 6 cross terms (hi*hi, hi*mid, mid*hi, hi*lo, mid*mid,
+                                lo*hi) accumulated in fp32 on the same tcgen05 kernels */
 } tc_ctx_desc;
 
 enum { TC_PREC_BF16 = 0, TC_PREC_F32 = 1 };

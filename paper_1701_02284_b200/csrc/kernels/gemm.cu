@@ -519,7 +519,7 @@ size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
 
 namespace tcb {
 // fprop / bwd-data with the output stored in bf16 (y_f32 = 0, the C ABI) or fp32 (the parity
-// precision mode's 3 x bf16 split contractions)
+// precision mode's 6-term bf16 split contractions)
 tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
                       int y_f32, void* ws, size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);

@@ -146,7 +146,7 @@ struct tc_ctx {
     float* h_loss = nullptr;     // pinned
     int input_cs = 8;
     StageLayout in_layout{};  // staged input image layout (space-to-depth when in_layout.s2d > 0)
-    bool f32 = false;         // TC_PREC_F32: fp32 activations, 3 x bf16 split contractions
+    bool f32 = false;         // TC_PREC_F32: fp32 activations, 6-term bf16 split contractions
     uint8_t* split_buf = nullptr;  // split operand copies of the current contraction (f32 mode)
     size_t split_bytes = 0;
     size_t input_bytes = 0;

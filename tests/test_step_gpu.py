@@ -265,7 +265,8 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
 
 # ---------------------------------------------------------------- fp32 precision mode
 # TC_PREC_F32: fp32 activations; every contraction runs on the same tcgen05 kernels over a
-# 3 x bf16 split of its operands (hi*hi + hi*lo + lo*hi: ~16-bit mantissa, rel. error ~1e-5).
+# 3-part bf16 split of its operands, 6 cross terms (hi*hi + hi*mid + mid*hi + hi*lo + mid*mid + lo*hi:
+# ~24-bit mantissa products, fp32 accumulation).
 # This is the mode the north star's fp32 tolerances are checked in: fp32 element-wise /
 # reduction ops within 1e-5, and the 100-step LeNet loss trajectory within 1e-3.
 
