@@ -1121,7 +1121,7 @@ __device__ __forceinline__ float rcp_pos(float x) {
 
 // HALF = n/2 is a template parameter so every window loop unrolls and the
 // per-thread channel windows stay in registers.
-template <int HALF, typename T>
+template <int HALF, typename T, typename IT>
 __global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, float alpha, float beta,
                            float kk) {
     pdl_wait();
@@ -1129,11 +1129,10 @@ __global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, f
     const int ng = a.cs / 8;
     const long long total = a.pixels() * ng;
     const float an = alpha / static_cast<float>(2 * HALF + 1);
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const bool i32 = total < (1ll << 31);
-        const int g = i32 ? static_cast<int>(t) % ng : static_cast<int>(t % ng);
-        const T* px = x + (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < static_cast<IT>(total);
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % ng);
+        const T* px = x + static_cast<long long>(t / ng) * a.cs;
         float v[24];
         load_chunk3<HALF>(px, g, ng, v);
         // channels outside [0, C) contribute nothing (pads are zero, neighbours beyond the tensor loaded as 0)
@@ -1143,13 +1142,13 @@ __global__ void k_lrn2_fwd(const T* __restrict__ x, T* __restrict__ y, Act4 a, f
             float s = 0.f;
 #pragma unroll
             for (int d = -HALF; d <= HALF; ++d) s += v[8 + j + d] * v[8 + j + d];
-            out[j] = (g * 8 + j) < a.C ? v[8 + j] * pow_pos(kk + an * s, -beta) : 0.f;
+            out[j] = (a.C == a.cs || (g * 8 + j) < a.C) ? v[8 + j] * pow_pos(kk + an * s, -beta) : 0.f;
         }
-        st8(y + t * 8, out);
+        st8(y + static_cast<long long>(t) * 8, out);
     }
 }
 
-template <int HALF, typename T>
+template <int HALF, typename T, typename IT>
 __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ y,
                            T* __restrict__ dx, Act4 a, float alpha, float beta, float kk, int relu) {
     pdl_wait();
@@ -1159,11 +1158,11 @@ __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, co
     const float an = alpha / static_cast<float>(2 * HALF + 1);
     const float coef = 2.f * alpha * beta / static_cast<float>(2 * HALF + 1);
     constexpr int L = 8 - HALF, U = 16 + HALF;  // window of channels g*8-HALF .. g*8+7+HALF
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const bool i32 = total < (1ll << 31);
-        const int g = i32 ? static_cast<int>(t) % ng : static_cast<int>(t % ng);
-        const long long base = (i32 ? static_cast<long long>(static_cast<int>(t) / ng) : t / ng) * a.cs;
+    const bool full = a.C == a.cs;                // no pad channels: skip the per-channel test
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < static_cast<IT>(total);
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % ng);
+        const long long base = static_cast<long long>(t / ng) * a.cs;
         float xv[24], dv[24], yv[24];
         load_chunk3<2 * HALF>(x + base, g, ng, xv);
         load_chunk3<HALF>(dy + base, g, ng, dv);
@@ -1184,7 +1183,7 @@ __global__ void k_lrn2_bwd(const T* __restrict__ dy, const T* __restrict__ x, co
             float s = 0.f;
 #pragma unroll
             for (int d = -HALF; d <= HALF; ++d) s += tt[8 + j + d];
-            out[j] = (g * 8 + j) < a.C ? dv[8 + j] * pow_pos(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
+            out[j] = (full || (g * 8 + j) < a.C) ? dv[8 + j] * pow_pos(sc[8 + j], -beta) - coef * xv[8 + j] * s : 0.f;
             if (relu && !(xv[8 + j] > 0.f)) out[j] = 0.f;  // folded ReLU backward: x is the ReLU output
         }
         st8(dx + base + g * 8, out);
@@ -1712,10 +1711,10 @@ tc_status launch_lrn_fwd(const T* x, T* y, Act4 a, int size, float alpha, float 
         }
     }
     switch (size) {  // odd windows up to 9: register-resident template kernels
-        case 3: TCB_LAUNCH((k_lrn2_fwd<1, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 5: TCB_LAUNCH((k_lrn2_fwd<2, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 7: TCB_LAUNCH((k_lrn2_fwd<3, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
-        case 9: TCB_LAUNCH((k_lrn2_fwd<4, T>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 3: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_fwd<1, T, int>), EW_GRID(n), x, y, a, alpha, beta, k); else TCB_LAUNCH((k_lrn2_fwd<1, T, long long>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 5: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_fwd<2, T, int>), EW_GRID(n), x, y, a, alpha, beta, k); else TCB_LAUNCH((k_lrn2_fwd<2, T, long long>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 7: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_fwd<3, T, int>), EW_GRID(n), x, y, a, alpha, beta, k); else TCB_LAUNCH((k_lrn2_fwd<3, T, long long>), EW_GRID(n), x, y, a, alpha, beta, k); break;
+        case 9: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_fwd<4, T, int>), EW_GRID(n), x, y, a, alpha, beta, k); else TCB_LAUNCH((k_lrn2_fwd<4, T, long long>), EW_GRID(n), x, y, a, alpha, beta, k); break;
         default: {  // general path: warp per pixel with the channel vector in shared memory
             const int warps = 8;
             TCB_LAUNCH(k_lrn_fwd<T>, grid_for(a.pixels(), warps), warps * 32, warps * a.cs * sizeof(float), st, x, y, a, size,
@@ -1746,10 +1745,10 @@ tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int
         }
     }
     switch (size) {
-        case 3: TCB_LAUNCH((k_lrn2_bwd<1, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
-        case 5: TCB_LAUNCH((k_lrn2_bwd<2, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
-        case 7: TCB_LAUNCH((k_lrn2_bwd<3, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
-        case 9: TCB_LAUNCH((k_lrn2_bwd<4, T>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 3: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_bwd<1, T, int>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); else TCB_LAUNCH((k_lrn2_bwd<1, T, long long>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 5: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_bwd<2, T, int>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); else TCB_LAUNCH((k_lrn2_bwd<2, T, long long>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 7: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_bwd<3, T, int>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); else TCB_LAUNCH((k_lrn2_bwd<3, T, long long>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
+        case 9: if (n < (1ll << 31)) TCB_LAUNCH((k_lrn2_bwd<4, T, int>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); else TCB_LAUNCH((k_lrn2_bwd<4, T, long long>), EW_GRID(n), dy, x, y, dx, a, alpha, beta, k, relu); break;
         default: {
             const int warps = 8;
             TCB_LAUNCH(k_lrn_bwd<T>, grid_for(a.pixels(), warps), warps * 32, warps * 3 * a.cs * sizeof(float), st, 
