@@ -370,6 +370,16 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         p.relu = relu;
         if (!make_tmap_store(&p.tmD, D, d_bf16 != 0, p.N, p.M, 1, ldd, &err)) return fail(TC_INVALID_ARG, err);
     }
+    // resident B (TCB_B_RESIDENT=0 disables): one N tile, no split-K and every k-block of B fits
+    // the ring's B slots -> B is loaded once per CTA, only A streams
+    static const bool resident_on = [] {
+        const char* e = std::getenv("TCB_B_RESIDENT");
+        return !(e && e[0] == '0');
+    }();
+    const int ring = lp.bn == 256 ? TileCfg<256, 1>::kStages : lp.bn == 128 ? TileCfg<128, 1>::kStages
+                                                                             : TileCfg<64, 1>::kStages;
+    p.b_resident = resident_on && lp.cg == 1 && p.tiles_n == 1 && lp.splits == 1 && lp.num_kb <= ring &&
+                   (p.b_mode == OP_TMA_K || p.b_mode == OP_TMA_MN);
     tc_status s;
     if (lp.cg == 2)
         s = lp.bn == 256 ? launch_bn<256, 2>(p, p.units, st) : launch_bn<128, 2>(p, p.units, st);

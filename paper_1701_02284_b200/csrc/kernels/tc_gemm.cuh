@@ -62,6 +62,8 @@ struct GemmParams {
     CUtensorMap tmD;  // 3-D store map {N, M, splits}, SW128, box {128 B of columns, 32 rows, 1}
     int M, N, K;
     int a_mode, b_mode;
+    int b_resident;  // 1: one N tile, no split-K, num_kb <= stages: B is loaded once per CTA into
+                     // ring slot kb and reused by every later unit (only A streams)
     int gather_kind;            // GatherKind for OP_GATHER_K
     const __nv_bfloat16* gsrc;  // gather source tensor
     ConvGeom g;
@@ -481,6 +483,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             for (int u = pair; u < p.units; u += npairs) {
                 const Unit w = decode_unit(p, u);
                 const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN + rank * Cfg::kBNL;
+                const bool load_b = !p.b_resident || u == pair;  // resident B: first unit only
+                const uint32_t tx_u = load_b || b_gather ? tx : tx - Cfg::kBBytes * CG;
                 // im2col A: first pixel of this row tile
                 int a_n = 0, a_y = 0, a_x = 0;
                 if (p.a_mode == OP_IM2COL_K || p.a_mode == OP_IM2COL32_K) {
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     const int s = it % S;
                     mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
                     uint8_t* a_dst = sA + s * Cfg::kABytes;
-                    uint8_t* b_dst = sB + s * Cfg::kBBytes;
+                    uint8_t* b_dst = sB + (p.b_resident ? kb : s) * Cfg::kBBytes;
                     // transaction barrier: the leader CTA's full[s] (own barrier for CG = 1)
                     const uint32_t bar = CG == 2 ? mapa_shared(smem_u32(&full[s]), 0) : smem_u32(&full[s]);
                     int kc = kb * BK;  // k coordinate of this block in the plain-TMA operand
@@ -528,7 +532,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                                                static_cast<uint16_t>(ow), static_cast<uint16_t>(oh));
                         }
                     }
-                    if (p.b_mode == OP_TMA_K) {
+                    if (!load_b) {
+                        // resident B: nothing to load for this k-block
+                    } else if (p.b_mode == OP_TMA_K) {
 #ifdef TCB_L2HINT
                         tma_load_2d_cg_hint<CG>(b_dst, &p.tmB, bar, kc, n0, pol_b);
 #else
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                                                static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
                         }
                     }
-                    if (rank == 0) mbar_arrive_expect_tx_e(&full[s], tx);
+                    if (rank == 0) mbar_arrive_expect_tx_e(&full[s], tx_u);
                 }
             }
         }
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 tc_fence_after();
                 // stage s descriptors = stage-0 descriptors + the stage offset in 16-byte units
                 const uint64_t a_s = a_desc0 + static_cast<uint64_t>(s * (Cfg::kABytes >> 4));
-                const uint64_t b_s = b_desc0 + static_cast<uint64_t>(s * (Cfg::kBBytes >> 4));
+                const uint64_t b_s = b_desc0 + static_cast<uint64_t>((p.b_resident ? kb : s) * (Cfg::kBBytes >> 4));
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k)
                     umma_bf16_elect<CG>(d_tmem, a_s + a_koff[k], b_s + b_koff[k], idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
