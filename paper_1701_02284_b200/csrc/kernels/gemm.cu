@@ -195,7 +195,7 @@ static bool make_tmap_store(CUtensorMap* map, void* base, bool bf16, uint64_t N,
 // out[m, n] = epilogue( sum_s ws[s][m][n] ), fixed summation order (deterministic).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
-                                     int n_bias, int relu, float beta) {
+                                     int n_bias, int relu, float beta, int trans) {
     pdl_wait();
     pdl_trigger();
     const long long total = static_cast<long long>(M) * N;
@@ -210,7 +210,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
         if (out_bf16) {
             reinterpret_cast<__nv_bfloat16*>(out)[m * ldd + n] = __float2bfloat16_rn(acc);
         } else {
-            float* o = reinterpret_cast<float*>(out) + m * ldd + n;
+            float* o = reinterpret_cast<float*>(out) + (trans ? n * ldd + m : m * ldd + n);
             *o = beta != 0.f ? acc + beta * *o : acc;
         }
     }
@@ -352,7 +352,8 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.tiles_m = ceil_div(p.M, BM * lp.cg);
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
-    const bool partial = lp.splits > 1 || beta != 0.f;
+    const bool partial = lp.splits > 1 || beta != 0.f || p.trans_out;
+    if (p.trans_out && d_bf16) return fail(TC_INVALID_ARG, "transposed GEMM output needs fp32");
     if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
     if (partial) {
@@ -396,7 +397,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         if (!ablate(64))
             TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
                                                      static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
-                                                     relu, beta);
+                                                     relu, beta, p.trans_out);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
@@ -506,6 +507,18 @@ static int dgrad_im2col(const tc_conv_desc* d) {
 }
 static int wgrad_im2col(const tc_conv_desc* d) { return fprop_im2col(d); }
 
+// Filter gradient with few output channels (Cout <= 64): computed as D^T = im2col(x)^T dy so the
+// wide R*S*cs side fills the 128-row MMA tile and Cout becomes the (narrow) N side, instead of
+// Cout filling 64 of 128 rows; the split-K reduce writes the transpose.  TCB_WGRAD_SWAP=0
+// disables.
+static bool wgrad_swap(const tc_conv_desc* d) {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_WGRAD_SWAP");
+        return !(e && e[0] == '0');
+    }();
+    return on && d->K <= 64 && (is_pointwise(d) || wgrad_im2col(d) == 64);
+}
+
 static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
     const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
     const long long npix_in = static_cast<long long>(d->N) * d->H * d->W;
@@ -513,6 +526,8 @@ static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
         return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2, is_pointwise(d) || fprop_im2col(d));
     if (which == 1)
         return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2, is_pointwise(d) || dgrad_im2col(d));
+    if (wgrad_swap(d))  // D^T = im2col(x)^T dy: M = R*S*cs, N = Cout
+        return plan_launch(d->R * d->S * d->cs, d->K, static_cast<int>(npix_out), 0, 4, false);
     const bool tma_ops = is_pointwise(d) || wgrad_im2col(d);
     return plan_launch(d->K, d->R * d->S * d->cs, static_cast<int>(npix_out), 0, 4, tma_ops, d->K >= 256);
 }
@@ -520,9 +535,10 @@ static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
 size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     if (!d) return 0;
     LaunchPlan lp = conv_plan(d, which);
-    if (lp.splits <= 1) return 0;
+    const bool swap = which == 2 && wgrad_swap(d);  // the transposed write goes through the reduce
+    if (lp.splits <= 1 && !swap) return 0;
     long long M = which == 2 ? d->K : 0, N = which == 2 ? static_cast<long long>(d->R) * d->S * d->cs : 0;
-    return static_cast<size_t>(lp.splits) * M * N * sizeof(float);
+    return static_cast<size_t>(std::max(1, lp.splits)) * M * N * sizeof(float);
 }
 
 }  // extern "C"
@@ -635,6 +651,27 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
     p.g = geom_of(d);
     LaunchPlan lp = conv_plan(d, 2);
     std::string err;
+    if (wgrad_swap(d)) {
+        p.M = d->R * d->S * d->cs;
+        p.N = d->K;
+        p.trans_out = 1;
+        p.b_mode = OP_TMA_MN;  // dy rows: Cout contiguous per pixel
+        if (!make_tmap_2d_bf16(&p.tmB, dy, d->ks, npix, d->ks, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+        if (is_pointwise(d)) {
+            p.a_mode = OP_TMA_MN;
+            if (!make_tmap_2d_bf16(&p.tmA, x, d->cs, npix, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+        } else {
+            p.a_mode = OP_IM2COL_MN;
+            p.i2c_lo_w = p.i2c_lo_h = -d->pad;
+            p.i2c_P = d->Ho;
+            p.i2c_Q = d->Wo;
+            if (!make_tmap_im2col(&p.tmA, x, d->N, d->H, d->W, d->cs, -d->pad, -d->pad, d->pad - (d->S - 1),
+                                  d->pad - (d->R - 1), d->stride, BK, &err, 64))
+                return fail(TC_INVALID_ARG, err);
+        }
+        return run_gemm(p, lp, dw, filter_ld(d), 0, nullptr, 0, 0, 0.f, ws, ws_bytes,
+                        static_cast<cudaStream_t>(stream));
+    }
     p.a_mode = OP_TMA_MN;
     if (!make_tmap_2d_bf16(&p.tmA, dy, d->ks, npix, d->ks, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
     if (is_pointwise(d)) {

@@ -62,6 +62,7 @@ struct GemmParams {
     CUtensorMap tmD;  // 3-D store map {N, M, splits}, SW128, box {128 B of columns, 32 rows, 1}
     int M, N, K;
     int a_mode, b_mode;
+    int trans_out;   // host-side: the split-K reduce writes D[n][m] (swapped filter gradient)
     int b_resident;  // 1: one N tile, no split-K, num_kb <= stages: B is loaded once per CTA into
                      // ring slot kb and reused by every later unit (only A streams)
     int gather_kind;            // GatherKind for OP_GATHER_K
@@ -513,6 +514,25 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
 #pragma unroll
                         for (int a = 0; a < BM / 64; ++a)
                             tma_load_2d_e<CG>(a_dst + a * BK * 128, &p.tmA, bar, m0 + a * 64, kc);
+                    } else if (p.a_mode == OP_IM2COL_MN) {
+                        // A = im2col(x)^T (swapped filter gradient): rows m = tap * cs + c in
+                        // 64-channel atoms, the 64 output pixels of this k-block along k
+                        const int pq = p.i2c_P * p.i2c_Q;
+                        const int pix = kb * BK;
+                        const int an_img = pix / pq;
+                        const int rem = pix - an_img * pq;
+                        const int oy = rem / p.i2c_Q;
+                        const int ay = oy * g.stride + p.i2c_lo_h;
+                        const int ax = (rem - oy * p.i2c_Q) * g.stride + p.i2c_lo_w;
+#pragma unroll
+                        for (int row = 0; row < BM; row += 64) {
+                            int m = m0 + row;
+                            if (m >= p.M) m = 0;  // rows past M are clipped by the reduce; load finite data
+                            const int tap = m / g.C, c = m - tap * g.C;
+                            const int kh = tap / g.S, kw = tap - kh * g.S;
+                            tma_load_im2col_4d_e<CG>(a_dst + row * BK * 2, &p.tmA, bar, c, ax, ay, an_img,
+                                                     static_cast<uint16_t>(kw), static_cast<uint16_t>(kh));
+                        }
                     } else if (p.a_mode == OP_IM2COL_K) {
                         const int tap = kb / p.i2c_cpb, cb = kb - tap * p.i2c_cpb;
                         const int kh = tap / g.S, kw = tap - kh * g.S;
@@ -573,7 +593,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         }
     } else if (warp == 1 && rank == 0) {
         // ---------------- MMA issuer (the leader CTA of a pair)
-        const bool a_mn = p.a_mode == OP_TMA_MN;
+        const bool a_mn = p.a_mode == OP_TMA_MN || p.a_mode == OP_IM2COL_MN;
         const bool a_sw64 = p.a_mode == OP_IM2COL32_K;
         const bool b_sw64 = p.b_mode == OP_IM2COL32_MN;
         const bool b_mn = p.b_mode == OP_TMA_MN || p.b_mode == OP_GATHER_MN || p.b_mode == OP_IM2COL_MN || b_sw64;
