@@ -163,6 +163,10 @@ IM2COL_CASES = [
     (2, 32, 14, 14, 96, 5, 1, 2),
     (1, 96, 12, 11, 192, 3, 2, 0),
     (2, 96, 26, 26, 256, 5, 1, 2),
+    # Cout <= 64: the filter gradient runs swapped (im2col(x)^T dy, transposed reduce)
+    (3, 64, 9, 9, 16, 3, 1, 1),
+    (2, 128, 10, 10, 32, 1, 1, 0),
+    (2, 64, 11, 11, 48, 3, 2, 1),
 ]
 
 
