@@ -45,7 +45,7 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint6
 // access before the previous kernel has completed and flushed) and immediately allows
 // its own dependents to launch, so a kernel's launch latency and prologue (barrier
 // init, TMEM allocation, tensor-map prefetch) overlap the tail of its predecessor.
-// Off by default (TCB_PDL=1 enables the attribute; see pdl_enabled()).
+// On for the GEMMs only by default (TCB_PDL, see pdl_mode() in gemm.cu).
 bool pdl_enabled();
 // Timing ablation (diagnostics only, results are wrong): TCB_ABLATE is a bit mask of kernel
 // classes whose launches are skipped, so the step-time delta is that class's in-graph cost.

@@ -13,15 +13,19 @@ namespace tcb {
 
 std::atomic<unsigned long long> g_launches{0};
 
-// Measured neutral-to-slightly-negative on the AlexNet / ResNet-50 steps (the graph already
-// hides launch latency and a GEMM CTA owns the whole register file), so it is opt-in: TCB_PDL=1.
-bool pdl_enabled() {
-    static const bool on = [] {
+// TCB_PDL: 0 off, 1 every kernel, 2 bandwidth kernels only, 3 (default) GEMMs only.  Measured
+// (same call): GEMMs only +1.1% AlexNet / +1.2% GoogLeNet, neutral ResNet-50 (the prologue --
+// barrier init, TMEM allocation, tensor-map prefetch -- overlaps the previous kernel's tail);
+// bandwidth kernels -4..-5% (their early-launched CTAs hold SM slots the predecessor needs).
+static int pdl_mode() {
+    static const int m = [] {
         const char* e = std::getenv("TCB_PDL");
-        return e && e[0] == '1';
+        return e ? std::atoi(e) : 3;
     }();
-    return on;
+    return m;
 }
+bool pdl_enabled() { return pdl_mode() == 1 || pdl_mode() == 2; }
+static bool pdl_gemm() { return pdl_mode() == 1 || pdl_mode() == 3; }
 
 static int priority_range(bool least) {
     static int lo = 0, hi = 0;
@@ -325,7 +329,7 @@ static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
     cudaLaunchAttribute attr[3];
     int na = 0;
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na++].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[na++].val.programmaticStreamSerializationAllowed = pdl_gemm() ? 1 : 0;
     attr[na].id = cudaLaunchAttributePriority;
     attr[na++].val.priority = launch_priority();
     if (CG == 2) {
