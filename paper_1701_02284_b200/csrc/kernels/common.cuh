@@ -108,6 +108,15 @@ inline cudaError_t launch_kernel_cluster(void (*kernel)(KArgs...), dim3 grid, di
 #define TCB_LAUNCH(kernel, ...) ::tcb::launch_kernel(kernel, __VA_ARGS__)  // (kernel, grid, block, smem, stream, args...)
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// Momentum-SGD update of one parameter: v = mu v + alpha (g + d p), p += v, with the
+// rounding pinned (explicit fma / mul / add) so the standalone update kernel and the update fused
+// into the FC filter-gradient epilogue produce identical bits.
+__device__ __forceinline__ void sgd_update1(float& p, float& v, float g, float mom, float lr, float decay) {
+    const float nv = __fmaf_rn(mom, v, __fmul_rn(lr, __fmaf_rn(decay, p, g)));
+    v = nv;
+    p = __fadd_rn(p, nv);
+}
 int num_sms();
 
 }  // namespace tcb

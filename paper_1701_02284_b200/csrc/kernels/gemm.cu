@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "ops.cuh"
 #include "tc_gemm.cuh"
 
 namespace tcb {
@@ -357,6 +358,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     p.tiles_n = ceil_div(p.N, lp.bn);
     p.units = p.tiles_m * p.tiles_n * p.splits;
     const bool partial = lp.splits > 1 || beta != 0.f || p.trans_out;
+    if (p.sgd_p && partial) return fail(TC_INVALID_ARG, "fused update needs an unsplit contraction");
     if (p.trans_out && d_bf16) return fail(TC_INVALID_ARG, "transposed GEMM output needs fp32");
     if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
@@ -368,6 +370,11 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         p.bias = nullptr;
         p.relu = 0;
         if (!make_tmap_store(&p.tmD, ws, false, p.N, p.M, lp.splits, p.N, &err)) return fail(TC_INVALID_ARG, err);
+    } else if (p.sgd_p) {  // fused momentum update: no gradient store
+        if (lp.cg != 1) return fail(TC_INVALID_ARG, "fused update needs single-CTA tiles");
+        p.epi = EPI_SGD;
+        p.bias = nullptr;
+        p.relu = 0;
     } else {
         p.epi = d_bf16 ? EPI_BF16 : EPI_F32;
         p.bias = bias;
@@ -427,7 +434,14 @@ size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
     return (lp.splits > 1 || a->beta != 0.f) ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
 }
 
-tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
+tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) { return tcb::gemm_args_ex(a, nullptr, stream); }
+
+}  // extern "C"
+
+namespace tcb {
+// tc_gemm_bf16, optionally with the momentum update of `sgd` fused into the epilogue (the
+// contraction is then the parameter's gradient: M x N = the parameter, unsplit, never stored)
+tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream) {
     if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0) return fail(TC_INVALID_ARG, "tc_gemm_bf16: bad shape");
     GemmParams p;
     init_params(p);
@@ -437,7 +451,19 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     p.alpha = a->alpha;
     p.mask = static_cast<const __nv_bfloat16*>(a->relu_mask);
     p.mask_ld = a->mask_ld;
-    LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
+    if (sgd) {
+        if ((reinterpret_cast<uintptr_t>(sgd->p) | reinterpret_cast<uintptr_t>(sgd->v)) & 15 ||
+            reinterpret_cast<uintptr_t>(sgd->shadow) & 7 || a->ldd % 4 || a->N % 4 || !sgd->shadow)
+            return fail(TC_INVALID_ARG, "fused update: misaligned parameter rows");
+        p.sgd_p = sgd->p;
+        p.sgd_v = sgd->v;
+        p.sgd_shadow = sgd->shadow;
+        p.sgd_ld = a->ldd;
+        p.sgd_lr = sgd->lr_alpha;
+        p.sgd_mom = sgd->momentum;
+        p.sgd_decay = sgd->decay;
+    }
+    LaunchPlan lp = plan_launch(a->M, a->N, a->K, sgd ? 1 : a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
     std::string err;
     if (a->a_layout == TC_LAYOUT_K) {
         p.a_mode = OP_TMA_K;
@@ -458,6 +484,9 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) {
     return run_gemm(p, lp, a->D, a->ldd, a->d_dtype == TC_DTYPE_BF16, a->bias, a->bias_n > 0 ? a->bias_n : a->N,
                     a->relu, a->beta, a->workspace, a->workspace_bytes, static_cast<cudaStream_t>(stream));
 }
+}  // namespace tcb
+
+extern "C" {
 
 // ---------------------------------------------------------------- convolution
 static ConvGeom geom_of(const tc_conv_desc* d) {

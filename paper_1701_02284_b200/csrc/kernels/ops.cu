@@ -1512,9 +1512,8 @@ struct SgdBatch {
 };
 
 __device__ __forceinline__ void sgd_scalar(const SgdTensor& t, long long i) {
-    const float p = t.p[i];
-    const float v = t.momentum * t.v[i] + t.lr_alpha * (t.g[i] + t.decay * p);
-    const float np = p + v;
+    float np = t.p[i], v = t.v[i];
+    sgd_update1(np, v, t.g[i], t.momentum, t.lr_alpha, t.decay);
     t.v[i] = v;
     t.p[i] = np;
     const bf16 b = __float2bfloat16_rn(np);
@@ -1545,14 +1544,13 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
             for (long long j = i; j < t.n; ++j) sgd_scalar(t, j);
             continue;
         }
-        const float4 p = *reinterpret_cast<const float4*>(t.p + i);
+        float4 np = *reinterpret_cast<const float4*>(t.p + i);
         const float4 g = __ldcs(reinterpret_cast<const float4*>(t.g + i));
         float4 v = *reinterpret_cast<const float4*>(t.v + i);
-        v.x = t.momentum * v.x + t.lr_alpha * (g.x + t.decay * p.x);
-        v.y = t.momentum * v.y + t.lr_alpha * (g.y + t.decay * p.y);
-        v.z = t.momentum * v.z + t.lr_alpha * (g.z + t.decay * p.z);
-        v.w = t.momentum * v.w + t.lr_alpha * (g.w + t.decay * p.w);
-        const float4 np = make_float4(p.x + v.x, p.y + v.y, p.z + v.z, p.w + v.w);
+        sgd_update1(np.x, v.x, g.x, t.momentum, t.lr_alpha, t.decay);
+        sgd_update1(np.y, v.y, g.y, t.momentum, t.lr_alpha, t.decay);
+        sgd_update1(np.z, v.z, g.z, t.momentum, t.lr_alpha, t.decay);
+        sgd_update1(np.w, v.w, g.w, t.momentum, t.lr_alpha, t.decay);
         *reinterpret_cast<float4*>(t.v + i) = v;
         *reinterpret_cast<float4*>(t.p + i) = np;
         if (t.shadow || t.shadow_rskc) {

@@ -145,6 +145,8 @@ struct SgdTensor {
     float lr_alpha, momentum, decay;
 };
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaStream_t st);
+// tc_gemm_bf16 with the momentum update of `sgd` (may be null) fused into the epilogue
+tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream);
 
 // fp32 parity mode: bf16 operand splits (see ops.cu).  kSplitN copies per operand; the part
 // (0 hi, 1 mid, 2 lo) of copy j is (parts >> 2j) & 3.  A-side and B-side part lists pair up as

@@ -46,7 +46,7 @@ enum OperandMode : int {
     OP_IM2COL32_MN = 7
 };
 enum GatherKind : int { GATHER_FPROP = 0, GATHER_DGRAD = 1 };
-enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1 };
+enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_SGD = 2 };
 
 // Implicit-GEMM geometry.  Activations are NHWC with a channel stride that is a
 // multiple of 8 (16-byte chunks never straddle two filter taps).
@@ -63,6 +63,13 @@ struct GemmParams {
     int M, N, K;
     int a_mode, b_mode;
     int trans_out;   // host-side: the split-K reduce writes D[n][m] (swapped filter gradient)
+    // EPI_SGD: the tile is a filter gradient; apply the momentum update to p / v (fp32, row
+    // stride sgd_ld) and refresh the bf16 shadow instead of storing the gradient
+    float* sgd_p;
+    float* sgd_v;
+    __nv_bfloat16* sgd_shadow;
+    long long sgd_ld;
+    float sgd_lr, sgd_mom, sgd_decay;
     int b_resident;  // 1: one N tile, no split-K, num_kb <= stages: B is loaded once per CTA into
                      // ring slot kb and reused by every later unit (only A streams)
     int gather_kind;            // GatherKind for OP_GATHER_K
@@ -841,6 +848,31 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                         r0[j] = __float_as_uint(fmaxf(__uint_as_float(r0[j]), 0.f));
                         r1[j] = __float_as_uint(fmaxf(__uint_as_float(r1[j]), 0.f));
                     }
+                }
+                if (p.epi == EPI_SGD) {
+                    // fused update: each lane owns one parameter row segment of 64 columns
+                    const int row = m0 + quarter * 32 + lane;
+                    if (row < p.M) {
+                        float* pp = p.sgd_p + row * p.sgd_ld + nb;
+                        float* vv = p.sgd_v + row * p.sgd_ld + nb;
+                        __nv_bfloat16* sh = p.sgd_shadow + row * p.sgd_ld + nb;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            if (nb + 4 * q >= p.N) break;
+                            const uint32_t* gq = q < 8 ? &r0[4 * q] : &r1[4 * (q - 8)];
+                            float4 P4 = *reinterpret_cast<const float4*>(pp + 4 * q);
+                            float4 V4 = *reinterpret_cast<const float4*>(vv + 4 * q);
+                            sgd_update1(P4.x, V4.x, __uint_as_float(gq[0]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P4.y, V4.y, __uint_as_float(gq[1]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P4.z, V4.z, __uint_as_float(gq[2]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P4.w, V4.w, __uint_as_float(gq[3]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            *reinterpret_cast<float4*>(pp + 4 * q) = P4;
+                            *reinterpret_cast<float4*>(vv + 4 * q) = V4;
+                            *reinterpret_cast<uint2*>(sh + 4 * q) =
+                                make_uint2(pack_bf16x2(P4.x, P4.y), pack_bf16x2(P4.z, P4.w));
+                        }
+                    }
+                    continue;
                 }
                 const int nrows = bf16_out ? 1 : 2;  // 128-byte staging rows in this chunk
                 for (int sub = 0; sub < nrows; ++sub) {

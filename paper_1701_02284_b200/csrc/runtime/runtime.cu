@@ -119,6 +119,8 @@ struct tc_ctx {
     std::vector<int> fuse_bias_param;
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
     std::vector<int> fuse_add_res, fuse_add_out;    // BN forward: folded residual add (other operand, output var)
+    std::vector<char> sgd_fused;                    // per param: momentum update fused into its FC filter gradient
+    bool fuse_sgd_active = false;                   // set by run_body for update steps
     std::vector<char> pool_flag_nonpos;             // max-pool forward: flag windows with max <= 0 in the index
     std::vector<char> pool_mask_in_idx;             // max-pool backward: its folded ReLU mask is in the index
 
@@ -876,6 +878,8 @@ static bool ablate_op(int op) {
     return std::find(ops.begin(), ops.end(), op) != ops.end();
 }
 
+SgdTensor sgd_tensor(tc_ctx* c, int pidx);
+
 template <typename T>
 tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
     const tc_stmt& s = c->plan->stmts[idx];
@@ -951,6 +955,12 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
             ga.ldd = q.in_dev;
             ga.d_dtype = TC_DTYPE_F32;
             ga.alpha = 1.f;
+            if (c->fuse_sgd_active && c->sgd_fused[pidx]) {  // update fused into the epilogue
+                const SgdTensor t = sgd_tensor(c, pidx);
+                ga.workspace = c->ws;
+                ga.workspace_bytes = c->ws_bytes;
+                return gemm_args_ex(&ga, &t, c->st);
+            }
             return run_gemm_args(c, ga);
         }
         default: break;
@@ -1282,13 +1292,19 @@ tc_status flush_bucket(tc_ctx* c, int b, int update, bool overlap) {
         return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
     if (!update) return TC_OK;
     std::vector<SgdTensor> ts;
-    for (int pidx : bk.params) ts.push_back(sgd_tensor(c, pidx));
+    for (int pidx : bk.params)
+        if (!(c->fuse_sgd_active && c->sgd_fused[pidx])) ts.push_back(sgd_tensor(c, pidx));
     return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
 }
 
 tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
     tc_status r = set_iter ? launch_set_iter(c->d_iter, c->h_iter[0], c->h_iter[1], c->st) : TC_OK;
     if (r != TC_OK) return r;
+    struct ActiveScope {  // the fused FC updates apply to update steps of the whole-step path only
+        tc_ctx* c;
+        ActiveScope(tc_ctx* cc, bool on) : c(cc) { c->fuse_sgd_active = on; }
+        ~ActiveScope() { c->fuse_sgd_active = false; }
+    } active(c, update != 0);
     for (int i = 0; i < c->plan->nstmts; ++i) {
         r = exec_stmt(c, i);
         if (r != TC_OK) return r;
@@ -1413,6 +1429,23 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     }
     for (size_t i = 0; i < c->params.size(); ++i)
         if (c->params[i].update_stmt < 0) return fail(TC_INTERNAL, "runtime: parameter without an Update statement");
+    // FC filter gradients whose momentum update runs in the GEMM epilogue (world size 1, no
+    // gradient clipping, not the keep / fp32 parity modes): the gradient never reaches HBM and
+    // the separate update pass skips them.  Opt-in (TCB_SGD_FUSE=1): bit-identical to the
+    // separate update (tests/test_step_gpu.py), but the epilogue's per-row fp32 p / v traffic is
+    // uncoalesced (one row per lane) and measured AlexNet 74.8k -> 60.4k images/s; a TMA-staged
+    // p / v tile would be needed to make it pay.
+    {
+        const char* e = std::getenv("TCB_SGD_FUSE");
+        const bool on = e && e[0] == '1' && c->desc.world <= 1 && !c->desc.keep && !c->f32 && plan->clip == 0.0;
+        c->sgd_fused.assign(c->params.size(), 0);
+        for (size_t i = 0; on && i < c->params.size(); ++i) {
+            const ParamL& q = c->params[i];
+            if (q.kind == ParamL::FC && q.update_stmt >= 0 && plan->stmts[q.update_stmt].op == TC_OP_MATMUL_BWD_W &&
+                q.in_dev % 4 == 0)
+                c->sgd_fused[i] = 1;
+        }
+    }
     const char* bmb = std::getenv("TCB_BUCKET_MB");
     const long long bucket_cap = static_cast<long long>((bmb ? std::atof(bmb) : 32.0) * (1 << 20) / 4);
     c->stmt_bucket.assign(plan->nstmts, -1);
