@@ -255,8 +255,22 @@ static int forced_cg() {
 // cycle), BN=64 461 TF/s; tools/gemm_bench.py).  CTA pairs split B across the two SMs,
 // which halves its shared-memory traffic per SM.
 static double t_kblock(int bn, int cg) {
-    if (cg == 2) return bn == 256 ? 0.46e-6 : 0.25e-6;
-    return bn == 256 ? 0.48e-6 : bn == 128 ? 0.36e-6 : 0.335e-6;
+    // TCB_KB_MODEL: 0 (default) the constants below, 1 re-measured after the issue fixes, 2 only
+    // the BN = 64 one re-measured.  In-graph A/B: 1 = AlexNet -2.4%, VGG-16 +1%; 2 = noise-level;
+    // the default keeps the headline's plans.
+    static const int model = [] {
+        const char* e = std::getenv("TCB_KB_MODEL");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (model == 2 && cg == 1 && bn == 64) return 0.227e-6;
+    if (model != 1) {
+        if (cg == 2) return bn == 256 ? 0.46e-6 : 0.25e-6;
+        return bn == 256 ? 0.48e-6 : bn == 128 ? 0.36e-6 : 0.335e-6;
+    }
+    // re-measured after the uniform-datapath issue fixes (8192^3, same call): 1250 / 1033 / 685
+    // TF/s single-CTA, 1392 / 1087 TF/s CTA pairs
+    if (cg == 2) return bn == 256 ? 0.446e-6 : 0.286e-6;
+    return bn == 256 ? 0.496e-6 : bn == 128 ? 0.30e-6 : 0.227e-6;
 }
 
 // Tile width and split-K chosen by a cost model over the persistent grid: waves of
