@@ -6,6 +6,7 @@
 // line it follows.
 #include "tc_oracle.h"
 
+#include <immintrin.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -13,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -26,53 +28,208 @@ namespace {
 using i64 = int64_t;
 
 // ----------------------------------------------------------------- GEMM
-// C[M,N] (+)= op(A)[M,K] * op(B)[K,N]; row-major; every C element sums k in
-// ascending order (deterministic for any thread count).
+// C[M,N] (+)= op(A)[M,K] * op(B)[K,N]; row-major.  Every C element sums k in
+// ascending order (k-blocks in order, k in order inside a block) whatever the
+// thread count, so results are deterministic.  Packed panels + a 6 x (2 vector)
+// register micro-kernel (AVX2 FMA): fast enough that the oracle runs the
+// BASELINE shapes (AlexNet b128 steps) in seconds; the arithmetic is the plain
+// dot product of the SPEC contraction.
+template <class T>
+struct Vec;
+template <>
+struct Vec<float> {
+    using V = __m256;
+    static constexpr int L = 8;
+    static V zero() { return _mm256_setzero_ps(); }
+    static V load(const float* p) { return _mm256_loadu_ps(p); }
+    static void store(float* p, V v) { _mm256_storeu_ps(p, v); }
+    static V bcast(float a) { return _mm256_set1_ps(a); }
+    static V fma(V a, V b, V c) { return _mm256_fmadd_ps(a, b, c); }
+};
+template <>
+struct Vec<double> {
+    using V = __m256d;
+    static constexpr int L = 4;
+    static V zero() { return _mm256_setzero_pd(); }
+    static V load(const double* p) { return _mm256_loadu_pd(p); }
+    static void store(double* p, V v) { _mm256_storeu_pd(p, v); }
+    static V bcast(double a) { return _mm256_set1_pd(a); }
+    static V fma(V a, V b, V c) { return _mm256_fmadd_pd(a, b, c); }
+};
+
+constexpr int GEMM_MR = 6;
+
+// acc[MR][NR] over kc steps of packed A (MR-interleaved) and packed B (NR-interleaved).
+template <class T>
+inline void micro_kernel(int kc, const T* ap, const T* bp, T* c, i64 ldc, int mr, int nr, bool load_c) {
+    using VT = Vec<T>;
+    using V = typename VT::V;
+    constexpr int L = VT::L, NR = 2 * L;
+    V acc[GEMM_MR][2];
+    T buf[GEMM_MR][NR];
+    if (load_c) {
+        for (int i = 0; i < GEMM_MR; ++i)
+            for (int j = 0; j < NR; ++j) buf[i][j] = (i < mr && j < nr) ? c[i * ldc + j] : T(0);
+        for (int i = 0; i < GEMM_MR; ++i) {
+            acc[i][0] = VT::load(&buf[i][0]);
+            acc[i][1] = VT::load(&buf[i][L]);
+        }
+    } else {
+        for (int i = 0; i < GEMM_MR; ++i) acc[i][0] = acc[i][1] = VT::zero();
+    }
+    for (int k = 0; k < kc; ++k) {
+        const V b0 = VT::load(bp), b1 = VT::load(bp + L);
+        for (int i = 0; i < GEMM_MR; ++i) {
+            const V a = VT::bcast(ap[i]);
+            acc[i][0] = VT::fma(a, b0, acc[i][0]);
+            acc[i][1] = VT::fma(a, b1, acc[i][1]);
+        }
+        ap += GEMM_MR;
+        bp += NR;
+    }
+    if (mr == GEMM_MR && nr == NR) {
+        for (int i = 0; i < GEMM_MR; ++i) {
+            VT::store(c + i * ldc, acc[i][0]);
+            VT::store(c + i * ldc + L, acc[i][1]);
+        }
+        return;
+    }
+    for (int i = 0; i < GEMM_MR; ++i) {
+        VT::store(&buf[i][0], acc[i][0]);
+        VT::store(&buf[i][L], acc[i][1]);
+    }
+    for (int i = 0; i < mr; ++i)
+        for (int j = 0; j < nr; ++j) c[i * ldc + j] = buf[i][j];
+}
+
 template <class T>
 void gemm(int M, int N, int K, const T* A, i64 lda, bool ta, const T* B, i64 ldb, bool tb, T* C, i64 ldc, bool acc) {
-    const int JB = 64, KB = 256;
-    const int nj = (N + JB - 1) / JB;
-#pragma omp parallel for schedule(static)
-    for (int jb = 0; jb < nj; ++jb) {
-        const int j0 = jb * JB, j1 = std::min(N, j0 + JB);
-        std::vector<T> bt(static_cast<size_t>(KB) * JB);
-        for (int i = 0; i < M && !acc; ++i)
-            for (int j = j0; j < j1; ++j) C[i * ldc + j] = T(0);
-        for (int k0 = 0; k0 < K; k0 += KB) {
-            const int k1 = std::min(K, k0 + KB);
-            for (int k = k0; k < k1; ++k)
-                for (int j = j0; j < j1; ++j) bt[(k - k0) * JB + (j - j0)] = tb ? B[j * ldb + k] : B[k * ldb + j];
-            for (int i = 0; i < M; ++i) {
-                T* c = C + i * ldc;
-                T cr[64];
-                for (int j = j0; j < j1; ++j) cr[j - j0] = c[j];
-                for (int k = k0; k < k1; ++k) {
-                    const T a = ta ? A[k * lda + i] : A[i * lda + k];
-                    const T* b = &bt[(k - k0) * JB];
-                    for (int j = 0; j < j1 - j0; ++j) cr[j] += a * b[j];
+    constexpr int NR = 2 * Vec<T>::L;
+    constexpr int MB = 16 * GEMM_MR, NB = 128, KB = 256;
+    const int nmb = (M + MB - 1) / MB, nnb = (N + NB - 1) / NB;
+    if (K == 0) {
+        if (!acc)
+            for (int i = 0; i < M; ++i)
+                for (int j = 0; j < N; ++j) C[i * ldc + j] = T(0);
+        return;
+    }
+#pragma omp parallel
+    {
+        std::vector<T> ap(static_cast<size_t>(MB) * KB), bp(static_cast<size_t>(NB) * KB);
+#pragma omp for collapse(2) schedule(static)
+        for (int mb = 0; mb < nmb; ++mb)
+            for (int nb = 0; nb < nnb; ++nb) {
+                const int i0 = mb * MB, i1 = std::min(M, i0 + MB), j0 = nb * NB, j1 = std::min(N, j0 + NB);
+                for (int k0 = 0; k0 < K; k0 += KB) {
+                    const int kc = std::min(K, k0 + KB) - k0;
+                    // pack B[k0:k0+kc, j0:j1] as NR-wide strips (zero padded), reading B contiguously
+                    const int jw = (j1 - j0 + NR - 1) / NR * NR, iw = (i1 - i0 + GEMM_MR - 1) / GEMM_MR * GEMM_MR;
+                    auto bslot = [&](int j, int k) -> T& { return bp[static_cast<i64>(j / NR) * kc * NR + k * NR + j % NR]; };
+                    auto aslot = [&](int i, int k) -> T& { return ap[static_cast<i64>(i / GEMM_MR) * kc * GEMM_MR + k * GEMM_MR + i % GEMM_MR]; };
+                    if (tb) {
+                        for (int j = 0; j < jw; ++j) {
+                            const T* col = B + static_cast<i64>(j0 + j) * ldb + k0;
+                            for (int k = 0; k < kc; ++k) bslot(j, k) = j0 + j < j1 ? col[k] : T(0);
+                        }
+                    } else {
+                        for (int k = 0; k < kc; ++k) {
+                            const T* row = B + static_cast<i64>(k0 + k) * ldb + j0;
+                            for (int j = 0; j < jw; ++j) bslot(j, k) = j0 + j < j1 ? row[j] : T(0);
+                        }
+                    }
+                    // pack A[i0:i1, k0:k0+kc] as MR-tall strips (zero padded)
+                    if (ta) {
+                        for (int k = 0; k < kc; ++k) {
+                            const T* row = A + static_cast<i64>(k0 + k) * lda + i0;
+                            for (int i = 0; i < iw; ++i) aslot(i, k) = i0 + i < i1 ? row[i] : T(0);
+                        }
+                    } else {
+                        for (int i = 0; i < iw; ++i) {
+                            const T* row = A + static_cast<i64>(i0 + i) * lda + k0;
+                            for (int k = 0; k < kc; ++k) aslot(i, k) = i0 + i < i1 ? row[k] : T(0);
+                        }
+                    }
+                    const bool load_c = acc || k0 > 0;
+                    for (int ir = i0; ir < i1; ir += GEMM_MR)
+                        for (int jr = j0; jr < j1; jr += NR)
+                            micro_kernel<T>(kc, ap.data() + static_cast<i64>(ir - i0) * kc,
+                                            bp.data() + static_cast<i64>(jr - j0) * kc, C + ir * ldc + jr, ldc,
+                                            std::min(GEMM_MR, i1 - ir), std::min(NR, j1 - jr), load_c);
                 }
-                for (int j = j0; j < j1; ++j) c[j] = cr[j - j0];
             }
-        }
     }
 }
 
 // ----------------------------------------------------------------- convolution
+// Lowered to GEMM over im2col columns, a chunk of G images per
+// GEMM so small feature maps still fill the machine: col[(c,r,s)][g*HWo + p].
 template <class T>
-void im2col(const T* x, T* col, int C, int H, int W, int R, int S, int stride, int pad, int Ho, int Wo) {
-#pragma omp parallel for schedule(static)
-    for (int c = 0; c < C; ++c)
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) {
-                T* dst = col + (static_cast<i64>(c * R + r) * S + s) * Ho * Wo;
-                for (int oh = 0; oh < Ho; ++oh) {
-                    const int ih = oh * stride - pad + r;
-                    for (int ow = 0; ow < Wo; ++ow) {
-                        const int iw = ow * stride - pad + s;
-                        dst[oh * Wo + ow] = (ih >= 0 && ih < H && iw >= 0 && iw < W) ? x[(static_cast<i64>(c) * H + ih) * W + iw] : T(0);
+void im2col(const T* x, T* col, int G, int C, int H, int W, int R, int S, int stride, int pad, int Ho, int Wo) {
+    const i64 HWo = static_cast<i64>(Ho) * Wo, ld = G * HWo;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int g = 0; g < G; ++g)
+        for (int c = 0; c < C; ++c) {
+            const T* xc = x + (static_cast<i64>(g) * C + c) * H * W;
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) {
+                    T* dst = col + static_cast<i64>((c * R + r) * S + s) * ld + g * HWo;
+                    for (int oh = 0; oh < Ho; ++oh) {
+                        const int ih = oh * stride - pad + r;
+                        for (int ow = 0; ow < Wo; ++ow) {
+                            const int iw = ow * stride - pad + s;
+                            dst[oh * Wo + ow] = (ih >= 0 && ih < H && iw >= 0 && iw < W) ? xc[static_cast<i64>(ih) * W + iw] : T(0);
+                        }
                     }
                 }
-            }
+        }
+}
+
+// dx[g, c, ih, iw] = sum over (r, s, oh, ow) that read it of col[(c,r,s)][g*HWo + oh*Wo + ow], fixed order.
+template <class T>
+void col2im(const T* col, T* dx, int G, int C, int H, int W, int R, int S, int stride, int pad, int Ho, int Wo) {
+    const i64 HWo = static_cast<i64>(Ho) * Wo, ld = G * HWo;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int g = 0; g < G; ++g)
+        for (int c = 0; c < C; ++c) {
+            T* xc = dx + (static_cast<i64>(g) * C + c) * H * W;
+            std::fill(xc, xc + static_cast<i64>(H) * W, T(0));
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) {
+                    const T* src = col + static_cast<i64>((c * R + r) * S + s) * ld + g * HWo;
+                    for (int oh = 0; oh < Ho; ++oh) {
+                        const int ih = oh * stride - pad + r;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int ow = 0; ow < Wo; ++ow) {
+                            const int iw = ow * stride - pad + s;
+                            if (iw >= 0 && iw < W) xc[static_cast<i64>(ih) * W + iw] += src[oh * Wo + ow];
+                        }
+                    }
+                }
+        }
+}
+
+// Grow-only scratch buffers reused across calls (no page-fault churn per call).
+template <class T>
+T* scratch(int slot, i64 n) {
+    static std::vector<T> bufs[4];
+    if (static_cast<i64>(bufs[slot].size()) < n) bufs[slot].resize(n);
+    return bufs[slot].data();
+}
+
+// Images per GEMM: >= ~16k columns, im2col buffer <= 64M elements.
+inline int conv_chunk(i64 CRS, i64 HWo, int N) {
+    const i64 want = (16384 + HWo - 1) / HWo;
+    const i64 cap = std::max<i64>(1, (static_cast<i64>(64) << 20) / std::max<i64>(1, CRS * HWo));
+    return static_cast<int>(std::max<i64>(1, std::min<i64>({want, cap, static_cast<i64>(N)})));
+}
+
+// [n][K][HWo] <-> [K][g*HWo] for a chunk of G images
+template <class T>
+void nk_to_kn(const T* src, T* dst, int G, int K, i64 HWo) {
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int g = 0; g < G; ++g)
+        for (int k = 0; k < K; ++k)
+            std::memcpy(dst + static_cast<i64>(k) * G * HWo + g * HWo, src + (static_cast<i64>(g) * K + k) * HWo, sizeof(T) * HWo);
 }
 
 template <class T>
@@ -80,7 +237,7 @@ void conv_fwd(const T* x, const T* w, const T* b, T* y, int N, int C, int H, int
               int pad, bool direct) {
     const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
     const i64 CRS = static_cast<i64>(C) * R * S, HWo = static_cast<i64>(Ho) * Wo;
-    if (direct) {
+    if (direct) {  // no im2col workspace
 #pragma omp parallel for collapse(2) schedule(static)
         for (int n = 0; n < N; ++n)
             for (int k = 0; k < K; ++k)
@@ -102,56 +259,56 @@ void conv_fwd(const T* x, const T* w, const T* b, T* y, int N, int C, int H, int
                     }
         return;
     }
-    std::vector<T> col(CRS * HWo);
-    for (int n = 0; n < N; ++n) {
-        im2col(x + static_cast<i64>(n) * C * H * W, col.data(), C, H, W, R, S, stride, pad, Ho, Wo);
-        T* yn = y + static_cast<i64>(n) * K * HWo;
-        gemm<T>(K, static_cast<int>(HWo), static_cast<int>(CRS), w, CRS, false, col.data(), HWo, false, yn, HWo, false);
-        if (b)
-            for (int k = 0; k < K; ++k)
-                for (i64 i = 0; i < HWo; ++i) yn[k * HWo + i] += b[k];
+    const int G = conv_chunk(CRS, HWo, N);
+    T* col = scratch<T>(0, CRS * G * HWo);
+    T* out = scratch<T>(1, static_cast<i64>(K) * G * HWo);
+    for (int n0 = 0; n0 < N; n0 += G) {
+        const int g = std::min(G, N - n0);
+        const i64 ld = g * HWo;
+        im2col(x + static_cast<i64>(n0) * C * H * W, col, g, C, H, W, R, S, stride, pad, Ho, Wo);
+        gemm<T>(K, static_cast<int>(ld), static_cast<int>(CRS), w, CRS, false, col, ld, false, out, ld, false);
+#pragma omp parallel for collapse(2) schedule(static)
+        for (int i = 0; i < g; ++i)
+            for (int k = 0; k < K; ++k) {
+                T* yk = y + ((static_cast<i64>(n0) + i) * K + k) * HWo;
+                const T* ok = out + static_cast<i64>(k) * ld + i * HWo;
+                const T bk = b ? b[k] : T(0);
+                for (i64 p = 0; p < HWo; ++p) yk[p] = b ? ok[p] + bk : ok[p];
+            }
     }
 }
 
+// dx = col2im(W^T dy): dcol[(c,r,s)][g*HWo+p] = sum_k w[k,(c,r,s)] dy[g,k,p]
 template <class T>
 void conv_bwd_data(const T* dy, const T* w, T* dx, int N, int C, int H, int W, int K, int R, int S, int stride, int pad) {
     const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
-    // dx[n,c,ih,iw] = sum_{k,r,s: ih = oh*stride - pad + r} dy[n,k,oh,ow] w[k,c,r,s]
-#pragma omp parallel for collapse(2) schedule(static)
-    for (int n = 0; n < N; ++n)
-        for (int c = 0; c < C; ++c)
-            for (int ih = 0; ih < H; ++ih)
-                for (int iw = 0; iw < W; ++iw) {
-                    T acc = T(0);
-                    for (int k = 0; k < K; ++k)
-                        for (int r = 0; r < R; ++r) {
-                            const int nh = ih + pad - r;
-                            if (nh < 0 || nh % stride) continue;
-                            const int oh = nh / stride;
-                            if (oh >= Ho) continue;
-                            for (int s = 0; s < S; ++s) {
-                                const int nw = iw + pad - s;
-                                if (nw < 0 || nw % stride) continue;
-                                const int ow = nw / stride;
-                                if (ow >= Wo) continue;
-                                acc += dy[((static_cast<i64>(n) * K + k) * Ho + oh) * Wo + ow] *
-                                       w[((static_cast<i64>(k) * C + c) * R + r) * S + s];
-                            }
-                        }
-                    dx[((static_cast<i64>(n) * C + c) * H + ih) * W + iw] = acc;
-                }
+    const i64 CRS = static_cast<i64>(C) * R * S, HWo = static_cast<i64>(Ho) * Wo;
+    const int G = conv_chunk(CRS, HWo, N);
+    T* dcol = scratch<T>(0, CRS * G * HWo);
+    T* dyk = scratch<T>(1, static_cast<i64>(K) * G * HWo);
+    for (int n0 = 0; n0 < N; n0 += G) {
+        const int g = std::min(G, N - n0);
+        const i64 ld = g * HWo;
+        nk_to_kn(dy + static_cast<i64>(n0) * K * HWo, dyk, g, K, HWo);
+        gemm<T>(static_cast<int>(CRS), static_cast<int>(ld), K, w, CRS, true, dyk, ld, false, dcol, ld, false);
+        col2im(dcol, dx + static_cast<i64>(n0) * C * H * W, g, C, H, W, R, S, stride, pad, Ho, Wo);
+    }
 }
 
+// dw[K, CRS] = sum over images and pixels (ascending) of dy[n,k,p] col[(c,r,s), p]
 template <class T>
 void conv_bwd_filter(const T* dy, const T* x, T* dw, int N, int C, int H, int W, int K, int R, int S, int stride, int pad) {
     const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
     const i64 CRS = static_cast<i64>(C) * R * S, HWo = static_cast<i64>(Ho) * Wo;
-    std::vector<T> col(CRS * HWo);
-    for (int n = 0; n < N; ++n) {
-        im2col(x + static_cast<i64>(n) * C * H * W, col.data(), C, H, W, R, S, stride, pad, Ho, Wo);
-        // dw[K, CRS] += dy_n[K, HWo] * col[CRS, HWo]^T
-        gemm<T>(K, static_cast<int>(CRS), static_cast<int>(HWo), dy + static_cast<i64>(n) * K * HWo, HWo, false,
-                col.data(), HWo, true, dw, CRS, n > 0);
+    const int G = conv_chunk(CRS, HWo, N);
+    T* col = scratch<T>(0, CRS * G * HWo);
+    T* dyk = scratch<T>(1, static_cast<i64>(K) * G * HWo);
+    for (int n0 = 0; n0 < N; n0 += G) {
+        const int g = std::min(G, N - n0);
+        const i64 ld = g * HWo;
+        im2col(x + static_cast<i64>(n0) * C * H * W, col, g, C, H, W, R, S, stride, pad, Ho, Wo);
+        nk_to_kn(dy + static_cast<i64>(n0) * K * HWo, dyk, g, K, HWo);
+        gemm<T>(K, static_cast<int>(CRS), static_cast<int>(ld), dyk, ld, false, col, ld, true, dw, CRS, n0 > 0);
     }
 }
 
@@ -469,6 +626,13 @@ public:
     std::vector<i64> trace_;
     double ws_cap_mb_ = -1.0;
     int iter_ = 0, n0_ = 0;
+    bool prof_ = std::getenv("ORC_PROFILE") != nullptr;  // per-op seconds to stderr at destruction
+    double prof_t_[TC_OP_COUNT] = {};
+    ~Exec() override {
+        if (!prof_) return;
+        for (int i = 0; i < TC_OP_COUNT; ++i)
+            if (prof_t_[i] > 0) std::fprintf(stderr, "orc op %2d: %.3f s\n", i, prof_t_[i]);
+    }
     bool bf16_ = false;  // emulate the device's bf16 activation storage and bf16 GEMM weight operands
     std::unordered_map<int, bool> f32_var_;  // vars the device keeps in fp32 / as masks (not rounded)
 
@@ -545,6 +709,7 @@ public:
         Dims a, b, c;
         switch (s.op) {
             case TC_OP_LOAD_X:
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = static_cast<T>(bx_[i]);
                 return;
             case TC_OP_LOAD_Y:
@@ -592,12 +757,14 @@ public:
             }
             case TC_OP_RELU_FWD: {
                 const T* x = get(s.in[0]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = x[i] > T(0) ? x[i] : T(0);
                 return;
             }
             case TC_OP_RELU_BWD: {
                 const T* dy = get(s.in[0]);
                 const T* fy = get(s.in[1]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = fy[i] > T(0) ? dy[i] : T(0);
                 return;
             }
@@ -628,27 +795,32 @@ public:
             case TC_OP_MUL: {
                 const T* p = get(s.in[0]);
                 const T* q = get(s.in[1]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] * q[i];
                 return;
             }
             case TC_OP_ADD: {
                 const T* p = get(s.in[0]);
                 const T* q = get(s.in[1]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] + q[i];
                 return;
             }
             case TC_OP_SCALE: {
                 const T* p = get(s.in[0]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = p[i] * static_cast<T>(s.scale);
                 return;
             }
             case TC_OP_LOG: {  // clamp at 1e-30 before Log
                 const T* p = get(s.in[0]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = std::log(std::max(p[i], static_cast<T>(1e-30)));
                 return;
             }
             case TC_OP_RECIP: {
                 const T* p = get(s.in[0]);
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = T(1) / std::max(p[i], static_cast<T>(1e-30));
                 return;
             }
@@ -678,6 +850,7 @@ public:
                 const T* x = get(s.in[0], &a);
                 const T* bb = get(s.in[1]);
                 const i64 C = a.d[1], hw = a.hw();
+#pragma omp parallel for schedule(static)
                 for (i64 i = 0; i < od.count(); ++i) y[i] = x[i] + bb[(i / hw) % C];
                 return;
             }
@@ -757,11 +930,13 @@ public:
                     Dims od;
                     od.rank = s.rank;
                     for (int j = 0; j < s.rank; ++j) od.d[j] = s.dims[j];
+                    const double t0 = prof_ ? omp_get_wtime() : 0.0;
                     eval(s, tmp, od);
+                    if (prof_) prof_t_[s.op] += omp_get_wtime() - t0;
                     if (bf16_ && !f32_var_[s.var])
                         for (auto& v : tmp) v = round_bf16(v);
                     if (!s.inplace) pool_.acquire(s.storage, od.count() * 4);
-                    store_[s.storage] = tmp;  // in place: same storage, new contents
+                    store_[s.storage].swap(tmp);  // in place: same storage, new contents
                     break;
                 }
                 case TC_STMT_DEALLOC:
@@ -773,7 +948,9 @@ public:
                     Dims od;
                     od.rank = pd.rank;
                     for (int j = 0; j < pd.rank; ++j) od.d[j] = pd.dims[j];
+                    const double t0 = prof_ ? omp_get_wtime() : 0.0;
                     eval(s, tmp, od);
+                    if (prof_) prof_t_[s.op] += omp_get_wtime() - t0;
                     grads_[s.param] = tmp;
                     if (update) {
                         // v = momentum*v + lr_alpha*(g + decay*p); p = p + v
@@ -822,7 +999,7 @@ public:
             } else {
                 eval(s, tmp, od);
             }
-            store_[s.storage] = tmp;
+            store_[s.storage].swap(tmp);
         }
         Dims d;
         const T* lg = get(tc_ref{TC_REF_VAR, plan_->logits_var}, &d);
