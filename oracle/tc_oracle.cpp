@@ -923,6 +923,7 @@ public:
         }
         double loss = 0.0;
         std::vector<T> tmp;
+        std::vector<const tc_stmt*> clipped;
         for (int i = 0; i < plan_->nstmts; ++i) {
             const tc_stmt& s = plan_->stmts[i];
             switch (s.kind) {
@@ -952,7 +953,9 @@ public:
                     eval(s, tmp, od);
                     if (prof_) prof_t_[s.op] += omp_get_wtime() - t0;
                     grads_[s.param] = tmp;
-                    if (update) {
+                    if (update && plan_->clip > 0) {
+                        clipped.push_back(&s);  // applied after the whole gradient is known
+                    } else if (update) {
                         // v = momentum*v + lr_alpha*(g + decay*p); p = p + v
                         std::vector<T>& p = params_[s.param];
                         std::vector<T>& v = vel_[s.param];
@@ -979,8 +982,34 @@ public:
             }
             trace_.push_back(pool_.st.live_bytes);
         }
+        if (!clipped.empty()) {
+            // g' = clip(g + decay p), clip = global L2-norm scaling over the
+            // concatenated gradient: g' *= min(1, clip / ||g'||_2)
+            double ss = 0.0;
+            for (const tc_stmt* u : clipped) {
+                const std::vector<T>& g = grads_[u->param];
+                const std::vector<T>& p = params_[u->param];
+                for (size_t j = 0; j < p.size(); ++j) {
+                    const double gr = static_cast<double>(g[j] + static_cast<T>(u->decay) * p[j]);
+                    ss += gr * gr;
+                }
+            }
+            const double norm = std::sqrt(ss);
+            const T sc = norm > plan_->clip ? static_cast<T>(plan_->clip / norm) : T(1);
+            last_clip_norm_ = norm;
+            for (const tc_stmt* u : clipped) {
+                const std::vector<T>& g = grads_[u->param];
+                std::vector<T>& p = params_[u->param];
+                std::vector<T>& v = vel_[u->param];
+                for (size_t j = 0; j < p.size(); ++j) {
+                    v[j] = static_cast<T>(u->momentum) * v[j] + static_cast<T>(u->lr_alpha) * (sc * (g[j] + static_cast<T>(u->decay) * p[j]));
+                    p[j] += v[j];
+                }
+            }
+        }
         return loss;
     }
+    double last_clip_norm_ = 0.0;
 
     double test(int iter, int n0) {
         iter_ = iter;

@@ -47,12 +47,6 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint6
 // init, TMEM allocation, tensor-map prefetch) overlap the tail of its predecessor.
 // On for the GEMMs only by default (TCB_PDL, see pdl_mode() in gemm.cu).
 bool pdl_enabled();
-// Timing ablation (diagnostics only, results are wrong): TCB_ABLATE is a bit mask of kernel
-// classes whose launches are skipped, so the step-time delta is that class's in-graph cost.
-//   1 channel-reduction finals, 2 channel reductions, 4 BN forward apply, 8 BN backward apply,
-//   16 residual add, 32 ReLU backward, 64 split-K reduce, 128 channel copy (concat), 256 SGD
-bool ablate(int bit);
-
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -114,6 +108,12 @@ inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b -
 // into the FC filter-gradient epilogue produce identical bits.
 __device__ __forceinline__ void sgd_update1(float& p, float& v, float g, float mom, float lr, float decay) {
     const float nv = __fmaf_rn(mom, v, __fmul_rn(lr, __fmaf_rn(decay, p, g)));
+    v = nv;
+    p = __fadd_rn(p, nv);
+}
+__device__ __forceinline__ void sgd_update1_scaled(float& p, float& v, float g, float mom, float lr, float decay,
+                                                   float scale) {
+    const float nv = __fmaf_rn(mom, v, __fmul_rn(lr, __fmul_rn(scale, __fmaf_rn(decay, p, g))));
     v = nv;
     p = __fadd_rn(p, nv);
 }

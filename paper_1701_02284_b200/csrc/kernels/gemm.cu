@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM core: tile / split-K selection, TMA
 // descriptors, the deterministic split-K reduction, and the three Convolv
 // entry points (fprop, bwd-data, bwd-filter) expressed as implicit GEMMs.
+#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -46,14 +47,6 @@ static thread_local int tl_low_priority = 0;
 int launch_priority() { return priority_range(tl_low_priority > 0); }
 LowPriorityScope::LowPriorityScope() { ++tl_low_priority; }
 LowPriorityScope::~LowPriorityScope() { --tl_low_priority; }
-
-bool ablate(int bit) {
-    static const int mask = [] {
-        const char* e = std::getenv("TCB_ABLATE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return (mask & bit) != 0;
-}
 
 int num_sms() {
     static int n = [] {
@@ -329,12 +322,16 @@ static LaunchPlan plan_launch(int M, int N, int K, int splits_req, int out_bytes
 template <int BN, int CG, int SK = 0>
 static tc_status launch_bn(const GemmParams& p, int units, cudaStream_t st) {
     const int smem = TileCfg<BN, CG, SK>::kSmemBytes;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
-    if (attr_err != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(attr_err));
+    // function attributes are per device context: opt in once per device
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TCB_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        const cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, CG, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("smem attr: ") + cudaGetErrorString(e));
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
     const int grid = std::min(units, num_sms() / CG) * CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -419,8 +416,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (partial) {
         const long long total = static_cast<long long>(p.M) * p.N;
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
-        if (!ablate(64))
-            TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
+        TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
                                                      static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
                                                      relu, beta, p.trans_out);
         TCB_LAUNCH_CHECK();

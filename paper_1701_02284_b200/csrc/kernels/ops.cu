@@ -1020,39 +1020,6 @@ __global__ void k_channel_copy8(const T* __restrict__ src, int src_cs, T* __rest
     }
 }
 
-// ---------------------------------------------------------------- dense im2col (small-C first layers)
-__global__ void k_im2col(const bf16* __restrict__ x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo,
-                         int Kp, bf16* __restrict__ col) {
-    pdl_wait();
-    pdl_trigger();
-    const int groups = Kp / 8;
-    const long long total = static_cast<long long>(xi.N) * Ho * Wo * groups;
-    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(t % groups);
-        long long m = t / groups;
-        const int ow = static_cast<int>(m % Wo);
-        long long q = m / Wo;
-        const int oh = static_cast<int>(q % Ho);
-        const int n = static_cast<int>(q / Ho);
-        __align__(16) bf16 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int kk = g * 8 + j;
-            bf16 val = __float2bfloat16_rn(0.f);
-            if (kk < R * S * xi.C) {
-                const int c = kk % xi.C;
-                const int rs = kk / xi.C;
-                const int r = rs / S, s = rs - (rs / S) * S;
-                const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
-                if (ih >= 0 && ih < xi.H && iw >= 0 && iw < xi.W)
-                    val = x[((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + c];
-            }
-            v[j] = val;
-        }
-        *reinterpret_cast<uint4*>(col + m * Kp + g * 8) = *reinterpret_cast<const uint4*>(v);
-    }
-}
 
 // ---------------------------------------------------------------- LRN v2: thread per (pixel, 8 channels)
 // Window sums over channels [c - n/2, c + n/2] read the neighbouring 16-byte
@@ -1513,7 +1480,8 @@ struct SgdBatch {
 
 __device__ __forceinline__ void sgd_scalar(const SgdTensor& t, long long i) {
     float np = t.p[i], v = t.v[i];
-    sgd_update1(np, v, t.g[i], t.momentum, t.lr_alpha, t.decay);
+    if (t.gscale) sgd_update1_scaled(np, v, t.g[i], t.momentum, t.lr_alpha, t.decay, *t.gscale);
+    else sgd_update1(np, v, t.g[i], t.momentum, t.lr_alpha, t.decay);
     t.v[i] = v;
     t.p[i] = np;
     const bf16 b = __float2bfloat16_rn(np);
@@ -1547,10 +1515,18 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
         float4 np = *reinterpret_cast<const float4*>(t.p + i);
         const float4 g = __ldcs(reinterpret_cast<const float4*>(t.g + i));
         float4 v = *reinterpret_cast<const float4*>(t.v + i);
-        sgd_update1(np.x, v.x, g.x, t.momentum, t.lr_alpha, t.decay);
-        sgd_update1(np.y, v.y, g.y, t.momentum, t.lr_alpha, t.decay);
-        sgd_update1(np.z, v.z, g.z, t.momentum, t.lr_alpha, t.decay);
-        sgd_update1(np.w, v.w, g.w, t.momentum, t.lr_alpha, t.decay);
+        if (t.gscale) {  // global-L2 gradient clipping: g' = scale * (g + decay p)
+            const float sc = *t.gscale;
+            sgd_update1_scaled(np.x, v.x, g.x, t.momentum, t.lr_alpha, t.decay, sc);
+            sgd_update1_scaled(np.y, v.y, g.y, t.momentum, t.lr_alpha, t.decay, sc);
+            sgd_update1_scaled(np.z, v.z, g.z, t.momentum, t.lr_alpha, t.decay, sc);
+            sgd_update1_scaled(np.w, v.w, g.w, t.momentum, t.lr_alpha, t.decay, sc);
+        } else {
+            sgd_update1(np.x, v.x, g.x, t.momentum, t.lr_alpha, t.decay);
+            sgd_update1(np.y, v.y, g.y, t.momentum, t.lr_alpha, t.decay);
+            sgd_update1(np.z, v.z, g.z, t.momentum, t.lr_alpha, t.decay);
+            sgd_update1(np.w, v.w, g.w, t.momentum, t.lr_alpha, t.decay);
+        }
         *reinterpret_cast<float4*>(t.v + i) = v;
         *reinterpret_cast<float4*>(t.p + i) = np;
         if (t.shadow || t.shadow_rskc) {
@@ -1570,6 +1546,50 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
     }
 }
 
+// Global L2 norm of the regularised gradient g' = g + decay * p over every parameter
+// (SPEC.md:323, 361 clipping).  Fixed grid-stride partition per launch, fp64 block
+// partials in a fixed slot per (launch, block); k_clip_scale sums them in slot order:
+// deterministic.
+constexpr int kClipBlocks = 148;
+__global__ void __launch_bounds__(256) k_sgd_sumsq(const __grid_constant__ SgdBatch b, double* partial) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double red[256];
+    const long long total = b.start4[b.nt];
+    double acc = 0.0;
+    for (long long u = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; u < total;
+         u += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = b.nt - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (b.start4[mid] <= u) lo = mid; else hi = mid - 1;
+        }
+        const SgdTensor& t = b.t[lo];
+        const long long i0 = (u - b.start4[lo]) * 4;
+        for (long long i = i0; i < i0 + 4 && i < t.n; ++i) {
+            const float gr = __fmaf_rn(t.decay, t.p[i], t.g[i]);
+            acc += static_cast<double>(gr) * gr;
+        }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int k = 128; k; k >>= 1) {
+        if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+__global__ void k_clip_scale(const double* partial, int n, float clip, float* scale) {
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x != 0) return;
+    double tot = 0.0;
+    for (int i = 0; i < n; ++i) tot += partial[i];
+    const double norm = sqrt(tot);
+    scale[0] = norm > clip ? static_cast<float>(clip / norm) : 1.f;
+    scale[1] = static_cast<float>(norm);
+}
+
 }  // namespace
 
 // ================================================================ launchers
@@ -1583,15 +1603,13 @@ tc_status launch_relu_fwd(const T* x, T* y, long long n, cudaStream_t st) {
 }
 template <typename T>
 tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStream_t st) {
-    if (!ablate(32))
-        TCB_LAUNCH(k_relu_bwd<T>, EW_GRID(n / 8), dy, y, dx, n / 8);
+    TCB_LAUNCH(k_relu_bwd<T>, EW_GRID(n / 8), dy, y, dx, n / 8);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
 template <typename T>
 tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st) {
-    if (!ablate(16))
-        TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
+    TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1756,13 +1774,6 @@ tc_status launch_lrn_bwd(const T* dy, const T* x, const T* y, T* dx, Act4 a, int
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
-tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
-                        cudaStream_t st) {
-    if (Kp % 8) return fail(TC_INVALID_ARG, "im2col: Kp must be a multiple of 8");
-    TCB_LAUNCH(k_im2col, EW_GRID(static_cast<long long>(xi.N) * Ho * Wo * (Kp / 8)), x, xi, R, S, stride, pad, Ho, Wo, Kp, col);
-    TCB_LAUNCH_CHECK();
-    return TC_OK;
-}
 template <typename T>
 tc_status launch_softmax_fwd(const T* x, long long in_ld, float* y, int rows, int F, cudaStream_t st) {
     TCB_LAUNCH(k_softmax_fwd<T>, grid_for(rows, 8), 256, 0, st, x, in_ld, y, rows, F);
@@ -1838,8 +1849,7 @@ static tc_status chan_reduce(const T* x, const T* x2, const float* stats, long l
     RedPlan rp = red_plan(rows, static_cast<int>(ld), max_clusters);
     if (2ll * rp.parts * C > max_partials) return fail(TC_INTERNAL, "channel reduction: scratch too small");
     dim3 grid(rp.tiles, rp.splits);
-    if (!ablate(2))
-        TCB_CUDA_CHECK(launch_kernel_cluster((k_chan_reduce<MODE, T>), grid, dim3(kRedThreads), 0, st, dim3(1, kRedCluster, 1),
+    TCB_CUDA_CHECK(launch_kernel_cluster((k_chan_reduce<MODE, T>), grid, dim3(kRedThreads), 0, st, dim3(1, kRedCluster, 1),
                                          x, x2, stats, rows, C, static_cast<int>(ld), rp.ct, rp.rps, rp.splits, part));
     TCB_LAUNCH_CHECK();
     *out_plan = rp;
@@ -1852,8 +1862,7 @@ tc_status launch_colsum(const T* x, long long rows, int cols, long long ld, floa
     RedPlan rp;
     tc_status s = chan_reduce<RED_SUM, T>(x, nullptr, nullptr, rows, cols, ld, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    if (!ablate(1))
-        TCB_LAUNCH((k_chan_final<RED_SUM, T>), (cols + 7) / 8, 256, 0, st, partials, rp.parts, cols, 1.f, out,
+    TCB_LAUNCH((k_chan_final<RED_SUM, T>), (cols + 7) / 8, 256, 0, st, partials, rp.parts, cols, 1.f, out,
                static_cast<const T*>(nullptr), rows, 0.f,
                                                                nullptr, nullptr, nullptr);
     TCB_LAUNCH_CHECK();
@@ -1870,8 +1879,7 @@ template <typename T>
 tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
                               cudaStream_t st) {
     if ((src_cs | dst_cs | off | c) % 8 == 0 && (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0) {
-        if (!ablate(128))
-            TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
+        TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
         TCB_LAUNCH_CHECK();
         return TC_OK;
     }
@@ -1891,13 +1899,11 @@ tc_status launch_bn_fwd(const T* x, const float* gamma, const float* beta, T* y,
     float* coef = partials + max_partials;  // caller sizes partials to max_partials + 3*C
     tc_status s = chan_reduce<RED_STATS, T>(x, nullptr, nullptr, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    if (!ablate(1))
-        TCB_LAUNCH((k_chan_final<RED_STATS, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C, 1.f, stats, x, pixels, eps, gamma,
+    TCB_LAUNCH((k_chan_final<RED_STATS, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C, 1.f, stats, x, pixels, eps, gamma,
                                                               beta, coef);
     TCB_LAUNCH_CHECK();
     const long long n8 = pixels * cs / 8;
-    if (!ablate(4))
-        TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu, res);
+    TCB_LAUNCH(k_chan_affine<T>, EW_GRID(n8), x, coef, y, n8, cs / 8, C, relu, res);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1908,8 +1914,7 @@ tc_status launch_bn_bwd_reduce(const T* dy, const T* x, const float* gamma, cons
     RedPlan rp;
     tc_status s = chan_reduce<RED_BNBWD, T>(dy, x, stats, pixels, C, cs, partials, max_partials, st, &rp);
     if (s != TC_OK) return s;
-    if (!ablate(1))
-        TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C,
+    TCB_LAUNCH((k_chan_final<RED_BNBWD, T>), (C + 7) / 8, 256, 0, st, partials, rp.parts, C,
                1.f / static_cast<float>(pixels), sums, static_cast<const T*>(nullptr), pixels, 0.f, gamma, stats,
                static_cast<float*>(nullptr));
     TCB_LAUNCH_CHECK();
@@ -1920,8 +1925,7 @@ template <typename T>
 tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, long long pixels, int C, int cs,
                               cudaStream_t st) {
     const long long n8 = pixels * cs / 8;
-    if (!ablate(8))
-        TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
+    TCB_LAUNCH(k_bn_bwd_apply<T>, EW_GRID(n8), dy, x, k, dx, n8, cs / 8, C);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -1978,12 +1982,30 @@ tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor*, cudaStream_t st) {
         const long long units = b.start4[b.nt];
         const int blocks = short_blocks ? static_cast<int>(std::min<long long>((units + kThreads - 1) / kThreads, 1ll << 30))
                                         : grid_for(units);
-        if (!ablate(256))
-            TCB_LAUNCH(k_sgd, blocks, kThreads, 0, st, b);
+        TCB_LAUNCH(k_sgd, blocks, kThreads, 0, st, b);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
 }
+
+tc_status launch_clip_scale(const SgdTensor* ts, int nt, float clip, double* partials, float* scale, cudaStream_t st) {
+    int launches = 0;
+    for (int base = 0; base < nt; base += kMaxSgd, ++launches) {
+        SgdBatch b;
+        b.nt = std::min(kMaxSgd, nt - base);
+        b.start4[0] = 0;
+        for (int i = 0; i < b.nt; ++i) {
+            b.t[i] = ts[base + i];
+            b.start4[i + 1] = b.start4[i] + (b.t[i].n + 3) / 4;
+        }
+        TCB_LAUNCH(k_sgd_sumsq, kClipBlocks, kThreads, 0, st, b, partials + static_cast<long long>(launches) * kClipBlocks);
+        TCB_LAUNCH_CHECK();
+    }
+    TCB_LAUNCH(k_clip_scale, 1, 32, 0, st, partials, launches * kClipBlocks, clip, scale);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+size_t clip_partials_doubles(int nt) { return static_cast<size_t>((nt + kMaxSgd - 1) / kMaxSgd + 1) * kClipBlocks; }
 
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st) {
     TCB_LAUNCH(k_set_iter, 1, 1, 0, st, d_iter, iter, n0);

@@ -106,11 +106,6 @@ template <typename T>
 tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, long long pixels, int C, int cs,
                               cudaStream_t st);
 
-// Dense im2col for small-channel (first-layer) convolutions: col[m][kk], m = (n, oh, ow),
-// kk = (kh, kw, c) over the REAL channels C, zero-padded to Kp (multiple of 8).
-tc_status launch_im2col(const bf16* x, Act4 xi, int R, int S, int stride, int pad, int Ho, int Wo, int Kp, bf16* col,
-                        cudaStream_t st);
-
 // Device layout of the staged input image.  s2d = 0: NHWC bf16 with channel stride cs.
 // s2d = s > 0 (space-to-depth for a stride-s first-layer conv): [N][Hs][Ws][s*s*cs] with
 // element (P, Q, (i*s + j)*cs + c) = x(n, c, s*P + i - pad, s*Q + j - pad) (0 outside).
@@ -143,8 +138,12 @@ struct SgdTensor {
     bf16* shadow_rskc;   // conv filters: [R][S][ks][cs] copy for bwd-data (may be null)
     int K, RS, cs, ks;   // shape info for the RSKC scatter (p is [K][RS][cs])
     float lr_alpha, momentum, decay;
+    const float* gscale;  // device scalar: global-L2 clip factor applied to g + decay p (null = 1)
 };
 tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaStream_t st);
+// scale[0] = min(1, clip / ||g + decay p||_2) over all tensors (scale[1] = the norm)
+tc_status launch_clip_scale(const SgdTensor* ts, int nt, float clip, double* partials, float* scale, cudaStream_t st);
+size_t clip_partials_doubles(int nt);
 // tc_gemm_bf16 with the momentum update of `sgd` (may be null) fused into the epilogue
 tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream);
 

@@ -170,6 +170,12 @@ struct tc_ctx {
     cudaEvent_t join_ev = nullptr;
     bool overlap = true;
 
+    // global-L2 gradient clipping (plan->clip > 0): every update waits for the
+    // whole gradient; the clip factor is a device scalar read by the update kernel
+    double* clip_partials = nullptr;
+    float* d_clip = nullptr;  // [0] scale, [1] norm
+    int last_update_stmt = -1;
+
     cudaGraph_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int runs[2] = {0, 0};
@@ -860,30 +866,11 @@ tc_status bn_group_sums(tc_ctx* c, int i, const float** sums) {
 }
 
 // Gradient op of an Update (or a parameter-shaped Let) into `g` (device param layout).
-// Timing ablation (diagnostics only, results are wrong): TCB_ABLATE_OPS="28,4" skips every Let
-// of those TC_OP_* codes, so the step-time delta is their in-graph cost.
-static bool ablate_op(int op) {
-    static const std::vector<int> ops = [] {
-        std::vector<int> v;
-        if (const char* e = std::getenv("TCB_ABLATE_OPS"))
-            for (const char* q = e; *q;) {
-                char* end = nullptr;
-                const long x = std::strtol(q, &end, 10);
-                if (end == q) break;
-                v.push_back(static_cast<int>(x));
-                q = *end ? end + 1 : end;
-            }
-        return v;
-    }();
-    return std::find(ops.begin(), ops.end(), op) != ops.end();
-}
-
 SgdTensor sgd_tensor(tc_ctx* c, int pidx);
 
 template <typename T>
 tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
     const tc_stmt& s = c->plan->stmts[idx];
-    if (ablate_op(s.op)) return TC_OK;
     Ptrs P{c};
     const ParamL& q = c->params[pidx];
     cudaStream_t st = c->st;
@@ -971,7 +958,6 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
 template <typename T>
 tc_status exec_let(tc_ctx* c, int i) {
     const tc_stmt& s = c->plan->stmts[i];
-    if (ablate_op(s.op)) return TC_OK;
     Ptrs P{c};
     cudaStream_t st = c->st;
     const VarL& out = c->vars.at(s.var);
@@ -1290,11 +1276,31 @@ tc_status flush_bucket(tc_ctx* c, int b, int update, bool overlap) {
     }
     if (c->comm && ncclAllReduce(c->grads + bk.off, c->grads + bk.off, bk.n, ncclFloat, ncclSum, c->comm, s2) != ncclSuccess)
         return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
-    if (!update) return TC_OK;
+    if (!update || c->plan->clip > 0) return TC_OK;  // clipped updates wait for the whole gradient (clip_update)
     std::vector<SgdTensor> ts;
     for (int pidx : bk.params)
         if (!(c->fuse_sgd_active && c->sgd_fused[pidx])) ts.push_back(sgd_tensor(c, pidx));
     return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+}
+
+// Clipped momentum update of every parameter (plan->clip > 0): the global norm of
+// g + decay p over the whole (all-reduced) gradient, then one multi-tensor update.
+tc_status clip_update(tc_ctx* c, cudaStream_t s2) {
+    std::vector<SgdTensor> ts;
+    for (size_t i = 0; i < c->params.size(); ++i) ts.push_back(sgd_tensor(c, static_cast<int>(i)));
+    tc_status r = launch_clip_scale(ts.data(), static_cast<int>(ts.size()), static_cast<float>(c->plan->clip),
+                                    c->clip_partials, c->d_clip, s2);
+    if (r != TC_OK) return r;
+    for (SgdTensor& t : ts) t.gscale = c->d_clip;
+    return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+}
+
+// Data parallel: every rank's Print holds its share of the global-batch loss (|N| = G*B);
+// the sum over ranks is the loss of the global batch.
+tc_status allreduce_loss(tc_ctx* c) {
+    if (c->comm && ncclAllReduce(c->d_loss, c->d_loss, 1, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
+        return fail(TC_NCCL_ERROR, "ncclAllReduce (loss) failed");
+    return TC_OK;
 }
 
 tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
@@ -1313,10 +1319,16 @@ tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
             if (r != TC_OK) return r;
         }
     }
+    if (update && c->plan->clip > 0) {
+        r = clip_update(c, overlap ? c->comm_st : c->st);
+        if (r != TC_OK) return r;
+    }
     if (overlap) {
         TCB_CUDA_CHECK(cudaEventRecord(c->join_ev, c->comm_st));
         TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->join_ev, 0));
     }
+    r = allreduce_loss(c);
+    if (r != TC_OK) return r;
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
     return TC_OK;
 }
@@ -1429,6 +1441,9 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     }
     for (size_t i = 0; i < c->params.size(); ++i)
         if (c->params[i].update_stmt < 0) return fail(TC_INTERNAL, "runtime: parameter without an Update statement");
+    if (!(plan->clip >= 0.0)) return fail(TC_INVALID_ARG, "solver clip must be >= 0 (0 = no clipping)");
+    for (int i = 0; i < plan->nstmts; ++i)
+        if (plan->stmts[i].kind == TC_STMT_UPDATE) c->last_update_stmt = i;
     // FC filter gradients whose momentum update runs in the GEMM epilogue (world size 1, no
     // gradient clipping, not the keep / fp32 parity modes): the gradient never reaches HBM and
     // the separate update pass skips them.  Opt-in (TCB_SGD_FUSE=1): bit-identical to the
@@ -1597,7 +1612,13 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
             for (size_t k = 0; k < c->bn_groups.size(); ++k) c->bn_groups[k].sums = c->bn_sums + offs[k];
         }
     }
-    if (desc->world > 1) {
+    if (plan->clip > 0) {
+        TCB_CUDA_CHECK(cudaMalloc(&c->clip_partials, clip_partials_doubles(static_cast<int>(c->params.size())) * sizeof(double)));
+        TCB_CUDA_CHECK(cudaMalloc(&c->d_clip, 256));
+    }
+    // NCCL: world > 1, or a 1-rank communicator when an id is supplied (exercises the
+    // all-reduce path, captured in the step's graph, on a single GPU)
+    if (desc->world > 1 || (desc->world == 1 && desc->nccl_id)) {
         if (!desc->nccl_id) return fail(TC_INVALID_ARG, "world > 1 needs an NCCL unique id");
         ncclUniqueId id;
         std::memcpy(&id, desc->nccl_id, sizeof id);
@@ -1631,6 +1652,8 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->split_buf);
     cudaFree(c->partials);
     cudaFree(c->bn_sums);
+    cudaFree(c->clip_partials);
+    cudaFree(c->d_clip);
     cudaFree(c->d_input);
     if (c->copy_st) cudaStreamSynchronize(c->copy_st);
     for (int k = 0; k < 2; ++k) {
@@ -1804,11 +1827,19 @@ tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
     r = exec_stmt(c, index);
     if (r != TC_OK) return r;
     const tc_stmt& s = c->plan->stmts[index];
+    if (s.kind == TC_STMT_PRINT) {
+        r = allreduce_loss(c);
+        if (r != TC_OK) return r;
+        TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+        return TC_OK;
+    }
     if (s.kind != TC_STMT_UPDATE) return TC_OK;
     // single-statement form: this parameter's all-reduce + update, in stream order
     ParamL& q = c->params[s.param];
     if (c->comm && ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
         return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
+    if (c->plan->clip > 0)  // the clipped update needs the whole gradient: applied at the last Update
+        return index == c->last_update_stmt ? clip_update(c, c->st) : TC_OK;
     SgdTensor t = sgd_tensor(c, s.param);
     return launch_sgd(&t, 1, nullptr, c->st);
 }
@@ -1930,6 +1961,7 @@ tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_m
     for (int i = 0; i < n && r == TC_OK; ++i) {
         r = exec_stmt(c, i);
         if (r == TC_OK && c->stmt_bucket[i] >= 0) r = flush_bucket(c, c->stmt_bucket[i], update, false);
+        if (r == TC_OK && update && i == c->last_update_stmt && c->plan->clip > 0) r = clip_update(c, c->st);
         cudaEventRecord(ev[i + 1], c->st);
     }
     cudaStreamSynchronize(c->st);

@@ -132,7 +132,7 @@ def oracle_op(net, tr, s):
 
 
 @pytest.mark.parametrize("name,batch", [("lenet", 8), ("alexnet", 2), ("inception", 4), ("googlenet", 1),
-                                        ("resnet50", 2)])
+                                        ("resnet50", 2), ("vgg16", 1)])
 def test_per_op_parity(name, batch):
     net, tr = run_device(name, batch)
     final = final_alias(net)
@@ -188,7 +188,8 @@ F32_TOL = {"CONV_FWD": 1e-4, "CONV_BWD_DATA": 1e-4, "CONV_BWD_FILTER": 1e-4, "MA
            "BN_BWD_GAMMA": 1e-4}
 
 
-@pytest.mark.parametrize("name,batch", [("lenet", 8), ("alexnet", 2), ("inception", 4), ("resnet50", 2)])
+@pytest.mark.parametrize("name,batch", [("lenet", 8), ("alexnet", 2), ("inception", 4), ("resnet50", 2),
+                                        ("vgg16", 1)])
 def test_per_op_parity_f32(name, batch):
     net, tr = run_device(name, batch, precision="f32")
     final = final_alias(net)
