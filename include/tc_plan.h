@@ -146,6 +146,14 @@ typedef struct tc_net tc_net;  /* a compiled network (plan producer output) */
  * (expr.hpp network builders).  name: lenet | alexnet |
  * vgg16 | googlenet | resnet50 | inception. */
 TC_API tc_status tc_net_compile(const char* name, int64_t batch, const tc_compile_opts* opts, tc_net** out);
+/* A network from its text description (the reference's netspec-frontend; grammar
+ * in csrc/host/netspec.hpp): data / net / solver sections, layer kinds conv, maxpool, avgpool, relu,
+ * full, flatten, softmax, dropout, lrn, concat (+ batchnorm, residual), `.` composition, weighted
+ * logloss terms.  batch > 0 overrides the data section; opts != NULL overrides its solver section.
+ * Errors: TC_COMPILE_ERROR with "<ErrKind> at line:col: message" (diag.hpp kinds). */
+TC_API tc_status tc_net_compile_spec(const char* text, int64_t batch, const tc_compile_opts* opts, tc_net** out);
+/* Data source seed and solver iteration counts of a spec-compiled network. */
+TC_API tc_status tc_net_spec_info(const tc_net* net, uint64_t* seed, int64_t* iters, int64_t* test_iters);
 TC_API void tc_net_destroy(tc_net* net);
 TC_API const tc_plan* tc_net_plan(const tc_net* net);
 /* Fig. 2 style IR dump / memory table (text or csv), verifier message ("" = valid). */

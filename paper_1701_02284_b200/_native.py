@@ -15,6 +15,8 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libtcb200" + (f"_{os.environ['TCB_LIB_VA
     "TCB_LIB_VARIANT") else "") + ".so")
 
 TC_OK = 0
+(TC_SHAPE_FAULT, TC_POOL_EXHAUSTED, TC_INVALID_ARG, TC_CUDA_ERROR, TC_NCCL_ERROR, TC_IO_ERROR,
+ TC_FORMAT_ERROR, TC_INTERNAL, TC_COMPILE_ERROR) = range(1, 10)
 STATUS_NAMES = {
     0: "TC_OK", 1: "TC_SHAPE_FAULT", 2: "TC_POOL_EXHAUSTED", 3: "TC_INVALID_ARG", 4: "TC_CUDA_ERROR",
     5: "TC_NCCL_ERROR", 6: "TC_IO_ERROR", 7: "TC_FORMAT_ERROR", 8: "TC_INTERNAL", 9: "TC_COMPILE_ERROR",
@@ -167,6 +169,8 @@ def _bind_runtime(L: C.CDLL) -> None:
 
 def _bind_plan(L: C.CDLL) -> None:
     L.tc_net_compile.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
+    L.tc_net_compile_spec.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
+    L.tc_net_spec_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.tc_net_destroy.argtypes = [C.c_void_p]
     L.tc_net_destroy.restype = None
     L.tc_net_plan.argtypes = [C.c_void_p]

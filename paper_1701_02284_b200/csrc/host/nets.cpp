@@ -14,6 +14,7 @@ ParamPtr LayerFactory::param(const std::string& name, const ParamInit& init, int
     p->name = name;
     p->init = init.kind;
     p->init_value = init.value;
+    p->sigma = init.sigma;
     p->lr_mult = init.lr_mult;
     p->decay_mult = init.decay_mult;
     p->rank = rank;

@@ -22,6 +22,7 @@ struct ParamInit {
     double value = 0.0;
     double lr_mult = 1.0;
     double decay_mult = 1.0;
+    double sigma = 0.0;  // Gaussian
     static ParamInit xavier() { return {}; }
     static ParamInit constant(double v, double lrm = 1.0, double dcm = 1.0) {
         return {InitKind::Constant, v, lrm, dcm};

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "host/compiler.hpp"
+#include "host/netspec.hpp"
 #include "status.hpp"
 #include "tc_plan.h"
 
@@ -21,6 +22,8 @@ struct tc_net {
     std::vector<tc_var_desc> vars;
     tc_plan plan{};
     std::string ir_text, table_text, table_csv, verify_text;
+    uint64_t spec_seed = 42;                       // netspec data source synthetic(seed)
+    int64_t spec_iters = 0, spec_test_iters = 0;   // netspec solver iters / test_iters
 };
 
 namespace {
@@ -193,6 +196,80 @@ void fill_param(tc_param_desc& d, const ParamSpec& ps, const Shape& s) {
     }
 }
 
+
+
+void apply_opts(CompileOptions& co, const tc_compile_opts* opts) {
+    co.solver.lr = opts->lr;
+    co.solver.momentum = opts->momentum;
+    co.solver.decay = opts->decay;
+    co.solver.clip = opts->clip;
+    co.mode = opts->mode == TC_MODE_REUSE ? MemMode::Reuse : MemMode::Dealloc;
+    co.workspace_cap_mb = opts->workspace_cap_mb;
+    co.greedy_schedule = opts->greedy_schedule != 0;
+}
+
+// Gradient derivation + IR pipeline + memplan of an elaborated network, flattened to tc_plan.
+void compile_into(tc_net* h, const CompileOptions& co) {
+    if (!(co.solver.clip >= 0.0)) fail(ErrKind::SyntaxError, "solver clip must be >= 0 (0 disables, SPEC.md:36)");
+    h->prog = compile_network(h->net, co);
+    h->report = analyze(h->prog);
+    Flattener fl(h->prog);
+    for (std::size_t i = 0; i < h->prog.params.size(); ++i) {
+        tc_param_desc d;
+        fill_param(d, *h->prog.params[i], h->prog.param_shapes[i]);
+        h->params.push_back(d);
+    }
+    for (const IrStmt& s : h->prog.train) h->stmts.push_back(fl.stmt(s));
+    for (const IrStmt& s : h->prog.test) h->test.push_back(fl.stmt(s));
+    int max_var = 0;
+    for (const auto& [id, shp] : h->prog.var_shapes) {
+        tc_var_desc v;
+        std::memset(&v, 0, sizeof v);
+        v.id = id;
+        v.rank = shp.rank();
+        for (int i = 0; i < v.rank && i < 4; ++i) v.dims[i] = shp.dims[i];
+        h->vars.push_back(v);
+        max_var = std::max(max_var, id + 1);
+    }
+    std::sort(h->vars.begin(), h->vars.end(), [](const tc_var_desc& a, const tc_var_desc& b) { return a.id < b.id; });
+    h->ir_text = dump_ir(h->prog);
+    h->table_text = format_report(h->report, false);
+    h->table_csv = format_report(h->report, true);
+    h->verify_text = verify(h->prog);
+    tc_plan& p = h->plan;
+    p.name = h->net.name.c_str();
+    p.batch = h->prog.batch;
+    p.classes = h->prog.classes;
+    for (int i = 0; i < 4; ++i) p.input_dims[i] = h->prog.input_shape.dims[i];
+    p.nparams = static_cast<int>(h->params.size());
+    p.params = h->params.data();
+    p.nstmts = static_cast<int>(h->stmts.size());
+    p.stmts = h->stmts.data();
+    p.ntest = static_cast<int>(h->test.size());
+    p.test_stmts = h->test.data();
+    p.logits_var = h->prog.logits_var;
+    p.nvars = static_cast<int>(h->vars.size());
+    p.vars = h->vars.data();
+    p.max_var = max_var;
+    p.lr = co.solver.lr;
+    p.momentum = co.solver.momentum;
+    p.decay = co.solver.decay;
+    p.clip = co.solver.clip;
+    p.mode = co.mode == MemMode::Reuse ? TC_MODE_REUSE : TC_MODE_DEALLOC;
+}
+
+template <class Fn>
+tc_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return TC_OK;
+    } catch (const CompileError& e) {
+        return tcb::fail(TC_COMPILE_ERROR, std::string(err_kind_name(e.kind)) + " at " + e.loc.to_string() + ": " + e.what());
+    } catch (const std::exception& e) {
+        return tcb::fail(TC_INTERNAL, e.what());
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -200,73 +277,47 @@ extern "C" {
 tc_status tc_net_compile(const char* name, int64_t batch, const tc_compile_opts* opts, tc_net** out) {
     if (!name || !out || batch <= 0) return tcb::fail(TC_INVALID_ARG, "tc_net_compile: bad arguments");
     *out = nullptr;
-    try {
+    return guarded([&] {
         auto h = std::make_unique<tc_net>();
         if (opts && opts->global_batch > 0) h->net.loss_card = opts->global_batch;
         build_by_name(h->net, name, batch);
         CompileOptions co;
-        if (opts) {
-            co.solver.lr = opts->lr;
-            co.solver.momentum = opts->momentum;
-            co.solver.decay = opts->decay;
-            co.solver.clip = opts->clip;
-            co.mode = opts->mode == TC_MODE_REUSE ? MemMode::Reuse : MemMode::Dealloc;
-            co.workspace_cap_mb = opts->workspace_cap_mb;
-            co.greedy_schedule = opts->greedy_schedule != 0;
-        }
+        if (opts) apply_opts(co, opts);
         co.solver.name = name;
-        h->prog = compile_network(h->net, co);
-        h->report = analyze(h->prog);
-        Flattener fl(h->prog);
-        for (std::size_t i = 0; i < h->prog.params.size(); ++i) {
-            tc_param_desc d;
-            fill_param(d, *h->prog.params[i], h->prog.param_shapes[i]);
-            h->params.push_back(d);
-        }
-        for (const IrStmt& s : h->prog.train) h->stmts.push_back(fl.stmt(s));
-        for (const IrStmt& s : h->prog.test) h->test.push_back(fl.stmt(s));
-        int max_var = 0;
-        for (const auto& [id, shp] : h->prog.var_shapes) {
-            tc_var_desc v;
-            std::memset(&v, 0, sizeof v);
-            v.id = id;
-            v.rank = shp.rank();
-            for (int i = 0; i < v.rank && i < 4; ++i) v.dims[i] = shp.dims[i];
-            h->vars.push_back(v);
-            max_var = std::max(max_var, id + 1);
-        }
-        std::sort(h->vars.begin(), h->vars.end(), [](const tc_var_desc& a, const tc_var_desc& b) { return a.id < b.id; });
-        h->ir_text = dump_ir(h->prog);
-        h->table_text = format_report(h->report, false);
-        h->table_csv = format_report(h->report, true);
-        h->verify_text = verify(h->prog);
-        tc_plan& p = h->plan;
-        p.name = h->net.name.c_str();
-        p.batch = h->prog.batch;
-        p.classes = h->prog.classes;
-        for (int i = 0; i < 4; ++i) p.input_dims[i] = h->prog.input_shape.dims[i];
-        p.nparams = static_cast<int>(h->params.size());
-        p.params = h->params.data();
-        p.nstmts = static_cast<int>(h->stmts.size());
-        p.stmts = h->stmts.data();
-        p.ntest = static_cast<int>(h->test.size());
-        p.test_stmts = h->test.data();
-        p.logits_var = h->prog.logits_var;
-        p.nvars = static_cast<int>(h->vars.size());
-        p.vars = h->vars.data();
-        p.max_var = max_var;
-        p.lr = co.solver.lr;
-        p.momentum = co.solver.momentum;
-        p.decay = co.solver.decay;
-        p.clip = co.solver.clip;
-        p.mode = co.mode == MemMode::Reuse ? TC_MODE_REUSE : TC_MODE_DEALLOC;
+        compile_into(h.get(), co);
         *out = h.release();
-        return TC_OK;
-    } catch (const CompileError& e) {
-        return tcb::fail(TC_COMPILE_ERROR, std::string(err_kind_name(e.kind)) + ": " + e.what());
-    } catch (const std::exception& e) {
-        return tcb::fail(TC_INTERNAL, e.what());
-    }
+    });
+}
+
+tc_status tc_net_compile_spec(const char* text, int64_t batch, const tc_compile_opts* opts, tc_net** out) {
+    if (!text || !out || batch < 0) return tcb::fail(TC_INVALID_ARG, "tc_net_compile_spec: bad arguments");
+    *out = nullptr;
+    return guarded([&] {
+        auto h = std::make_unique<tc_net>();
+        if (opts && opts->global_batch > 0) h->net.loss_card = opts->global_batch;
+        SpecSolver sv;
+        build_from_spec(h->net, text, batch, &sv);
+        CompileOptions co;
+        co.solver.lr = sv.lr;
+        co.solver.momentum = sv.momentum;
+        co.solver.decay = sv.decay;
+        co.solver.clip = sv.clip;
+        if (opts) apply_opts(co, opts);  // explicit options override the spec's solver section
+        co.solver.name = h->net.name;
+        h->spec_seed = sv.seed;
+        h->spec_iters = sv.iters;
+        h->spec_test_iters = sv.test_iters;
+        compile_into(h.get(), co);
+        *out = h.release();
+    });
+}
+
+tc_status tc_net_spec_info(const tc_net* net, uint64_t* seed, int64_t* iters, int64_t* test_iters) {
+    if (!net) return tcb::fail(TC_INVALID_ARG, "tc_net_spec_info: null net");
+    if (seed) *seed = net->spec_seed;
+    if (iters) *iters = net->spec_iters;
+    if (test_iters) *test_iters = net->spec_test_iters;
+    return TC_OK;
 }
 
 void tc_net_destroy(tc_net* net) { delete net; }

@@ -42,19 +42,23 @@ class CompiledNetwork:
 
     def __init__(self, name: str, batch: int, *, lr: float = 0.01, momentum: float = 0.9, decay: float = 0.0005,
                  clip: float = 0.0, mode: str = "dealloc", workspace_cap_mb: float = -1.0, greedy: bool = False,
-                 global_batch: int = 0):
+                 global_batch: int = 0, spec: str | None = None, solver_from_spec: bool = False):
         L = nat.lib()
         opts = nat.CompileOpts(lr=lr, momentum=momentum, decay=decay, clip=clip,
                                mode=nat.TC_MODE_REUSE if mode == "reuse" else nat.TC_MODE_DEALLOC,
                                workspace_cap_mb=workspace_cap_mb, greedy_schedule=int(greedy),
                                global_batch=global_batch)
         h = C.c_void_p()
-        nat.check(L.tc_net_compile(name.encode(), batch, C.byref(opts), C.byref(h)))
+        if spec is None:
+            nat.check(L.tc_net_compile(name.encode(), batch, C.byref(opts), C.byref(h)))
+        else:
+            nat.check(L.tc_net_compile_spec(spec.encode(), batch, None if solver_from_spec else C.byref(opts),
+                                            C.byref(h)))
         self._h = h
-        self.name = name
-        self.batch = batch
         self.plan_ptr = L.tc_net_plan(h)
         self.plan = self.plan_ptr.contents
+        self.name = self.plan.name.decode() if spec is not None else name
+        self.batch = self.plan.batch
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -109,5 +113,24 @@ class CompiledNetwork:
         return tuple(self.plan.input_dims[i] for i in range(4))
 
 
+    def spec_info(self) -> dict:
+        """Data-source seed and solver iteration counts of a spec-compiled network."""
+        seed, it, ti = C.c_uint64(), C.c_int64(), C.c_int64()
+        nat.check(nat.lib().tc_net_spec_info(self._h, C.byref(seed), C.byref(it), C.byref(ti)))
+        return {"seed": seed.value, "iters": it.value, "test_iters": ti.value}
+
+
 def compile_network(name: str, batch: int, **kw) -> CompiledNetwork:
     return CompiledNetwork(name, batch, **kw)
+
+
+def compile_spec(text: str, batch: int = 0, **kw) -> CompiledNetwork:
+    """parse_netspec + elaborate + compile: a user network from its text description.
+    With no solver keyword the spec's own solver section is used."""
+    solver_keys = {"lr", "momentum", "decay", "clip"}
+    return CompiledNetwork("", batch, spec=text, solver_from_spec=not (solver_keys & kw.keys()), **kw)
+
+
+def load_spec(path: str, batch: int = 0, **kw) -> CompiledNetwork:
+    with open(path) as f:
+        return compile_spec(f.read(), batch, **kw)
