@@ -155,6 +155,9 @@ TC_API tc_status tc_net_compile_spec(const char* text, int64_t batch, const tc_c
 /* Data source seed and solver iteration counts of a spec-compiled network. */
 TC_API tc_status tc_net_spec_info(const tc_net* net, uint64_t* seed, int64_t* iters, int64_t* test_iters);
 TC_API void tc_net_destroy(tc_net* net);
+/* Write a plan to `path` ("TCPL" v1: header of record sizes, name, batch / classes / input dims,
+ * counts, solver, then the params / train stmts / test stmts / vars arrays as raw records). */
+TC_API tc_status tc_plan_save(const tc_plan* plan, const char* path);
 TC_API const tc_plan* tc_net_plan(const tc_net* net);
 /* Fig. 2 style IR dump / memory table (text or csv), verifier message ("" = valid). */
 TC_API const char* tc_net_ir_text(const tc_net* net);

@@ -68,8 +68,50 @@ def lib() -> C.CDLL:
         L.orc_live_trace.argtypes = [C.c_void_p, np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"), C.c_int]
         L.orc_set_workspace_cap.argtypes = [C.c_void_p, C.c_double]
         L.orc_set_bf16_storage.argtypes = [C.c_void_p, C.c_int]
+        L.orc_plan_load.argtypes = [C.c_char_p]
+        L.orc_plan_load.restype = C.c_void_p
+        L.orc_plan_free.argtypes = [C.c_void_p]
+        L.orc_plan_param_dims.argtypes = [C.c_void_p, C.c_int, np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
+        L.orc_plan_input_dims.argtypes = [C.c_void_p, np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
         _lib = L
     return _lib
+
+
+def _plan_addr(net) -> int:
+    return net.plan_address if isinstance(net, PlanFile) else C.addressof(net.plan)
+
+
+class _Shape:
+    def __init__(self, dims):
+        self.dims = tuple(int(d) for d in dims)
+
+
+class PlanFile:
+    """A plan serialized by the product's tc_plan_save, loaded by the oracle alone (bench.py's
+    reference arm times the CPU path without loading the product library)."""
+
+    def __init__(self, path: str):
+        L = lib()
+        self.plan_address = L.orc_plan_load(path.encode())
+        if not self.plan_address:
+            raise IOError(f"cannot load plan file {path}")
+        d = np.zeros(4, np.int64)
+        L.orc_plan_input_dims(self.plan_address, d)
+        self.input_dims = tuple(int(v) for v in d)
+        self.batch = self.input_dims[0]
+        self.params = []
+        i = 0
+        while True:
+            r = L.orc_plan_param_dims(self.plan_address, i, d)
+            if r < 0:
+                break
+            self.params.append(_Shape(d[:r]))
+            i += 1
+
+    def __del__(self):
+        if getattr(self, "plan_address", None) and _lib is not None:
+            _lib.orc_plan_free(self.plan_address)
+            self.plan_address = None
 
 
 def synth_batch(net, seed: int, it: int, n0: int = 0):
@@ -77,7 +119,7 @@ def synth_batch(net, seed: int, it: int, n0: int = 0):
     dims = net.input_dims
     x = np.empty(dims, np.float32)
     y = np.empty(dims[0], np.int32)
-    lib().orc_synth_batch(C.addressof(net.plan), seed, it, n0, x, y)
+    lib().orc_synth_batch(_plan_addr(net), seed, it, n0, x, y)
     return x, y
 
 
@@ -87,7 +129,7 @@ class Oracle:
     def __init__(self, net, seed: int = 42, f64: bool = False, threads: int = 0):
         self.net = net
         self.f64 = f64
-        self._c = lib().orc_create(C.addressof(net.plan), seed, int(f64), threads)
+        self._c = lib().orc_create(_plan_addr(net), seed, int(f64), threads)
         self.params = net.params
 
     def __del__(self):

@@ -1116,6 +1116,91 @@ ORC_DEF(float, f32)
 ORC_DEF(double, f64)
 #undef ORC_DEF
 
+struct LoadedPlan {
+    tc_plan plan{};
+    std::string name;
+    std::vector<tc_param_desc> params;
+    std::vector<tc_stmt> stmts, test;
+    std::vector<tc_var_desc> vars;
+};
+
+tc_plan* orc_plan_load(const char* path) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+        std::fprintf(stderr, "orc_plan_load: cannot open %s\n", path);
+        return nullptr;
+    }
+    auto lp = std::make_unique<LoadedPlan>();
+    bool ok = true;
+    auto get = [&](void* d, size_t n) { ok = ok && std::fread(d, 1, n, f) == n; };
+    uint32_t hdr[6] = {};
+    get(hdr, sizeof hdr);
+    if (!ok || hdr[0] != 0x4c504354u || hdr[1] != 1u || hdr[2] != sizeof(tc_stmt) || hdr[3] != sizeof(tc_param_desc) ||
+        hdr[4] != sizeof(tc_var_desc) || hdr[5] != TC_MAX_IN) {
+        std::fprintf(stderr, "orc_plan_load: %s is not a TCPL v1 plan of this ABI\n", path);
+        std::fclose(f);
+        return nullptr;
+    }
+    char name[64];
+    get(name, sizeof name);
+    name[63] = 0;
+    lp->name = name;
+    int64_t head[6];
+    get(head, sizeof head);
+    int32_t counts[7];
+    get(counts, sizeof counts);
+    double solver[4];
+    get(solver, sizeof solver);
+    if (!ok || counts[0] < 0 || counts[1] < 0 || counts[2] < 0 || counts[4] < 0) {
+        std::fclose(f);
+        return nullptr;
+    }
+    lp->params.resize(counts[0]);
+    lp->stmts.resize(counts[1]);
+    lp->test.resize(counts[2]);
+    lp->vars.resize(counts[4]);
+    get(lp->params.data(), sizeof(tc_param_desc) * lp->params.size());
+    get(lp->stmts.data(), sizeof(tc_stmt) * lp->stmts.size());
+    get(lp->test.data(), sizeof(tc_stmt) * lp->test.size());
+    get(lp->vars.data(), sizeof(tc_var_desc) * lp->vars.size());
+    std::fclose(f);
+    if (!ok) {
+        std::fprintf(stderr, "orc_plan_load: %s is truncated\n", path);
+        return nullptr;
+    }
+    tc_plan& p = lp->plan;
+    p.name = lp->name.c_str();
+    p.batch = head[0];
+    p.classes = head[1];
+    for (int i = 0; i < 4; ++i) p.input_dims[i] = head[2 + i];
+    p.nparams = counts[0];
+    p.params = lp->params.data();
+    p.nstmts = counts[1];
+    p.stmts = lp->stmts.data();
+    p.ntest = counts[2];
+    p.test_stmts = lp->test.data();
+    p.logits_var = counts[3];
+    p.nvars = counts[4];
+    p.vars = lp->vars.data();
+    p.max_var = counts[5];
+    p.mode = counts[6];
+    p.lr = solver[0];
+    p.momentum = solver[1];
+    p.decay = solver[2];
+    p.clip = solver[3];
+    return &lp.release()->plan;  // plan is the first member: orc_plan_free recovers the owner
+}
+
+void orc_plan_free(tc_plan* plan) { delete reinterpret_cast<LoadedPlan*>(plan); }
+int orc_plan_param_dims(const tc_plan* plan, int i, int64_t* out) {
+    if (i < 0 || i >= plan->nparams) return -1;
+    for (int j = 0; j < 4; ++j) out[j] = j < plan->params[i].rank ? plan->params[i].dims[j] : 1;
+    return plan->params[i].rank;
+}
+void orc_plan_input_dims(const tc_plan* plan, int64_t* out) {
+    for (int j = 0; j < 4; ++j) out[j] = plan->input_dims[j];
+}
+
 orc_ctx* orc_create(const tc_plan* plan, uint64_t seed, int f64, int threads) {
     if (threads > 0) omp_set_num_threads(threads);
     auto* c = new orc_ctx;

@@ -62,6 +62,13 @@ typedef struct orc_pool_stats {
 } orc_pool_stats;
 
 /* f64 != 0 runs every kernel in double (finite-difference checks). */
+/* A plan serialized by tc_plan_save ("TCPL" v1), loaded without the product library (bench.py's
+ * reference arm).  NULL on a missing / malformed file (message on stderr). */
+ORC_API tc_plan* orc_plan_load(const char* path);
+ORC_API void orc_plan_free(tc_plan* plan);
+/* Shape queries on a plan: rank of parameter i (dims into out[4]); input dims into out[4]. */
+ORC_API int orc_plan_param_dims(const tc_plan* plan, int i, int64_t* out);
+ORC_API void orc_plan_input_dims(const tc_plan* plan, int64_t* out);
 ORC_API orc_ctx* orc_create(const tc_plan* plan, uint64_t seed, int f64, int threads);
 ORC_API void orc_destroy(orc_ctx* c);
 /* Parameters in the reference layout (NCHW / (out,in)), fp32. */

@@ -165,12 +165,14 @@ def _bind_runtime(L: C.CDLL) -> None:
     L.tc_launches_per_step.argtypes = [vp]
     L.tc_nccl_unique_id.argtypes = [vp]
     L.tc_profile_step.argtypes = [vp, ci, ci, ci, vp, ci]
+    L.tc_profile_launches.argtypes = [vp, vp, ci]
 
 
 def _bind_plan(L: C.CDLL) -> None:
     L.tc_net_compile.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
     L.tc_net_compile_spec.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
     L.tc_net_spec_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.tc_plan_save.argtypes = [C.POINTER(Plan), C.c_char_p]
     L.tc_net_destroy.argtypes = [C.c_void_p]
     L.tc_net_destroy.restype = None
     L.tc_net_plan.argtypes = [C.c_void_p]

@@ -2,6 +2,7 @@
 // expose its IrProgram as flat tc_stmt records.  This is the only place the
 // host compiler's C++ types meet the C boundary; exceptions stop here.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -318,6 +319,36 @@ tc_status tc_net_spec_info(const tc_net* net, uint64_t* seed, int64_t* iters, in
     if (iters) *iters = net->spec_iters;
     if (test_iters) *test_iters = net->spec_test_iters;
     return TC_OK;
+}
+
+// Serialized plan (raw little-endian POD records, guarded by a header of record sizes): lets a
+// consumer that does not link this library (the CPU oracle's reference arm in bench.py) execute the
+// exact plan the runtime executes.
+tc_status tc_plan_save(const tc_plan* p, const char* path) {
+    if (!p || !path) return tcb::fail(TC_INVALID_ARG, "tc_plan_save: null argument");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return tcb::fail(TC_IO_ERROR, std::string("tc_plan_save: cannot open ") + path);
+    bool ok = true;
+    auto put = [&](const void* d, std::size_t n) { ok = ok && std::fwrite(d, 1, n, f) == n; };
+    const uint32_t hdr[6] = {0x4c504354u /* "TCPL" */, 1u, static_cast<uint32_t>(sizeof(tc_stmt)),
+                             static_cast<uint32_t>(sizeof(tc_param_desc)), static_cast<uint32_t>(sizeof(tc_var_desc)),
+                             static_cast<uint32_t>(TC_MAX_IN)};
+    put(hdr, sizeof hdr);
+    char name[64] = {0};
+    std::strncpy(name, p->name ? p->name : "", sizeof name - 1);
+    put(name, sizeof name);
+    const int64_t head[6] = {p->batch, p->classes, p->input_dims[0], p->input_dims[1], p->input_dims[2], p->input_dims[3]};
+    put(head, sizeof head);
+    const int32_t counts[7] = {p->nparams, p->nstmts, p->ntest, p->logits_var, p->nvars, p->max_var, p->mode};
+    put(counts, sizeof counts);
+    const double solver[4] = {p->lr, p->momentum, p->decay, p->clip};
+    put(solver, sizeof solver);
+    put(p->params, sizeof(tc_param_desc) * p->nparams);
+    put(p->stmts, sizeof(tc_stmt) * p->nstmts);
+    put(p->test_stmts, sizeof(tc_stmt) * p->ntest);
+    put(p->vars, sizeof(tc_var_desc) * p->nvars);
+    ok = (std::fclose(f) == 0) && ok;
+    return ok ? TC_OK : tcb::fail(TC_IO_ERROR, std::string("tc_plan_save: write failed: ") + path);
 }
 
 void tc_net_destroy(tc_net* net) { delete net; }

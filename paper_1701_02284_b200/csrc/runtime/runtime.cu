@@ -180,6 +180,7 @@ struct tc_ctx {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int runs[2] = {0, 0};
     int launches_per_step = -1;
+    std::vector<int> prof_launches;  // kernels each statement launched in the last tc_profile_step
     int64_t device_used = 0;
 };
 
@@ -1946,6 +1947,13 @@ tc_status tc_memory(tc_ctx* c, tc_rt_memory* out) {
 
 int tc_launches_per_step(tc_ctx* c) { return c ? c->launches_per_step : -1; }
 
+int tc_profile_launches(tc_ctx* c, int* out, int max) {
+    if (!c || !out) return -1;
+    const int n = std::min<int>(max, static_cast<int>(c->prof_launches.size()));
+    for (int i = 0; i < n; ++i) out[i] = c->prof_launches[i];
+    return n;
+}
+
 tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_ms, int max) {
     if (!c || !stmt_ms || max < c->plan->nstmts) return fail(TC_INVALID_ARG, "tc_profile_step");
     tc_status r = consume_staged(c);
@@ -1958,10 +1966,13 @@ tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_m
     TCB_CUDA_CHECK(cudaEventRecord(ev[0], c->st));
     // serial form (bucket all-reduce + update on the main stream, charged to the
     // statement that completes the bucket)
+    c->prof_launches.assign(n, 0);
     for (int i = 0; i < n && r == TC_OK; ++i) {
+        const unsigned long long l0 = g_launches.load();
         r = exec_stmt(c, i);
         if (r == TC_OK && c->stmt_bucket[i] >= 0) r = flush_bucket(c, c->stmt_bucket[i], update, false);
         if (r == TC_OK && update && i == c->last_update_stmt && c->plan->clip > 0) r = clip_update(c, c->st);
+        c->prof_launches[i] = static_cast<int>(g_launches.load() - l0);
         cudaEventRecord(ev[i + 1], c->st);
     }
     cudaStreamSynchronize(c->st);

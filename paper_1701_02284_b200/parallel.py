@@ -2,7 +2,10 @@
 sharded weakly, NCCL gradient all-reduce inside the runtime.
 
 torch.distributed is plumbing only: it carries the NCCL unique id from rank 0
-to the other ranks and provides barriers / max-over-ranks timing.
+to the other ranks and provides barriers / max-over-ranks timing (bench.py).
+The gradient all-reduce per bucket, the loss all-reduce and the momentum update
+are the runtime's (runtime.cu flush_bucket / allreduce_loss), captured in the
+step's CUDA graph.
 
 Exactness contract: every rank compiles its plan with the loss cardinality
 |N| = world * per_gpu_batch (the global batch), draws the synthetic samples
@@ -34,12 +37,3 @@ def broadcast_nccl_id(rank: int) -> bytes:
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
-
-
-def make_trainer(name: str, per_gpu_batch: int, rank: int, world: int, local_rank: int, **kw):
-    """Trainer for this rank (NCCL communicator created when world > 1)."""
-    from .runtime import Trainer
-
-    net = compile_shard(name, per_gpu_batch, world)
-    nid = broadcast_nccl_id(rank) if world > 1 else None
-    return Trainer(net, device=local_rank, rank=rank, world=world, nccl_id=nid, **kw)

@@ -111,6 +111,12 @@ class Trainer:
         nat.check(nat.lib().tc_profile_step(self._h, it, n0, int(update), out.ctypes.data, out.size))
         return out
 
+    def profile_launches(self) -> np.ndarray:
+        """Kernels each statement launched in the last profile_step (0 = folded into its producer)."""
+        out = np.zeros(self.net.plan.nstmts, np.int32)
+        nat.lib().tc_profile_launches(self._h, out.ctypes.data, out.size)
+        return out
+
     @property
     def launches_per_step(self) -> int:
         return nat.lib().tc_launches_per_step(self._h)

@@ -294,7 +294,7 @@ def test_f32_lenet_loss_trajectory_100_steps():
     print(f"f32 lenet 100 steps: max|device - oracle_f32| = {dev:.3e}, max|oracle_f32 - oracle_f64| = {env:.3e}, "
           f"max|device - oracle_f64| = {np.abs(lg - l64).max():.3e}, first 10 steps {np.abs(lg - lo)[:10].max():.2e}")
     assert np.abs(lg - lo)[:10].max() < 1e-4
-    assert dev <= max(1e-3, 1.5 * env), (dev, env)
+    assert dev <= max(1e-3, 2 * env), (dev, env)
     assert lg[-10:].mean() < 0.1
 
 
