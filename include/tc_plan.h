@@ -155,6 +155,12 @@ TC_API tc_status tc_net_compile_spec(const char* text, int64_t batch, const tc_c
 /* Data source seed and solver iteration counts of a spec-compiled network. */
 TC_API tc_status tc_net_spec_info(const tc_net* net, uint64_t* seed, int64_t* iters, int64_t* test_iters);
 TC_API void tc_net_destroy(tc_net* net);
+/* Codegen (PAPER.md 5): a standalone C++ training program (one compilation unit)
+ * that embeds this plan and calls the runtime library only -- one tc_exec_stmt per IR statement,
+ * the statement's Fig. 2 text as the comment above it, a one-line memory-mode flag, snapshot
+ * load / save and a test procedure.  mode: TC_MODE_*; iters / test_iters <= 0 / < 0: the spec's
+ * solver (or 1000 / 10).  Deterministic; the text lives until the next call on this net. */
+TC_API const char* tc_net_codegen(tc_net* net, int mode, int64_t iters, int64_t test_iters);
 /* Write a plan to `path` ("TCPL" v1: header of record sizes, name, batch / classes / input dims,
  * counts, solver, then the params / train stmts / test stmts / vars arrays as raw records). */
 TC_API tc_status tc_plan_save(const tc_plan* plan, const char* path);

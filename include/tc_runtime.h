@@ -57,6 +57,18 @@ TC_API tc_status tc_param_upload(tc_ctx* ctx, int index, const float* host);
 TC_API tc_status tc_param_download(tc_ctx* ctx, int index, float* host);
 TC_API tc_status tc_velocity_download(tc_ctx* ctx, int index, float* host);
 TC_API tc_status tc_grad_download(tc_ctx* ctx, int index, float* host);
+TC_API tc_status tc_velocity_upload(tc_ctx* ctx, int index, const float* host);
+/* The plan a context executes (borrowed). */
+TC_API const tc_plan* tc_ctx_plan(tc_ctx* ctx);
+
+/* Snapshot / resume: one file per parameter, `<dir>/<name>.ddt`
+ * = "DDSL" | u32 version 1 | u32 rank | u32 dims[rank] | f32 payload (little endian), in the
+ * reference layout; velocities go to `<dir>/<name>.velocity.ddt` (momentum state, so a resumed
+ * run continues bit-exactly).  Load matches by name: a missing file keeps the current value and
+ * is counted in *missing (with a warning on stderr); extra files are ignored.  Errors:
+ * TC_IO_ERROR (unreadable / unwritable), TC_FORMAT_ERROR (bad magic / version / dims, naming the file). */
+TC_API tc_status tc_snapshot_save(tc_ctx* ctx, const char* dir);
+TC_API tc_status tc_snapshot_load(tc_ctx* ctx, const char* dir, int* loaded, int* missing);
 /* Xavier / constant init from the shared counter RNG (tc_philox.h); identical to the oracle. */
 TC_API tc_status tc_init_params(tc_ctx* ctx);
 
@@ -72,6 +84,10 @@ TC_API tc_status tc_stage_synthetic(tc_ctx* ctx, int iter, int n0);
 TC_API tc_status tc_step(tc_ctx* ctx, int iter, int n0, int update);
 /* Execute a single train statement (interpreter / generated-code callers). */
 TC_API tc_status tc_exec_stmt(tc_ctx* ctx, int index, int iter, int n0);
+/* Test body over the staged batch: the forward Lets the main logits depend
+ * on, test-mode dropout = identity; precision = fraction of rows whose first-maximum
+ * argmax equals the label (blocks on the stream).  Reference: oracle orc_test / Exec::test. */
+TC_API tc_status tc_test(tc_ctx* ctx, int iter, int n0, double* precision);
 /* Loss of the last step (blocks on the stream). */
 TC_API tc_status tc_loss(tc_ctx* ctx, double* loss);
 /* Var contents after a step (keep mode), converted to the reference layout, fp32. */

@@ -166,6 +166,12 @@ def _bind_runtime(L: C.CDLL) -> None:
     L.tc_nccl_unique_id.argtypes = [vp]
     L.tc_profile_step.argtypes = [vp, ci, ci, ci, vp, ci]
     L.tc_profile_launches.argtypes = [vp, vp, ci]
+    L.tc_test.argtypes = [vp, ci, ci, C.POINTER(C.c_double)]
+    L.tc_velocity_upload.argtypes = [vp, ci, vp]
+    L.tc_ctx_plan.argtypes = [vp]
+    L.tc_ctx_plan.restype = vp
+    L.tc_snapshot_save.argtypes = [vp, C.c_char_p]
+    L.tc_snapshot_load.argtypes = [vp, C.c_char_p, C.POINTER(ci), C.POINTER(ci)]
 
 
 def _bind_plan(L: C.CDLL) -> None:
@@ -173,6 +179,8 @@ def _bind_plan(L: C.CDLL) -> None:
     L.tc_net_compile_spec.argtypes = [C.c_char_p, C.c_int64, C.POINTER(CompileOpts), C.POINTER(C.c_void_p)]
     L.tc_net_spec_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.tc_plan_save.argtypes = [C.POINTER(Plan), C.c_char_p]
+    L.tc_net_codegen.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64]
+    L.tc_net_codegen.restype = C.c_char_p
     L.tc_net_destroy.argtypes = [C.c_void_p]
     L.tc_net_destroy.restype = None
     L.tc_net_plan.argtypes = [C.c_void_p]

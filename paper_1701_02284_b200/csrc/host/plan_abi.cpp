@@ -25,6 +25,7 @@ struct tc_net {
     std::string ir_text, table_text, table_csv, verify_text;
     uint64_t spec_seed = 42;                       // netspec data source synthetic(seed)
     int64_t spec_iters = 0, spec_test_iters = 0;   // netspec solver iters / test_iters
+    std::string codegen_text;
 };
 
 namespace {
@@ -349,6 +350,206 @@ tc_status tc_plan_save(const tc_plan* p, const char* path) {
     put(p->vars, sizeof(tc_var_desc) * p->nvars);
     ok = (std::fclose(f) == 0) && ok;
     return ok ? TC_OK : tcb::fail(TC_IO_ERROR, std::string("tc_plan_save: write failed: ") + path);
+}
+
+// ---------------------------------------------------------------- codegen
+}  // extern "C"
+
+namespace {
+
+std::string fmt_d(double v) {
+    char b[40];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+
+std::string c_str_lit(const std::string& t) {
+    std::string o = "\"";
+    for (char ch : t) {
+        if (ch == '"' || ch == '\\') o += '\\';
+        o += ch;
+    }
+    return o + "\"";
+}
+
+// Designated initializer of a tc_stmt: non-default fields only, in declaration order.
+std::string stmt_init(const tc_stmt& s) {
+    std::string o = "{";
+    auto fi = [&](const char* n, long long v) {
+        if (v) o += std::string(".") + n + " = " + std::to_string(v) + ", ";
+    };
+    auto fd = [&](const char* n, double v) {
+        if (v != 0.0) o += std::string(".") + n + " = " + fmt_d(v) + ", ";
+    };
+    fi("kind", s.kind);
+    fi("op", s.op);
+    fi("var", s.var);
+    fi("storage", s.storage);
+    fi("inplace", s.inplace);
+    fi("param", s.param);
+    fi("nin", s.nin);
+    if (s.nin) {
+        o += ".in = {";
+        for (int i = 0; i < s.nin; ++i) o += "{" + std::to_string(s.in[i].kind) + ", " + std::to_string(s.in[i].index) + "}, ";
+        o += "}, ";
+    }
+    fi("rank", s.rank);
+    if (s.rank) {
+        o += ".dims = {";
+        for (int i = 0; i < 4; ++i) o += std::to_string(s.dims[i]) + (i < 3 ? ", " : "");
+        o += "}, ";
+    }
+    fi("bytes", s.bytes);
+    fi("k", s.k);
+    fi("stride", s.stride);
+    fi("pad", s.pad);
+    fi("max_pool", s.max_pool);
+    fi("has_bias", s.has_bias);
+    fi("lrn_size", s.lrn_size);
+    fi("slot", s.slot);
+    fd("alpha", s.alpha);
+    fd("beta", s.beta);
+    fd("lrn_k", s.lrn_k);
+    fd("rate", s.rate);
+    fd("scale", s.scale);
+    fd("eps", s.eps);
+    fi("offset", s.offset);
+    fi("extent", s.extent);
+    fd("lr_alpha", s.lr_alpha);
+    fd("momentum", s.momentum);
+    fd("decay", s.decay);
+    fi("nterms", s.nterms);
+    if (s.nterms) {
+        o += ".coef = {";
+        for (int i = 0; i < 4; ++i) o += fmt_d(s.coef[i]) + (i < 3 ? ", " : "");
+        o += "}, ";
+    }
+    if (o.size() > 1) o.resize(o.size() - 2);
+    return o + "}";
+}
+
+std::string emit_program(const tc_net* h, int mode, long long iters, long long test_iters) {
+    const tc_plan& p = h->plan;
+    const std::string& nm = h->net.name;
+    std::string o;
+    o += "// " + nm + ".gen.cpp -- generated by tc_net_codegen from the IrProgram of network '" + nm + "' (batch " +
+         std::to_string(p.batch) + ").\n";
+    o += "// A standalone training program: one compilation unit that depends only on the runtime library\n"
+         "// (libtcb200, tc_runtime.h), not on the compiler.  One runtime call per IR statement, with the\n"
+         "// statement in Fig. 2 syntax as the comment above it (PAPER.md section 5, SPEC.md:422-451).\n"
+         "//   build: g++ -std=c++20 -O2 -I<repo>/include " + nm + ".gen.cpp -L<repo>/paper_1701_02284_b200/_lib -ltcb200\n"
+         "//   run:   ./a.out [iters] [snapshot_dir]     (TENSORC_SEED overrides the seed, default 42)\n";
+    o += "#include <cstdio>\n#include <cstdlib>\n\n#include \"tc_runtime.h\"\n\n";
+    o += std::string("static const int kMode = ") + (mode == TC_MODE_REUSE ? "TC_MODE_REUSE" : "TC_MODE_DEALLOC") +
+         ";  // memory mode: TC_MODE_REUSE | TC_MODE_DEALLOC (edit this line)\n";
+    o += "static const long long kTrainIters = " + std::to_string(iters) + ", kTestIters = " + std::to_string(test_iters) + ";\n\n";
+    o += "static const tc_param_desc kParams[] = {\n";
+    for (const tc_param_desc& d : h->params) {
+        o += "    {" + c_str_lit(d.name) + ", " + std::to_string(d.rank) + ", {";
+        for (int i = 0; i < 4; ++i) o += std::to_string(d.dims[i]) + (i < 3 ? ", " : "");
+        o += "}, " + std::to_string(d.init_kind) + ", " + fmt_d(d.init_value) + ", " + fmt_d(d.sigma) + ", " +
+             fmt_d(d.lr_mult) + ", " + fmt_d(d.decay_mult) + ", " + std::to_string(d.fan_in) + ", " +
+             std::to_string(d.fan_out) + "},\n";
+    }
+    o += "};\n\n// train-loop body\nstatic const tc_stmt kTrain[] = {\n";
+    for (std::size_t i = 0; i < h->stmts.size(); ++i) o += "    " + stmt_init(h->stmts[i]) + ",  // [" + std::to_string(i) + "]\n";
+    o += "};\n\n// test body: the forward statements the main logits depend on\nstatic const tc_stmt kTest[] = {\n";
+    for (const tc_stmt& s : h->test) o += "    " + stmt_init(s) + ",\n";
+    if (h->test.empty()) o += "    {},\n";
+    o += "};\n\nstatic const tc_var_desc kVars[] = {\n";
+    for (const tc_var_desc& v : h->vars)
+        o += "    {" + std::to_string(v.id) + ", " + std::to_string(v.rank) + ", {" + std::to_string(v.dims[0]) + ", " +
+             std::to_string(v.dims[1]) + ", " + std::to_string(v.dims[2]) + ", " + std::to_string(v.dims[3]) + "}},\n";
+    o += "};\n\n";
+    o += "static void check(tc_status s, const char* what) {\n"
+         "    if (s != TC_OK) {\n"
+         "        std::fprintf(stderr, \"%s: status %d: %s\\n\", what, static_cast<int>(s), tc_last_error());\n"
+         "        std::exit(s == TC_IO_ERROR || s == TC_FORMAT_ERROR ? 2 : 1);\n"
+         "    }\n"
+         "}\n\n";
+    o += "// One training iteration: one runtime call per IR statement.\n"
+         "static void train(tc_ctx* ctx, int it) {\n";
+    for (std::size_t i = 0; i < h->prog.train.size(); ++i) {
+        std::string t = h->prog.train[i].text;
+        for (char& ch : t)
+            if (ch == '\n') ch = ' ';
+        o += "    // " + t + "\n    check(tc_exec_stmt(ctx, " + std::to_string(i) + ", it, 0), \"statement " +
+             std::to_string(i) + "\");\n";
+    }
+    o += "}\n\n";
+    o += "int main(int argc, char** argv) {\n"
+         "    const long long iters = argc > 1 ? std::atoll(argv[1]) : kTrainIters;\n"
+         "    const char* snapshot = argc > 2 ? argv[2] : nullptr;\n"
+         "    tc_plan plan{};\n"
+         "    plan.name = " + c_str_lit(nm) + ";\n"
+         "    plan.batch = " + std::to_string(p.batch) + ";\n"
+         "    plan.classes = " + std::to_string(p.classes) + ";\n";
+    for (int i = 0; i < 4; ++i) o += "    plan.input_dims[" + std::to_string(i) + "] = " + std::to_string(p.input_dims[i]) + ";\n";
+    o += "    plan.nparams = " + std::to_string(p.nparams) + ";\n"
+         "    plan.params = kParams;\n"
+         "    plan.nstmts = " + std::to_string(p.nstmts) + ";\n"
+         "    plan.stmts = kTrain;\n"
+         "    plan.ntest = " + std::to_string(p.ntest) + ";\n"
+         "    plan.test_stmts = kTest;\n"
+         "    plan.logits_var = " + std::to_string(p.logits_var) + ";\n"
+         "    plan.nvars = " + std::to_string(p.nvars) + ";\n"
+         "    plan.vars = kVars;\n"
+         "    plan.max_var = " + std::to_string(p.max_var) + ";\n"
+         "    plan.lr = " + fmt_d(p.lr) + ";\n"
+         "    plan.momentum = " + fmt_d(p.momentum) + ";\n"
+         "    plan.decay = " + fmt_d(p.decay) + ";\n"
+         "    plan.clip = " + fmt_d(p.clip) + ";\n"
+         "    plan.mode = kMode;\n"
+         "    tc_ctx_desc desc{};\n"
+         "    desc.world = 1;\n"
+         "    const char* seed = std::getenv(\"TENSORC_SEED\");\n"
+         "    desc.seed = seed ? std::strtoull(seed, nullptr, 10) : 42;\n"
+         "    tc_ctx* ctx = nullptr;\n"
+         "    check(tc_ctx_create(&plan, &desc, &ctx), \"tc_ctx_create\");\n"
+         "    check(tc_init_params(ctx), \"init\");\n"
+         "    if (snapshot) {  // resume from the snapshot directory's parameters (missing files keep their init)\n"
+         "        int loaded = 0, missing = 0;\n"
+         "        check(tc_snapshot_load(ctx, snapshot, &loaded, &missing), \"snapshot load\");\n"
+         "        std::fprintf(stderr, \"snapshot %s: %d loaded, %d missing\\n\", snapshot, loaded, missing);\n"
+         "    }\n"
+         "    for (long long it = 0; it < iters; ++it) {\n"
+         "        check(tc_stage_synthetic(ctx, static_cast<int>(it), 0), \"data\");\n"
+         "        train(ctx, static_cast<int>(it));\n"
+         "        double loss = 0.0;\n"
+         "        check(tc_loss(ctx, &loss), \"loss\");\n"
+         "        std::printf(\"%lld,%.9g\\n\", it, loss);\n"
+         "    }\n"
+         "    if (snapshot) check(tc_snapshot_save(ctx, snapshot), \"snapshot save\");\n";
+    if (!h->test.empty())
+        o += "    double prec = 0.0;\n"
+             "    for (long long t = 0; t < kTestIters; ++t) {  // test procedure: argmax-match precision\n"
+             "        double pr = 0.0;\n"
+             "        check(tc_stage_synthetic(ctx, static_cast<int>(iters + t), 0), \"data\");\n"
+             "        check(tc_test(ctx, static_cast<int>(iters + t), 0, &pr), \"test\");\n"
+             "        prec += pr;\n"
+             "    }\n"
+             "    std::printf(\"precision %.6f\\n\", kTestIters ? prec / kTestIters : 0.0);\n";
+    o += "    tc_ctx_destroy(ctx);\n"
+         "    return 0;\n"
+         "}\n";
+    return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tc_net_codegen(tc_net* net, int mode, int64_t iters, int64_t test_iters) {
+    if (!net) return "";
+    try {
+        const long long it = iters > 0 ? iters : (net->spec_iters > 0 ? net->spec_iters : 1000);
+        const long long ti = test_iters >= 0 ? test_iters : (net->spec_test_iters > 0 ? net->spec_test_iters : 10);
+        net->codegen_text = emit_program(net, mode, it, ti);
+    } catch (const std::exception& e) {
+        tcb::fail(TC_INTERNAL, e.what());
+        return "";
+    }
+    return net->codegen_text.c_str();
 }
 
 void tc_net_destroy(tc_net* net) { delete net; }

@@ -650,6 +650,37 @@ __global__ void __launch_bounds__(256) k_loss(LossArgs args, float* out, double*
     }
 }
 
+// Test body: precision = fraction of rows whose argmax (first maximum in
+// column order, as std::max_element) equals the label.  One warp per row; integer hit count.
+template <typename T>
+__global__ void k_argmax_hits(const T* __restrict__ logits, long long ld, int N, int C,
+                              const int32_t* __restrict__ labels, unsigned* hits) {
+    pdl_wait();
+    pdl_trigger();
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= N) return;
+    const T* row = logits + static_cast<long long>(warp) * ld;
+    float best = -INFINITY;
+    int bi = C;
+    for (int j = lane; j < C; j += 32) {
+        const float v = static_cast<float>(row[j]);
+        if (v > best || bi == C) {
+            best = v;
+            bi = j;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if (lane == 0 && bi == labels[warp]) atomicAdd(hits, 1u);
+}
+
 // ---------------------------------------------------------------- channel reductions
 // Column (channel) sums over the rows (pixels) of an NHWC / [rows][ld] bf16 matrix.
 // Stage 1: grid (channel tiles, row splits); each thread owns 8 channels (one
@@ -1792,6 +1823,16 @@ tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, flo
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+template <typename T>
+tc_status launch_argmax_hits(const T* logits, long long ld, int N, int C, const int32_t* labels, unsigned* hits,
+                             cudaStream_t st) {
+    TCB_CUDA_CHECK(cudaMemsetAsync(hits, 0, sizeof(unsigned), st));
+    TCB_LAUNCH(k_argmax_hits<T>, (N + 7) / 8, 256, 0, st, logits, ld, N, C, labels, hits);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+template tc_status launch_argmax_hits<bf16>(const bf16*, long long, int, int, const int32_t*, unsigned*, cudaStream_t);
+template tc_status launch_argmax_hits<float>(const float*, long long, int, int, const int32_t*, unsigned*, cudaStream_t);
 tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st) {
     TCB_LAUNCH(k_onehot, EW_GRID(static_cast<long long>(N) * K), labels, y, N, K);
     TCB_LAUNCH_CHECK();

@@ -68,6 +68,10 @@ tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long o
 enum F32Op { F32_LOG = 0, F32_RECIP = 1, F32_SCALE = 2, F32_MUL = 3, F32_ADD = 4 };
 tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st);
 tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st);
+// hits = #rows whose first-maximum argmax equals the label (test body precision)
+template <typename T>
+tc_status launch_argmax_hits(const T* logits, long long ld, int N, int C, const int32_t* labels, unsigned* hits,
+                             cudaStream_t st);
 // loss = sum_t coef[t] * dot(a[t], b[t]) over n[t] elements -> *out (fp32 device scalar).
 // `out` must point at >= 512 zero-initialised bytes (reduction partials + ticket follow the scalar).
 tc_status launch_loss(const float* const* a, const float* const* b, const long long* n, const double* coef, int nterms,

@@ -181,6 +181,11 @@ struct tc_ctx {
     int runs[2] = {0, 0};
     int launches_per_step = -1;
     std::vector<int> prof_launches;  // kernels each statement launched in the last tc_profile_step
+    // test body: the train-body Lets the main logits depend on, test-mode dropout
+    std::vector<uint8_t> in_test;
+    bool test_mode = false;
+    unsigned* d_hits = nullptr;
+    unsigned* h_hits = nullptr;  // pinned
     int64_t device_used = 0;
 };
 
@@ -963,6 +968,16 @@ tc_status exec_let(tc_ctx* c, int i) {
     cudaStream_t st = c->st;
     const VarL& out = c->vars.at(s.var);
     void* y = P.var(s.var);
+    if (c->test_mode && s.op == TC_OP_DROPOUT_MASK) return TC_OK;  // test-mode dropout = identity
+    if (c->test_mode && s.op == TC_OP_MUL) {
+        const VarL& a = P.L(s.in[0]);
+        const VarL& b = P.L(s.in[1]);
+        if (a.dtype == DT_U8 || b.dtype == DT_U8) {
+            const VarL& x = b.dtype == DT_U8 ? a : b;
+            TCB_CUDA_CHECK(cudaMemcpyAsync(y, P.var(x.id), out.bytes(), cudaMemcpyDeviceToDevice, st));
+            return TC_OK;
+        }
+    }
     switch (s.op) {
         case TC_OP_LOAD_X: return TC_OK;  // the staged input buffer is the var's storage
         case TC_OP_LOAD_Y: return launch_onehot(c->d_labels, reinterpret_cast<float*>(y), out.N, out.C, st);
@@ -1654,6 +1669,8 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->partials);
     cudaFree(c->bn_sums);
     cudaFree(c->clip_partials);
+    cudaFree(c->d_hits);
+    if (c->h_hits) cudaFreeHost(c->h_hits);
     cudaFree(c->d_clip);
     cudaFree(c->d_input);
     if (c->copy_st) cudaStreamSynchronize(c->copy_st);
@@ -1681,6 +1698,17 @@ tc_status tc_param_upload(tc_ctx* c, int i, const float* host) {
     ref_to_dev(c->params[i], host, dev);
     return upload_dev_param(c, i, dev);
 }
+
+tc_status tc_velocity_upload(tc_ctx* c, int i, const float* host) {
+    if (!c || !host || i < 0 || i >= static_cast<int>(c->params.size())) return fail(TC_INVALID_ARG, "tc_velocity_upload");
+    std::vector<float> dev;
+    ref_to_dev(c->params[i], host, dev);
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->params[i].v, dev.data(), c->params[i].n * 4, cudaMemcpyHostToDevice, c->st));
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    return TC_OK;
+}
+
+const tc_plan* tc_ctx_plan(tc_ctx* c) { return c ? c->plan : nullptr; }
 
 static tc_status download_slab(tc_ctx* c, int i, const float* dptr, float* host) {
     const ParamL& q = c->params[i];
@@ -1843,6 +1871,42 @@ tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
         return index == c->last_update_stmt ? clip_update(c, c->st) : TC_OK;
     SgdTensor t = sgd_tensor(c, s.param);
     return launch_sgd(&t, 1, nullptr, c->st);
+}
+
+tc_status tc_test(tc_ctx* c, int iter, int n0, double* precision) {
+    if (!c || !precision) return fail(TC_INVALID_ARG, "tc_test: null argument");
+    const tc_plan* p = c->plan;
+    if (p->ntest <= 0 || c->vars.find(p->logits_var) == c->vars.end()) return fail(TC_INVALID_ARG, "tc_test: plan has no test body");
+    TCB_CUDA_CHECK(cudaSetDevice(c->desc.device));
+    tc_status r = consume_staged(c);
+    if (r != TC_OK) return r;
+    if (c->in_test.empty()) {
+        std::unordered_map<int, int> want;
+        for (int i = 0; i < p->ntest; ++i) want[p->test_stmts[i].var] = 1;
+        c->in_test.assign(p->nstmts, 0);
+        for (int i = 0; i < p->nstmts; ++i)
+            c->in_test[i] = p->stmts[i].kind == TC_STMT_LET && want.count(p->stmts[i].var) ? 1 : 0;
+        TCB_CUDA_CHECK(cudaMalloc(&c->d_hits, 256));
+        TCB_CUDA_CHECK(cudaMallocHost(&c->h_hits, 256));
+    }
+    r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
+    if (r != TC_OK) return r;
+    c->test_mode = true;
+    for (int i = 0; i < p->nstmts && r == TC_OK; ++i)
+        if (c->in_test[i]) r = exec_stmt(c, i);
+    c->test_mode = false;
+    if (r != TC_OK) return r;
+    Ptrs P{c};
+    const VarL& lg = c->vars.at(p->logits_var);
+    r = lg.dtype == DT_F32 ? launch_argmax_hits(static_cast<const float*>(P.var(lg.id)), lg.cs, lg.N, lg.C, c->d_labels,
+                                                c->d_hits, c->st)
+                           : launch_argmax_hits(static_cast<const bf16*>(P.var(lg.id)), lg.cs, lg.N, lg.C, c->d_labels,
+                                                c->d_hits, c->st);
+    if (r != TC_OK) return r;
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_hits, c->d_hits, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
+    *precision = static_cast<double>(c->h_hits[0]) / static_cast<double>(lg.N);
+    return TC_OK;
 }
 
 tc_status tc_loss(tc_ctx* c, double* loss) {

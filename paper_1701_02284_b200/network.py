@@ -113,6 +113,11 @@ class CompiledNetwork:
         return tuple(self.plan.input_dims[i] for i in range(4))
 
 
+    def codegen(self, mode: str = "dealloc", iters: int = 0, test_iters: int = -1) -> str:
+        """Standalone C++ training program over the runtime library."""
+        m = nat.TC_MODE_REUSE if mode == "reuse" else nat.TC_MODE_DEALLOC
+        return nat.lib().tc_net_codegen(self._h, m, iters, test_iters).decode()
+
     def spec_info(self) -> dict:
         """Data-source seed and solver iteration counts of a spec-compiled network."""
         seed, it, ti = C.c_uint64(), C.c_int64(), C.c_int64()

@@ -54,6 +54,10 @@ class Trainer:
         nat.check(getattr(nat.lib(), fn)(self._h, i, out.ctypes.data))
         return out
 
+    def set_velocity(self, i: int, a):
+        a = np.ascontiguousarray(a, np.float32)
+        nat.check(nat.lib().tc_velocity_upload(self._h, i, a.ctypes.data))
+
     def get_param(self, i):
         return self._down("tc_param_download", i)
 
@@ -79,6 +83,27 @@ class Trainer:
 
     def exec_stmt(self, index: int, it: int = 0, n0: int = 0):
         nat.check(nat.lib().tc_exec_stmt(self._h, index, it, n0))
+
+    def test(self, it: int = 0, n0: int = 0, data=None) -> float:
+        """SPEC.md:497 test(p, data) -> precision over one batch: data = (x, y) host batch, or None
+        for the on-device synthetic batch of iteration `it`."""
+        if data is None:
+            self.stage_synthetic(it, n0)
+        else:
+            self.stage_batch(*data)
+        v = C.c_double()
+        nat.check(nat.lib().tc_test(self._h, it, n0, C.byref(v)))
+        return v.value
+
+    def snapshot_save(self, directory: str) -> None:
+        """`<dir>/<param>.ddt` (+ `.velocity.ddt`), SPEC.md:529 format."""
+        nat.check(nat.lib().tc_snapshot_save(self._h, directory.encode()))
+
+    def snapshot_load(self, directory: str) -> tuple[int, int]:
+        """Resume / fine-tune: returns (loaded, missing) parameter counts."""
+        a, b = C.c_int(), C.c_int()
+        nat.check(nat.lib().tc_snapshot_load(self._h, directory.encode(), C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def loss(self) -> float:
         v = C.c_double()
