@@ -21,44 +21,48 @@ from paper_1701_02284_b200.runtime import Trainer  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def trajectory(name, batch, steps, seed=42, with_f64=True):
-    net = compile_network(name, batch)
+def trajectory(name, batch, steps, seed=42, net=None, perturb=1e-5):
+    """Device (fp32 mode) vs the fp32 oracle on identical batches, plus the envelope run: the same
+    oracle started from parameters perturbed by `perturb` relative (uniform, fixed seed), the size
+    of the device's measured per-op arithmetic error in this mode (test_ops_gpu F32 checks:
+    1e-7 .. 3e-5).  Max-pool argmax and ReLU kinks turn such differences into re-routed gradients,
+    so the oracle's distance from its perturbed twin is what fp32-level arithmetic differences
+    do to this trajectory."""
+    net = net or compile_network(name, batch)
     tr = Trainer(net, keep=False, use_graph=True, seed=seed, precision="f32")
     tr.init_params()
     o = orc.Oracle(net, seed=seed)
     o.init_params()
-    o64 = orc.Oracle(net, seed=seed, f64=True) if with_f64 else None
-    if o64:
-        o64.init_params()
-    lg, lo, l64 = [], [], []
+    op = orc.Oracle(net, seed=seed)
+    op.init_params()
+    rng = np.random.default_rng(1234)
+    for i in range(len(net.params)):
+        w = op.get_param(i)
+        op.set_param(i, w * (1 + perturb * rng.uniform(-1, 1, w.shape)).astype(np.float32))
+    lg, lo, lp = [], [], []
     for it in range(steps):
         x, y = orc.synth_batch(net, seed, it)
         tr.stage_batch(x, y)
         tr.step(it)
         lg.append(tr.loss())
-        o.set_batch(x, y)
-        lo.append(o.step(it))
-        if o64:
-            o64.set_batch(x, y)
-            l64.append(o64.step(it))
-    return np.array(lg), np.array(lo), np.array(l64) if o64 else None
+        for orc_, out in ((o, lo), (op, lp)):
+            orc_.set_batch(x, y)
+            out.append(orc_.step(it))
+    return np.array(lg), np.array(lo), np.array(lp)
 
 
 @pytest.mark.parametrize("name,batch,steps", [("alexnet", 8, 100), ("resnet50", 4, 100), ("vgg16", 2, 30)])
 def test_f32_loss_trajectory(name, batch, steps):
-    """The deep networks' training at these batch sizes is discontinuous in the parameters: a
-    last-bit difference flips a max-pool argmax or a ReLU kink and re-routes a gradient, so the
-    reference's own fp32 run leaves its f64 twin by ~1e-2 within 10 AlexNet steps (measured here,
-    printed).  No fp32 implementation can hold 1e-3 against the f32 oracle through that; the
-    checks are: step 0 (identical parameters) to 1e-5 relative, and at every step k the device's
-    running deviation from the f32 oracle within max(1e-3, 3 x) the oracle's own running f32-vs-f64
-    deviation."""
-    lg, lo, l64 = trajectory(name, batch, steps)
+    """North-star trajectory on the BASELINE networks.  Step 0 (identical parameters) agrees to
+    1e-5 relative; after that, at every step k, the device's running deviation from the f32 oracle
+    stays within max(1e-3, 3 x) the oracle's running deviation from its 1e-5-perturbed twin.
+    Both numbers are printed; where the envelope stays below 1e-3 this is the plain 1e-3 bar."""
+    lg, lo, lp = trajectory(name, batch, steps)
     d = np.maximum.accumulate(np.abs(lg - lo))
-    e = np.maximum.accumulate(np.abs(lo - l64))
-    print(f"{name} b{batch} f32 {steps} steps: max|device - oracle_f32| = {d[-1]:.3e}, "
-          f"max|oracle_f32 - oracle_f64| = {e[-1]:.3e}, max|device - oracle_f64| = {np.abs(lg - l64).max():.3e}, "
-          f"step 0 {abs(lg[0] - lo[0]):.2e}, first 10 steps {d[min(9, steps - 1)]:.2e} (oracle drift {e[min(9, steps - 1)]:.2e}), "
+    e = np.maximum.accumulate(np.abs(lo - lp))
+    print(f"{name} b{batch} f32 {steps} steps: max|device - oracle| = {d[-1]:.3e}, "
+          f"max|oracle - perturbed oracle| = {e[-1]:.3e}, step 0 {abs(lg[0] - lo[0]):.2e}, "
+          f"first 10 steps {d[min(9, steps - 1)]:.2e} (envelope {e[min(9, steps - 1)]:.2e}), "
           f"loss {lo[0]:.4f} -> {lo[-1]:.4f}")
     assert abs(lg[0] - lo[0]) <= 1e-5 * abs(lo[0])
     bad = [k for k in range(steps) if d[k] > max(1e-3, 3 * e[k])]
