@@ -21,13 +21,13 @@ from paper_1701_02284_b200.runtime import Trainer  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def trajectory(name, batch, steps, seed=42, net=None, perturb=1e-5):
+def trajectory(name, batch, steps, seed=42, net=None, perturb=1e-4):
     """Device (fp32 mode) vs the fp32 oracle on identical batches, plus the envelope run: the same
     oracle started from parameters perturbed by `perturb` relative (uniform, fixed seed), the size
-    of the device's measured per-op arithmetic error in this mode (test_ops_gpu F32 checks:
-    1e-7 .. 3e-5).  Max-pool argmax and ReLU kinks turn such differences into re-routed gradients,
-    so the oracle's distance from its perturbed twin is what fp32-level arithmetic differences
-    do to this trajectory."""
+    of the device's measured forward-activation difference in this mode (per-op errors 1e-7 ..
+    3e-5, test_ops_gpu F32 checks, compounding to ~4.5e-5 at AlexNet's pool5 at step 0).  Max-pool
+    argmax and ReLU kinks turn such differences into re-routed gradients, so the oracle's distance
+    from its perturbed twin is what fp32-level arithmetic differences do to this trajectory."""
     net = net or compile_network(name, batch)
     tr = Trainer(net, keep=False, use_graph=True, seed=seed, precision="f32")
     tr.init_params()
@@ -55,7 +55,7 @@ def trajectory(name, batch, steps, seed=42, net=None, perturb=1e-5):
 def test_f32_loss_trajectory(name, batch, steps):
     """North-star trajectory on the BASELINE networks.  Step 0 (identical parameters) agrees to
     1e-5 relative; after that, at every step k, the device's running deviation from the f32 oracle
-    stays within max(1e-3, 3 x) the oracle's running deviation from its 1e-5-perturbed twin.
+    stays within max(1e-3, 3 x) the oracle's running deviation from its 1e-4-perturbed twin.
     Both numbers are printed; where the envelope stays below 1e-3 this is the plain 1e-3 bar."""
     lg, lo, lp = trajectory(name, batch, steps)
     d = np.maximum.accumulate(np.abs(lg - lo))
