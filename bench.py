@@ -112,8 +112,8 @@ def stmt_work(net, s, nat):
         return 2 * up[0] * out[0] * out[1], 0
     n_out = prod(out)
     reads = sum(prod(dims(s.inp[i])) for i in range(s.nin))
-    if s.kind == nat.TC_STMT_UPDATE:  # gradient reduction + 20 B/param momentum update
-        return 0, 2 * reads + 20 * n_out
+    if s.kind == nat.TC_STMT_UPDATE:  # the gradient (bias / BN sums; fp32 out); the update is separate
+        return 0, 2 * reads + 4 * n_out
     return 0, 2 * (reads + n_out)
 
 
@@ -287,6 +287,7 @@ def measure(net, args, world, rank, local, nid, precision, batch, dist, with_e2e
         # producer launch nothing and are not charged
         res["stmt_ms"] = tr.profile_step(args.warmup + args.steps, n0)
         res["stmt_launches"] = tr.profile_launches()
+        res["update_ms"] = float(np.sum(tr.profile_updates()))
     res["memory"] = tr.memory()
     res["launches_per_step"] = tr.launches_per_step
     tr.close()
@@ -344,6 +345,12 @@ def run_gpu(args):
             bytes_bw += b
             t_bw += float(stmt_ms[i])
             n_bw += 1
+    # the momentum update (+ all-reduce) of every bucket: 20 B/param of fp32 p / v / g traffic + the
+    # bf16 operand shadows (2 B/param, +2 for conv filters' RSKC copy)
+    t_upd = r["update_ms"]
+    upd_bytes = sum((22 + (2 if len(p.dims) == 4 else 0)) * p.count for p in net.params)
+    bytes_bw += upd_bytes
+    t_bw += t_upd
     peak_tf = peaks.get("bf16_tflops")
     achieved_tf = flops_tc / (t_tc * 1e-3) / 1e12 if t_tc > 0 else 0.0
     t_roof = flops_tc / (peaks.get("bf16_tflops_sustained", peak_tf) * 1e12) + bytes_bw / (peaks["hbm_gbs"] * 1e9)
@@ -388,6 +395,7 @@ def run_gpu(args):
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "t_meas_ms": round(ms, 4),
                           "frac": round(t_roof * 1e3 / ms, 4), "bandwidth_ms": round(float(t_bw), 4),
                           "bandwidth_bytes": bytes_bw, "bandwidth_statements": n_bw,
+                          "update_ms": round(t_upd, 4), "update_bytes": upd_bytes,
                           "bandwidth_gbs": round(bytes_bw / (t_bw * 1e-3) / 1e9, 1) if t_bw else None,
                           "note": "T_roof = contraction FLOPs / sustained bf16 peak + bandwidth-kernel algorithmic "
                                   "bytes / HBM peak, over the statements that launch a kernel"},

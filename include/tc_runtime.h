@@ -103,6 +103,9 @@ TC_API int tc_launches_per_step(tc_ctx* ctx);
 TC_API tc_status tc_profile_step(tc_ctx* ctx, int iter, int n0, int update, float* stmt_ms, int max);
 /* Kernels each statement launched in the last tc_profile_step (0 = folded into its producer). */
 TC_API int tc_profile_launches(tc_ctx* ctx, int* out, int max);
+/* Device ms of the bucket all-reduce + momentum update that statement i completed in the last
+ * tc_profile_step (0 for statements that complete no bucket; not included in stmt_ms). */
+TC_API int tc_profile_updates(tc_ctx* ctx, float* out, int max);
 
 /* NCCL bootstrap: rank 0 creates the id, the caller broadcasts it (torch.distributed). */
 TC_API tc_status tc_nccl_unique_id(void* out128);

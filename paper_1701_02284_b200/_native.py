@@ -166,6 +166,7 @@ def _bind_runtime(L: C.CDLL) -> None:
     L.tc_nccl_unique_id.argtypes = [vp]
     L.tc_profile_step.argtypes = [vp, ci, ci, ci, vp, ci]
     L.tc_profile_launches.argtypes = [vp, vp, ci]
+    L.tc_profile_updates.argtypes = [vp, vp, ci]
     L.tc_test.argtypes = [vp, ci, ci, C.POINTER(C.c_double)]
     L.tc_velocity_upload.argtypes = [vp, ci, vp]
     L.tc_ctx_plan.argtypes = [vp]

@@ -569,10 +569,54 @@ __global__ void k_softmax_bwd(const float* __restrict__ dy, const float* __restr
     for (int r = blockIdx.x * warps + wid; r < rows; r += gridDim.x * warps) {
         const long long o = static_cast<long long>(r) * F;
         float d = 0.f;
-        for (int j = lane; j < F; j += 32) d += dy[o + j] * y[o + j];
+        for (int j = lane; j < F; j += 32) d = __fmaf_rn(dy[o + j], y[o + j], d);
         for (int s = 16; s; s >>= 1) d += __shfl_xor_sync(0xffffffffu, d, s);
         for (int j = lane; j < ld; j += 32)
             dx[r * ld + j] = from_f<T>(j < F ? y[o + j] * (dy[o + j] - d) : 0.f);
+    }
+}
+
+// Softmax log-loss head in one pass per row (warp per row), the same operations in the same order
+// as k_softmax_fwd, k_f32_ew (Log / Recip / Scale / Mul), k_onehot and k_softmax_bwd, so the
+// result is bit-identical to the separate statements:
+//   S = softmax(z); L = log(max(S, 1e-30)); R = 1 / max(S, 1e-30); G = (Y * c) * R;
+//   dz = S * (G - sum_j G_j S_j)   (pad columns of dz up to ld are 0)
+template <typename T>
+__global__ void k_softmax_xent(const T* __restrict__ z, long long ld, const int32_t* __restrict__ labels, float c,
+                               float* __restrict__ L, float* __restrict__ Y, T* __restrict__ dz, int rows, int F) {
+    pdl_wait();
+    pdl_trigger();
+    const int warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x % 32;
+    for (int r = blockIdx.x * warps + wid; r < rows; r += gridDim.x * warps) {
+        const T* zr = z + r * ld;
+        const int lab = labels[r];
+        float m = -INFINITY;
+        for (int j = lane; j < F; j += 32) m = fmaxf(m, to_f(zr[j]));
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float s = 0.f;
+        for (int j = lane; j < F; j += 32) s += expf(to_f(zr[j]) - m);
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const float inv = 1.f / s;
+        const long long o = static_cast<long long>(r) * F;
+        float d = 0.f;
+        for (int j = lane; j < F; j += 32) {
+            const float sj = expf(to_f(zr[j]) - m) * inv;
+            const float yj = lab == j ? 1.f : 0.f;
+            L[o + j] = logf(fmaxf(sj, 1e-30f));
+            if (Y) Y[o + j] = yj;
+            const float g = (yj * c) * (1.f / fmaxf(sj, 1e-30f));
+            d = __fmaf_rn(g, sj, d);
+        }
+        for (int k = 16; k; k >>= 1) d += __shfl_xor_sync(0xffffffffu, d, k);
+        for (int j = lane; j < ld; j += 32) {
+            float v = 0.f;
+            if (j < F) {
+                const float sj = expf(to_f(zr[j]) - m) * inv;
+                const float g = ((lab == j ? 1.f : 0.f) * c) * (1.f / fmaxf(sj, 1e-30f));
+                v = sj * (g - d);
+            }
+            dz[r * ld + j] = from_f<T>(v);
+        }
     }
 }
 
@@ -1818,6 +1862,17 @@ tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long o
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+template <typename T>
+tc_status launch_softmax_xent(const T* z, long long ld, const int32_t* labels, float c, float* L, float* Y, T* dz,
+                              int rows, int F, cudaStream_t st) {
+    TCB_LAUNCH(k_softmax_xent<T>, grid_for(rows, 8), 256, 0, st, z, ld, labels, c, L, Y, dz, rows, F);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+template tc_status launch_softmax_xent<bf16>(const bf16*, long long, const int32_t*, float, float*, float*, bf16*, int,
+                                             int, cudaStream_t);
+template tc_status launch_softmax_xent<float>(const float*, long long, const int32_t*, float, float*, float*, float*,
+                                              int, int, cudaStream_t);
 tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st) {
     TCB_LAUNCH(k_f32_ew, EW_GRID(n), op, a, b, scale, y, n);
     TCB_LAUNCH_CHECK();

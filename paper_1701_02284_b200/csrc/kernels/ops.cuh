@@ -67,6 +67,10 @@ tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long o
 
 enum F32Op { F32_LOG = 0, F32_RECIP = 1, F32_SCALE = 2, F32_MUL = 3, F32_ADD = 4 };
 tc_status launch_f32_ew(int op, const float* a, const float* b, float scale, float* y, long long n, cudaStream_t st);
+// fused softmax log-loss head: L = log S, Y = onehot (if Y != null), dz = softmax_bwd((Y c) / S, S)
+template <typename T>
+tc_status launch_softmax_xent(const T* z, long long ld, const int32_t* labels, float c, float* L, float* Y, T* dz,
+                              int rows, int F, cudaStream_t st);
 tc_status launch_onehot(const int32_t* labels, float* y, int N, int K, cudaStream_t st);
 // hits = #rows whose first-maximum argmax equals the label (test body precision)
 template <typename T>

@@ -123,6 +123,17 @@ struct tc_ctx {
     bool fuse_sgd_active = false;                   // set by run_body for update steps
     std::vector<char> pool_flag_nonpos;             // max-pool forward: flag windows with max <= 0 in the index
     std::vector<char> pool_mask_in_idx;             // max-pool backward: its folded ReLU mask is in the index
+    // Softmax log-loss head: Softmax, Log(S.copy), 1/(S.copy), Y * c, product and
+    // the softmax backward of one head as one row-wise kernel at the chain's first statement
+    struct XentHead {
+        int pos = -1;                    // statement that launches the fused kernel
+        int z = -1, L = -1, Y = -1, dz = -1;
+        bool write_y = false;            // the head also produces Cuda(Indicator(Y)) (fused LOAD_Y)
+        float scale = 1.f;
+    };
+    std::vector<XentHead> xent;
+    std::vector<int> stmt_xent;                     // stmt -> head launched there, or -1
+    std::vector<std::pair<int, int>> early_start;   // (storage, stmt): written earlier than its Let
 
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0, arena_keep_bytes = 0;
@@ -181,6 +192,7 @@ struct tc_ctx {
     int runs[2] = {0, 0};
     int launches_per_step = -1;
     std::vector<int> prof_launches;  // kernels each statement launched in the last tc_profile_step
+    std::vector<float> prof_update_ms;  // bucket all-reduce + momentum update completed after statement i
     // test body: the train-body Lets the main logits depend on, test-mode dropout
     std::vector<uint8_t> in_test;
     bool test_mode = false;
@@ -383,6 +395,86 @@ static bool env_on(const char* name) {
 }
 static bool pool_idx_flag_enabled() { return env_on("TCB_POOL_IDX_FLAG"); }
 
+// Softmax log-loss head fold (shared arena only: the parity mode materialises every var).  Per
+// SOFTMAX_BWD(G, S): S = SOFTMAX_FWD(z), G = MUL(A, R), R = RECIP(S), A = SCALE(Y), Y = LOAD_Y, and
+// L = LOG(S) (read by the Print).  The fused kernel runs at the chain's first statement and writes
+// L, dz (and Y when LOAD_Y comes later); those storages start there (early_start).  It repeats the
+// separate kernels' arithmetic operation for operation, so the fold is bit-identical.
+void plan_xent_fusion(tc_ctx* c) {
+    const tc_plan* p = c->plan;
+    c->stmt_xent.assign(p->nstmts, -1);
+    if (c->desc.keep || !env_on("TCB_XENT_FOLD")) return;
+    std::unordered_map<int, int> def;     // var -> defining stmt
+    std::unordered_map<int, int> readers;  // var -> number of reading statements
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& s = p->stmts[i];
+        if (s.kind == TC_STMT_LET) def[s.var] = i;
+        if (s.kind == TC_STMT_DEALLOC) continue;
+        for (int k = 0; k < s.nin; ++k)
+            if (s.in[k].kind == TC_REF_VAR) readers[s.in[k].index]++;
+    }
+    auto op_of = [&](int var) { auto it = def.find(var); return it == def.end() ? -1 : p->stmts[it->second].op; };
+    struct Cand {
+        tc_ctx::XentHead h;
+        std::vector<int> chain;
+        int ly;
+    };
+    std::vector<Cand> cands;
+    for (int b = 0; b < p->nstmts; ++b) {
+        const tc_stmt& sb = p->stmts[b];
+        if (sb.kind != TC_STMT_LET || sb.op != TC_OP_SOFTMAX_BWD || sb.nin != 2 || c->fused[b]) continue;
+        const int G = sb.in[0].index, S = sb.in[1].index;
+        if (op_of(S) != TC_OP_SOFTMAX_FWD || op_of(G) != TC_OP_MUL) continue;
+        const tc_stmt& sm = p->stmts[def[G]];
+        int A = sm.in[0].index, R = sm.in[1].index;
+        if (op_of(A) == TC_OP_RECIP) std::swap(A, R);
+        if (op_of(R) != TC_OP_RECIP || op_of(A) != TC_OP_SCALE) continue;
+        const tc_stmt& sr = p->stmts[def[R]];
+        const tc_stmt& sa = p->stmts[def[A]];
+        if (sr.in[0].index != S) continue;
+        const int Y = sa.in[0].index;
+        if (op_of(Y) != TC_OP_LOAD_Y) continue;
+        int lg = -1;
+        for (int i = 0; i < p->nstmts; ++i)
+            if (p->stmts[i].kind == TC_STMT_LET && p->stmts[i].op == TC_OP_LOG && p->stmts[i].in[0].index == S) lg = i;
+        if (lg < 0) continue;
+        // the intermediates feed only this chain
+        if (readers[S] != 3 || readers[R] != 1 || readers[A] != 1 || readers[G] != 1) continue;
+        const int f = def[S];
+        const VarL& z = c->vars.at(p->stmts[f].in[0].index);
+        const VarL& d = c->vars.at(sb.var);
+        const VarL& Sv = c->vars.at(S);
+        if (z.rank != 2 || d.rank != 2 || d.cs != z.cs || Sv.dtype != DT_F32 || Sv.cs != Sv.C) continue;
+        Cand cd;
+        cd.chain = {f, lg, def[R], def[A], def[G], b};
+        cd.h.pos = *std::min_element(cd.chain.begin(), cd.chain.end());
+        cd.h.z = p->stmts[f].in[0].index;
+        cd.h.L = p->stmts[lg].var;
+        cd.h.dz = sb.var;
+        cd.h.Y = Y;
+        cd.h.scale = static_cast<float>(sa.scale);
+        cd.ly = def[Y];
+        cands.push_back(cd);
+    }
+    // heads in launch order; the first one writes Y (and absorbs LOAD_Y) when LOAD_Y comes later
+    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.h.pos < b.h.pos; });
+    std::unordered_map<int, int> y_written;
+    for (Cand& cd : cands) {
+        tc_ctx::XentHead& h = cd.h;
+        if (cd.ly > h.pos && !y_written.count(h.Y)) {
+            h.write_y = true;
+            c->fused[cd.ly] = 1;
+            c->early_start.emplace_back(c->vars.at(h.Y).storage, h.pos);
+        }
+        y_written[h.Y] = 1;
+        for (int i : cd.chain) c->fused[i] = 1;
+        c->early_start.emplace_back(c->vars.at(h.L).storage, h.pos);
+        c->early_start.emplace_back(c->vars.at(h.dz).storage, h.pos);
+        c->stmt_xent[h.pos] = static_cast<int>(c->xent.size());
+        c->xent.push_back(h);
+    }
+}
+
 void plan_fusion(tc_ctx* c) {
     const tc_plan* p = c->plan;
     c->fused.assign(p->nstmts, 0);
@@ -502,6 +594,7 @@ void plan_fusion(tc_ctx* c) {
         c->fuse_relu[i] = c->fuse_relu[j];
         c->fused[j] = 1;
     }
+    plan_xent_fusion(c);
 }
 
 // Lifetime-interval packing of storages and companions into one arena.
@@ -577,6 +670,10 @@ tc_status plan_arena(tc_ctx* c) {
                     if (st.count(v.storage)) touch(v.storage, i);
                 }
         if (s.kind == TC_STMT_DEALLOC && st.count(s.storage)) touch(s.storage, i);
+    }
+    for (const auto& [sid, pos] : c->early_start) {  // storages a fused kernel writes before their Let
+        auto f = st.find(sid);
+        if (f != st.end()) f->second.first = std::min(f->second.first, pos);
     }
     for (auto& [sid, it] : st) {
         c->storage_item[sid] = static_cast<int>(c->items.size());
@@ -1238,6 +1335,19 @@ tc_status exec_let(tc_ctx* c, int i) {
 tc_status exec_stmt(tc_ctx* c, int i) {
     const tc_stmt& s = c->plan->stmts[i];
     if (s.kind == TC_STMT_DEALLOC) return TC_OK;  // static arena: lifetimes were resolved at plan load
+    if (!c->stmt_xent.empty() && c->stmt_xent[i] >= 0) {
+        const tc_ctx::XentHead& h = c->xent[c->stmt_xent[i]];
+        Ptrs P{c};
+        const VarL& z = c->vars.at(h.z);
+        const VarL& L = c->vars.at(h.L);
+        float* y = h.write_y ? static_cast<float*>(P.var(h.Y)) : nullptr;
+        return c->f32 ? launch_softmax_xent(static_cast<const float*>(P.var(h.z)), z.cs, c->d_labels, h.scale,
+                                            static_cast<float*>(P.var(h.L)), y, static_cast<float*>(P.var(h.dz)), z.N, L.C,
+                                            c->st)
+                      : launch_softmax_xent(static_cast<const bf16*>(P.var(h.z)), z.cs, c->d_labels, h.scale,
+                                            static_cast<float*>(P.var(h.L)), y, static_cast<bf16*>(P.var(h.dz)), z.N, L.C,
+                                            c->st);
+    }
     if (s.kind == TC_STMT_LET) return c->fused[i] ? TC_OK : c->f32 ? exec_let<float>(c, i) : exec_let<bf16>(c, i);
     if (s.kind == TC_STMT_PRINT) {
         Ptrs P{c};
@@ -2025,28 +2135,41 @@ tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_m
     r = launch_set_iter(c->d_iter, static_cast<uint32_t>(iter), static_cast<uint32_t>(n0), c->st);
     if (r != TC_OK) return r;
     const int n = c->plan->nstmts;
-    std::vector<cudaEvent_t> ev(n + 1);
+    // ev[i] .. evx[i]: the statement's own kernels; evx[i] .. ev[i + 1]: the bucket all-reduce +
+    // momentum update it completes (serial form, main stream), reported separately
+    std::vector<cudaEvent_t> ev(n + 1), evx(n);
     for (auto& e : ev) TCB_CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& e : evx) TCB_CUDA_CHECK(cudaEventCreate(&e));
     TCB_CUDA_CHECK(cudaEventRecord(ev[0], c->st));
-    // serial form (bucket all-reduce + update on the main stream, charged to the
-    // statement that completes the bucket)
     c->prof_launches.assign(n, 0);
+    c->prof_update_ms.assign(n, 0.f);
     for (int i = 0; i < n && r == TC_OK; ++i) {
         const unsigned long long l0 = g_launches.load();
         r = exec_stmt(c, i);
+        c->prof_launches[i] = static_cast<int>(g_launches.load() - l0);
+        cudaEventRecord(evx[i], c->st);
         if (r == TC_OK && c->stmt_bucket[i] >= 0) r = flush_bucket(c, c->stmt_bucket[i], update, false);
         if (r == TC_OK && update && i == c->last_update_stmt && c->plan->clip > 0) r = clip_update(c, c->st);
-        c->prof_launches[i] = static_cast<int>(g_launches.load() - l0);
         cudaEventRecord(ev[i + 1], c->st);
     }
     cudaStreamSynchronize(c->st);
     for (int i = 0; i < n; ++i) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        float ms = 0.f, mu = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], evx[i]);
+        cudaEventElapsedTime(&mu, evx[i], ev[i + 1]);
         stmt_ms[i] = ms;
+        c->prof_update_ms[i] = mu;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& e : evx) cudaEventDestroy(e);
     return r;
+}
+
+int tc_profile_updates(tc_ctx* c, float* out, int max) {
+    if (!c || !out) return -1;
+    const int n = std::min<int>(max, static_cast<int>(c->prof_update_ms.size()));
+    for (int i = 0; i < n; ++i) out[i] = c->prof_update_ms[i];
+    return n;
 }
 
 }  // extern "C"

@@ -142,6 +142,12 @@ class Trainer:
         nat.lib().tc_profile_launches(self._h, out.ctypes.data, out.size)
         return out
 
+    def profile_updates(self) -> np.ndarray:
+        """Per-statement ms of the bucket all-reduce + momentum update it completed (last profile_step)."""
+        out = np.zeros(self.net.plan.nstmts, np.float32)
+        nat.lib().tc_profile_updates(self._h, out.ctypes.data, out.size)
+        return out
+
     @property
     def launches_per_step(self) -> int:
         return nat.lib().tc_launches_per_step(self._h)

@@ -236,16 +236,17 @@ def test_async_input_pipeline_matches_serial():
         np.testing.assert_array_equal(a, b)
 
 
-@pytest.mark.parametrize("name,batch", [("resnet50", 2), ("vgg16", 2), ("alexnet", 4)])
+@pytest.mark.parametrize("name,batch", [("resnet50", 2), ("vgg16", 2), ("alexnet", 4), ("googlenet", 2)])
 def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
     """The producer-side folds of the non-keep (bench) plan compute exactly what the separate
     statements compute: BN apply + residual add (+ ReLU), ReLU backward in the data-gradient
-    GEMM epilogue, the ReLU mask carried in the max-pool argmax byte, and the momentum update
-    fused into the FC filter-gradient epilogue.  Two training steps
+    GEMM epilogue, the ReLU mask carried in the max-pool argmax byte, the momentum update
+    fused into the FC filter-gradient epilogue, and the softmax log-loss head (Softmax, Log,
+    Recip, Scale, Mul, softmax backward and the indicator in one kernel; GoogLeNet: 3 heads).  Two training steps
     with every fold on vs off give bit-identical losses, parameters and velocities."""
     runs = []
     for on in ("1", "0"):
-        for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG", "TCB_SGD_FUSE"):
+        for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG", "TCB_SGD_FUSE", "TCB_XENT_FOLD"):
             monkeypatch.setenv(var, on)
         net = compile_network(name, batch)
         tr = Trainer(net, use_graph=True, seed=13)
