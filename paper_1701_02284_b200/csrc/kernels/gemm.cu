@@ -562,13 +562,39 @@ static bool wgrad_swap(const tc_conv_desc* d) {
     return on && d->K <= 64 && (is_pointwise(d) || wgrad_im2col(d) == 64);
 }
 
-static LaunchPlan conv_plan(const tc_conv_desc* d, int which) {
+// Narrow bwd-data (N = Cin not a multiple of 256) with a K-major filter operand: 256-row CTA-pair
+// tiles issuing only the real columns (N = 96: 256 x 96 per pair, 48 filter rows per CTA), so
+// each SM streams its A rows against half the filter.  Opt-in (TCB_DGRAD_PAIR=1): measured
+// slower on AlexNet conv2 (204 -> 214 us): the im2col A stream, not the filter, fills the L2 ->
+// SM path (1.66 GB per launch at ~7.8 TB/s).
+static bool narrow_pair(long long M, int N, int K) {
+    return N % 256 != 0 && K >= 8 * BK && ceil_div(M, 2LL * BM) >= 2LL * (num_sms() / 2);
+}
+static bool dgrad_pair(const tc_conv_desc* d, bool w_kmajor) {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_DGRAD_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on && w_kmajor && narrow_pair(static_cast<long long>(d->N) * d->H * d->W, d->cs, d->R * d->S * d->ks);
+}
+// The same for fprop (the filter operand is always K-major there).  TCB_FPROP_PAIR=1 enables.
+static bool fprop_pair(const tc_conv_desc* d) {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_FPROP_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on && narrow_pair(static_cast<long long>(d->N) * d->Ho * d->Wo, d->ks, d->R * d->S * d->cs);
+}
+
+static LaunchPlan conv_plan(const tc_conv_desc* d, int which, bool w_kmajor = false) {
     const long long npix_out = static_cast<long long>(d->N) * d->Ho * d->Wo;
     const long long npix_in = static_cast<long long>(d->N) * d->H * d->W;
     if (which == 0)
-        return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2, is_pointwise(d) || fprop_im2col(d));
+        return plan_launch(static_cast<int>(npix_out), d->ks, d->R * d->S * d->cs, 1, 2, is_pointwise(d) || fprop_im2col(d),
+                           fprop_pair(d));
     if (which == 1)
-        return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2, is_pointwise(d) || dgrad_im2col(d));
+        return plan_launch(static_cast<int>(npix_in), d->cs, d->R * d->S * d->ks, 1, 2, is_pointwise(d) || dgrad_im2col(d),
+                           dgrad_pair(d, w_kmajor));
     if (wgrad_swap(d))  // D^T = im2col(x)^T dy: M = R*S*cs, N = Cout
         return plan_launch(d->R * d->S * d->cs, d->K, static_cast<int>(npix_out), 0, 4, false);
     const bool tma_ops = is_pointwise(d) || wgrad_im2col(d);
@@ -627,7 +653,7 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
 }
 
 tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
-                           size_t ws_bytes, void* stream, const void* relu_mask) {
+                           size_t ws_bytes, void* stream, const void* relu_mask, int w_kmajor) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
     if (d->cs % 8) return fail(TC_INVALID_ARG, "conv bwd-data needs a channel stride multiple of 8");
@@ -639,7 +665,7 @@ tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_
     p.N = d->cs;
     p.K = d->R * d->S * d->ks;
     p.g = geom_of(d);
-    LaunchPlan lp = conv_plan(d, 1);
+    LaunchPlan lp = conv_plan(d, 1, w_kmajor != 0);
     std::string err;
     if (is_pointwise(d)) {
         p.a_mode = OP_TMA_K;
@@ -662,8 +688,13 @@ tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_
         p.gather_kind = GATHER_DGRAD;
         p.gsrc = static_cast<const __nv_bfloat16*>(dy);
     }
-    p.b_mode = OP_TMA_MN;
-    if (!make_tmap_2d_bf16(&p.tmB, w_rskc, d->cs, p.K, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    if (w_kmajor) {  // [cs][R][S][ks]: filter rows of input channel c, K = (tap, k) contiguous
+        p.b_mode = OP_TMA_K;
+        if (!make_tmap_2d_bf16(&p.tmB, w_rskc, p.K, d->cs, p.K, BK, lp.bn / lp.cg, &err)) return fail(TC_INVALID_ARG, err);
+    } else {  // [R][S][ks][cs]
+        p.b_mode = OP_TMA_MN;
+        if (!make_tmap_2d_bf16(&p.tmB, w_rskc, d->cs, p.K, d->cs, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    }
     return run_gemm(p, lp, dx, d->cs, dx_f32 ? 0 : 1, nullptr, 0, 0, 0.f, ws, ws_bytes,
                     static_cast<cudaStream_t>(stream));
 }

@@ -1566,7 +1566,10 @@ __device__ __forceinline__ void sgd_scalar(const SgdTensor& t, long long i) {
         const long long q = i / t.cs;
         const int rs = static_cast<int>(q % t.RS);
         const int k = static_cast<int>(q / t.RS);
-        t.shadow_rskc[(static_cast<long long>(rs) * t.ks + k) * t.cs + c] = b;
+        if (t.rskc_kmajor)
+            t.shadow_rskc[(static_cast<long long>(c) * t.RS + rs) * t.ks + k] = b;
+        else
+            t.shadow_rskc[(static_cast<long long>(rs) * t.ks + k) * t.cs + c] = b;
     }
 }
 
@@ -1615,7 +1618,16 @@ __global__ void __launch_bounds__(256) k_sgd(const __grid_constant__ SgdBatch b)
                 const unsigned q = ui / static_cast<unsigned>(t.cs);
                 const unsigned rs = q % static_cast<unsigned>(t.RS);
                 const unsigned k = q / static_cast<unsigned>(t.RS);
-                *reinterpret_cast<uint2*>(t.shadow_rskc + (static_cast<long long>(rs) * t.ks + k) * t.cs + c) = h;
+                if (t.rskc_kmajor) {  // [c][rs][k]: the 4 channels are RS*ks apart
+                    const long long row = static_cast<long long>(t.RS) * t.ks;
+                    bf16* d = t.shadow_rskc + static_cast<long long>(c) * row + static_cast<long long>(rs) * t.ks + k;
+                    d[0] = __ushort_as_bfloat16(static_cast<unsigned short>(h.x & 0xFFFFu));
+                    d[row] = __ushort_as_bfloat16(static_cast<unsigned short>(h.x >> 16));
+                    d[2 * row] = __ushort_as_bfloat16(static_cast<unsigned short>(h.y & 0xFFFFu));
+                    d[3 * row] = __ushort_as_bfloat16(static_cast<unsigned short>(h.y >> 16));
+                } else {
+                    *reinterpret_cast<uint2*>(t.shadow_rskc + (static_cast<long long>(rs) * t.ks + k) * t.cs + c) = h;
+                }
             }
         }
     }

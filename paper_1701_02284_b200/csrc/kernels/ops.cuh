@@ -143,8 +143,10 @@ struct SgdTensor {
     const float* g;
     long long n;
     bf16* shadow;        // same layout as p (may be null)
-    bf16* shadow_rskc;   // conv filters: [R][S][ks][cs] copy for bwd-data (may be null)
+    bf16* shadow_rskc;   // conv filters: copy for bwd-data (may be null): [R][S][ks][cs], or
+                         // [cs][R][S][ks] (K-major bwd-data operand) when rskc_kmajor
     int K, RS, cs, ks;   // shape info for the RSKC scatter (p is [K][RS][cs])
+    int rskc_kmajor;
     float lr_alpha, momentum, decay;
     const float* gscale;  // device scalar: global-L2 clip factor applied to g + decay p (null = 1)
 };
@@ -170,7 +172,7 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
                       int y_f32, void* ws, size_t ws_bytes, void* stream);
 // relu_mask: bf16 [N*H*W][cs] forward ReLU output; dx *= [mask > 0] in the epilogue (may be null)
 tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
-                           size_t ws_bytes, void* stream, const void* relu_mask = nullptr);
+                           size_t ws_bytes, void* stream, const void* relu_mask = nullptr, int w_kmajor = 0);
 
 // d_iter[0] = iter, d_iter[1] = n0 (kernel arguments travel with the launch: no host sync)
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st);

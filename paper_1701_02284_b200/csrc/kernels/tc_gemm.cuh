@@ -145,6 +145,14 @@ __device__ __forceinline__ Unit decode_unit(const GemmParams& p, int u) {
     return w;
 }
 
+// Columns a CTA-pair tile issues (K-major B): all BN, or N left rounded up to 16 on the last
+// column tile (M = 256 needs N % 16 == 0; each CTA then holds N/2 rows, a multiple of 8).
+template <int BN>
+__device__ __forceinline__ int pair_n_issue(const GemmParams& p, int nt) {
+    const int n_left = p.N - nt * BN;
+    return n_left >= BN ? BN : (n_left + 15) / 16 * 16;
+}
+
 // ---- A gather (K-major rows of an implicit im2col) --------------------------------
 // Each of the 128 producer threads owns one tile row; its 8 chunks per k-block
 // walk (kh, kw, c) incrementally (no division in the steady state).
@@ -490,7 +498,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             int it = 0;
             for (int u = pair; u < p.units; u += npairs) {
                 const Unit w = decode_unit(p, u);
-                const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN + rank * Cfg::kBNL;
+                // CTA pair with a K-major B: the last column tile issues only round16(N left)
+                // columns, so the peer's B half starts at half of that (see the MMA issuer)
+                const int n_half = CG == 2 && p.b_mode == OP_TMA_K ? pair_n_issue<BN>(p, w.nt) / 2 : Cfg::kBNL;
+                const int m0 = w.mt * (BM * CG) + rank * BM, n0 = w.nt * BN + rank * n_half;
                 const bool load_b = !p.b_resident || u == pair;  // resident B: first unit only
                 const uint32_t tx_u = load_b || b_gather ? tx : tx - Cfg::kBBytes * CG;
                 // im2col A: first pixel of this row tile
@@ -638,7 +649,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
             // the last column tile issues only the columns that exist (rounded to 16): N = 96 on
             // a 128-wide tile costs 96/128 of the MMA time (single-CTA tiles)
             uint32_t idesc = idesc_full;
-            if (CG == 1) {
+            if (CG == 2 && p.b_mode == OP_TMA_K) {
+                const int n_issue = pair_n_issue<BN>(p, w.nt);
+                if (n_issue < BN) idesc = umma_idesc_bf16(BM * CG, static_cast<uint32_t>(n_issue), a_mn ? 1u : 0u, 0u);
+            } else if (CG == 1) {
                 // K-major B: any multiple of 16; MN-major B: whole swizzle atoms (64 / 32 columns)
                 const int gran = b_sw64 ? 32 : b_mn ? 64 : 16;
                 const int n_left = p.N - w.nt * BN;
@@ -850,26 +864,51 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     }
                 }
                 if (p.epi == EPI_SGD) {
-                    // fused update: each lane owns one parameter row segment of 64 columns
-                    const int row = m0 + quarter * 32 + lane;
-                    if (row < p.M) {
-                        float* pp = p.sgd_p + row * p.sgd_ld + nb;
-                        float* vv = p.sgd_v + row * p.sgd_ld + nb;
-                        __nv_bfloat16* sh = p.sgd_shadow + row * p.sgd_ld + nb;
+                    // fused update.  The accumulator arrives one parameter row per lane; it is
+                    // transposed through this warp's staging buffer (32 rows x 32 fp32 columns per
+                    // pass, SW128 chunk order) so that eight lanes cover one 128-byte row segment and
+                    // the p / v / shadow traffic is fully coalesced.  All eight row groups' loads
+                    // are issued before the first update (memory-level parallelism).
+                    const uint32_t stg = smem_u32(stage_base);
+                    const int rsub = lane >> 3, j = lane & 7;
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            if (nb + 4 * q >= p.N) break;
-                            const uint32_t* gq = q < 8 ? &r0[4 * q] : &r1[4 * (q - 8)];
-                            float4 P4 = *reinterpret_cast<const float4*>(pp + 4 * q);
-                            float4 V4 = *reinterpret_cast<const float4*>(vv + 4 * q);
-                            sgd_update1(P4.x, V4.x, __uint_as_float(gq[0]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
-                            sgd_update1(P4.y, V4.y, __uint_as_float(gq[1]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
-                            sgd_update1(P4.z, V4.z, __uint_as_float(gq[2]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
-                            sgd_update1(P4.w, V4.w, __uint_as_float(gq[3]), p.sgd_mom, p.sgd_lr, p.sgd_decay);
-                            *reinterpret_cast<float4*>(pp + 4 * q) = P4;
-                            *reinterpret_cast<float4*>(vv + 4 * q) = V4;
-                            *reinterpret_cast<uint2*>(sh + 4 * q) =
-                                make_uint2(pack_bf16x2(P4.x, P4.y), pack_bf16x2(P4.z, P4.w));
+                    for (int half = 0; half < 2; ++half) {
+                        const uint32_t* src = half ? r1 : r0;
+                        __syncwarp();  // the previous pass's reads of the buffer are done
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            st_shared_v4(stg + sw128_off(lane, q), src[4 * q], src[4 * q + 1], src[4 * q + 2],
+                                         src[4 * q + 3]);
+                        __syncwarp();
+                        const int col = nb + half * 32 + 4 * j;
+                        if (col >= p.N) continue;  // N % 4 == 0: a float4 never straddles N
+                        float4 P4[8], V4[8];
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int row = m0 + quarter * 32 + it * 4 + rsub;
+                            if (row < p.M) {
+                                P4[it] = *reinterpret_cast<const float4*>(p.sgd_p + row * p.sgd_ld + col);
+                                V4[it] = *reinterpret_cast<const float4*>(p.sgd_v + row * p.sgd_ld + col);
+                            }
+                        }
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int rr = it * 4 + rsub, row = m0 + quarter * 32 + rr;
+                            if (row >= p.M) continue;
+                            uint32_t g0, g1, g2, g3;
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(g0), "=r"(g1), "=r"(g2), "=r"(g3)
+                                         : "r"(stg + sw128_off(rr, j)));
+                            float4 P = P4[it], V = V4[it];
+                            sgd_update1(P.x, V.x, __uint_as_float(g0), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P.y, V.y, __uint_as_float(g1), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P.z, V.z, __uint_as_float(g2), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            sgd_update1(P.w, V.w, __uint_as_float(g3), p.sgd_mom, p.sgd_lr, p.sgd_decay);
+                            const long long o = row * p.sgd_ld + col;
+                            *reinterpret_cast<float4*>(p.sgd_p + o) = P;
+                            *reinterpret_cast<float4*>(p.sgd_v + o) = V;
+                            *reinterpret_cast<uint2*>(p.sgd_shadow + o) =
+                                make_uint2(pack_bf16x2(P.x, P.y), pack_bf16x2(P.z, P.w));
                         }
                     }
                     continue;
