@@ -4,12 +4,14 @@
 #include <atomic>
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
 #include "common.cuh"
 #include "ops.cuh"
 #include "tc_gemm.cuh"
+#include "tc_conv_halo.cuh"
 
 namespace tcb {
 
@@ -424,6 +426,239 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     return TC_OK;
 }
 
+// ------------------------------------------------------------------ halo-tile convolutions
+// Geometry of the halo path (tc_conv_halo.cuh) for a stride-1 conv whose GEMM writes an
+// Hout x Wout image from an Hsrc x Wsrc source with a 64-multiple channel stride.
+struct HaloGeom {
+    int wr = 0, th = 0, hh = 0, wv = 0, wst = 0, xt = 0, yt = 0, ms = 1;
+    double util = 0;
+};
+
+// TCB_HALO: unset / "1" both forms, "0" off, "f" fprop only, "d" bwd-data only.
+static bool halo_enabled(char which) {
+    static const char mode = [] {
+        const char* e = std::getenv("TCB_HALO");
+        return e && e[0] ? e[0] : '1';
+    }();
+    return mode == '1' || mode == which;
+}
+static bool halo_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_HALO_DEBUG");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+// TCB_HALO_MS: 0 (default) cost model, 1 / 2 force one / two 128-row subtiles per unit
+static int halo_ms_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("TCB_HALO_MS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+static double halo_min_util() {
+    static const double v = [] {
+        const char* e = std::getenv("TCB_HALO_MIN_UTIL");
+        return e ? std::atof(e) : 0.7;
+    }();
+    return v;
+}
+
+// Row stride wr of the 128-pixel tile (th = 128 / wr output rows): the one with the highest
+// fraction of valid output pixels; 0 when none reaches TCB_HALO_MIN_UTIL (default 0.7; AlexNet
+// conv2 26 x 26 under 5 x 5: 75%) -- the im2col path (no junk columns) is kept for small images
+// (12 x 12: 56%, 7 x 7: 38%).
+static HaloGeom halo_geom(int Hout, int Wout, int R, int S, int ms = 1, int wr_only = 0) {
+    HaloGeom best;
+    for (int wr : {16, 32, 64, 128}) {
+        if (wr_only && wr != wr_only) continue;
+        HaloGeom g;
+        g.wr = wr;
+        g.th = BM / wr;
+        g.ms = ms;
+        g.wv = wr - (S - 1);
+        if (g.wv <= 0) continue;
+        g.xt = ceil_div(Wout, g.wv);
+        if (wr >= 64 && g.xt > 1) continue;  // 32-pixel store segments: junk columns only past the image edge
+        g.yt = ceil_div(Hout, g.th * ms);
+        g.hh = g.th * ms + R - 1;
+        if (g.hh > 256) continue;
+        g.wst = wr <= 32 ? g.wv : 32;
+        g.util = static_cast<double>(Hout) * Wout / (static_cast<double>(g.yt) * g.th * ms * g.xt * wr);
+        if (g.util > best.util + 1e-9) best = g;
+    }
+    if (!wr_only && best.util < halo_min_util()) best = HaloGeom{};
+    return best;
+}
+
+template <int BN>
+static tc_status launch_halo(HaloParams& p, cudaStream_t st) {
+    using Cfg = HaloCfg<BN>;
+    constexpr int kMaxSmem = 232448;
+    const int fixed = 1024 + 512 + Cfg::kStaging + 2 * static_cast<int>(p.halo_bytes);
+    p.stages = std::min(8, (kMaxSmem - fixed) / Cfg::kBBytes);
+    if (p.stages < 2) return fail(TC_INTERNAL, "halo conv: shared memory too small for the halo tile");
+    const int smem = fixed + p.stages * Cfg::kBBytes;
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TCB_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(tc_conv_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("halo smem attr: ") + cudaGetErrorString(e));
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::min(p.units, num_sms()));
+    cfg.blockDim = dim3(kNumThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_gemm() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = launch_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, tc_conv_halo_kernel<BN>, p);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
+// 4-D tensor maps of the halo path: the tiled source {cs, W, H, N} (box {64, wr, hh, 1}) and the
+// output store {ncols, Wout, Hout, N} (box {128 B of columns, wst, 1, 1}).
+static bool make_tmap_halo_src(CUtensorMap* map, const void* base, int N, int H, int W, int cs, int wr, int hh,
+                               std::string* err) {
+    auto fn = encode_fn();
+    if (!fn) {
+        *err = "cuTensorMapEncodeTiled unavailable (no CUDA driver)";
+        return false;
+    }
+    if (reinterpret_cast<uintptr_t>(base) & 15) {
+        *err = "halo conv source must be 16-byte aligned";
+        return false;
+    }
+    const cuuint64_t row = static_cast<cuuint64_t>(cs) * 2;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(cs), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                          static_cast<cuuint64_t>(N)};
+    cuuint64_t strides[3] = {row, row * W, row * W * H};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(wr), static_cast<cuuint32_t>(hh), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled (halo source) failed (" + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
+}
+static bool make_tmap_halo_store(CUtensorMap* map, void* base, bool bf16, int ncols, int Wout, int Hout, int N, int wst,
+                                 std::string* err) {
+    auto fn = encode_fn();
+    if (!fn) {
+        *err = "cuTensorMapEncodeTiled unavailable (no CUDA driver)";
+        return false;
+    }
+    const cuuint64_t es = bf16 ? 2 : 4;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ncols * es) & 15)) {
+        *err = "halo conv output must be 16-byte aligned with a 16-byte multiple row";
+        return false;
+    }
+    const cuuint64_t row = ncols * es;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(ncols), static_cast<cuuint64_t>(Wout), static_cast<cuuint64_t>(Hout),
+                          static_cast<cuuint64_t>(N)};
+    cuuint64_t strides[3] = {row, row * Wout, row * Wout * Hout};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(wst), 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled (halo store) failed (" + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
+}
+
+// Launch one halo-path contraction.  src: the NHWC source (x for fprop, dy for bwd-data) with
+// channel stride src_cs (a multiple of 64); N = output channel stride; B = the filter (K-major
+// [N rows][R*S*src_cs], or MN-major [R*S*src_cs][N] when b_mn).
+static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, int Ws, int src_cs, int Hout, int Wout,
+                          int R, int S, int pad, bool flip, const void* w, int w_rows, long long w_ld, bool b_mn, int N,
+                          void* out, bool out_bf16, const float* bias, int n_bias, int relu, const void* mask,
+                          cudaStream_t st) {
+    HaloParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.N = N;
+    p.b_mn = b_mn ? 1 : 0;
+    p.R = R;
+    p.S = S;
+    p.flip = flip ? 1 : 0;
+    p.ncb = src_cs / 64;
+    p.ldk = src_cs;
+    p.wr = g.wr;
+    p.th = g.th;
+    p.hh = g.hh;
+    p.wv = g.wv;
+    p.wst = g.wst;
+    p.xt = g.xt;
+    p.yt = g.yt;
+    p.nimg = nimg;
+    p.Ho = Hout;
+    p.Wo = Wout;
+    p.lo_x = flip ? pad - (S - 1) : -pad;
+    p.lo_y = flip ? pad - (R - 1) : -pad;
+    p.halo_tx = static_cast<uint32_t>(g.hh) * g.wr * 128;
+    p.halo_bytes = (p.halo_tx + static_cast<uint32_t>(S - 1) * 128 + 1023) & ~1023u;
+    p.epi = out_bf16 ? EPI_BF16 : EPI_F32;
+    p.bias = bias;
+    p.n_bias = n_bias;
+    p.relu = relu;
+    p.alpha = 1.f;
+    p.mask = static_cast<const __nv_bfloat16*>(mask);
+    p.mask_ld = N;
+    // tile width: per-k-block cost model of plan_launch over the column tiles
+    int bn = N > 128 ? 256 : N > 64 ? 128 : 64;
+    if (N > 128 && N % 256 != 0 && ceil_div(N, 128) * t_kblock(128, 1) < ceil_div(N, 256) * t_kblock(256, 1)) bn = 128;
+    if (forced_bn()) bn = forced_bn();
+    p.tiles_n = ceil_div(N, bn);
+    // two subtiles per unit (ms = 2, BN <= 128) when it is faster by a simple model: waves x
+    // k-blocks x max(MMA cycles, filter bytes at ~40 B/clk of the L2 -> SM path per SM)
+    HaloGeom gm = g;
+    if (bn <= 128 && halo_ms_mode() != 1) {
+        const HaloGeom g2 = halo_geom(Hout, Wout, R, S, 2, g.wr);
+        const int n_issue = b_mn ? std::min(bn, (std::min(N, bn) + 63) / 64 * 64) : std::min(bn, (std::min(N, bn) + 15) / 16 * 16);
+        auto model = [&](const HaloGeom& q) {
+            const long long units = static_cast<long long>(nimg) * q.yt * q.xt * p.tiles_n;
+            const double waves = static_cast<double>((units + num_sms() - 1) / num_sms());
+            return waves * std::max(q.ms * 2.0 * n_issue, bn * 128.0 / 40.0);
+        };
+        const uint32_t h2 = (static_cast<uint32_t>(g2.hh) * g2.wr * 128 + static_cast<uint32_t>(S - 1) * 128 + 1023) & ~1023u;
+        const bool fits = 2 * h2 + 3 * bn * BK * 2 + 8 * kStagingBytes + 2048 <= 232448;  // >= 3 filter stages
+        if (g2.wr && fits && (halo_ms_mode() == 2 || model(g2) < model(g))) gm = g2;
+    }
+    p.ms = gm.ms;
+    p.th = gm.th;
+    p.hh = gm.hh;
+    p.yt = gm.yt;
+    p.halo_tx = static_cast<uint32_t>(gm.hh) * gm.wr * 128;
+    p.halo_bytes = (p.halo_tx + static_cast<uint32_t>(S - 1) * 128 + 1023) & ~1023u;
+    p.units = nimg * gm.yt * gm.xt * p.tiles_n;
+    std::string err;
+    if (!make_tmap_halo_src(&p.tmA, src, nimg, Hs, Ws, src_cs, gm.wr, gm.hh, &err)) return fail(TC_INVALID_ARG, err);
+    const long long K = static_cast<long long>(R) * S * src_cs;
+    if (b_mn) {
+        if (!make_tmap_2d_bf16(&p.tmB, w, w_rows, K, w_ld, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
+    } else {
+        if (!make_tmap_2d_bf16(&p.tmB, w, K, w_rows, w_ld, BK, bn, &err)) return fail(TC_INVALID_ARG, err);
+    }
+    if (!make_tmap_halo_store(&p.tmD, out, out_bf16, N, Wout, Hout, nimg, g.wst, &err)) return fail(TC_INVALID_ARG, err);
+    return bn == 256 ? launch_halo<256>(p, st) : bn == 128 ? launch_halo<128>(p, st) : launch_halo<64>(p, st);
+}
+
 static void init_params(GemmParams& p) {
     std::memset(&p, 0, sizeof(p));
     p.alpha = 1.f;
@@ -567,6 +802,24 @@ static bool wgrad_swap(const tc_conv_desc* d) {
 // each SM streams its A rows against half the filter.  Opt-in (TCB_DGRAD_PAIR=1): measured
 // slower on AlexNet conv2 (204 -> 214 us): the im2col A stream, not the filter, fills the L2 ->
 // SM path (1.66 GB per launch at ~7.8 TB/s).
+// Halo path eligibility: stride 1, a real filter window, 64-multiple source channel stride.
+static HaloGeom halo_log(const char* what, const tc_conv_desc* d, HaloGeom g) {
+    if (halo_debug())
+        std::fprintf(stderr, "[tcb halo] %s N%d C%d %dx%d K%d %dx%d s%d p%d cs%d ks%d -> wr %d util %.3f\n", what, d->N, d->C,
+                     d->H, d->W, d->K, d->R, d->S, d->stride, d->pad, d->cs, d->ks, g.wr, g.util);
+    return g;
+}
+static HaloGeom fprop_halo(const tc_conv_desc* d) {
+    if (!halo_enabled('f') || d->stride != 1 || d->R * d->S == 1 || d->cs % 64 || d->ks % 8)
+        return halo_log("fprop (not eligible)", d, HaloGeom{});
+    return halo_log("fprop", d, halo_geom(d->Ho, d->Wo, d->R, d->S));
+}
+static HaloGeom dgrad_halo(const tc_conv_desc* d) {
+    if (!halo_enabled('d') || d->stride != 1 || d->R * d->S == 1 || d->ks % 64 || d->cs % 8)
+        return halo_log("dgrad (not eligible)", d, HaloGeom{});
+    return halo_log("dgrad", d, halo_geom(d->H, d->W, d->R, d->S));
+}
+
 static bool narrow_pair(long long M, int N, int K) {
     return N % 256 != 0 && K >= 8 * BK && ceil_div(M, 2LL * BM) >= 2LL * (num_sms() / 2);
 }
@@ -619,6 +872,9 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
                       int y_f32, void* ws, size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (const HaloGeom hg = fprop_halo(d); hg.wr)
+        return run_halo(hg, x, d->N, d->H, d->W, d->cs, d->Ho, d->Wo, d->R, d->S, d->pad, false, w, d->K, filter_ld(d),
+                        false, d->ks, y, !y_f32, bias, d->K, relu, nullptr, static_cast<cudaStream_t>(stream));
     GemmParams p;
     init_params(p);
     p.M = d->N * d->Ho * d->Wo;
@@ -657,6 +913,14 @@ tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
     if (d->cs % 8) return fail(TC_INVALID_ARG, "conv bwd-data needs a channel stride multiple of 8");
+    if (const HaloGeom hg = dgrad_halo(d); hg.wr) {
+        if (w_kmajor)
+            return run_halo(hg, dy, d->N, d->Ho, d->Wo, d->ks, d->H, d->W, d->R, d->S, d->pad, true, w_rskc, d->cs,
+                            static_cast<long long>(d->R) * d->S * d->ks, false, d->cs, dx, !dx_f32, nullptr, 0, 0,
+                            relu_mask, static_cast<cudaStream_t>(stream));
+        return run_halo(hg, dy, d->N, d->Ho, d->Wo, d->ks, d->H, d->W, d->R, d->S, d->pad, true, w_rskc, d->cs, d->cs,
+                        true, d->cs, dx, !dx_f32, nullptr, 0, 0, relu_mask, static_cast<cudaStream_t>(stream));
+    }
     GemmParams p;
     init_params(p);
     p.mask = static_cast<const __nv_bfloat16*>(relu_mask);

@@ -119,6 +119,7 @@ struct tc_ctx {
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
     std::vector<int> fuse_bias_param;
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
+    std::vector<uint8_t> relu_next;                 // data-gradient GEMM whose output feeds a ReLU backward
     std::vector<int> fuse_add_res, fuse_add_out;    // BN forward: folded residual add (other operand, output var)
     std::vector<char> sgd_fused;                    // per param: momentum update fused into its FC filter gradient
     bool fuse_sgd_active = false;                   // set by run_body for update steps
@@ -487,6 +488,7 @@ void plan_fusion(tc_ctx* c) {
     c->fuse_add_res.assign(p->nstmts, -1);
     c->fuse_add_out.assign(p->nstmts, -1);
     c->pool_mask_in_idx.assign(p->nstmts, 0);
+    c->relu_next.assign(p->nstmts, 0);
     auto next_let = [&](int i) {
         for (int j = i + 1; j < p->nstmts; ++j) {
             if (p->stmts[j].kind == TC_STMT_DEALLOC) continue;
@@ -501,7 +503,7 @@ void plan_fusion(tc_ctx* c) {
         const tc_stmt& s = p->stmts[i];
         if (s.kind != TC_STMT_LET) continue;
         const bool gemm_fold = env_on("TCB_GEMM_RELU_FOLD");
-        const bool gemm = gemm_fold && (s.op == TC_OP_CONV_BWD_DATA || s.op == TC_OP_MATMUL_BWD_DATA);
+        const bool gemm = s.op == TC_OP_CONV_BWD_DATA || s.op == TC_OP_MATMUL_BWD_DATA;
         if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD) continue;
         // the next Let, skipping Update / Print statements that do not read this output (the
         // filter-gradient Update sits between a data gradient and its ReLU backward)
@@ -526,6 +528,10 @@ void plan_fusion(tc_ctx* c) {
         const VarL& m = c->vars.at(r.in[1].index);
         if (m.dtype != y.dtype || m.cs != y.cs || m.elems() != y.elems()) continue;
         if (s.op == TC_OP_LRN_BWD && r.in[1].index != s.in[2].index) continue;  // mask must be the LRN input
+        // a data-gradient GEMM followed by its ReLU backward runs unsplit whether or not the mask
+        // is folded in, so the fold changes nothing but the launch count (bit-identical)
+        if (gemm) c->relu_next[i] = 1;
+        if (gemm && !gemm_fold) continue;
         c->fuse_mask_var[i] = r.in[1].index;
         c->fused[j] = 1;
         if (s.op == TC_OP_POOL_BWD && s.max_pool && s.k * s.k <= 127 && pool_idx_flag_enabled()) {
@@ -1272,8 +1278,10 @@ tc_status exec_let(tc_ctx* c, int i) {
             if (c->fuse_mask_var[i] >= 0) {  // the following ReLU backward, folded into the epilogue
                 ga.relu_mask = P.var(c->fuse_mask_var[i]);
                 ga.mask_ld = w.in_dev;
-                ga.splits = 1;  // the mask is applied by the tile epilogue, not by a split-K reduce
             }
+            // the mask is applied by the tile epilogue, not by a split-K reduce; unfolded, the same
+            // unsplit contraction runs (identical summation order either way)
+            if (c->relu_next[i]) ga.splits = 1;
             return run_gemm_args(c, ga);
         }
         case TC_OP_BIAS_ADD: {

@@ -170,6 +170,21 @@ IM2COL_CASES = [
 ]
 
 
+# stride-1 convs over 64-multiple channel strides whose tiles keep >= 80% valid pixels take the
+# halo-tile path (tc_conv_halo.cuh): tile row stride wr = 16 / 32 / 64 / 128, several x / y tiles,
+# pad 0 / 1 / 2, 3x3 and 5x5, several channel blocks and column tiles (N = 96 / 128 / 384)
+HALO_CASES = [
+    (2, 64, 56, 56, 128, 3, 1, 1),    # wr 32, 2 x-tiles, 14 y-tiles
+    (2, 64, 27, 27, 128, 5, 1, 2),    # wr 32, one x-tile (27 <= 28 valid columns), 5x5
+    (2, 64, 56, 56, 96, 3, 1, 0),     # pad 0 (space-to-depth first layer shape), N = 96
+    (2, 64, 16, 14, 64, 3, 1, 1),     # wr 16 (two output rows per 32-row chunk)
+    (1, 64, 6, 62, 128, 3, 1, 1),     # wr 64
+    (1, 64, 3, 126, 64, 3, 1, 1),     # wr 128
+    (2, 128, 28, 28, 384, 3, 1, 1),   # 2 channel blocks, 256-wide column tiles
+    (1, 256, 30, 30, 256, 3, 1, 1),   # 4 channel blocks
+]
+
+
 @pytest.mark.parametrize("case", [(2, 3, 35, 35, 96, 11, 4, 0), (2, 3, 32, 32, 64, 7, 2, 3), (2, 1, 28, 28, 20, 5, 1, 0)])
 def test_conv_channel_stride4_fwd_and_filter(case):
     """First-layer convs: input staged with channel stride 4 (8-byte tap gathers),
@@ -199,7 +214,7 @@ def test_conv_channel_stride4_fwd_and_filter(case):
     assert rel_err(got, refw) < TOL
 
 
-@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES)
+@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES + HALO_CASES)
 def test_conv_fwd(case):
     x, w, b, d = conv_case(*case)
     xs = nhwc_pad(x, d.cs)
@@ -213,7 +228,7 @@ def test_conv_fwd(case):
     assert torch.all(y[..., d.K:] == 0)
 
 
-@pytest.mark.parametrize("case", CONV_CASES[2:] + [(2, 8, 13, 13, 64, 3, 1, 1)] + IM2COL_CASES)
+@pytest.mark.parametrize("case", CONV_CASES[2:] + [(2, 8, 13, 13, 64, 3, 1, 1)] + IM2COL_CASES + HALO_CASES)
 def test_conv_bwd_data(case):
     x, w, b, d = conv_case(*case, seed=1)
     g = torch.Generator(device="cpu").manual_seed(5)
@@ -242,3 +257,21 @@ def test_conv_bwd_filter(case):
     torch.cuda.synchronize()
     ref = torch.nn.grad.conv2d_weight(x, w.shape, dy, stride=d.stride, padding=d.pad).permute(0, 2, 3, 1)
     assert rel_err(dw[..., :d.C], ref) < TOL
+
+
+@pytest.mark.parametrize("case", HALO_CASES + [(2, 64, 56, 56, 192, 3, 1, 1), (2, 128, 28, 28, 192, 3, 1, 1)])
+def test_conv_fwd_deterministic(case):
+    """Bit-identical output across repeated launches and output-buffer contents (bias + ReLU
+    epilogue): every output element is written exactly once from a fixed summation order."""
+    x, w, b, d = conv_case(*case)
+    xs = nhwc_pad(x, d.cs)
+    ws = w_krsc(w, d.cs)
+    outs = []
+    for fill in (float("nan"), 0.0, 7.0):
+        y = torch.full((d.N, d.Ho, d.Wo, d.ks), fill, dtype=torch.bfloat16, device="cuda")
+        nat.check(nat.lib().tc_conv2d_fwd(C.byref(d), xs.data_ptr(), ws.data_ptr(), b.data_ptr(), 1, y.data_ptr(),
+                                          None, 0, None))
+        torch.cuda.synchronize()
+        outs.append(y.clone())
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
