@@ -492,21 +492,21 @@ static HaloGeom halo_geom(int Hout, int Wout, int R, int S, int ms = 1, int wr_o
     return best;
 }
 
-template <int BN>
+template <int BN, int MS>
 static tc_status launch_halo(HaloParams& p, cudaStream_t st) {
     using Cfg = HaloCfg<BN>;
     constexpr int kMaxSmem = 232448;
     const int fixed = 1024 + 512 + Cfg::kStaging + 2 * static_cast<int>(p.halo_bytes);
-    p.stages = std::min(8, (kMaxSmem - fixed) / Cfg::kBBytes);
+    p.stages = std::min(8, (kMaxSmem - fixed) / static_cast<int>(p.b_bytes));
     if (p.stages < 2) return fail(TC_INTERNAL, "halo conv: shared memory too small for the halo tile");
-    const int smem = fixed + p.stages * Cfg::kBBytes;
+    const int smem = fixed + p.stages * static_cast<int>(p.b_bytes);
     static std::atomic<uint64_t> attr_done{0};
     int dev = 0;
     TCB_CUDA_CHECK(cudaGetDevice(&dev));
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_done.load(std::memory_order_acquire) & bit)) {
         const cudaError_t e =
-            cudaFuncSetAttribute(tc_conv_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+            cudaFuncSetAttribute(tc_conv_halo_kernel<BN, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
         if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("halo smem attr: ") + cudaGetErrorString(e));
         attr_done.fetch_or(bit, std::memory_order_acq_rel);
     }
@@ -522,7 +522,7 @@ static tc_status launch_halo(HaloParams& p, cudaStream_t st) {
     attr[1].val.priority = launch_priority();
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, tc_conv_halo_kernel<BN>, p);
+    cudaLaunchKernelEx(&cfg, tc_conv_halo_kernel<BN, MS>, p);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -650,13 +650,18 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
     std::string err;
     if (!make_tmap_halo_src(&p.tmA, src, nimg, Hs, Ws, src_cs, gm.wr, gm.hh, &err)) return fail(TC_INVALID_ARG, err);
     const long long K = static_cast<long long>(R) * S * src_cs;
+    // K-major filter with one column tile: load only round16(N) filter rows per k-block (AlexNet
+    // conv2 bwd-data: 96 of 128 -> 12 KB slots, two more slots in the ring)
+    const int b_rows_box = !b_mn && p.tiles_n == 1 ? std::min(bn, (N + 15) / 16 * 16) : bn;
+    p.b_bytes = static_cast<uint32_t>(b_rows_box) * BK * 2;
     if (b_mn) {
         if (!make_tmap_2d_bf16(&p.tmB, w, w_rows, K, w_ld, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
     } else {
-        if (!make_tmap_2d_bf16(&p.tmB, w, K, w_rows, w_ld, BK, bn, &err)) return fail(TC_INVALID_ARG, err);
+        if (!make_tmap_2d_bf16(&p.tmB, w, K, w_rows, w_ld, BK, b_rows_box, &err)) return fail(TC_INVALID_ARG, err);
     }
     if (!make_tmap_halo_store(&p.tmD, out, out_bf16, N, Wout, Hout, nimg, g.wst, &err)) return fail(TC_INVALID_ARG, err);
-    return bn == 256 ? launch_halo<256>(p, st) : bn == 128 ? launch_halo<128>(p, st) : launch_halo<64>(p, st);
+    if (p.ms == 2) return bn == 128 ? launch_halo<128, 2>(p, st) : launch_halo<64, 2>(p, st);
+    return bn == 256 ? launch_halo<256, 1>(p, st) : bn == 128 ? launch_halo<128, 1>(p, st) : launch_halo<64, 1>(p, st);
 }
 
 static void init_params(GemmParams& p) {

@@ -1461,6 +1461,28 @@ __global__ void k_synth(T* __restrict__ x, int32_t* __restrict__ labels, StageLa
     }
 }
 
+// bf16 filter shadow [K][RS][cs] (row stride ld) -> K-major bwd-data operand [cs][RS][ks]: one 32 x 32
+// (k, c) tile of one filter tap per block, transposed through shared memory (coalesced both ways).
+__global__ void __launch_bounds__(256) k_krsc_to_crsk(const bf16* __restrict__ src, int K, int RS, int cs, long long ld,
+                                                      bf16* __restrict__ dst, int ks) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ bf16 tile[32][33];
+    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32, rs = blockIdx.z;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int y = 0; y < 32; y += 8) {
+        const int k = k0 + ty + y, c = c0 + tx;
+        tile[ty + y][tx] = k < K && c < cs ? src[k * ld + static_cast<long long>(rs) * cs + c] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int y = 0; y < 32; y += 8) {
+        const int c = c0 + ty + y, k = k0 + tx;
+        if (c < cs && k < K) dst[(static_cast<long long>(c) * RS + rs) * ks + k] = tile[tx][ty + y];
+    }
+}
+
 __global__ void k_s2d_mask_grad(float* __restrict__ g, int K, long long ld, int Rp, int s, int cs, int R, int S) {
     pdl_wait();
     pdl_trigger();
@@ -2058,6 +2080,12 @@ template <typename T>
 tc_status launch_synth_batch(T* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,
                              uint32_t n0, cudaStream_t st) {
     TCB_LAUNCH(k_synth<T>, EW_GRID(L.elems()), x, labels, L, classes, seed, iter, n0);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+tc_status launch_krsc_to_crsk(const bf16* src, int K, int RS, int cs, long long ld, bf16* dst, int ks, cudaStream_t st) {
+    LowPriorityScope low;  // runs beside the update on the side stream
+    TCB_LAUNCH(k_krsc_to_crsk, dim3(ceil_div(cs, 32), ceil_div(K, 32), RS), 256, 0, st, src, K, RS, cs, ld, dst, ks);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

@@ -134,6 +134,8 @@ tc_status launch_synth_batch(T* x, int32_t* labels, StageLayout L, int classes, 
 // Space-to-depth filter gradient [K][ld]: zero the taps outside the original R x S window
 // (column (a*Rp + b)*s*s*cs + (i*s + j)*cs + c is tap (s*a + i, s*b + j)).
 tc_status launch_s2d_mask_grad(float* g, int K, long long ld, int Rp, int s, int cs, int R, int S, cudaStream_t st);
+// [K][RS][cs] bf16 filter shadow (row stride ld) -> [cs][RS][ks] (K-major bwd-data filter operand)
+tc_status launch_krsc_to_crsk(const bf16* src, int K, int RS, int cs, long long ld, bf16* dst, int ks, cudaStream_t st);
 
 // Momentum SGD: v = mom*v + lr_alpha*(g + decay*p); p += v;
 // refreshes the bf16 shadow(s) used as GEMM operands.

@@ -50,6 +50,7 @@ struct HaloParams {
     uint32_t halo_bytes;  // bytes per halo slot (1024-aligned, includes the over-read slack)
     uint32_t halo_tx;     // bytes one halo box delivers
     int stages;           // B ring slots
+    uint32_t b_bytes;     // bytes per B slot: BN rows, or (K-major, one column tile) round16(N) rows
     int epi;              // EPI_BF16 / EPI_F32
     const float* bias;
     int n_bias;
@@ -83,7 +84,7 @@ __device__ __forceinline__ HaloTile halo_tile(const HaloParams& p, int u) {
     return t;
 }
 
-template <int BN>
+template <int BN, int MS>
 __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __grid_constant__ HaloParams p) {
     using Cfg = HaloCfg<BN>;
     constexpr int NACC = Cfg::kAcc;
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
     const int S = p.stages;
     uint8_t* sHalo = smem;                                   // 2 slots
     uint8_t* sB = smem + 2 * p.halo_bytes;                   // S slots
-    uint8_t* sStage = sB + S * Cfg::kBBytes;                 // epilogue staging
+    uint8_t* sStage = sB + S * p.b_bytes;                    // epilogue staging
     uint64_t* a_full = reinterpret_cast<uint64_t*>(sStage + Cfg::kStaging);
     uint64_t* a_empty = a_full + 2;
     uint64_t* b_full = a_empty + 2;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int taps = p.R * p.S;
-    const int nbuf = NACC / p.ms;  // unit accumulator buffers (ms * BN TMEM columns each)
+    constexpr int nbuf = NACC / MS;  // unit accumulator buffers (MS * BN TMEM columns each)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.tmA);
@@ -134,21 +135,34 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
 
     if (warp == 0) {
         // ---------------- TMA producer
-        int ai = 0, bi = 0;
+        int ai = 0, bs = 0;
+        uint32_t bph = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
             const HaloTile t = halo_tile(p, u);
             const int n0 = t.nt * BN;
             for (int cb = 0; cb < p.ncb; ++cb, ++ai) {
                 const int as = ai & 1;
                 mbar_wait(&a_empty[as], ((ai >> 1) & 1) ^ 1);
+#if defined(TCB_EXP_NOLOAD) || defined(TCB_EXP_NOHALO)
+                if (lane == 0) mbar_arrive(&a_full[as]);  // experiment: no halo loads
+#else
                 tma_load_4d_e(sHalo + as * p.halo_bytes, &p.tmA, smem_u32(&a_full[as]), cb * 64, t.x0 + p.lo_x,
                               t.y0 + p.lo_y, t.img);
                 mbar_arrive_expect_tx_e(&a_full[as], p.halo_tx);
-                for (int tap = 0; tap < taps; ++tap, ++bi) {
-                    const int s = bi % S;
-                    mbar_wait(&b_empty[s], ((bi / S) & 1) ^ 1);
-                    uint8_t* b_dst = sB + s * Cfg::kBBytes;
+#endif
+                for (int tap = 0; tap < taps; ++tap) {
+                    const int s = bs;
+                    mbar_wait(&b_empty[s], bph ^ 1);
+                    if (++bs == S) {
+                        bs = 0;
+                        bph ^= 1;
+                    }
+                    uint8_t* b_dst = sB + s * p.b_bytes;
                     const int kc = tap * p.ldk + cb * 64;
+#ifdef TCB_EXP_NOLOAD
+                    if (lane == 0) mbar_arrive(&b_full[s]);  // experiment: no filter loads
+                    continue;
+#endif
                     if (p.b_mn) {
 #pragma unroll
                         for (int a = 0; a < BN / 64; ++a)
@@ -156,7 +170,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
                     } else {
                         tma_load_2d_e<1>(b_dst, &p.tmB, smem_u32(&b_full[s]), kc, n0);
                     }
-                    mbar_arrive_expect_tx_e(&b_full[s], Cfg::kBBytes);
+                    mbar_arrive_expect_tx_e(&b_full[s], p.b_bytes);
                 }
             }
         }
@@ -171,13 +185,19 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
         uint64_t b_koff[BK / 16];
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) b_koff[k] = b_desc_at(smem_u32(sB), k) - b_desc0;
-        int ai = 0, bi = 0, tc = 0;
+        int ai = 0, tc = 0, bs = 0;
+        uint32_t bph = 0;
+        uint64_t b_off = 0;
+        const uint64_t b_step = p.b_bytes >> 4;
+        // per tap +-1 row; at the end of a filter row +-(wr - S) more (descriptor units)
+        const int64_t tap_step = p.flip ? -8 : 8;
+        const int64_t row_step = (p.flip ? -8 : 8) * static_cast<int64_t>(p.wr - p.S);
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++tc) {
             const HaloTile t = halo_tile(p, u);
             const int buf = tc % nbuf;
             mbar_wait(&tempty[buf], ((tc / nbuf) & 1) ^ 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + buf * p.ms * BN;
+            const uint32_t d_tmem = tmem_base + buf * MS * BN;
             uint32_t idesc = idesc_full;
             const int n_left = p.N - t.nt * BN;
             if (n_left < BN) {
@@ -188,26 +208,36 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
                 const int as = ai & 1;
                 mbar_wait(&a_full[as], (ai >> 1) & 1);
                 tc_fence_after();
-                const uint64_t a_slot = a_desc0 + static_cast<uint64_t>((as * p.halo_bytes) >> 4);
-                int kh = 0, kw = 0;
-                for (int tap = 0; tap < taps; ++tap, ++bi) {
-                    const int s = bi % S;
-                    mbar_wait(&b_full[s], (bi / S) & 1);
+                // tap (kh, kw) reads the halo shifted by kh*wr + kw rows (bwd-data: (R-1-kh)*wr +
+                // (S-1-kw)); walked incrementally, in 16-byte descriptor units (8 per row)
+                uint64_t a_tap = a_desc0 + static_cast<uint64_t>((as * p.halo_bytes) >> 4) +
+                                 static_cast<uint64_t>(p.flip ? ((p.R - 1) * p.wr + p.S - 1) * 8 : 0);
+                int kw = 0;
+                for (int tap = 0; tap < taps; ++tap) {
+                    mbar_wait(&b_full[bs], bph);
                     tc_fence_after();
-                    const int sh = p.flip ? (p.R - 1 - kh) * p.wr + (p.S - 1 - kw) : kh * p.wr + kw;
-                    const uint64_t a_s = a_slot + static_cast<uint64_t>(sh * (128 >> 4));
-                    const uint64_t b_s = b_desc0 + static_cast<uint64_t>(s * (Cfg::kBBytes >> 4));
-                    for (int sub = 0; sub < p.ms; ++sub) {
-                        const uint64_t a_sub = a_s + static_cast<uint64_t>(sub * (BM * 128 >> 4));
+                    const uint64_t b_s = b_desc0 + b_off;
+                    const bool first = cb == 0 && tap == 0;
+#pragma unroll
+                    for (int sub = 0; sub < MS; ++sub) {
+                        const uint64_t a_sub = a_tap + static_cast<uint64_t>(sub * (BM * 128 >> 4));
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)
                             umma_bf16_elect<1>(d_tmem + sub * BN, a_sub + static_cast<uint64_t>(k * 2), b_s + b_koff[k],
-                                               idesc, (cb > 0 || tap > 0 || k > 0) ? 1u : 0u);
+                                               idesc, (!first || k > 0) ? 1u : 0u);
                     }
-                    umma_commit_elect<1>(&b_empty[s]);
+                    umma_commit_elect<1>(&b_empty[bs]);
+                    if (++bs == S) {
+                        bs = 0;
+                        bph ^= 1;
+                        b_off = 0;
+                    } else {
+                        b_off += b_step;
+                    }
+                    a_tap += tap_step;
                     if (++kw == p.S) {
                         kw = 0;
-                        ++kh;
+                        a_tap += row_step;
                     }
                 }
                 umma_commit_elect<1>(&a_empty[as]);
@@ -237,10 +267,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
                 if (lane == 0) mbar_arrive(&tempty[buf]);
                 continue;
             }
-          for (int sub = 0; sub < p.ms; ++sub) {
+          for (int sub = 0; sub < MS; ++sub) {
             HaloTile t = t0;
             t.y0 += sub * p.th;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + (buf * p.ms + sub) * BN;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + (buf * MS + sub) * BN;
             const int oy = t.y0 + ry, ox = t.x0 + rx;
             const bool row_valid = rx < p.wv && oy < p.Ho && ox < p.Wo;
             for (int c0 = grp * 64; c0 < BN; c0 += 128) {
@@ -254,7 +284,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
                     if (nb + 32 + lane < p.n_bias) b1 = __ldg(p.bias + nb + 32 + lane);
                 }
                 tmem_ld_wait();
-                if (c0 + 128 >= BN && sub == p.ms - 1) {
+                if (c0 + 128 >= BN && sub == MS - 1) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[buf]);

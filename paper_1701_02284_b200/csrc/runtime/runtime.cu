@@ -1387,8 +1387,8 @@ SgdTensor sgd_tensor(tc_ctx* c, int pidx) {
     t.g = q.g;
     t.n = q.n;
     t.shadow = q.shadow;
-    t.shadow_rskc = q.rskc;
-    t.rskc_kmajor = q.crsk ? 1 : 0;
+    t.shadow_rskc = q.crsk ? nullptr : q.rskc;  // K-major copies: refresh_crsk after the update
+    t.rskc_kmajor = 0;
     t.K = q.K;
     t.RS = q.R * q.S;
     t.cs = q.cs;
@@ -1403,6 +1403,19 @@ SgdTensor sgd_tensor(tc_ctx* c, int pidx) {
 // bucket.  With overlap, both run on comm_st after the bucket's last gradient: every
 // read of these parameters by the backward precedes their Update statements in the
 // plan (PAPER.md:292-293 ordering), hence precedes the event.
+// K-major bwd-data filter copies ([cs][R][S][ks]) of the updated conv filters, transposed from
+// the fresh bf16 shadow in one coalesced pass each (the update kernel itself writes only the
+// [K][R][S][cs] shadow for these).
+tc_status refresh_crsk(tc_ctx* c, const std::vector<int>& params, cudaStream_t s2) {
+    for (int pidx : params) {
+        const ParamL& q = c->params[pidx];
+        if (!q.crsk || !q.rskc || !q.shadow || q.s2d || c->f32) continue;
+        tc_status r = launch_krsc_to_crsk(q.shadow, q.K, q.R * q.S, q.cs, q.Kw, q.rskc, q.ks, s2);
+        if (r != TC_OK) return r;
+    }
+    return TC_OK;
+}
+
 tc_status flush_bucket(tc_ctx* c, int b, int update, bool overlap) {
     tc_ctx::Bucket& bk = c->buckets[b];
     cudaStream_t s2 = c->st;
@@ -1417,7 +1430,8 @@ tc_status flush_bucket(tc_ctx* c, int b, int update, bool overlap) {
     std::vector<SgdTensor> ts;
     for (int pidx : bk.params)
         if (!(c->fuse_sgd_active && c->sgd_fused[pidx])) ts.push_back(sgd_tensor(c, pidx));
-    return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+    tc_status r = launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+    return r != TC_OK ? r : refresh_crsk(c, bk.params, s2);
 }
 
 // Clipped momentum update of every parameter (plan->clip > 0): the global norm of
@@ -1429,7 +1443,11 @@ tc_status clip_update(tc_ctx* c, cudaStream_t s2) {
                                     c->clip_partials, c->d_clip, s2);
     if (r != TC_OK) return r;
     for (SgdTensor& t : ts) t.gscale = c->d_clip;
-    return launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+    r = launch_sgd(ts.data(), static_cast<int>(ts.size()), nullptr, s2);
+    if (r != TC_OK) return r;
+    std::vector<int> all(c->params.size());
+    for (size_t i = 0; i < all.size(); ++i) all[i] = static_cast<int>(i);
+    return refresh_crsk(c, all, s2);
 }
 
 // Data parallel: every rank's Print holds its share of the global-batch loss (|N| = G*B);
@@ -1651,13 +1669,12 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
         if (offs[4 * i + 2] != SIZE_MAX) q.shadow = reinterpret_cast<bf16*>(c->slab + offs[4 * i + 2]);
         if (offs[4 * i + 3] != SIZE_MAX) {
             q.rskc = reinterpret_cast<bf16*>(c->slab + offs[4 * i + 3]);
-            // bwd-data filter operand K-major ([cs][R][S][ks]) when TCB_DGRAD_KMAJOR=1: the MMA
-            // issues exactly Cin columns and CTA-pair tiles can split the filter rows.  Default
-            // [R][S][ks][cs]: measured equal on AlexNet (74.4k vs 74.8k images/s) while the
-            // update's scattered 2-byte shadow stores cost 3x on the conv bucket
+            // bwd-data filter operand K-major ([cs][R][S][ks]; TCB_DGRAD_KMAJOR=0: [R][S][ks][cs]):
+            // the MMA issues exactly Cin columns (N = 96: 96 instead of 128) and the halo kernel
+            // loads only those filter rows; refreshed by a transpose of the shadow after the update
             static const bool kmajor = [] {
                 const char* e = std::getenv("TCB_DGRAD_KMAJOR");
-                return e && e[0] == '1';
+                return !(e && e[0] == '0');
             }();
             q.crsk = kmajor;
         }
