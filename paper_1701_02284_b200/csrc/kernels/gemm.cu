@@ -12,6 +12,7 @@
 #include "ops.cuh"
 #include "tc_gemm.cuh"
 #include "tc_conv_halo.cuh"
+#include "tc_wgrad_halo.cuh"
 
 namespace tcb {
 
@@ -664,6 +665,130 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
     return bn == 256 ? launch_halo<256, 1>(p, st) : bn == 128 ? launch_halo<128, 1>(p, st) : launch_halo<64, 1>(p, st);
 }
 
+// ------------------------------------------------------------------ halo-tile filter gradient
+struct WgradHaloPlan {
+    int ok = 0;
+    int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
+    int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0;
+    uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
+    size_t ws_bytes = 0;
+};
+
+static bool wgrad_halo_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_WGRAD_HALO");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Geometry of the halo filter gradient (tc_wgrad_halo.cuh) for a stride-1 conv with 64-multiple
+// channel strides: the pixel tile row stride wr with the most valid pixels per 128 positions, two
+// 64-channel blocks per unit when cs allows (MMA N = 128), tap groups sized to 512 TMEM columns,
+// and enough pixel splits to cover the SMs.
+static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
+    WgradHaloPlan pl;
+    // channel strides: 32-multiples for x (a partial last 64-channel block is zero-filled by TMA and
+    // its missing 32-column chunks are not stored), any 8-multiple for dy (a partial 64-wide k-atom)
+    if (!wgrad_halo_enabled() || d->stride != 1 || d->R * d->S == 1 || d->cs % 32 || d->ks % 8) return pl;
+    const int taps = d->R * d->S;
+    double best = 0;
+    for (int wr : {16, 32, 64, 128}) {
+        const int wv = wr - (d->S - 1);
+        if (wv <= 0) continue;
+        const int th = BM / wr, xt = ceil_div(d->Wo, wv), yt = ceil_div(d->Ho, th);
+        const double util = static_cast<double>(d->Ho) * d->Wo / (static_cast<double>(xt) * yt * BM);
+        if (th + d->R - 1 > 256 || util <= best + 1e-9) continue;
+        best = util;
+        pl.wr = wr, pl.th = th, pl.wv = wv, pl.xt = xt, pl.yt = yt, pl.hh = th + d->R - 1;
+    }
+    if (best < 0.5) return WgradHaloPlan{};  // (AlexNet conv3-5, 12 x 12: 56%, still ahead of im2col)
+    constexpr int kMaxSmem = 232448, kFixed = 1024 + 256 + 4 * kStagingBytes;
+    pl.dy_bytes = 2 * BM * 128;
+    pl.halo_bytes = (static_cast<uint32_t>(pl.hh) * pl.wr * 128 + static_cast<uint32_t>(d->S - 1) * 128 + 1023) & ~1023u;
+    for (int cb : {2, 1}) {
+        if (cb == 2 && d->cs <= 64) continue;
+        const uint32_t stage = pl.dy_bytes + cb * pl.halo_bytes;
+        const int stages = std::min(4, static_cast<int>((kMaxSmem - kFixed) / stage));
+        if (stages < 2) continue;
+        pl.cb = cb;
+        pl.stage_bytes = stage;
+        pl.stages = stages;
+        break;
+    }
+    if (!pl.stages) return WgradHaloPlan{};
+    const int max_taps = 512 / (pl.cb * 64);
+    pl.ntg = ceil_div(taps, max_taps);
+    pl.ntap = ceil_div(taps, pl.ntg);
+    pl.ncg = ceil_div(d->cs, 64 * pl.cb);
+    pl.mt = ceil_div(d->K, BM);
+    pl.tiles = d->N * pl.yt * pl.xt;
+    const int base = pl.mt * pl.ncg * pl.ntg;
+    const int want = std::max(1, num_sms() / base);
+    pl.tiles_per_split = ceil_div(pl.tiles, std::min(want, pl.tiles));
+    pl.splits = ceil_div(pl.tiles, pl.tiles_per_split);
+    pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * taps * d->cs * sizeof(float);
+    pl.ok = 1;
+    return pl;
+}
+
+static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, const void* dy, const void* x, float* dw,
+                                long long ldw, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (!ws || ws_bytes < pl.ws_bytes)
+        return fail(TC_INVALID_ARG, "halo filter gradient: workspace too small: need " + std::to_string(pl.ws_bytes));
+    WgradHaloParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.K = d->K;
+    p.R = d->R;
+    p.S = d->S;
+    p.pad = d->pad;
+    p.wr = pl.wr, p.th = pl.th, p.hh = pl.hh, p.wv = pl.wv, p.xt = pl.xt, p.yt = pl.yt, p.nimg = d->N;
+    p.Ho = d->Ho;
+    p.Wo = d->Wo;
+    p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.cs = d->cs, p.mt = pl.mt;
+    p.splits = pl.splits, p.tiles = pl.tiles, p.tiles_per_split = pl.tiles_per_split;
+    p.dy_bytes = pl.dy_bytes, p.halo_bytes = pl.halo_bytes, p.stage_bytes = pl.stage_bytes, p.stages = pl.stages;
+    std::string err;
+    if (!make_tmap_halo_src(&p.tmX, x, d->N, d->H, d->W, d->cs, pl.wr, pl.hh, &err)) return fail(TC_INVALID_ARG, err);
+    if (!make_tmap_halo_src(&p.tmDy, dy, d->N, d->Ho, d->Wo, d->ks, pl.wv, 1, &err)) return fail(TC_INVALID_ARG, err);
+    const uint64_t ncol = static_cast<uint64_t>(d->R) * d->S * d->cs;
+    if (!make_tmap_store(&p.tmWs, ws, false, ncol, d->K, pl.splits, ncol, &err)) return fail(TC_INVALID_ARG, err);
+    const int smem = 1024 + pl.stages * static_cast<int>(pl.stage_bytes) + 4 * kStagingBytes + 256;
+    auto kern = pl.cb == 2 ? tc_wgrad_halo_kernel<2> : tc_wgrad_halo_kernel<1>;
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TCB_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        for (auto k : {tc_wgrad_halo_kernel<1>, tc_wgrad_halo_kernel<2>}) {
+            const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+            if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("wgrad halo smem attr: ") + cudaGetErrorString(e));
+        }
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.mt * pl.ncg * pl.ntg * pl.splits);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_gemm() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = launch_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, kern, p);
+    TCB_LAUNCH_CHECK();
+    const long long total = static_cast<long long>(d->K) * static_cast<long long>(ncol);
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
+    TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K,
+               static_cast<int>(ncol), total, static_cast<void*>(dw), ldw, 0, static_cast<const float*>(nullptr), 0, 0,
+               0.f, 0);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
 static void init_params(GemmParams& p) {
     std::memset(&p, 0, sizeof(p));
     p.alpha = 1.f;
@@ -861,6 +986,8 @@ static LaunchPlan conv_plan(const tc_conv_desc* d, int which, bool w_kmajor = fa
 
 size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     if (!d) return 0;
+    if (which == 2)
+        if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok) return pl.ws_bytes;
     LaunchPlan lp = conv_plan(d, which);
     const bool swap = which == 2 && wgrad_swap(d);  // the transposed write goes through the reduce
     if (lp.splits <= 1 && !swap) return 0;
@@ -985,6 +1112,8 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
                                size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok)
+        return run_wgrad_halo(pl, d, dy, x, dw, filter_ld(d), ws, ws_bytes, static_cast<cudaStream_t>(stream));
     GemmParams p;
     init_params(p);
     const int npix = d->N * d->Ho * d->Wo;

@@ -1,0 +1,220 @@
+// Halo-tile filter gradient for stride-1 convolutions:
+//
+//   dW[k][tap][c] = sum over output pixels p of dy[p][k] * x[p + off(tap)][c]
+//
+// The im2col form (tc_gemm_kernel with an OP_IM2COL_MN B operand) streams x from L2 once per filter
+// tap.  Here a pixel tile is 128 positions laid out with row stride wr (th = 128 / wr output rows of
+// wv = wr - (S - 1) pixels each); per tile ONE tiled TMA box per 64-channel block stages the
+// (th + R - 1) x wr input halo, and every tap of the unit's tap group reads it as a row-shifted
+// MN-major SW128 view (start shifted by kh * wr + kw rows; the swizzle is address-based).  dy is
+// staged one output row at a time (box {64, wv, 1, 1}) into the same row-stride-wr layout, so the
+// wr - wv gap positions of every row stay zero (written once at kernel start) and contribute nothing
+// (they pair with wrapped halo rows).
+//
+//   unit  = (128-channel block of k (M), tap group (nt taps), channel group (CB x 64 c), pixel split)
+//   TMEM  = nt accumulators of CB * 64 fp32 columns, live for the whole pixel range of the unit
+//   MMA   = per tile, per tap, 8 k-steps of 16 pixels: M = 128 (k), N = CB * 64 (c), MN-major A / B
+//   out   = fp32 partials [split][K][R*S*cs] (TMA store), summed in fixed order by splitk_reduce
+//
+// Warp roles (256 threads): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-7 epilogue.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+#include "tc_gemm.cuh"
+
+namespace tcb {
+
+struct WgradHaloParams {
+    CUtensorMap tmX;   // 4-D tiled {cs, W, H, N} over x, box {64, wr, hh, 1}, SW128
+    CUtensorMap tmDy;  // 4-D tiled {ks, Wo, Ho, N} over dy, box {64, wv, 1, 1}, SW128
+    CUtensorMap tmWs;  // 3-D store {R*S*cs, K, splits} fp32, box {32, 32, 1}, SW128
+    int K;             // output channels (GEMM M)
+    int R, S, pad;
+    int wr, th, hh, wv, xt, yt, nimg;
+    int Ho, Wo;
+    int ntap, ntg;     // taps per group (accumulators), tap groups
+    int ncg;           // channel groups of CB x 64 channels
+    int cs;            // x channel stride (D column of tap t, channel c: t * cs + c)
+    int mt;            // 128-row blocks of K
+    int splits, tiles, tiles_per_split;
+    uint32_t dy_bytes;    // dy tile: 2 k-atoms x 128 rows x 128 B
+    uint32_t halo_bytes;  // per 64-channel halo (1024-aligned, includes the over-read slack)
+    uint32_t stage_bytes; // dy tile + CB halos
+    int stages;
+};
+
+template <int CB>
+__global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_constant__ WgradHaloParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    uint8_t* sStage = smem + S * p.stage_bytes;  // epilogue staging: 4 warps x 4 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * kStagingBytes);
+    uint64_t* empty = full + 4;
+    uint64_t* tdone = empty + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+
+    // unit decode: m block fastest (units sharing a tile of x / dy run side by side)
+    int u = blockIdx.x;
+    const int mb = u % p.mt;
+    u /= p.mt;
+    const int cg = u % p.ncg;
+    u /= p.ncg;
+    const int tg = u % p.ntg;
+    const int sp = u / p.ntg;
+    const int t0 = tg * p.ntap;
+    const int taps_here = min(p.ntap, p.R * p.S - t0);
+    const int tile0 = sp * p.tiles_per_split;
+    const int tile1 = min(p.tiles, tile0 + p.tiles_per_split);
+    const uint32_t ncols = static_cast<uint32_t>(p.ntap) * CB * 64;
+    const uint32_t tmem_cols = ncols <= 32 ? 32 : ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
+
+    // zero every stage and the staging once: the dy gap positions (wr - wv per row) and the halo
+    // over-read slack are never written by TMA (gap rows must be 0, slack rows finite: they meet
+    // in the products of the wrapped positions)
+    for (uint32_t i = threadIdx.x; i < (S * p.stage_bytes + 4 * kStagingBytes) / 16; i += blockDim.x)
+        st_shared_v4(smem_u32(smem) + i * 16, 0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.tmX);
+        tma_prefetch(&p.tmDy);
+        tma_prefetch(&p.tmWs);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tdone, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<1>(tmem_slot, tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+
+    const int per_img = p.yt * p.xt;
+    if (warp == 0) {
+        // ---------------- TMA producer: per tile, th dy row loads per k-atom + CB halo boxes
+        int s = 0;
+        uint32_t ph = 0;
+        const uint32_t tx = static_cast<uint32_t>(2 * p.th * p.wv * 128) + CB * static_cast<uint32_t>(p.hh * p.wr * 128);
+        for (int t = tile0; t < tile1; ++t) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const int img = t / per_img;
+            const int r = t - img * per_img;
+            const int ty = r / p.xt;
+            const int y0 = ty * p.th, x0 = (r - ty * p.xt) * p.wv;
+            uint8_t* st = smem + s * p.stage_bytes;
+            const uint32_t bar = smem_u32(&full[s]);
+            for (int a = 0; a < 2; ++a)
+                for (int j = 0; j < p.th; ++j)
+                    tma_load_4d_e(st + a * (p.dy_bytes / 2) + j * p.wr * 128, &p.tmDy, bar, mb * 128 + a * 64, x0,
+                                  y0 + j, img);
+            for (int c = 0; c < CB; ++c)
+                tma_load_4d_e(st + p.dy_bytes + c * p.halo_bytes, &p.tmX, bar, (cg * CB + c) * 64, x0 - p.pad,
+                              y0 - p.pad, img);
+            mbar_arrive_expect_tx_e(&full[s], tx);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        const uint32_t idesc = umma_idesc_bf16(BM, CB * 64, 1u, 1u);
+        // A = dy tile, MN-major: k-atoms 128 rows x 128 B apart (LBO), 8-row groups 1 KB (SBO);
+        // a k-step of 16 pixels = 2 KB.  B = halo, MN-major: channel blocks halo_bytes apart.
+        const uint64_t a0 = umma_desc_sw128(smem_u32(smem), p.dy_bytes / 2, 1024);
+        const uint64_t b0 = umma_desc_sw128(smem_u32(smem) + p.dy_bytes, p.halo_bytes, 1024);
+        const uint64_t step16 = p.stage_bytes >> 4;
+        int s = 0;
+        uint32_t ph = 0;
+        bool first = true;
+        for (int t = tile0; t < tile1; ++t) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint64_t so = static_cast<uint64_t>(s) * step16;
+            int kh = t0 / p.S, kw = t0 - (t0 / p.S) * p.S;
+            for (int j = 0; j < taps_here; ++j) {
+                const uint64_t b_tap = b0 + so + static_cast<uint64_t>((kh * p.wr + kw) * 8);
+                const uint32_t d = tmem_base + j * CB * 64;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma_bf16_elect<1>(d, a0 + so + static_cast<uint64_t>(k * 128), b_tap + static_cast<uint64_t>(k * 128),
+                                       idesc, (!first || k > 0) ? 1u : 0u);
+                if (++kw == p.S) {
+                    kw = 0;
+                    ++kh;
+                }
+            }
+            first = false;
+            umma_commit_elect<1>(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        umma_commit_elect<1>(tdone);
+    } else if (warp >= 4) {
+        // ---------------- epilogue: warp e reads TMEM lanes 32 (e - 4) .. +32 (rows k)
+        const int quarter = warp - 4;
+        uint8_t* stg = sStage + quarter * kStagingBytes;
+        mbar_wait(tdone, 0);
+        tc_fence_after();
+        const int m0 = mb * 128 + quarter * 32;
+        int nstore = 0;
+        if (tile1 > tile0) {
+            for (int j = 0; j < taps_here; ++j) {
+                for (int c0 = 0; c0 < CB * 64; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + j * CB * 64 + c0, r);
+                    tmem_ld_wait();
+                    if (nstore > 0) bulk_wait_read<0>();
+                    __syncwarp();
+                    const uint32_t row_addr = smem_u32(stg);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        st_shared_v4(row_addr + sw128_off(lane, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    const int col = (t0 + j) * p.cs + cg * CB * 64 + c0;
+                    if (m0 < p.K && cg * CB * 64 + c0 < p.cs) tma_store_3d_e(&p.tmWs, stg, col, m0, sp);
+                    bulk_commit();
+                    ++nstore;
+                }
+            }
+        } else {
+            // empty pixel range: this split's partial is zero
+            for (int i = lane; i < 32 * 32; i += 32) reinterpret_cast<uint32_t*>(stg)[i] = 0u;
+            fence_proxy_async_smem();
+            __syncwarp();
+            for (int j = 0; j < taps_here; ++j)
+                for (int c0 = 0; c0 < CB * 64; c0 += 32) {
+                    if (nstore > 0) bulk_wait_read<0>();
+                    __syncwarp();
+                    if (m0 < p.K && cg * CB * 64 + c0 < p.cs)
+                        tma_store_3d_e(&p.tmWs, stg, (t0 + j) * p.cs + cg * CB * 64 + c0, m0, sp);
+                    bulk_commit();
+                    ++nstore;
+                }
+        }
+        bulk_wait<0>();
+        __syncwarp();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem_base, tmem_cols);
+    }
+}
+
+}  // namespace tcb

@@ -242,7 +242,7 @@ def test_conv_bwd_data(case):
     assert rel_err(dx[..., :d.C], ref) < TOL
 
 
-@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES)
+@pytest.mark.parametrize("case", CONV_CASES + IM2COL_CASES + HALO_CASES)
 def test_conv_bwd_filter(case):
     x, w, b, d = conv_case(*case, seed=2)
     g = torch.Generator(device="cpu").manual_seed(6)
