@@ -2019,7 +2019,8 @@ tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
     if (c->plan->clip > 0)  // the clipped update needs the whole gradient: applied at the last Update
         return index == c->last_update_stmt ? clip_update(c, c->st) : TC_OK;
     SgdTensor t = sgd_tensor(c, s.param);
-    return launch_sgd(&t, 1, nullptr, c->st);
+    r = launch_sgd(&t, 1, nullptr, c->st);
+    return r != TC_OK ? r : refresh_crsk(c, {s.param}, c->st);
 }
 
 tc_status tc_test(tc_ctx* c, int iter, int n0, double* precision) {
