@@ -706,8 +706,13 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
     constexpr int kMaxSmem = 232448, kFixed = 1024 + 256 + 4 * kStagingBytes;
     pl.dy_bytes = 2 * BM * 128;
     pl.halo_bytes = (static_cast<uint32_t>(pl.hh) * pl.wr * 128 + static_cast<uint32_t>(d->S - 1) * 128 + 1023) & ~1023u;
+    static const int force_cb = [] {
+        const char* e = std::getenv("TCB_WGRAD_CB");
+        return e ? std::atoi(e) : 0;
+    }();
     for (int cb : {2, 1}) {
         if (cb == 2 && d->cs <= 64) continue;
+        if (force_cb && cb != force_cb) continue;
         const uint32_t stage = pl.dy_bytes + cb * pl.halo_bytes;
         const int stages = std::min(4, static_cast<int>((kMaxSmem - kFixed) / stage));
         if (stages < 2) continue;
