@@ -668,6 +668,7 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
 // ------------------------------------------------------------------ halo-tile filter gradient
 struct WgradHaloPlan {
     int ok = 0;
+    int swap = 0;  // K <= 64: tc_wgrad_halo_swap_kernel (M = two taps x 64 channels, N = K)
     int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
     int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0;
     uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
@@ -704,14 +705,19 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
     }
     if (best < 0.5) return WgradHaloPlan{};  // (AlexNet conv3-5, 12 x 12: 56%, still ahead of im2col)
     constexpr int kMaxSmem = 232448, kFixed = 1024 + 256 + 4 * kStagingBytes;
-    pl.dy_bytes = 2 * BM * 128;
+    static const bool swap_on = [] {
+        const char* e = std::getenv("TCB_WGRAD_SWAP_HALO");
+        return !(e && e[0] == '0');
+    }();
+    pl.swap = swap_on && d->K <= 64;
+    pl.dy_bytes = (pl.swap ? 1 : 2) * BM * 128;
     pl.halo_bytes = (static_cast<uint32_t>(pl.hh) * pl.wr * 128 + static_cast<uint32_t>(d->S - 1) * 128 + 1023) & ~1023u;
     static const int force_cb = [] {
         const char* e = std::getenv("TCB_WGRAD_CB");
         return e ? std::atoi(e) : 0;
     }();
     for (int cb : {2, 1}) {
-        if (cb == 2 && d->cs <= 64) continue;
+        if (cb == 2 && (d->cs <= 64 || pl.swap)) continue;
         if (force_cb && cb != force_cb) continue;
         const uint32_t stage = pl.dy_bytes + cb * pl.halo_bytes;
         const int stages = std::min(4, static_cast<int>((kMaxSmem - kFixed) / stage));
@@ -722,11 +728,11 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
         break;
     }
     if (!pl.stages) return WgradHaloPlan{};
-    const int max_taps = 512 / (pl.cb * 64);
+    const int max_taps = pl.swap ? 16 : 512 / (pl.cb * 64);  // swap: 8 tap pairs x 64 columns
     pl.ntg = ceil_div(taps, max_taps);
     pl.ntap = ceil_div(taps, pl.ntg);
     pl.ncg = ceil_div(d->cs, 64 * pl.cb);
-    pl.mt = ceil_div(d->K, BM);
+    pl.mt = pl.swap ? 1 : ceil_div(d->K, BM);
     pl.tiles = d->N * pl.yt * pl.xt;
     const int base = pl.mt * pl.ncg * pl.ntg;
     const int want = std::max(1, num_sms() / base);
@@ -759,13 +765,13 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     const uint64_t ncol = static_cast<uint64_t>(d->R) * d->S * d->cs;
     if (!make_tmap_store(&p.tmWs, ws, false, ncol, d->K, pl.splits, ncol, &err)) return fail(TC_INVALID_ARG, err);
     const int smem = 1024 + pl.stages * static_cast<int>(pl.stage_bytes) + 4 * kStagingBytes + 256;
-    auto kern = pl.cb == 2 ? tc_wgrad_halo_kernel<2> : tc_wgrad_halo_kernel<1>;
+    auto kern = pl.swap ? tc_wgrad_halo_swap_kernel : pl.cb == 2 ? tc_wgrad_halo_kernel<2> : tc_wgrad_halo_kernel<1>;
     static std::atomic<uint64_t> attr_done{0};
     int dev = 0;
     TCB_CUDA_CHECK(cudaGetDevice(&dev));
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_done.load(std::memory_order_acquire) & bit)) {
-        for (auto k : {tc_wgrad_halo_kernel<1>, tc_wgrad_halo_kernel<2>}) {
+        for (auto k : {tc_wgrad_halo_kernel<1>, tc_wgrad_halo_kernel<2>, tc_wgrad_halo_swap_kernel}) {
             const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
             if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("wgrad halo smem attr: ") + cudaGetErrorString(e));
         }

@@ -660,7 +660,7 @@ struct LossArgs {
 // Deterministic two-level reduction in one launch: kLossBlocks blocks write fp64
 // partials; the last block to finish (ticket counter) sums them in block order and
 // resets the counter for the next step (graph replays).
-constexpr int kLossBlocks = 32;
+constexpr int kLossBlocks = 128;
 __global__ void __launch_bounds__(256) k_loss(LossArgs args, float* out, double* partial, unsigned* ticket) {
     pdl_wait();
     pdl_trigger();
@@ -1899,7 +1899,9 @@ tc_status launch_softmax_bwd(const float* dy, const float* y, T* dx, long long o
 template <typename T>
 tc_status launch_softmax_xent(const T* z, long long ld, const int32_t* labels, float c, float* L, float* Y, T* dz,
                               int rows, int F, cudaStream_t st) {
-    TCB_LAUNCH(k_softmax_xent<T>, grid_for(rows, 8), 256, 0, st, z, ld, labels, c, L, Y, dz, rows, F);
+    // one warp per block: every row's warp on its own SM (the head is latency-bound: 128 rows of
+    // 1000 classes on 16 blocks of 8 warps measured 15.9 us)
+    TCB_LAUNCH(k_softmax_xent<T>, rows, 32, 0, st, z, ld, labels, c, L, Y, dz, rows, F);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

@@ -217,4 +217,157 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
     }
 }
 
+// Narrow-k form (K <= 64 output channels, e.g. VGG conv1_2): the transposed product
+//   dW^T[(tap, c)][k] = sum_p x[p + off(tap)][c] * dy[p][k]
+// with M = two taps x 64 channels of the halo (two MN-major atoms of one halo, LBO = the two taps'
+// shift difference), N = 64 (k), so the 128-row MMA is full where the direct form would fill 64 of
+// its rows.  Up to 8 tap pairs (512 TMEM columns) per unit; the epilogue transposes each 32 x 32
+// chunk through shared memory into the [k][tap][c] partials.
+__global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid_constant__ WgradHaloParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = p.stages;
+    uint8_t* sStage = smem + S * p.stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 4 * kStagingBytes);
+    uint64_t* empty = full + 4;
+    uint64_t* tdone = empty + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdone + 1);
+
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    int u = blockIdx.x;
+    const int cg = u % p.ncg;
+    u /= p.ncg;
+    const int tg = u % p.ntg;
+    const int sp = u / p.ntg;
+    const int t0 = tg * p.ntap;
+    const int taps_here = min(p.ntap, p.R * p.S - t0);
+    const int pairs = (taps_here + 1) / 2;
+    const int tile0 = sp * p.tiles_per_split;
+    const int tile1 = min(p.tiles, tile0 + p.tiles_per_split);
+    const uint32_t ncols = static_cast<uint32_t>((p.ntap + 1) / 2) * 64;
+    const uint32_t tmem_cols = ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
+
+    for (uint32_t i = threadIdx.x; i < (S * p.stage_bytes + 4 * kStagingBytes) / 16; i += blockDim.x)
+        st_shared_v4(smem_u32(smem) + i * 16, 0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.tmX);
+        tma_prefetch(&p.tmDy);
+        tma_prefetch(&p.tmWs);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tdone, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<1>(tmem_slot, tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+
+    const int per_img = p.yt * p.xt;
+    if (warp == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        const uint32_t tx = static_cast<uint32_t>(p.th * p.wv * 128) + static_cast<uint32_t>(p.hh * p.wr * 128);
+        for (int t = tile0; t < tile1; ++t) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const int img = t / per_img;
+            const int r = t - img * per_img;
+            const int ty = r / p.xt;
+            const int y0 = ty * p.th, x0 = (r - ty * p.xt) * p.wv;
+            uint8_t* st = smem + s * p.stage_bytes;
+            const uint32_t bar = smem_u32(&full[s]);
+            for (int j = 0; j < p.th; ++j) tma_load_4d_e(st + j * p.wr * 128, &p.tmDy, bar, 0, x0, y0 + j, img);
+            tma_load_4d_e(st + p.dy_bytes, &p.tmX, bar, cg * 64, x0 - p.pad, y0 - p.pad, img);
+            mbar_arrive_expect_tx_e(&full[s], tx);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = umma_idesc_bf16(BM, 64, 1u, 1u);
+        const uint64_t step16 = p.stage_bytes >> 4;
+        const uint64_t b0 = umma_desc_sw128(smem_u32(smem), 0, 1024);  // dy: one 64-wide k atom
+        int s = 0;
+        uint32_t ph = 0;
+        bool first = true;
+        for (int t = tile0; t < tile1; ++t) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t halo = smem_u32(smem) + s * p.stage_bytes + p.dy_bytes;
+            const uint64_t so = static_cast<uint64_t>(s) * step16;
+            for (int q = 0; q < pairs; ++q) {
+                const int ta = t0 + 2 * q, tb = min(ta + 1, t0 + taps_here - 1);
+                const int sa = (ta / p.S) * p.wr + ta % p.S, sb = (tb / p.S) * p.wr + tb % p.S;
+                // atom 1 (rows 64-127 of M) = tap tb's view: LBO = the shift difference (>= 0;
+                // a lone last tap repeats itself and its rows are not stored)
+                const uint64_t a_pair = umma_desc_sw128(halo + sa * 128, (sb - sa) * 128, 1024);
+                const uint32_t d = tmem_base + q * 64;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma_bf16_elect<1>(d, a_pair + static_cast<uint64_t>(k * 128), b0 + so + static_cast<uint64_t>(k * 128),
+                                       idesc, (!first || k > 0) ? 1u : 0u);
+            }
+            first = false;
+            umma_commit_elect<1>(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        umma_commit_elect<1>(tdone);
+    } else if (warp >= 4) {
+        // warp e: TMEM lanes 32 (e - 4) .. +32 = tap (e - 4) / 2 of each pair, channels 32 ((e - 4) % 2) + lane
+        const int quarter = warp - 4;
+        uint8_t* stg = sStage + quarter * kStagingBytes;
+        mbar_wait(tdone, 0);
+        tc_fence_after();
+        const int csub = (quarter & 1) * 32;
+        int nstore = 0;
+        for (int q = 0; q < pairs; ++q) {
+            const int tap = t0 + 2 * q + (quarter >> 1);
+            const bool tap_ok = tap < t0 + taps_here && cg * 64 + csub < p.cs;
+            for (int k0 = 0; k0 < 64; k0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + q * 64 + k0, r);
+                tmem_ld_wait();
+                if (tile1 <= tile0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = 0u;
+                }
+                if (nstore > 0) bulk_wait_read<0>();
+                __syncwarp();
+                // transpose: staging row j (= output channel k0 + j) holds the 32 channels c (lanes)
+                const uint32_t base = smem_u32(stg);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + j * 128 + ((((lane >> 2) ^ (j & 7)) << 4) | ((lane & 3) << 2))),
+                                 "r"(r[j])
+                                 : "memory");
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (tap_ok && k0 < p.K) tma_store_3d_e(&p.tmWs, stg, tap * p.cs + cg * 64 + csub, k0, sp);
+                bulk_commit();
+                ++nstore;
+            }
+        }
+        bulk_wait<0>();
+        __syncwarp();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem_base, tmem_cols);
+    }
+}
+
 }  // namespace tcb

@@ -1715,8 +1715,8 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->d_labels, 0, plan->input_dims[0] * sizeof(int32_t), c->st));
-    TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 1024));
-    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_loss, 0, 1024, c->st));
+    TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 4096));  // loss, fp64 block partials, ticket (launch_loss)
+    TCB_CUDA_CHECK(cudaMemsetAsync(c->d_loss, 0, 4096, c->st));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_iter, 256));
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_iter, 256));
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_loss, 256));

@@ -182,6 +182,8 @@ HALO_CASES = [
     (1, 64, 3, 126, 64, 3, 1, 1),     # wr 128
     (2, 128, 28, 28, 384, 3, 1, 1),   # 2 channel blocks, 256-wide column tiles
     (1, 256, 30, 30, 256, 3, 1, 1),   # 4 channel blocks
+    (2, 64, 20, 20, 32, 5, 1, 2),     # filter gradient with K <= 64: the tap-pair (swapped) form, 5x5
+    (2, 128, 14, 14, 48, 3, 1, 1),    # K = 48, two channel blocks
 ]
 
 
