@@ -13,6 +13,7 @@
 #include "tc_gemm.cuh"
 #include "tc_conv_halo.cuh"
 #include "tc_wgrad_halo.cuh"
+#include "tc_conv_c4.cuh"
 
 namespace tcb {
 
@@ -800,6 +801,80 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     return TC_OK;
 }
 
+// ------------------------------------------------------------------ channel-stride-4 first layer
+static bool conv_c4_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_CONV_C4");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Eligible: a channel-stride-4 image, whole 128-pixel tiles per image, rows wide enough that a
+// tile spans at most 5 output rows, and 64 output channels (the first layers of the configs).
+static bool conv_c4_fwd_ok(const tc_conv_desc* d) {
+    const long long hw = static_cast<long long>(d->Ho) * d->Wo;
+    return conv_c4_enabled() && d->cs == 4 && hw % BM == 0 && d->Wo >= 32 && d->ks == 64 && d->K <= 64 &&
+           d->R * d->S <= 64 && d->stride <= 4;
+}
+
+static tc_status run_conv_c4_fwd(const tc_conv_desc* d, const void* x, const void* w, const float* bias, int relu,
+                                 void* y, cudaStream_t st) {
+    constexpr int BN = 64;
+    ConvC4Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.x = static_cast<const __nv_bfloat16*>(x);
+    p.H = d->H, p.W = d->W, p.Ho = d->Ho, p.Wo = d->Wo, p.R = d->R, p.S = d->S, p.stride = d->stride, p.pad = d->pad;
+    p.taps = d->R * d->S;
+    p.nkb = ceil_div(p.taps, 16);
+    p.margin = (d->pad + 1) & ~1;
+    const int rows_out = ceil_div(BM, d->Wo) + 1;
+    p.rows_in = (rows_out - 1) * d->stride + d->R;
+    p.pitch = ((d->W + 2 * p.margin) * 8 + 15) & ~15;
+    p.tiles = static_cast<int>(static_cast<long long>(d->N) * d->Ho * d->Wo / BM);
+    p.bias = bias;
+    p.n_bias = d->K;
+    p.relu = relu;
+    // staged-row slots first (the loader's lead over the builders hides the row-copy latency),
+    // then A ring slots: up to 8 / 8, at least 2 / 2
+    constexpr int kMaxSmem = 232448;
+    const int base = 1024 + p.nkb * ConvC4Cfg<BN>::kBBytes + 16 * kStagingBytes + 1024 + 512;
+    const int slot = p.rows_in * p.pitch;
+    p.h_slots = std::max(2, std::min(6, (kMaxSmem - base - 4 * BM * 128) / slot));
+    p.a_stages = std::min(8, (kMaxSmem - base - p.h_slots * slot) / (BM * 128));
+    if (p.a_stages < 2) return fail(TC_INTERNAL, "c4 conv: shared memory too small");
+    const int smem = base + p.h_slots * slot + p.a_stages * BM * 128;
+    std::string err;
+    const int wld = d->wld ? d->wld : d->R * d->S * d->cs;  // [Cout][R][S][4] rows, padded to a multiple of 8
+    if (!make_tmap_2d_bf16(&p.tmB, w, static_cast<uint64_t>(wld), d->K, wld, BK, BN, &err)) return fail(TC_INVALID_ARG, err);
+    const long long M = static_cast<long long>(d->N) * d->Ho * d->Wo;
+    if (!make_tmap_store(&p.tmD, y, true, d->ks, M, 1, d->ks, &err)) return fail(TC_INVALID_ARG, err);
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TCB_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        const cudaError_t e = cudaFuncSetAttribute(tc_conv_c4_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("c4 conv smem attr: ") + cudaGetErrorString(e));
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::min(p.tiles, num_sms()));
+    cfg.blockDim = dim3(kC4Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_gemm() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = launch_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, tc_conv_c4_fwd_kernel<BN>, p);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
 static void init_params(GemmParams& p) {
     std::memset(&p, 0, sizeof(p));
     p.alpha = 1.f;
@@ -1015,6 +1090,7 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
                       int y_f32, void* ws, size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (!y_f32 && conv_c4_fwd_ok(d)) return run_conv_c4_fwd(d, x, w, bias, relu, y, static_cast<cudaStream_t>(stream));
     if (const HaloGeom hg = fprop_halo(d); hg.wr)
         return run_halo(hg, x, d->N, d->H, d->W, d->cs, d->Ho, d->Wo, d->R, d->S, d->pad, false, w, d->K, filter_ld(d),
                         false, d->ks, y, !y_f32, bias, d->K, relu, nullptr, static_cast<cudaStream_t>(stream));

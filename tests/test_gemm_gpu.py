@@ -187,7 +187,10 @@ HALO_CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", [(2, 3, 35, 35, 96, 11, 4, 0), (2, 3, 32, 32, 64, 7, 2, 3), (2, 1, 28, 28, 20, 5, 1, 0)])
+# the last three take the first-layer fprop kernel (tc_conv_c4.cuh): 64 outputs, whole 128-pixel
+# tiles, 3x3/1 (VGG conv1_1), 7x7/2 pad 3 (GoogLeNet / ResNet conv1), tiles spanning 3-4 rows
+@pytest.mark.parametrize("case", [(2, 3, 35, 35, 96, 11, 4, 0), (2, 3, 32, 32, 64, 7, 2, 3), (2, 1, 28, 28, 20, 5, 1, 0),
+                                  (2, 3, 64, 64, 64, 3, 1, 1), (2, 3, 128, 128, 64, 7, 2, 3), (1, 3, 96, 96, 64, 7, 2, 3)])
 def test_conv_channel_stride4_fwd_and_filter(case):
     """First-layer convs: input staged with channel stride 4 (8-byte tap gathers),
     filter rows padded to a multiple of 8 (wld)."""
