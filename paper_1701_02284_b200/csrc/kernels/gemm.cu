@@ -875,6 +875,88 @@ static tc_status run_conv_c4_fwd(const tc_conv_desc* d, const void* x, const voi
     return TC_OK;
 }
 
+struct ConvC4WgradPlan {
+    int ok = 0, splits = 0, tiles = 0, tps = 0;
+    size_t ws_bytes = 0;
+};
+static ConvC4WgradPlan conv_c4_wgrad_plan(const tc_conv_desc* d) {
+    ConvC4WgradPlan pl;
+    if (!conv_c4_fwd_ok(d)) return pl;
+    static const bool on = [] {
+        const char* e = std::getenv("TCB_CONV_C4_WGRAD");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) return pl;
+    pl.tiles = static_cast<int>(static_cast<long long>(d->N) * d->Ho * d->Wo / BM);
+    pl.tps = ceil_div(pl.tiles, std::min(pl.tiles, num_sms()));
+    pl.splits = ceil_div(pl.tiles, pl.tps);
+    const int wld = d->wld ? d->wld : d->R * d->S * d->cs;
+    pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * wld * sizeof(float);
+    pl.ok = 1;
+    return pl;
+}
+
+static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc* d, const void* dy, const void* x,
+                                   float* dw, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (!ws || ws_bytes < pl.ws_bytes)
+        return fail(TC_INVALID_ARG, "c4 filter gradient: workspace too small: need " + std::to_string(pl.ws_bytes));
+    ConvC4WgradParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.x = static_cast<const __nv_bfloat16*>(x);
+    p.H = d->H, p.W = d->W, p.Ho = d->Ho, p.Wo = d->Wo, p.R = d->R, p.S = d->S, p.stride = d->stride, p.pad = d->pad;
+    p.taps = d->R * d->S;
+    p.nkb = ceil_div(p.taps, 16);
+    p.nkb2 = (p.nkb + 1) & ~1;
+    p.margin = (d->pad + 1) & ~1;
+    const int rows_out = ceil_div(BM, d->Wo) + 1;
+    p.rows_in = (rows_out - 1) * d->stride + d->R;
+    p.pitch = ((d->W + 2 * p.margin) * 8 + 15) & ~15;
+    p.K = d->K;
+    p.Kw = d->wld ? d->wld : d->R * d->S * d->cs;
+    p.tiles = pl.tiles;
+    p.tiles_per_split = pl.tps;
+    constexpr int kMaxSmem = 232448;
+    const int tile_bytes = (p.nkb2 + 1) * BM * 128;
+    const int base = 1024 + 2 * tile_bytes + 4 * kStagingBytes + 1024 + 512;
+    const int slot = p.rows_in * p.pitch;
+    p.h_slots = std::min(8, (kMaxSmem - base) / slot);
+    if (p.h_slots < 2) return fail(TC_INTERNAL, "c4 filter gradient: shared memory too small");
+    const int smem = base + p.h_slots * slot;
+    std::string err;
+    const long long M = static_cast<long long>(d->N) * d->Ho * d->Wo;
+    if (!make_tmap_2d_bf16(&p.tmDy, dy, d->ks, M, d->ks, 64, BM, &err)) return fail(TC_INVALID_ARG, err);
+    if (!make_tmap_store(&p.tmWs, ws, false, p.Kw, d->K, pl.splits, p.Kw, &err)) return fail(TC_INVALID_ARG, err);
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TCB_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+        const cudaError_t e = cudaFuncSetAttribute(tc_conv_c4_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if (e != cudaSuccess) return fail(TC_CUDA_ERROR, std::string("c4 wgrad smem attr: ") + cudaGetErrorString(e));
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.splits);
+    cfg.blockDim = dim3(kC4Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_gemm() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = launch_priority();
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, tc_conv_c4_wgrad_kernel, p);
+    TCB_LAUNCH_CHECK();
+    const long long total = static_cast<long long>(d->K) * p.Kw;
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
+    TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K, p.Kw, total,
+               static_cast<void*>(dw), static_cast<long long>(p.Kw), 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
 static void init_params(GemmParams& p) {
     std::memset(&p, 0, sizeof(p));
     p.alpha = 1.f;
@@ -1072,8 +1154,10 @@ static LaunchPlan conv_plan(const tc_conv_desc* d, int which, bool w_kmajor = fa
 
 size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     if (!d) return 0;
-    if (which == 2)
+    if (which == 2) {
+        if (const ConvC4WgradPlan pl = conv_c4_wgrad_plan(d); pl.ok) return pl.ws_bytes;
         if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok) return pl.ws_bytes;
+    }
     LaunchPlan lp = conv_plan(d, which);
     const bool swap = which == 2 && wgrad_swap(d);  // the transposed write goes through the reduce
     if (lp.splits <= 1 && !swap) return 0;
@@ -1199,6 +1283,8 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
                                size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (const ConvC4WgradPlan pl = conv_c4_wgrad_plan(d); pl.ok)
+        return run_conv_c4_wgrad(pl, d, dy, x, dw, ws, ws_bytes, static_cast<cudaStream_t>(stream));
     if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok)
         return run_wgrad_halo(pl, d, dy, x, dw, filter_ld(d), ws, ws_bytes, static_cast<cudaStream_t>(stream));
     GemmParams p;

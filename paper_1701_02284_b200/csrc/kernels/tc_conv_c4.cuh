@@ -300,4 +300,244 @@ __global__ void __launch_bounds__(kC4Threads, 1) tc_conv_c4_fwd_kernel(const __g
     }
 }
 
+// Filter gradient of the same layers:  dW^T[k][cout] = sum_p A[p][k] * dy[p][cout]  with the A
+// tiles (k = tap * 4 + channel) assembled exactly as in the forward from staged input rows.  The
+// built [128 pixel][64 k] k-blocks are MN-major operands for M = k (two k-blocks per 128-row MMA,
+// LBO = one k-block), dy tiles ([128 pixel][64 cout], one TMA box) are the MN-major N = 64 side,
+// and the accumulators (ceil(nkb / 2) x 64 TMEM columns) live for the CTA's whole pixel range;
+// fp32 partials go out transposed to [split][cout][Kw] for the fixed-order reduce.
+struct ConvC4WgradParams {
+    CUtensorMap tmDy;  // dy [M pixels][ks] K... box {64 cout, 128 pixels}, SW128
+    CUtensorMap tmWs;  // partials {Kw, K, splits} fp32, box {32, 32, 1}
+    const __nv_bfloat16* x;
+    int H, W, Ho, Wo, R, S, stride, pad, taps, nkb, nkb2;  // nkb2 = nkb rounded up to even
+    int margin, rows_in, pitch, h_slots;
+    int K, Kw;
+    int tiles, tiles_per_split;
+};
+
+__global__ void __launch_bounds__(kC4Threads, 1) tc_conv_c4_wgrad_kernel(const __grid_constant__ ConvC4WgradParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t tile_bytes = static_cast<uint32_t>(p.nkb2) * BM * 128 + BM * 128;  // A k-blocks + dy
+    uint8_t* sT = smem;                                                    // 2 tile slots
+    uint8_t* sHalo = sT + 2 * tile_bytes;                                  // h_slots x rows_in x pitch
+    uint8_t* sStage = sHalo + ((p.h_slots * p.rows_in * p.pitch + 1023) & ~1023);  // 4 warps x 4 KB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 4 * kStagingBytes);
+    uint64_t* h_full = bars;        // [8]
+    uint64_t* h_empty = bars + 8;   // [8]
+    uint64_t* t_full = bars + 16;   // [2]
+    uint64_t* t_empty = bars + 18;  // [2]
+    uint64_t* tdone = bars + 20;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const int HW = p.Ho * p.Wo;
+    const uint32_t row_bytes = static_cast<uint32_t>(p.W) * 8;
+    const int sp = blockIdx.x;
+    const int tile0 = sp * p.tiles_per_split, tile1 = min(p.tiles, tile0 + p.tiles_per_split);
+    const int halves = p.nkb2 / 2;
+    const uint32_t tmem_cols = halves * 64 <= 64 ? 64 : halves * 64 <= 128 ? 128 : 256;
+
+    // zero the staged-row slots (margins) and both tile slots (an odd nkb leaves one k-block
+    // per tile that the builders never write: it must read as zeros)
+    for (uint32_t i = threadIdx.x; i < (2 * tile_bytes) / 16; i += blockDim.x) st_shared_v4(smem_u32(sT) + i * 16, 0u, 0u, 0u, 0u);
+    for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(p.h_slots * p.rows_in * p.pitch) / 16; i += blockDim.x)
+        st_shared_v4(smem_u32(sHalo) + i * 16, 0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.tmDy);
+        tma_prefetch(&p.tmWs);
+        for (int s = 0; s < p.h_slots; ++s) {
+            mbar_init(&h_full[s], 1);
+            mbar_init(&h_empty[s], 256);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&t_full[s], 256 + 1);  // both builder groups + the dy load's arrive
+            mbar_init(&t_empty[s], 1);
+        }
+        mbar_init(tdone, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<1>(tmem_slot, tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+
+    if (warp == 0) {
+        // ---------------- loader: staged input rows of the tile + its dy box
+        int hs = 0, ts = 0;
+        uint32_t hph = 0, tph = 0;
+        for (int u = tile0; u < tile1; ++u) {
+            mbar_wait(&h_empty[hs], hph ^ 1);
+            const int m0 = u * BM;
+            const int n = m0 / HW;
+            const int y0 = (m0 - n * HW) / p.Wo, y1 = (m0 + BM - 1 - n * HW) / p.Wo;
+            const int iy0 = y0 * p.stride - p.pad;
+            const int rows = (y1 - y0) * p.stride + p.R;
+            uint8_t* slot = sHalo + hs * p.rows_in * p.pitch;
+            int valid = 0;
+            for (int r = 0; r < rows; ++r) {
+                const int iy = iy0 + r;
+                if (iy >= 0 && iy < p.H) {
+                    ++valid;
+                } else {
+                    for (uint32_t o = lane * 16; o < row_bytes; o += 32 * 16)
+                        st_shared_v4(smem_u32(slot + r * p.pitch + p.margin * 8) + o, 0u, 0u, 0u, 0u);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&h_full[hs], valid * row_bytes);
+                for (int r = 0; r < rows; ++r) {
+                    const int iy = iy0 + r;
+                    if (iy < 0 || iy >= p.H) continue;
+                    const __nv_bfloat16* src = p.x + (static_cast<long long>(n) * p.H + iy) * p.W * 4;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_u32(slot + r * p.pitch + p.margin * 8)),
+                        "l"(src), "r"(row_bytes), "r"(smem_u32(&h_full[hs]))
+                        : "memory");
+                }
+            }
+            __syncwarp();
+            // dy of the tile into the tile slot (after the MMA released it)
+            mbar_wait(&t_empty[ts], tph ^ 1);
+            tma_load_2d_e<1>(sT + ts * tile_bytes + p.nkb2 * BM * 128, &p.tmDy, smem_u32(&t_full[ts]), 0, m0);
+            mbar_arrive_expect_tx_e(&t_full[ts], BM * 128);
+            if (++hs == p.h_slots) {
+                hs = 0;
+                hph ^= 1;
+            }
+            if (++ts == 2) {
+                ts = 0;
+                tph ^= 1;
+            }
+        }
+    } else if ((warp >= 4 && warp < 8) || warp >= 12) {
+        // ---------------- A builders (as in the forward), k-blocks alternating between the groups
+        const int bg = warp >= 12 ? 1 : 0;
+        const int t = threadIdx.x - (bg ? 384 : 128);
+        int hs = 0, ts = 0;
+        uint32_t hph = 0, tph = 0;
+        for (int u = tile0; u < tile1; ++u) {
+            const int m0 = u * BM;
+            const int n = m0 / HW;
+            const int y0 = (m0 - n * HW) / p.Wo;
+            const int pix = m0 + t - n * HW;
+            const int oy = pix / p.Wo, ox = pix - (pix / p.Wo) * p.Wo;
+            mbar_wait(&h_full[hs], hph);
+            mbar_wait(&t_empty[ts], tph ^ 1);
+            const uint32_t base = smem_u32(sHalo + hs * p.rows_in * p.pitch) +
+                                  static_cast<uint32_t>((oy - y0) * p.stride * p.pitch + (ox * p.stride - p.pad + p.margin) * 8);
+            for (int kb = bg; kb < p.nkb; kb += 2) {
+                const uint32_t dst = smem_u32(sT + ts * tile_bytes + kb * (BM * 128)) + t * 128;
+                int kh = (kb * 16) / p.S, kw = kb * 16 - kh * p.S;
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (kb * 16 + j + h < p.taps) {
+                            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
+                                         : "=r"(v[2 * h]), "=r"(v[2 * h + 1])
+                                         : "r"(base + kh * p.pitch + kw * 8));
+                            if (++kw == p.S) {
+                                kw = 0;
+                                ++kh;
+                            }
+                        }
+                    }
+                    st_shared_v4(dst + (((j >> 1) ^ (t & 7)) << 4), v[0], v[1], v[2], v[3]);
+                }
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&t_full[ts]);
+            mbar_arrive(&h_empty[hs]);
+            if (++hs == p.h_slots) {
+                hs = 0;
+                hph ^= 1;
+            }
+            if (++ts == 2) {
+                ts = 0;
+                tph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA: M = 128 k (two k-blocks), N = 64 cout, K = 128 pixels per tile
+        const uint32_t idesc = umma_idesc_bf16(BM, 64, 1u, 1u);
+        int ts = 0;
+        uint32_t tph = 0;
+        bool first = true;
+        for (int u = tile0; u < tile1; ++u) {
+            mbar_wait(&t_full[ts], tph);
+            tc_fence_after();
+            const uint32_t tb = smem_u32(sT + ts * tile_bytes);
+            const uint64_t b0 = umma_desc_sw128(tb + p.nkb2 * BM * 128, 0, 1024);
+            for (int h = 0; h < halves; ++h) {
+                const uint64_t a0 = umma_desc_sw128(tb + 2 * h * BM * 128, BM * 128, 1024);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma_bf16_elect<1>(tmem_base + h * 64, a0 + static_cast<uint64_t>(k * 128),
+                                       b0 + static_cast<uint64_t>(k * 128), idesc, (!first || k > 0) ? 1u : 0u);
+            }
+            first = false;
+            umma_commit_elect<1>(&t_empty[ts]);
+            if (++ts == 2) {
+                ts = 0;
+                tph ^= 1;
+            }
+        }
+        umma_commit_elect<1>(tdone);
+    } else if (warp >= 8 && warp < 12) {
+        // ---------------- epilogue: warp q holds k = 128 h + 32 q + lane; transposed 32 x 32 stores
+        const int quarter = warp - 8;
+        uint8_t* stg = sStage + quarter * kStagingBytes;
+        if (tile1 > tile0) {
+            mbar_wait(tdone, 0);
+            tc_fence_after();
+        }
+        int nstore = 0;
+        for (int h = 0; h < halves; ++h) {
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                uint32_t r[32];
+                if (tile1 > tile0) {
+                    tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + h * 64 + c0, r);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = 0u;
+                }
+                if (nstore > 0) bulk_wait_read<0>();
+                __syncwarp();
+                const uint32_t base = smem_u32(stg);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + j * 128 + ((((lane >> 2) ^ (j & 7)) << 4) | ((lane & 3) << 2))),
+                                 "r"(r[j])
+                                 : "memory");
+                fence_proxy_async_smem();
+                __syncwarp();
+                const int k0 = h * 128 + quarter * 32;
+                if (k0 < p.Kw && c0 < p.K) tma_store_3d_e(&p.tmWs, stg, k0, c0, sp);
+                bulk_commit();
+                ++nstore;
+            }
+        }
+        bulk_wait<0>();
+        __syncwarp();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem_base, tmem_cols);
+    }
+}
+
 }  // namespace tcb
