@@ -280,7 +280,7 @@ def measure(net, args, world, rank, local, nid, precision, batch, dist, with_e2e
             tr.loss()  # D2H of the step's loss, synchronising like a training loop that logs it
         tr.sync()
         res["e2e_ms"] = (time.perf_counter() - t0) * 1e3 / args.steps
-        res["h2d"] = int(x_host.numel() * 4 + y_host.numel() * 4)
+        res["h2d"] = tr.stage_bytes  # as copied: bf16 images when the runtime rounds them on the host
         barrier()
     if with_profile:
         # per-statement profile (one eager step) for the roofline; statements folded into their

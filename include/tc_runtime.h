@@ -78,6 +78,9 @@ TC_API tc_status tc_init_params(tc_ctx* ctx);
  * tc_step / tc_exec_stmt converts it to the device layout.  The host buffers are borrowed
  * until tc_sync() or until the step after the consuming one has been enqueued. */
 TC_API tc_status tc_stage_batch(tc_ctx* ctx, const float* x_host, const int32_t* labels_host);
+/* Bytes one tc_stage_batch moves host -> device (images + labels): the images cross as bf16 when
+ * the context rounds them on the host (bf16 precision, TCB_HOST_BF16 unset or 1), else fp32. */
+TC_API int64_t tc_stage_bytes(const tc_ctx* ctx);
 /* Generate the synthetic batch of `iter` on the device (global samples [n0, n0+batch)). */
 TC_API tc_status tc_stage_synthetic(tc_ctx* ctx, int iter, int n0);
 /* One training iteration over the staged batch (train body; update != 0 applies Updates). */

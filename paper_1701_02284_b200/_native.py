@@ -154,6 +154,8 @@ def _bind_runtime(L: C.CDLL) -> None:
         getattr(L, fn).argtypes = [vp, ci, vp]
     L.tc_init_params.argtypes = [vp]
     L.tc_stage_batch.argtypes = [vp, vp, vp]
+    L.tc_stage_bytes.argtypes = [vp]
+    L.tc_stage_bytes.restype = C.c_int64
     L.tc_stage_synthetic.argtypes = [vp, ci, ci]
     L.tc_step.argtypes = [vp, ci, ci, ci]
     L.tc_exec_stmt.argtypes = [vp, ci, ci, ci]

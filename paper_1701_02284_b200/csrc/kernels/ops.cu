@@ -1383,8 +1383,8 @@ __device__ __forceinline__ bool stage_src(const StageLayout& L, long long i, int
 // Row-tiled staging: block (n, output row) reads the source rows it needs coalesced into
 // shared memory ([c][row][w] fp32, zero outside the image), then writes the output row as
 // 16-byte chunks.  Output row = image row h (NHWC) or space-to-depth row P (rows s*P - pad + i).
-template <typename T>
-__global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x, T* __restrict__ y, StageLayout L,
+template <typename T, typename SRC>
+__global__ void __launch_bounds__(256) k_stage_rows(const SRC* __restrict__ x, T* __restrict__ y, StageLayout L,
                                                     int log2_cs, int log2_s) {
     pdl_wait();
     pdl_trigger();
@@ -1397,8 +1397,8 @@ __global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x,
     for (int ci = 0; ci < C * s; ++ci) {  // tile row (c, i): source row h0 + i of channel c
         const int c = ci >> log2_s, h = h0 + (ci & (s - 1));
         const bool ok = h >= 0 && h < L.H;
-        const float* src = x + ((static_cast<long long>(n) * C + c) * L.H + h) * W;
-        for (int w = threadIdx.x; w < W; w += blockDim.x) tile[ci * W + w] = ok ? __ldcs(src + w) : 0.f;
+        const SRC* src = x + ((static_cast<long long>(n) * C + c) * L.H + h) * W;
+        for (int w = threadIdx.x; w < W; w += blockDim.x) tile[ci * W + w] = ok ? to_f(__ldcs(src + w)) : 0.f;
     }
     __syncthreads();
     const int log2_cc = 2 * log2_s + log2_cs;  // output channels per output pixel = s*s*cs
@@ -1420,8 +1420,8 @@ __global__ void __launch_bounds__(256) k_stage_rows(const float* __restrict__ x,
     }
 }
 
-template <typename T>
-__global__ void k_nchw_to_nhwc(const float* __restrict__ x, T* __restrict__ y, StageLayout L) {
+template <typename T, typename SRC>
+__global__ void k_nchw_to_nhwc(const SRC* __restrict__ x, T* __restrict__ y, StageLayout L) {
     pdl_wait();
     pdl_trigger();
     const long long total = L.elems();
@@ -1429,7 +1429,7 @@ __global__ void k_nchw_to_nhwc(const float* __restrict__ x, T* __restrict__ y, S
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         int n, c, h, w;
         const bool ok = stage_src(L, i, n, c, h, w);
-        y[i] = from_f<T>(ok ? x[((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W + w] : 0.f);
+        y[i] = from_f<T>(ok ? to_f(x[((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W + w]) : 0.f);
     }
 }
 
@@ -2062,19 +2062,19 @@ tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, lo
     return TC_OK;
 }
 
-template <typename T>
-tc_status launch_nchw_to_nhwc(const float* x, T* y, StageLayout L, cudaStream_t st) {
+template <typename T, typename SRC>
+tc_status launch_nchw_to_nhwc(const SRC* x, T* y, StageLayout L, cudaStream_t st) {
     const int s = L.s2d ? L.s2d : 1;
     const size_t smem = static_cast<size_t>(L.C) * s * L.W * sizeof(float);
     const int wout = L.s2d ? L.Ws : L.W;
     auto log2i = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
     const int lcs = log2i(L.cs), ls = log2i(s);
     if (smem <= 48 * 1024 && lcs >= 0 && ls >= 0 && (static_cast<long long>(wout) * s * s * L.cs) % 8 == 0) {
-        TCB_LAUNCH(k_stage_rows<T>, L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
+        TCB_LAUNCH((k_stage_rows<T, SRC>), L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
         TCB_LAUNCH_CHECK();
         return TC_OK;
     }
-    TCB_LAUNCH(k_nchw_to_nhwc<T>, EW_GRID(L.elems()), x, y, L);
+    TCB_LAUNCH((k_nchw_to_nhwc<T, SRC>), EW_GRID(L.elems()), x, y, L);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -2187,7 +2187,8 @@ template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const fl
                                             int, int, float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_apply<bf16>(const bf16*, const bf16*, const float*, bf16*, long long, int, int,
                                            cudaStream_t);
-template tc_status launch_nchw_to_nhwc<bf16>(const float*, bf16*, StageLayout, cudaStream_t);
+template tc_status launch_nchw_to_nhwc<bf16, float>(const float*, bf16*, StageLayout, cudaStream_t);
+template tc_status launch_nchw_to_nhwc<bf16, bf16>(const bf16*, bf16*, StageLayout, cudaStream_t);
 template tc_status launch_synth_batch<bf16>(bf16*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaStream_t);
 template tc_status launch_relu_bwd<float>(const float*, const float*, float*, long long, cudaStream_t);
@@ -2210,7 +2211,7 @@ template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const
                                             int, int, float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_apply<float>(const float*, const float*, const float*, float*, long long, int, int,
                                            cudaStream_t);
-template tc_status launch_nchw_to_nhwc<float>(const float*, float*, StageLayout, cudaStream_t);
+template tc_status launch_nchw_to_nhwc<float, float>(const float*, float*, StageLayout, cudaStream_t);
 template tc_status launch_synth_batch<float>(float*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 
 }  // namespace tcb

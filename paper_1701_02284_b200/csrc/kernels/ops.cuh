@@ -125,8 +125,8 @@ struct StageLayout {
     }
 };
 // Input staging: NCHW fp32 -> the staged layout (bf16, pads zero).
-template <typename T>
-tc_status launch_nchw_to_nhwc(const float* x, T* y, StageLayout L, cudaStream_t st);
+template <typename T, typename SRC>
+tc_status launch_nchw_to_nhwc(const SRC* x, T* y, StageLayout L, cudaStream_t st);
 // Synthetic batch generated on the device (identical law to oracle/tc_philox.h).
 template <typename T>
 tc_status launch_synth_batch(T* x, int32_t* labels, StageLayout L, int classes, uint64_t seed, uint32_t iter,

@@ -24,6 +24,9 @@
 #include <memory>
 #include <string>
 #include <unordered_map>
+#include <thread>
+#include <condition_variable>
+#include <mutex>
 #include <vector>
 
 #include "kernels/common.cuh"
@@ -92,6 +95,66 @@ struct Item {  // arena allocation
 
 using namespace tcb;
 
+// Fork-join pool of host threads for the fp32 -> bf16 rounding of staged host batches.
+struct HostPool {
+    std::vector<std::thread> th;
+    std::mutex m;
+    std::condition_variable cv, done_cv;
+    const float* src = nullptr;
+    uint16_t* dst = nullptr;
+    size_t n = 0;
+    int gen = 0, pending = 0;
+    bool stop = false;
+    explicit HostPool(int workers) {
+        for (int w = 0; w < workers; ++w)
+            th.emplace_back([this, w, workers] {
+                int seen = 0;
+                for (;;) {
+                    std::unique_lock<std::mutex> lk(m);
+                    cv.wait(lk, [&] { return stop || gen != seen; });
+                    if (stop) return;
+                    seen = gen;
+                    const size_t chunk = (n / workers + 63) / 64 * 64;
+                    const size_t a = std::min(n, chunk * w), b = std::min(n, a + chunk);
+                    const float* s0 = src;
+                    uint16_t* d0 = dst;
+                    lk.unlock();
+                    round_bf16(s0 + a, d0 + a, b - a);
+                    lk.lock();
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : th) t.join();
+    }
+    // round-to-nearest-even, as __float2bfloat16_rn for every finite value (NaN / Inf keep their
+    // top half); written so the compiler vectorises it
+    __attribute__((optimize("O3"))) static void round_bf16(const float* __restrict__ s, uint16_t* __restrict__ d, size_t n) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(s);
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t x = u[i];
+            const uint32_t r = ((x & 0x7f800000u) == 0x7f800000u) ? x : x + 0x7fffu + ((x >> 16) & 1u);
+            d[i] = static_cast<uint16_t>(r >> 16);
+        }
+    }
+    void run(const float* s, uint16_t* d, size_t count) {
+        std::unique_lock<std::mutex> lk(m);
+        src = s;
+        dst = d;
+        n = count;
+        pending = static_cast<int>(th.size());
+        ++gen;
+        cv.notify_all();
+        done_cv.wait(lk, [&] { return pending == 0; });
+    }
+};
+
 struct tc_ctx {
     const tc_plan* plan = nullptr;
     tc_ctx_desc desc{};
@@ -150,6 +213,12 @@ struct tc_ctx {
     // device staging slots on copy_st, overlapping the running step; the next step
     // converts the pending slot into the staged input layout on the main stream.
     float* d_stage[2] = {nullptr, nullptr};
+    // bf16 host staging (TCB_HOST_BF16, default on in the bf16 mode): the host batch is rounded to
+    // bf16 by a pool of host threads into pinned memory, so half the bytes cross the host link;
+    // the device staging kernel then reads bf16 (bit-identical staged values)
+    uint16_t* h_stage16[2] = {nullptr, nullptr};
+    bool host_bf16 = false;
+    struct HostPool* pool = nullptr;
     int32_t* d_label_stage[2] = {nullptr, nullptr};
     cudaStream_t copy_st = nullptr;
     cudaEvent_t h2d_done[2] = {nullptr, nullptr}, conv_done[2] = {nullptr, nullptr};
@@ -1712,6 +1781,15 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
         TCB_CUDA_CHECK(cudaEventRecord(c->conv_done[k], c->st));
     }
     TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+    {
+        const char* e = std::getenv("TCB_HOST_BF16");
+        c->host_bf16 = !c->f32 && !(e && e[0] == '0');
+        if (c->host_bf16) {
+            for (int k = 0; k < 2; ++k) TCB_CUDA_CHECK(cudaMallocHost(&c->h_stage16[k], stage_el * 2));
+            const unsigned hw = std::thread::hardware_concurrency();
+            c->pool = new HostPool(static_cast<int>(std::max(1u, std::min(16u, hw ? hw : 4u))));
+        }
+    }
     TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
     TCB_CUDA_CHECK(cudaMemsetAsync(c->d_labels, 0, plan->input_dims[0] * sizeof(int32_t), c->st));
     TCB_CUDA_CHECK(cudaMalloc(&c->d_loss, 4096));  // loss, fp64 block partials, ticket (launch_loss)
@@ -1822,7 +1900,9 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->d_clip);
     cudaFree(c->d_input);
     if (c->copy_st) cudaStreamSynchronize(c->copy_st);
+    delete c->pool;
     for (int k = 0; k < 2; ++k) {
+        if (c->h_stage16[k]) cudaFreeHost(c->h_stage16[k]);
         cudaFree(c->d_stage[k]);
         cudaFree(c->d_label_stage[k]);
         if (c->h2d_done[k]) cudaEventDestroy(c->h2d_done[k]);
@@ -1916,12 +1996,26 @@ tc_status tc_stage_batch(tc_ctx* c, const float* x, const int32_t* labels) {
     // the slot's previous batch must have been converted by its step before it is overwritten
     const int k = c->stage_next;
     TCB_CUDA_CHECK(cudaStreamWaitEvent(c->copy_st, c->conv_done[k], 0));
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], x, el * 4, cudaMemcpyHostToDevice, c->copy_st));
+    if (c->host_bf16) {
+        // the slot's previous host->device copy has finished reading the pinned buffer
+        TCB_CUDA_CHECK(cudaEventSynchronize(c->h2d_done[k]));
+        c->pool->run(x, c->h_stage16[k], el);
+        TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], c->h_stage16[k], el * 2, cudaMemcpyHostToDevice, c->copy_st));
+    } else {
+        TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], x, el * 4, cudaMemcpyHostToDevice, c->copy_st));
+    }
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_label_stage[k], labels, p->input_dims[0] * 4, cudaMemcpyHostToDevice, c->copy_st));
     TCB_CUDA_CHECK(cudaEventRecord(c->h2d_done[k], c->copy_st));
     c->stage_pending = k;
     c->stage_next = k ^ 1;
     return TC_OK;
+}
+
+int64_t tc_stage_bytes(const tc_ctx* c) {
+    if (!c) return 0;
+    const tc_plan* p = c->plan;
+    const int64_t el = p->input_dims[0] * p->input_dims[1] * p->input_dims[2] * p->input_dims[3];
+    return el * (c->host_bf16 ? 2 : 4) + p->input_dims[0] * 4;
 }
 
 // Convert a pending host batch (if any) into the staged input layout on the main stream.
@@ -1932,8 +2026,12 @@ static tc_status consume_staged(tc_ctx* c) {
     TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->h2d_done[k], 0));
     TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_labels, c->d_label_stage[k], c->plan->input_dims[0] * sizeof(int32_t),
                                    cudaMemcpyDeviceToDevice, c->st));
-    tc_status r = c->f32 ? launch_nchw_to_nhwc(c->d_stage[k], static_cast<float*>(c->d_input), c->in_layout, c->st)
-                         : launch_nchw_to_nhwc(c->d_stage[k], static_cast<bf16*>(c->d_input), c->in_layout, c->st);
+    tc_status r = c->f32 ? launch_nchw_to_nhwc(static_cast<const float*>(c->d_stage[k]), static_cast<float*>(c->d_input),
+                                               c->in_layout, c->st)
+                  : c->host_bf16 ? launch_nchw_to_nhwc(reinterpret_cast<const bf16*>(c->d_stage[k]),
+                                                       static_cast<bf16*>(c->d_input), c->in_layout, c->st)
+                                 : launch_nchw_to_nhwc(static_cast<const float*>(c->d_stage[k]),
+                                                       static_cast<bf16*>(c->d_input), c->in_layout, c->st);
     if (r != TC_OK) return r;
     TCB_CUDA_CHECK(cudaEventRecord(c->conv_done[k], c->st));
     return TC_OK;

@@ -75,6 +75,11 @@ class Trainer:
         self._staged = (getattr(self, "_staged", (None,))[-1], (x, y))
         nat.check(nat.lib().tc_stage_batch(self._h, x.ctypes.data, y.ctypes.data))
 
+    @property
+    def stage_bytes(self) -> int:
+        """Bytes one stage_batch moves host -> device (bf16 images when rounded on the host)."""
+        return int(nat.lib().tc_stage_bytes(self._h))
+
     def stage_synthetic(self, it: int, n0: int = 0):
         nat.check(nat.lib().tc_stage_synthetic(self._h, it, n0))
 
