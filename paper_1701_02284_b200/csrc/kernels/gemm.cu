@@ -669,7 +669,7 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
 // ------------------------------------------------------------------ halo-tile filter gradient
 struct WgradHaloPlan {
     int ok = 0;
-    int swap = 0;  // K <= 64: tc_wgrad_halo_swap_kernel (M = two taps x 64 channels, N = K)
+    int swap = 0;  // K <= 64 or 64 < K < 128: tc_wgrad_halo_swap_kernel (M = two taps x 64 channels, N = K)
     int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
     int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0;
     uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
@@ -710,8 +710,8 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
         const char* e = std::getenv("TCB_WGRAD_SWAP_HALO");
         return !(e && e[0] == '0');
     }();
-    pl.swap = swap_on && d->K <= 64;
-    pl.dy_bytes = (pl.swap ? 1 : 2) * BM * 128;
+    pl.swap = swap_on && (d->K <= 64 || (d->K < 128 && d->K % 64 != 0));
+    pl.dy_bytes = (pl.swap && d->K <= 64 ? 1 : 2) * BM * 128;
     pl.halo_bytes = (static_cast<uint32_t>(pl.hh) * pl.wr * 128 + static_cast<uint32_t>(d->S - 1) * 128 + 1023) & ~1023u;
     static const int force_cb = [] {
         const char* e = std::getenv("TCB_WGRAD_CB");
@@ -729,7 +729,7 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
         break;
     }
     if (!pl.stages) return WgradHaloPlan{};
-    const int max_taps = pl.swap ? 16 : 512 / (pl.cb * 64);  // swap: 8 tap pairs x 64 columns
+    const int max_taps = pl.swap ? (d->K <= 64 ? 16 : 8) : 512 / (pl.cb * 64);  // swap: tap pairs x 64 / 128 columns
     pl.ntg = ceil_div(taps, max_taps);
     pl.ntap = ceil_div(taps, pl.ntg);
     pl.ncg = ceil_div(d->cs, 64 * pl.cb);

@@ -217,12 +217,14 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
     }
 }
 
-// Narrow-k form (K <= 64 output channels, e.g. VGG conv1_2): the transposed product
+// Narrow-k form (K <= 64 output channels, e.g. VGG conv1_2, or K < 128 not a multiple of 64,
+// e.g. AlexNet conv1's 96): the transposed product
 //   dW^T[(tap, c)][k] = sum_p x[p + off(tap)][c] * dy[p][k]
 // with M = two taps x 64 channels of the halo (two MN-major atoms of one halo, LBO = the two taps'
-// shift difference), N = 64 (k), so the 128-row MMA is full where the direct form would fill 64 of
-// its rows.  Up to 8 tap pairs (512 TMEM columns) per unit; the epilogue transposes each 32 x 32
-// chunk through shared memory into the [k][tap][c] partials.
+// shift difference), N = K rounded to 16 (one or two 64-channel dy atoms), so the 128-row MMA is
+// full where the direct form would fill K of its rows.  Up to 512 TMEM columns of tap pairs per
+// unit (8 pairs at K <= 64, 4 at K <= 128); the epilogue transposes each 32 x 32 chunk through
+// shared memory into the [k][tap][c] partials.
 __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid_constant__ WgradHaloParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -245,7 +247,8 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
     const int pairs = (taps_here + 1) / 2;
     const int tile0 = sp * p.tiles_per_split;
     const int tile1 = min(p.tiles, tile0 + p.tiles_per_split);
-    const uint32_t ncols = static_cast<uint32_t>((p.ntap + 1) / 2) * 64;
+    const int NK = p.K <= 64 ? 64 : 128;  // accumulator columns per tap pair (k padded to 64 / 128)
+    const uint32_t ncols = static_cast<uint32_t>((p.ntap + 1) / 2) * NK;
     const uint32_t tmem_cols = ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
 
     for (uint32_t i = threadIdx.x; i < (S * p.stage_bytes + 4 * kStagingBytes) / 16; i += blockDim.x)
@@ -274,7 +277,8 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
     if (warp == 0) {
         int s = 0;
         uint32_t ph = 0;
-        const uint32_t tx = static_cast<uint32_t>(p.th * p.wv * 128) + static_cast<uint32_t>(p.hh * p.wr * 128);
+        const int natoms = NK / 64;  // 64-channel dy atoms
+        const uint32_t tx = static_cast<uint32_t>(natoms * p.th * p.wv * 128) + static_cast<uint32_t>(p.hh * p.wr * 128);
         for (int t = tile0; t < tile1; ++t) {
             mbar_wait(&empty[s], ph ^ 1);
             const int img = t / per_img;
@@ -283,7 +287,9 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
             const int y0 = ty * p.th, x0 = (r - ty * p.xt) * p.wv;
             uint8_t* st = smem + s * p.stage_bytes;
             const uint32_t bar = smem_u32(&full[s]);
-            for (int j = 0; j < p.th; ++j) tma_load_4d_e(st + j * p.wr * 128, &p.tmDy, bar, 0, x0, y0 + j, img);
+            for (int a = 0; a < natoms; ++a)
+                for (int j = 0; j < p.th; ++j)
+                    tma_load_4d_e(st + a * (BM * 128) + j * p.wr * 128, &p.tmDy, bar, a * 64, x0, y0 + j, img);
             tma_load_4d_e(st + p.dy_bytes, &p.tmX, bar, cg * 64, x0 - p.pad, y0 - p.pad, img);
             mbar_arrive_expect_tx_e(&full[s], tx);
             if (++s == S) {
@@ -292,9 +298,10 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc = umma_idesc_bf16(BM, 64, 1u, 1u);
+        // N = the real output channels rounded to 16 (MN-major dy atoms of 64 channels, LBO = one atom)
+        const uint32_t idesc = umma_idesc_bf16(BM, static_cast<uint32_t>((p.K + 15) / 16 * 16), 1u, 1u);
         const uint64_t step16 = p.stage_bytes >> 4;
-        const uint64_t b0 = umma_desc_sw128(smem_u32(smem), 0, 1024);  // dy: one 64-wide k atom
+        const uint64_t b0 = umma_desc_sw128(smem_u32(smem), BM * 128, 1024);
         int s = 0;
         uint32_t ph = 0;
         bool first = true;
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
                 // atom 1 (rows 64-127 of M) = tap tb's view: LBO = the shift difference (>= 0;
                 // a lone last tap repeats itself and its rows are not stored)
                 const uint64_t a_pair = umma_desc_sw128(halo + sa * 128, (sb - sa) * 128, 1024);
-                const uint32_t d = tmem_base + q * 64;
+                const uint32_t d = tmem_base + q * NK;
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     umma_bf16_elect<1>(d, a_pair + static_cast<uint64_t>(k * 128), b0 + so + static_cast<uint64_t>(k * 128),
@@ -334,9 +341,9 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
         for (int q = 0; q < pairs; ++q) {
             const int tap = t0 + 2 * q + (quarter >> 1);
             const bool tap_ok = tap < t0 + taps_here && cg * 64 + csub < p.cs;
-            for (int k0 = 0; k0 < 64; k0 += 32) {
+            for (int k0 = 0; k0 < NK; k0 += 32) {
                 uint32_t r[32];
-                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + q * 64 + k0, r);
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + q * NK + k0, r);
                 tmem_ld_wait();
                 if (tile1 <= tile0) {
 #pragma unroll

@@ -184,6 +184,7 @@ HALO_CASES = [
     (1, 256, 30, 30, 256, 3, 1, 1),   # 4 channel blocks
     (2, 64, 20, 20, 32, 5, 1, 2),     # filter gradient with K <= 64: the tap-pair (swapped) form, 5x5
     (2, 128, 14, 14, 48, 3, 1, 1),    # K = 48, two channel blocks
+    (2, 64, 30, 30, 96, 3, 1, 0),     # K = 96: tap pairs against two 64-channel dy atoms (N = 96)
 ]
 
 
