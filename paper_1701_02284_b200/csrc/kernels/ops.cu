@@ -262,21 +262,12 @@ __global__ void k_pool_fwd(const T* __restrict__ x, Act4 xi, T* __restrict__ y, 
 // instructions per channel).  The argmax half-words track the first maximum in row-major
 // window order exactly like k_pool_fwd; the max of bf16 values is one of them, so y is
 // bit-identical to the fp32-compare path.
-template <typename IT, int K, int S>
-__global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
-                                   uint8_t* __restrict__ idx, int pad, int flag_nonpos) {
-    pdl_wait();
-    pdl_trigger();
-    const int cg = xi.cs / 8;
-    const IT total = static_cast<IT>(yo.pixels() * cg);
-    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<IT>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(t % cg);
-        IT p = t / cg;
-        const int ow = static_cast<int>(p % yo.W);
-        p /= yo.W;
-        const int oh = static_cast<int>(p % yo.H);
-        const int n = static_cast<int>(p / yo.H);
+// One output pixel x 8 channels of a fixed-window max pool (see the kernels below).
+template <int K, int S>
+__device__ __forceinline__ void maxpool_fwd_px(const bf16* __restrict__ x, const Act4& xi, bf16* __restrict__ y,
+                                               const Act4& yo, uint8_t* __restrict__ idx, int pad, int flag_nonpos,
+                                               int n, int oh, int ow, int g) {
+    {
         const int ih0 = oh * S - pad, iw0 = ow * S - pad;
         const bf16* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
         uint4 v[K * K];
@@ -326,6 +317,118 @@ __global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __
     }
 }
 
+template <typename IT, int K, int S>
+__global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
+                                   uint8_t* __restrict__ idx, int pad, int flag_nonpos) {
+    pdl_wait();
+    pdl_trigger();
+    const int cg = xi.cs / 8;
+    const IT total = static_cast<IT>(yo.pixels() * cg);
+    for (IT t = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<IT>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(t % cg);
+        IT p = t / cg;
+        const int ow = static_cast<int>(p % yo.W);
+        p /= yo.W;
+        const int oh = static_cast<int>(p % yo.H);
+        const int n = static_cast<int>(p / yo.H);
+        maxpool_fwd_px<K, S>(x, xi, y, yo, idx, pad, flag_nonpos, n, oh, ow, g);
+    }
+}
+
+// Stride-1 K x K max pool over column strips: a thread owns one output column x 8 channels for
+// R consecutive output rows and keeps the horizontal (max, first column) of the last K input rows
+// in a register ring, so each input row is loaded once per strip (K loads per output instead of
+// K*K).  Row-major first-strict-max is preserved: the row pass keeps the first column reaching the
+// row maximum, the column pass the first row whose maximum strictly exceeds the earlier ones, and
+// a window of -inf / NaN keeps the first in-bounds tap exactly as maxpool_fwd_px does.
+template <int K, int R>
+__global__ void k_maxpool_fwd_strip(const bf16* __restrict__ x, Act4 xi, bf16* __restrict__ y, Act4 yo,
+                                    uint8_t* __restrict__ idx, int pad, int flag_nonpos) {
+    pdl_wait();
+    pdl_trigger();
+    const int cg = xi.cs / 8;
+    const int strips = (yo.H + R - 1) / R;
+    long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(yo.N) * strips * yo.W * cg) return;
+    const int g = static_cast<int>(t % cg);
+    t /= cg;
+    const int ow = static_cast<int>(t % yo.W);
+    t /= yo.W;
+    const int oh0 = static_cast<int>(t % strips) * R;
+    const int n = static_cast<int>(t / strips);
+    const int iw0 = ow - pad;
+    const int s0 = iw0 < 0 ? -iw0 : 0;
+    const bf16* img = x + static_cast<long long>(n) * xi.H * xi.W * xi.cs + g * 8;
+    uint32_t hm[K][4], hv[K][4];  // ring slot = input row mod K
+    auto load_row = [&](int ih, uint32_t (&m)[4], uint32_t (&vi)[4]) {
+        uint4 v[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const int iw = iw0 + c;
+            if (ih >= 0 && ih < xi.H && iw >= 0 && iw < xi.W)
+                v[c] = *reinterpret_cast<const uint4*>(img + (static_cast<long long>(ih) * xi.W + iw) * xi.cs);
+            else
+                v[c] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            m[i] = 0xFF80FF80u;
+            vi[i] = static_cast<uint32_t>(s0) * 0x10001u;
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const uint32_t* f = reinterpret_cast<const uint32_t*>(&v[c]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t mk = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&f[i]),
+                                                *reinterpret_cast<const __nv_bfloat162*>(&m[i]));
+                m[i] = (f[i] & mk) | (m[i] & ~mk);
+                vi[i] = ((static_cast<uint32_t>(c) * 0x10001u) & mk) | (vi[i] & ~mk);
+            }
+        }
+    };
+#pragma unroll
+    for (int u = 0; u < K - 1; ++u) load_row(oh0 - pad + u, hm[u], hv[u]);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int oh = oh0 + j;
+        if (oh >= yo.H) break;
+        load_row(oh - pad + K - 1, hm[(j + K - 1) % K], hv[(j + K - 1) % K]);
+        const int r0 = oh - pad < 0 ? pad - oh : 0;
+        uint32_t best[4], bi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            best[i] = 0xFF80FF80u;
+            bi[i] = static_cast<uint32_t>(r0 * K + s0) * 0x10001u;
+        }
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const int sl = (j + u) % K;
+            const uint32_t rowid = static_cast<uint32_t>(u * K) * 0x10001u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t mk = __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&hm[sl][i]),
+                                                *reinterpret_cast<const __nv_bfloat162*>(&best[i]));
+                best[i] = (hm[sl][i] & mk) | (best[i] & ~mk);
+                bi[i] = ((rowid + hv[sl][i]) & mk) | (bi[i] & ~mk);
+            }
+        }
+        const long long o = ((static_cast<long long>(n) * yo.H + oh) * yo.W + ow) * yo.cs + g * 8;
+        *reinterpret_cast<uint4*>(y + o) = make_uint4(best[0], best[1], best[2], best[3]);
+        if (idx) {
+            if (flag_nonpos) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    bi[i] |= ~__hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&best[i]), __float2bfloat162_rn(0.f)) &
+                             0x00800080u;
+            }
+            *reinterpret_cast<uint2*>(idx + o) =
+                make_uint2(__byte_perm(bi[0], bi[1], 0x6420), __byte_perm(bi[2], bi[3], 0x6420));
+        }
+    }
+}
+
 // Fixed-window max-pool backward, patch formulation.  Input rows r = a*S - pad + u (0 <= u < S)
 // of patch a are covered exactly by the windows oh = a - (NW-1) + da, 0 <= da < NW = ceil(K/S),
 // and the window-local tap of (u, da) is u + (NW-1-da)*S: a compile-time constant.  One thread
@@ -334,21 +437,12 @@ __global__ void k_maxpool_fwd_bf16(const bf16* __restrict__ x, Act4 xi, bf16* __
 // k_pool_bwd (bit-identical sums).  An argmax byte with bit 7 set (flagged forward) matches no
 // tap, which is how a folded ReLU backward is applied without reading the ReLU output.
 template <typename T, int K, int S>
-__global__ void k_maxpool_bwd_patch(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
-                                    T* __restrict__ dx, Act4 xi, int pad, const T* __restrict__ relu_y) {
-    pdl_wait();
-    pdl_trigger();
+__device__ __forceinline__ void maxpool_bwd_patch_px(const T* __restrict__ dy, const Act4& yo,
+                                                     const uint8_t* __restrict__ idx, T* __restrict__ dx,
+                                                     const Act4& xi, int pad, const T* __restrict__ relu_y, int n,
+                                                     int pa, int pb, int g) {
     constexpr int NW = (K + S - 1) / S;
-    const int cg = xi.cs / 8;
-    const int PA = (xi.H + pad + S - 1) / S, PB = (xi.W + pad + S - 1) / S;
-    const int total = xi.N * PA * PB * cg;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int g = t % cg;
-        int p = t / cg;
-        const int pb = p % PB;
-        p /= PB;
-        const int pa = p % PA;
-        const int n = p / PA;
+    {
         const long long obase = static_cast<long long>(n) * yo.H * yo.W * yo.cs + g * 8;
         Raw8<T> d[NW * NW];
         uint2 q[NW * NW];
@@ -405,6 +499,100 @@ __global__ void k_maxpool_bwd_patch(const T* __restrict__ dy, Act4 yo, const uin
                 st8(dx + o, acc);
             }
         }
+    }
+}
+
+template <typename T, int K, int S>
+__global__ void k_maxpool_bwd_patch(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
+                                    T* __restrict__ dx, Act4 xi, int pad, const T* __restrict__ relu_y) {
+    pdl_wait();
+    pdl_trigger();
+    const int cg = xi.cs / 8;
+    const int PA = (xi.H + pad + S - 1) / S, PB = (xi.W + pad + S - 1) / S;
+    const int total = xi.N * PA * PB * cg;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int g = t % cg;
+        int p = t / cg;
+        const int pb = p % PB;
+        p /= PB;
+        const int pa = p % PA;
+        const int n = p / PA;
+        maxpool_bwd_patch_px<T, K, S>(dy, yo, idx, dx, xi, pad, relu_y, n, pa, pb, g);
+    }
+}
+
+// Stride-1 backward over column strips: a thread owns one input column x 8 channels for R
+// consecutive input rows; the K covering window rows (K columns each, gradient + argmax bytes)
+// sit in a register ring, so each window is loaded once per strip instead of K*K times.  The
+// per-pixel sums run in the same (oh, ow)-ascending order as maxpool_bwd_patch_px.
+template <typename T, int K, int R>
+__global__ void k_maxpool_bwd_strip(const T* __restrict__ dy, Act4 yo, const uint8_t* __restrict__ idx,
+                                    T* __restrict__ dx, Act4 xi, int pad, const T* __restrict__ relu_y) {
+    pdl_wait();
+    pdl_trigger();
+    const int cg = xi.cs / 8;
+    const int strips = (xi.H + R - 1) / R;
+    long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(xi.N) * strips * xi.W * cg) return;
+    const int g = static_cast<int>(t % cg);
+    t /= cg;
+    const int iw = static_cast<int>(t % xi.W);
+    t /= xi.W;
+    const int ih0 = static_cast<int>(t % strips) * R;
+    const int n = static_cast<int>(t / strips);
+    const long long obase = static_cast<long long>(n) * yo.H * yo.W * yo.cs + g * 8;
+    const int ow0 = iw + pad - (K - 1);
+    Raw8<T> d[K][K];
+    uint2 q[K][K];
+    auto load_row = [&](int oh, Raw8<T> (&dr)[K], uint2 (&qr)[K]) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const int ow = ow0 + c;
+            if (oh >= 0 && oh < yo.H && ow >= 0 && ow < yo.W) {
+                const long long o = obase + (static_cast<long long>(oh) * yo.W + ow) * yo.cs;
+                dr[c] = ld_raw8(dy + o);
+                qr[c] = __ldg(reinterpret_cast<const uint2*>(idx + o));
+            } else {
+                qr[c] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                dr[c] = raw8_zero<T>();
+            }
+        }
+    };
+#pragma unroll
+    for (int da = 0; da < K - 1; ++da) load_row(ih0 + pad - (K - 1) + da, d[da], q[da]);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int ih = ih0 + j;
+        if (ih >= xi.H) break;
+        load_row(ih + pad, d[(j + K - 1) % K], q[(j + K - 1) % K]);
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+        for (int da = 0; da < K; ++da) {
+            const int sl = (j + da) % K;
+            const int tr = K - 1 - da;
+#pragma unroll
+            for (int db = 0; db < K; ++db) {
+                const int tc = K - 1 - db;
+                const uint32_t mm = static_cast<uint32_t>(tr * K + tc) * 0x01010101u;
+                const uint32_t e0 = __vcmpeq4(q[sl][db].x, mm), e1 = __vcmpeq4(q[sl][db].y, mm);
+                float f[8];
+                unpack_raw(d[sl][db], f);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if ((((e < 4 ? e0 : e1) >> (8 * (e & 3))) & 1u) != 0u) acc[e] += f[e];
+            }
+        }
+        const long long o = ((static_cast<long long>(n) * xi.H + ih) * xi.W + iw) * xi.cs + g * 8;
+        if (relu_y) {
+            float m[8];
+            ld8(relu_y + o, m);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!(m[e] > 0.f)) acc[e] = 0.f;
+        }
+        st8(dx + o, acc);
     }
 }
 
@@ -1739,6 +1927,13 @@ tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs,
 long long patch_threads(const Act4& xi, int pad, int S) {
     return static_cast<long long>(xi.N) * ((xi.H + pad + S - 1) / S) * ((xi.W + pad + S - 1) / S) * (xi.cs / 8);
 }
+// Rows per strip of the stride-1 3x3 max-pool kernels: TCB_POOL_STRIP = 4 | 8 (default),
+// 0 = one thread per pixel (A/B)
+static int pool_strip() {
+    const char* e = std::getenv("TCB_POOL_STRIP");
+    const int v = e ? std::atoi(e) : 8;
+    return v == 0 || v == 4 ? v : 8;
+}
 bool fixed_pool_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TCB_FIXED_POOL");
@@ -1765,7 +1960,14 @@ tc_status launch_pool_fwd(const T* x, Act4 xi, T* y, Act4 yo, uint8_t* idx, int 
                 return TC_OK;
             }
             if (k == 3 && stride == 1) {
-                TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 1>), EW_GRID(n), x, xi, y, yo, idx, pad, flag_nonpos);
+                if (const int R = pool_strip()) {
+                    const long long th = static_cast<long long>(yo.N) * ((yo.H + R - 1) / R) * yo.W * (xi.cs / 8);
+                    const int blocks = static_cast<int>((th + 255) / 256);
+                    if (R == 4) TCB_LAUNCH((k_maxpool_fwd_strip<3, 4>), blocks, 256, 0, st, x, xi, y, yo, idx, pad, flag_nonpos);
+                    else TCB_LAUNCH((k_maxpool_fwd_strip<3, 8>), blocks, 256, 0, st, x, xi, y, yo, idx, pad, flag_nonpos);
+                } else {
+                    TCB_LAUNCH((k_maxpool_fwd_bf16<int, 3, 1>), EW_GRID(n), x, xi, y, yo, idx, pad, flag_nonpos);
+                }
                 TCB_LAUNCH_CHECK();
                 return TC_OK;
             }
@@ -1794,7 +1996,15 @@ tc_status launch_pool_bwd(const T* dy, Act4 yo, const uint8_t* idx, T* dx, Act4 
             return TC_OK;
         }
         if (k == 3 && stride == 1) {
-            TCB_LAUNCH((k_maxpool_bwd_patch<T, 3, 1>), EW_GRID(patch_threads(xi, pad, 1)), dy, yo, idx, dx, xi, pad, relu_y);
+            if (const int R = pool_strip()) {
+                const long long th = static_cast<long long>(xi.N) * ((xi.H + R - 1) / R) * xi.W * (xi.cs / 8);
+                const int blocks = static_cast<int>((th + 255) / 256);
+                if (R == 4) TCB_LAUNCH((k_maxpool_bwd_strip<T, 3, 4>), blocks, 256, 0, st, dy, yo, idx, dx, xi, pad, relu_y);
+                else TCB_LAUNCH((k_maxpool_bwd_strip<T, 3, 8>), blocks, 256, 0, st, dy, yo, idx, dx, xi, pad, relu_y);
+            } else {
+                TCB_LAUNCH((k_maxpool_bwd_patch<T, 3, 1>), EW_GRID(patch_threads(xi, pad, 1)), dy, yo, idx, dx, xi, pad,
+                           relu_y);
+            }
             TCB_LAUNCH_CHECK();
             return TC_OK;
         }

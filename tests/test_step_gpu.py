@@ -265,6 +265,31 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,batch", [("googlenet", 2), ("inception", 3)])
+def test_pool_strip_kernels_bit_identical(name, batch, monkeypatch):
+    """The stride-1 3x3 max-pool column-strip kernels (4 or 8 rows per thread, ragged last strip)
+    give bit-identical pooled values, argmax bytes and gradients to the one-pixel-per-thread
+    kernels: two training steps agree in losses, parameters and velocities."""
+    runs = []
+    for rows in ("0", "8", "4"):
+        monkeypatch.setenv("TCB_POOL_STRIP", rows)
+        net = compile_network(name, batch)
+        tr = Trainer(net, use_graph=True, seed=21)
+        tr.init_params()
+        losses = []
+        for it in range(2):
+            tr.stage_synthetic(it, 0)
+            tr.step(it)
+            losses.append(tr.loss())
+        runs.append((losses, [tr.get_param(i) for i in range(len(net.params))],
+                     [tr.velocity(i) for i in range(len(net.params))]))
+        tr.close()
+    for r in runs[1:]:
+        assert r[0] == runs[0][0], (r[0], runs[0][0])
+        for a, b in zip(r[1] + r[2], runs[0][1] + runs[0][2]):
+            np.testing.assert_array_equal(a, b)
+
+
 # ---------------------------------------------------------------- fp32 precision mode
 # TC_PREC_F32: fp32 activations; every contraction runs on the same tcgen05 kernels over a
 # 3-part bf16 split of its operands, 6 cross terms (hi*hi + hi*mid + mid*hi + hi*lo + mid*mid + lo*hi:
