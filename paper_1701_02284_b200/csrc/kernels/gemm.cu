@@ -471,7 +471,7 @@ static double halo_min_util() {
 // fraction of valid output pixels; 0 when none reaches TCB_HALO_MIN_UTIL (default 0.7; AlexNet
 // conv2 26 x 26 under 5 x 5: 75%) -- the im2col path (no junk columns) is kept for small images
 // (12 x 12: 56%, 7 x 7: 38%).
-static HaloGeom halo_geom(int Hout, int Wout, int R, int S, int ms = 1, int wr_only = 0) {
+static HaloGeom halo_geom(int Hout, int Wout, int R, int S, int ms = 1, int wr_only = 0, double min_util = -1) {
     HaloGeom best;
     for (int wr : {16, 32, 64, 128}) {
         if (wr_only && wr != wr_only) continue;
@@ -490,8 +490,19 @@ static HaloGeom halo_geom(int Hout, int Wout, int R, int S, int ms = 1, int wr_o
         g.util = static_cast<double>(Hout) * Wout / (static_cast<double>(g.yt) * g.th * ms * g.xt * wr);
         if (g.util > best.util + 1e-9) best = g;
     }
-    if (!wr_only && best.util < halo_min_util()) best = HaloGeom{};
+    if (!wr_only && best.util < (min_util < 0 ? halo_min_util() : min_util)) best = HaloGeom{};
     return best;
+}
+// Valid-pixel bar of the halo path for a reduction over `red_cs` source channels into `n_out`
+// GEMM columns: TCB_HALO_MIN_UTIL where the 64-channel im2col GEMM is the alternative and the
+// tile is MMA-bound (wide N); TCB_HALO_MIN_UTIL_LO (default 0.3) where the alternative is the
+// 32-channel im2col or gather producer, or N <= 64 (the MMA issue is cheap and junk rows cost little)
+static double halo_util_bar(int red_cs, int n_out) {
+    static const double lo = [] {
+        const char* e = std::getenv("TCB_HALO_MIN_UTIL_LO");
+        return e ? std::atof(e) : 0.3;
+    }();
+    return red_cs % 64 == 0 && n_out > 64 ? halo_min_util() : lo;
 }
 
 template <int BN, int MS>
@@ -599,7 +610,8 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
     p.R = R;
     p.S = S;
     p.flip = flip ? 1 : 0;
-    p.ncb = src_cs / 64;
+    p.ncb = ceil_div(src_cs, 64);
+    p.k_last = ceil_div(src_cs - (p.ncb - 1) * 64, 16);
     p.ldk = src_cs;
     p.wr = g.wr;
     p.th = g.th;
@@ -1108,14 +1120,14 @@ static HaloGeom halo_log(const char* what, const tc_conv_desc* d, HaloGeom g) {
     return g;
 }
 static HaloGeom fprop_halo(const tc_conv_desc* d) {
-    if (!halo_enabled('f') || d->stride != 1 || d->R * d->S == 1 || d->cs % 64 || d->ks % 8)
+    if (!halo_enabled('f') || d->stride != 1 || d->R * d->S == 1 || d->cs % 8 || d->ks % 8)
         return halo_log("fprop (not eligible)", d, HaloGeom{});
-    return halo_log("fprop", d, halo_geom(d->Ho, d->Wo, d->R, d->S));
+    return halo_log("fprop", d, halo_geom(d->Ho, d->Wo, d->R, d->S, 1, 0, halo_util_bar(d->cs, d->ks)));
 }
 static HaloGeom dgrad_halo(const tc_conv_desc* d) {
-    if (!halo_enabled('d') || d->stride != 1 || d->R * d->S == 1 || d->ks % 64 || d->cs % 8)
+    if (!halo_enabled('d') || d->stride != 1 || d->R * d->S == 1 || d->ks % 8 || d->cs % 8)
         return halo_log("dgrad (not eligible)", d, HaloGeom{});
-    return halo_log("dgrad", d, halo_geom(d->H, d->W, d->R, d->S));
+    return halo_log("dgrad", d, halo_geom(d->H, d->W, d->R, d->S, 1, 0, halo_util_bar(d->ks, d->cs)));
 }
 
 static bool narrow_pair(long long M, int N, int K) {

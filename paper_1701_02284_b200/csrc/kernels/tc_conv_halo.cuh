@@ -38,7 +38,8 @@ struct HaloParams {
     int N;            // GEMM columns (output channel stride)
     int b_mn;         // B is MN-major
     int R, S, flip;   // flip: bwd-data (tap (kh, kw) reads halo offset (R-1-kh, S-1-kw))
-    int ncb;          // 64-channel blocks of the source
+    int ncb;          // 64-channel blocks of the source (the last may be partial: TMA zero-fills it)
+    int k_last;       // 16-channel MMA steps of the last block (1..4): the zero-filled rest is not issued
     int ldk;          // B k coordinate of tap t, channel block cb: t * ldk + 64 * cb
     int wr, th, hh;   // halo row stride (pixels), output rows per 128-row subtile, halo rows
     int ms;           // 128-row subtiles per unit (1 or 2; 2 needs BN <= 128)
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
             }
             for (int cb = 0; cb < p.ncb; ++cb, ++ai) {
                 const int as = ai & 1;
+                const int kn = cb == p.ncb - 1 ? p.k_last : BK / 16;
                 mbar_wait(&a_full[as], (ai >> 1) & 1);
                 tc_fence_after();
                 // tap (kh, kw) reads the halo shifted by kh*wr + kw rows (bwd-data: (R-1-kh)*wr +
@@ -223,8 +225,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_conv_halo_kernel(const __gr
                         const uint64_t a_sub = a_tap + static_cast<uint64_t>(sub * (BM * 128 >> 4));
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)
-                            umma_bf16_elect<1>(d_tmem + sub * BN, a_sub + static_cast<uint64_t>(k * 2), b_s + b_koff[k],
-                                               idesc, (!first || k > 0) ? 1u : 0u);
+                            if (k < kn)
+                                umma_bf16_elect<1>(d_tmem + sub * BN, a_sub + static_cast<uint64_t>(k * 2),
+                                                   b_s + b_koff[k], idesc, (!first || k > 0) ? 1u : 0u);
                     }
                     umma_commit_elect<1>(&b_empty[bs]);
                     if (++bs == S) {

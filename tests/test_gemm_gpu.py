@@ -185,6 +185,11 @@ HALO_CASES = [
     (2, 64, 20, 20, 32, 5, 1, 2),     # filter gradient with K <= 64: the tap-pair (swapped) form, 5x5
     (2, 128, 14, 14, 48, 3, 1, 1),    # K = 48, two channel blocks
     (2, 64, 30, 30, 96, 3, 1, 0),     # K = 96: tap pairs against two 64-channel dy atoms (N = 96)
+    (2, 16, 28, 28, 32, 5, 1, 2),     # 16 channels: one zero-filled partial block, one 16-channel MMA step
+    (2, 24, 14, 14, 64, 5, 1, 2),     # 24 channels (two MMA steps), 14 x 14 under 5 x 5: 38% valid rows
+    (2, 48, 7, 7, 128, 5, 1, 2),      # 7 x 7 image, one tile per image
+    (2, 96, 14, 14, 208, 3, 1, 1),    # K = 208: bwd-data reduces over 3 full + 1 partial dy block
+    (2, 384, 7, 7, 192, 3, 1, 1),     # 7 x 7 under 3 x 3 with wide N (6 channel blocks)
 ]
 
 

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--top", type=int, default=60)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--shapes", action="store_true", help="append operand shapes of contractions")
+    ap.add_argument("--only", default="", help="comma-separated op kinds to list (e.g. CONV_FWD,CONV_BWD_DATA)")
     args = ap.parse_args()
     import bench
     from paper_1701_02284_b200 import _native as nat
@@ -40,11 +42,22 @@ def main():
             continue
         f, b = bench.stmt_work(net, s, nat)
         t = float(ms[i])
-        rows.append((t, i, nat.OP_NAMES[s.op], net.stmt_text(i), f / (t * 1e-3) / 1e12 if t > 0 else 0,
+        op = nat.OP_NAMES[s.op]
+        txt = net.stmt_text(i)[:70]
+        if args.shapes and f > 0:
+            dims = lambda r: tuple(net.params[r.index].dims if r.kind == nat.TC_REF_PARAM else net.var_dims(r.index))  # noqa: E731
+            out = tuple(s.dims[k] for k in range(s.rank)) if s.kind == nat.TC_STMT_LET else tuple(net.params[s.param].dims)
+            txt = f"{op[:4]} {dims(s.inp[0])} x {dims(s.inp[1]) if s.nin > 1 else ''} -> {out}"
+        rows.append((t, i, op, txt, f / (t * 1e-3) / 1e12 if t > 0 else 0,
                      b / (t * 1e-3) / 1e9 if t > 0 else 0))
     total = sum(r[0] for r in rows)
     print(f"{args.net} b{args.batch}: total {total:.3f} ms over {len(rows)} statements (eager, per-stmt CUDA events)")
-    for t, i, op, txt, tf, gb in sorted(rows, reverse=True)[: args.top]:
+    by_op = {}
+    for r in rows:
+        by_op[r[2]] = by_op.get(r[2], 0.0) + r[0]
+    print("  by op: " + ", ".join(f"{k} {v:.3f}" for k, v in sorted(by_op.items(), key=lambda kv: -kv[1]) if v > 0.005))
+    only = set(args.only.split(",")) if args.only else None
+    for t, i, op, txt, tf, gb in [r for r in sorted(rows, reverse=True) if only is None or r[2] in only][: args.top]:
         print(f"{t:.3f} ms  #{i:<4d} {op:16s} {txt[:70]:70s} {tf:7.1f} TF/s {gb:8.1f} GB/s")
 
 
