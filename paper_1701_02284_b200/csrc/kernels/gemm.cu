@@ -195,9 +195,11 @@ static bool make_tmap_store(CUtensorMap* map, void* base, bool bf16, uint64_t N,
 
 // ------------------------------------------------------------------ split-K reduce
 // out[m, n] = epilogue( sum_s ws[s][m][n] ), fixed summation order (deterministic).
+// seg_out > 0: the partials hold each segment of seg_out columns padded to seg_in columns
+// (ws row = N / seg_out * seg_in; the halo filter gradient's per-tap channel blocks).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
-                                     int n_bias, int relu, float beta, int trans) {
+                                     int n_bias, int relu, float beta, int trans, int seg_in, int seg_out) {
     pdl_wait();
     pdl_trigger();
     const long long total = static_cast<long long>(M) * N;
@@ -205,8 +207,10 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int m = static_cast<int>(i / N);
         const int n = static_cast<int>(i - static_cast<long long>(m) * N);
+        const long long src =
+            seg_out ? static_cast<long long>(m) * (N / seg_out) * seg_in + (n / seg_out) * seg_in + n % seg_out : i;
         float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += ws[s * split_stride + i];
+        for (int s = 0; s < splits; ++s) acc += ws[s * split_stride + src];
         if (bias && n < n_bias) acc += bias[n];
         if (relu) acc = fmaxf(acc, 0.f);
         if (out_bf16) {
@@ -422,7 +426,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
         TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
                                                      static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
-                                                     relu, beta, p.trans_out);
+                                                     relu, beta, p.trans_out, 0, 0);
         TCB_LAUNCH_CHECK();
     }
     return TC_OK;
@@ -683,7 +687,7 @@ struct WgradHaloPlan {
     int ok = 0;
     int swap = 0;  // K <= 64 or 64 < K < 128: tc_wgrad_halo_swap_kernel (M = two taps x 64 channels, N = K)
     int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
-    int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0;
+    int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0, wcs = 0;
     uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
     size_t ws_bytes = 0;
 };
@@ -702,9 +706,11 @@ static bool wgrad_halo_enabled() {
 // and enough pixel splits to cover the SMs.
 static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
     WgradHaloPlan pl;
-    // channel strides: 32-multiples for x (a partial last 64-channel block is zero-filled by TMA and
-    // its missing 32-column chunks are not stored), any 8-multiple for dy (a partial 64-wide k-atom)
-    if (!wgrad_halo_enabled() || d->stride != 1 || d->R * d->S == 1 || d->cs % 32 || d->ks % 8) return pl;
+    // channel strides: 8-multiples for x (a partial last 64-channel block is zero-filled by TMA, its
+    // missing 32-column chunks are not stored and a partial chunk lands in the workspace's per-tap
+    // padding to a 32-multiple), any 8-multiple for dy (a partial 64-wide k-atom)
+    if (!wgrad_halo_enabled() || d->stride != 1 || d->R * d->S == 1 || d->cs % 8 || d->ks % 8) return pl;
+    pl.wcs = (d->cs + 31) & ~31;  // a partial 32-column chunk is stored into per-tap padding
     const int taps = d->R * d->S;
     double best = 0;
     for (int wr : {16, 32, 64, 128}) {
@@ -716,7 +722,13 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
         best = util;
         pl.wr = wr, pl.th = th, pl.wv = wv, pl.xt = xt, pl.yt = yt, pl.hh = th + d->R - 1;
     }
-    if (best < 0.5) return WgradHaloPlan{};  // (AlexNet conv3-5, 12 x 12: 56%, still ahead of im2col)
+    // (AlexNet conv3-5, 12 x 12: 56%, still ahead of im2col); channel strides that are not
+    // 32-multiples would otherwise take the gather producer: TCB_WGRAD_MIN_UTIL_LO (default 0.3)
+    static const double lo = [] {
+        const char* e = std::getenv("TCB_WGRAD_MIN_UTIL_LO");
+        return e ? std::atof(e) : 0.3;
+    }();
+    if (best < (d->cs % 32 ? lo : 0.5)) return WgradHaloPlan{};
     constexpr int kMaxSmem = 232448, kFixed = 1024 + 256 + 4 * kStagingBytes;
     static const bool swap_on = [] {
         const char* e = std::getenv("TCB_WGRAD_SWAP_HALO");
@@ -751,7 +763,7 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
     const int want = std::max(1, num_sms() / base);
     pl.tiles_per_split = ceil_div(pl.tiles, std::min(want, pl.tiles));
     pl.splits = ceil_div(pl.tiles, pl.tiles_per_split);
-    pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * taps * d->cs * sizeof(float);
+    pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * taps * pl.wcs * sizeof(float);
     pl.ok = 1;
     return pl;
 }
@@ -769,14 +781,14 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     p.wr = pl.wr, p.th = pl.th, p.hh = pl.hh, p.wv = pl.wv, p.xt = pl.xt, p.yt = pl.yt, p.nimg = d->N;
     p.Ho = d->Ho;
     p.Wo = d->Wo;
-    p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.cs = d->cs, p.mt = pl.mt;
+    p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.cs = d->cs, p.wcs = pl.wcs, p.mt = pl.mt;
     p.splits = pl.splits, p.tiles = pl.tiles, p.tiles_per_split = pl.tiles_per_split;
     p.dy_bytes = pl.dy_bytes, p.halo_bytes = pl.halo_bytes, p.stage_bytes = pl.stage_bytes, p.stages = pl.stages;
     std::string err;
     if (!make_tmap_halo_src(&p.tmX, x, d->N, d->H, d->W, d->cs, pl.wr, pl.hh, &err)) return fail(TC_INVALID_ARG, err);
     if (!make_tmap_halo_src(&p.tmDy, dy, d->N, d->Ho, d->Wo, d->ks, pl.wv, 1, &err)) return fail(TC_INVALID_ARG, err);
-    const uint64_t ncol = static_cast<uint64_t>(d->R) * d->S * d->cs;
-    if (!make_tmap_store(&p.tmWs, ws, false, ncol, d->K, pl.splits, ncol, &err)) return fail(TC_INVALID_ARG, err);
+    const uint64_t ncol = static_cast<uint64_t>(d->R) * d->S * d->cs, wcol = static_cast<uint64_t>(d->R) * d->S * pl.wcs;
+    if (!make_tmap_store(&p.tmWs, ws, false, wcol, d->K, pl.splits, wcol, &err)) return fail(TC_INVALID_ARG, err);
     const int smem = 1024 + pl.stages * static_cast<int>(pl.stage_bytes) + 4 * kStagingBytes + 256;
     auto kern = pl.swap ? tc_wgrad_halo_swap_kernel : pl.cb == 2 ? tc_wgrad_halo_kernel<2> : tc_wgrad_halo_kernel<1>;
     static std::atomic<uint64_t> attr_done{0};
@@ -806,9 +818,10 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     TCB_LAUNCH_CHECK();
     const long long total = static_cast<long long>(d->K) * static_cast<long long>(ncol);
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
+    const bool padded = pl.wcs != d->cs;
     TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K,
-               static_cast<int>(ncol), total, static_cast<void*>(dw), ldw, 0, static_cast<const float*>(nullptr), 0, 0,
-               0.f, 0);
+               static_cast<int>(ncol), static_cast<long long>(d->K) * static_cast<long long>(wcol), static_cast<void*>(dw),
+               ldw, 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0, padded ? pl.wcs : 0, padded ? d->cs : 0);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -964,7 +977,8 @@ static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc
     const long long total = static_cast<long long>(d->K) * p.Kw;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
     TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K, p.Kw, total,
-               static_cast<void*>(dw), static_cast<long long>(p.Kw), 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0);
+               static_cast<void*>(dw), static_cast<long long>(p.Kw), 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0,
+               0, 0);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }

@@ -14,7 +14,7 @@
 //   unit  = (128-channel block of k (M), tap group (nt taps), channel group (CB x 64 c), pixel split)
 //   TMEM  = nt accumulators of CB * 64 fp32 columns, live for the whole pixel range of the unit
 //   MMA   = per tile, per tap, 8 k-steps of 16 pixels: M = 128 (k), N = CB * 64 (c), MN-major A / B
-//   out   = fp32 partials [split][K][R*S*cs] (TMA store), summed in fixed order by splitk_reduce
+//   out   = fp32 partials [split][K][R*S][wcs] (TMA store), summed in fixed order by splitk_reduce
 //
 // Warp roles (256 threads): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-7 epilogue.
 #pragma once
@@ -29,14 +29,15 @@ namespace tcb {
 struct WgradHaloParams {
     CUtensorMap tmX;   // 4-D tiled {cs, W, H, N} over x, box {64, wr, hh, 1}, SW128
     CUtensorMap tmDy;  // 4-D tiled {ks, Wo, Ho, N} over dy, box {64, wv, 1, 1}, SW128
-    CUtensorMap tmWs;  // 3-D store {R*S*cs, K, splits} fp32, box {32, 32, 1}, SW128
+    CUtensorMap tmWs;  // 3-D store {R*S*wcs, K, splits} fp32, box {32, 32, 1}, SW128
     int K;             // output channels (GEMM M)
     int R, S, pad;
     int wr, th, hh, wv, xt, yt, nimg;
     int Ho, Wo;
     int ntap, ntg;     // taps per group (accumulators), tap groups
     int ncg;           // channel groups of CB x 64 channels
-    int cs;            // x channel stride (D column of tap t, channel c: t * cs + c)
+    int cs;            // x channel stride
+    int wcs;           // workspace columns per tap (cs rounded up to 32: D column of tap t, channel c: t * wcs + c)
     int mt;            // 128-row blocks of K
     int splits, tiles, tiles_per_split;
     uint32_t dy_bytes;    // dy tile: 2 k-atoms x 128 rows x 128 B
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
                         st_shared_v4(row_addr + sw128_off(lane, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    const int col = (t0 + j) * p.cs + cg * CB * 64 + c0;
+                    const int col = (t0 + j) * p.wcs + cg * CB * 64 + c0;
                     if (m0 < p.K && cg * CB * 64 + c0 < p.cs) tma_store_3d_e(&p.tmWs, stg, col, m0, sp);
                     bulk_commit();
                     ++nstore;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
                     if (nstore > 0) bulk_wait_read<0>();
                     __syncwarp();
                     if (m0 < p.K && cg * CB * 64 + c0 < p.cs)
-                        tma_store_3d_e(&p.tmWs, stg, (t0 + j) * p.cs + cg * CB * 64 + c0, m0, sp);
+                        tma_store_3d_e(&p.tmWs, stg, (t0 + j) * p.wcs + cg * CB * 64 + c0, m0, sp);
                     bulk_commit();
                     ++nstore;
                 }
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
                                  : "memory");
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (tap_ok && k0 < p.K) tma_store_3d_e(&p.tmWs, stg, tap * p.cs + cg * 64 + csub, k0, sp);
+                if (tap_ok && k0 < p.K) tma_store_3d_e(&p.tmWs, stg, tap * p.wcs + cg * 64 + csub, k0, sp);
                 bulk_commit();
                 ++nstore;
             }

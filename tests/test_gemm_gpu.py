@@ -190,6 +190,8 @@ HALO_CASES = [
     (2, 48, 7, 7, 128, 5, 1, 2),      # 7 x 7 image, one tile per image
     (2, 96, 14, 14, 208, 3, 1, 1),    # K = 208: bwd-data reduces over 3 full + 1 partial dy block
     (2, 384, 7, 7, 192, 3, 1, 1),     # 7 x 7 under 3 x 3 with wide N (6 channel blocks)
+    (2, 144, 14, 14, 160, 3, 1, 1),   # 144 channels: a 16-column partial chunk in the padded workspace, K = 160
+    (2, 112, 14, 14, 224, 3, 1, 1),   # 112 channels (two blocks, the second 48 wide), K = 224
 ]
 
 
