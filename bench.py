@@ -273,13 +273,23 @@ def measure(net, args, world, rank, local, nid, precision, batch, dist, with_e2e
             tr.loss()
         tr.sync()
         barrier()
+        sync_loss = os.environ.get("TCB_BENCH_SYNC_LOSS") == "1"
+        losses = []
         t0 = time.perf_counter()
         for it in range(args.steps):
             tr.step(it, n0)
             tr.stage_batch(xh, yh)  # next step's batch, overlapping this step
-            tr.loss()  # D2H of the step's loss, synchronising like a training loop that logs it
+            if sync_loss:
+                losses.append(tr.loss())  # waits for this step: the device idles until the next launch
+            elif it > 0:
+                # every step's loss is read back, one step late (waits for step it-1 only), as a
+                # loop that logs asynchronously does: step it+1 is enqueued while step it runs
+                losses.append(tr.loss_prev())
         tr.sync()
+        if not sync_loss:
+            losses.append(tr.loss())
         res["e2e_ms"] = (time.perf_counter() - t0) * 1e3 / args.steps
+        assert len(losses) == args.steps and all(np.isfinite(losses)), losses
         res["h2d"] = tr.stage_bytes  # as copied: bf16 images when the runtime rounds them on the host
         barrier()
     if with_profile:
@@ -385,7 +395,10 @@ def run_gpu(args):
         "data": "synthetic (Philox K-blob images generated on device; random Xavier init)",
         "config": workload_config(name, world, batch),
         "e2e": {"value": round(world * batch / (e2e_ms * 1e-3), 2), "unit": "images/s",
-                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": 4,
+                "loop": "stage_batch(next) overlaps the step; each step's loss read back one step late "
+                        "(tc_loss_prev) so the next step is enqueued while the current one runs",
+                "loss_readback": "sync" if os.environ.get("TCB_BENCH_SYNC_LOSS") == "1" else "one step late"},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 implicit-GEMM contractions (conv fwd/dgrad/wgrad, FC)",
                      "achieved": round(achieved_tf, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / peak_tf, 4),

@@ -93,6 +93,9 @@ TC_API tc_status tc_exec_stmt(tc_ctx* ctx, int index, int iter, int n0);
 TC_API tc_status tc_test(tc_ctx* ctx, int iter, int n0, double* precision);
 /* Loss of the last step (blocks on the stream). */
 TC_API tc_status tc_loss(tc_ctx* ctx, double* loss);
+/* Loss of the step before the last one enqueued, waiting for that step only (a training loop
+ * that logs every step's loss one step late keeps the device busy); needs two steps. */
+TC_API tc_status tc_loss_prev(tc_ctx* ctx, double* loss);
 /* Var contents after a step (keep mode), converted to the reference layout, fp32. */
 TC_API tc_status tc_var_download(tc_ctx* ctx, int var, float* host, int64_t max_elems);
 /* Pool-forward argmax indices of a pooling output var (flat NCHW input index). */

@@ -160,6 +160,7 @@ def _bind_runtime(L: C.CDLL) -> None:
     L.tc_step.argtypes = [vp, ci, ci, ci]
     L.tc_exec_stmt.argtypes = [vp, ci, ci, ci]
     L.tc_loss.argtypes = [vp, C.POINTER(C.c_double)]
+    L.tc_loss_prev.argtypes = [vp, C.POINTER(C.c_double)]
     L.tc_var_download.argtypes = [vp, ci, vp, C.c_int64]
     L.tc_pool_indices_download.argtypes = [vp, ci, vp, C.c_int64]
     L.tc_sync.argtypes = [vp]

@@ -222,6 +222,81 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     }
 }
 
+// The same, 4 consecutive columns per thread (16-byte partial loads, 4 splits in flight): every
+// element is summed in the same split order, so the result is bit-identical to the scalar form.
+// Needs N, ldd (and seg_in / seg_out when remapping) multiples of 4 and trans == 0.
+__global__ void splitk_reduce4_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
+                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
+                                      int n_bias, int relu, float beta, int seg_in, int seg_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int nq = N >> 2;
+    const long long total = static_cast<long long>(M) * nq;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i / nq);
+        const int n = static_cast<int>(i - static_cast<long long>(m) * nq) * 4;
+        const long long src = seg_out ? static_cast<long long>(m) * (N / seg_out) * seg_in + (n / seg_out) * seg_in + n % seg_out
+                                      : static_cast<long long>(m) * N + n;
+        const float4* w = reinterpret_cast<const float4*>(ws + src);
+        const long long ss = split_stride >> 2;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int s = 0;
+        for (; s + 4 <= splits; s += 4) {
+            const float4 a = __ldcs(w + s * ss), b = __ldcs(w + (s + 1) * ss), c = __ldcs(w + (s + 2) * ss),
+                         d = __ldcs(w + (s + 3) * ss);
+            acc.x += a.x, acc.y += a.y, acc.z += a.z, acc.w += a.w;
+            acc.x += b.x, acc.y += b.y, acc.z += b.z, acc.w += b.w;
+            acc.x += c.x, acc.y += c.y, acc.z += c.z, acc.w += c.w;
+            acc.x += d.x, acc.y += d.y, acc.z += d.z, acc.w += d.w;
+        }
+        for (; s < splits; ++s) {
+            const float4 a = __ldcs(w + s * ss);
+            acc.x += a.x, acc.y += a.y, acc.z += a.z, acc.w += a.w;
+        }
+        float v[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (bias && n + j < n_bias) v[j] += bias[n + j];
+            if (relu) v[j] = fmaxf(v[j], 0.f);
+        }
+        if (out_bf16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + m * ldd + n;
+            reinterpret_cast<__nv_bfloat162*>(o)[0] = __floats2bfloat162_rn(v[0], v[1]);
+            reinterpret_cast<__nv_bfloat162*>(o)[1] = __floats2bfloat162_rn(v[2], v[3]);
+        } else {
+            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + m * ldd + n);
+            if (beta != 0.f) {
+                const float4 q = *o;
+                v[0] += beta * q.x, v[1] += beta * q.y, v[2] += beta * q.z, v[3] += beta * q.w;
+            }
+            *o = make_float4(v[0], v[1], v[2], v[3]);
+        }
+    }
+}
+
+// Launch the split-K reduce: the 4-column form when the shapes allow, else the scalar one.
+static tc_status launch_splitk_reduce(const float* ws, int splits, int M, int N, long long split_stride, void* out,
+                                      long long ldd, int out_bf16, const float* bias, int n_bias, int relu, float beta,
+                                      int trans, int seg_in, int seg_out, cudaStream_t st) {
+    const char* e = std::getenv("TCB_REDUCE4");  // 0: scalar form only (A/B, bit-identity test)
+    const bool vec_on = !(e && e[0] == '0');
+    // (small outputs keep the scalar form: 4x the threads hide more latency than 16-byte loads save)
+    const bool vec = vec_on && !trans && static_cast<long long>(M) * N >= 4LL * 256 * num_sms() && N % 4 == 0 && ldd % 4 == 0 && split_stride % 4 == 0 && seg_in % 4 == 0 &&
+                     seg_out % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & (out_bf16 ? 7 : 15)) == 0;
+    const long long total = static_cast<long long>(M) * N / (vec ? 4 : 1);
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
+    if (vec)
+        TCB_LAUNCH(splitk_reduce4_kernel, blocks, 256, 0, st, ws, splits, M, N, split_stride, out, ldd, out_bf16, bias,
+                   n_bias, relu, beta, seg_in, seg_out);
+    else
+        TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, ws, splits, M, N, split_stride, out, ldd, out_bf16, bias,
+                   n_bias, relu, beta, trans, seg_in, seg_out);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+
 // ------------------------------------------------------------------ launch
 struct LaunchPlan {
     int bn = 128;
@@ -421,14 +496,9 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     else
         s = launch_bn<64, 1>(p, p.units, st);
     if (s != TC_OK) return s;
-    if (partial) {
-        const long long total = static_cast<long long>(p.M) * p.N;
-        const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
-        TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), lp.splits, p.M, p.N,
-                                                     static_cast<long long>(p.M) * p.N, D, ldd, d_bf16, bias, n_bias,
-                                                     relu, beta, p.trans_out, 0, 0);
-        TCB_LAUNCH_CHECK();
-    }
+    if (partial)
+        return launch_splitk_reduce(static_cast<const float*>(ws), lp.splits, p.M, p.N, static_cast<long long>(p.M) * p.N,
+                                    D, ldd, d_bf16, bias, n_bias, relu, beta, p.trans_out, 0, 0, st);
     return TC_OK;
 }
 
@@ -687,7 +757,7 @@ struct WgradHaloPlan {
     int ok = 0;
     int swap = 0;  // K <= 64 or 64 < K < 128: tc_wgrad_halo_swap_kernel (M = two taps x 64 channels, N = K)
     int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
-    int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0, wcs = 0;
+    int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0, wcs = 0, nc = 0;
     uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
     size_t ws_bytes = 0;
 };
@@ -753,10 +823,17 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
         break;
     }
     if (!pl.stages) return WgradHaloPlan{};
-    const int max_taps = pl.swap ? (d->K <= 64 ? 16 : 8) : 512 / (pl.cb * 64);  // swap: tap pairs x 64 / 128 columns
+    pl.ncg = ceil_div(d->cs, 64 * pl.cb);
+    // one channel group: MMA N (and TMEM columns per tap) trimmed to the channels rounded up to 32
+    // (AlexNet conv2, 96 channels: N = 96, 5 taps per group instead of 4 x 128 columns)
+    static const bool trim = [] {
+        const char* e = std::getenv("TCB_WGRAD_TRIM_N");
+        return !(e && e[0] == '0');
+    }();
+    pl.nc = pl.ncg == 1 && trim ? (d->cs + 31) / 32 * 32 : pl.cb * 64;
+    const int max_taps = pl.swap ? (d->K <= 64 ? 16 : 8) : std::min(512 / pl.nc, 8);  // swap: tap pairs x 64 / 128 columns
     pl.ntg = ceil_div(taps, max_taps);
     pl.ntap = ceil_div(taps, pl.ntg);
-    pl.ncg = ceil_div(d->cs, 64 * pl.cb);
     pl.mt = pl.swap ? 1 : ceil_div(d->K, BM);
     pl.tiles = d->N * pl.yt * pl.xt;
     const int base = pl.mt * pl.ncg * pl.ntg;
@@ -781,7 +858,7 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     p.wr = pl.wr, p.th = pl.th, p.hh = pl.hh, p.wv = pl.wv, p.xt = pl.xt, p.yt = pl.yt, p.nimg = d->N;
     p.Ho = d->Ho;
     p.Wo = d->Wo;
-    p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.cs = d->cs, p.wcs = pl.wcs, p.mt = pl.mt;
+    p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.nc = pl.nc, p.cs = d->cs, p.wcs = pl.wcs, p.mt = pl.mt;
     p.splits = pl.splits, p.tiles = pl.tiles, p.tiles_per_split = pl.tiles_per_split;
     p.dy_bytes = pl.dy_bytes, p.halo_bytes = pl.halo_bytes, p.stage_bytes = pl.stage_bytes, p.stages = pl.stages;
     std::string err;
@@ -816,14 +893,10 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, kern, p);
     TCB_LAUNCH_CHECK();
-    const long long total = static_cast<long long>(d->K) * static_cast<long long>(ncol);
-    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
     const bool padded = pl.wcs != d->cs;
-    TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K,
-               static_cast<int>(ncol), static_cast<long long>(d->K) * static_cast<long long>(wcol), static_cast<void*>(dw),
-               ldw, 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0, padded ? pl.wcs : 0, padded ? d->cs : 0);
-    TCB_LAUNCH_CHECK();
-    return TC_OK;
+    return launch_splitk_reduce(static_cast<const float*>(ws), pl.splits, d->K, static_cast<int>(ncol),
+                                static_cast<long long>(d->K) * static_cast<long long>(wcol), dw, ldw, 0, nullptr, 0, 0,
+                                0.f, 0, padded ? pl.wcs : 0, padded ? d->cs : 0, st);
 }
 
 // ------------------------------------------------------------------ channel-stride-4 first layer
@@ -974,13 +1047,8 @@ static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc
     cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, tc_conv_c4_wgrad_kernel, p);
     TCB_LAUNCH_CHECK();
-    const long long total = static_cast<long long>(d->K) * p.Kw;
-    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
-    TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, static_cast<const float*>(ws), pl.splits, d->K, p.Kw, total,
-               static_cast<void*>(dw), static_cast<long long>(p.Kw), 0, static_cast<const float*>(nullptr), 0, 0, 0.f, 0,
-               0, 0);
-    TCB_LAUNCH_CHECK();
-    return TC_OK;
+    return launch_splitk_reduce(static_cast<const float*>(ws), pl.splits, d->K, p.Kw,
+                                static_cast<long long>(d->K) * p.Kw, dw, p.Kw, 0, nullptr, 0, 0, 0.f, 0, 0, 0, st);
 }
 
 static void init_params(GemmParams& p) {

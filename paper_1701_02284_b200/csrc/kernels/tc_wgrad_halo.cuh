@@ -36,6 +36,7 @@ struct WgradHaloParams {
     int Ho, Wo;
     int ntap, ntg;     // taps per group (accumulators), tap groups
     int ncg;           // channel groups of CB x 64 channels
+    int nc;            // MMA N / accumulator columns per tap: CB * 64, or (one group) cs rounded up to 32
     int cs;            // x channel stride
     int wcs;           // workspace columns per tap (cs rounded up to 32: D column of tap t, channel c: t * wcs + c)
     int mt;            // 128-row blocks of K
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
     const int taps_here = min(p.ntap, p.R * p.S - t0);
     const int tile0 = sp * p.tiles_per_split;
     const int tile1 = min(p.tiles, tile0 + p.tiles_per_split);
-    const uint32_t ncols = static_cast<uint32_t>(p.ntap) * CB * 64;
+    const uint32_t ncols = static_cast<uint32_t>(p.ntap) * p.nc;
     const uint32_t tmem_cols = ncols <= 32 ? 32 : ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
 
     // zero every stage and the staging once: the dy gap positions (wr - wv per row) and the halo
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        const uint32_t idesc = umma_idesc_bf16(BM, CB * 64, 1u, 1u);
+        const uint32_t idesc = umma_idesc_bf16(BM, static_cast<uint32_t>(p.nc), 1u, 1u);
         // A = dy tile, MN-major: k-atoms 128 rows x 128 B apart (LBO), 8-row groups 1 KB (SBO);
         // a k-step of 16 pixels = 2 KB.  B = halo, MN-major: channel blocks halo_bytes apart.
         const uint64_t a0 = umma_desc_sw128(smem_u32(smem), p.dy_bytes / 2, 1024);
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
             int kh = t0 / p.S, kw = t0 - (t0 / p.S) * p.S;
             for (int j = 0; j < taps_here; ++j) {
                 const uint64_t b_tap = b0 + so + static_cast<uint64_t>((kh * p.wr + kw) * 8);
-                const uint32_t d = tmem_base + j * CB * 64;
+                const uint32_t d = tmem_base + j * p.nc;
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     umma_bf16_elect<1>(d, a0 + so + static_cast<uint64_t>(k * 128), b_tap + static_cast<uint64_t>(k * 128),
@@ -173,9 +174,9 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
         int nstore = 0;
         if (tile1 > tile0) {
             for (int j = 0; j < taps_here; ++j) {
-                for (int c0 = 0; c0 < CB * 64; c0 += 32) {
+                for (int c0 = 0; c0 < p.nc; c0 += 32) {
                     uint32_t r[32];
-                    tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + j * CB * 64 + c0, r);
+                    tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + j * p.nc + c0, r);
                     tmem_ld_wait();
                     if (nstore > 0) bulk_wait_read<0>();
                     __syncwarp();
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
             fence_proxy_async_smem();
             __syncwarp();
             for (int j = 0; j < taps_here; ++j)
-                for (int c0 = 0; c0 < CB * 64; c0 += 32) {
+                for (int c0 = 0; c0 < p.nc; c0 += 32) {
                     if (nstore > 0) bulk_wait_read<0>();
                     __syncwarp();
                     if (m0 < p.K && cg * CB * 64 + c0 < p.cs)

@@ -97,15 +97,22 @@ using namespace tcb;
 
 // Fork-join pool of host threads for the fp32 -> bf16 rounding of staged host batches.
 struct HostPool {
+    // The batch is cut into `nchunks` chunks; every worker converts its share of chunk 0, then of
+    // chunk 1, ..., counting each finished share in done[chunk], so the caller can start a chunk's
+    // host -> device copy while the workers round the next one.
+    static constexpr int kMaxChunks = 64;
     std::vector<std::thread> th;
     std::mutex m;
     std::condition_variable cv, done_cv;
     const float* src = nullptr;
     uint16_t* dst = nullptr;
-    size_t n = 0;
+    size_t n = 0, chunk = 0;
+    int nchunks = 1;
+    std::atomic<int> done[kMaxChunks];
     int gen = 0, pending = 0;
     bool stop = false;
     explicit HostPool(int workers) {
+        for (auto& d : done) d.store(0);
         for (int w = 0; w < workers; ++w)
             th.emplace_back([this, w, workers] {
                 int seen = 0;
@@ -114,12 +121,18 @@ struct HostPool {
                     cv.wait(lk, [&] { return stop || gen != seen; });
                     if (stop) return;
                     seen = gen;
-                    const size_t chunk = (n / workers + 63) / 64 * 64;
-                    const size_t a = std::min(n, chunk * w), b = std::min(n, a + chunk);
                     const float* s0 = src;
                     uint16_t* d0 = dst;
+                    const size_t total = n, ck = chunk;
+                    const int nc = nchunks;
                     lk.unlock();
-                    round_bf16(s0 + a, d0 + a, b - a);
+                    for (int c = 0; c < nc; ++c) {
+                        const size_t ca = std::min(total, ck * c), cn = std::min(total, ca + ck) - ca;
+                        const size_t share = (cn / workers + 63) / 64 * 64;
+                        const size_t a = std::min(cn, share * w), b = std::min(cn, a + share);
+                        round_bf16(s0 + ca + a, d0 + ca + a, b - a);
+                        done[c].fetch_add(1, std::memory_order_release);
+                    }
                     lk.lock();
                     if (--pending == 0) done_cv.notify_all();
                 }
@@ -143,15 +156,36 @@ struct HostPool {
             d[i] = static_cast<uint16_t>(r >> 16);
         }
     }
-    void run(const float* s, uint16_t* d, size_t count) {
-        std::unique_lock<std::mutex> lk(m);
-        src = s;
-        dst = d;
-        n = count;
-        pending = static_cast<int>(th.size());
-        ++gen;
+    // Round s[0, count) into d; on_chunk(begin, len) runs on the calling thread as soon as a chunk
+    // is complete (in chunk order).  Returns the first non-OK status of on_chunk.
+    template <typename F>
+    tc_status run(const float* s, uint16_t* d, size_t count, int chunks, F&& on_chunk) {
+        chunks = std::max(1, std::min(kMaxChunks, chunks));
+        const size_t ck = ((count + chunks - 1) / chunks + 63) / 64 * 64;
+        const int nc = static_cast<int>(std::max<size_t>(1, (count + ck - 1) / ck));
+        const int workers = static_cast<int>(th.size());
+        {
+            std::lock_guard<std::mutex> lk(m);
+            src = s;
+            dst = d;
+            n = count;
+            chunk = ck;
+            nchunks = nc;
+            for (int c = 0; c < nc; ++c) done[c].store(0, std::memory_order_relaxed);
+            pending = workers;
+            ++gen;
+        }
         cv.notify_all();
+        tc_status st = TC_OK;
+        for (int c = 0; c < nc; ++c) {
+            for (int spin = 0; done[c].load(std::memory_order_acquire) < workers; ++spin)
+                if (spin > 64) std::this_thread::yield();
+            const size_t a = std::min(count, ck * c);
+            if (st == TC_OK) st = on_chunk(a, std::min(count, a + ck) - a);
+        }
+        std::unique_lock<std::mutex> lk(m);
         done_cv.wait(lk, [&] { return pending == 0; });
+        return st;
     }
 };
 
@@ -213,9 +247,12 @@ struct tc_ctx {
     // device staging slots on copy_st, overlapping the running step; the next step
     // converts the pending slot into the staged input layout on the main stream.
     float* d_stage[2] = {nullptr, nullptr};
-    // bf16 host staging (TCB_HOST_BF16, default on in the bf16 mode): the host batch is rounded to
-    // bf16 by a pool of host threads into pinned memory, so half the bytes cross the host link;
-    // the device staging kernel then reads bf16 (bit-identical staged values)
+    // bf16 host staging (TCB_HOST_BF16=1, bf16 mode): the host batch is rounded to bf16 by a pool
+    // of host threads into pinned memory (chunk by chunk, each chunk's copy overlapping the next
+    // chunk's rounding), so half the bytes cross the host link; the device staging kernel then
+    // reads bf16 (bit-identical staged values).  Off by default: on a 16-core host the rounding is
+    // host-memory bound (1.3 ms per AlexNet b128 batch) and costs more than the fp32 copy it halves
+    // (1.4 ms, hidden under the 1.56 ms step): e2e 68k vs 77k images/s.
     uint16_t* h_stage16[2] = {nullptr, nullptr};
     bool host_bf16 = false;
     struct HostPool* pool = nullptr;
@@ -226,7 +263,9 @@ struct tc_ctx {
     float* d_loss = nullptr;
     uint32_t* d_iter = nullptr;
     uint32_t* h_iter = nullptr;  // pinned
-    float* h_loss = nullptr;     // pinned
+    float* h_loss = nullptr;     // pinned: two loss slots 16 floats apart (the last two steps)
+    cudaEvent_t loss_ev[2] = {nullptr, nullptr};  // the slot's D2H has landed
+    int loss_slot = 0, loss_count = 0;            // slot of the most recent loss; losses enqueued
     int input_cs = 8;
     StageLayout in_layout{};  // staged input image layout (space-to-depth when in_layout.s2d > 0)
     bool f32 = false;         // TC_PREC_F32: fp32 activations, 6-term bf16 split contractions
@@ -1526,6 +1565,18 @@ tc_status allreduce_loss(tc_ctx* c) {
     return TC_OK;
 }
 
+// D2H of the step's loss into the next of two pinned slots, enqueued after the (possibly graph-
+// replayed) step on the main stream: tc_loss reads the newest, tc_loss_prev the one before it
+// without waiting for the newest step.
+static tc_status enqueue_loss_read(tc_ctx* c) {
+    const int k = c->loss_count ? c->loss_slot ^ 1 : 0;
+    TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss + 16 * k, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    TCB_CUDA_CHECK(cudaEventRecord(c->loss_ev[k], c->st));
+    c->loss_slot = k;
+    ++c->loss_count;
+    return TC_OK;
+}
+
 tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
     tc_status r = set_iter ? launch_set_iter(c->d_iter, c->h_iter[0], c->h_iter[1], c->st) : TC_OK;
     if (r != TC_OK) return r;
@@ -1550,10 +1601,7 @@ tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
         TCB_CUDA_CHECK(cudaEventRecord(c->join_ev, c->comm_st));
         TCB_CUDA_CHECK(cudaStreamWaitEvent(c->st, c->join_ev, 0));
     }
-    r = allreduce_loss(c);
-    if (r != TC_OK) return r;
-    TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
-    return TC_OK;
+    return allreduce_loss(c);  // the loss read-back is enqueued by tc_step, outside any capture
 }
 
 // Largest split-K workspace over the plan's contractions (and, in TC_PREC_F32, the largest
@@ -1783,11 +1831,13 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
     {
         const char* e = std::getenv("TCB_HOST_BF16");
-        c->host_bf16 = !c->f32 && !(e && e[0] == '0');
+        c->host_bf16 = !c->f32 && e && e[0] == '1';
         if (c->host_bf16) {
             for (int k = 0; k < 2; ++k) TCB_CUDA_CHECK(cudaMallocHost(&c->h_stage16[k], stage_el * 2));
             const unsigned hw = std::thread::hardware_concurrency();
-            c->pool = new HostPool(static_cast<int>(std::max(1u, std::min(16u, hw ? hw : 4u))));
+            const char* te = std::getenv("TCB_HOST_THREADS");
+            const int want = te ? std::atoi(te) : static_cast<int>(std::min(16u, hw ? hw : 4u));
+            c->pool = new HostPool(std::max(1, want));
         }
     }
     TCB_CUDA_CHECK(cudaMalloc(&c->d_labels, plan->input_dims[0] * sizeof(int32_t)));
@@ -1798,7 +1848,10 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_iter, 256));
     TCB_CUDA_CHECK(cudaMallocHost(&c->h_loss, 256));
     c->h_iter[0] = c->h_iter[1] = 0;
-    c->h_loss[0] = 0.f;
+    for (int k = 0; k < 2; ++k) {
+        c->h_loss[16 * k] = 0.f;
+        TCB_CUDA_CHECK(cudaEventCreateWithFlags(&c->loss_ev[k], cudaEventDisableTiming));
+    }
     // workspace + reduction partials
     c->ws_bytes = workspace_need(c.get(), &c->split_bytes);
     if (c->split_bytes) TCB_CUDA_CHECK(cudaMalloc(&c->split_buf, c->split_bytes));
@@ -1914,6 +1967,8 @@ void tc_ctx_destroy(tc_ctx* c) {
     cudaFree(c->d_iter);
     cudaFreeHost(c->h_iter);
     cudaFreeHost(c->h_loss);
+    for (int k = 0; k < 2; ++k)
+        if (c->loss_ev[k]) cudaEventDestroy(c->loss_ev[k]);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
 }
@@ -1999,8 +2054,18 @@ tc_status tc_stage_batch(tc_ctx* c, const float* x, const int32_t* labels) {
     if (c->host_bf16) {
         // the slot's previous host->device copy has finished reading the pinned buffer
         TCB_CUDA_CHECK(cudaEventSynchronize(c->h2d_done[k]));
-        c->pool->run(x, c->h_stage16[k], el);
-        TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], c->h_stage16[k], el * 2, cudaMemcpyHostToDevice, c->copy_st));
+        // each rounded chunk is copied while the pool rounds the next (TCB_STAGE_CHUNKS, default 8)
+        static const int chunks = [] {
+            const char* e = std::getenv("TCB_STAGE_CHUNKS");
+            return e ? std::max(1, std::atoi(e)) : 8;
+        }();
+        uint16_t* h = c->h_stage16[k];
+        uint16_t* dv = reinterpret_cast<uint16_t*>(c->d_stage[k]);
+        tc_status r = c->pool->run(x, h, el, chunks, [&](size_t a, size_t len) -> tc_status {
+            TCB_CUDA_CHECK(cudaMemcpyAsync(dv + a, h + a, len * 2, cudaMemcpyHostToDevice, c->copy_st));
+            return TC_OK;
+        });
+        if (r != TC_OK) return r;
     } else {
         TCB_CUDA_CHECK(cudaMemcpyAsync(c->d_stage[k], x, el * 4, cudaMemcpyHostToDevice, c->copy_st));
     }
@@ -2065,7 +2130,7 @@ tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
         if (r != TC_OK) return r;
         TCB_CUDA_CHECK(cudaGraphLaunch(c->gexec[k], c->st));
         count_launch(static_cast<unsigned>(std::max(0, c->launches_per_step - 1)));
-        return TC_OK;
+        return enqueue_loss_read(c);
     }
     c->h_iter[0] = static_cast<uint32_t>(iter);
     c->h_iter[1] = static_cast<uint32_t>(n0);
@@ -2090,7 +2155,7 @@ tc_status tc_step(tc_ctx* c, int iter, int n0, int update) {
     if (r != TC_OK) return r;
     if (c->launches_per_step < 0) c->launches_per_step = static_cast<int>(g_launches.load() - before);
     c->runs[k]++;
-    return TC_OK;
+    return enqueue_loss_read(c);
 }
 
 tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
@@ -2105,8 +2170,7 @@ tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
     if (s.kind == TC_STMT_PRINT) {
         r = allreduce_loss(c);
         if (r != TC_OK) return r;
-        TCB_CUDA_CHECK(cudaMemcpyAsync(c->h_loss, c->d_loss, sizeof(float), cudaMemcpyDeviceToHost, c->st));
-        return TC_OK;
+        return enqueue_loss_read(c);
     }
     if (s.kind != TC_STMT_UPDATE) return TC_OK;
     // single-statement form: this parameter's all-reduce + update, in stream order
@@ -2159,7 +2223,16 @@ tc_status tc_test(tc_ctx* c, int iter, int n0, double* precision) {
 tc_status tc_loss(tc_ctx* c, double* loss) {
     if (!c || !loss) return fail(TC_INVALID_ARG, "tc_loss");
     TCB_CUDA_CHECK(cudaStreamSynchronize(c->st));
-    *loss = c->h_loss[0];
+    *loss = c->h_loss[16 * c->loss_slot];
+    return TC_OK;
+}
+
+tc_status tc_loss_prev(tc_ctx* c, double* loss) {
+    if (!c || !loss) return fail(TC_INVALID_ARG, "tc_loss_prev");
+    if (c->loss_count < 2) return fail(TC_INVALID_ARG, "tc_loss_prev: fewer than two steps enqueued");
+    const int k = c->loss_slot ^ 1;
+    TCB_CUDA_CHECK(cudaEventSynchronize(c->loss_ev[k]));  // that step only, not the one running now
+    *loss = c->h_loss[16 * k];
     return TC_OK;
 }
 

@@ -115,6 +115,12 @@ class Trainer:
         nat.check(nat.lib().tc_loss(self._h, C.byref(v)))
         return v.value
 
+    def loss_prev(self) -> float:
+        """Loss of the step before the last one enqueued (waits for that step only)."""
+        v = C.c_double()
+        nat.check(nat.lib().tc_loss_prev(self._h, C.byref(v)))
+        return v.value
+
     def sync(self):
         nat.check(nat.lib().tc_sync(self._h))
 

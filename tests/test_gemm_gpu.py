@@ -192,6 +192,8 @@ HALO_CASES = [
     (2, 384, 7, 7, 192, 3, 1, 1),     # 7 x 7 under 3 x 3 with wide N (6 channel blocks)
     (2, 144, 14, 14, 160, 3, 1, 1),   # 144 channels: a 16-column partial chunk in the padded workspace, K = 160
     (2, 112, 14, 14, 224, 3, 1, 1),   # 112 channels (two blocks, the second 48 wide), K = 224
+    (2, 96, 27, 27, 256, 5, 1, 2),    # AlexNet conv2: filter gradient with MMA N = 96, 5 taps per group
+    (2, 32, 14, 14, 128, 3, 1, 1),    # filter gradient N = 32 (two tap groups of 5 + 4)
 ]
 
 

@@ -210,9 +210,63 @@ def test_bucket_overlap_matches_serial(name, batch, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
-def test_async_input_pipeline_matches_serial():
+def test_loss_prev_reads_each_step_one_late():
+    """tc_loss_prev returns the loss of the step before the last enqueued one (two pinned slots
+    written after the graph replay): reading every loss one step late gives the same sequence as
+    reading each synchronously."""
+    net = compile_network("alexnet", 4)
+    runs = []
+    for late in (False, True):
+        tr = Trainer(net, use_graph=True, seed=17)
+        tr.init_params()
+        losses = []
+        for it in range(5):
+            tr.stage_synthetic(it, 0)
+            tr.step(it)
+            if not late:
+                losses.append(tr.loss())
+            elif it > 0:
+                losses.append(tr.loss_prev())
+        if late:
+            tr.sync()
+            losses.append(tr.loss())
+        runs.append(losses)
+        tr.close()
+    assert runs[0] == runs[1], runs
+    assert len(set(runs[0])) > 1, runs[0]  # distinct steps, not one slot read twice
+
+
+def test_host_bf16_staging_bit_identical(monkeypatch):
+    """Rounding the host batch to bf16 on the host (TCB_HOST_BF16=1, chunked, half the H2D bytes)
+    stages exactly the values the device conversion of the fp32 batch produces: identical
+    losses and parameters after two steps, and tc_stage_bytes reports the halved copy."""
+    net = compile_network("alexnet", 4)
+    batches = [orc.synth_batch(net, 4, it) for it in range(2)]
+    runs = []
+    for hb in ("0", "1"):
+        monkeypatch.setenv("TCB_HOST_BF16", hb)
+        tr = Trainer(net, use_graph=True, seed=3)
+        tr.init_params()
+        losses = []
+        for it in range(2):
+            tr.stage_batch(*batches[it])
+            tr.step(it)
+            losses.append(tr.loss())
+        runs.append((losses, [tr.get_param(i) for i in range(len(net.params))], tr.stage_bytes))
+        tr.close()
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        np.testing.assert_array_equal(a, b)
+    el = int(np.prod(net.input_dims))
+    assert runs[0][2] == 4 * el + 4 * 4 and runs[1][2] == 2 * el + 4 * 4, (runs[0][2], runs[1][2])
+
+
+@pytest.mark.parametrize("host_bf16", ["0", "1"])
+def test_async_input_pipeline_matches_serial(host_bf16, monkeypatch):
     """Batches staged one step ahead (H2D on the copy stream overlapping the running step,
-    two staging slots) train exactly like batches staged and consumed one at a time."""
+    two staging slots) train exactly like batches staged and consumed one at a time; with host
+    bf16 rounding (TCB_HOST_BF16=1: chunked rounding overlapping the copies) as well."""
+    monkeypatch.setenv("TCB_HOST_BF16", host_bf16)
     net = compile_network("alexnet", 4)
     batches = [orc.synth_batch(net, 3, it) for it in range(4)]
     runs = []
@@ -262,6 +316,28 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
     assert runs[0][3] < runs[1][3], (runs[0][3], runs[1][3])  # the folds removed launches
     assert runs[0][0] == runs[1][0], (runs[0][0], runs[1][0])
     for a, b in zip(runs[0][1] + runs[0][2], runs[1][1] + runs[1][2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,batch", [("alexnet", 8), ("resnet50", 2), ("googlenet", 2)])
+def test_reduce4_bit_identical(name, batch, monkeypatch):
+    """The 4-column split-K reduce (16-byte partial loads) sums every element in the same split
+    order as the scalar reduce: two training steps agree bit for bit."""
+    runs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("TCB_REDUCE4", v)
+        net = compile_network(name, batch)
+        tr = Trainer(net, use_graph=True, seed=23)
+        tr.init_params()
+        losses = []
+        for it in range(2):
+            tr.stage_synthetic(it, 0)
+            tr.step(it)
+            losses.append(tr.loss())
+        runs.append((losses, [tr.get_param(i) for i in range(len(net.params))]))
+        tr.close()
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
         np.testing.assert_array_equal(a, b)
 
 
