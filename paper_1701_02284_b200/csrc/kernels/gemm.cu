@@ -195,11 +195,20 @@ static bool make_tmap_store(CUtensorMap* map, void* base, bool bf16, uint64_t N,
 
 // ------------------------------------------------------------------ split-K reduce
 // out[m, n] = epilogue( sum_s ws[s][m][n] ), fixed summation order (deterministic).
+// Folded bias gradient (halo filter gradient): out[m] = sum over splits of the [split][M] partials,
+// in split order, by the thread that reduces column 0 of row m.
+__device__ __forceinline__ float sum_bias_partials(const float* __restrict__ b, int splits, int M, int m) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += b[static_cast<long long>(s) * M + m];
+    return acc;
+}
+
 // seg_out > 0: the partials hold each segment of seg_out columns padded to seg_in columns
 // (ws row = N / seg_out * seg_in; the halo filter gradient's per-tap channel blocks).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
-                                     int n_bias, int relu, float beta, int trans, int seg_in, int seg_out) {
+                                     int n_bias, int relu, float beta, int trans, int seg_in, int seg_out,
+                                     const float* __restrict__ bias_ws, float* __restrict__ bias_out) {
     pdl_wait();
     pdl_trigger();
     const long long total = static_cast<long long>(M) * N;
@@ -209,6 +218,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
         const int n = static_cast<int>(i - static_cast<long long>(m) * N);
         const long long src =
             seg_out ? static_cast<long long>(m) * (N / seg_out) * seg_in + (n / seg_out) * seg_in + n % seg_out : i;
+        if (bias_out && n == 0) bias_out[m] = sum_bias_partials(bias_ws, splits, M, m);
         float acc = 0.f;
         for (int s = 0; s < splits; ++s) acc += ws[s * split_stride + src];
         if (bias && n < n_bias) acc += bias[n];
@@ -227,7 +237,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 // Needs N, ldd (and seg_in / seg_out when remapping) multiples of 4 and trans == 0.
 __global__ void splitk_reduce4_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                       void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
-                                      int n_bias, int relu, float beta, int seg_in, int seg_out) {
+                                      int n_bias, int relu, float beta, int seg_in, int seg_out,
+                                      const float* __restrict__ bias_ws, float* __restrict__ bias_out) {
     pdl_wait();
     pdl_trigger();
     const int nq = N >> 2;
@@ -238,6 +249,7 @@ __global__ void splitk_reduce4_kernel(const float* __restrict__ ws, int splits, 
         const int n = static_cast<int>(i - static_cast<long long>(m) * nq) * 4;
         const long long src = seg_out ? static_cast<long long>(m) * (N / seg_out) * seg_in + (n / seg_out) * seg_in + n % seg_out
                                       : static_cast<long long>(m) * N + n;
+        if (bias_out && n == 0) bias_out[m] = sum_bias_partials(bias_ws, splits, M, m);
         const float4* w = reinterpret_cast<const float4*>(ws + src);
         const long long ss = split_stride >> 2;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -278,7 +290,8 @@ __global__ void splitk_reduce4_kernel(const float* __restrict__ ws, int splits, 
 // Launch the split-K reduce: the 4-column form when the shapes allow, else the scalar one.
 static tc_status launch_splitk_reduce(const float* ws, int splits, int M, int N, long long split_stride, void* out,
                                       long long ldd, int out_bf16, const float* bias, int n_bias, int relu, float beta,
-                                      int trans, int seg_in, int seg_out, cudaStream_t st) {
+                                      int trans, int seg_in, int seg_out, cudaStream_t st,
+                                      const float* bias_ws = nullptr, float* bias_out = nullptr) {
     const char* e = std::getenv("TCB_REDUCE4");  // 0: scalar form only (A/B, bit-identity test)
     const bool vec_on = !(e && e[0] == '0');
     // (small outputs keep the scalar form: 4x the threads hide more latency than 16-byte loads save)
@@ -289,10 +302,10 @@ static tc_status launch_splitk_reduce(const float* ws, int splits, int M, int N,
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, num_sms() * 8LL));
     if (vec)
         TCB_LAUNCH(splitk_reduce4_kernel, blocks, 256, 0, st, ws, splits, M, N, split_stride, out, ldd, out_bf16, bias,
-                   n_bias, relu, beta, seg_in, seg_out);
+                   n_bias, relu, beta, seg_in, seg_out, bias_ws, bias_out);
     else
         TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, ws, splits, M, N, split_stride, out, ldd, out_bf16, bias,
-                   n_bias, relu, beta, trans, seg_in, seg_out);
+                   n_bias, relu, beta, trans, seg_in, seg_out, bias_ws, bias_out);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -759,7 +772,7 @@ struct WgradHaloPlan {
     int wr = 0, th = 0, hh = 0, wv = 0, xt = 0, yt = 0, cb = 1, ntap = 0, ntg = 0, ncg = 0, mt = 0;
     int splits = 0, tiles = 0, tiles_per_split = 0, stages = 0, wcs = 0, nc = 0;
     uint32_t dy_bytes = 0, halo_bytes = 0, stage_bytes = 0;
-    size_t ws_bytes = 0;
+    size_t ws_bytes = 0, bias_off = 0;
 };
 
 static bool wgrad_halo_enabled() {
@@ -841,12 +854,15 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
     pl.tiles_per_split = ceil_div(pl.tiles, std::min(want, pl.tiles));
     pl.splits = ceil_div(pl.tiles, pl.tiles_per_split);
     pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * taps * pl.wcs * sizeof(float);
+    pl.bias_off = (pl.ws_bytes + 255) & ~static_cast<size_t>(255);  // folded bias partials [splits][K]
+    pl.ws_bytes = pl.bias_off + static_cast<size_t>(pl.splits) * d->K * sizeof(float);
     pl.ok = 1;
     return pl;
 }
 
 static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, const void* dy, const void* x, float* dw,
-                                long long ldw, void* ws, size_t ws_bytes, cudaStream_t st) {
+                                long long ldw, void* ws, size_t ws_bytes, cudaStream_t st, float* dbias = nullptr) {
+    if (dbias && pl.swap) return fail(TC_INVALID_ARG, "halo filter gradient: bias fold needs the unswapped kernel");
     if (!ws || ws_bytes < pl.ws_bytes)
         return fail(TC_INVALID_ARG, "halo filter gradient: workspace too small: need " + std::to_string(pl.ws_bytes));
     WgradHaloParams p;
@@ -861,6 +877,8 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     p.ntap = pl.ntap, p.ntg = pl.ntg, p.ncg = pl.ncg, p.nc = pl.nc, p.cs = d->cs, p.wcs = pl.wcs, p.mt = pl.mt;
     p.splits = pl.splits, p.tiles = pl.tiles, p.tiles_per_split = pl.tiles_per_split;
     p.dy_bytes = pl.dy_bytes, p.halo_bytes = pl.halo_bytes, p.stage_bytes = pl.stage_bytes, p.stages = pl.stages;
+    float* bias_ws = dbias ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.bias_off) : nullptr;
+    p.bias_ws = bias_ws;
     std::string err;
     if (!make_tmap_halo_src(&p.tmX, x, d->N, d->H, d->W, d->cs, pl.wr, pl.hh, &err)) return fail(TC_INVALID_ARG, err);
     if (!make_tmap_halo_src(&p.tmDy, dy, d->N, d->Ho, d->Wo, d->ks, pl.wv, 1, &err)) return fail(TC_INVALID_ARG, err);
@@ -896,7 +914,7 @@ static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, 
     const bool padded = pl.wcs != d->cs;
     return launch_splitk_reduce(static_cast<const float*>(ws), pl.splits, d->K, static_cast<int>(ncol),
                                 static_cast<long long>(d->K) * static_cast<long long>(wcol), dw, ldw, 0, nullptr, 0, 0,
-                                0.f, 0, padded ? pl.wcs : 0, padded ? d->cs : 0, st);
+                                0.f, 0, padded ? pl.wcs : 0, padded ? d->cs : 0, st, bias_ws, dbias);
 }
 
 // ------------------------------------------------------------------ channel-stride-4 first layer
@@ -1375,12 +1393,27 @@ tc_status tc_conv2d_bwd_data(const tc_conv_desc* d, const void* dy, const void* 
 
 tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void* x, float* dw, void* ws,
                                size_t ws_bytes, void* stream) {
+    return tcb::conv_bwd_filter_ex(d, dy, x, dw, nullptr, ws, ws_bytes, stream);
+}
+}  // extern "C"
+
+namespace tcb {
+bool wgrad_bias_foldable(const tc_conv_desc* d) {
+    const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");  // read at plan time
+    if ((e && e[0] == '0') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
+    const WgradHaloPlan pl = wgrad_halo_plan(d);
+    return pl.ok && !pl.swap;
+}
+
+tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* x, float* dw, float* dbias, void* ws,
+                             size_t ws_bytes, void* stream) {
     tc_status s = check_conv(d);
     if (s != TC_OK) return s;
+    if (dbias && !wgrad_bias_foldable(d)) return fail(TC_INVALID_ARG, "filter gradient: bias fold not available here");
     if (const ConvC4WgradPlan pl = conv_c4_wgrad_plan(d); pl.ok)
         return run_conv_c4_wgrad(pl, d, dy, x, dw, ws, ws_bytes, static_cast<cudaStream_t>(stream));
     if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok)
-        return run_wgrad_halo(pl, d, dy, x, dw, filter_ld(d), ws, ws_bytes, static_cast<cudaStream_t>(stream));
+        return run_wgrad_halo(pl, d, dy, x, dw, filter_ld(d), ws, ws_bytes, static_cast<cudaStream_t>(stream), dbias);
     GemmParams p;
     init_params(p);
     const int npix = d->N * d->Ho * d->Wo;
@@ -1430,5 +1463,4 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
     }
     return run_gemm(p, lp, dw, filter_ld(d), 0, nullptr, 0, 0, 0.f, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
-
-}  // extern "C"
+}  // namespace tcb

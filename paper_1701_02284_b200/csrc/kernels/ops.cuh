@@ -175,6 +175,11 @@ tc_status conv_fwd_ex(const tc_conv_desc* d, const void* x, const void* w, const
 // relu_mask: bf16 [N*H*W][cs] forward ReLU output; dx *= [mask > 0] in the epilogue (may be null)
 tc_status conv_bwd_data_ex(const tc_conv_desc* d, const void* dy, const void* w_rskc, void* dx, int dx_f32, void* ws,
                            size_t ws_bytes, void* stream, const void* relu_mask = nullptr, int w_kmajor = 0);
+// Filter gradient that also writes the bias gradient (sum of dy over the pixels) when dbias is
+// non-null; only for convs where wgrad_bias_foldable() holds (the halo filter-gradient kernel).
+tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* x, float* dw, float* dbias, void* ws,
+                             size_t ws_bytes, void* stream);
+bool wgrad_bias_foldable(const tc_conv_desc* d);
 
 // d_iter[0] = iter, d_iter[1] = n0 (kernel arguments travel with the launch: no host sync)
 tc_status launch_set_iter(uint32_t* d_iter, uint32_t iter, uint32_t n0, cudaStream_t st);

@@ -45,6 +45,7 @@ struct WgradHaloParams {
     uint32_t halo_bytes;  // per 64-channel halo (1024-aligned, includes the over-read slack)
     uint32_t stage_bytes; // dy tile + CB halos
     int stages;
+    float* bias_ws;       // folded bias gradient: per-split partial sums [splits][K] of dy, or nullptr
 };
 
 template <int CB>
@@ -74,6 +75,10 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
     const int tile0 = sp * p.tiles_per_split;
     const int tile1 = min(p.tiles, tile0 + p.tiles_per_split);
     const uint32_t ncols = static_cast<uint32_t>(p.ntap) * p.nc;
+    // the (channel group 0, tap group 0) unit of each (m block, split) also sums its dy tiles over
+    // the pixels (the bias gradient): its epilogue warps read every staged dy tile from shared
+    // memory while the MMA runs, so each stage is released by the MMA commit + 4 warp arrivals
+    const bool do_bias = p.bias_ws != nullptr && cg == 0 && tg == 0;
     const uint32_t tmem_cols = ncols <= 32 ? 32 : ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
 
     // zero every stage and the staging once: the dy gap positions (wr - wv per row) and the halo
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
         tma_prefetch(&p.tmWs);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], do_bias ? 5 : 1);
         }
         mbar_init(tdone, 1);
         fence_mbar_init();
@@ -168,6 +173,48 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
         // ---------------- epilogue: warp e reads TMEM lanes 32 (e - 4) .. +32 (rows k)
         const int quarter = warp - 4;
         uint8_t* stg = sStage + quarter * kStagingBytes;
+        if (do_bias) {
+            // thread e: 16-byte column chunk kc of k-atom a (8 k values), rows rg, rg + 8, ... of
+            // the 128-row tile: the SW128 chunk of row r is kc ^ (r & 7) = kc ^ rg for all of them
+            const int e = threadIdx.x - 128, a = (e >> 3) & 1, kc = e & 7, rg = e >> 4;
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = tile0; t < tile1; ++t) {
+                mbar_wait(&full[s], ph);
+                const uint8_t* src = smem + s * p.stage_bytes + a * (p.dy_bytes / 2) + rg * 128 + ((kc ^ rg) << 4);
+#pragma unroll 4
+                for (int i = 0; i < 16; ++i) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(src + i * 1024);
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 f = __bfloat1622float2(h[q]);
+                        acc[2 * q] += f.x;
+                        acc[2 * q + 1] += f.y;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            // the 8 row groups of each column, summed in fixed order through the staging buffers
+            float* red = reinterpret_cast<float*>(sStage);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red[rg * 128 + a * 64 + kc * 8 + j] = acc[j];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            float sum = 0.f;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) sum += red[g * 128 + e];
+            const int k = mb * 128 + e;
+            if (k < p.K) p.bias_ws[static_cast<long long>(sp) * p.K + k] = sum;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging reused by the stores below
+        }
         mbar_wait(tdone, 0);
         tc_fence_after();
         const int m0 = mb * 128 + quarter * 32;

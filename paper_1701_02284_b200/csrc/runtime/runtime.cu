@@ -218,6 +218,9 @@ struct tc_ctx {
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
     std::vector<int> fuse_add_res, fuse_add_out;    // BN forward: folded residual add (other operand, output var)
     std::vector<char> sgd_fused;                    // per param: momentum update fused into its FC filter gradient
+    // bias gradient folded into the halo filter-gradient kernel of the same conv (bf16 mode):
+    // per filter-gradient stmt the bias param it also produces; per bias stmt the producer (-1)
+    std::vector<int> wgrad_bias_param, bias_fold_by;
     bool fuse_sgd_active = false;                   // set by run_body for update steps
     std::vector<char> pool_flag_nonpos;             // max-pool forward: flag windows with max <= 0 in the index
     std::vector<char> pool_mask_in_idx;             // max-pool backward: its folded ReLU mask is in the index
@@ -283,7 +286,7 @@ struct tc_ctx {
         cudaEvent_t ready = nullptr;
     };
     std::vector<Bucket> buckets;
-    std::vector<int> stmt_bucket;  // stmt -> bucket it completes, or -1
+    std::vector<std::vector<int>> stmt_flush;  // stmt -> buckets flushed after it (bucket order)
     float* grads = nullptr;        // contiguous gradient region inside the slab
     long long grads_n = 0;
     cudaStream_t comm_st = nullptr;
@@ -1098,7 +1101,9 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
             if constexpr (std::is_same_v<T, float>)
                 return split_conv(c, 2, d, q, static_cast<const float*>(P.var(dy.id)), static_cast<const float*>(P.var(x.id)),
                                   0, g);
-            tc_status r = tc_conv2d_bwd_filter(&d, P.var(dy.id), P.var(x.id), g, c->ws, c->ws_bytes, st);
+            const int bp = c->wgrad_bias_param[idx];
+            tc_status r = conv_bwd_filter_ex(&d, P.var(dy.id), P.var(x.id), g, bp >= 0 ? c->params[bp].g : nullptr,
+                                             c->ws, c->ws_bytes, st);
             if (r != TC_OK || !q.s2d) return r;
             return launch_s2d_mask_grad(g, q.K, q.Kw, q.Rp, q.s2d, q.cs, q.R, q.S, st);
         }
@@ -1481,6 +1486,7 @@ tc_status exec_stmt(tc_ctx* c, int i) {
         return launch_loss(a, b, n, coef, s.nterms, c->d_loss, c->st);
     }
     // Update: the gradient only; all-reduce + momentum SGD run per bucket (flush_bucket)
+    if (c->bias_fold_by[i] >= 0) return TC_OK;  // produced by its conv's filter-gradient kernel
     ParamL& q = c->params[s.param];
     return c->f32 ? compute_param_grad<float>(c, i, s.param, q.g) : compute_param_grad<bf16>(c, i, s.param, q.g);
 }
@@ -1577,6 +1583,57 @@ static tc_status enqueue_loss_read(tc_ctx* c) {
     return TC_OK;
 }
 
+// Bias gradient of a conv (CONV_BWD_BIAS over the same dy) computed by its halo filter-gradient
+// kernel (conv_bwd_filter_ex): the kernel's epilogue warps sum the staged dy tiles while the MMA
+// runs, and the split-K reduce adds the per-split partials -- no separate two-pass column sum
+// over dy.  The gradient-bucket flush that ran after the bias statement moves to the producer
+// when the bias statement comes first.  TCB_WGRAD_BIAS_FOLD=0 disables.
+void plan_bias_fold(tc_ctx* c) {
+    const tc_plan* p = c->plan;
+    c->wgrad_bias_param.assign(p->nstmts, -1);
+    c->bias_fold_by.assign(p->nstmts, -1);
+    if (c->f32) return;
+    Ptrs P{c};
+    for (int i = 0; i < p->nstmts; ++i) {
+        const tc_stmt& b = p->stmts[i];
+        if (b.kind != TC_STMT_UPDATE || b.op != TC_OP_CONV_BWD_BIAS || b.in[0].kind != TC_REF_VAR) continue;
+        for (int j = 0; j < p->nstmts; ++j) {
+            const tc_stmt& f = p->stmts[j];
+            if (f.kind != TC_STMT_UPDATE || f.op != TC_OP_CONV_BWD_FILTER || f.in[0].kind != TC_REF_VAR ||
+                f.in[0].index != b.in[0].index || c->wgrad_bias_param[j] >= 0)
+                continue;
+            const ParamL& w = c->params[f.param];
+            if (c->params[b.param].K != w.K) continue;
+            const tc_conv_desc d = conv_desc(P.L(f.in[1]), w, P.L(f.in[0]), f);
+            if (!wgrad_bias_foldable(&d)) continue;
+            if (i < j) {  // bucket flushes at statements i .. j-1 move to just before j's own, in order
+                std::vector<int> moved;
+                for (int k = i; k < j; ++k) {
+                    moved.insert(moved.end(), c->stmt_flush[k].begin(), c->stmt_flush[k].end());
+                    c->stmt_flush[k].clear();
+                }
+                c->stmt_flush[j].insert(c->stmt_flush[j].begin(), moved.begin(), moved.end());
+                for (int bki : moved) c->buckets[bki].last_stmt = j;
+            }
+            c->wgrad_bias_param[j] = b.param;
+            c->bias_fold_by[i] = j;
+            break;
+        }
+    }
+}
+
+// Per-statement form of one parameter's all-reduce + momentum update (tc_exec_stmt).
+static tc_status exec_stmt_update(tc_ctx* c, int index, int param) {
+    ParamL& q = c->params[param];
+    if (c->comm && ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
+        return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
+    if (c->plan->clip > 0)  // the clipped update needs the whole gradient: applied at the last Update
+        return index == c->last_update_stmt ? clip_update(c, c->st) : TC_OK;
+    SgdTensor t = sgd_tensor(c, param);
+    tc_status r = launch_sgd(&t, 1, nullptr, c->st);
+    return r != TC_OK ? r : refresh_crsk(c, {param}, c->st);
+}
+
 tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
     tc_status r = set_iter ? launch_set_iter(c->d_iter, c->h_iter[0], c->h_iter[1], c->st) : TC_OK;
     if (r != TC_OK) return r;
@@ -1588,8 +1645,8 @@ tc_status run_body(tc_ctx* c, int update, bool overlap, bool set_iter) {
     for (int i = 0; i < c->plan->nstmts; ++i) {
         r = exec_stmt(c, i);
         if (r != TC_OK) return r;
-        if (c->stmt_bucket[i] >= 0) {
-            r = flush_bucket(c, c->stmt_bucket[i], update, overlap);
+        for (int bki : c->stmt_flush[i]) {
+            r = flush_bucket(c, bki, update, overlap);
             if (r != TC_OK) return r;
         }
     }
@@ -1734,7 +1791,7 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     }
     const char* bmb = std::getenv("TCB_BUCKET_MB");
     const long long bucket_cap = static_cast<long long>((bmb ? std::atof(bmb) : 32.0) * (1 << 20) / 4);
-    c->stmt_bucket.assign(plan->nstmts, -1);
+    c->stmt_flush.assign(plan->nstmts, {});
     long long goff = 0;
     for (size_t j = 0; j < order.size(); ++j) {
         ParamL& q = c->params[order[j]];
@@ -1748,10 +1805,11 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
         bk.n = goff - static_cast<long long>(bk.off);
         if (bk.n >= bucket_cap || j + 1 == order.size() || bk.params.size() >= 32) {
             bk.last_stmt = q.update_stmt;
-            c->stmt_bucket[q.update_stmt] = static_cast<int>(c->buckets.size()) - 1;
+            c->stmt_flush[q.update_stmt].push_back(static_cast<int>(c->buckets.size()) - 1);
         }
     }
     c->grads_n = goff;
+    plan_bias_fold(c.get());
     // parameter slab: [gradients (contiguous, bucket order)] then per parameter p, v, bf16 shadows
     size_t slab = static_cast<size_t>(goff) * 4;
     auto reserve = [&](size_t bytes) {
@@ -2173,15 +2231,13 @@ tc_status tc_exec_stmt(tc_ctx* c, int index, int iter, int n0) {
         return enqueue_loss_read(c);
     }
     if (s.kind != TC_STMT_UPDATE) return TC_OK;
-    // single-statement form: this parameter's all-reduce + update, in stream order
-    ParamL& q = c->params[s.param];
-    if (c->comm && ncclAllReduce(q.g, q.g, q.n, ncclFloat, ncclSum, c->comm, c->st) != ncclSuccess)
-        return fail(TC_NCCL_ERROR, "ncclAllReduce failed");
-    if (c->plan->clip > 0)  // the clipped update needs the whole gradient: applied at the last Update
-        return index == c->last_update_stmt ? clip_update(c, c->st) : TC_OK;
-    SgdTensor t = sgd_tensor(c, s.param);
-    r = launch_sgd(&t, 1, nullptr, c->st);
-    return r != TC_OK ? r : refresh_crsk(c, {s.param}, c->st);
+    // a folded bias gradient computed by a later statement is updated there
+    if (c->bias_fold_by[index] > index) return TC_OK;
+    r = exec_stmt_update(c, index, s.param);
+    const int bp = c->wgrad_bias_param[index];
+    if (r == TC_OK && bp >= 0 && c->params[bp].update_stmt < index && c->plan->clip <= 0)  // (clip: one pass did all)
+        r = exec_stmt_update(c, index, bp);
+    return r;
 }
 
 tc_status tc_test(tc_ctx* c, int iter, int n0, double* precision) {
@@ -2358,7 +2414,7 @@ tc_status tc_profile_step(tc_ctx* c, int iter, int n0, int update, float* stmt_m
         r = exec_stmt(c, i);
         c->prof_launches[i] = static_cast<int>(g_launches.load() - l0);
         cudaEventRecord(evx[i], c->st);
-        if (r == TC_OK && c->stmt_bucket[i] >= 0) r = flush_bucket(c, c->stmt_bucket[i], update, false);
+        for (size_t b = 0; r == TC_OK && b < c->stmt_flush[i].size(); ++b) r = flush_bucket(c, c->stmt_flush[i][b], update, false);
         if (r == TC_OK && update && i == c->last_update_stmt && c->plan->clip > 0) r = clip_update(c, c->st);
         cudaEventRecord(ev[i + 1], c->st);
     }

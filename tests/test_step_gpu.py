@@ -319,6 +319,34 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,batch", [("alexnet", 16), ("vgg16", 2), ("googlenet", 2)])
+def test_wgrad_bias_fold(name, batch, monkeypatch):
+    """Conv bias gradients summed by the halo filter-gradient kernel (TCB_WGRAD_BIAS_FOLD, default
+    on) match the separate two-pass column sum to fp32 summation-order error, the filter gradients
+    are bit-identical, and the fold removes launches."""
+    runs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("TCB_WGRAD_BIAS_FOLD", v)
+        net = compile_network(name, batch)
+        tr = Trainer(net, use_graph=True, seed=29)
+        tr.init_params()
+        tr.stage_synthetic(0, 0)
+        tr.step(0, update=False)
+        runs.append(([tr.grad(i) for i in range(len(net.params))], tr.launches_per_step))
+        tr.close()
+    assert runs[1][1] < runs[0][1], (runs[0][1], runs[1][1])
+    folded = 0
+    for i, p in enumerate(net.params):
+        a, b = runs[0][0][i], runs[1][0][i]
+        if p.name.endswith("_B") and not np.array_equal(a, b):
+            folded += 1
+            err = np.abs(a - b).max() / max(np.abs(a).max(), 1e-30)
+            assert err < 1e-5, (p.name, err)
+        else:
+            np.testing.assert_array_equal(a, b, err_msg=p.name)
+    assert folded > 0
+
+
 @pytest.mark.parametrize("name,batch", [("alexnet", 8), ("resnet50", 2), ("googlenet", 2)])
 def test_reduce4_bit_identical(name, batch, monkeypatch):
     """The 4-column split-K reduce (16-byte partial loads) sums every element in the same split
