@@ -862,7 +862,6 @@ static WgradHaloPlan wgrad_halo_plan(const tc_conv_desc* d) {
 
 static tc_status run_wgrad_halo(const WgradHaloPlan& pl, const tc_conv_desc* d, const void* dy, const void* x, float* dw,
                                 long long ldw, void* ws, size_t ws_bytes, cudaStream_t st, float* dbias = nullptr) {
-    if (dbias && pl.swap) return fail(TC_INVALID_ARG, "halo filter gradient: bias fold needs the unswapped kernel");
     if (!ws || ws_bytes < pl.ws_bytes)
         return fail(TC_INVALID_ARG, "halo filter gradient: workspace too small: need " + std::to_string(pl.ws_bytes));
     WgradHaloParams p;
@@ -1401,8 +1400,7 @@ namespace tcb {
 bool wgrad_bias_foldable(const tc_conv_desc* d) {
     const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");  // read at plan time
     if ((e && e[0] == '0') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
-    const WgradHaloPlan pl = wgrad_halo_plan(d);
-    return pl.ok && !pl.swap;
+    return wgrad_halo_plan(d).ok;
 }
 
 tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* x, float* dw, float* dbias, void* ws,

@@ -48,6 +48,58 @@ struct WgradHaloParams {
     float* bias_ws;       // folded bias gradient: per-split partial sums [splits][K] of dy, or nullptr
 };
 
+// Folded bias gradient, run by the 4 epilogue warps (threads 128..255) of one unit per (k block,
+// split) while the MMA consumes the same stages: per staged dy tile (natoms k-atoms of 128 rows x
+// 64 k, SW128, zero gap rows) the column sums over the 128 rows; each stage is released by one
+// arrival per warp (the stage's empty barrier counts the MMA commit + 4).  Thread e owns the
+// 16-byte chunk kc of atom a over rows rg, rg + rgs, ...: with rgs a multiple of 8 the SW128
+// chunk of all its rows is kc ^ (rg & 7).  The row groups are summed in fixed order at the end,
+// through the (not yet used) epilogue staging; out: bias_ws[sp][k_base + k].
+__device__ __forceinline__ void wgrad_bias_sums(const WgradHaloParams& p, const uint8_t* smem, uint8_t* sStage,
+                                                uint64_t* full, uint64_t* empty, int tile0, int tile1, int natoms,
+                                                int k_base, int sp, int lane) {
+    const int e = threadIdx.x - 128;
+    const int combos = natoms * 8, rgs = 128 / combos;
+    const int combo = e % combos, rg = e / combos, a = combo >> 3, kc = combo & 7;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = tile0; t < tile1; ++t) {
+        mbar_wait(&full[s], ph);
+        const uint8_t* src = smem + s * p.stage_bytes + a * (BM * 128) + rg * 128 + ((kc ^ (rg & 7)) << 4);
+        for (int i = 0; i < 128 / rgs; ++i) {
+            const uint4 v = *reinterpret_cast<const uint4*>(src + i * rgs * 128);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(h[q]);
+                acc[2 * q] += f.x;
+                acc[2 * q + 1] += f.y;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+    float* red = reinterpret_cast<float*>(sStage);  // [rgs][natoms * 64]
+    const int row = natoms * 64;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[rg * row + combo * 8 + j] = acc[j];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (e < row) {
+        float sum = 0.f;
+        for (int g = 0; g < rgs; ++g) sum += red[g * row + e];
+        const int k = k_base + e;
+        if (k < p.K) p.bias_ws[static_cast<long long>(sp) * p.K + k] = sum;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the staging is reused by the stores that follow
+}
+
 template <int CB>
 __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_constant__ WgradHaloParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -173,48 +225,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_kernel(const __grid_cons
         // ---------------- epilogue: warp e reads TMEM lanes 32 (e - 4) .. +32 (rows k)
         const int quarter = warp - 4;
         uint8_t* stg = sStage + quarter * kStagingBytes;
-        if (do_bias) {
-            // thread e: 16-byte column chunk kc of k-atom a (8 k values), rows rg, rg + 8, ... of
-            // the 128-row tile: the SW128 chunk of row r is kc ^ (r & 7) = kc ^ rg for all of them
-            const int e = threadIdx.x - 128, a = (e >> 3) & 1, kc = e & 7, rg = e >> 4;
-            float acc[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = tile0; t < tile1; ++t) {
-                mbar_wait(&full[s], ph);
-                const uint8_t* src = smem + s * p.stage_bytes + a * (p.dy_bytes / 2) + rg * 128 + ((kc ^ rg) << 4);
-#pragma unroll 4
-                for (int i = 0; i < 16; ++i) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(src + i * 1024);
-                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float2 f = __bfloat1622float2(h[q]);
-                        acc[2 * q] += f.x;
-                        acc[2 * q + 1] += f.y;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-            // the 8 row groups of each column, summed in fixed order through the staging buffers
-            float* red = reinterpret_cast<float*>(sStage);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) red[rg * 128 + a * 64 + kc * 8 + j] = acc[j];
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            float sum = 0.f;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) sum += red[g * 128 + e];
-            const int k = mb * 128 + e;
-            if (k < p.K) p.bias_ws[static_cast<long long>(sp) * p.K + k] = sum;
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging reused by the stores below
-        }
+        if (do_bias) wgrad_bias_sums(p, smem, sStage, full, empty, tile0, tile1, 2, mb * 128, sp, lane);
         mbar_wait(tdone, 0);
         tc_fence_after();
         const int m0 = mb * 128 + quarter * 32;
@@ -299,6 +310,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
     const int NK = p.K <= 64 ? 64 : 128;  // accumulator columns per tap pair (k padded to 64 / 128)
     const uint32_t ncols = static_cast<uint32_t>((p.ntap + 1) / 2) * NK;
     const uint32_t tmem_cols = ncols <= 64 ? 64 : ncols <= 128 ? 128 : ncols <= 256 ? 256 : 512;
+    const bool do_bias = p.bias_ws != nullptr && cg == 0 && tg == 0;  // see wgrad_bias_sums
 
     for (uint32_t i = threadIdx.x; i < (S * p.stage_bytes + 4 * kStagingBytes) / 16; i += blockDim.x)
         st_shared_v4(smem_u32(smem) + i * 16, 0u, 0u, 0u, 0u);
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
         tma_prefetch(&p.tmWs);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], do_bias ? 5 : 1);
         }
         mbar_init(tdone, 1);
         fence_mbar_init();
@@ -383,6 +395,7 @@ __global__ void __launch_bounds__(256, 1) tc_wgrad_halo_swap_kernel(const __grid
         // warp e: TMEM lanes 32 (e - 4) .. +32 = tap (e - 4) / 2 of each pair, channels 32 ((e - 4) % 2) + lane
         const int quarter = warp - 4;
         uint8_t* stg = sStage + quarter * kStagingBytes;
+        if (do_bias) wgrad_bias_sums(p, smem, sStage, full, empty, tile0, tile1, NK / 64, 0, sp, lane);
         mbar_wait(tdone, 0);
         tc_fence_after();
         const int csub = (quarter & 1) * 32;
