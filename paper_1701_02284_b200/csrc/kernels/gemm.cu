@@ -546,6 +546,13 @@ static int halo_ms_mode() {
     }();
     return v;
 }
+static int halo_model_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("TCB_HALO_MODEL");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
 static double halo_min_util() {
     static const double v = [] {
         const char* e = std::getenv("TCB_HALO_MIN_UTIL");
@@ -721,26 +728,69 @@ static tc_status run_halo(const HaloGeom& g, const void* src, int nimg, int Hs, 
     p.alpha = 1.f;
     p.mask = static_cast<const __nv_bfloat16*>(mask);
     p.mask_ld = N;
-    // tile width: per-k-block cost model of plan_launch over the column tiles
-    int bn = N > 128 ? 256 : N > 64 ? 128 : 64;
-    if (N > 128 && N % 256 != 0 && ceil_div(N, 128) * t_kblock(128, 1) < ceil_div(N, 256) * t_kblock(256, 1)) bn = 128;
-    if (forced_bn()) bn = forced_bn();
-    p.tiles_n = ceil_div(N, bn);
-    // two subtiles per unit (ms = 2, BN <= 128) when it is faster by a simple model: waves x
-    // k-blocks x max(MMA cycles, filter bytes at ~40 B/clk of the L2 -> SM path per SM)
+    // Tile shape (BN, MS) by a per-unit cost model: waves x sum over channel blocks of
+    // max(MMA issue, filter bytes at ~40 B/clk of the L2 -> SM path per SM).  A 256-wide tile issues
+    // half the MMAs per output but streams 32 KB of filter per 64-channel block per 128 rows; with a
+    // partial last block (k_last < 4) the filter bytes stay while the MMA work shrinks (AlexNet conv2
+    // fprop, 96 channels: 256 x 1 117 us, 128 x 2 faster).  TCB_FORCE_BN / TCB_HALO_MS pin it.
+    const int ncb = p.ncb, k_last = p.k_last;
+    auto unit_cost = [&](int bn_, const HaloGeom& q) {
+        const int n_issue = b_mn ? std::min(bn_, (std::min(N, bn_) + 63) / 64 * 64)
+                                 : std::min(bn_, (std::min(N, bn_) + 15) / 16 * 16);
+        const double mma = std::max(n_issue / 2.0, n_issue / 4.0 + 32.0);  // clk per M = 128, K = 16 MMA
+        const double bytes_clk = bn_ * 128.0 / 40.0;
+        double per_tap = 0;
+        for (int cb = 0; cb < ncb; ++cb) per_tap += std::max(q.ms * (cb == ncb - 1 ? k_last : 4) * mma, bytes_clk);
+        const long long units = static_cast<long long>(nimg) * q.yt * q.xt * ceil_div(N, bn_);
+        return static_cast<double>((units + num_sms() - 1) / num_sms()) * per_tap;
+    };
+    auto fits = [&](int bn_, const HaloGeom& q) {
+        const uint32_t h = (static_cast<uint32_t>(q.hh) * q.wr * 128 + static_cast<uint32_t>(S - 1) * 128 + 1023) & ~1023u;
+        return 2 * h + 3 * bn_ * BK * 2 + 8 * kStagingBytes + 2048 <= 232448;  // >= 3 filter stages
+    };
+    const HaloGeom g2 = halo_geom(Hout, Wout, R, S, 2, g.wr);
+    int bn = 0;
     HaloGeom gm = g;
-    if (bn <= 128 && halo_ms_mode() != 1) {
-        const HaloGeom g2 = halo_geom(Hout, Wout, R, S, 2, g.wr);
-        const int n_issue = b_mn ? std::min(bn, (std::min(N, bn) + 63) / 64 * 64) : std::min(bn, (std::min(N, bn) + 15) / 16 * 16);
-        auto model = [&](const HaloGeom& q) {
-            const long long units = static_cast<long long>(nimg) * q.yt * q.xt * p.tiles_n;
-            const double waves = static_cast<double>((units + num_sms() - 1) / num_sms());
-            return waves * std::max(q.ms * 2.0 * n_issue, bn * 128.0 / 40.0);
-        };
-        const uint32_t h2 = (static_cast<uint32_t>(g2.hh) * g2.wr * 128 + static_cast<uint32_t>(S - 1) * 128 + 1023) & ~1023u;
-        const bool fits = 2 * h2 + 3 * bn * BK * 2 + 8 * kStagingBytes + 2048 <= 232448;  // >= 3 filter stages
-        if (g2.wr && fits && (halo_ms_mode() == 2 || model(g2) < model(g))) gm = g2;
+    double best = 0;
+    for (int cand : {256, 128, 64}) {
+        if (cand == 64 && N > 128) continue;
+        if (cand == 256 && N <= 128) continue;
+        if (forced_bn() && cand != forced_bn()) continue;
+        for (int ms : {1, 2}) {
+            if (ms == 2 && (cand > 128 || !g2.wr || !fits(cand, g2))) continue;
+            if (halo_ms_mode() && ms != halo_ms_mode()) continue;
+            const HaloGeom& q = ms == 2 ? g2 : g;
+            const double c = unit_cost(cand, q);
+            if (!bn || c < best - 1e-9) {
+                best = c;
+                bn = cand;
+                gm = q;
+            }
+        }
     }
+    if (!bn) {  // forced shape outside the candidates
+        bn = forced_bn() ? forced_bn() : N > 128 ? 256 : N > 64 ? 128 : 64;
+        gm = g;
+    }
+    // TCB_HALO_MODEL: 1 the model above everywhere, 2 (default) only for wide N with a partial last
+    // channel block, 0 / 3 the MMA-only choice everywhere (3 also sends such fprops to im2col)
+    const int hm = halo_model_mode();
+    if (hm == 0 || hm == 3 || (hm == 2 && !(N > 128 && k_last < 4))) {
+        bn = N > 128 ? 256 : N > 64 ? 128 : 64;
+        if (N > 128 && N % 256 != 0 && ceil_div(N, 128) * t_kblock(128, 1) < ceil_div(N, 256) * t_kblock(256, 1)) bn = 128;
+        if (forced_bn()) bn = forced_bn();
+        gm = g;
+        if (bn <= 128 && halo_ms_mode() != 1) {
+            const int n_issue = b_mn ? std::min(bn, (std::min(N, bn) + 63) / 64 * 64) : std::min(bn, (std::min(N, bn) + 15) / 16 * 16);
+            auto model = [&](const HaloGeom& q) {
+                const long long units = static_cast<long long>(nimg) * q.yt * q.xt * ceil_div(N, bn);
+                const double waves = static_cast<double>((units + num_sms() - 1) / num_sms());
+                return waves * std::max(q.ms * 2.0 * n_issue, bn * 128.0 / 40.0);
+            };
+            if (g2.wr && fits(bn, g2) && (halo_ms_mode() == 2 || model(g2) < model(g))) gm = g2;
+        }
+    }
+    p.tiles_n = ceil_div(N, bn);
     p.ms = gm.ms;
     p.th = gm.th;
     p.hh = gm.hh;
@@ -1221,6 +1271,8 @@ static HaloGeom halo_log(const char* what, const tc_conv_desc* d, HaloGeom g) {
 static HaloGeom fprop_halo(const tc_conv_desc* d) {
     if (!halo_enabled('f') || d->stride != 1 || d->R * d->S == 1 || d->cs % 8 || d->ks % 8)
         return halo_log("fprop (not eligible)", d, HaloGeom{});
+    if (halo_model_mode() == 3 && d->cs % 64 && d->cs % 32 == 0 && d->K > 128)
+        return halo_log("fprop (im2col32)", d, HaloGeom{});
     return halo_log("fprop", d, halo_geom(d->Ho, d->Wo, d->R, d->S, 1, 0, halo_util_bar(d->cs, d->ks)));
 }
 static HaloGeom dgrad_halo(const tc_conv_desc* d) {
