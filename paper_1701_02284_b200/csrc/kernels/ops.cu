@@ -1582,11 +1582,34 @@ __global__ void __launch_bounds__(256) k_stage_rows(const SRC* __restrict__ x, T
     const int s = 1 << log2_s;
     const int h0 = L.s2d ? r * s - L.pad : r;
     const int C = L.C, W = L.W;
-    for (int ci = 0; ci < C * s; ++ci) {  // tile row (c, i): source row h0 + i of channel c
-        const int c = ci >> log2_s, h = h0 + (ci & (s - 1));
-        const bool ok = h >= 0 && h < L.H;
-        const SRC* src = x + ((static_cast<long long>(n) * C + c) * L.H + h) * W;
-        for (int w = threadIdx.x; w < W; w += blockDim.x) tile[ci * W + w] = ok ? to_f(__ldcs(src + w)) : 0.f;
+    constexpr int VW = 16 / sizeof(SRC);  // source elements per 16-byte load
+    if (W % VW == 0) {
+        // tile row (c, i) = source row h0 + i of channel c; all 16-byte loads of the block in flight
+        const int wv = W / VW, total = C * s * wv;
+#pragma unroll 4
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int ci = idx / wv, w = (idx - ci * wv) * VW;
+            const int c = ci >> log2_s, h = h0 + (ci & (s - 1));
+            float f[VW];
+            if (h >= 0 && h < L.H) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * C + c) * L.H + h) * W + w));
+                const SRC* e = reinterpret_cast<const SRC*>(&v);
+#pragma unroll
+                for (int j = 0; j < VW; ++j) f[j] = to_f(e[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < VW; ++j) f[j] = 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < VW; ++j) tile[ci * W + w + j] = f[j];
+        }
+    } else {
+        for (int ci = 0; ci < C * s; ++ci) {
+            const int c = ci >> log2_s, h = h0 + (ci & (s - 1));
+            const bool ok = h >= 0 && h < L.H;
+            const SRC* src = x + ((static_cast<long long>(n) * C + c) * L.H + h) * W;
+            for (int w = threadIdx.x; w < W; w += blockDim.x) tile[ci * W + w] = ok ? to_f(__ldcs(src + w)) : 0.f;
+        }
     }
     __syncthreads();
     const int log2_cc = 2 * log2_s + log2_cs;  // output channels per output pixel = s*s*cs
@@ -2279,7 +2302,8 @@ tc_status launch_nchw_to_nhwc(const SRC* x, T* y, StageLayout L, cudaStream_t st
     const int wout = L.s2d ? L.Ws : L.W;
     auto log2i = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
     const int lcs = log2i(L.cs), ls = log2i(s);
-    if (smem <= 48 * 1024 && lcs >= 0 && ls >= 0 && (static_cast<long long>(wout) * s * s * L.cs) % 8 == 0) {
+    if (smem <= 48 * 1024 && lcs >= 0 && ls >= 0 && (static_cast<long long>(wout) * s * s * L.cs) % 8 == 0 &&
+        (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
         TCB_LAUNCH((k_stage_rows<T, SRC>), L.N * (L.s2d ? L.Hs : L.H), 256, smem, st, x, y, L, lcs, ls);
         TCB_LAUNCH_CHECK();
         return TC_OK;

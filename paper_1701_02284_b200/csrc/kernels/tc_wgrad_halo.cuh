@@ -68,9 +68,13 @@ __device__ __forceinline__ void wgrad_bias_sums(const WgradHaloParams& p, const 
     uint32_t ph = 0;
     for (int t = tile0; t < tile1; ++t) {
         mbar_wait(&full[s], ph);
-        const uint8_t* src = smem + s * p.stage_bytes + a * (BM * 128) + rg * 128 + ((kc ^ (rg & 7)) << 4);
+        const uint32_t src = smem_u32(smem) + s * p.stage_bytes + a * (BM * 128) + rg * 128 + ((kc ^ (rg & 7)) << 4);
         for (int i = 0; i < 128 / rgs; ++i) {
-            const uint4 v = *reinterpret_cast<const uint4*>(src + i * rgs * 128);
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(src + i * rgs * 128)
+                         : "memory");
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {

@@ -1918,6 +1918,11 @@ tc_status tc_ctx_create(const tc_plan* plan, const tc_ctx_desc* desc, tc_ctx** o
     for (const ParamL& q : c->params) maxc = std::max(maxc, q.K);
     c->max_partials = static_cast<int>(colsum_partials_floats(maxc));
     TCB_CUDA_CHECK(cudaMalloc(&c->ws, std::max<size_t>(c->ws_bytes, 256)));
+    if (const char* e = std::getenv("TCB_POISON"); e && e[0] == '1') {  // debug: NaN-fill scratch, arena, gradients
+        TCB_CUDA_CHECK(cudaMemset(c->ws, 0xFF, std::max<size_t>(c->ws_bytes, 256)));
+        TCB_CUDA_CHECK(cudaMemset(c->arena, 0xFF, std::max<size_t>(c->arena_bytes, 256)));
+        TCB_CUDA_CHECK(cudaMemset(c->grads, 0xFF, static_cast<size_t>(c->grads_n) * 4));
+    }
     TCB_CUDA_CHECK(cudaMalloc(&c->partials, (static_cast<size_t>(c->max_partials) + 3 * maxc + 64) * sizeof(float)));
     // BN backward groups
     {
