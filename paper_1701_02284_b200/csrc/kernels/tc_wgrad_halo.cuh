@@ -83,6 +83,10 @@ __device__ __forceinline__ void wgrad_bias_sums(const WgradHaloParams& p, const 
                 acc[2 * q + 1] += f.y;
             }
         }
+        // generic-proxy reads of a TMA-written stage must be ordered before the async-proxy refill
+        // the release enables (without this fence a refill could land under the last reads: rare
+        // wrong tiles in the sums, seen only with a concurrent side-stream kernel)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (++s == p.stages) {

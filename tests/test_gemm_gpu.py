@@ -290,3 +290,38 @@ def test_conv_fwd_deterministic(case):
         outs.append(y.clone())
     for o in outs[1:]:
         assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
+
+
+@pytest.mark.parametrize("case", [(16, 512, 14, 14, 512, 3, 1, 1), (16, 128, 28, 28, 128, 3, 1, 1),
+                                  (8, 64, 28, 28, 96, 3, 1, 1), (8, 64, 30, 30, 64, 3, 1, 1)])
+def test_wgrad_bias_fold_under_concurrent_load(case):
+    """The folded bias gradient (halo filter-gradient epilogue warps summing the staged dy tiles)
+    equals the fp64 pixel sum of dy to fp32 rounding and is bit-identical across repeated runs
+    while another stream keeps the SMs busy (the stage-release ordering the sums depend on)."""
+    L = nat.lib()
+    L.tcb_test_conv2d_bwd_filter_bias.argtypes = [C.POINTER(nat.ConvDesc)] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
+    x, w, b, d = conv_case(*case, seed=2)
+    g = torch.Generator(device="cpu").manual_seed(6)
+    dy = torch.randn(d.N, d.K, d.Ho, d.Wo, generator=g).to(torch.bfloat16).float().cuda()
+    xs, dys = nhwc_pad(x, d.cs), nhwc_pad(dy, d.ks)
+    ref = dys.double().sum(dim=(0, 1, 2))[: d.K]
+    wsb = L.tc_conv2d_workspace_bytes(C.byref(d), 2)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    dw = torch.empty(d.K, d.R, d.S, d.cs, dtype=torch.float32, device="cuda")
+    s_main, s_noise = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
+    big = torch.randn(32 << 20, device="cuda")
+    outs = []
+    for trial in range(12):
+        db = torch.full((d.K,), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        if trial % 2:
+            with torch.cuda.stream(s_noise):
+                for _ in range(10):
+                    big.mul_(1.0000001)
+        nat.check(L.tcb_test_conv2d_bwd_filter_bias(C.byref(d), dys.data_ptr(), xs.data_ptr(), dw.data_ptr(),
+                                                    db.data_ptr(), ws.data_ptr(), wsb, C.c_void_p(s_main.cuda_stream)))
+        torch.cuda.synchronize()
+        outs.append(db.clone())
+    assert float((outs[0].double() - ref).abs().max() / ref.abs().max()) < 1e-5
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])

@@ -321,7 +321,8 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
 
 @pytest.mark.parametrize("name,batch", [("alexnet", 16), ("vgg16", 2), ("googlenet", 2)])
 def test_wgrad_bias_fold(name, batch, monkeypatch):
-    """Conv bias gradients summed by the halo filter-gradient kernel (TCB_WGRAD_BIAS_FOLD=1) match the separate two-pass column sum to fp32 summation-order error, the filter gradients
+    """Conv bias gradients summed by the halo filter-gradient kernel (TCB_WGRAD_BIAS_FOLD, default
+    on) match the separate two-pass column sum to fp32 summation-order error, the filter gradients
     are bit-identical, and the fold removes launches."""
     runs = []
     for v in ("0", "1"):
