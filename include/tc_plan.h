@@ -138,6 +138,7 @@ typedef struct tc_compile_opts {
     double workspace_cap_mb;            /* < 0: unlimited */
     int greedy_schedule;
     int64_t global_batch;               /* loss cardinality |N| (data parallel: G*B); 0 = batch */
+    int no_cse;                         /* 1: skip common sub-expression elimination */
 } tc_compile_opts;
 
 typedef struct tc_net tc_net;  /* a compiled network (plan producer output) */

@@ -123,7 +123,7 @@ class CompileOpts(C.Structure):
     _fields_ = [
         ("lr", C.c_double), ("momentum", C.c_double), ("decay", C.c_double), ("clip", C.c_double),
         ("mode", C.c_int), ("workspace_cap_mb", C.c_double), ("greedy_schedule", C.c_int),
-        ("global_batch", C.c_int64),
+        ("global_batch", C.c_int64), ("no_cse", C.c_int),
     ]
 
 

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <functional>
 #include <set>
+#include <iomanip>
 #include <sstream>
 #include <unordered_set>
 
@@ -46,6 +47,8 @@ bool match_contraction(const TensorExpr& t, TPtr* a, TPtr* w) {
 
 class Vectorizer {
 public:
+    explicit Vectorizer(bool cse) : cse_(cse) {}
+    int merged() const { return merged_; }
     TPtr run(const TPtr& t) {
         if (!t) return t;
         auto hit = memo_.find(t);
@@ -65,6 +68,7 @@ public:
         } else if (c->kind == TKind::AddT && c->operands[1]->kind == TKind::RowBcast) {
             out = t_prim(PrimOp::BiasAdd, Hyper{}, {c->operands[0], c->operands[1]->operands[0]}, c->rank, c->id);
         }
+        if (cse_) out = canonical(out);
         memo_.emplace(t, out);
         return out;
     }
@@ -83,18 +87,50 @@ public:
     }
 
 private:
+    // cse: operands are already canonical, so syntactic identity is identity of (kind, operator,
+    // hyper-parameters, operand nodes); leaves are keyed by what they denote.
+    TPtr canonical(const TPtr& t) {
+        std::ostringstream k;
+        k << std::setprecision(17);
+        switch (t->kind) {
+            case TKind::Param: k << "P" << t->param.get(); break;
+            case TKind::Input: k << "I" << t->name; break;
+            case TKind::Prim:
+                if (t->prim == PrimOp::DropoutMask) return t;  // randomized: never merged
+                k << "F" << static_cast<int>(t->prim) << ":" << t->rank;
+                break;
+            case TKind::AddT: k << "A" << t->rank; break;
+            case TKind::Concat: k << "C" << t->rank; break;
+            case TKind::Flatten: k << "L" << t->flat_axis; break;
+            case TKind::Reshape: k << "R" << t->reshape_to.to_string(); break;
+            default: return t;  // Copy (each backs its own in-place op), Var, Load, index expressions, grads
+        }
+        const Hyper& h = t->hyper;
+        k << "|" << h.k << "," << h.stride << "," << h.pad << "," << h.max_pool << "," << h.rank << "," << h.rate << ","
+          << h.lrn_size << "," << h.alpha << "," << h.beta << "," << h.transpose_a << "," << h.transpose_b << ","
+          << h.scale << "," << h.classes << "," << h.indicator << "," << h.has_bias << "," << h.eps << "," << h.lrn_k << ","
+          << h.offset << "," << h.extent << "," << h.eltwise << "," << h.out << "|";
+        for (const TPtr& o : t->operands) k << o.get() << ";";
+        auto [it, fresh] = canon_.emplace(k.str(), t);
+        if (!fresh) ++merged_;
+        return it->second;
+    }
+    bool cse_ = false;
+    int merged_ = 0;
+    std::unordered_map<std::string, TPtr> canon_;
     std::unordered_map<TPtr, TPtr> memo_;
     std::unordered_map<SPtr, SPtr> smemo_;
 };
 
 }  // namespace
 
-void vectorize(NetworkDef& net) {
-    Vectorizer v;
+int vectorize(NetworkDef& net, bool cse) {
+    Vectorizer v(cse);
     net.loss = v.run_s(net.loss);
     net.logits_main = v.run(net.logits_main);
     net.x_load = v.run(net.x_load);
     net.y_load = v.run(net.y_load);
+    return v.merged();
 }
 
 // ================================================================ shapes
@@ -555,7 +591,7 @@ std::vector<int> stmt_reads(const IrStmt& s) {
 }
 
 IrProgram compile_network(NetworkDef& net, const CompileOptions& opt) {
-    vectorize(net);
+    vectorize(net, opt.cse);
     ShapeTable st;
     infer_shapes(net, st);
     GradInfo gi = derive_gradients(net, st);

@@ -40,7 +40,10 @@ struct ShapeTable {
 };
 
 // Rewrites FC index patterns into MatMul / BiasAdd (in place on net).
-void vectorize(NetworkDef& net);
+// Contraction / bias-add recognition; with cse, syntactically identical pure nodes (same kind,
+// operator, hyper-parameters and operands) are built once (Copy and the
+// randomized dropout mask are never merged).  Returns the number of nodes merged.
+int vectorize(NetworkDef& net, bool cse = false);
 void infer_shapes(const NetworkDef& net, ShapeTable& st);
 
 struct GradInfo {
@@ -89,6 +92,7 @@ struct CompileOptions {
     MemMode mode = MemMode::Dealloc;
     double workspace_cap_mb = -1.0;
     bool greedy_schedule = false;   // SPEC.md:331 greedy release-most-bytes list scheduler
+    bool cse = true;                // SPEC.md:313-319 common sub-expression elimination
 };
 
 IrProgram compile_network(NetworkDef& net, const CompileOptions& opt);

@@ -388,7 +388,30 @@ void build_inception_block(NetworkDef& net, std::int64_t batch) {
     finish(net);
 }
 
+// A small net with a duplicated sub-expression for the cse pass: the same
+// full layer applied twice to the same hidden activations, the two logits summed.  With cse the
+// second MatMul / BiasAdd pair is the first one (one Let each); without, two identical Lets.
+void build_csedemo(NetworkDef& net, std::int64_t batch) {
+    init_net(net, "csedemo", batch, Shape{batch, 1, 8, 8}, 10);
+    LayerFactory L(net);
+    FunPtr body = L.seq({L.flatten(4, 1), L.full("fc1", 32), L.relu(2)});
+    FunPtr head = L.full("fc2", net.classes);
+    net.x_load = t_load(t_input("X", 4), net.ctx.fresh_id());
+    TPtr h = apply_norm(net, body, net.x_load);
+    TPtr a = apply_norm(net, head, h);
+    TPtr b = apply_norm(net, head, h);
+    Hyper add;
+    add.eltwise = ELT_ADD;
+    TPtr logits = t_prim(PrimOp::Eltwise, add, {a, b}, 2, net.ctx.fresh_id());
+    TPtr s = apply_norm(net, L.softmax(), logits);
+    net.logits_main = logits;
+    net.y_load = t_load_indicator(t_input("Y", 1), net.classes, net.ctx.fresh_id());
+    net.loss = L.log_loss(s, 1.0, "");
+    finish(net);
+}
+
 void build_by_name(NetworkDef& net, const std::string& name, std::int64_t batch) {
+    if (name == "csedemo") return build_csedemo(net, batch);
     if (name == "lenet") return build_lenet(net, batch);
     if (name == "alexnet") return build_alexnet(net, batch);
     if (name == "vgg16") return build_vgg16(net, batch);

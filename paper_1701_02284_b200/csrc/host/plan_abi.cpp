@@ -208,6 +208,7 @@ void apply_opts(CompileOptions& co, const tc_compile_opts* opts) {
     co.mode = opts->mode == TC_MODE_REUSE ? MemMode::Reuse : MemMode::Dealloc;
     co.workspace_cap_mb = opts->workspace_cap_mb;
     co.greedy_schedule = opts->greedy_schedule != 0;
+    co.cse = opts->no_cse == 0;
 }
 
 // Gradient derivation + IR pipeline + memplan of an elaborated network, flattened to tc_plan.

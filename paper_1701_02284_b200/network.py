@@ -42,12 +42,12 @@ class CompiledNetwork:
 
     def __init__(self, name: str, batch: int, *, lr: float = 0.01, momentum: float = 0.9, decay: float = 0.0005,
                  clip: float = 0.0, mode: str = "dealloc", workspace_cap_mb: float = -1.0, greedy: bool = False,
-                 global_batch: int = 0, spec: str | None = None, solver_from_spec: bool = False):
+                 global_batch: int = 0, spec: str | None = None, solver_from_spec: bool = False, cse: bool = True):
         L = nat.lib()
         opts = nat.CompileOpts(lr=lr, momentum=momentum, decay=decay, clip=clip,
                                mode=nat.TC_MODE_REUSE if mode == "reuse" else nat.TC_MODE_DEALLOC,
                                workspace_cap_mb=workspace_cap_mb, greedy_schedule=int(greedy),
-                               global_batch=global_batch)
+                               global_batch=global_batch, no_cse=0 if cse else 1)
         h = C.c_void_p()
         if spec is None:
             nat.check(L.tc_net_compile(name.encode(), batch, C.byref(opts), C.byref(h)))

@@ -1,6 +1,7 @@
 """Plan producers: shape rules, gradient derivation shape
 (SPEC.md:206), IR verifier (acceptance 4), update formation
  and the flattened plan crossing the C ABI."""
+import numpy as np
 import pytest
 
 from paper_1701_02284_b200 import _native as nat
@@ -89,3 +90,34 @@ def test_compile_error_unknown_network():
     with pytest.raises(nat.TcError) as e:
         compile_network("nosuchnet", 2)
     assert "UnboundName" in str(e.value)
+
+
+def test_cse_merges_duplicate_subexpressions():
+    """SPEC.md:313-319 cse: the same full layer applied twice to the same activations compiles to
+    one MatMul / BiasAdd Let pair (statement-count oracle), the built-in networks (no duplicates)
+    are unchanged, `.copy` operands are never merged (both Log S.copy and 1/(S.copy) remain), and
+    the merged program computes the same loss and gradients (value oracle, CPU)."""
+    from oracle import oracle as orc
+
+    with_cse = compile_network("csedemo", 4)
+    without = compile_network("csedemo", 4, cse=False)
+
+    def lets(net, op):
+        return sum(1 for s in net.stmts if s.kind == nat.TC_STMT_LET and nat.OP_NAMES[s.op] == op)
+
+    assert lets(without, "MATMUL_FWD") == 3 and lets(with_cse, "MATMUL_FWD") == 2
+    assert lets(without, "BIAS_ADD") == 3 and lets(with_cse, "BIAS_ADD") == 2
+    texts = [with_cse.stmt_text(i) for i in range(len(with_cse.stmts))]
+    assert any("Log X" in t and ".copy" in t for t in texts) and any("1/(X" in t and ".copy" in t for t in texts)
+    for name in ("lenet", "alexnet"):
+        assert len(compile_network(name, 2).stmts) == len(compile_network(name, 2, cse=False).stmts)
+    results = []
+    for net in (with_cse, without):
+        o = orc.Oracle(net, seed=5)
+        o.init_params()
+        x, y = orc.synth_batch(net, 5, 0)
+        o.set_batch(x, y)
+        results.append((o.step(0, update=False), [o.grad(i) for i in range(len(net.params))]))
+    assert abs(results[0][0] - results[1][0]) <= 1e-6 * abs(results[1][0])
+    for a, b in zip(results[0][1], results[1][1]):
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-7)
