@@ -485,10 +485,14 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (p.trans_out && d_bf16) return fail(TC_INVALID_ARG, "transposed GEMM output needs fp32");
     if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
+    if (p.bias_out && (lp.cg != 1 || p.a_mode != OP_TMA_MN || p.trans_out))
+        return fail(TC_INVALID_ARG, "GEMM bias fold needs single-CTA tiles and an MN-major TMA A operand");
     if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
-        if (!ws || ws_bytes < need)
+        const size_t bias_off = (need + 255) & ~static_cast<size_t>(255);
+        if (!ws || ws_bytes < (p.bias_out ? bias_off + static_cast<size_t>(lp.splits) * p.M * sizeof(float) : need))
             return fail(TC_INVALID_ARG, "split-K workspace too small: need " + std::to_string(need) + " bytes");
+        if (p.bias_out) p.bias_ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + bias_off);
         p.epi = EPI_F32;
         p.bias = nullptr;
         p.relu = 0;
@@ -498,7 +502,9 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
         p.epi = EPI_SGD;
         p.bias = nullptr;
         p.relu = 0;
+        p.bias_ws = p.bias_out;
     } else {
+        p.bias_ws = p.bias_out;  // unsplit: the column sums are final
         p.epi = d_bf16 ? EPI_BF16 : EPI_F32;
         p.bias = bias;
         p.n_bias = n_bias;
@@ -527,7 +533,8 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (s != TC_OK) return s;
     if (partial)
         return launch_splitk_reduce(static_cast<const float*>(ws), lp.splits, p.M, p.N, static_cast<long long>(p.M) * p.N,
-                                    D, ldd, d_bf16, bias, n_bias, relu, beta, p.trans_out, 0, 0, st);
+                                    D, ldd, d_bf16, bias, n_bias, relu, beta, p.trans_out, 0, 0, st,
+                                    p.bias_out ? p.bias_ws : nullptr, p.bias_out);
     return TC_OK;
 }
 
@@ -1151,7 +1158,9 @@ unsigned long long tc_kernel_launch_count(void) { return tcb::g_launches.load();
 size_t tc_gemm_workspace_bytes(const tc_gemm_args* a) {
     if (!a) return 0;
     LaunchPlan lp = plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true);
-    return (lp.splits > 1 || a->beta != 0.f) ? static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float) : 0;
+    if (!(lp.splits > 1 || a->beta != 0.f)) return 0;
+    const size_t main = static_cast<size_t>(lp.splits) * a->M * a->N * sizeof(float);
+    return ((main + 255) & ~static_cast<size_t>(255)) + static_cast<size_t>(lp.splits) * a->M * sizeof(float);  // + bias partials
 }
 
 tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) { return tcb::gemm_args_ex(a, nullptr, stream); }
@@ -1161,10 +1170,12 @@ tc_status tc_gemm_bf16(const tc_gemm_args* a, void* stream) { return tcb::gemm_a
 namespace tcb {
 // tc_gemm_bf16, optionally with the momentum update of `sgd` fused into the epilogue (the
 // contraction is then the parameter's gradient: M x N = the parameter, unsplit, never stored)
-tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream) {
+tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream, float* bias_out) {
     if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0) return fail(TC_INVALID_ARG, "tc_gemm_bf16: bad shape");
+    if (bias_out && !gemm_bias_foldable(a)) return fail(TC_INVALID_ARG, "GEMM bias fold not available here");
     GemmParams p;
     init_params(p);
+    p.bias_out = bias_out;
     p.M = a->M;
     p.N = a->N;
     p.K = a->K;
@@ -1341,7 +1352,9 @@ size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     const bool swap = which == 2 && wgrad_swap(d);  // the transposed write goes through the reduce
     if (lp.splits <= 1 && !swap) return 0;
     long long M = which == 2 ? d->K : 0, N = which == 2 ? static_cast<long long>(d->R) * d->S * d->cs : 0;
-    return static_cast<size_t>(std::max(1, lp.splits)) * M * N * sizeof(float);
+    const size_t main = static_cast<size_t>(std::max(1, lp.splits)) * M * N * sizeof(float);
+    // + the folded bias partials [splits][M] behind them (conv_bwd_filter_ex with dbias)
+    return ((main + 255) & ~static_cast<size_t>(255)) + static_cast<size_t>(std::max(1, lp.splits)) * M * sizeof(float);
 }
 
 }  // extern "C"
@@ -1474,7 +1487,15 @@ namespace tcb {
 bool wgrad_bias_foldable(const tc_conv_desc* d) {
     const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");  // 0 disables (read at plan time)
     if ((e && e[0] == '0') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
-    return wgrad_halo_plan(d).ok;
+    if (wgrad_halo_plan(d).ok) return true;
+    // the generic implicit-GEMM filter gradient: dy is its MN-major TMA A operand (not the
+    // swapped form, where dy is B), single-CTA tiles
+    return !wgrad_swap(d) && conv_plan(d, 2).cg == 1;
+}
+bool gemm_bias_foldable(const tc_gemm_args* a) {
+    const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");
+    if ((e && e[0] == '0') || !a || a->a_layout != TC_LAYOUT_MN) return false;
+    return plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true).cg == 1;
 }
 
 tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* x, float* dw, float* dbias, void* ws,
@@ -1517,6 +1538,7 @@ tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* 
                         static_cast<cudaStream_t>(stream));
     }
     p.a_mode = OP_TMA_MN;
+    p.bias_out = dbias;
     if (!make_tmap_2d_bf16(&p.tmA, dy, d->ks, npix, d->ks, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
     if (is_pointwise(d)) {
         p.b_mode = OP_TMA_MN;

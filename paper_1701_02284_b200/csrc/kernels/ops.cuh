@@ -157,7 +157,10 @@ tc_status launch_sgd(const SgdTensor* ts, int nt, SgdTensor* dev_scratch, cudaSt
 tc_status launch_clip_scale(const SgdTensor* ts, int nt, float clip, double* partials, float* scale, cudaStream_t st);
 size_t clip_partials_doubles(int nt);
 // tc_gemm_bf16 with the momentum update of `sgd` (may be null) fused into the epilogue
-tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream);
+// bias_out: also the column sums of the MN-major A operand over k (the bias gradient of a weight
+// gradient whose A is dy), when gemm_bias_foldable(a)
+tc_status gemm_args_ex(const tc_gemm_args* a, const SgdTensor* sgd, void* stream, float* bias_out = nullptr);
+bool gemm_bias_foldable(const tc_gemm_args* a);
 
 // fp32 parity mode: bf16 operand splits (see ops.cu).  kSplitN copies per operand; the part
 // (0 hi, 1 mid, 2 lo) of copy j is (parts >> 2j) & 3.  A-side and B-side part lists pair up as

@@ -95,6 +95,11 @@ struct GemmParams {
     int i2c_lo_w, i2c_lo_h;  // first source pixel of output pixel (y, x) = (y * stride + lo_h, x * stride + lo_w)
     int i2c_flip;            // bwd-data: tap (kh, kw) is the offset (R-1-kh, S-1-kw)
     int i2c_P, i2c_Q;        // pixel grid the rows (A) / k-blocks (B) walk: P x Q per image
+    // Folded bias gradient (CG = 1, MN-major TMA A: filter / FC-weight gradients, A = dy): warps
+    // 2-3 sum every staged A tile of the units in column tile 0 over k and write the per-split
+    // column sums bias_ws[split][M] (the final bias gradient when unsplit).  bias_out: host side.
+    float* bias_ws;
+    float* bias_out;
 };
 
 constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         tma_prefetch(&p.tmD);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1 + (any_gather ? 128 : 0));
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 1 + (p.bias_ws != nullptr ? 2 : 0));  // + the bias warps 2-3
         }
         for (int b = 0; b < NACC; ++b) {
             mbar_init(&tfull[b], 1);
@@ -673,6 +678,59 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                     umma_bf16_elect<CG>(d_tmem, a_s + a_koff[k], b_s + b_koff[k], idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
                 umma_commit_elect<CG>(&empty[s]);
                 if (kb == w.kb1 - 1) umma_commit_elect<CG>(&tfull[buf]);
+            }
+        }
+    } else if ((warp == 2 || warp == 3) && CG == 1 && p.bias_ws != nullptr) {
+        // ---------------- folded bias gradient: warp 2 / 3 sums A atom 0 / 1 (64 rows of M each)
+        // of every stage over its 64 k rows; lane = (row group rg, 16-byte chunk kc), rows
+        // rg + 4 i, so the row groups combine with two xor shuffles in a fixed order
+        const int a = warp - 2, kc = lane & 7, rg = lane >> 3;
+        int it = 0;
+        for (int u = pair; u < p.units; u += npairs) {
+            const Unit w = decode_unit(p, u);
+            const bool need = w.nt == 0;
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                const int s = it % S;
+                mbar_wait(&full[s], (it / S) & 1);
+                if (need) {
+                    const uint32_t base = smem_u32(sA + s * Cfg::kABytes + a * BK * 128);
+#pragma unroll 4
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = rg + 4 * i;
+                        uint4 v;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                     : "r"(base + r * 128 + ((kc ^ (r & 7)) << 4))
+                                     : "memory");
+                        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float2 f = __bfloat1622float2(h[q]);
+                            acc[2 * q] += f.x;
+                            acc[2 * q + 1] += f.y;
+                        }
+                    }
+                }
+                fence_proxy_async_smem();  // generic reads before the async-proxy refill (see wgrad_bias_sums)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (need) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
+                    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+                }
+                if (rg == 0) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int m = w.mt * BM + a * 64 + kc * 8 + j;
+                        if (m < p.M) p.bias_ws[static_cast<long long>(w.sp) * p.M + m] = acc[j];
+                    }
+                }
             }
         }
     } else if (warp >= 8 && any_gather) {

@@ -1163,11 +1163,17 @@ tc_status compute_param_grad(tc_ctx* c, int idx, int pidx, float* g) {
             ga.ldd = q.in_dev;
             ga.d_dtype = TC_DTYPE_F32;
             ga.alpha = 1.f;
+            const int bp = c->wgrad_bias_param[idx];  // folded FC bias gradient (column sums of dy)
             if (c->fuse_sgd_active && c->sgd_fused[pidx]) {  // update fused into the epilogue
                 const SgdTensor t = sgd_tensor(c, pidx);
                 ga.workspace = c->ws;
                 ga.workspace_bytes = c->ws_bytes;
-                return gemm_args_ex(&ga, &t, c->st);
+                return gemm_args_ex(&ga, &t, c->st, bp >= 0 ? c->params[bp].g : nullptr);
+            }
+            if (bp >= 0) {
+                ga.workspace = c->ws;
+                ga.workspace_bytes = c->ws_bytes;
+                return gemm_args_ex(&ga, nullptr, c->st, c->params[bp].g);
             }
             return run_gemm_args(c, ga);
         }
@@ -1596,16 +1602,31 @@ void plan_bias_fold(tc_ctx* c) {
     Ptrs P{c};
     for (int i = 0; i < p->nstmts; ++i) {
         const tc_stmt& b = p->stmts[i];
-        if (b.kind != TC_STMT_UPDATE || b.op != TC_OP_CONV_BWD_BIAS || b.in[0].kind != TC_REF_VAR) continue;
+        const bool conv_bias = b.op == TC_OP_CONV_BWD_BIAS, fc_bias = b.op == TC_OP_BIAS_GRAD;
+        if (b.kind != TC_STMT_UPDATE || !(conv_bias || fc_bias) || b.in[0].kind != TC_REF_VAR) continue;
         for (int j = 0; j < p->nstmts; ++j) {
             const tc_stmt& f = p->stmts[j];
-            if (f.kind != TC_STMT_UPDATE || f.op != TC_OP_CONV_BWD_FILTER || f.in[0].kind != TC_REF_VAR ||
-                f.in[0].index != b.in[0].index || c->wgrad_bias_param[j] >= 0)
+            if (f.kind != TC_STMT_UPDATE || f.op != (conv_bias ? TC_OP_CONV_BWD_FILTER : TC_OP_MATMUL_BWD_W) ||
+                f.in[0].kind != TC_REF_VAR || f.in[0].index != b.in[0].index || c->wgrad_bias_param[j] >= 0)
                 continue;
             const ParamL& w = c->params[f.param];
             if (c->params[b.param].K != w.K) continue;
-            const tc_conv_desc d = conv_desc(P.L(f.in[1]), w, P.L(f.in[0]), f);
-            if (!wgrad_bias_foldable(&d)) continue;
+            if (conv_bias) {
+                const tc_conv_desc d = conv_desc(P.L(f.in[1]), w, P.L(f.in[0]), f);
+                if (!wgrad_bias_foldable(&d)) continue;
+            } else {
+                // the FC filter gradient's GEMM view (compute_param_grad): M = out features,
+                // N = in features, K = batch, A = dy MN-major
+                const VarL& up = P.L(f.in[0]);
+                tc_gemm_args ga{};
+                ga.M = w.K;
+                ga.N = w.in_dev;
+                ga.K = up.N;
+                ga.a_layout = TC_LAYOUT_MN;
+                ga.b_layout = TC_LAYOUT_MN;
+                ga.d_dtype = TC_DTYPE_F32;
+                if (up.cs < w.K || !gemm_bias_foldable(&ga)) continue;
+            }
             if (i < j) {  // bucket flushes at statements i .. j-1 move to just before j's own, in order
                 std::vector<int> moved;
                 for (int k = i; k < j; ++k) {
