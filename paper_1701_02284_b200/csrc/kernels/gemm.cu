@@ -216,7 +216,7 @@ __device__ __forceinline__ float sum_bias_partials(const float* __restrict__ b, 
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, long long split_stride,
                                      void* out, long long ldd, int out_bf16, const float* __restrict__ bias,
                                      int n_bias, int relu, float beta, int trans, int seg_in, int seg_out,
-                                     const float* __restrict__ bias_ws, float* __restrict__ bias_out) {
+                                     const float* __restrict__ bias_ws, float* __restrict__ bias_out, int bias_by_col) {
     pdl_wait();
     pdl_trigger();
     const long long total = static_cast<long long>(M) * N;
@@ -226,7 +226,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
         const int n = static_cast<int>(i - static_cast<long long>(m) * N);
         const long long src =
             seg_out ? static_cast<long long>(m) * (N / seg_out) * seg_in + (n / seg_out) * seg_in + n % seg_out : i;
-        if (bias_out && n == 0) bias_out[m] = sum_bias_partials(bias_ws, splits, M, m);
+        if (bias_out && (bias_by_col ? m == 0 : n == 0))
+            bias_out[bias_by_col ? n : m] = sum_bias_partials(bias_ws, splits, bias_by_col ? N : M, bias_by_col ? n : m);
         float acc = 0.f;
         int s = 0;
         for (; s + 8 <= splits; s += 8) {  // 8 loads in flight, added in split order (bit-identical)
@@ -307,11 +308,11 @@ __global__ void splitk_reduce4_kernel(const float* __restrict__ ws, int splits, 
 static tc_status launch_splitk_reduce(const float* ws, int splits, int M, int N, long long split_stride, void* out,
                                       long long ldd, int out_bf16, const float* bias, int n_bias, int relu, float beta,
                                       int trans, int seg_in, int seg_out, cudaStream_t st,
-                                      const float* bias_ws = nullptr, float* bias_out = nullptr) {
+                                      const float* bias_ws = nullptr, float* bias_out = nullptr, int bias_by_col = 0) {
     const char* e = std::getenv("TCB_REDUCE4");  // 0: scalar form only (A/B, bit-identity test)
     const bool vec_on = !(e && e[0] == '0');
     // (small outputs keep the scalar form: 4x the threads hide more latency than 16-byte loads save)
-    const bool vec = vec_on && !trans && static_cast<long long>(M) * N >= 4LL * 256 * num_sms() && N % 4 == 0 && ldd % 4 == 0 && split_stride % 4 == 0 && seg_in % 4 == 0 &&
+    const bool vec = vec_on && !trans && !bias_by_col && static_cast<long long>(M) * N >= 4LL * 256 * num_sms() && N % 4 == 0 && ldd % 4 == 0 && split_stride % 4 == 0 && seg_in % 4 == 0 &&
                      seg_out % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(out) & (out_bf16 ? 7 : 15)) == 0;
     const long long total = static_cast<long long>(M) * N / (vec ? 4 : 1);
@@ -321,7 +322,7 @@ static tc_status launch_splitk_reduce(const float* ws, int splits, int M, int N,
                    n_bias, relu, beta, seg_in, seg_out, bias_ws, bias_out);
     else
         TCB_LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, ws, splits, M, N, split_stride, out, ldd, out_bf16, bias,
-                   n_bias, relu, beta, trans, seg_in, seg_out, bias_ws, bias_out);
+                   n_bias, relu, beta, trans, seg_in, seg_out, bias_ws, bias_out, bias_by_col);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -485,12 +486,15 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (p.trans_out && d_bf16) return fail(TC_INVALID_ARG, "transposed GEMM output needs fp32");
     if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
-    if (p.bias_out && (lp.cg != 1 || p.a_mode != OP_TMA_MN || p.trans_out))
-        return fail(TC_INVALID_ARG, "GEMM bias fold needs single-CTA tiles and an MN-major TMA A operand");
+    if (p.bias_out && !p.bias_src) p.bias_src = 1;
+    if (p.bias_out && (lp.cg != 1 || (p.bias_src == 1 && (p.a_mode != OP_TMA_MN || p.trans_out)) ||
+                       (p.bias_src == 2 && (p.b_mode != OP_TMA_MN || lp.bn > 128))))
+        return fail(TC_INVALID_ARG, "GEMM bias fold needs single-CTA tiles and an MN-major TMA dy operand");
+    const long long bias_len = p.bias_src == 2 ? p.N : p.M;
     if (partial) {
         const size_t need = static_cast<size_t>(lp.splits) * p.M * p.N * sizeof(float);
         const size_t bias_off = (need + 255) & ~static_cast<size_t>(255);
-        if (!ws || ws_bytes < (p.bias_out ? bias_off + static_cast<size_t>(lp.splits) * p.M * sizeof(float) : need))
+        if (!ws || ws_bytes < (p.bias_out ? bias_off + static_cast<size_t>(lp.splits) * bias_len * sizeof(float) : need))
             return fail(TC_INVALID_ARG, "split-K workspace too small: need " + std::to_string(need) + " bytes");
         if (p.bias_out) p.bias_ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + bias_off);
         p.epi = EPI_F32;
@@ -520,7 +524,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     const int ring = lp.bn == 256 ? TileCfg<256, 1>::kStages : lp.bn == 128 ? TileCfg<128, 1>::kStages
                                                                              : TileCfg<64, 1>::kStages;
     p.b_resident = resident_on && lp.cg == 1 && p.tiles_n == 1 && lp.splits == 1 && lp.num_kb <= ring &&
-                   (p.b_mode == OP_TMA_K || p.b_mode == OP_TMA_MN);
+                   (p.b_mode == OP_TMA_K || p.b_mode == OP_TMA_MN) && !(p.bias_out && p.bias_src == 2);
     tc_status s;
     if (lp.cg == 2)
         s = lp.bn == 256 ? launch_bn<256, 2>(p, p.units, st) : launch_bn<128, 2>(p, p.units, st);
@@ -534,7 +538,7 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (partial)
         return launch_splitk_reduce(static_cast<const float*>(ws), lp.splits, p.M, p.N, static_cast<long long>(p.M) * p.N,
                                     D, ldd, d_bf16, bias, n_bias, relu, beta, p.trans_out, 0, 0, st,
-                                    p.bias_out ? p.bias_ws : nullptr, p.bias_out);
+                                    p.bias_out ? p.bias_ws : nullptr, p.bias_out, p.bias_src == 2);
     return TC_OK;
 }
 
@@ -1354,7 +1358,8 @@ size_t tc_conv2d_workspace_bytes(const tc_conv_desc* d, int which) {
     long long M = which == 2 ? d->K : 0, N = which == 2 ? static_cast<long long>(d->R) * d->S * d->cs : 0;
     const size_t main = static_cast<size_t>(std::max(1, lp.splits)) * M * N * sizeof(float);
     // + the folded bias partials [splits][M] behind them (conv_bwd_filter_ex with dbias)
-    return ((main + 255) & ~static_cast<size_t>(255)) + static_cast<size_t>(std::max(1, lp.splits)) * M * sizeof(float);
+    return ((main + 255) & ~static_cast<size_t>(255)) +
+           static_cast<size_t>(std::max(1, lp.splits)) * std::max<long long>(M, N) * sizeof(float);
 }
 
 }  // extern "C"
@@ -1490,7 +1495,9 @@ bool wgrad_bias_foldable(const tc_conv_desc* d) {
     if (wgrad_halo_plan(d).ok) return true;
     // the generic implicit-GEMM filter gradient: dy is its MN-major TMA A operand (not the
     // swapped form, where dy is B), single-CTA tiles
-    return !wgrad_swap(d) && conv_plan(d, 2).cg == 1;
+    const LaunchPlan lp = conv_plan(d, 2);
+    if (wgrad_swap(d)) return lp.cg == 1 && lp.bn <= 128;  // swapped: dy is the MN-major B operand
+    return lp.cg == 1;
 }
 bool gemm_bias_foldable(const tc_gemm_args* a) {
     const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");
@@ -1521,6 +1528,8 @@ tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* 
         p.N = d->K;
         p.trans_out = 1;
         p.b_mode = OP_TMA_MN;  // dy rows: Cout contiguous per pixel
+        p.bias_out = dbias;
+        p.bias_src = 2;
         if (!make_tmap_2d_bf16(&p.tmB, dy, d->ks, npix, d->ks, 64, BK, &err)) return fail(TC_INVALID_ARG, err);
         if (is_pointwise(d)) {
             p.a_mode = OP_TMA_MN;

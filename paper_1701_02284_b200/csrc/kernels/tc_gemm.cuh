@@ -100,6 +100,7 @@ struct GemmParams {
     // column sums bias_ws[split][M] (the final bias gradient when unsplit).  bias_out: host side.
     float* bias_ws;
     float* bias_out;
+    int bias_src;  // 1: column sums of A (index m, length M); 2: of the MN-major TMA B (index n, length N)
 };
 
 constexpr int BK = 64;  // bf16 elements per k-block = one 128-byte swizzle row
@@ -685,10 +686,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
         // of every stage over its 64 k rows; lane = (row group rg, 16-byte chunk kc), rows
         // rg + 4 i, so the row groups combine with two xor shuffles in a fixed order
         const int a = warp - 2, kc = lane & 7, rg = lane >> 3;
+        const bool from_b = p.bias_src == 2;
+        const int natoms = from_b ? Cfg::kBNL / 64 : BM / 64;  // B: host keeps BN <= 128
+        const int len = from_b ? p.N : p.M;
         int it = 0;
         for (int u = pair; u < p.units; u += npairs) {
             const Unit w = decode_unit(p, u);
-            const bool need = w.nt == 0;
+            const bool need = (from_b ? w.mt == 0 : w.nt == 0) && a < natoms;
             float acc[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = 0.f;
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 const int s = it % S;
                 mbar_wait(&full[s], (it / S) & 1);
                 if (need) {
-                    const uint32_t base = smem_u32(sA + s * Cfg::kABytes + a * BK * 128);
+                    const uint32_t base = smem_u32((from_b ? sB + s * Cfg::kBBytes : sA + s * Cfg::kABytes) + a * BK * 128);
 #pragma unroll 4
                     for (int i = 0; i < 16; ++i) {
                         const int r = rg + 4 * i;
@@ -727,8 +731,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 if (rg == 0) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int m = w.mt * BM + a * 64 + kc * 8 + j;
-                        if (m < p.M) p.bias_ws[static_cast<long long>(w.sp) * p.M + m] = acc[j];
+                        const int m = (from_b ? w.nt * BN : w.mt * BM) + a * 64 + kc * 8 + j;
+                        if (m < len) p.bias_ws[static_cast<long long>(w.sp) * len + m] = acc[j];
                     }
                 }
             }
