@@ -144,9 +144,11 @@ __global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __res
     }
 }
 
+// relu_y (may be null): a folded in-place ReLU backward behind the dropout backward product,
+// y *= [relu_y > 0] (relu_y is the forward ReLU output)
 template <typename T>
 __global__ void k_mask_mul(const T* __restrict__ x, const uint2* __restrict__ keep, float scale, T* __restrict__ y,
-                           long long n8) {
+                           long long n8, const T* __restrict__ relu_y) {
     pdl_wait();
     pdl_trigger();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
@@ -157,7 +159,52 @@ __global__ void k_mask_mul(const T* __restrict__ x, const uint2* __restrict__ ke
         const uint8_t* mb = reinterpret_cast<const uint8_t*>(&m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = mb[j] ? f[j] * scale : 0.f;
+        if (relu_y) {
+            float r[8];
+            ld8(relu_y + i * 8, r);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (!(r[j] > 0.f)) f[j] = 0.f;
+        }
         st8(y + i * 8, f);
+    }
+}
+
+// Dropout forward in one pass: the keep mask of k_dropout_mask (same Philox stream, element by
+// element) written for the backward, and y = x * keep * scale.
+template <typename T>
+__global__ void k_dropout_apply(const T* __restrict__ x, uint8_t* __restrict__ keep, T* __restrict__ y, int N, int H,
+                                int W, int C, int cs, float rate, float scale, uint64_t seed, uint32_t var,
+                                const uint32_t* iter_n0) {
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t iter = iter_n0[0], n0 = iter_n0[1];
+    const long long n8 = static_cast<long long>(N) * H * W * cs / 8;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n8;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i0 = q * 8;
+        const int c0 = static_cast<int>(i0 % cs);  // cs % 8 == 0: the 8 elements share the pixel
+        long long pix = i0 / cs;
+        const int w = static_cast<int>(pix % W);
+        pix /= W;
+        const int h = static_cast<int>(pix % H);
+        const int n = static_cast<int>(pix / H);
+        float f[8];
+        ld8(x + i0, f);
+        uint8_t kb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = c0 + j;
+            uint8_t k = 0;
+            if (c < C) {
+                const uint32_t e = static_cast<uint32_t>((static_cast<long long>(c) * H + h) * W + w);
+                k = tcp_dropout_value(seed, var, n0 + n, iter, e, rate) != 0.f;
+            }
+            kb[j] = k;
+            f[j] = k ? f[j] * scale : 0.f;
+        }
+        *reinterpret_cast<uint2*>(keep + i0) = *reinterpret_cast<const uint2*>(kb);
+        st8(y + i0, f);
     }
 }
 
@@ -1934,11 +1981,26 @@ tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaSt
     return TC_OK;
 }
 template <typename T>
-tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st) {
-    TCB_LAUNCH(k_mask_mul<T>, EW_GRID(n / 8), x, reinterpret_cast<const uint2*>(keep), scale, y, n / 8);
+tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st,
+                          const T* relu_y) {
+    TCB_LAUNCH(k_mask_mul<T>, EW_GRID(n / 8), x, reinterpret_cast<const uint2*>(keep), scale, y, n / 8, relu_y);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
+template <typename T>
+tc_status launch_dropout_apply(const T* x, uint8_t* keep, T* y, int N, int H, int W, int C, int cs, float rate,
+                               uint64_t seed, uint32_t var, const uint32_t* iter_n0, cudaStream_t st) {
+    if (cs % 8) return fail(TC_INVALID_ARG, "dropout apply: channel stride must be a multiple of 8");
+    const long long n = static_cast<long long>(N) * H * W * cs;
+    TCB_LAUNCH(k_dropout_apply<T>, EW_GRID(n / 8), x, keep, y, N, H, W, C, cs, rate, 1.f / (1.f - rate), seed, var,
+               iter_n0);
+    TCB_LAUNCH_CHECK();
+    return TC_OK;
+}
+template tc_status launch_dropout_apply<bf16>(const bf16*, uint8_t*, bf16*, int, int, int, int, int, float, uint64_t,
+                                              uint32_t, const uint32_t*, cudaStream_t);
+template tc_status launch_dropout_apply<float>(const float*, uint8_t*, float*, int, int, int, int, int, float, uint64_t,
+                                               uint32_t, const uint32_t*, cudaStream_t);
 tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st) {
     const long long n = static_cast<long long>(N) * H * W * cs;
@@ -2403,7 +2465,7 @@ tc_status launch_split_rskc(const float* p, long long ld, int K, int RS, int cs,
 template tc_status launch_relu_fwd<bf16>(const bf16*, bf16*, long long, cudaStream_t);
 template tc_status launch_relu_bwd<bf16>(const bf16*, const bf16*, bf16*, long long, cudaStream_t);
 template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t);
-template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t);
+template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t, const bf16*);
 template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int,
                                          const bf16*, cudaStream_t);
@@ -2427,7 +2489,7 @@ template tc_status launch_synth_batch<bf16>(bf16*, int32_t*, StageLayout, int, u
 template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaStream_t);
 template tc_status launch_relu_bwd<float>(const float*, const float*, float*, long long, cudaStream_t);
 template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t);
-template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t);
+template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t, const float*);
 template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int,
                                          const float*, cudaStream_t);

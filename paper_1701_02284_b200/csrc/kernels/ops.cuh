@@ -34,7 +34,12 @@ template <typename T>
 tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st);
 // y = x * keep * scale (inverted dropout; keep is a 0/1 byte mask)
 template <typename T>
-tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st);
+tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st,
+                          const T* relu_y = nullptr);
+// mask + product in one pass (the DropoutMask statement folded into its forward product)
+template <typename T>
+tc_status launch_dropout_apply(const T* x, uint8_t* keep, T* y, int N, int H, int W, int C, int cs, float rate,
+                               uint64_t seed, uint32_t var, const uint32_t* iter_n0, cudaStream_t st);
 // keep[n, e] for every stored element; e = NCHW element index within the sample (tc_philox.h)
 tc_status launch_dropout_mask(uint8_t* keep, int N, int H, int W, int C, int cs, float rate, uint64_t seed,
                               uint32_t var, const uint32_t* iter_n0, cudaStream_t st);

@@ -216,6 +216,7 @@ struct tc_ctx {
     std::vector<uint8_t> fuse_bias, fuse_relu;      // producer flags
     std::vector<int> fuse_bias_param;
     std::vector<int> fuse_mask_var;                 // data-gradient producer: ReLU output var folded in (-1)
+    std::vector<int> dropout_apply;                 // forward dropout product: its DropoutMask statement, folded in (-1)
     std::vector<int> fuse_add_res, fuse_add_out;    // BN forward: folded residual add (other operand, output var)
     std::vector<char> sgd_fused;                    // per param: momentum update fused into its FC filter gradient
     // bias gradient folded into the halo filter-gradient kernel of the same conv (bf16 mode):
@@ -594,6 +595,7 @@ void plan_fusion(tc_ctx* c) {
     c->fuse_relu.assign(p->nstmts, 0);
     c->fuse_bias_param.assign(p->nstmts, -1);
     c->fuse_mask_var.assign(p->nstmts, -1);
+    c->dropout_apply.assign(p->nstmts, -1);
     c->pool_flag_nonpos.assign(p->nstmts, 0);
     c->fuse_add_res.assign(p->nstmts, -1);
     c->fuse_add_out.assign(p->nstmts, -1);
@@ -613,7 +615,11 @@ void plan_fusion(tc_ctx* c) {
         if (s.kind != TC_STMT_LET) continue;
         const bool gemm_fold = env_on("TCB_GEMM_RELU_FOLD");
         const bool gemm = s.op == TC_OP_CONV_BWD_DATA || s.op == TC_OP_MATMUL_BWD_DATA;
-        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD) continue;
+        // dropout backward product (one operand the byte mask) followed by the ReLU backward
+        const bool drop_mul = s.op == TC_OP_MUL && s.nin == 2 && s.in[0].kind == TC_REF_VAR && s.in[1].kind == TC_REF_VAR &&
+                              (c->vars.at(s.in[0].index).dtype == DT_U8 || c->vars.at(s.in[1].index).dtype == DT_U8);
+        if (drop_mul && !env_on("TCB_DROPOUT_FOLD")) continue;
+        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD && !drop_mul) continue;
         // the next Let, skipping Update / Print statements that do not read this output (the
         // filter-gradient Update sits between a data gradient and its ReLU backward)
         int j = -1;
@@ -708,6 +714,23 @@ void plan_fusion(tc_ctx* c) {
         c->fuse_add_out[i] = a.var;
         c->fuse_relu[i] = c->fuse_relu[j];
         c->fused[j] = 1;
+    }
+    // DropoutMask folded into the forward product that consumes it: the product statement writes
+    // the mask (kept for the backward) and x * mask * scale in one pass (TCB_DROPOUT_FOLD=0: off)
+    for (int i = 0; env_on("TCB_DROPOUT_FOLD") && i < p->nstmts; ++i) {
+        const tc_stmt& d = p->stmts[i];
+        if (d.kind != TC_STMT_LET || d.op != TC_OP_DROPOUT_MASK || d.in[0].kind != TC_REF_VAR || c->fused[i]) continue;
+        const int j = next_let(i);
+        if (j < 0 || c->fused[j]) continue;
+        const tc_stmt& m = p->stmts[j];
+        if (m.op != TC_OP_MUL || m.nin != 2 || m.in[0].kind != TC_REF_VAR || m.in[1].kind != TC_REF_VAR) continue;
+        const int xi = m.in[0].index == d.var ? 1 : m.in[1].index == d.var ? 0 : -1;
+        if (xi < 0 || m.in[xi].index != d.in[0].index) continue;
+        const VarL& x = c->vars.at(d.in[0].index);
+        const VarL& y = c->vars.at(m.var);
+        if (x.cs % 8 || y.cs != x.cs || y.dtype != x.dtype || c->vars.at(d.var).cs != x.cs) continue;
+        c->dropout_apply[j] = i;
+        c->fused[i] = 1;
     }
     plan_xent_fusion(c);
 }
@@ -1281,8 +1304,13 @@ tc_status exec_let(tc_ctx* c, int i) {
             const VarL& x = b.dtype == DT_U8 ? a : b;
             if (m.dtype != DT_U8) return fail(TC_INTERNAL, "runtime: activation x activation MUL is not in the op set");
             const float rate = c->mask_rate.at(m.id);
+            if (const int di = c->dropout_apply[i]; di >= 0)  // the folded DropoutMask statement
+                return launch_dropout_apply(reinterpret_cast<const T*>(P.var(x.id)), reinterpret_cast<uint8_t*>(P.var(m.id)),
+                                            reinterpret_cast<T*>(y), m.N, m.H, m.W, m.C, m.cs, rate, c->desc.seed,
+                                            static_cast<uint32_t>(c->plan->stmts[di].var), c->d_iter, st);
             return launch_mask_mul(reinterpret_cast<const T*>(P.var(x.id)), reinterpret_cast<const uint8_t*>(P.var(m.id)),
-                                   1.f / (1.f - rate), reinterpret_cast<T*>(y), out.elems(), st);
+                                   1.f / (1.f - rate), reinterpret_cast<T*>(y), out.elems(), st,
+                                   c->fuse_mask_var[i] >= 0 ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i])) : nullptr);
         }
         case TC_OP_ADD:
             // loss-head sums (fp32, unpadded rows) take the scalar kernel; activations the vector one

@@ -296,11 +296,13 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
     statements compute: BN apply + residual add (+ ReLU), ReLU backward in the data-gradient
     GEMM epilogue, the ReLU mask carried in the max-pool argmax byte, the momentum update
     fused into the FC filter-gradient epilogue, and the softmax log-loss head (Softmax, Log,
-    Recip, Scale, Mul, softmax backward and the indicator in one kernel; GoogLeNet: 3 heads).  Two training steps
+    Recip, Scale, Mul, softmax backward and the indicator in one kernel; GoogLeNet: 3 heads), the dropout mask
+    generated inside its forward product and the ReLU backward applied by the dropout backward product.  Two training steps
     with every fold on vs off give bit-identical losses, parameters and velocities."""
     runs = []
     for on in ("1", "0"):
-        for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG", "TCB_SGD_FUSE", "TCB_XENT_FOLD"):
+        for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG", "TCB_SGD_FUSE", "TCB_XENT_FOLD",
+                    "TCB_DROPOUT_FOLD"):
             monkeypatch.setenv(var, on)
         net = compile_network(name, batch)
         tr = Trainer(net, use_graph=True, seed=13)
