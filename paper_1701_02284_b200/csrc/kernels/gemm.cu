@@ -1069,7 +1069,7 @@ static tc_status run_conv_c4_fwd(const tc_conv_desc* d, const void* x, const voi
 
 struct ConvC4WgradPlan {
     int ok = 0, splits = 0, tiles = 0, tps = 0;
-    size_t ws_bytes = 0;
+    size_t ws_bytes = 0, bias_off = 0;
 };
 static ConvC4WgradPlan conv_c4_wgrad_plan(const tc_conv_desc* d) {
     ConvC4WgradPlan pl;
@@ -1084,12 +1084,14 @@ static ConvC4WgradPlan conv_c4_wgrad_plan(const tc_conv_desc* d) {
     pl.splits = ceil_div(pl.tiles, pl.tps);
     const int wld = d->wld ? d->wld : d->R * d->S * d->cs;
     pl.ws_bytes = static_cast<size_t>(pl.splits) * d->K * wld * sizeof(float);
+    pl.bias_off = (pl.ws_bytes + 255) & ~static_cast<size_t>(255);  // folded bias partials [splits][K]
+    pl.ws_bytes = pl.bias_off + static_cast<size_t>(pl.splits) * d->K * sizeof(float);
     pl.ok = 1;
     return pl;
 }
 
 static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc* d, const void* dy, const void* x,
-                                   float* dw, void* ws, size_t ws_bytes, cudaStream_t st) {
+                                   float* dw, void* ws, size_t ws_bytes, cudaStream_t st, float* dbias = nullptr) {
     if (!ws || ws_bytes < pl.ws_bytes)
         return fail(TC_INVALID_ARG, "c4 filter gradient: workspace too small: need " + std::to_string(pl.ws_bytes));
     ConvC4WgradParams p;
@@ -1107,6 +1109,7 @@ static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc
     p.Kw = d->wld ? d->wld : d->R * d->S * d->cs;
     p.tiles = pl.tiles;
     p.tiles_per_split = pl.tps;
+    p.bias_ws = dbias ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.bias_off) : nullptr;
     constexpr int kMaxSmem = 232448;
     const int tile_bytes = (p.nkb2 + 1) * BM * 128;
     const int base = 1024 + 2 * tile_bytes + 4 * kStagingBytes + 1024 + 512;
@@ -1142,7 +1145,8 @@ static tc_status run_conv_c4_wgrad(const ConvC4WgradPlan& pl, const tc_conv_desc
     cudaLaunchKernelEx(&cfg, tc_conv_c4_wgrad_kernel, p);
     TCB_LAUNCH_CHECK();
     return launch_splitk_reduce(static_cast<const float*>(ws), pl.splits, d->K, p.Kw,
-                                static_cast<long long>(d->K) * p.Kw, dw, p.Kw, 0, nullptr, 0, 0, 0.f, 0, 0, 0, st);
+                                static_cast<long long>(d->K) * p.Kw, dw, p.Kw, 0, nullptr, 0, 0, 0.f, 0, 0, 0, st,
+                                p.bias_ws, dbias);
 }
 
 static void init_params(GemmParams& p) {
@@ -1491,8 +1495,8 @@ TC_API tc_status tcb_test_conv2d_bwd_filter_bias(const tc_conv_desc* d, const vo
 namespace tcb {
 bool wgrad_bias_foldable(const tc_conv_desc* d) {
     const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");  // 0 disables (read at plan time)
-    if ((e && e[0] == '0') || check_conv(d) != TC_OK || conv_c4_wgrad_plan(d).ok) return false;
-    if (wgrad_halo_plan(d).ok) return true;
+    if ((e && e[0] == '0') || check_conv(d) != TC_OK) return false;
+    if (conv_c4_wgrad_plan(d).ok || wgrad_halo_plan(d).ok) return true;
     // the generic implicit-GEMM filter gradient: dy is its MN-major TMA A operand (not the
     // swapped form, where dy is B), single-CTA tiles
     const LaunchPlan lp = conv_plan(d, 2);
@@ -1511,7 +1515,7 @@ tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* 
     if (s != TC_OK) return s;
     if (dbias && !wgrad_bias_foldable(d)) return fail(TC_INVALID_ARG, "filter gradient: bias fold not available here");
     if (const ConvC4WgradPlan pl = conv_c4_wgrad_plan(d); pl.ok)
-        return run_conv_c4_wgrad(pl, d, dy, x, dw, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+        return run_conv_c4_wgrad(pl, d, dy, x, dw, ws, ws_bytes, static_cast<cudaStream_t>(stream), dbias);
     if (const WgradHaloPlan pl = wgrad_halo_plan(d); pl.ok)
         return run_wgrad_halo(pl, d, dy, x, dw, filter_ld(d), ws, ws_bytes, static_cast<cudaStream_t>(stream), dbias);
     GemmParams p;

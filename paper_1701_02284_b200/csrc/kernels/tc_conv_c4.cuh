@@ -314,6 +314,7 @@ struct ConvC4WgradParams {
     int margin, rows_in, pitch, h_slots;
     int K, Kw;
     int tiles, tiles_per_split;
+    float* bias_ws;  // folded bias gradient: per-split dy column sums [splits][K], or nullptr
 };
 
 __global__ void __launch_bounds__(kC4Threads, 1) tc_conv_c4_wgrad_kernel(const __grid_constant__ ConvC4WgradParams p) {
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(kC4Threads, 1) tc_conv_c4_wgrad_kernel(const _
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&t_full[s], 256 + 1);  // both builder groups + the dy load's arrive
-            mbar_init(&t_empty[s], 1);
+            mbar_init(&t_empty[s], p.bias_ws ? 5 : 1);  // + the 4 epilogue warps summing dy
         }
         mbar_init(tdone, 1);
         fence_mbar_init();
@@ -497,6 +498,52 @@ __global__ void __launch_bounds__(kC4Threads, 1) tc_conv_c4_wgrad_kernel(const _
         // ---------------- epilogue: warp q holds k = 128 h + 32 q + lane; transposed 32 x 32 stores
         const int quarter = warp - 8;
         uint8_t* stg = sStage + quarter * kStagingBytes;
+        if (p.bias_ws) {
+            // folded bias gradient (as wgrad_bias_sums): thread e sums 16-byte chunk kc of the
+            // tile's dy rows rg, rg + 16, ... (SW128 chunk kc ^ (rg & 7)) while the MMA runs
+            const int e = threadIdx.x - 256, kc = e & 7, rg = e >> 3;
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            int ts = 0;
+            uint32_t tph = 0;
+            for (int u = tile0; u < tile1; ++u) {
+                mbar_wait(&t_full[ts], tph);
+                const uint32_t src = smem_u32(sT + ts * tile_bytes + p.nkb2 * BM * 128) + rg * 128 + ((kc ^ (rg & 7)) << 4);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint4 v;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "r"(src + i * 16 * 128)
+                                 : "memory");
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 f = __bfloat1622float2(h[q]);
+                        acc[2 * q] += f.x;
+                        acc[2 * q + 1] += f.y;
+                    }
+                }
+                fence_proxy_async_smem();  // generic reads ordered before the slot's async-proxy refill
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t_empty[ts]);
+                if (++ts == 2) {
+                    ts = 0;
+                    tph ^= 1;
+                }
+            }
+            float* red = reinterpret_cast<float*>(sStage);  // [16 row groups][64 channels]
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red[rg * 64 + kc * 8 + j] = acc[j];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (e < 64) {
+                float sum = 0.f;
+                for (int g = 0; g < 16; ++g) sum += red[g * 64 + e];
+                if (e < p.K) p.bias_ws[static_cast<long long>(sp) * p.K + e] = sum;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the staging is reused below
+        }
         if (tile1 > tile0) {
             mbar_wait(tdone, 0);
             tc_fence_after();
