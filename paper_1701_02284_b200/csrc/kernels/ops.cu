@@ -121,17 +121,21 @@ __global__ void k_relu_bwd(const T* __restrict__ dy, const T* __restrict__ y, T*
 }
 
 template <typename T>
-__global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y, long long n8, int relu) {
+// relu: forward y = max(a + b, 0); relu_y (may be null): a folded in-place ReLU backward behind
+// an adjoint sum, y = [relu_y > 0] (a + b) (relu_y is the forward ReLU output)
+__global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y, long long n8, int relu,
+                      const T* __restrict__ relu_y) {
     pdl_wait();
     pdl_trigger();
     const long long S = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i0 < n8; i0 += 2 * S) {
-        float p[2][8], q[2][8];
+        float p[2][8], q[2][8], r[2][8];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             if (i0 + u * S < n8) {
                 ld8(a + (i0 + u * S) * 8, p[u]);
                 ld8(b + (i0 + u * S) * 8, q[u]);
+                if (relu_y) ld8(relu_y + (i0 + u * S) * 8, r[u]);
             }
         }
 #pragma unroll
@@ -139,6 +143,11 @@ __global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __res
             if (i0 + u * S >= n8) break;
 #pragma unroll
             for (int j = 0; j < 8; ++j) p[u][j] = relu ? fmaxf(p[u][j] + q[u][j], 0.f) : p[u][j] + q[u][j];
+            if (relu_y) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (!(r[u][j] > 0.f)) p[u][j] = 0.f;
+            }
             st8(y + (i0 + u * S) * 8, p[u]);
         }
     }
@@ -1975,8 +1984,8 @@ tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStrea
     return TC_OK;
 }
 template <typename T>
-tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st) {
-    TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu);
+tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st, const T* relu_y) {
+    TCB_LAUNCH(k_add<T>, EW_GRID(n / 8), a, b, y, n / 8, relu, relu_y);
     TCB_LAUNCH_CHECK();
     return TC_OK;
 }
@@ -2464,7 +2473,7 @@ tc_status launch_split_rskc(const float* p, long long ld, int K, int RS, int cs,
 // storage types: bf16 (default) and fp32 (parity precision mode)
 template tc_status launch_relu_fwd<bf16>(const bf16*, bf16*, long long, cudaStream_t);
 template tc_status launch_relu_bwd<bf16>(const bf16*, const bf16*, bf16*, long long, cudaStream_t);
-template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t);
+template tc_status launch_add<bf16>(const bf16*, const bf16*, bf16*, long long, int, cudaStream_t, const bf16*);
 template tc_status launch_mask_mul<bf16>(const bf16*, const uint8_t*, float, bf16*, long long, cudaStream_t, const bf16*);
 template tc_status launch_pool_fwd<bf16>(const bf16*, Act4, bf16*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<bf16>(const bf16*, Act4, const uint8_t*, bf16*, Act4, int, int, int, int,
@@ -2488,7 +2497,7 @@ template tc_status launch_nchw_to_nhwc<bf16, bf16>(const bf16*, bf16*, StageLayo
 template tc_status launch_synth_batch<bf16>(bf16*, int32_t*, StageLayout, int, uint64_t, uint32_t, uint32_t, cudaStream_t);
 template tc_status launch_relu_fwd<float>(const float*, float*, long long, cudaStream_t);
 template tc_status launch_relu_bwd<float>(const float*, const float*, float*, long long, cudaStream_t);
-template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t);
+template tc_status launch_add<float>(const float*, const float*, float*, long long, int, cudaStream_t, const float*);
 template tc_status launch_mask_mul<float>(const float*, const uint8_t*, float, float*, long long, cudaStream_t, const float*);
 template tc_status launch_pool_fwd<float>(const float*, Act4, float*, Act4, uint8_t*, int, int, int, int, int, cudaStream_t);
 template tc_status launch_pool_bwd<float>(const float*, Act4, const uint8_t*, float*, Act4, int, int, int, int,

@@ -31,7 +31,7 @@ template <typename T>
 tc_status launch_relu_bwd(const T* dy, const T* y, T* dx, long long n, cudaStream_t st);
 // y = a + b (then max(y, 0) when relu: a residual add followed by an in-place ReLU)
 template <typename T>
-tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st);
+tc_status launch_add(const T* a, const T* b, T* y, long long n, int relu, cudaStream_t st, const T* relu_y = nullptr);
 // y = x * keep * scale (inverted dropout; keep is a 0/1 byte mask)
 template <typename T>
 tc_status launch_mask_mul(const T* x, const uint8_t* keep, float scale, T* y, long long n, cudaStream_t st,

@@ -619,7 +619,10 @@ void plan_fusion(tc_ctx* c) {
         const bool drop_mul = s.op == TC_OP_MUL && s.nin == 2 && s.in[0].kind == TC_REF_VAR && s.in[1].kind == TC_REF_VAR &&
                               (c->vars.at(s.in[0].index).dtype == DT_U8 || c->vars.at(s.in[1].index).dtype == DT_U8);
         if (drop_mul && !env_on("TCB_DROPOUT_FOLD")) continue;
-        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD && !drop_mul) continue;
+        // adjoint sum of an activation gradient (vector add kernel) followed by the ReLU backward
+        const bool act_add = s.op == TC_OP_ADD && s.nin == 2 && c->vars.at(s.var).cs % 8 == 0 &&
+                             c->vars.at(s.var).dtype == (c->f32 ? DT_F32 : DT_BF16) && env_on("TCB_ADD_RELU_FOLD");
+        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD && !drop_mul && !act_add) continue;
         // the next Let, skipping Update / Print statements that do not read this output (the
         // filter-gradient Update sits between a data gradient and its ReLU backward)
         int j = -1;
@@ -1320,7 +1323,8 @@ tc_status exec_let(tc_ctx* c, int i) {
                                      out.elems(), st);
             return launch_add(reinterpret_cast<const T*>(P.var(s.in[0].index)),
                                    reinterpret_cast<const T*>(P.var(s.in[1].index)), reinterpret_cast<T*>(y),
-                                   out.elems(), c->fuse_relu[i], st);
+                                   out.elems(), c->fuse_relu[i], st,
+                                   c->fuse_mask_var[i] >= 0 ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i])) : nullptr);
         case TC_OP_SCALE:
         case TC_OP_LOG:
         case TC_OP_RECIP: {

@@ -302,7 +302,7 @@ def test_fusions_bit_identical_to_unfused(name, batch, monkeypatch):
     runs = []
     for on in ("1", "0"):
         for var in ("TCB_BN_ADD_FOLD", "TCB_GEMM_RELU_FOLD", "TCB_POOL_IDX_FLAG", "TCB_SGD_FUSE", "TCB_XENT_FOLD",
-                    "TCB_DROPOUT_FOLD"):
+                    "TCB_DROPOUT_FOLD", "TCB_ADD_RELU_FOLD"):
             monkeypatch.setenv(var, on)
         net = compile_network(name, batch)
         tr = Trainer(net, use_graph=True, seed=13)
