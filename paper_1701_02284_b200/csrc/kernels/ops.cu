@@ -1323,8 +1323,9 @@ __global__ void k_channel_copy(const T* __restrict__ src, int src_cs, T* __restr
 
 // 8-channel chunks when strides, offset and width are multiples of 8 (every GoogLeNet concat)
 template <typename T>
+// relu_y (may be null, dst layout): a folded in-place ReLU backward of the copied gradient slice
 __global__ void k_channel_copy8(const T* __restrict__ src, int src_cs, T* __restrict__ dst, int dst_cs, int off, int c8,
-                                long long pixels) {
+                                long long pixels, const T* __restrict__ relu_y) {
     pdl_wait();
     pdl_trigger();
     const long long total = pixels * c8;
@@ -1335,6 +1336,13 @@ __global__ void k_channel_copy8(const T* __restrict__ src, int src_cs, T* __rest
         const int g = static_cast<int>(t - p * c8);
         float f[8];
         ld8(src + p * src_cs + g * 8, f);
+        if (relu_y) {
+            float r[8];
+            ld8(relu_y + p * dst_cs + off + g * 8, r);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (!(r[j] > 0.f)) f[j] = 0.f;
+        }
         st8(dst + p * dst_cs + off + g * 8, f);
     }
 }
@@ -2313,12 +2321,13 @@ tc_status launch_bias_add(const T* x, const float* b, T* y, long long rows, int 
 }
 template <typename T>
 tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
-                              cudaStream_t st) {
+                              cudaStream_t st, const T* relu_y) {
     if ((src_cs | dst_cs | off | c) % 8 == 0 && (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0) {
-        TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels);
+        TCB_LAUNCH(k_channel_copy8<T>, EW_GRID(pixels * (c / 8)), src, src_cs, dst, dst_cs, off, c / 8, pixels, relu_y);
         TCB_LAUNCH_CHECK();
         return TC_OK;
     }
+    if (relu_y) return fail(TC_INTERNAL, "channel copy: folded ReLU backward needs 8-channel alignment");
     TCB_LAUNCH(k_channel_copy<T>, EW_GRID(pixels * c), src, src_cs, dst, dst_cs, off, c, pixels);
     TCB_LAUNCH_CHECK();
     return TC_OK;
@@ -2485,7 +2494,7 @@ template tc_status launch_softmax_fwd<bf16>(const bf16*, long long, float*, int,
 template tc_status launch_softmax_bwd<bf16>(const float*, const float*, bf16*, long long, int, int, cudaStream_t);
 template tc_status launch_colsum<bf16>(const bf16*, long long, int, long long, float*, float*, int, cudaStream_t);
 template tc_status launch_bias_add<bf16>(const bf16*, const float*, bf16*, long long, int, long long, int, cudaStream_t);
-template tc_status launch_channel_copy<bf16>(const bf16*, int, bf16*, int, int, int, long long, cudaStream_t);
+template tc_status launch_channel_copy<bf16>(const bf16*, int, bf16*, int, int, int, long long, cudaStream_t, const bf16*);
 template tc_status launch_bn_fwd<bf16>(const bf16*, const float*, const float*, bf16*, float*, long long, int, int, float, int, const bf16*,
                                      float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_reduce<bf16>(const bf16*, const bf16*, const float*, const float*, float*, long long,
@@ -2509,7 +2518,7 @@ template tc_status launch_softmax_fwd<float>(const float*, long long, float*, in
 template tc_status launch_softmax_bwd<float>(const float*, const float*, float*, long long, int, int, cudaStream_t);
 template tc_status launch_colsum<float>(const float*, long long, int, long long, float*, float*, int, cudaStream_t);
 template tc_status launch_bias_add<float>(const float*, const float*, float*, long long, int, long long, int, cudaStream_t);
-template tc_status launch_channel_copy<float>(const float*, int, float*, int, int, int, long long, cudaStream_t);
+template tc_status launch_channel_copy<float>(const float*, int, float*, int, int, int, long long, cudaStream_t, const float*);
 template tc_status launch_bn_fwd<float>(const float*, const float*, const float*, float*, float*, long long, int, int, float, int, const float*,
                                      float*, int, cudaStream_t);
 template tc_status launch_bn_bwd_reduce<float>(const float*, const float*, const float*, const float*, float*, long long,

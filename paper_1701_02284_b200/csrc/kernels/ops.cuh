@@ -98,7 +98,7 @@ tc_status launch_bias_add(const T* x, const float* b, T* y, long long rows, int 
 // Concat: copy `c` channels of src (stride src_cs) into dst channel offset `off` (stride dst_cs).
 template <typename T>
 tc_status launch_channel_copy(const T* src, int src_cs, T* dst, int dst_cs, int off, int c, long long pixels,
-                              cudaStream_t st);
+                              cudaStream_t st, const T* relu_y = nullptr);
 tc_status launch_zero(void* p, size_t bytes, cudaStream_t st);
 
 // BatchNorm over NHWC [pixels][cs] (training-mode batch statistics, biased variance):

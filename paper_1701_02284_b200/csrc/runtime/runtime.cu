@@ -622,7 +622,12 @@ void plan_fusion(tc_ctx* c) {
         // adjoint sum of an activation gradient (vector add kernel) followed by the ReLU backward
         const bool act_add = s.op == TC_OP_ADD && s.nin == 2 && c->vars.at(s.var).cs % 8 == 0 &&
                              c->vars.at(s.var).dtype == (c->f32 ? DT_F32 : DT_BF16) && env_on("TCB_ADD_RELU_FOLD");
-        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD && !drop_mul && !act_add) continue;
+        // concat backward slice copy (8-channel aligned) followed by the branch's ReLU backward
+        const bool cat_bwd = s.op == TC_OP_CONCAT_BWD && s.offset % 8 == 0 && s.extent % 8 == 0 &&
+                             c->vars.at(s.var).cs % 8 == 0 && s.in[0].kind == TC_REF_VAR &&
+                             c->vars.at(s.in[0].index).cs % 8 == 0 && env_on("TCB_ADD_RELU_FOLD");
+        if (!(gemm && !c->f32) && s.op != TC_OP_POOL_BWD && s.op != TC_OP_LRN_BWD && !drop_mul && !act_add && !cat_bwd)
+            continue;
         // the next Let, skipping Update / Print statements that do not read this output (the
         // filter-gradient Update sits between a data gradient and its ReLU backward)
         int j = -1;
@@ -1463,7 +1468,8 @@ tc_status exec_let(tc_ctx* c, int i) {
             }
             return launch_channel_copy(reinterpret_cast<const T*>(P.var(up.id)) + s.offset, up.cs,
                                        reinterpret_cast<T*>(y), out.cs, 0, static_cast<int>(s.extent),
-                                       static_cast<long long>(out.N) * out.H * out.W, st);
+                                       static_cast<long long>(out.N) * out.H * out.W, st,
+                                       c->fuse_mask_var[i] >= 0 ? reinterpret_cast<const T*>(P.var(c->fuse_mask_var[i])) : nullptr);
         }
         case TC_OP_BN_FWD: {
             const VarL& x = P.L(s.in[0]);
