@@ -487,8 +487,8 @@ static tc_status run_gemm(GemmParams& p, const LaunchPlan& lp, void* D, long lon
     if (p.mask && (partial || !d_bf16)) return fail(TC_INVALID_ARG, "GEMM relu_mask needs a bf16 output without split-K");
     std::string err;
     if (p.bias_out && !p.bias_src) p.bias_src = 1;
-    if (p.bias_out && (lp.cg != 1 || (p.bias_src == 1 && (p.a_mode != OP_TMA_MN || p.trans_out)) ||
-                       (p.bias_src == 2 && (p.b_mode != OP_TMA_MN || lp.bn > 128))))
+    if (p.bias_out && ((p.bias_src == 1 && (p.a_mode != OP_TMA_MN || p.trans_out)) ||
+                       (p.bias_src == 2 && (lp.cg != 1 || p.b_mode != OP_TMA_MN || lp.bn > 128))))
         return fail(TC_INVALID_ARG, "GEMM bias fold needs single-CTA tiles and an MN-major TMA dy operand");
     const long long bias_len = p.bias_src == 2 ? p.N : p.M;
     if (partial) {
@@ -1501,12 +1501,11 @@ bool wgrad_bias_foldable(const tc_conv_desc* d) {
     // swapped form, where dy is B), single-CTA tiles
     const LaunchPlan lp = conv_plan(d, 2);
     if (wgrad_swap(d)) return lp.cg == 1 && lp.bn <= 128;  // swapped: dy is the MN-major B operand
-    return lp.cg == 1;
+    return true;
 }
 bool gemm_bias_foldable(const tc_gemm_args* a) {
     const char* e = std::getenv("TCB_WGRAD_BIAS_FOLD");
-    if ((e && e[0] == '0') || !a || a->a_layout != TC_LAYOUT_MN) return false;
-    return plan_launch(a->M, a->N, a->K, a->splits, a->d_dtype == TC_DTYPE_BF16 ? 2 : 4, true).cg == 1;
+    return !((e && e[0] == '0') || !a || a->a_layout != TC_LAYOUT_MN);
 }
 
 tc_status conv_bwd_filter_ex(const tc_conv_desc* d, const void* dy, const void* x, float* dw, float* dbias, void* ws,

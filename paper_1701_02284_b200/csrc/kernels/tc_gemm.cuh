@@ -681,58 +681,82 @@ __global__ void __launch_bounds__(kNumThreads, 1) tc_gemm_kernel(const __grid_co
                 if (kb == w.kb1 - 1) umma_commit_elect<CG>(&tfull[buf]);
             }
         }
-    } else if ((warp == 2 || warp == 3) && CG == 1 && p.bias_ws != nullptr) {
+    } else if ((warp == 2 || warp == 3) && p.bias_ws != nullptr && (CG == 1 || rank == 0)) {
         // ---------------- folded bias gradient: warp 2 / 3 sums A atom 0 / 1 (64 rows of M each)
         // of every stage over its 64 k rows; lane = (row group rg, 16-byte chunk kc), rows
-        // rg + 4 i, so the row groups combine with two xor shuffles in a fixed order
+        // rg + 4 i, so the row groups combine with two xor shuffles in a fixed order.  CTA pair:
+        // the leader (whose full barrier counts both CTAs' bytes) also reads the peer's A rows
+        // through DSMEM and releases the peer's stage with a remote arrive.
         const int a = warp - 2, kc = lane & 7, rg = lane >> 3;
         const bool from_b = p.bias_src == 2;
-        const int natoms = from_b ? Cfg::kBNL / 64 : BM / 64;  // B: host keeps BN <= 128
+        const int natoms = from_b ? Cfg::kBNL / 64 : BM / 64;  // B: host keeps BN <= 128 (CG = 1)
         const int len = from_b ? p.N : p.M;
         int it = 0;
         for (int u = pair; u < p.units; u += npairs) {
             const Unit w = decode_unit(p, u);
             const bool need = (from_b ? w.mt == 0 : w.nt == 0) && a < natoms;
-            float acc[8];
+            float acc[CG][8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int h = 0; h < CG; ++h)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[h][j] = 0.f;
             for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
                 const int s = it % S;
                 mbar_wait(&full[s], (it / S) & 1);
                 if (need) {
-                    const uint32_t base = smem_u32((from_b ? sB + s * Cfg::kBBytes : sA + s * Cfg::kABytes) + a * BK * 128);
-#pragma unroll 4
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = rg + 4 * i;
-                        uint4 v;
-                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                     : "r"(base + r * 128 + ((kc ^ (r & 7)) << 4))
-                                     : "memory");
-                        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+                    const uint32_t local = smem_u32((from_b ? sB + s * Cfg::kBBytes : sA + s * Cfg::kABytes) + a * BK * 128);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float2 f = __bfloat1622float2(h[q]);
-                            acc[2 * q] += f.x;
-                            acc[2 * q + 1] += f.y;
+                    for (int h = 0; h < CG; ++h) {
+                        const uint32_t base = CG == 2 ? mapa_shared(local, h) : local;
+#pragma unroll 4
+                        for (int i = 0; i < 16; ++i) {
+                            const int r = rg + 4 * i;
+                            uint4 v;
+                            if constexpr (CG == 2)
+                                asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                             : "r"(base + r * 128 + ((kc ^ (r & 7)) << 4))
+                                             : "memory");
+                            else
+                                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                             : "r"(base + r * 128 + ((kc ^ (r & 7)) << 4))
+                                             : "memory");
+                            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float2 f = __bfloat1622float2(hv[q]);
+                                acc[h][2 * q] += f.x;
+                                acc[h][2 * q + 1] += f.y;
+                            }
                         }
                     }
                 }
-                fence_proxy_async_smem();  // generic reads before the async-proxy refill (see wgrad_bias_sums)
+                // generic reads before the async-proxy refill of the stage (see wgrad_bias_sums)
+                if constexpr (CG == 2)
+                    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+                else
+                    fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                if (lane == 0) {
+                    mbar_arrive(&empty[s]);
+                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[s]), 1));
+                }
             }
             if (need) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 8);
-                    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
-                }
-                if (rg == 0) {
+                for (int h = 0; h < CG; ++h) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int m = (from_b ? w.nt * BN : w.mt * BM) + a * 64 + kc * 8 + j;
-                        if (m < len) p.bias_ws[static_cast<long long>(w.sp) * len + m] = acc[j];
+                        acc[h][j] += __shfl_xor_sync(0xffffffffu, acc[h][j], 8);
+                        acc[h][j] += __shfl_xor_sync(0xffffffffu, acc[h][j], 16);
+                    }
+                    if (rg == 0) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int m = (from_b ? w.nt * BN : w.mt * (BM * CG) + h * BM) + a * 64 + kc * 8 + j;
+                            if (m < len) p.bias_ws[static_cast<long long>(w.sp) * len + m] = acc[h][j];
+                        }
                     }
                 }
             }

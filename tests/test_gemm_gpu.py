@@ -293,11 +293,15 @@ def test_conv_fwd_deterministic(case):
 
 
 @pytest.mark.parametrize("case", [(16, 512, 14, 14, 512, 3, 1, 1), (16, 128, 28, 28, 128, 3, 1, 1),
-                                  (8, 64, 28, 28, 96, 3, 1, 1), (8, 64, 30, 30, 64, 3, 1, 1)])
+                                  (8, 64, 28, 28, 96, 3, 1, 1), (8, 64, 30, 30, 64, 3, 1, 1),
+                                  (16, 256, 14, 14, 512, 1, 1, 0), (16, 256, 14, 14, 128, 1, 1, 0),
+                                  (16, 256, 14, 14, 32, 1, 1, 0), (8, 192, 7, 7, 384, 3, 1, 1),
+                                  (4, 3, 64, 64, 64, 3, 1, 1)])
 def test_wgrad_bias_fold_under_concurrent_load(case):
-    """The folded bias gradient (halo filter-gradient epilogue warps summing the staged dy tiles)
-    equals the fp64 pixel sum of dy to fp32 rounding and is bit-identical across repeated runs
-    while another stream keeps the SMs busy (the stage-release ordering the sums depend on)."""
+    """The folded bias gradient (halo / first-layer filter-gradient epilogue warps or the generic
+    GEMM's warps 2-3 summing the staged dy tiles; 1x1 cases cover the plain, CTA-pair and swapped
+    forms) equals the fp64 pixel sum of dy to fp32 rounding and is bit-identical across repeated
+    runs while another stream keeps the SMs busy (the stage-release ordering the sums depend on)."""
     L = nat.lib()
     L.tcb_test_conv2d_bwd_filter_bias.argtypes = [C.POINTER(nat.ConvDesc)] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     x, w, b, d = conv_case(*case, seed=2)
