@@ -1797,6 +1797,58 @@ __global__ void __launch_bounds__(256) k_stage_rows(const SRC* __restrict__ x, T
     }
 }
 
+// Direct staging for 4-channel strides (cs = 4, C <= 4): every staged 8-element chunk is two
+// horizontally adjacent source positions x 4 channels (a pixel pair, or with space-to-depth two
+// neighbouring taps of one pixel), so a thread reads one 8-byte pair per real channel straight
+// from the NCHW rows (each input element is used once: no shared-memory tile) and writes 16 B.
+template <typename T>
+__global__ void k_stage_direct(const float* __restrict__ x, T* __restrict__ y, StageLayout L, int log2_s) {
+    pdl_wait();
+    pdl_trigger();
+    const long long chunks = L.elems() / 8;
+    const int s = 1 << log2_s;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < chunks;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long e0 = q * 8;
+        int n, h, w0;
+        if (L.s2d) {
+            const int lcc = 2 * log2_s + 2;  // channels per staged pixel = s * s * 4
+            const long long pix = e0 >> lcc;
+            const int ij0 = static_cast<int>(e0 & ((1 << lcc) - 1)) >> 2;
+            const int Q = static_cast<int>(pix % L.Ws);
+            const long long t = pix / L.Ws;
+            const int P = static_cast<int>(t % L.Hs);
+            n = static_cast<int>(t / L.Hs);
+            h = P * s + (ij0 >> log2_s) - L.pad;
+            w0 = Q * s + (ij0 & (s - 1)) - L.pad;
+        } else {
+            const long long pix = e0 >> 2;
+            w0 = static_cast<int>(pix % L.W);
+            const long long t = pix / L.W;
+            h = static_cast<int>(t % L.H);
+            n = static_cast<int>(t / L.H);
+        }
+        float f[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float a = 0.f, b = 0.f;
+            if (c < L.C && h >= 0 && h < L.H) {
+                const float* row = x + ((static_cast<long long>(n) * L.C + c) * L.H + h) * L.W;
+                if (w0 >= 0 && w0 + 1 < L.W && ((reinterpret_cast<uintptr_t>(row + w0) & 7) == 0)) {
+                    const float2 v = __ldcs(reinterpret_cast<const float2*>(row + w0));
+                    a = v.x, b = v.y;
+                } else {
+                    if (w0 >= 0 && w0 < L.W) a = __ldcs(row + w0);
+                    if (w0 + 1 >= 0 && w0 + 1 < L.W) b = __ldcs(row + w0 + 1);
+                }
+            }
+            f[c] = a;
+            f[4 + c] = b;
+        }
+        st8(y + e0, f);
+    }
+}
+
 template <typename T, typename SRC>
 __global__ void k_nchw_to_nhwc(const SRC* __restrict__ x, T* __restrict__ y, StageLayout L) {
     pdl_wait();
@@ -2503,6 +2555,17 @@ tc_status launch_bn_bwd_apply(const T* dy, const T* x, const float* k, T* dx, lo
 template <typename T, typename SRC>
 tc_status launch_nchw_to_nhwc(const SRC* x, T* y, StageLayout L, cudaStream_t st) {
     const int s = L.s2d ? L.s2d : 1;
+    if constexpr (std::is_same_v<SRC, float>) {
+        const char* e = std::getenv("TCB_STAGE_DIRECT");  // 0: the row-tiled kernel (A/B)
+        const int ls = (s & (s - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(s)) : -1;
+        if (!(e && e[0] == '0') && L.cs == 4 && L.C <= 4 && ls >= 0 && (L.s2d || L.W % 2 == 0)) {
+            const long long chunks = L.elems() / 8;
+            TCB_LAUNCH((k_stage_direct<T>), static_cast<int>(std::min<long long>((chunks + 255) / 256, num_sms() * 16LL)),
+                       256, 0, st, static_cast<const float*>(x), y, L, ls);
+            TCB_LAUNCH_CHECK();
+            return TC_OK;
+        }
+    }
     const size_t smem = static_cast<size_t>(L.C) * s * L.W * sizeof(float);
     const int wout = L.s2d ? L.Ws : L.W;
     auto log2i = [](int v) { int l = 0; while ((1 << l) < v) ++l; return (1 << l) == v ? l : -1; };
